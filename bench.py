@@ -1,0 +1,368 @@
+"""Benchmark: image-slices/s of the fused project+CTF+adjoint (loss+grad) step on B200.
+
+Workload (BASELINE.json configs[2], "cfg3"): M=128 complex64 Gaussian-blob
+volume, 50,000 masked 128x128 images (12,645 px each), trilinear slicing,
+physical astigmatic CTF, N(0,2px) shifts, SNR 0.05, batch 512 images PER GPU
+(weak scaling).  One step = zero the gradient accumulator + the fused
+slice->CTF/shift->residual->|r|^2->adjoint kernel over one batch + the
+fixed-order loss reduction + ||v||^2 + the gradient epilogue
+(scale*acc + lam*v), and for N>1 one NCCL all-reduce of the packed
+[gradient | loss] buffer.  Inputs are synthetic (seeded).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--config cfg3]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+L2_FLUSH_BYTES = 512 << 20  # > 126 MB L2
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="cfg3")
+    ap.add_argument("--images", type=int, default=0, help="override dataset size (debug)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--lam", type=float, default=1e-3)
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def algorithmic_bytes(M, n_mask, B):
+    """Compulsory HBM bytes of one fused loss+grad launch:
+    B*(8 n_mask [x, complex64] + 128 [record]) + 16 M^3 [read v + write grad]."""
+    return B * (8 * n_mask + 128) + 16 * M ** 3
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 3 + i and s[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# CPU legs (oracle port: test infrastructure, only the checker / baseline)
+# ---------------------------------------------------------------------------
+
+def cpu_workload(cfg, n_images, seed=0):
+    """Host-side copy of the workload for the C oracle (same generators, fp64)."""
+    from oracle import oracle as O
+    from paper_2311_16100_b200 import synth
+
+    M = cfg.M
+    mask = O.disk_mask(M, M // 2 - 1)
+    pix = O.mask_pix(M, mask)
+    v = synth.gaussian_blob_volume(M, seed)
+    q = synth.haar_quaternions(n_images, seed + 1)
+    sh = synth.normal_shifts(n_images, seed + 2) if cfg.shifts else np.zeros((n_images, 2))
+    ctab = (O.ctf_table_physical(synth.ctf_param_array(synth.physical_ctfs(n_images, seed + 3)), pix, M)
+            if cfg.ctf else None)
+    op = O.OracleOperator(M, cfg.mode, mask, q, sh, ctab, None)
+    clean = op.project(v, np.arange(n_images))
+    sigma = np.sqrt(np.mean(np.abs(clean) ** 2) / cfg.snr)
+    rng = np.random.default_rng(seed + 100)
+    op.x = clean + (sigma / np.sqrt(2)) * (rng.standard_normal(clean.shape) + 1j * rng.standard_normal(clean.shape))
+    return op, v
+
+
+def time_cpu(op, v, batch, lam, n_total, steps, warmup):
+    from oracle import oracle as O
+
+    rng = np.random.default_rng(7)
+    for _ in range(warmup):
+        O.loss_and_grad(op, v, rng.choice(op.n_images, batch, replace=False), lam, n_total)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        O.loss_and_grad(op, v, rng.choice(op.n_images, batch, replace=False), lam, n_total)
+    return (time.perf_counter() - t0) / steps
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def run_reference(args):
+    """--impl reference: the reference's CPU path (oracle port, all host threads) on this config."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    from paper_2311_16100_b200 import synth
+
+    cfg = synth.CONFIGS[args.config]
+    B = cfg.batch
+    n_sub = min(cfg.n_images, max(4 * B, 2048))
+    op, v = cpu_workload(cfg, n_sub)
+    threads = O.max_threads()
+    per = time_cpu(op, v * 0.9, B, args.lam, cfg.n_images, args.steps, args.warmup)
+    val = B / per
+    line = {
+        "impl": "reference", "metric": "image-slices/sec (fused project+CTF+adjoint, loss+grad)",
+        "value": val, "unit": "images/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": per * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded generators of BASELINE cfg; SURVEY.md 8d)",
+        "config": {"workload": cfg.name, "M": cfg.M, "batch_per_step": B, "n_images_total": cfg.n_images,
+                   "images_sampled_from": n_sub, "mode": cfg.mode},
+        "cpu_baseline": {"value": val, "unit": "images/s", "cores": threads, "kind": "port",
+                         "sample": f"{args.steps} steps x {B} images drawn from a {n_sub}-image host subset, "
+                                   f"C oracle (fp64, OpenMP {threads} threads, {cpu_model()})"},
+        "e2e": {"value": val, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+# ---------------------------------------------------------------------------
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2311_16100_b200 import synth
+    from paper_2311_16100_b200.engine import _stream, ctypes_ptr
+    from paper_2311_16100_b200 import _capi as C
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = synth.CONFIGS[args.config]
+    B = cfg.batch if args.config != "cfg2" else 2048
+    wl = synth.build_workload(cfg, seed=0, n_images=args.images or None)
+    eng = wl.engine
+    M, n = eng.M, eng.n_mask
+    lib = C.load()
+    dev = eng.dev
+    lam = args.lam
+    n_total = eng.n_images * world
+    scale = n_total / (B * world)
+
+    v = torch.from_numpy((wl.v_true * 0.9).astype(np.complex64)).to(dev)
+    packed = torch.zeros(2 * M ** 3 + 2, dtype=torch.float32, device=dev)
+    acc = packed[:2 * M ** 3].view(torch.complex64)
+    grad = torch.empty(M ** 3, dtype=torch.complex64, device=dev)
+    sq = torch.empty(1, dtype=torch.float64, device=dev)
+    nrm = torch.empty(1, dtype=torch.float64, device=dev)
+    scr = eng.scratch(B)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    gen = np.random.default_rng(1234 + rank)
+    n_steps = args.warmup + args.steps
+    batches = [torch.from_numpy(gen.choice(eng.n_images, B, replace=False).astype(np.int32)).to(dev)
+               for _ in range(n_steps)]
+    stream = _stream()
+    launches_per_step = 5  # loss_grad (slice + reduce), norm2 (2), grad_finalize
+
+    def step(idx, ev_k0=None, ev_k1=None):
+        acc.zero_()
+        if ev_k0 is not None:
+            ev_k0.record()
+        C.check(lib.fsld_loss_grad(M, eng.mode_id, n, ctypes_ptr(eng.pix), ctypes_ptr(eng.recs), ctypes_ptr(idx),
+                                   B, ctypes_ptr(v), ctypes_ptr(eng.x), ctypes_ptr(acc), ctypes_ptr(sq), 0, 0,
+                                   ctypes_ptr(scr), scr.numel() * 8, stream), "loss_grad")
+        if ev_k1 is not None:
+            ev_k1.record()
+        C.check(lib.fsld_norm2(M ** 3, ctypes_ptr(v), ctypes_ptr(nrm), ctypes_ptr(scr), scr.numel() * 8, stream),
+                "norm2")
+        if world > 1:
+            s32 = sq.float()
+            packed[-2:-1].copy_(s32)
+            packed[-1:].copy_((sq - s32.double()).float())
+            dist.all_reduce(packed)
+        C.check(lib.fsld_grad_finalize(M ** 3, ctypes_ptr(acc), 0, 0, ctypes_ptr(v), scale, lam, ctypes_ptr(grad),
+                                       stream), "finalize")
+        return 0.5 * scale * sq + 0.5 * lam * nrm
+
+    for i in range(args.warmup):
+        step(batches[i])
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    E = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    ev = [(E(), E(), E(), E()) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        for i in range(args.steps):
+            flush.fill_(float(i))  # L2 flush between timed steps (outside the step events)
+            s0, k0, k1, s1 = ev[i]
+            s0.record()
+            step(batches[args.warmup + i], k0, k1)
+            s1.record()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    step_ms = [e[0].elapsed_time(e[3]) for e in ev]
+    kern_ms = [e[1].elapsed_time(e[2]) for e in ev]
+    t_step = float(np.mean(step_ms))
+    t_kern = float(np.mean(kern_ms))
+    if world > 1:
+        t = torch.tensor([t_step, t_kern], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_step, t_kern = float(t[0]), float(t[1])
+    value = world * B / (t_step * 1e-3)
+
+    # e2e through the public API: host v in (pinned), host grad + loss out
+    e2e = None
+    if not args.no_e2e:
+        e2e = e2e_leg(eng, wl, B, lam, n_total, args, world)
+
+    hbm, src = peaks()
+    abytes = algorithmic_bytes(M, n, B)
+    achieved = abytes / (t_kern * 1e-3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get(cfg.name)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg, B, lam)
+    if rank == 0:
+        line = {
+            "metric": "image-slices/sec (fused project+CTF+adjoint, loss+grad)",
+            "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": t_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "c64/f32 (fp64 coords, CTF phase)", "data": "synthetic (seeded generators of BASELINE cfg; SURVEY.md 8d)",
+            "config": {"workload": cfg.name, "M": M, "n_mask": n, "batch_per_gpu": B,
+                       "n_images_per_gpu": eng.n_images, "mode": cfg.mode, "ctf": "physical astigmatic",
+                       "parallelism": f"dp{world}", "l2": "flushed between timed steps (512 MB write)"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": achieved / hbm, "traffic": traffic, "peak_source": src,
+                         "kernel": "fsld slice_kernel<TRI,LOSS_GRAD> (+fixed-order loss reduce)",
+                         "kernel_ms": t_kern, "algorithmic_bytes_per_launch": abytes},
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clk.summary(),
+        }
+        if e2e is not None:
+            line["e2e"] = e2e
+        if cpu is not None:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def e2e_leg(eng, wl, B, lam, n_total, args, world):
+    """Same step through DatasetOperator/loss_and_grad with host (pinned) v in and host grad/loss out."""
+    import torch
+
+    from paper_2311_16100_b200.forward import DatasetOperator
+
+    op = DatasetOperator.from_engine(eng)
+    M = eng.M
+    v_h = torch.from_numpy((wl.v_true * 0.9).astype(np.complex64)).pin_memory()
+    g_h = torch.empty(M ** 3, dtype=torch.complex64).pin_memory()
+    gen = np.random.default_rng(99)
+    idx_h = [torch.from_numpy(gen.choice(eng.n_images, B, replace=False).astype(np.int32)).pin_memory()
+             for _ in range(args.warmup + args.steps)]
+    for i in range(args.warmup):
+        op.loss_and_grad_host(v_h, idx_h[i], lam, g_h, n_total=n_total)
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for i in range(args.steps):
+        op.loss_and_grad_host(v_h, idx_h[args.warmup + i], lam, g_h, n_total=n_total)
+    t1.record()
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / args.steps
+    return {"value": world * B / (ms * 1e-3), "unit": "images/s", "ms_per_step": ms,
+            "h2d_bytes_per_step": 8 * M ** 3 + 4 * B, "d2h_bytes_per_step": 8 * M ** 3 + 8,
+            "path": "DatasetOperator.loss_and_grad_host (pinned host v/idx in, pinned host grad + loss out)"}
+
+
+def cpu_baseline(cfg, B, lam):
+    from oracle import oracle as O
+
+    n_sub = 2 * B
+    op, v = cpu_workload(cfg, n_sub)
+    threads = O.max_threads()
+    steps = 4
+    per = time_cpu(op, v * 0.9, B, lam, cfg.n_images, steps, 1)
+    return {"value": B / per, "unit": "images/s", "cores": threads, "kind": "port",
+            "sample": f"{steps} loss+grad steps x {B} images from a {n_sub}-image host subset, C oracle "
+                      f"(fp64, OpenMP {threads} threads, {cpu_model()})"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

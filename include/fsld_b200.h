@@ -1,0 +1,224 @@
+/*
+ * fsld_b200.h -- C ABI of the B200 (sm_100a) Fourier-slice project/adjoint path.
+ *
+ * Drop-in boundary for the hot path of the reference package `fsld`
+ * (/root/reference/pkg/src/fsld).  The reference has no native ABI of its
+ * own: its "native" layer is the numba kernel module kernels.py, called from
+ * Python (Projector / DatasetOperator / optim).  Each entry point below names
+ * the reference interface it replaces.  INTEGRATION.md shows the ctypes
+ * binding a maintainer would add on the reference side.
+ *
+ * Conventions (all entry points):
+ *  - every pointer argument is a DEVICE pointer unless documented otherwise;
+ *  - work is enqueued on `stream` (a cudaStream_t, NULL = legacy default
+ *    stream) and is stream-ordered; nothing synchronises the host;
+ *  - outputs are caller-allocated (mirrors the numba output-parameter style,
+ *    kernels.py:138-302); accumulating outputs ("acc") are ADDED to, so the
+ *    caller zeroes them (as Projector.backproject_batch does, forward.py:326-328);
+ *  - return value: FSLD_OK (0) or a negative status; nothing throws across
+ *    the ABI.  fsld_status_string() gives a message.
+ *
+ * Layouts (reference layout contract, grid.py:9-31):
+ *  - volume: M^3 complex64 (interleaved re, im float32), linear index
+ *    j = (z_index*M + y_index)*M + x_index, x/y centred (k + ceil(M/2)),
+ *    z in FFT order (kz < 0 -> kz + M);
+ *  - masked pixels: `pix` is (n_mask, 2) int16 (kx, ky) in ascending pixel
+ *    index order (disk_mask, grid.py:185-189);
+ *  - images: (rows, n_mask) complex64, compact masked (DatasetOperator.x,
+ *    forward.py:527);
+ *  - batch: `idx` (B,) int32 row numbers into the per-image records and the
+ *    image rows (DatasetOperator.project(values, idx), forward.py:540-545).
+ */
+#ifndef FSLD_B200_H
+#define FSLD_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FSLD_ABI_VERSION 1
+
+/* status codes */
+#define FSLD_OK 0
+#define FSLD_EINVAL (-1)     /* invalid argument (reference: ValueError) */
+#define FSLD_ECUDA (-2)      /* CUDA launch / runtime error */
+#define FSLD_ENODEV (-3)     /* no sm_100 device */
+
+/* interpolation modes (forward.py:35 MODES = ("nn", "tri")) */
+#define FSLD_MODE_NN 0
+#define FSLD_MODE_TRI 1
+
+/* flags */
+#define FSLD_DETERMINISTIC 1u /* accumulate in int64 fixed point: bitwise repeatable */
+
+/* fsld_image_rec.flags */
+#define FSLD_REC_CTF 1u
+#define FSLD_REC_SHIFT 2u
+
+/*
+ * Per-image parameter record, 128 bytes, read with one coalesced load per
+ * image.  Replaces the reference's per-(image, pixel) tables rots/phases/
+ * ctf_vals (forward.py:296-312, 524-527): phase and CTF are evaluated
+ * in-kernel, so nothing of size (N, n_mask) but the images themselves lives
+ * in HBM.
+ *   rot   : R[0][0..2], R[1][0..2] (kernels.py:42-47 reads rows 0 and 1 only)
+ *   shift : phase(kx,ky) = exp(i*pi*(shift[0]*kx + shift[1]*ky)), i.e.
+ *           shift = -2 t / M (forward.py:299-303)
+ *   gamma : CTF phase g = gamma[0]*(kx^2+ky^2) + gamma[1]*(kx^2-ky^2)
+ *                        + gamma[2]*(2 kx ky) + gamma[3]*(kx^2+ky^2)^2
+ *   env   : envelope exp(-env*(kx^2+ky^2))
+ *   C(kx,ky) = -(wsin*sin g + wcos*cos g) * envelope     (if FSLD_REC_CTF)
+ * The reference's radial toy CTF (forward.py:93-111) is the special case
+ * gamma = {pi*defocus/r_max^2, 0, 0, 0}, env = b_factor/r_max^2,
+ * wsin = 1-w, wcos = w; the physical astigmatic CTF of the BASELINE configs
+ * fills all four gamma terms with wsin = sqrt(1-A^2), wcos = A.
+ */
+typedef struct fsld_image_rec {
+    double rot[6];
+    double shift[2];
+    double gamma[4];
+    double env;
+    float wsin, wcos;
+    uint32_t flags;
+    uint32_t pad[3];
+} fsld_image_rec;
+
+int fsld_abi_version(void);
+const char* fsld_status_string(int status);
+/* number of visible devices with compute capability 10.x (host call) */
+int fsld_device_count(int* count);
+
+/*
+ * Scratch bytes needed by the reducing entry points for a batch of B images
+ * (per-block partial sums, reduced in a fixed order -> deterministic loss).
+ */
+size_t fsld_scratch_bytes(int M, int n_mask, int B);
+
+/*
+ * Fused slice -> CTF/shift -> residual -> |r|^2 -> adjoint scatter.
+ * Replaces optim._resid_pass(want_grad=True) (optim.py:147-162), i.e.
+ * kernels.project_{tri,nn} (kernels.py:138-190) + residual numpy +
+ * kernels.backproject_{tri,nn} (kernels.py:193-248) + fold_chunks.
+ *   sq_out   : device double, receives sum over batch of |P v - x|^2
+ *   grad_acc : += sum_i P_i^* conj(f_i) r_i   (unscaled; see fsld_grad_finalize)
+ *              complex64 M^3, or int64 pairs M^3 when FSLD_DETERMINISTIC
+ *   fx_scale : device double fixed-point scale (FSLD_DETERMINISTIC only,
+ *              from fsld_fixed_scale), else NULL
+ */
+int fsld_loss_grad(int M, int mode, int n_mask, const int16_t* pix,
+                   const fsld_image_rec* recs, const int32_t* idx, int B,
+                   const void* v, const void* x, void* grad_acc, double* sq_out,
+                   unsigned flags, const double* fx_scale,
+                   void* scratch, size_t scratch_bytes, void* stream);
+
+/* Loss only (Armijo trials): optim._resid_pass(want_grad=False) (optim.py:193-207). */
+int fsld_loss(int M, int mode, int n_mask, const int16_t* pix,
+              const fsld_image_rec* recs, const int32_t* idx, int B,
+              const void* v, const void* x, double* sq_out,
+              void* scratch, size_t scratch_bytes, void* stream);
+
+/* Projection out[b, p] = f_b(p) * (P_b v)(p), (B, n_mask) complex64.
+ * Replaces Projector.project_batch / DatasetOperator.project (forward.py:316-324, 540-545). */
+int fsld_project(int M, int mode, int n_mask, const int16_t* pix,
+                 const fsld_image_rec* recs, const int32_t* idx, int B,
+                 const void* v, void* out, void* stream);
+
+/* Adjoint acc += sum_b P_b^* conj(f_b) img[b]; img is (B, n_mask) complex64 (batch-local rows).
+ * Replaces Projector.backproject_batch / DatasetOperator.backproject (forward.py:326-335, 547-552). */
+int fsld_backproject(int M, int mode, int n_mask, const int16_t* pix,
+                     const fsld_image_rec* recs, const int32_t* idx, int B,
+                     const void* img, void* acc, unsigned flags, const double* fx_scale,
+                     void* stream);
+
+/* Normal operator acc += sum_b P_b^* C_b^2 P_b z (z complex64 M^3); the shift phase cancels.
+ * Replaces the loop body of DatasetOperator.hvp (forward.py:554-570). */
+int fsld_hvp(int M, int mode, int n_mask, const int16_t* pix,
+             const fsld_image_rec* recs, const int32_t* idx, int B,
+             const void* z, void* acc, unsigned flags, const double* fx_scale,
+             void* stream);
+
+/*
+ * Hutchinson probe batcher: k Rademacher probes bit-packed as zbits
+ * (M^3, words) uint32, words = ceil(k/32), bit p of word w = probe 32w+p
+ * (1 -> +1, 0 -> -1, as optim.rademacher, optim.py:142-144).  Accumulates the
+ * probe-folded sample  acc[j] += sum_p z_p[j] * (sum_b P_b^* C_b^2 P_b z_p)[j]
+ * (float32 M^3, or int64 M^3 when FSLD_DETERMINISTIC) in one pass over the
+ * batch; hutchinson_update (optim.py:210-229) then needs only
+ * scale/k * acc + lam.
+ */
+int fsld_hutch_fold(int M, int mode, int n_mask, const int16_t* pix,
+                    const fsld_image_rec* recs, const int32_t* idx, int B,
+                    const uint32_t* zbits, int k, void* acc, unsigned flags,
+                    const double* fx_scale, void* stream);
+
+/* Pack k real probe vectors z ((k, n) float64, entries +-1, probe-major) into zbits
+ * (n, ceil(k/32)) uint32; unused bits of the last word are zero.  Sets *bad (device
+ * int, may be NULL) to 1 if an entry is not exactly +-1. */
+int fsld_pack_probes(int64_t n, int k, const double* z, uint32_t* zbits, int* bad, void* stream);
+
+/* Generate k counter-based Rademacher probes in place (no host RNG, no z bytes read):
+ * bit = hash(seed, voxel, word).  For throughput runs; parity runs pack the
+ * reference's numpy stream with fsld_pack_probes. */
+int fsld_gen_probes(int64_t n, int k, uint64_t seed, uint32_t* zbits, void* stream);
+
+/* Exact diagonal of sum_b P_b^* C_b^2 P_b: tri: acc[j] += C^2 w_j^2, nn: acc[j] += C^2
+ * (kernels.scatter_sq_tri kernels.py:251-294; nn bincount forward.py:341-349, hessian.py:62-107). */
+int fsld_exact_diag(int M, int mode, int n_mask, const int16_t* pix,
+                    const fsld_image_rec* recs, const int32_t* idx, int B,
+                    void* acc, unsigned flags, const double* fx_scale, void* stream);
+
+/* Nearest-neighbour voxel index per (image, pixel), int32 (B, n_mask); bit-exact with
+ * kernels.assign_nn (kernels.py:123-135). */
+int fsld_assign_nn(int M, int n_mask, const int16_t* pix, const fsld_image_rec* recs,
+                   const int32_t* idx, int B, int32_t* out, void* stream);
+
+/*
+ * Table-driven variants with the numba kernel signatures (kernels.py:138-294):
+ * the caller supplies the per-(image, pixel) factor table instead of the
+ * in-kernel CTF/shift model.  Batch entry b uses record b (no idx).
+ *   ftab : (B, n_mask) complex64, f = phase * ctf  (project: out = f * P v;
+ *          adjoint: acc += P^* conj(f) img, the numba `img*conj(phase)*ctf`)
+ *   wtab : (B, n_mask) complex64 whose real part is the per-pixel weight
+ *          (scatter_sq_tri `weights`; nn mode: the bincount weights)
+ */
+int fsld_project_tab(int M, int mode, int n_mask, const int16_t* pix, const fsld_image_rec* recs, int B,
+                     const void* v, const void* ftab, void* out, void* stream);
+int fsld_backproject_tab(int M, int mode, int n_mask, const int16_t* pix, const fsld_image_rec* recs, int B,
+                         const void* img, const void* ftab, void* acc, unsigned flags,
+                         const double* fx_scale, void* stream);
+int fsld_scatter_sq_tab(int M, int mode, int n_mask, const int16_t* pix, const fsld_image_rec* recs, int B,
+                        const void* wtab, void* acc, unsigned flags, const double* fx_scale, void* stream);
+
+/*
+ * Fixed-point scale for FSLD_DETERMINISTIC accumulation: writes
+ * 2^floor(61 - log2(bound)) to *fx_scale, bound = mult * (max_i |data_i| + add),
+ * data complex64 of n elements (data may be NULL -> max = 0).
+ */
+int fsld_fixed_scale(const void* data, int64_t n, double mult, double add, double* fx_scale,
+                     void* stream);
+
+/*
+ * Finalize an accumulator into complex64:
+ *   out = scale * acc_value + lam * v      (v may be NULL -> 0)
+ * acc_value = acc (complex64) or int64 pairs / fx_scale when FSLD_DETERMINISTIC.
+ * The loss_and_grad epilogue (optim.py:186-189) and hvp's (forward.py:570).
+ */
+int fsld_grad_finalize(int64_t nvox, const void* acc, unsigned flags, const double* fx_scale,
+                       const void* v, double scale, double lam, void* out, void* stream);
+
+/* Real-accumulator variant (Hutchinson fold / exact diag): out = scale*acc + add, float32. */
+int fsld_real_finalize(int64_t nvox, const void* acc, unsigned flags, const double* fx_scale,
+                       double scale, double add, float* out, void* stream);
+
+/* sum |v|^2 over complex64 M^3 in a fixed order (fp64), for the lam/2 ||v||^2 term. */
+int fsld_norm2(int64_t n, const void* v, double* out, void* scratch, size_t scratch_bytes,
+               void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FSLD_B200_H */

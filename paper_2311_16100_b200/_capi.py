@@ -1,0 +1,105 @@
+"""ctypes binding of libfsld_b200.so (the C ABI declared in include/fsld_b200.h).
+
+The product has exactly one compute path: the sm_100a kernels behind this
+ABI.  If the shared library is missing, or no compute-capability-10 device
+is visible, calls raise -- there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "_lib", "libfsld_b200.so")
+
+FSLD_OK = 0
+FSLD_EINVAL = -1
+FSLD_ECUDA = -2
+FSLD_ENODEV = -3
+MODE_NN = 0
+MODE_TRI = 1
+DETERMINISTIC = 1
+REC_CTF = 1
+REC_SHIFT = 2
+ABI_VERSION = 1
+
+# fsld_image_rec (include/fsld_b200.h): 128 bytes
+REC_DTYPE = np.dtype([
+    ("rot", "<f8", (6,)),
+    ("shift", "<f8", (2,)),
+    ("gamma", "<f8", (4,)),
+    ("env", "<f8"),
+    ("wsin", "<f4"),
+    ("wcos", "<f4"),
+    ("flags", "<u4"),
+    ("pad", "<u4", (3,)),
+])
+assert REC_DTYPE.itemsize == 128
+
+P = ctypes.c_void_p
+I = ctypes.c_int
+I64 = ctypes.c_int64
+U = ctypes.c_uint
+D = ctypes.c_double
+SZ = ctypes.c_size_t
+
+# name -> (restype, argtypes); the exported surface of include/fsld_b200.h
+SIGNATURES = {
+    "fsld_abi_version": (I, []),
+    "fsld_status_string": (ctypes.c_char_p, [I]),
+    "fsld_device_count": (I, [P]),
+    "fsld_scratch_bytes": (SZ, [I, I, I]),
+    "fsld_loss_grad": (I, [I, I, I, P, P, P, I, P, P, P, P, U, P, P, SZ, P]),
+    "fsld_loss": (I, [I, I, I, P, P, P, I, P, P, P, P, SZ, P]),
+    "fsld_project": (I, [I, I, I, P, P, P, I, P, P, P]),
+    "fsld_backproject": (I, [I, I, I, P, P, P, I, P, P, U, P, P]),
+    "fsld_hvp": (I, [I, I, I, P, P, P, I, P, P, U, P, P]),
+    "fsld_hutch_fold": (I, [I, I, I, P, P, P, I, P, I, P, U, P, P]),
+    "fsld_pack_probes": (I, [I64, I, P, P, P, P]),
+    "fsld_gen_probes": (I, [I64, I, ctypes.c_uint64, P, P]),
+    "fsld_exact_diag": (I, [I, I, I, P, P, P, I, P, U, P, P]),
+    "fsld_assign_nn": (I, [I, I, P, P, P, I, P, P]),
+    "fsld_project_tab": (I, [I, I, I, P, P, I, P, P, P, P]),
+    "fsld_backproject_tab": (I, [I, I, I, P, P, I, P, P, P, U, P, P]),
+    "fsld_scatter_sq_tab": (I, [I, I, I, P, P, I, P, P, U, P, P]),
+    "fsld_fixed_scale": (I, [P, I64, D, D, P, P]),
+    "fsld_grad_finalize": (I, [I64, P, U, P, P, D, D, P, P]),
+    "fsld_real_finalize": (I, [I64, P, U, P, D, D, P, P]),
+    "fsld_norm2": (I, [I64, P, P, P, SZ, P]),
+}
+
+_lib = None
+
+
+class FsldError(RuntimeError):
+    pass
+
+
+def load():
+    """Load libfsld_b200.so (raises if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with `python -m paper_2311_16100_b200._build` "
+                "(nvcc, sm_100a). There is no CPU fallback.")
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        if lib.fsld_abi_version() != ABI_VERSION:
+            raise ImportError("libfsld_b200.so ABI version mismatch; rebuild it")
+        _lib = lib
+    return _lib
+
+
+def check(status: int, what: str) -> None:
+    if status == FSLD_OK:
+        return
+    msg = load().fsld_status_string(status).decode()
+    if status == FSLD_EINVAL:
+        raise ValueError(f"{what}: {msg}")
+    raise FsldError(f"{what}: {msg} (status {status})")

@@ -1,0 +1,126 @@
+// fsld_aux.cu -- volume-sized elementwise / reduction kernels (HBM-streaming).
+//
+//  - fixed-point scale for the deterministic int64 accumulators;
+//  - accumulator finalize: grad = scale*acc + lam*v (optim.py:186-189,
+//    forward.py:570), real variant for Hutchinson / exact diagonal;
+//  - ||v||^2 in a fixed order (optim.py:187).
+#include "fsld_kernels.cuh"
+
+namespace fsld {
+
+// max |data| over complex64, via atomicMax on the (non-negative) float bits:
+// order-independent, hence deterministic.
+__global__ void maxabs_kernel(const float2* __restrict__ d, int64_t n, unsigned* out) {
+    float m = 0.f;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const float2 z = d[i];
+        m = fmaxf(m, fmaxf(fabsf(z.x), fabsf(z.y)));
+    }
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0 && m > 0.f) atomicMax(out, __float_as_uint(m));
+}
+
+// fx = 2^floor(61 - log2(bound)), bound = mult * (2*max|component| + add).
+// 2*max|component| bounds |z|.  Accumulated totals then stay below 2^62 in
+// magnitude as long as sum_contributions |value| <= bound.
+__global__ void fixed_scale_kernel(const unsigned* mx, double mult, double add, double* fx) {
+    const double m = mx ? (double)__uint_as_float(*mx) : 0.0;
+    double bound = mult * (2.0 * m + add);
+    if (!(bound > 0.0)) bound = 1.0;
+    int e;
+    frexp(bound, &e);  // bound < 2^e
+    *fx = ldexp(1.0, 61 - e);
+}
+
+cudaError_t launch_fixed_scale(const float2* data, int64_t n, double mult, double add, double* fx,
+                               cudaStream_t s) {
+    // scratch for the max: the fx slot itself is reused as a 4-byte counter
+    unsigned* mx = nullptr;
+    if (data && n > 0) {
+        mx = reinterpret_cast<unsigned*>(fx);
+        cudaError_t e = cudaMemsetAsync(mx, 0, sizeof(double), s);
+        if (e != cudaSuccess) return e;
+        int blocks = (int)((n + 255) / 256);
+        blocks = blocks > 1184 ? 1184 : blocks;
+        maxabs_kernel<<<blocks, 256, 0, s>>>(data, n, mx);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    fixed_scale_kernel<<<1, 1, 0, s>>>(mx, mult, add, fx);
+    return cudaGetLastError();
+}
+
+template <bool DET>
+__global__ void grad_finalize_kernel(int64_t n, const void* __restrict__ acc, const double* fxp,
+                                     const float2* __restrict__ v, double scale, double lam, float2* out) {
+    const double inv = DET ? 1.0 / *fxp : 1.0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        double re, im;
+        if (DET) {
+            const longlong2 q = reinterpret_cast<const longlong2*>(acc)[i];
+            re = (double)q.x * inv;
+            im = (double)q.y * inv;
+        } else {
+            const float2 q = reinterpret_cast<const float2*>(acc)[i];
+            re = q.x;
+            im = q.y;
+        }
+        re *= scale;
+        im *= scale;
+        if (v) {
+            const float2 w = v[i];
+            re += lam * (double)w.x;
+            im += lam * (double)w.y;
+        }
+        out[i] = make_float2((float)re, (float)im);
+    }
+}
+
+cudaError_t launch_grad_finalize(int64_t nvox, const void* acc, bool det, const double* fx, const float2* v,
+                                 double scale, double lam, float2* out, cudaStream_t s) {
+    int blocks = (int)((nvox + 255) / 256);
+    blocks = blocks > 148 * 16 ? 148 * 16 : blocks;
+    if (det) grad_finalize_kernel<true><<<blocks, 256, 0, s>>>(nvox, acc, fx, v, scale, lam, out);
+    else grad_finalize_kernel<false><<<blocks, 256, 0, s>>>(nvox, acc, fx, v, scale, lam, out);
+    return cudaGetLastError();
+}
+
+template <bool DET>
+__global__ void real_finalize_kernel(int64_t n, const void* __restrict__ acc, const double* fxp, double scale,
+                                     double add, float* out) {
+    const double inv = DET ? 1.0 / *fxp : 1.0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        double a = DET ? (double)reinterpret_cast<const long long*>(acc)[i] * inv
+                       : (double)reinterpret_cast<const float*>(acc)[i];
+        out[i] = (float)(scale * a + add);
+    }
+}
+
+cudaError_t launch_real_finalize(int64_t nvox, const void* acc, bool det, const double* fx, double scale,
+                                 double add, float* out, cudaStream_t s) {
+    int blocks = (int)((nvox + 255) / 256);
+    blocks = blocks > 148 * 16 ? 148 * 16 : blocks;
+    if (det) real_finalize_kernel<true><<<blocks, 256, 0, s>>>(nvox, acc, fx, scale, add, out);
+    else real_finalize_kernel<false><<<blocks, 256, 0, s>>>(nvox, acc, fx, scale, add, out);
+    return cudaGetLastError();
+}
+
+__global__ void norm2_kernel(int64_t n, const float2* __restrict__ v, double* part) {
+    __shared__ double smem[32];
+    double s = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const float2 z = v[i];
+        s += (double)z.x * z.x + (double)z.y * z.y;
+    }
+    s = block_sum(s, smem);
+    if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+cudaError_t launch_norm2(int64_t n, const float2* v, double* out, double* part, int nparts, cudaStream_t s) {
+    norm2_kernel<<<nparts, 256, 0, s>>>(n, v, part);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return launch_reduce(part, nparts, out, s);
+}
+
+}  // namespace fsld

@@ -1,0 +1,269 @@
+// fsld_capi.cu -- extern "C" entry points of libfsld_b200.so (include/fsld_b200.h).
+//
+// Validates arguments the way the reference raises ValueError (empty batch
+// forward.py:562-563 / optim.py:179-180, bad mode forward.py:280-281), picks
+// the launch geometry and enqueues the kernels on the caller's stream.
+// Never throws, never synchronises.
+#include <cstdio>
+
+#include "fsld_kernels.cuh"
+
+using namespace fsld;
+
+namespace {
+
+constexpr int kPixPerThreadTarget = 4;
+
+int status_of(cudaError_t e) { return e == cudaSuccess ? FSLD_OK : FSLD_ECUDA; }
+
+bool geom_ok(int M, int mode, int n_mask, int B) {
+    if (M < 2 || M > 1024) return false;
+    if (mode != FSLD_MODE_NN && mode != FSLD_MODE_TRI) return false;
+    if (n_mask < 1 || n_mask > M * M) return false;
+    if (B < 1) return false;
+    return true;
+}
+
+void tiling(int n_mask, int& tiles, int& ppt) {
+    tiles = (n_mask + kThreads * kPixPerThreadTarget - 1) / (kThreads * kPixPerThreadTarget);
+    if (tiles < 1) tiles = 1;
+    ppt = (n_mask + kThreads * tiles - 1) / (kThreads * tiles);
+}
+
+SliceArgs make_args(int M, int n_mask, const int16_t* pix, const fsld_image_rec* recs, const int32_t* idx) {
+    SliceArgs a{};
+    a.M = M;
+    a.c2 = (M + 1) / 2;
+    a.bnd = (double)(M / 2 - 1);
+    a.n_mask = n_mask;
+    tiling(n_mask, a.tiles, a.ppt);
+    a.pix = reinterpret_cast<const short2*>(pix);
+    a.recs = recs;
+    a.idx = idx;
+    return a;
+}
+
+}  // namespace
+
+extern "C" {
+
+int fsld_abi_version(void) { return FSLD_ABI_VERSION; }
+
+const char* fsld_status_string(int status) {
+    switch (status) {
+        case FSLD_OK: return "ok";
+        case FSLD_EINVAL: return "invalid argument";
+        case FSLD_ECUDA: return "CUDA error";
+        case FSLD_ENODEV: return "no compute-capability-10.x device";
+    }
+    return "unknown status";
+}
+
+int fsld_device_count(int* count) {
+    if (!count) return FSLD_EINVAL;
+    int n = 0;
+    *count = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return FSLD_ENODEV;
+    }
+    int good = 0;
+    for (int d = 0; d < n; ++d) {
+        cudaDeviceProp p;
+        if (cudaGetDeviceProperties(&p, d) == cudaSuccess && p.major == 10) ++good;
+    }
+    *count = good;
+    return good > 0 ? FSLD_OK : FSLD_ENODEV;
+}
+
+size_t fsld_scratch_bytes(int M, int n_mask, int B) {
+    (void)M;
+    int tiles, ppt;
+    tiling(n_mask > 0 ? n_mask : 1, tiles, ppt);
+    size_t blocks = (size_t)(B > 0 ? B : 1) * tiles;
+    size_t norm_parts = 148 * 8;
+    return (blocks > norm_parts ? blocks : norm_parts) * sizeof(double);
+}
+
+static int run_reducing(int op, int M, int mode, int n_mask, const int16_t* pix, const fsld_image_rec* recs,
+                        const int32_t* idx, int B, const void* v, const void* x, void* grad_acc,
+                        double* sq_out, unsigned flags, const double* fx_scale, void* scratch,
+                        size_t scratch_bytes, void* stream) {
+    if (!geom_ok(M, mode, n_mask, B)) return FSLD_EINVAL;
+    if (!pix || !recs || !idx || !v || !x || !sq_out || !scratch) return FSLD_EINVAL;
+    if (op == OP_LOSS_GRAD && !grad_acc) return FSLD_EINVAL;
+    const bool det = (flags & FSLD_DETERMINISTIC) != 0;
+    if (det && !fx_scale) return FSLD_EINVAL;
+    SliceArgs a = make_args(M, n_mask, pix, recs, idx);
+    const int nblocks = B * a.tiles;
+    if (scratch_bytes < (size_t)nblocks * sizeof(double)) return FSLD_EINVAL;
+    a.v = reinterpret_cast<const float2*>(v);
+    a.x = reinterpret_cast<const float2*>(x);
+    a.x_by_idx = 1;
+    a.acc = grad_acc;
+    a.partials = reinterpret_cast<double*>(scratch);
+    a.fx = fx_scale;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    cudaError_t e = launch_slice(op, mode, det, a, nblocks, s);
+    if (e != cudaSuccess) return FSLD_ECUDA;
+    return status_of(launch_reduce(a.partials, nblocks, sq_out, s));
+}
+
+int fsld_loss_grad(int M, int mode, int n_mask, const int16_t* pix, const fsld_image_rec* recs,
+                   const int32_t* idx, int B, const void* v, const void* x, void* grad_acc, double* sq_out,
+                   unsigned flags, const double* fx_scale, void* scratch, size_t scratch_bytes, void* stream) {
+    return run_reducing(OP_LOSS_GRAD, M, mode, n_mask, pix, recs, idx, B, v, x, grad_acc, sq_out, flags,
+                        fx_scale, scratch, scratch_bytes, stream);
+}
+
+int fsld_loss(int M, int mode, int n_mask, const int16_t* pix, const fsld_image_rec* recs, const int32_t* idx,
+              int B, const void* v, const void* x, double* sq_out, void* scratch, size_t scratch_bytes,
+              void* stream) {
+    return run_reducing(OP_LOSS, M, mode, n_mask, pix, recs, idx, B, v, x, nullptr, sq_out, 0u, nullptr,
+                        scratch, scratch_bytes, stream);
+}
+
+int fsld_project(int M, int mode, int n_mask, const int16_t* pix, const fsld_image_rec* recs,
+                 const int32_t* idx, int B, const void* v, void* out, void* stream) {
+    if (!geom_ok(M, mode, n_mask, B)) return FSLD_EINVAL;
+    if (!pix || !recs || !idx || !v || !out) return FSLD_EINVAL;
+    SliceArgs a = make_args(M, n_mask, pix, recs, idx);
+    a.v = reinterpret_cast<const float2*>(v);
+    a.out = reinterpret_cast<float2*>(out);
+    return status_of(launch_slice(OP_PROJECT, mode, false, a, B * a.tiles, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+static int run_scatter(int op, int M, int mode, int n_mask, const int16_t* pix, const fsld_image_rec* recs,
+                       const int32_t* idx, int B, const void* src, void* acc, unsigned flags,
+                       const double* fx_scale, void* stream) {
+    if (!geom_ok(M, mode, n_mask, B)) return FSLD_EINVAL;
+    if (!pix || !recs || !idx || !acc) return FSLD_EINVAL;
+    if (op != OP_DIAG && !src) return FSLD_EINVAL;
+    const bool det = (flags & FSLD_DETERMINISTIC) != 0;
+    if (det && !fx_scale) return FSLD_EINVAL;
+    SliceArgs a = make_args(M, n_mask, pix, recs, idx);
+    if (op == OP_BACKPROJECT) {
+        a.x = reinterpret_cast<const float2*>(src);
+        a.x_by_idx = 0;
+    } else {
+        a.v = reinterpret_cast<const float2*>(src);
+    }
+    a.acc = acc;
+    a.fx = fx_scale;
+    return status_of(launch_slice(op, mode, det, a, B * a.tiles, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+int fsld_backproject(int M, int mode, int n_mask, const int16_t* pix, const fsld_image_rec* recs,
+                     const int32_t* idx, int B, const void* img, void* acc, unsigned flags,
+                     const double* fx_scale, void* stream) {
+    return run_scatter(OP_BACKPROJECT, M, mode, n_mask, pix, recs, idx, B, img, acc, flags, fx_scale, stream);
+}
+
+int fsld_hvp(int M, int mode, int n_mask, const int16_t* pix, const fsld_image_rec* recs, const int32_t* idx,
+             int B, const void* z, void* acc, unsigned flags, const double* fx_scale, void* stream) {
+    return run_scatter(OP_HVP, M, mode, n_mask, pix, recs, idx, B, z, acc, flags, fx_scale, stream);
+}
+
+int fsld_exact_diag(int M, int mode, int n_mask, const int16_t* pix, const fsld_image_rec* recs,
+                    const int32_t* idx, int B, void* acc, unsigned flags, const double* fx_scale, void* stream) {
+    return run_scatter(OP_DIAG, M, mode, n_mask, pix, recs, idx, B, nullptr, acc, flags, fx_scale, stream);
+}
+
+int fsld_hutch_fold(int M, int mode, int n_mask, const int16_t* pix, const fsld_image_rec* recs,
+                    const int32_t* idx, int B, const uint32_t* zbits, int k, void* acc, unsigned flags,
+                    const double* fx_scale, void* stream) {
+    if (!geom_ok(M, mode, n_mask, B) || k < 1) return FSLD_EINVAL;
+    if (!pix || !recs || !idx || !zbits || !acc) return FSLD_EINVAL;
+    const bool det = (flags & FSLD_DETERMINISTIC) != 0;
+    if (det && !fx_scale) return FSLD_EINVAL;
+    SliceArgs a = make_args(M, n_mask, pix, recs, idx);
+    a.acc = acc;
+    a.fx = fx_scale;
+    return status_of(launch_hutch(mode, det, a, B * a.tiles, zbits, (k + 31) / 32, k,
+                                  reinterpret_cast<cudaStream_t>(stream)));
+}
+
+int fsld_pack_probes(int64_t n, int k, const double* z, uint32_t* zbits, int* bad, void* stream) {
+    if (n < 1 || k < 1 || !z || !zbits) return FSLD_EINVAL;
+    return status_of(launch_pack_probes(n, k, z, zbits, bad, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+int fsld_gen_probes(int64_t n, int k, uint64_t seed, uint32_t* zbits, void* stream) {
+    if (n < 1 || k < 1 || !zbits) return FSLD_EINVAL;
+    return status_of(launch_gen_probes(n, k, seed, zbits, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+int fsld_assign_nn(int M, int n_mask, const int16_t* pix, const fsld_image_rec* recs, const int32_t* idx, int B,
+                   int32_t* out, void* stream) {
+    if (!geom_ok(M, FSLD_MODE_NN, n_mask, B) || !pix || !recs || !idx || !out) return FSLD_EINVAL;
+    SliceArgs a = make_args(M, n_mask, pix, recs, idx);
+    return status_of(launch_assign_nn(a, B * a.tiles, out, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+int fsld_project_tab(int M, int mode, int n_mask, const int16_t* pix, const fsld_image_rec* recs, int B,
+                     const void* v, const void* ftab, void* out, void* stream) {
+    if (!geom_ok(M, mode, n_mask, B) || !pix || !recs || !v || !ftab || !out) return FSLD_EINVAL;
+    SliceArgs a = make_args(M, n_mask, pix, recs, nullptr);
+    a.v = reinterpret_cast<const float2*>(v);
+    a.ftab = reinterpret_cast<const float2*>(ftab);
+    a.out = reinterpret_cast<float2*>(out);
+    return status_of(launch_slice(OP_PROJECT, mode, false, a, B * a.tiles, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+int fsld_backproject_tab(int M, int mode, int n_mask, const int16_t* pix, const fsld_image_rec* recs, int B,
+                         const void* img, const void* ftab, void* acc, unsigned flags, const double* fx_scale,
+                         void* stream) {
+    if (!geom_ok(M, mode, n_mask, B) || !pix || !recs || !img || !ftab || !acc) return FSLD_EINVAL;
+    const bool det = (flags & FSLD_DETERMINISTIC) != 0;
+    if (det && !fx_scale) return FSLD_EINVAL;
+    SliceArgs a = make_args(M, n_mask, pix, recs, nullptr);
+    a.x = reinterpret_cast<const float2*>(img);
+    a.ftab = reinterpret_cast<const float2*>(ftab);
+    a.acc = acc;
+    a.fx = fx_scale;
+    return status_of(launch_slice(OP_BACKPROJECT, mode, det, a, B * a.tiles, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+int fsld_scatter_sq_tab(int M, int mode, int n_mask, const int16_t* pix, const fsld_image_rec* recs, int B,
+                        const void* wtab, void* acc, unsigned flags, const double* fx_scale, void* stream) {
+    if (!geom_ok(M, mode, n_mask, B) || !pix || !recs || !wtab || !acc) return FSLD_EINVAL;
+    const bool det = (flags & FSLD_DETERMINISTIC) != 0;
+    if (det && !fx_scale) return FSLD_EINVAL;
+    SliceArgs a = make_args(M, n_mask, pix, recs, nullptr);
+    a.ftab = reinterpret_cast<const float2*>(wtab);
+    a.acc = acc;
+    a.fx = fx_scale;
+    return status_of(launch_slice(OP_DIAG, mode, det, a, B * a.tiles, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+int fsld_fixed_scale(const void* data, int64_t n, double mult, double add, double* fx_scale, void* stream) {
+    if (!fx_scale || mult <= 0.0 || add < 0.0) return FSLD_EINVAL;
+    return status_of(launch_fixed_scale(reinterpret_cast<const float2*>(data), n, mult, add, fx_scale,
+                                        reinterpret_cast<cudaStream_t>(stream)));
+}
+
+int fsld_grad_finalize(int64_t nvox, const void* acc, unsigned flags, const double* fx_scale, const void* v,
+                       double scale, double lam, void* out, void* stream) {
+    const bool det = (flags & FSLD_DETERMINISTIC) != 0;
+    if (nvox < 1 || !acc || !out || (det && !fx_scale)) return FSLD_EINVAL;
+    return status_of(launch_grad_finalize(nvox, acc, det, fx_scale, reinterpret_cast<const float2*>(v), scale,
+                                          lam, reinterpret_cast<float2*>(out),
+                                          reinterpret_cast<cudaStream_t>(stream)));
+}
+
+int fsld_real_finalize(int64_t nvox, const void* acc, unsigned flags, const double* fx_scale, double scale,
+                       double add, float* out, void* stream) {
+    const bool det = (flags & FSLD_DETERMINISTIC) != 0;
+    if (nvox < 1 || !acc || !out || (det && !fx_scale)) return FSLD_EINVAL;
+    return status_of(launch_real_finalize(nvox, acc, det, fx_scale, scale, add, out,
+                                          reinterpret_cast<cudaStream_t>(stream)));
+}
+
+int fsld_norm2(int64_t n, const void* v, double* out, void* scratch, size_t scratch_bytes, void* stream) {
+    const int nparts = 148 * 8;
+    if (n < 1 || !v || !out || !scratch || scratch_bytes < nparts * sizeof(double)) return FSLD_EINVAL;
+    return status_of(launch_norm2(n, reinterpret_cast<const float2*>(v), out, reinterpret_cast<double*>(scratch),
+                                  nparts, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+}  // extern "C"

@@ -1,0 +1,331 @@
+"""Device-resident slice engine: the B200 dataset operator core.
+
+Holds one dataset in HBM in the layout of include/fsld_b200.h and enqueues
+the C-ABI kernels on the current torch CUDA stream:
+
+  pix   (n_mask, 2) int16          masked pixel frequencies (grid.disk_mask order)
+  recs  (N, 128 B) fsld_image_rec  rotation rows 0-1, shift, CTF coefficients
+  x     (N, n_mask) complex64      compact masked observed images
+  v / grad accumulators            M^3 complex64 (or int64 pairs, deterministic)
+
+Every method takes and returns torch CUDA tensors and never synchronises the
+host, except where a Python float is explicitly requested.  PyTorch is only
+the allocator / stream provider here; all arithmetic of the path runs in the
+sm_100a kernels of libfsld_b200.so.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _capi as C
+from .grid import disk_mask, pixel_coords
+
+# per-image bound on how many pixels of one image can touch one voxel's
+# 2x2x2 support (cube cross-section 4*sqrt(2) ~ 5.7 -> at most ~12 lattice points)
+HITS_PER_IMAGE = 16
+
+
+def ctypes_ptr(t) -> int:
+    return 0 if t is None else int(t.data_ptr())
+
+
+def _stream() -> int:
+    return int(torch.cuda.current_stream().cuda_stream)
+
+
+def require_device() -> torch.device:
+    """The B200 path needs a CUDA device; there is no CPU fallback."""
+    C.load()
+    if not torch.cuda.is_available():
+        raise C.FsldError("no CUDA device visible: the fsld B200 path has no CPU fallback")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+class SliceEngine:
+    """One dataset resident on one GPU (see module docstring)."""
+
+    def __init__(self, M: int, mode: str, mask: np.ndarray, recs: np.ndarray, x=None,
+                 deterministic: bool = False, device=None):
+        if mode not in ("nn", "tri"):
+            raise ValueError("mode must be one of ('nn', 'tri')")
+        self.dev = device or require_device()
+        self.M = int(M)
+        self.mode = mode
+        self.mode_id = C.MODE_TRI if mode == "tri" else C.MODE_NN
+        self.mask = np.asarray(mask, dtype=np.int64)
+        self.n_mask = int(self.mask.size)
+        self.n_voxels = self.M ** 3
+        self.deterministic = bool(deterministic)
+        self.flags = C.DETERMINISTIC if self.deterministic else 0
+        pix = pixel_coords(self.M)[self.mask].astype(np.int16)
+        self.pix = torch.from_numpy(np.ascontiguousarray(pix)).to(self.dev)
+        recs = np.ascontiguousarray(recs, dtype=C.REC_DTYPE)
+        self.n_images = int(recs.shape[0])
+        self.recs = torch.from_numpy(recs.view(np.uint8).copy()).to(self.dev)
+        self.x = None
+        self.x_maxabs = 0.0
+        if x is not None:
+            self.set_images(x)
+        self._scratch = None
+        self._bad = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        self._all_idx = None
+
+    # ---- data -----------------------------------------------------------
+    def set_images(self, x):
+        """Upload observed images (N, n_mask) as complex64 (DatasetOperator.x, forward.py:527)."""
+        if isinstance(x, torch.Tensor):
+            xd = x.to(self.dev, torch.complex64).contiguous()
+        else:
+            xd = torch.from_numpy(np.ascontiguousarray(x, dtype=np.complex64)).to(self.dev)
+        if tuple(xd.shape) != (self.n_images, self.n_mask):
+            raise ValueError(f"images shape {tuple(xd.shape)} != ({self.n_images}, {self.n_mask})")
+        self.x = xd
+        self.x_maxabs = float(torch.view_as_real(xd).abs().max().item()) * 2.0 if xd.numel() else 0.0
+
+    def idx_tensor(self, idx) -> torch.Tensor:
+        if isinstance(idx, torch.Tensor):
+            t = idx.to(self.dev, torch.int32).contiguous()
+        else:
+            a = np.asarray(idx)
+            if a.size and (a.min() < 0 or a.max() >= self.n_images):
+                raise IndexError("batch index out of range")
+            t = torch.from_numpy(np.ascontiguousarray(a, dtype=np.int32)).to(self.dev, non_blocking=True)
+        if t.numel() == 0:
+            raise ValueError("batch must be nonempty")
+        return t
+
+    def all_indices(self) -> torch.Tensor:
+        if self._all_idx is None:
+            self._all_idx = torch.arange(self.n_images, dtype=torch.int32, device=self.dev)
+        return self._all_idx
+
+    def scratch(self, B: int) -> torch.Tensor:
+        nbytes = int(C.load().fsld_scratch_bytes(self.M, self.n_mask, int(B)))
+        if self._scratch is None or self._scratch.numel() * 8 < nbytes:
+            self._scratch = torch.empty((nbytes + 7) // 8, dtype=torch.float64, device=self.dev)
+        return self._scratch
+
+    # ---- accumulators -----------------------------------------------------
+    def new_cacc(self) -> torch.Tensor:
+        """Complex accumulator (M^3): complex64, or int64 pairs when deterministic."""
+        if self.deterministic:
+            return torch.zeros((self.n_voxels, 2), dtype=torch.int64, device=self.dev)
+        return torch.zeros(self.n_voxels, dtype=torch.complex64, device=self.dev)
+
+    def new_racc(self) -> torch.Tensor:
+        if self.deterministic:
+            return torch.zeros(self.n_voxels, dtype=torch.int64, device=self.dev)
+        return torch.zeros(self.n_voxels, dtype=torch.float32, device=self.dev)
+
+    def fixed_scale(self, data, mult: float, add: float, out=None) -> torch.Tensor:
+        """Device scalar 2^k for int64 fixed-point accumulation (deterministic mode)."""
+        fx = torch.empty(1, dtype=torch.float64, device=self.dev) if out is None else out
+        n = 0 if data is None else data.numel()
+        C.check(C.load().fsld_fixed_scale(ctypes_ptr(data), n, float(mult), float(add),
+                                          ctypes_ptr(fx), _stream()), "fixed_scale")
+        return fx
+
+    def _vol(self, v) -> torch.Tensor:
+        if v.dtype != torch.complex64 or v.device != self.dev or not v.is_contiguous():
+            v = v.to(self.dev, torch.complex64).contiguous()
+        if v.numel() != self.n_voxels:
+            raise ValueError(f"volume has {v.numel()} entries, expected {self.n_voxels}")
+        return v.reshape(-1)
+
+    # ---- hot path ---------------------------------------------------------
+    def loss_grad(self, v, idx, acc=None, fx=None, fx_batch=None):
+        """sum|P v - x|^2 (device double) and acc += sum P^* conj(f) r (optim.py:147-162)."""
+        lib = C.load()
+        v = self._vol(v)
+        idx = self.idx_tensor(idx)
+        B = idx.numel()
+        acc = self.new_cacc() if acc is None else acc
+        if self.deterministic and fx is None:
+            fx = self.fixed_scale(v, HITS_PER_IMAGE * (fx_batch or B), self.x_maxabs)
+        sq = torch.empty(1, dtype=torch.float64, device=self.dev)
+        scr = self.scratch(B)
+        C.check(lib.fsld_loss_grad(self.M, self.mode_id, self.n_mask, ctypes_ptr(self.pix),
+                                   ctypes_ptr(self.recs), ctypes_ptr(idx), B, ctypes_ptr(v),
+                                   ctypes_ptr(self.x), ctypes_ptr(acc), ctypes_ptr(sq), self.flags,
+                                   ctypes_ptr(fx), ctypes_ptr(scr), scr.numel() * 8, _stream()),
+                "fsld_loss_grad")
+        return sq, acc, fx
+
+    def loss(self, v, idx):
+        """sum|P v - x|^2 over the batch, device double (optim.py:193-207 data term)."""
+        lib = C.load()
+        v = self._vol(v)
+        idx = self.idx_tensor(idx)
+        B = idx.numel()
+        sq = torch.empty(1, dtype=torch.float64, device=self.dev)
+        scr = self.scratch(B)
+        C.check(lib.fsld_loss(self.M, self.mode_id, self.n_mask, ctypes_ptr(self.pix), ctypes_ptr(self.recs),
+                              ctypes_ptr(idx), B, ctypes_ptr(v), ctypes_ptr(self.x), ctypes_ptr(sq),
+                              ctypes_ptr(scr), scr.numel() * 8, _stream()), "fsld_loss")
+        return sq
+
+    def project(self, v, idx) -> torch.Tensor:
+        lib = C.load()
+        v = self._vol(v)
+        idx = self.idx_tensor(idx)
+        out = torch.empty((idx.numel(), self.n_mask), dtype=torch.complex64, device=self.dev)
+        C.check(lib.fsld_project(self.M, self.mode_id, self.n_mask, ctypes_ptr(self.pix), ctypes_ptr(self.recs),
+                                 ctypes_ptr(idx), idx.numel(), ctypes_ptr(v), ctypes_ptr(out), _stream()),
+                "fsld_project")
+        return out
+
+    def backproject(self, imgs, idx, acc=None, fx=None, fx_batch=None):
+        lib = C.load()
+        idx = self.idx_tensor(idx)
+        B = idx.numel()
+        imgs = imgs.to(self.dev, torch.complex64).contiguous()
+        if tuple(imgs.shape) != (B, self.n_mask):
+            raise ValueError(f"images shape {tuple(imgs.shape)} != ({B}, {self.n_mask})")
+        acc = self.new_cacc() if acc is None else acc
+        if self.deterministic and fx is None:
+            fx = self.fixed_scale(imgs, HITS_PER_IMAGE * (fx_batch or B), 0.0)
+        C.check(lib.fsld_backproject(self.M, self.mode_id, self.n_mask, ctypes_ptr(self.pix),
+                                     ctypes_ptr(self.recs), ctypes_ptr(idx), B, ctypes_ptr(imgs),
+                                     ctypes_ptr(acc), self.flags, ctypes_ptr(fx), _stream()),
+                "fsld_backproject")
+        return acc, fx
+
+    def hvp_acc(self, z, idx, acc=None, fx=None, fx_batch=None):
+        lib = C.load()
+        z = self._vol(z)
+        idx = self.idx_tensor(idx)
+        B = idx.numel()
+        acc = self.new_cacc() if acc is None else acc
+        if self.deterministic and fx is None:
+            fx = self.fixed_scale(z, HITS_PER_IMAGE * (fx_batch or B), 0.0)
+        C.check(lib.fsld_hvp(self.M, self.mode_id, self.n_mask, ctypes_ptr(self.pix), ctypes_ptr(self.recs),
+                             ctypes_ptr(idx), B, ctypes_ptr(z), ctypes_ptr(acc), self.flags, ctypes_ptr(fx),
+                             _stream()), "fsld_hvp")
+        return acc, fx
+
+    def pack_probes(self, z) -> tuple[torch.Tensor, int]:
+        """(k, M^3) or (M^3,) +-1 float64 -> bit-packed (M^3, ceil(k/32)) uint32 words."""
+        lib = C.load()
+        if isinstance(z, torch.Tensor):
+            zd = z.to(self.dev, torch.float64).contiguous()
+        else:
+            zd = torch.from_numpy(np.ascontiguousarray(z, dtype=np.float64)).to(self.dev)
+        if zd.dim() == 1:
+            zd = zd.reshape(1, -1)
+        k = zd.shape[0]
+        if zd.shape[1] != self.n_voxels:
+            raise ValueError("probe length must be M^3")
+        words = (k + 31) // 32
+        zbits = torch.empty((self.n_voxels, words), dtype=torch.int32, device=self.dev)
+        self._bad.zero_()
+        C.check(lib.fsld_pack_probes(self.n_voxels, k, ctypes_ptr(zd), ctypes_ptr(zbits), ctypes_ptr(self._bad),
+                                     _stream()), "fsld_pack_probes")
+        return zbits, k
+
+    def probes_are_rademacher(self) -> bool:
+        """Host check of the last pack_probes call (synchronises)."""
+        return int(self._bad.item()) == 0
+
+    def gen_probes(self, k: int, seed: int) -> torch.Tensor:
+        lib = C.load()
+        words = (k + 31) // 32
+        zbits = torch.empty((self.n_voxels, words), dtype=torch.int32, device=self.dev)
+        C.check(lib.fsld_gen_probes(self.n_voxels, int(k), int(seed) & 0xFFFFFFFFFFFFFFFF, ctypes_ptr(zbits),
+                                    _stream()), "fsld_gen_probes")
+        return zbits
+
+    def hutch_fold(self, zbits, k: int, idx, acc=None, fx=None, fx_batch=None):
+        """acc[j] += sum_p z_p[j] (sum_b P_b^* C_b^2 P_b z_p)[j] (optim.py:210-229 numerator)."""
+        lib = C.load()
+        idx = self.idx_tensor(idx)
+        B = idx.numel()
+        acc = self.new_racc() if acc is None else acc
+        if self.deterministic and fx is None:
+            fx = self.fixed_scale(None, HITS_PER_IMAGE * (fx_batch or B) * k, 1.0)
+        C.check(lib.fsld_hutch_fold(self.M, self.mode_id, self.n_mask, ctypes_ptr(self.pix),
+                                    ctypes_ptr(self.recs), ctypes_ptr(idx), B, ctypes_ptr(zbits), int(k),
+                                    ctypes_ptr(acc), self.flags, ctypes_ptr(fx), _stream()), "fsld_hutch_fold")
+        return acc, fx
+
+    def exact_diag_acc(self, idx, acc=None, fx=None, fx_batch=None):
+        lib = C.load()
+        idx = self.idx_tensor(idx)
+        B = idx.numel()
+        acc = self.new_racc() if acc is None else acc
+        if self.deterministic and fx is None:
+            fx = self.fixed_scale(None, HITS_PER_IMAGE * (fx_batch or B), 1.0)
+        C.check(lib.fsld_exact_diag(self.M, self.mode_id, self.n_mask, ctypes_ptr(self.pix),
+                                    ctypes_ptr(self.recs), ctypes_ptr(idx), B, ctypes_ptr(acc), self.flags,
+                                    ctypes_ptr(fx), _stream()), "fsld_exact_diag")
+        return acc, fx
+
+    def assign_nn(self, idx) -> torch.Tensor:
+        lib = C.load()
+        idx = self.idx_tensor(idx)
+        out = torch.empty((idx.numel(), self.n_mask), dtype=torch.int32, device=self.dev)
+        C.check(lib.fsld_assign_nn(self.M, self.n_mask, ctypes_ptr(self.pix), ctypes_ptr(self.recs),
+                                   ctypes_ptr(idx), idx.numel(), ctypes_ptr(out), _stream()), "fsld_assign_nn")
+        return out
+
+    # ---- epilogues --------------------------------------------------------
+    def finalize_c(self, acc, fx, scale: float, lam: float, v=None, out=None) -> torch.Tensor:
+        """scale * acc + lam * v -> complex64 (optim.py:189, forward.py:570)."""
+        lib = C.load()
+        out = torch.empty(self.n_voxels, dtype=torch.complex64, device=self.dev) if out is None else out
+        vv = self._vol(v) if v is not None else None
+        C.check(lib.fsld_grad_finalize(self.n_voxels, ctypes_ptr(acc), self.flags, ctypes_ptr(fx),
+                                       ctypes_ptr(vv), float(scale), float(lam), ctypes_ptr(out), _stream()),
+                "fsld_grad_finalize")
+        return out
+
+    def finalize_r(self, acc, fx, scale: float, add: float, out=None) -> torch.Tensor:
+        lib = C.load()
+        out = torch.empty(self.n_voxels, dtype=torch.float32, device=self.dev) if out is None else out
+        C.check(lib.fsld_real_finalize(self.n_voxels, ctypes_ptr(acc), self.flags, ctypes_ptr(fx), float(scale),
+                                       float(add), ctypes_ptr(out), _stream()), "fsld_real_finalize")
+        return out
+
+    def norm2(self, v) -> torch.Tensor:
+        """||v||^2 (device double, fixed reduction order)."""
+        lib = C.load()
+        v = self._vol(v)
+        out = torch.empty(1, dtype=torch.float64, device=self.dev)
+        scr = self.scratch(1)
+        C.check(lib.fsld_norm2(self.n_voxels, ctypes_ptr(v), ctypes_ptr(out), ctypes_ptr(scr), scr.numel() * 8,
+                               _stream()), "fsld_norm2")
+        return out
+
+
+def records_for(M: int, quats, shifts=None, ctfs=None) -> np.ndarray:
+    """Build fsld_image_rec records on the host (one 128-byte record per image).
+
+    quats (N,4) unit quaternions (w,x,y,z) -> rows 0-1 of quat_to_matrix
+    (forward.py:42-51, same fp64 expression order so nn indices are
+    bit-exact); shifts (N,2) pixels -> shift = -2 t / M (forward.py:299-303);
+    ctfs: None, or a sequence of CtfParams-like (defocus, amp_contrast,
+    b_factor) / PhysicalCtf objects (see forward.ctf_coefficients).
+    """
+    from .forward import ctf_coefficients, quat_to_matrix
+
+    quats = np.asarray(quats, dtype=np.float64).reshape(-1, 4)
+    N = quats.shape[0]
+    recs = np.zeros(N, dtype=C.REC_DTYPE)
+    for i in range(N):
+        R = quat_to_matrix(quats[i])
+        recs["rot"][i] = (R[0, 0], R[0, 1], R[0, 2], R[1, 0], R[1, 1], R[1, 2])
+    if shifts is not None:
+        t = np.asarray(shifts, dtype=np.float64).reshape(N, 2)
+        recs["shift"] = -2.0 * t / M
+        recs["flags"] |= np.where(np.any(t != 0.0, axis=1), C.REC_SHIFT, 0).astype(np.uint32)
+    if ctfs is not None:
+        if len(ctfs) != N:
+            raise ValueError("ctfs length must match poses")
+        for i, c in enumerate(ctfs):
+            g, env, ws, wc = ctf_coefficients(c, M)
+            recs["gamma"][i] = g
+            recs["env"][i] = env
+            recs["wsin"][i] = ws
+            recs["wcos"][i] = wc
+        recs["flags"] |= np.uint32(C.REC_CTF)
+    return recs

@@ -1,0 +1,111 @@
+"""Grid layout contract of the reference (grid.py:9-31), restated for the B200 path.
+
+Volumes are M^3 vectors: x/y axes centred (index = k + ceil(M/2)), z axis in
+FFT order (kz < 0 -> kz + M), linear index j = (z*M + y)*M + x; the first M^2
+entries are the kz = 0 slice, which is also the image (pixel) layout.
+Masks keep points whose rounded radius is <= the cutoff (grid.py:185-196).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from functools import lru_cache
+
+import numpy as np
+
+
+@dataclass(frozen=True)
+class GridSpec:
+    """Cubic Fourier grid of side M (grid.py:50-94)."""
+
+    M: int
+
+    def __post_init__(self):
+        if self.M < 2:
+            raise ValueError(f"grid side length must be >= 2, got {self.M}")
+
+    @property
+    def n_pixels(self) -> int:
+        return self.M * self.M
+
+    @property
+    def n_voxels(self) -> int:
+        return self.M ** 3
+
+    @property
+    def half(self) -> int:
+        return self.M // 2
+
+    @property
+    def centre(self) -> int:
+        return (self.M + 1) // 2
+
+    @property
+    def max_mask_radius(self) -> int:
+        return self.half - 1
+
+    @property
+    def dc_index(self) -> int:
+        return self.centre * (self.M + 1)
+
+    def pixel_coords(self) -> np.ndarray:
+        return pixel_coords(self.M)
+
+    def voxel_coords(self) -> np.ndarray:
+        return voxel_coords(self.M)
+
+
+@lru_cache(maxsize=16)
+def _pix(M: int) -> np.ndarray:
+    k = np.arange(M, dtype=np.int64) - (M + 1) // 2
+    ky, kx = np.meshgrid(k, k, indexing="ij")
+    out = np.stack([kx.ravel(), ky.ravel()], axis=1)
+    out.setflags(write=False)
+    return out
+
+
+def pixel_coords(M: int) -> np.ndarray:
+    """(M^2, 2) int64 (kx, ky) per ascending pixel index."""
+    return _pix(int(M))
+
+
+def voxel_coords(M: int) -> np.ndarray:
+    """(M^3, 3) int64 (kx, ky, kz) per ascending voxel index."""
+    c = (M + 1) // 2
+    k = np.arange(M, dtype=np.int64) - c
+    zi = np.arange(M, dtype=np.int64)
+    kz_axis = np.where(zi < M - c, zi, zi - M)
+    kz, ky, kx = np.meshgrid(kz_axis, k, k, indexing="ij")
+    return np.stack([kx.ravel(), ky.ravel(), kz.ravel()], axis=1)
+
+
+def _as_M(spec_or_M) -> int:
+    return int(spec_or_M.M) if hasattr(spec_or_M, "M") else int(spec_or_M)
+
+
+def disk_mask(spec_or_M, mask_radius: int) -> np.ndarray:
+    """Pixel indices with rounded radius <= mask_radius, ascending (grid.py:185-189)."""
+    M = _as_M(spec_or_M)
+    if not 0 <= mask_radius <= M // 2 - 1:
+        raise ValueError(f"mask_radius must be in [0, {M // 2 - 1}] for M={M}, got {mask_radius}")
+    c = pixel_coords(M)
+    r = np.round(np.sqrt((c.astype(np.float64) ** 2).sum(axis=1))).astype(np.int64)
+    return np.flatnonzero(r <= mask_radius)
+
+
+def ball_mask(spec_or_M, mask_radius: int) -> np.ndarray:
+    """Voxel indices with rounded radius <= mask_radius, ascending (grid.py:192-196)."""
+    M = _as_M(spec_or_M)
+    if not 0 <= mask_radius <= M // 2 - 1:
+        raise ValueError(f"mask_radius must be in [0, {M // 2 - 1}] for M={M}, got {mask_radius}")
+    c = voxel_coords(M)
+    r = np.round(np.sqrt((c.astype(np.float64) ** 2).sum(axis=1))).astype(np.int64)
+    return np.flatnonzero(r <= mask_radius)
+
+
+def shell_counts(M: int, mask_radius: int) -> tuple[np.ndarray, np.ndarray]:
+    """Per-integer-radius pixel and voxel populations P_x(r), P_v(r) (grid.py:228-257)."""
+    pr = np.round(np.sqrt((pixel_coords(M).astype(np.float64) ** 2).sum(axis=1))).astype(np.int64)
+    vr = np.round(np.sqrt((voxel_coords(M).astype(np.float64) ** 2).sum(axis=1))).astype(np.int64)
+    px = np.bincount(pr[pr <= mask_radius], minlength=mask_radius + 1)
+    vx = np.bincount(vr[vr <= mask_radius], minlength=mask_radius + 1)
+    return px, vx

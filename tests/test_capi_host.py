@@ -1,0 +1,131 @@
+"""CPU-only checks of the C ABI library and the host-side logic (no kernel launches)."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+from oracle import oracle as O
+
+from paper_2311_16100_b200 import _capi as C
+from paper_2311_16100_b200.engine import records_for
+from paper_2311_16100_b200.forward import CtfParams, PhysicalCtf, quat_to_matrix
+from paper_2311_16100_b200.grid import disk_mask, pixel_coords
+from paper_2311_16100_b200.kernels import ctf_table_row
+from paper_2311_16100_b200 import synth
+
+
+def header_symbols():
+    txt = open(os.path.join(ROOT, "include", "fsld_b200.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:int|size_t|const char\*)\s+(fsld_\w+)\s*\(", txt, re.M)))
+
+
+def test_library_exports_every_header_symbol():
+    lib = C.load()
+    syms = header_symbols()
+    assert len(syms) >= 20
+    for s in syms:
+        assert hasattr(lib, s), s
+    # the ctypes signature table covers the header exactly
+    assert set(syms) == set(C.SIGNATURES)
+
+
+def test_abi_version_and_status_strings():
+    lib = C.load()
+    assert lib.fsld_abi_version() == C.ABI_VERSION
+    assert lib.fsld_status_string(C.FSLD_EINVAL) == b"invalid argument"
+    assert lib.fsld_status_string(0) == b"ok"
+
+
+def test_record_layout_is_128_bytes():
+    assert C.REC_DTYPE.itemsize == 128
+    txt = open(os.path.join(ROOT, "include", "fsld_b200.h")).read()
+    assert "double rot[6];" in txt and "double gamma[4];" in txt
+
+
+def test_invalid_arguments_rejected_without_gpu():
+    lib = C.load()
+    # empty batch -> EINVAL (reference: ValueError "batch must be nonempty")
+    st = lib.fsld_loss_grad(32, C.MODE_TRI, 749, 1, 1, 1, 0, 1, 1, 1, 1, 0, 0, 1, 1 << 20, 0)
+    assert st == C.FSLD_EINVAL
+    st = lib.fsld_project(32, 7, 749, 1, 1, 1, 4, 1, 1, 0)  # bad mode
+    assert st == C.FSLD_EINVAL
+    st = lib.fsld_loss_grad(32, C.MODE_TRI, 749, 1, 1, 1, 4, 1, 1, 1, 1, C.DETERMINISTIC, 0, 1, 1 << 20, 0)
+    assert st == C.FSLD_EINVAL  # deterministic without a fixed-point scale
+    with pytest.raises(ValueError):
+        C.check(C.FSLD_EINVAL, "x")
+
+
+def test_scratch_bytes_grows_with_batch():
+    lib = C.load()
+    assert lib.fsld_scratch_bytes(128, 12645, 512) >= 512 * 13 * 8
+    assert lib.fsld_scratch_bytes(128, 12645, 1024) > lib.fsld_scratch_bytes(128, 12645, 512)
+
+
+def test_records_rotation_rows_bitexact_with_reference_formula(golden):
+    g = golden("kernels_m16.npz")
+    recs = records_for(16, g["quats"], g["shifts"], None)
+    rt = g["rt"]
+    assert np.array_equal(recs["rot"][:, :3], rt[:, 0, :])
+    assert np.array_equal(recs["rot"][:, 3:], rt[:, 1, :])
+    assert np.allclose(recs["shift"], -2.0 * g["shifts"] / 16, rtol=0, atol=0)
+
+
+def test_inkernel_ctf_model_matches_reference_radial_table(golden):
+    g = golden("kernels_m16.npz")
+    M = 16
+    pix = O.mask_pix(M, g["mask"])
+    for i, (d, w, b) in enumerate(g["ctf_params"]):
+        row = ctf_table_row(CtfParams(d, w, b), pix, M)
+        assert np.max(np.abs(row - g["ctf"][i])) < 1e-13
+
+
+def test_inkernel_ctf_model_matches_oracle_physical_table(golden):
+    g = golden("kernels_m16.npz")
+    M = 16
+    pix = O.mask_pix(M, g["mask"])
+    for i, p in enumerate(g["phys_params"]):
+        c = PhysicalCtf(*p)
+        row = ctf_table_row(c, pix, M)
+        assert np.max(np.abs(row - g["phys_ctf"][i])) < 1e-12
+
+
+def test_phase_from_record_matches_reference_phase(golden):
+    g = golden("kernels_m16.npz")
+    M = 16
+    pix = O.mask_pix(M, g["mask"])
+    recs = records_for(M, g["quats"], g["shifts"], None)
+    ph = np.exp(1j * np.pi * (recs["shift"] @ pix.T))
+    assert np.max(np.abs(ph - g["phase"])) < 1e-13
+
+
+def test_mask_and_pixel_layout_match_oracle():
+    for M in (4, 8, 32, 64, 128):
+        assert np.array_equal(disk_mask(M, M // 2 - 1), O.disk_mask(M, M // 2 - 1))
+        assert np.array_equal(pixel_coords(M), O.pixel_coords(M))
+
+
+def test_quat_to_matrix_bitexact():
+    q = synth.haar_quaternions(50, 3)
+    for qq in q:
+        assert np.array_equal(quat_to_matrix(qq), O.quat_to_matrix(qq))
+
+
+def test_blob_volume_layout_is_reference_layout():
+    """The synthetic volume's DC sits at grid.dc_index and is the (real) total mass."""
+    M = 16
+    v = synth.gaussian_blob_volume(M, seed=0)
+    dc = ((M + 1) // 2) * (M + 1)
+    assert np.argmax(np.abs(v)) == dc
+    assert abs(v[dc].imag) < 1e-9 * abs(v[dc].real)
+    # Hermitian symmetry of the FT of a real volume: v(-k) = conj(v(k)) under the layout map
+    vc = O.voxel_coords(M)
+    j = 5 * M * M + 3 * M + 9
+    k = vc[j]
+    neg = -k
+    if np.all(neg >= -((M + 1) // 2)) and np.all(neg < M // 2):
+        zi = neg[2] if neg[2] >= 0 else neg[2] + M
+        jn = (zi * M + neg[1] + (M + 1) // 2) * M + neg[0] + (M + 1) // 2
+        assert abs(v[jn] - np.conj(v[j])) < 1e-9 * np.abs(v).max()

@@ -1,0 +1,351 @@
+"""GPU parity: the sm_100a path vs the CPU oracle (pinned to the reference) on identical inputs.
+
+Bars (BASELINE.json north_star): nn voxel indices bit-exact; projections,
+gradients, Hessian products and Hutchinson diagonals within relative L2
+1e-5 (fp32 path vs fp64 reference); SGD loss trajectory within 1e-4
+relative over 10 steps.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+
+from harness import sgd_harness
+import paper_2311_16100_b200 as F
+from paper_2311_16100_b200 import kernels as K
+from paper_2311_16100_b200 import optim as Opt
+from paper_2311_16100_b200 import synth
+from paper_2311_16100_b200.engine import SliceEngine, records_for
+from paper_2311_16100_b200.forward import CtfParams, DatasetOperator, PhysicalCtf
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-5  # relative L2, fp32 path (north_star)
+
+
+def rel(a, b):
+    return O.relative_l2(np.asarray(a), np.asarray(b))
+
+
+def radial_ctfs(params):
+    return [CtfParams(float(d), float(w), float(b)) for d, w, b in params] if len(params) else None
+
+
+def gpu_op(M, mode, mask, quats, shifts, ctfs, x, deterministic=False):
+    recs = records_for(M, quats, shifts, ctfs)
+    eng = SliceEngine(M, mode, mask, recs, x, deterministic=deterministic)
+    return DatasetOperator.from_engine(eng)
+
+
+def golden_ops(g, deterministic=False):
+    M = int(g["M"])
+    mode = str(g["mode"])
+    ctfs = radial_ctfs(g["ctf_params"])
+    op = gpu_op(M, mode, g["mask"], g["quats"], g["shifts"], ctfs, g["x"], deterministic)
+    ctab = None if ctfs is None else O.ctf_table_radial(g["ctf_params"], O.mask_pix(M, g["mask"]), M)
+    oop = O.OracleOperator(M, mode, g["mask"], g["quats"], g["shifts"], ctab, g["x"])
+    return op, oop
+
+
+# ---------------------------------------------------------------- kernels.* (table-driven)
+
+@pytest.mark.parametrize("name", ["kernels_m8.npz", "kernels_m16.npz"])
+def test_assign_nn_bitexact_golden(golden, name):
+    g = golden(name)
+    out = K.assign_nn(g["rt"], g["pix"], int(g["M"]))
+    assert np.array_equal(out, g["assign_nn"])
+
+
+@pytest.mark.parametrize("name", ["kernels_m8.npz", "kernels_m16.npz"])
+@pytest.mark.parametrize("mode", ["tri", "nn"])
+def test_numba_signature_kernels_golden(golden, name, mode):
+    g = golden(name)
+    M = int(g["M"])
+    B, n = g["phase"].shape
+    out = np.empty((B, n), dtype=np.complex128)
+    (K.project_tri if mode == "tri" else K.project_nn)(g["v"], g["rt"], g["pix"], g["phase"], g["ctf"], M, out)
+    assert rel(out, g[f"project_{mode}"]) < TOL
+    vols = np.zeros((K.n_chunks(B), M ** 3), dtype=np.complex128)
+    (K.backproject_tri if mode == "tri" else K.backproject_nn)(g["img"], g["rt"], g["pix"], g["phase"], g["ctf"],
+                                                                 M, vols)
+    assert rel(K.fold_chunks(vols), g[f"backproject_{mode}"]) < TOL
+
+
+def test_scatter_sq_tri_golden(golden):
+    g = golden("kernels_m16.npz")
+    M = int(g["M"])
+    vols = np.zeros((1, M ** 3))
+    K.scatter_sq_tri(np.ascontiguousarray(g["ctf"] ** 2), g["rt"], g["pix"], M, vols)
+    assert rel(vols[0], g["scatter_sq_tri"]) < TOL
+
+
+# ---------------------------------------------------------------- in-kernel CTF / shift model
+
+@pytest.mark.parametrize("name", ["kernels_m8.npz", "kernels_m16.npz"])
+def test_inkernel_radial_ctf_and_shift_project(golden, name):
+    g = golden(name)
+    M = int(g["M"])
+    ctfs = radial_ctfs(g["ctf_params"])
+    recs = records_for(M, g["quats"], g["shifts"], ctfs)
+    eng = SliceEngine(M, "tri", g["mask"], recs)
+    B = len(g["quats"])
+    out = eng.project(torch.from_numpy(g["v"].astype(np.complex64)).cuda(), np.arange(B))
+    assert rel(out.cpu().numpy(), g["project_tri"]) < TOL
+    acc, fx = eng.backproject(torch.from_numpy(g["img"].astype(np.complex64)).cuda(), np.arange(B))
+    assert rel(eng.finalize_c(acc, fx, 1.0, 0.0).cpu().numpy(), g["backproject_tri"]) < TOL
+
+
+def test_inkernel_physical_ctf_matches_reference_kernels_with_table(golden):
+    g = golden("kernels_m16.npz")
+    M = int(g["M"])
+    ctfs = [PhysicalCtf(*p) for p in g["phys_params"]]
+    recs = records_for(M, g["quats"], g["shifts"], ctfs)
+    eng = SliceEngine(M, "tri", g["mask"], recs)
+    B = len(g["quats"])
+    out = eng.project(torch.from_numpy(g["v"].astype(np.complex64)).cuda(), np.arange(B))
+    assert rel(out.cpu().numpy(), g["project_tri_phys"]) < TOL
+    acc, fx = eng.backproject(torch.from_numpy(g["img"].astype(np.complex64)).cuda(), np.arange(B))
+    assert rel(eng.finalize_c(acc, fx, 1.0, 0.0).cpu().numpy(), g["backproject_tri_phys"]) < TOL
+
+
+@pytest.mark.parametrize("M", [32, 64, 128])
+def test_assign_nn_bitexact_vs_oracle_large(M):
+    mask = O.disk_mask(M, M // 2 - 1)
+    q = synth.haar_quaternions(64, M)
+    eng = SliceEngine(M, "nn", mask, records_for(M, q))
+    out = eng.assign_nn(np.arange(64)).cpu().numpy().astype(np.int64)
+    ref = O.assign_nn(O.rot_table(q), O.mask_pix(M, mask), M)
+    assert np.array_equal(out, ref)
+
+
+# ---------------------------------------------------------------- DatasetOperator / optim
+
+@pytest.mark.parametrize("name", ["dataset_m16_nn.npz", "dataset_m16_tri.npz"])
+def test_dataset_operator_golden(golden, name):
+    g = golden(name)
+    op, _ = golden_ops(g)
+    M = int(g["M"])
+    lam = float(g["lam"])
+    idx = np.arange(op.n_images)
+    loss, grad = F.loss_and_grad(op, np.zeros(M ** 3, complex), idx, lam)
+    assert abs(loss - float(g["loss0_full"])) / float(g["loss0_full"]) < TOL
+    assert rel(grad, g["grad0_full"]) < TOL
+    loss, grad = F.loss_and_grad(op, g["v1"], g["batch"], lam)
+    assert abs(loss - float(g["loss1_batch"])) / float(g["loss1_batch"]) < TOL
+    assert rel(grad, g["grad1_batch"]) < TOL
+    bl = F.batch_loss(op, g["v1"], g["batch"], lam)
+    assert abs(bl - float(g["bloss1_batch"])) / float(g["bloss1_batch"]) < TOL
+    assert rel(op.hvp(g["z"], g["batch"], lam), g["hvp_batch"]) < TOL
+    assert rel(op.hvp(g["v1"], idx, lam), g["hvp_full_complex"]) < TOL
+    assert rel(op.b_vector(), g["b_vector"]) < TOL
+
+
+@pytest.mark.parametrize("name,seed", [("dataset_m16_nn.npz", 3), ("dataset_m16_tri.npz", 4)])
+def test_hutchinson_epoch_golden(golden, name, seed):
+    g = golden(name)
+    op, _ = golden_ops(g)
+    M = int(g["M"])
+    st = F.PreconditionerState.initial(M ** 3, 1.0)
+    zr = Opt.z_stream(seed)
+    for b in F.epoch_batches(op.n_images, op.n_images // 4, seed, 0):
+        F.hutchinson_update(st, op, F.rademacher(zr, M ** 3), b, float(g["lam"]))
+    assert rel(st.d_avg, g["d_avg_epoch"]) < TOL
+
+
+def test_nn_hutchinson_is_exact_diag(golden):
+    g = golden("dataset_m16_nn.npz")
+    op, _ = golden_ops(g)
+    M = int(g["M"])
+    lam = float(g["lam"])
+    st = F.PreconditionerState.initial(M ** 3, 1.0)
+    zr = Opt.z_stream(3)
+    for b in F.epoch_batches(op.n_images, op.n_images // 4, 3, 0):
+        F.hutchinson_update(st, op, F.rademacher(zr, M ** 3), b, lam)
+    exact = F.exact_diag([F.Pose(q, t) for q, t in zip(g["quats"], g["shifts"])], None, lam, "nn",
+                         F.GridSpec(M), g["mask"])
+    assert rel(exact, g["exact_diag"]) < 1e-6
+    assert rel(st.d_avg, exact) < 1e-6
+
+
+@pytest.mark.parametrize("name", ["dataset_m16_nn.npz", "dataset_m16_tri.npz"])
+def test_exact_diag_golden(golden, name):
+    g = golden(name)
+    M = int(g["M"])
+    poses = [F.Pose(q, t) for q, t in zip(g["quats"], g["shifts"])]
+    d = F.exact_diag(poses, radial_ctfs(g["ctf_params"]), float(g["lam"]), str(g["mode"]), F.GridSpec(M),
+                     g["mask"])
+    assert rel(d, g["exact_diag"]) < TOL
+
+
+class _GpuNS:
+    """The harness namespace bound to the B200 facade (numpy in/out, reference semantics)."""
+    new_state = staticmethod(lambda n, a: F.PreconditionerState.initial(n, a))
+    z_stream = staticmethod(Opt.z_stream)
+    rademacher = staticmethod(F.rademacher)
+    epoch_batches = staticmethod(F.epoch_batches)
+    hutchinson_update = staticmethod(F.hutchinson_update)
+    ema_and_threshold = staticmethod(F.ema_and_threshold)
+    loss_and_grad = staticmethod(F.loss_and_grad)
+    batch_loss = staticmethod(F.batch_loss)
+
+    @staticmethod
+    def armijo_search(v, grad, dhat, loss_fn, eta, c, f0):
+        return F.armijo_search(v, grad, dhat, loss_fn, eta, c, f0=f0)
+
+
+@pytest.mark.parametrize("name,seed", [("dataset_m16_nn.npz", 3), ("dataset_m16_tri.npz", 4)])
+def test_sgd_trajectory_10_steps(golden, name, seed):
+    g = golden(name)
+    op, _ = golden_ops(g)
+    rec, v, st = sgd_harness(_GpuNS, op, op.spec.M ** 3, op.n_images, float(g["lam"]), float(g["alpha"]),
+                             int(g["batch"].size), seed, 10)
+    ref = g["sgd_rec"]
+    assert np.max(np.abs(rec[:, 0] - ref[:, 0]) / np.abs(ref[:, 0])) < 1e-4  # f0 per step
+    assert np.max(np.abs(rec[:, 2] - ref[:, 2]) / np.abs(ref[:, 2])) < 1e-4  # accepted loss
+    assert np.array_equal(rec[:, 1], ref[:, 1])  # identical step sizes (Armijo decisions)
+    assert rel(v, g["sgd_v_end"]) < 1e-4
+
+
+# ---------------------------------------------------------------- deterministic mode
+
+def test_deterministic_mode_bitwise_repeatable_and_close(golden):
+    g = golden("dataset_m16_tri.npz")
+    opd, _ = golden_ops(g, deterministic=True)
+    op, _ = golden_ops(g)
+    lam = float(g["lam"])
+    l1, g1 = F.loss_and_grad(opd, g["v1"], g["batch"], lam)
+    l2, g2 = F.loss_and_grad(opd, g["v1"], g["batch"], lam)
+    assert l1 == l2 and np.array_equal(g1.view(np.uint64), g2.view(np.uint64))
+    l3, g3 = F.loss_and_grad(op, g["v1"], g["batch"], lam)
+    assert rel(g1, g3) < TOL
+    assert rel(g1, g["grad1_batch"]) < TOL
+    # batch order does not matter bitwise (integer accumulation)
+    l4, g4 = F.loss_and_grad(opd, g["v1"], g["batch"][::-1].copy(), lam)
+    assert np.array_equal(g1.view(np.uint64), g4.view(np.uint64))
+
+
+# ---------------------------------------------------------------- probe batcher
+
+@pytest.mark.parametrize("k", [1, 5, 37, 64])
+def test_probe_batcher_matches_k_single_probe_samples(k):
+    M = 32
+    mask = O.disk_mask(M, M // 2 - 1)
+    N = 40
+    q = synth.haar_quaternions(N, 7)
+    sh = synth.normal_shifts(N, 8)
+    ctfs = synth.physical_ctfs(N, 9)
+    pix = O.mask_pix(M, mask)
+    oop = O.OracleOperator(M, "tri", mask, q, sh, O.ctf_table_physical(synth.ctf_param_array(ctfs), pix, M), None)
+    op = gpu_op(M, "tri", mask, q, sh, ctfs, np.zeros((N, mask.size), np.complex64))
+    rng = np.random.default_rng(k)
+    Z = rng.integers(0, 2, size=(k, M ** 3)).astype(np.float64) * 2 - 1
+    batch = np.arange(N)
+    lam = 0.5
+    ref = np.mean([z * oop.hvp(z, batch, lam).real for z in Z], axis=0)
+    got, kk = Opt.hutchinson_sample(op, Z, batch, lam)
+    assert kk == k
+    assert rel(got, ref) < TOL
+
+
+# ---------------------------------------------------------------- SPEC known-answer tests on GPU
+
+def test_kat_90deg_permutation_m4_gpu():
+    M = 4
+    mask = O.disk_mask(M, 1)
+    s = np.sqrt(0.5)
+    eng = SliceEngine(M, "nn", mask, records_for(M, [[s, 0, 0, s]]))
+    v = torch.arange(M ** 3, dtype=torch.float32).to(torch.complex64).cuda()
+    out = eng.project(v, [0]).cpu().numpy()
+    assert list(out[0].real.astype(int)) == [13, 9, 5, 14, 10, 6, 15, 11, 7]
+
+
+@pytest.mark.parametrize("mode", ["nn", "tri"])
+def test_kat_identity_pose_is_z0_slice_gpu(mode):
+    M = 32
+    mask = O.disk_mask(M, M // 2 - 1)
+    v = np.random.default_rng(0).standard_normal(M ** 3).astype(np.complex64)
+    eng = SliceEngine(M, mode, mask, records_for(M, [[1.0, 0, 0, 0]]))
+    out = eng.project(torch.from_numpy(v).cuda(), [0]).cpu().numpy()
+    assert np.array_equal(out[0], v[mask])
+
+
+def test_kat_shift_phase_gpu():
+    M = 8
+    mask = O.disk_mask(M, M // 2 - 1)
+    eng = SliceEngine(M, "nn", mask, records_for(M, [[1.0, 0, 0, 0]], [[1.0, 0.0]]))
+    v = torch.ones(M ** 3, dtype=torch.complex64).cuda()
+    out = eng.project(v, [0]).cpu().numpy()[0]
+    pix = O.mask_pix(M, mask)
+    k1 = np.flatnonzero((pix[:, 0] == 1) & (pix[:, 1] == 0))[0]
+    assert abs(out[k1] - np.exp(-2j * np.pi / M)) < 1e-6
+
+
+def test_empty_batch_raises_value_error(golden):
+    g = golden("dataset_m16_nn.npz")
+    op, _ = golden_ops(g)
+    with pytest.raises(ValueError):
+        F.loss_and_grad(op, np.zeros(16 ** 3, complex), np.array([], dtype=int), 0.1)
+    with pytest.raises(ValueError):
+        op.hvp(np.zeros(16 ** 3), np.array([], dtype=int), 0.1)
+
+
+# ---------------------------------------------------------------- full-size, size-independent properties
+
+@pytest.mark.parametrize("M,mode", [(128, "tri"), (128, "nn"), (256, "tri")])
+def test_adjointness_full_size(M, mode):
+    """<P v, y> = <v, P^* y> at BASELINE sizes with the physical CTF and shifts."""
+    B = 64
+    mask = O.disk_mask(M, M // 2 - 1)
+    q = synth.haar_quaternions(B, 11)
+    recs = records_for(M, q, synth.normal_shifts(B, 12), synth.physical_ctfs(B, 13))
+    eng = SliceEngine(M, mode, mask, recs)
+    gen = torch.Generator(device="cuda").manual_seed(0)
+    v = torch.randn(M ** 3, dtype=torch.complex64, device="cuda", generator=gen)
+    y = torch.randn((B, mask.size), dtype=torch.complex64, device="cuda", generator=gen)
+    idx = np.arange(B)
+    pv = eng.project(v, idx)
+    acc, fx = eng.backproject(y, idx)
+    pty = eng.finalize_c(acc, fx, 1.0, 0.0)
+    lhs = torch.vdot(y.reshape(-1).to(torch.complex128), pv.reshape(-1).to(torch.complex128))
+    rhs = torch.vdot(pty.to(torch.complex128), v.to(torch.complex128))
+    assert abs(complex(lhs - rhs)) / abs(complex(lhs)) < 1e-5
+
+
+def test_loss_grad_vs_oracle_cfg3_subset():
+    """cfg3 shapes (M=128, physical CTF, shifts, tri) on a 64-image batch vs the fp64 oracle."""
+    M = 128
+    B = 64
+    mask = O.disk_mask(M, M // 2 - 1)
+    pix = O.mask_pix(M, mask)
+    v = synth.gaussian_blob_volume(M, 0)
+    q = synth.haar_quaternions(B, 1)
+    sh = synth.normal_shifts(B, 2)
+    ctfs = synth.physical_ctfs(B, 3)
+    ctab = O.ctf_table_physical(synth.ctf_param_array(ctfs), pix, M)
+    rng = np.random.default_rng(5)
+    clean = O.project("tri", v, O.rot_table(q), pix, O.phase_table(sh, pix, M), ctab, M)
+    x = clean + 0.5 * np.sqrt(np.mean(np.abs(clean) ** 2)) * (rng.standard_normal(clean.shape)
+                                                               + 1j * rng.standard_normal(clean.shape))
+    oop = O.OracleOperator(M, "tri", mask, q, sh, ctab, x)
+    op = gpu_op(M, "tri", mask, q, sh, ctfs, x)
+    v1 = v * (1 + 0.05 * rng.standard_normal(v.size))
+    batch = np.arange(B)
+    lam = 1e-3
+    lr, gr = O.loss_and_grad(oop, v1, batch, lam, n_total=50000)
+    lg, gg = F.loss_and_grad(op, v1, batch, lam, n_total=50000)
+    assert abs(lg - lr) / lr < TOL
+    assert rel(gg, gr) < TOL
+    assert rel(op.project(v1, batch), oop.project(v1, batch)) < TOL
+
+
+def test_device_resident_loss_grad_matches_numpy_api():
+    wl = synth.build_workload(synth.CONFIGS["cfg2"], seed=0, n_images=512)
+    op = DatasetOperator.from_engine(wl.engine)
+    batch = np.arange(0, 512, 2)
+    v = wl.v_true * 0.9
+    l_np, g_np = F.loss_and_grad(op, v, batch, 1e-3)
+    vd = torch.from_numpy(v.astype(np.complex64)).cuda()
+    l_d, g_d = F.loss_and_grad(op, vd, torch.from_numpy(batch).cuda(), 1e-3)
+    assert abs(float(l_d) - l_np) / l_np < 1e-6
+    assert rel(g_d.cpu().numpy(), g_np) < 1e-6
