@@ -27,7 +27,8 @@
  *  - images: (rows, n_mask) complex64, compact masked (DatasetOperator.x,
  *    forward.py:527);
  *  - batch: `idx` (B,) int32 row numbers into the per-image records and the
- *    image rows (DatasetOperator.project(values, idx), forward.py:540-545).
+ *    image rows (DatasetOperator.project(values, idx), forward.py:540-545);
+ *    idx may be NULL, meaning batch entry b uses record (and image row) b.
  */
 #ifndef FSLD_B200_H
 #define FSLD_B200_H

@@ -90,7 +90,7 @@ static int run_reducing(int op, int M, int mode, int n_mask, const int16_t* pix,
                         double* sq_out, unsigned flags, const double* fx_scale, void* scratch,
                         size_t scratch_bytes, void* stream) {
     if (!geom_ok(M, mode, n_mask, B)) return FSLD_EINVAL;
-    if (!pix || !recs || !idx || !v || !x || !sq_out || !scratch) return FSLD_EINVAL;
+    if (!pix || !recs || !v || !x || !sq_out || !scratch) return FSLD_EINVAL;
     if (op == OP_LOSS_GRAD && !grad_acc) return FSLD_EINVAL;
     const bool det = (flags & FSLD_DETERMINISTIC) != 0;
     if (det && !fx_scale) return FSLD_EINVAL;
@@ -126,7 +126,7 @@ int fsld_loss(int M, int mode, int n_mask, const int16_t* pix, const fsld_image_
 int fsld_project(int M, int mode, int n_mask, const int16_t* pix, const fsld_image_rec* recs,
                  const int32_t* idx, int B, const void* v, void* out, void* stream) {
     if (!geom_ok(M, mode, n_mask, B)) return FSLD_EINVAL;
-    if (!pix || !recs || !idx || !v || !out) return FSLD_EINVAL;
+    if (!pix || !recs || !v || !out) return FSLD_EINVAL;
     SliceArgs a = make_args(M, n_mask, pix, recs, idx);
     a.v = reinterpret_cast<const float2*>(v);
     a.out = reinterpret_cast<float2*>(out);
@@ -137,7 +137,7 @@ static int run_scatter(int op, int M, int mode, int n_mask, const int16_t* pix, 
                        const int32_t* idx, int B, const void* src, void* acc, unsigned flags,
                        const double* fx_scale, void* stream) {
     if (!geom_ok(M, mode, n_mask, B)) return FSLD_EINVAL;
-    if (!pix || !recs || !idx || !acc) return FSLD_EINVAL;
+    if (!pix || !recs || !acc) return FSLD_EINVAL;
     if (op != OP_DIAG && !src) return FSLD_EINVAL;
     const bool det = (flags & FSLD_DETERMINISTIC) != 0;
     if (det && !fx_scale) return FSLD_EINVAL;
@@ -173,7 +173,7 @@ int fsld_hutch_fold(int M, int mode, int n_mask, const int16_t* pix, const fsld_
                     const int32_t* idx, int B, const uint32_t* zbits, int k, void* acc, unsigned flags,
                     const double* fx_scale, void* stream) {
     if (!geom_ok(M, mode, n_mask, B) || k < 1) return FSLD_EINVAL;
-    if (!pix || !recs || !idx || !zbits || !acc) return FSLD_EINVAL;
+    if (!pix || !recs || !zbits || !acc) return FSLD_EINVAL;
     const bool det = (flags & FSLD_DETERMINISTIC) != 0;
     if (det && !fx_scale) return FSLD_EINVAL;
     SliceArgs a = make_args(M, n_mask, pix, recs, idx);
@@ -195,7 +195,7 @@ int fsld_gen_probes(int64_t n, int k, uint64_t seed, uint32_t* zbits, void* stre
 
 int fsld_assign_nn(int M, int n_mask, const int16_t* pix, const fsld_image_rec* recs, const int32_t* idx, int B,
                    int32_t* out, void* stream) {
-    if (!geom_ok(M, FSLD_MODE_NN, n_mask, B) || !pix || !recs || !idx || !out) return FSLD_EINVAL;
+    if (!geom_ok(M, FSLD_MODE_NN, n_mask, B) || !pix || !recs || !out) return FSLD_EINVAL;
     SliceArgs a = make_args(M, n_mask, pix, recs, idx);
     return status_of(launch_assign_nn(a, B * a.tiles, out, reinterpret_cast<cudaStream_t>(stream)));
 }
