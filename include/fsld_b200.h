@@ -54,6 +54,7 @@ extern "C" {
 
 /* flags */
 #define FSLD_DETERMINISTIC 1u /* accumulate in int64 fixed point: bitwise repeatable */
+#define FSLD_TILE_PATH 2u     /* force the per-pixel tile kernel (global atomics) instead of bricks */
 
 /* fsld_image_rec.flags */
 #define FSLD_REC_CTF 1u
@@ -84,7 +85,9 @@ typedef struct fsld_image_rec {
     double env;
     float wsin, wcos;
     uint32_t flags;
-    uint32_t pad[3];
+    float xmax;        /* >= max |x(p)| over this image's masked pixels (bounds the
+                          fixed-point brick accumulator; set when images are uploaded) */
+    uint32_t pad[2];
 } fsld_image_rec;
 
 int fsld_abi_version(void);
@@ -93,10 +96,19 @@ const char* fsld_status_string(int status);
 int fsld_device_count(int* count);
 
 /*
- * Scratch bytes needed by the reducing entry points for a batch of B images
- * (per-block partial sums, reduced in a fixed order -> deterministic loss).
+ * Scratch bytes needed by the reducing entry points for batches of up to B
+ * images: prepared geometry (pixel lookup, mask rows), brick binning work
+ * space and per-CTA partial sums (reduced in a fixed order).
  */
 size_t fsld_scratch_bytes(int M, int n_mask, int B);
+
+/*
+ * Prepare `scratch` for a grid/mask (once per scratch buffer and mask, like a
+ * plan): pixel -> compact-index lookup, per-row mask extents, max radius.
+ * fsld_loss_grad / fsld_loss require a prepared scratch; an unprepared one
+ * makes them return a NaN loss.
+ */
+int fsld_prepare(int M, int n_mask, const int16_t* pix, void* scratch, size_t scratch_bytes, void* stream);
 
 /*
  * Fused slice -> CTF/shift -> residual -> |r|^2 -> adjoint scatter.

@@ -21,6 +21,7 @@ FSLD_ENODEV = -3
 MODE_NN = 0
 MODE_TRI = 1
 DETERMINISTIC = 1
+TILE_PATH = 2
 REC_CTF = 1
 REC_SHIFT = 2
 ABI_VERSION = 1
@@ -34,7 +35,8 @@ REC_DTYPE = np.dtype([
     ("wsin", "<f4"),
     ("wcos", "<f4"),
     ("flags", "<u4"),
-    ("pad", "<u4", (3,)),
+    ("xmax", "<f4"),
+    ("pad", "<u4", (2,)),
 ])
 assert REC_DTYPE.itemsize == 128
 
@@ -51,6 +53,7 @@ SIGNATURES = {
     "fsld_status_string": (ctypes.c_char_p, [I]),
     "fsld_device_count": (I, [P]),
     "fsld_scratch_bytes": (SZ, [I, I, I]),
+    "fsld_prepare": (I, [I, I, P, P, SZ, P]),
     "fsld_loss_grad": (I, [I, I, I, P, P, P, I, P, P, P, P, U, P, P, SZ, P]),
     "fsld_loss": (I, [I, I, I, P, P, P, I, P, P, P, P, SZ, P]),
     "fsld_project": (I, [I, I, I, P, P, P, I, P, P, P]),

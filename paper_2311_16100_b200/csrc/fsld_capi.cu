@@ -77,12 +77,16 @@ int fsld_device_count(int* count) {
 }
 
 size_t fsld_scratch_bytes(int M, int n_mask, int B) {
-    (void)M;
-    int tiles, ppt;
-    tiling(n_mask > 0 ? n_mask : 1, tiles, ppt);
-    size_t blocks = (size_t)(B > 0 ? B : 1) * tiles;
-    size_t norm_parts = 148 * 8;
-    return (blocks > norm_parts ? blocks : norm_parts) * sizeof(double);
+    if (M < 2 || M > 1024) return 0;
+    return scratch_layout(M, n_mask > 0 ? n_mask : 1, B > 0 ? B : 1).total;
+}
+
+int fsld_prepare(int M, int n_mask, const int16_t* pix, void* scratch, size_t scratch_bytes, void* stream) {
+    if (M < 2 || M > 1024 || n_mask < 1 || n_mask > M * M || !pix || !scratch) return FSLD_EINVAL;
+    const ScratchLayout L = scratch_layout(M, n_mask, 1);
+    if (scratch_bytes < L.total) return FSLD_EINVAL;
+    return status_of(launch_geom_prepare(M, n_mask, reinterpret_cast<const short2*>(pix), L,
+                                         reinterpret_cast<char*>(scratch), reinterpret_cast<cudaStream_t>(stream)));
 }
 
 static int run_reducing(int op, int M, int mode, int n_mask, const int16_t* pix, const fsld_image_rec* recs,
@@ -94,16 +98,47 @@ static int run_reducing(int op, int M, int mode, int n_mask, const int16_t* pix,
     if (op == OP_LOSS_GRAD && !grad_acc) return FSLD_EINVAL;
     const bool det = (flags & FSLD_DETERMINISTIC) != 0;
     if (det && !fx_scale) return FSLD_EINVAL;
+    const ScratchLayout L = scratch_layout(M, n_mask, B);
+    if (scratch_bytes < L.total) return FSLD_EINVAL;
+    char* scr = reinterpret_cast<char*>(scratch);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (op == OP_LOSS_GRAD && mode == FSLD_MODE_TRI && !det && !(flags & FSLD_TILE_PATH)) {
+        BrickArgs b{};
+        b.M = M;
+        b.c = (M + 1) / 2;
+        b.nb = L.nb;
+        b.nbr = L.nbr;
+        b.n_mask = n_mask;
+        b.B = B;
+        b.bnd = (float)(M / 2 - 1);
+        b.pix2p = reinterpret_cast<const int*>(scr + L.pix2p);
+        b.rowmin = reinterpret_cast<const int*>(scr + L.rowmin);
+        b.rowmax = reinterpret_cast<const int*>(scr + L.rowmax);
+        b.hdr = reinterpret_cast<const GeomHeader*>(scr + L.hdr);
+        b.recs = recs;
+        b.idx = idx;
+        b.v = reinterpret_cast<const float2*>(v);
+        b.x = reinterpret_cast<const float2*>(x);
+        b.acc = reinterpret_cast<float2*>(grad_acc);
+        b.cnt = reinterpret_cast<int*>(scr + L.cnt);
+        b.off = reinterpret_cast<int*>(scr + L.off);
+        b.fill = reinterpret_cast<int*>(scr + L.fill);
+        b.pairs = reinterpret_cast<int*>(scr + L.pairs);
+        b.items = reinterpret_cast<int4*>(scr + L.items);
+        b.ctl = reinterpret_cast<int*>(scr + L.ctl);
+        b.part = reinterpret_cast<double*>(scr + L.part);
+        b.cap_pairs = L.cap_pairs;
+        b.cap_items = L.cap_items;
+        return status_of(launch_brick_loss_grad(b, sq_out, s));
+    }
     SliceArgs a = make_args(M, n_mask, pix, recs, idx);
     const int nblocks = B * a.tiles;
-    if (scratch_bytes < (size_t)nblocks * sizeof(double)) return FSLD_EINVAL;
     a.v = reinterpret_cast<const float2*>(v);
     a.x = reinterpret_cast<const float2*>(x);
     a.x_by_idx = 1;
     a.acc = grad_acc;
-    a.partials = reinterpret_cast<double*>(scratch);
+    a.partials = reinterpret_cast<double*>(scr + L.part);
     a.fx = fx_scale;
-    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     cudaError_t e = launch_slice(op, mode, det, a, nblocks, s);
     if (e != cudaSuccess) return FSLD_ECUDA;
     return status_of(launch_reduce(a.partials, nblocks, sq_out, s));
@@ -262,6 +297,7 @@ int fsld_real_finalize(int64_t nvox, const void* acc, unsigned flags, const doub
 int fsld_norm2(int64_t n, const void* v, double* out, void* scratch, size_t scratch_bytes, void* stream) {
     const int nparts = 148 * 8;
     if (n < 1 || !v || !out || !scratch || scratch_bytes < nparts * sizeof(double)) return FSLD_EINVAL;
+    // uses the first nparts doubles of the caller's scratch (a dedicated buffer, or any free region)
     return status_of(launch_norm2(n, reinterpret_cast<const float2*>(v), out, reinterpret_cast<double*>(scratch),
                                   nparts, reinterpret_cast<cudaStream_t>(stream)));
 }

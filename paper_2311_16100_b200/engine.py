@@ -46,7 +46,7 @@ class SliceEngine:
     """One dataset resident on one GPU (see module docstring)."""
 
     def __init__(self, M: int, mode: str, mask: np.ndarray, recs: np.ndarray, x=None,
-                 deterministic: bool = False, device=None):
+                 deterministic: bool = False, device=None, tile_path: bool = False):
         if mode not in ("nn", "tri"):
             raise ValueError("mode must be one of ('nn', 'tri')")
         self.dev = device or require_device()
@@ -57,7 +57,7 @@ class SliceEngine:
         self.n_mask = int(self.mask.size)
         self.n_voxels = self.M ** 3
         self.deterministic = bool(deterministic)
-        self.flags = C.DETERMINISTIC if self.deterministic else 0
+        self.flags = (C.DETERMINISTIC if self.deterministic else 0) | (C.TILE_PATH if tile_path else 0)
         pix = pixel_coords(self.M)[self.mask].astype(np.int16)
         self.pix = torch.from_numpy(np.ascontiguousarray(pix)).to(self.dev)
         recs = np.ascontiguousarray(recs, dtype=C.REC_DTYPE)
@@ -81,7 +81,13 @@ class SliceEngine:
         if tuple(xd.shape) != (self.n_images, self.n_mask):
             raise ValueError(f"images shape {tuple(xd.shape)} != ({self.n_images}, {self.n_mask})")
         self.x = xd
-        self.x_maxabs = float(torch.view_as_real(xd).abs().max().item()) * 2.0 if xd.numel() else 0.0
+        if xd.numel():
+            # per-image max |x| into fsld_image_rec.xmax (bounds the brick fixed-point accumulator)
+            xm = xd.abs().amax(dim=1).float() * (1.0 + 1e-6)
+            self.recs.view(torch.float32).view(self.n_images, 32)[:, 29] = xm
+            self.x_maxabs = float(xm.max().item())
+        else:
+            self.x_maxabs = 0.0
 
     def idx_tensor(self, idx) -> torch.Tensor:
         if isinstance(idx, torch.Tensor):
@@ -101,9 +107,13 @@ class SliceEngine:
         return self._all_idx
 
     def scratch(self, B: int) -> torch.Tensor:
-        nbytes = int(C.load().fsld_scratch_bytes(self.M, self.n_mask, int(B)))
+        """Prepared scratch (fsld_prepare) large enough for batches of B images."""
+        lib = C.load()
+        nbytes = int(lib.fsld_scratch_bytes(self.M, self.n_mask, int(B)))
         if self._scratch is None or self._scratch.numel() * 8 < nbytes:
             self._scratch = torch.empty((nbytes + 7) // 8, dtype=torch.float64, device=self.dev)
+            C.check(lib.fsld_prepare(self.M, self.n_mask, ctypes_ptr(self.pix), ctypes_ptr(self._scratch),
+                                     self._scratch.numel() * 8, _stream()), "fsld_prepare")
         return self._scratch
 
     # ---- accumulators -----------------------------------------------------
@@ -268,6 +278,11 @@ class SliceEngine:
                                    ctypes_ptr(idx), idx.numel(), ctypes_ptr(out), _stream()), "fsld_assign_nn")
         return out
 
+    def _norm_scratch(self) -> torch.Tensor:
+        if getattr(self, "_nscr", None) is None:
+            self._nscr = torch.empty(148 * 8, dtype=torch.float64, device=self.dev)
+        return self._nscr
+
     # ---- epilogues --------------------------------------------------------
     def finalize_c(self, acc, fx, scale: float, lam: float, v=None, out=None) -> torch.Tensor:
         """scale * acc + lam * v -> complex64 (optim.py:189, forward.py:570)."""
@@ -291,7 +306,7 @@ class SliceEngine:
         lib = C.load()
         v = self._vol(v)
         out = torch.empty(1, dtype=torch.float64, device=self.dev)
-        scr = self.scratch(1)
+        scr = self._norm_scratch()
         C.check(lib.fsld_norm2(self.n_voxels, ctypes_ptr(v), ctypes_ptr(out), ctypes_ptr(scr), scr.numel() * 8,
                                _stream()), "fsld_norm2")
         return out
