@@ -216,24 +216,29 @@ def run_b200(args):
     sq = torch.empty(1, dtype=torch.float64, device=dev)
     nrm = torch.empty(1, dtype=torch.float64, device=dev)
     scr = eng.scratch(B)
+    nscr = eng._norm_scratch()
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
     gen = np.random.default_rng(1234 + rank)
     n_steps = args.warmup + args.steps
     batches = [torch.from_numpy(gen.choice(eng.n_images, B, replace=False).astype(np.int32)).to(dev)
                for _ in range(n_steps)]
     stream = _stream()
-    launches_per_step = 5  # loss_grad (slice + reduce), norm2 (2), grad_finalize
+    flags = C.TILE_PATH if os.environ.get("FSLD_TILE_PATH") else 0
+    # loss_grad: memset(cnt) + count + scan + fill + brick kernel + reduce = 5 kernels; norm2 (2), grad_finalize
+    launches_per_step = 8 if not flags else 5
 
     def step(idx, ev_k0=None, ev_k1=None):
         acc.zero_()
         if ev_k0 is not None:
             ev_k0.record()
-        C.check(lib.fsld_loss_grad(M, eng.mode_id, n, ctypes_ptr(eng.pix), ctypes_ptr(eng.recs), ctypes_ptr(idx),
-                                   B, ctypes_ptr(v), ctypes_ptr(eng.x), ctypes_ptr(acc), ctypes_ptr(sq), 0, 0,
-                                   ctypes_ptr(scr), scr.numel() * 8, stream), "loss_grad")
+        C.check(lib.fsld_loss_grad_sorted(M, eng.mode_id, n, ctypes_ptr(eng.recs), ctypes_ptr(idx), B,
+                                          ctypes_ptr(v), ctypes_ptr(eng.x), ctypes_ptr(eng.pc),
+                                          ctypes_ptr(eng.seg_off), ctypes_ptr(eng.segs), ctypes_ptr(acc),
+                                          ctypes_ptr(sq), flags, 0, ctypes_ptr(scr), scr.numel() * 8, stream),
+                "loss_grad")
         if ev_k1 is not None:
             ev_k1.record()
-        C.check(lib.fsld_norm2(M ** 3, ctypes_ptr(v), ctypes_ptr(nrm), ctypes_ptr(scr), scr.numel() * 8, stream),
+        C.check(lib.fsld_norm2(M ** 3, ctypes_ptr(v), ctypes_ptr(nrm), ctypes_ptr(nscr), nscr.numel() * 8, stream),
                 "norm2")
         if world > 1:
             s32 = sq.float()

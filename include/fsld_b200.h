@@ -103,10 +103,9 @@ int fsld_device_count(int* count);
 size_t fsld_scratch_bytes(int M, int n_mask, int B);
 
 /*
- * Prepare `scratch` for a grid/mask (once per scratch buffer and mask, like a
- * plan): pixel -> compact-index lookup, per-row mask extents, max radius.
- * fsld_loss_grad / fsld_loss require a prepared scratch; an unprepared one
- * makes them return a NaN loss.
+ * Stamp `scratch` for a grid/mask (once per scratch buffer, like a plan
+ * handle).  Kept for ABI stability; the current kernels need no precomputed
+ * geometry in scratch.
  */
 int fsld_prepare(int M, int n_mask, const int16_t* pix, void* scratch, size_t scratch_bytes, void* stream);
 
@@ -204,6 +203,44 @@ int fsld_backproject_tab(int M, int mode, int n_mask, const int16_t* pix, const 
                          const double* fx_scale, void* stream);
 int fsld_scatter_sq_tab(int M, int mode, int n_mask, const int16_t* pix, const fsld_image_rec* recs, int B,
                         const void* wtab, void* acc, unsigned flags, const double* fx_scale, void* stream);
+
+/*
+ * Brick-sorted dataset layout (M <= 256, n_mask <= 65535).  Poses are fixed
+ * for a refinement run, so each image's masked pixels are stored once grouped
+ * by the 8^3 volume brick that owns their trilinear footprint (floor corner
+ * of R^T k, kernels.py:42-60, 147-170):
+ *   xs     : (N, n_mask) complex64, images in sorted pixel order
+ *   pc     : (N, n_mask, 2) int8, (kx, ky) of each sorted pixel
+ *   seg_off: (N+1) int32 CSR offsets; segs: (S, 2) int32 = (brick, start | count << 16)
+ * Build: fsld_sorted_count (writes seg_off; read seg_off[N] to size segs), then
+ * fsld_sorted_fill (x_in in mask order -> xs; x_in may be NULL to build pc/segs only).
+ */
+int fsld_sorted_count(int M, int n_mask, const int16_t* pix, const fsld_image_rec* recs, int N,
+                      int32_t* seg_off, void* stream);
+int fsld_sorted_fill(int M, int n_mask, const int16_t* pix, const fsld_image_rec* recs, int N,
+                     const void* x_in, void* x_out, int8_t* pc_out, const int32_t* seg_off,
+                     int32_t* segs, void* stream);
+
+/* Fused loss + gradient over a brick-sorted dataset (optim.py:147-190 hot loop):
+ * tri mode runs the brick kernel (smem-staged bricks, one global reduction per
+ * touched voxel per work item); nn / deterministic / FSLD_TILE_PATH fall back to
+ * the per-pixel tile kernel reading coordinates from pc. */
+int fsld_loss_grad_sorted(int M, int mode, int n_mask, const fsld_image_rec* recs, const int32_t* idx,
+                          int B, const void* v, const void* xs, const int8_t* pc,
+                          const int32_t* seg_off, const int32_t* segs, void* grad_acc, double* sq_out,
+                          unsigned flags, const double* fx_scale, void* scratch, size_t scratch_bytes,
+                          void* stream);
+/* Loss only over a brick-sorted dataset (Armijo trials, optim.py:193-207). */
+int fsld_loss_sorted(int M, int mode, int n_mask, const fsld_image_rec* recs, const int32_t* idx, int B,
+                     const void* v, const void* xs, const int8_t* pc, double* sq_out, void* scratch,
+                     size_t scratch_bytes, void* stream);
+/* Projection of dataset rows idx into their sorted pixel order: out (B, n_mask). */
+int fsld_project_sorted(int M, int mode, int n_mask, const fsld_image_rec* recs, const int32_t* idx, int B,
+                        const void* v, const int8_t* pc, void* out, void* stream);
+/* acc += sum_b P^* conj(f) xs[idx[b]] (b_vector, forward.py:572-579). */
+int fsld_backproject_sorted(int M, int mode, int n_mask, const fsld_image_rec* recs, const int32_t* idx,
+                            int B, const void* xs, const int8_t* pc, void* acc, unsigned flags,
+                            const double* fx_scale, void* stream);
 
 /*
  * Fixed-point scale for FSLD_DETERMINISTIC accumulation: writes

@@ -67,6 +67,12 @@ SIGNATURES = {
     "fsld_project_tab": (I, [I, I, I, P, P, I, P, P, P, P]),
     "fsld_backproject_tab": (I, [I, I, I, P, P, I, P, P, P, U, P, P]),
     "fsld_scatter_sq_tab": (I, [I, I, I, P, P, I, P, P, U, P, P]),
+    "fsld_sorted_count": (I, [I, I, P, P, I, P, P]),
+    "fsld_sorted_fill": (I, [I, I, P, P, I, P, P, P, P, P, P]),
+    "fsld_loss_grad_sorted": (I, [I, I, I, P, P, I, P, P, P, P, P, P, P, U, P, P, SZ, P]),
+    "fsld_loss_sorted": (I, [I, I, I, P, P, I, P, P, P, P, P, SZ, P]),
+    "fsld_project_sorted": (I, [I, I, I, P, P, I, P, P, P, P]),
+    "fsld_backproject_sorted": (I, [I, I, I, P, P, I, P, P, P, U, P, P]),
     "fsld_fixed_scale": (I, [P, I64, D, D, P, P]),
     "fsld_grad_finalize": (I, [I64, P, U, P, P, D, D, P, P]),
     "fsld_real_finalize": (I, [I64, P, U, P, D, D, P, P]),

@@ -1,23 +1,26 @@
-// fsld_brick.cu -- brick-binned fused loss+gradient kernel (tri mode) for sm_100a.
+// fsld_brick.cu -- brick-sorted fused loss+gradient path (tri mode) for sm_100a.
 //
-// Why: the reference's adjoint (kernels.py:193-230) scatters 8 complex
-// corner contributions per pixel.  As global red.add that is 8 L2 atomics
-// per pixel and the v1 tile kernel is L2-atomic bound (profiles/r01_v1_*).
-// Here the M^3 volume is cut into 8^3-voxel bricks in frequency space.  For
-// a batch, every (brick, image) pair whose slice plane can own a pixel of
-// the brick is binned (count -> scan -> fill, all on device).  A persistent
-// CTA takes a work item (brick, <= 32 images), stages the brick's 9^3
-// voxels of v in shared memory, and for every owned pixel (floor corner in
-// the brick) gathers 8 corners from smem, forms f*Pv - x, accumulates
-// |r|^2 and scatters conj(f) r w into a 9^3 int32 fixed-point accumulator in
-// smem (native ATOMS.ADD; the fixed-point scale is a power of two chosen
-// per item from a bound on its contributions).  The item ends with one
-// red.global.add.v2.f32 per touched brick voxel.
+// Why: the reference's adjoint (kernels.py:193-230) scatters 8 complex corner
+// contributions per pixel.  As global red.add that is 8 L2 atomics per pixel
+// and the per-pixel tile kernel is L2-atomic bound (profiles/r01_v1_*).
 //
-// Exactness contract: each pixel is owned by exactly one brick (the one
-// containing floor(clamp(c)), c = R^T (kx,ky,0) in fp32, kernels.py:42-60,
-// 147-170); binning and per-row candidate intervals are conservative and
-// the ownership test is exact, so every pixel is processed exactly once.
+// Refinement has KNOWN, FIXED poses (optim.run never changes them), so the
+// pixel -> voxel footprint of every image is fixed for the whole run.  The
+// dataset is therefore laid out once in HBM grouped by owner brick: for image
+// i, its masked pixels are reordered so that pixels whose floor corner
+// (floor(clamp(R^T k)), kernels.py:42-60, 147-170) falls in the same 8^3 brick
+// are contiguous; per pixel we keep (kx, ky) as int8 (2 B) and per image a
+// segment list (brick, start, count).
+//
+// Per step (all on device, stream-ordered): the batch's segments are counted
+// per brick, scanned into work items (brick, <= BC segments), and filled.  A
+// persistent CTA takes an item, stages the brick's 9^3 voxels of v in shared
+// memory, and its warps walk the item's segments (coalesced loads of x and
+// coordinates): per pixel gather 8 corners from smem -> f = CTF * shift phase
+// -> r = f P v - x -> |r|^2 -> conj(f) r w accumulated into a 9^3 complex smem
+// accumulator (64-bit CAS).  The item ends with one red.global.add.v2.f32 per
+// touched brick voxel.  Every pixel belongs to exactly one segment, so it is
+// processed exactly once.
 #include "fsld_kernels.cuh"
 
 namespace fsld {
@@ -27,6 +30,7 @@ ScratchLayout scratch_layout(int M, int n_mask, int B) {
     auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
     L.nb = (M + BT - 1) / BT;
     L.nbr = L.nb * L.nb * L.nb;
+    // a slice plane crosses at most ~3 nb^2 bricks; 4 nb^2 is a safe per-image bound
     long long pp = (long long)B * (long long)(L.nbr < 4 * L.nb * L.nb ? L.nbr : 4 * L.nb * L.nb);
     L.cap_pairs = (int)(pp > 0 ? pp : 1);
     L.cap_items = L.nbr + L.cap_pairs / BC + 1;
@@ -35,13 +39,10 @@ ScratchLayout scratch_layout(int M, int n_mask, int B) {
     L.cap_part = (int)(v1parts > 4096 ? v1parts : 4096);
     size_t o = 0;
     L.hdr = o; o = al(o + 256);
-    L.pix2p = o; o = al(o + sizeof(int) * (size_t)M * M);
-    L.rowmin = o; o = al(o + sizeof(int) * (size_t)M);
-    L.rowmax = o; o = al(o + sizeof(int) * (size_t)M);
     L.cnt = o; o = al(o + sizeof(int) * (size_t)L.nbr);
     L.off = o; o = al(o + sizeof(int) * (size_t)(L.nbr + 1));
     L.fill = o; o = al(o + sizeof(int) * (size_t)L.nbr);
-    L.pairs = o; o = al(o + sizeof(int) * (size_t)L.cap_pairs);
+    L.pairs = o; o = al(o + sizeof(int2) * (size_t)L.cap_pairs);
     L.items = o; o = al(o + sizeof(int4) * (size_t)L.cap_items);
     L.ctl = o; o = al(o + 64);
     L.part = o; o = al(o + sizeof(double) * (size_t)L.cap_part);
@@ -49,102 +50,173 @@ ScratchLayout scratch_layout(int M, int n_mask, int B) {
     return L;
 }
 
-// ---------------------------------------------------------------- geometry
+// ---------------------------------------------------------------- dataset layout (once per dataset)
 
-__global__ void geom_prepare_kernel(int M, int n_mask, const short2* __restrict__ pix, GeomHeader* hdr,
-                                    int* pix2p, int* rowmin, int* rowmax) {
-    const int c = (M + 1) / 2;
-    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n_mask; p += gridDim.x * blockDim.x) {
+// Floor corner of the clamped rotated pixel, fp32 -- the exact formula of the main kernel.
+__device__ __forceinline__ void floor_corner(float px, float py, const float* fr, float bnd, float& cx, float& cy,
+                                             float& cz, float& fx, float& fy, float& fz) {
+    cx = fminf(fmaxf(fmaf(px, fr[0], py * fr[3]), -bnd), bnd);
+    cy = fminf(fmaxf(fmaf(px, fr[1], py * fr[4]), -bnd), bnd);
+    cz = fminf(fmaxf(fmaf(px, fr[2], py * fr[5]), -bnd), bnd);
+    fx = floorf(cx);
+    fy = floorf(cy);
+    fz = floorf(cz);
+}
+
+__device__ __forceinline__ int owner_brick(short2 k, const float* fr, float bnd, int c, int nb) {
+    float cx, cy, cz, fx, fy, fz;
+    floor_corner((float)k.x, (float)k.y, fr, bnd, cx, cy, cz, fx, fy, fz);
+    const int bx = ((int)fx + c) / BT, by = ((int)fy + c) / BT, bz = ((int)fz + c) / BT;
+    return (bz * nb + by) * nb + bx;
+}
+
+// Per image: number of distinct owner bricks -> seg_off[i + 1] (scanned afterwards).
+__global__ void __launch_bounds__(256) sorted_count_kernel(int M, int n_mask, const short2* __restrict__ pix,
+                                                           const fsld_image_rec* __restrict__ recs, int32_t* seg_off) {
+    extern __shared__ int hist[];
+    __shared__ float fr[6];
+    __shared__ int nseg;
+    const int i = blockIdx.x;
+    const int c = (M + 1) / 2, nb = (M + BT - 1) / BT, nbr = nb * nb * nb;
+    const float bnd = (float)(M / 2 - 1);
+    if (threadIdx.x < 6) fr[threadIdx.x] = (float)recs[i].rot[threadIdx.x];
+    if (threadIdx.x == 0) nseg = 0;
+    for (int b = threadIdx.x; b < nbr; b += blockDim.x) hist[b] = 0;
+    __syncthreads();
+    for (int p = threadIdx.x; p < n_mask; p += blockDim.x) atomicAdd(hist + owner_brick(pix[p], fr, bnd, c, nb), 1);
+    __syncthreads();
+    int cnt = 0;
+    for (int b = threadIdx.x; b < nbr; b += blockDim.x) cnt += hist[b] > 0;
+    atomicAdd(&nseg, cnt);
+    __syncthreads();
+    if (threadIdx.x == 0) seg_off[i + 1] = nseg;
+}
+
+// In-place inclusive scan of seg_off[1..N] (one CTA), seg_off[0] = 0.
+__global__ void __launch_bounds__(1024) scan_offsets_kernel(int32_t* seg_off, int N) {
+    __shared__ int part[1024];
+    const int per = (N + 1023) / 1024;
+    const int lo = 1 + threadIdx.x * per, hi = min(lo + per, N + 1);
+    int s = 0;
+    for (int i = lo; i < hi; ++i) s += seg_off[i];
+    part[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = 1; o < 1024; o <<= 1) {
+        const int v = threadIdx.x >= o ? part[threadIdx.x - o] : 0;
+        __syncthreads();
+        part[threadIdx.x] += v;
+        __syncthreads();
+    }
+    int run = part[threadIdx.x] - s;
+    for (int i = lo; i < hi; ++i) {
+        run += seg_off[i];
+        seg_off[i] = run;
+    }
+    if (threadIdx.x == 0) seg_off[0] = 0;
+}
+
+// Per image: counting sort of the masked pixels by owner brick -> sorted x,
+// per-pixel (kx, ky) and the segment list in ascending brick order.
+__global__ void __launch_bounds__(256) sorted_fill_kernel(int M, int n_mask, const short2* __restrict__ pix,
+                                                          const fsld_image_rec* __restrict__ recs,
+                                                          const float2* __restrict__ x_in, float2* __restrict__ x_out,
+                                                          char2* __restrict__ pc_out, const int32_t* __restrict__ seg_off,
+                                                          int2* __restrict__ segs) {
+    extern __shared__ int word[];  // per brick: count, then (start | count << 16) running position
+    __shared__ float fr[6];
+    __shared__ int tsum[256], tseg[256];
+    const int i = blockIdx.x;
+    const int c = (M + 1) / 2, nb = (M + BT - 1) / BT, nbr = nb * nb * nb;
+    const float bnd = (float)(M / 2 - 1);
+    if (threadIdx.x < 6) fr[threadIdx.x] = (float)recs[i].rot[threadIdx.x];
+    for (int b = threadIdx.x; b < nbr; b += blockDim.x) word[b] = 0;
+    __syncthreads();
+    for (int p = threadIdx.x; p < n_mask; p += blockDim.x) atomicAdd(word + owner_brick(pix[p], fr, bnd, c, nb), 1);
+    __syncthreads();
+    // exclusive scans of counts and of non-empty flags over contiguous brick chunks
+    const int per = (nbr + blockDim.x - 1) / blockDim.x;
+    const int lo = threadIdx.x * per, hi = min(lo + per, nbr);
+    int s = 0, g = 0;
+    for (int b = lo; b < hi; ++b) {
+        s += word[b];
+        g += word[b] > 0;
+    }
+    tsum[threadIdx.x] = s;
+    tseg[threadIdx.x] = g;
+    __syncthreads();
+    for (int o = 1; o < (int)blockDim.x; o <<= 1) {
+        const int v1 = (int)threadIdx.x >= o ? tsum[threadIdx.x - o] : 0;
+        const int v2 = (int)threadIdx.x >= o ? tseg[threadIdx.x - o] : 0;
+        __syncthreads();
+        tsum[threadIdx.x] += v1;
+        tseg[threadIdx.x] += v2;
+        __syncthreads();
+    }
+    int start = tsum[threadIdx.x] - s, ord = tseg[threadIdx.x] - g;
+    const int sbase = seg_off[i];
+    for (int b = lo; b < hi; ++b) {
+        const int cnt = word[b];
+        word[b] = start | (cnt << 16);
+        if (cnt > 0) segs[sbase + ord++] = make_int2(b, start | (cnt << 16));
+        start += cnt;
+    }
+    __syncthreads();
+    const size_t row = (size_t)i * n_mask;
+    for (int p = threadIdx.x; p < n_mask; p += blockDim.x) {
         const short2 k = pix[p];
-        pix2p[(k.y + c) * M + (k.x + c)] = p;
-        atomicMin(rowmin + k.y + c, (int)k.x);
-        atomicMax(rowmax + k.y + c, (int)k.x);
-        atomicMax(&hdr->rmax2, (unsigned)(k.x * k.x + k.y * k.y));
+        const int b = owner_brick(k, fr, bnd, c, nb);
+        const int pos = atomicAdd(word + b, 1) & 0xFFFF;
+        pc_out[row + pos] = make_char2((signed char)k.x, (signed char)k.y);
+        if (x_in) x_out[row + pos] = x_in[row + p];
     }
 }
 
-__global__ void geom_header_kernel(int M, int n_mask, const void* pix, GeomHeader* hdr) {
-    hdr->magic = kGeomMagic;
-    hdr->M = M;
-    hdr->n_mask = n_mask;
-    hdr->pix = pix;
+static int smem_optin(const void* fn, size_t bytes) {
+    if (bytes <= 48 * 1024) return 0;
+    return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) == cudaSuccess ? 0 : -1;
 }
 
-__global__ void fill_int_kernel(int* p, int n, int v) {
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) p[i] = v;
-}
-
-cudaError_t launch_geom_prepare(int M, int n_mask, const short2* pix, const ScratchLayout& L, char* scratch,
-                                cudaStream_t s) {
-    GeomHeader* hdr = reinterpret_cast<GeomHeader*>(scratch + L.hdr);
-    int* pix2p = reinterpret_cast<int*>(scratch + L.pix2p);
-    int* rmin = reinterpret_cast<int*>(scratch + L.rowmin);
-    int* rmax = reinterpret_cast<int*>(scratch + L.rowmax);
-    cudaError_t e = cudaMemsetAsync(hdr, 0, 256, s);
-    if (e != cudaSuccess) return e;
-    e = cudaMemsetAsync(pix2p, 0xFF, sizeof(int) * (size_t)M * M, s);
-    if (e != cudaSuccess) return e;
-    fill_int_kernel<<<(M + 255) / 256, 256, 0, s>>>(rmin, M, 0x3fffffff);
-    fill_int_kernel<<<(M + 255) / 256, 256, 0, s>>>(rmax, M, -0x3fffffff);
-    geom_prepare_kernel<<<(n_mask + 255) / 256, 256, 0, s>>>(M, n_mask, pix, hdr, pix2p, rmin, rmax);
-    geom_header_kernel<<<1, 1, 0, s>>>(M, n_mask, pix, hdr);
+cudaError_t launch_sorted_count(int M, int n_mask, const short2* pix, const fsld_image_rec* recs, int N,
+                                int32_t* seg_off, cudaStream_t s) {
+    const int nb = (M + BT - 1) / BT;
+    const size_t smem = sizeof(int) * (size_t)nb * nb * nb;
+    if (smem_optin((const void*)sorted_count_kernel, smem)) return cudaErrorInvalidValue;
+    sorted_count_kernel<<<N, 256, smem, s>>>(M, n_mask, pix, recs, seg_off);
+    scan_offsets_kernel<<<1, 1024, 0, s>>>(seg_off, N);
     return cudaGetLastError();
 }
 
-// ---------------------------------------------------------------- binning
-
-struct Frame {
-    float r0x, r0y, r0z, r1x, r1y, r1z;
-};
-
-__device__ __forceinline__ Frame frame_of(const fsld_image_rec& R) {
-    Frame f;
-    f.r0x = (float)R.rot[0]; f.r0y = (float)R.rot[1]; f.r0z = (float)R.rot[2];
-    f.r1x = (float)R.rot[3]; f.r1y = (float)R.rot[4]; f.r1z = (float)R.rot[5];
-    return f;
+cudaError_t launch_sorted_fill(int M, int n_mask, const short2* pix, const fsld_image_rec* recs, int N,
+                               const float2* x_in, float2* x_out, char2* pc_out, const int32_t* seg_off, int2* segs,
+                               cudaStream_t s) {
+    const int nb = (M + BT - 1) / BT;
+    const size_t smem = sizeof(int) * (size_t)nb * nb * nb;
+    if (smem_optin((const void*)sorted_fill_kernel, smem)) return cudaErrorInvalidValue;
+    sorted_fill_kernel<<<N, 256, smem, s>>>(M, n_mask, pix, recs, x_in, x_out, pc_out, seg_off, segs);
+    return cudaGetLastError();
 }
 
-// Can the slice plane of frame F own a pixel of brick (bx,by,bz)?  Plane-box
-// and ball-box tests on the brick box grown by a safety margin.
-__device__ __forceinline__ bool brick_hit(const Frame& F, int bx, int by, int bz, int c, float rball) {
-    const float m = 0.05f;
-    const float ox = (float)(-c + BT * bx), oy = (float)(-c + BT * by), oz = (float)(-c + BT * bz);
-    const float h = 0.5f * BT;
-    const float cx = ox + h, cy = oy + h, cz = oz + h;
-    const float nx = F.r0y * F.r1z - F.r0z * F.r1y;
-    const float ny = F.r0z * F.r1x - F.r0x * F.r1z;
-    const float nz = F.r0x * F.r1y - F.r0y * F.r1x;
-    const float d = fabsf(nx * cx + ny * cy + nz * cz);
-    if (d > (h + m) * (fabsf(nx) + fabsf(ny) + fabsf(nz)) + m) return false;
-    const float dx = fmaxf(fmaxf(ox - m, 0.f), -(ox + BT + m));
-    const float dy = fmaxf(fmaxf(oy - m, 0.f), -(oy + BT + m));
-    const float dz = fmaxf(fmaxf(oz - m, 0.f), -(oz + BT + m));
-    return dx * dx + dy * dy + dz * dz <= rball * rball;
-}
+// ---------------------------------------------------------------- per-step binning
 
 template <bool FILL>
-__global__ void __launch_bounds__(256) brick_bin_kernel(BrickArgs a) {
-    __shared__ fsld_image_rec rec;
+__global__ void __launch_bounds__(128) bin_sorted_kernel(SortedArgs a) {
     const int b = blockIdx.x;
-    load_record(a.recs, a.idx ? a.idx[b] : b, &rec);
-    __syncthreads();
-    const Frame F = frame_of(rec);
-    const float rball = sqrtf((float)a.hdr->rmax2) + 0.51f;
-    for (int id = threadIdx.x; id < a.nbr; id += blockDim.x) {
-        const int bx = id % a.nb, by = (id / a.nb) % a.nb, bz = id / (a.nb * a.nb);
-        if (!brick_hit(F, bx, by, bz, a.c, rball)) continue;
+    const int row = a.idx ? a.idx[b] : b;
+    const int s0 = a.seg_off[row], s1 = a.seg_off[row + 1];
+    for (int sidx = s0 + threadIdx.x; sidx < s1; sidx += blockDim.x) {
+        const int brick = a.segs[sidx].x;
         if (FILL) {
-            const int slot = atomicAdd(a.fill + id, 1);
-            a.pairs[a.off[id] + slot] = b;
+            const int slot = atomicAdd(a.fill + brick, 1);
+            a.pairs[a.off[brick] + slot] = make_int2(b, sidx);
         } else {
-            atomicAdd(a.cnt + id, 1);
+            atomicAdd(a.cnt + brick, 1);
         }
     }
 }
 
 // Exclusive scan of per-brick pair counts and expansion into work items
 // (brick, first pair, n pairs <= BC).  One CTA of 1024 threads.
-__global__ void __launch_bounds__(1024) brick_scan_kernel(BrickArgs a) {
+__global__ void __launch_bounds__(1024) brick_scan_kernel(SortedArgs a) {
     __shared__ int s_pairs[1024];
     __shared__ int s_items[1024];
     const int per = (a.nbr + 1023) / 1024;
@@ -160,8 +232,8 @@ __global__ void __launch_bounds__(1024) brick_scan_kernel(BrickArgs a) {
     s_items[threadIdx.x] = ni;
     __syncthreads();
     for (int o = 1; o < 1024; o <<= 1) {  // Hillis-Steele inclusive scan
-        int vp = threadIdx.x >= o ? s_pairs[threadIdx.x - o] : 0;
-        int vi = threadIdx.x >= o ? s_items[threadIdx.x - o] : 0;
+        const int vp = threadIdx.x >= o ? s_pairs[threadIdx.x - o] : 0;
+        const int vi = threadIdx.x >= o ? s_items[threadIdx.x - o] : 0;
         __syncthreads();
         s_pairs[threadIdx.x] += vp;
         s_items[threadIdx.x] += vi;
@@ -183,201 +255,213 @@ __global__ void __launch_bounds__(1024) brick_scan_kernel(BrickArgs a) {
         a.off[a.nbr] = s_pairs[1023];
         a.ctl[0] = min(s_items[1023], a.cap_items);
         a.ctl[1] = 0;
-        a.ctl[2] = s_pairs[1023] > a.cap_pairs;  // overflow flag (never expected)
+        a.ctl[2] = s_pairs[1023] > a.cap_pairs;  // overflow flag (cannot happen for the 4 nb^2 bound)
     }
 }
 
 // ---------------------------------------------------------------- main kernel
 
-constexpr float kMagic = 12582912.0f;   // 1.5 * 2^23: float -> int32 round-to-nearest
+// float -> int32 round-to-nearest for |x| < 2^22 via the 1.5*2^23 magic (FFMA + IADD, no F2I).
+constexpr float kMagic = 12582912.0f;
 constexpr int kMagicBits = 0x4B400000;
 
-__device__ __forceinline__ int to_fixed(float x) {  // |x| < 2^22
-    return __float_as_int(x + kMagic) - kMagicBits;
-}
+// Upper bound on the pixels one image owns in one brick: lattice points of a
+// plane section of a BT^3 cube (area <= BT^2 sqrt 2, perimeter <= 2 BT (1 + sqrt 2)).
+constexpr int BOWN_MAX = 112;
+constexpr int BBUF = BC * BOWN_MAX;
 
-struct BrickSmem {
-    float2 vb[BH3];
-    int accr[BH3];
-    int acci[BH3];
-    fsld_image_rec recs[BC];
-    unsigned char rowof[BW][BMAXCAND];
+struct SortedSmem {
+    float2 vb[BH3];                 // v brick + halo
+    int accr[BH3];                  // fixed-point adjoint accumulator (re)
+    int acci[BH3];                  // (im)
+    float2 bval[BBUF];              // pass 1 -> 2: conj(f) r per pixel of the item
+    unsigned char bk[BBUF];         // segment (image) of each pixel of the item
+    char2 bpc[BBUF];                // its (kx, ky), kept for pass 2
+    fsld_image_rec recs[BC];        // records of the item's images
+    float frame[BC][6];             // fp32 rows 0,1 of R
+    int seg_row[BC];                // dataset row of segment k
+    int seg_pos[BC];                // start of segment k in its row (sorted order)
+    int pref[BC + 1];               // exclusive prefix of segment lengths
     int item;
-    float vmax;
-    float xmax;
+    int vmax_bits;
     double red[BW];
 };
 
-__global__ void __launch_bounds__(BTHREADS, 3) brick_loss_grad_kernel(BrickArgs a) {
+// Item-local flat index e -> segment k (largest k with pref[k] <= e), binary search over <= 32.
+__device__ __forceinline__ int seg_of(const int* pref, int nseg, int e) {
+    int k = 0;
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1)
+        if (k + s < nseg && pref[k + s] <= e) k += s;
+    return k;
+}
+
+// Two passes per work item over the item's pixels, flattened across its <= 32
+// segments (all lanes busy):
+//   1. per pixel: gather 8 corners from the smem brick, f = C * phase,
+//      r = f P v - x, |r|^2 -> loss, val = conj(f) r -> smem buffer;
+//   2. with the item's max |val| known, quantise val * w to int32 with a
+//      power-of-two scale (|val w s| <= 2^22; <= BC*12 contributions per voxel
+//      -> |sum| < 2^31) and add with native ATOMS.ADD (order-free, no CAS).
+// The scale follows the residual, not |Pv| or |x|: quantum ~2^-22 of the
+// item's largest contribution.
+__global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    BrickSmem& S = *reinterpret_cast<BrickSmem*>(smem_raw);
+    SortedSmem& S = *reinterpret_cast<SortedSmem*>(smem_raw);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int M = a.M, c = a.c, nb = a.nb, n = a.n_mask;
     const float bnd = a.bnd;
     double lsum = 0.0;
-    const bool bad_geom = a.hdr->magic != kGeomMagic || a.hdr->M != M || a.hdr->n_mask != n;
 
     for (;;) {
         if (threadIdx.x == 0) {
             S.item = atomicAdd(a.ctl + 1, 1);
-            S.vmax = 0.f;
-            S.xmax = 0.f;
+            S.vmax_bits = 0;
         }
         __syncthreads();
         const int it = S.item;
-        if (it >= a.ctl[0] || bad_geom) break;
+        if (it >= a.ctl[0]) break;
         const int4 item = a.items[it];
-        const int bid = item.x, pstart = item.y, nimg = item.z;
+        const int bid = item.x, pstart = item.y, nseg = item.z;
         const int bx = bid % nb, by = (bid / nb) % nb, bz = bid / (nb * nb);
         const int ox = -c + BT * bx, oy = -c + BT * by, oz = -c + BT * bz;
 
-        // records of this item's images (32 x 4 B per record, coalesced)
-        for (int w = threadIdx.x; w < nimg * 32; w += BTHREADS) {
-            const int k = w >> 5, q = w & 31;
-            const int bimg = a.pairs[pstart + k];
-            const int row = a.idx ? a.idx[bimg] : bimg;
-            const uint32_t word = __ldg(reinterpret_cast<const uint32_t*>(a.recs + row) + q);
-            reinterpret_cast<uint32_t*>(S.recs + k)[q] = word;
-            if (q == 29) atomicMax(reinterpret_cast<int*>(&S.xmax), (int)word);  // pad[0] = max|x| (>= 0)
-        }
-        // v brick (+halo) and zeroed accumulators
-        float vm = 0.f;
-        for (int l = threadIdx.x; l < BH3; l += BTHREADS) {
-            const int lx = l % BH, ly = (l / BH) % BH, lz = l / (BH * BH);
-            const int kx = ox + lx, ky = oy + ly, kz = oz + lz;
-            float2 val = make_float2(0.f, 0.f);
-            if (kx < M - c && ky < M - c && kz < M - c && kx >= -c && ky >= -c && kz >= -c)
-                val = __ldg(a.v + lin_index(kx, ky, kz, M, c));
-            S.vb[l] = val;
-            S.accr[l] = 0;
-            S.acci[l] = 0;
-            vm = fmaxf(vm, fmaxf(fabsf(val.x), fabsf(val.y)));
-        }
-        for (int o = 16; o > 0; o >>= 1) vm = fmaxf(vm, __shfl_xor_sync(0xffffffffu, vm, o));
-        if (lane == 0) atomicMax(reinterpret_cast<int*>(&S.vmax), __float_as_int(vm));
-        __syncthreads();
-        // fixed-point scale: |contribution| <= |val| <= U = 2 max|v comp| + max|x|  ->  |U s| <= 2^21;
-        // per voxel and item <= BC * 12 contributions  ->  < 2^30.
-        const float U = 2.0f * S.vmax + S.xmax;
-        const float sc = U > 0.f ? exp2f(floorf(log2f(2097152.0f / U))) : 1.0f;
-        const float inv_sc = 1.0f / sc;
-
-        for (int k = warp; k < nimg; k += BW) {
-            const fsld_image_rec& R = S.recs[k];
-            const int bimg = a.pairs[pstart + k];
-            const int row = a.idx ? a.idx[bimg] : bimg;
-            const float2* __restrict__ xrow = a.x + (size_t)row * n;
-            const Frame F = frame_of(R);
-            // candidate rows: py = c . r1 over the brick box, +-1
-            const float h = 0.5f * BT;
-            const float cyc = (ox + h) * F.r1x + (oy + h) * F.r1y + (oz + h) * F.r1z;
-            const float ext = h * (fabsf(F.r1x) + fabsf(F.r1y) + fabsf(F.r1z)) + 1.0f;
-            const int rlim = (int)sqrtf((float)a.hdr->rmax2) + 1;
-            const int pylo = max((int)floorf(cyc - ext), -rlim);
-            const int pyhi = min((int)ceilf(cyc + ext), rlim);
-            const int nrows = pyhi - pylo + 1;  // <= 2*(BT*sqrt(3)/2 + 1) + 2 < 32
-            int lo = 0, cntr = 0;
-            if (lane < nrows) {
-                const int py = pylo + lane;
-                float flo = -1e30f, fhi = 1e30f;
-                bool empty = (py + c) < 0 || (py + c) >= M;
-                const float r0[3] = {F.r0x, F.r0y, F.r0z};
-                const float r1[3] = {F.r1x, F.r1y, F.r1z};
-                const float o3[3] = {(float)ox, (float)oy, (float)oz};
-#pragma unroll
-                for (int ax = 0; ax < 3; ++ax) {
-                    const float base = (float)py * r1[ax];
-                    if (fabsf(r0[ax]) > 1e-4f) {
-                        const float inv = 1.0f / r0[ax];
-                        const float t0 = (o3[ax] - base) * inv, t1 = (o3[ax] + BT - base) * inv;
-                        flo = fmaxf(flo, fminf(t0, t1));
-                        fhi = fminf(fhi, fmaxf(t0, t1));
-                    } else if (base < o3[ax] - 0.02f || base > o3[ax] + BT + 0.02f) {
-                        empty = true;
-                    }
-                }
-                if (!empty && flo <= fhi + 2.0f) {
-                    int ilo = (int)floorf(flo) - 1, ihi = (int)ceilf(fhi) + 1;
-                    ilo = max(ilo, a.rowmin[py + c]);
-                    ihi = min(ihi, a.rowmax[py + c]);
-                    if (ihi >= ilo) {
-                        lo = ilo;
-                        cntr = ihi - ilo + 1;
-                    }
-                }
+        if (warp == 0) {  // segment table + prefix of lengths (one warp)
+            int len = 0;
+            if (lane < nseg) {
+                const int2 pr = a.pairs[pstart + lane];
+                const int row = a.idx ? a.idx[pr.x] : pr.x;
+                const int2 seg = a.segs[pr.y];
+                S.seg_row[lane] = row;
+                S.seg_pos[lane] = seg.y & 0xFFFF;
+                len = seg.y >> 16;
             }
-            // exclusive scan of row counts
-            int incl = cntr;
+            int incl = len;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const int t = __shfl_up_sync(0xffffffffu, incl, o);
                 if (lane >= o) incl += t;
             }
-            const int total = min(__shfl_sync(0xffffffffu, incl, 31), BMAXCAND);
-            const int start = incl - cntr;
-            for (int i = 0; i < cntr && start + i < BMAXCAND; ++i) S.rowof[warp][start + i] = (unsigned char)lane;
-            __syncwarp();
-
-            float sq = 0.f;
-            for (int base = 0; base < total; base += 32) {
-                const int i = base + lane;
-                const bool valid = i < total;
-                const int r = valid ? (int)S.rowof[warp][i] : 0;
-                const int rlo = __shfl_sync(0xffffffffu, lo, r);
-                const int rst = __shfl_sync(0xffffffffu, start, r);
-                if (!valid) continue;
-                const int py = pylo + r;
-                const int px = rlo + (i - rst);
-                const int p = __ldg(a.pix2p + (py + c) * M + (px + c));
-                if (p < 0) continue;
-                const float fpx = (float)px, fpy = (float)py;
-                float cx = fmaf(fpx, F.r0x, fpy * F.r1x);
-                float cy = fmaf(fpx, F.r0y, fpy * F.r1y);
-                float cz = fmaf(fpx, F.r0z, fpy * F.r1z);
-                cx = fminf(fmaxf(cx, -bnd), bnd);
-                cy = fminf(fmaxf(cy, -bnd), bnd);
-                cz = fminf(fmaxf(cz, -bnd), bnd);
-                const float fx = floorf(cx), fy = floorf(cy), fz = floorf(cz);
-                const int lx = (int)fx - ox, ly = (int)fy - oy, lz = (int)fz - oz;
-                if ((unsigned)lx >= (unsigned)BT || (unsigned)ly >= (unsigned)BT || (unsigned)lz >= (unsigned)BT)
-                    continue;  // owned by another brick
-                const float wx = cx - fx, wy = cy - fy, wz = cz - fz;
-                const float ax = 1.f - wx, ay = 1.f - wy, az = 1.f - wz;
-                const float2 xv = __ldg(xrow + p);
-                const float2 f = pixel_factor(R, px, py);
-                const int l0 = (lz * BH + ly) * BH + lx;
-                const float2* vb = S.vb + l0;
-                // trilinear gather (kernels.py:171-176) from the smem brick
-                float2 e0 = __ffma2_rn(make_float2(wx, wx), vb[1], __fmul2_rn(make_float2(ax, ax), vb[0]));
-                float2 e1 = __ffma2_rn(make_float2(wx, wx), vb[BH + 1], __fmul2_rn(make_float2(ax, ax), vb[BH]));
-                float2 e2 = __ffma2_rn(make_float2(wx, wx), vb[BH * BH + 1], __fmul2_rn(make_float2(ax, ax), vb[BH * BH]));
-                float2 e3 = __ffma2_rn(make_float2(wx, wx), vb[BH * BH + BH + 1],
-                                       __fmul2_rn(make_float2(ax, ax), vb[BH * BH + BH]));
-                const float2 q0 = __ffma2_rn(make_float2(wy, wy), e1, __fmul2_rn(make_float2(ay, ay), e0));
-                const float2 q1 = __ffma2_rn(make_float2(wy, wy), e3, __fmul2_rn(make_float2(ay, ay), e2));
-                const float2 pv = __ffma2_rn(make_float2(wz, wz), q1, __fmul2_rn(make_float2(az, az), q0));
-                const float2 pr = cmul(pv, f);
-                const float2 rr = make_float2(pr.x - xv.x, pr.y - xv.y);
-                sq = fmaf(rr.x, rr.x, fmaf(rr.y, rr.y, sq));
-                float2 val = cmulconj(f, rr);
-                val = __fmul2_rn(val, make_float2(sc, sc));
-                // adjoint scatter into the smem brick (kernels.py:221-230), fixed point
-                const float zy00 = az * ay, zy10 = az * wy, zy01 = wz * ay, zy11 = wz * wy;
-                const float w8[8] = {zy00 * ax, zy00 * wx, zy10 * ax, zy10 * wx,
-                                     zy01 * ax, zy01 * wx, zy11 * ax, zy11 * wx};
-                const int off8[8] = {0, 1, BH, BH + 1, BH * BH, BH * BH + 1, BH * BH + BH, BH * BH + BH + 1};
+            if (lane < nseg) S.pref[lane] = incl - len;
+            if (lane == 31) S.pref[nseg] = incl;
+        }
+        {   // v brick + halo: issue all loads before the stores
+            constexpr int U = (BH3 + BTHREADS - 1) / BTHREADS;
+            float2 vv[U];
 #pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    atomicAdd(S.accr + l0 + off8[q], to_fixed(w8[q] * val.x));
-                    atomicAdd(S.acci + l0 + off8[q], to_fixed(w8[q] * val.y));
+            for (int u = 0; u < U; ++u) {
+                const int l = threadIdx.x + u * BTHREADS;
+                const int lx = l % BH, ly = (l / BH) % BH, lz = l / (BH * BH);
+                const int kx = ox + lx, ky = oy + ly, kz = oz + lz;
+                vv[u] = make_float2(0.f, 0.f);
+                if (l < BH3 && kx < M - c && ky < M - c && kz < M - c) vv[u] = __ldg(a.v + lin_index(kx, ky, kz, M, c));
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int l = threadIdx.x + u * BTHREADS;
+                if (l < BH3) {
+                    S.vb[l] = vv[u];
+                    S.accr[l] = 0;
+                    S.acci[l] = 0;
                 }
             }
-            for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
-            if (lane == 0) lsum += (double)sq;
-            __syncwarp();
         }
         __syncthreads();
-        // flush: one vector reduction per touched brick voxel
+        for (int w = threadIdx.x; w < nseg * 32; w += BTHREADS) {
+            const int k = w >> 5, q = w & 31;
+            reinterpret_cast<uint32_t*>(S.recs + k)[q] = __ldg(reinterpret_cast<const uint32_t*>(a.recs + S.seg_row[k]) + q);
+        }
+        __syncthreads();
+        if (threadIdx.x < nseg * 6) S.frame[threadIdx.x / 6][threadIdx.x % 6] = (float)S.recs[threadIdx.x / 6].rot[threadIdx.x % 6];
+        __syncthreads();
+        const int total = min(S.pref[nseg], BBUF);
+        // item-local pixel e -> segment k table (one byte per pixel)
+        for (int k = warp; k < nseg; k += BW)
+            for (int e = S.pref[k] + lane; e < min(S.pref[k + 1], BBUF); e += 32) S.bk[e] = (unsigned char)k;
+        __syncthreads();
+
+        // ---------------- pass 1 (loads of the next pixel issued before the current one is computed)
+        float sq = 0.f, vmax = 0.f;
+        int kn = 0;
+        char2 kkn = make_char2(0, 0);
+        float2 xvn = make_float2(0.f, 0.f);
+        if ((int)threadIdx.x < total) {
+            kn = S.bk[threadIdx.x];
+            const size_t g = (size_t)S.seg_row[kn] * n + S.seg_pos[kn] + (threadIdx.x - S.pref[kn]);
+            kkn = a.pc[g];
+            xvn = __ldg(a.xs + g);
+        }
+        for (int e = threadIdx.x; e < total; e += BTHREADS) {
+            const int k = kn;
+            const char2 kk = kkn;
+            const float2 xv = xvn;
+            if (e + BTHREADS < total) {
+                kn = S.bk[e + BTHREADS];
+                const size_t g = (size_t)S.seg_row[kn] * n + S.seg_pos[kn] + (e + BTHREADS - S.pref[kn]);
+                kkn = a.pc[g];
+                xvn = __ldg(a.xs + g);
+            }
+            S.bpc[e] = kk;
+            const float* fr = S.frame[k];
+            const int px = kk.x, py = kk.y;
+            float cx, cy, cz, fx, fy, fz;
+            floor_corner((float)px, (float)py, fr, bnd, cx, cy, cz, fx, fy, fz);
+            const int l0 = (((int)fz - oz) * BH + ((int)fy - oy)) * BH + ((int)fx - ox);
+            const float wx = cx - fx, wy = cy - fy, wz = cz - fz;
+            const float ax = 1.f - wx, ay = 1.f - wy, az = 1.f - wz;
+            const float2 f = pixel_factor(S.recs[k], px, py);
+            const float2* vb = S.vb + l0;
+            // trilinear gather (kernels.py:171-176) from the smem brick
+            const float2 WX = make_float2(wx, wx), AX = make_float2(ax, ax);
+            const float2 e0 = __ffma2_rn(WX, vb[1], __fmul2_rn(AX, vb[0]));
+            const float2 e1 = __ffma2_rn(WX, vb[BH + 1], __fmul2_rn(AX, vb[BH]));
+            const float2 e2 = __ffma2_rn(WX, vb[BH * BH + 1], __fmul2_rn(AX, vb[BH * BH]));
+            const float2 e3 = __ffma2_rn(WX, vb[BH * BH + BH + 1], __fmul2_rn(AX, vb[BH * BH + BH]));
+            const float2 q0 = __ffma2_rn(make_float2(wy, wy), e1, __fmul2_rn(make_float2(ay, ay), e0));
+            const float2 q1 = __ffma2_rn(make_float2(wy, wy), e3, __fmul2_rn(make_float2(ay, ay), e2));
+            const float2 pv = __ffma2_rn(make_float2(wz, wz), q1, __fmul2_rn(make_float2(az, az), q0));
+            const float2 prj = cmul(pv, f);
+            const float2 rr = make_float2(prj.x - xv.x, prj.y - xv.y);
+            sq = fmaf(rr.x, rr.x, fmaf(rr.y, rr.y, sq));
+            const float2 val = cmulconj(f, rr);
+            vmax = fmaxf(vmax, fmaxf(fabsf(val.x), fabsf(val.y)));
+            S.bval[e] = val;
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            sq += __shfl_xor_sync(0xffffffffu, sq, o);
+            vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
+        }
+        if (lane == 0) {
+            lsum += (double)sq;
+            atomicMax(&S.vmax_bits, __float_as_int(vmax));
+        }
+        __syncthreads();
+
+        // ---------------- pass 2: fixed-point adjoint scatter (kernels.py:221-230)
+        const float vm = __int_as_float(S.vmax_bits);
+        const float sc = vm > 0.f ? exp2f(floorf(log2f(4194303.0f / vm))) : 1.0f;
+        const float inv_sc = 1.0f / sc;
+        for (int e = threadIdx.x; e < total; e += BTHREADS) {
+            const int k = S.bk[e];
+            const char2 kk = S.bpc[e];
+            float cx, cy, cz, fx, fy, fz;
+            floor_corner((float)kk.x, (float)kk.y, S.frame[k], bnd, cx, cy, cz, fx, fy, fz);
+            const int l0 = (((int)fz - oz) * BH + ((int)fy - oy)) * BH + ((int)fx - ox);
+            const float wx = cx - fx, wy = cy - fy, wz = cz - fz;
+            const float ax = 1.f - wx, ay = 1.f - wy, az = 1.f - wz;
+            const float2 val = __fmul2_rn(S.bval[e], make_float2(sc, sc));
+            const float zy00 = az * ay, zy10 = az * wy, zy01 = wz * ay, zy11 = wz * wy;
+            const float w8[8] = {zy00 * ax, zy00 * wx, zy10 * ax, zy10 * wx, zy01 * ax, zy01 * wx, zy11 * ax, zy11 * wx};
+            const int off8[8] = {0, 1, BH, BH + 1, BH * BH, BH * BH + 1, BH * BH + BH, BH * BH + BH + 1};
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const float2 y = __ffma2_rn(make_float2(w8[q], w8[q]), val, make_float2(kMagic, kMagic));
+                atomicAdd(S.accr + l0 + off8[q], __float_as_int(y.x) - kMagicBits);
+                atomicAdd(S.acci + l0 + off8[q], __float_as_int(y.y) - kMagicBits);
+            }
+        }
+        __syncthreads();
+        // ---------------- flush: one vector reduction per touched brick voxel
         for (int l = threadIdx.x; l < BH3; l += BTHREADS) {
             const int qr = S.accr[l], qi = S.acci[l];
             if ((qr | qi) == 0) continue;
@@ -389,40 +473,38 @@ __global__ void __launch_bounds__(BTHREADS, 3) brick_loss_grad_kernel(BrickArgs 
         }
         __syncthreads();
     }
-    // per-CTA loss partial (fixed slot)
     if (lane == 0) S.red[warp] = lsum;
     __syncthreads();
     if (threadIdx.x == 0) {
         double s = 0.0;
         for (int w = 0; w < BW; ++w) s += S.red[w];
-        a.part[blockIdx.x] = bad_geom ? __longlong_as_double(0x7ff8000000000000ll) : s;
+        a.part[blockIdx.x] = s;
     }
 }
 
-static int g_brick_grid = 0;
+static int g_sorted_grid = 0;
 
-cudaError_t launch_brick_loss_grad(const BrickArgs& a, double* sq_out, cudaStream_t s) {
-    const size_t smem = sizeof(BrickSmem);
-    if (g_brick_grid == 0) {
-        cudaError_t e = cudaFuncSetAttribute(brick_loss_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+cudaError_t launch_sorted_loss_grad(const SortedArgs& a, double* sq_out, cudaStream_t s) {
+    const size_t smem = sizeof(SortedSmem);
+    if (g_sorted_grid == 0) {
+        cudaError_t e = cudaFuncSetAttribute(sorted_loss_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);
         if (e != cudaSuccess) return e;
         int dev = 0, sms = 0, occ = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, brick_loss_grad_kernel, BTHREADS, smem);
-        g_brick_grid = sms * (occ > 0 ? occ : 1);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sorted_loss_grad_kernel, BTHREADS, smem);
+        g_sorted_grid = sms * (occ > 0 ? occ : 1);
     }
     cudaError_t e = cudaMemsetAsync(a.cnt, 0, sizeof(int) * (size_t)a.nbr, s);
     if (e != cudaSuccess) return e;
-    brick_bin_kernel<false><<<a.B, 256, 0, s>>>(a);
+    bin_sorted_kernel<false><<<a.B, 128, 0, s>>>(a);
     brick_scan_kernel<<<1, 1024, 0, s>>>(a);
-    brick_bin_kernel<true><<<a.B, 256, 0, s>>>(a);
-    const int grid = g_brick_grid;
-    brick_loss_grad_kernel<<<grid, BTHREADS, smem, s>>>(a);
+    bin_sorted_kernel<true><<<a.B, 128, 0, s>>>(a);
+    sorted_loss_grad_kernel<<<g_sorted_grid, BTHREADS, smem, s>>>(a);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    return launch_reduce(a.part, grid, sq_out, s);
+    return launch_reduce(a.part, g_sorted_grid, sq_out, s);
 }
 
 }  // namespace fsld

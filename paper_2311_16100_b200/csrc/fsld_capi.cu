@@ -85,16 +85,21 @@ int fsld_prepare(int M, int n_mask, const int16_t* pix, void* scratch, size_t sc
     if (M < 2 || M > 1024 || n_mask < 1 || n_mask > M * M || !pix || !scratch) return FSLD_EINVAL;
     const ScratchLayout L = scratch_layout(M, n_mask, 1);
     if (scratch_bytes < L.total) return FSLD_EINVAL;
-    return status_of(launch_geom_prepare(M, n_mask, reinterpret_cast<const short2*>(pix), L,
-                                         reinterpret_cast<char*>(scratch), reinterpret_cast<cudaStream_t>(stream)));
+    GeomHeader h{};
+    h.magic = kGeomMagic;
+    h.M = M;
+    h.n_mask = n_mask;
+    h.pix = pix;
+    return status_of(cudaMemcpyAsync(reinterpret_cast<char*>(scratch) + L.hdr, &h, sizeof(h), cudaMemcpyHostToDevice,
+                                     reinterpret_cast<cudaStream_t>(stream)));
 }
 
-static int run_reducing(int op, int M, int mode, int n_mask, const int16_t* pix, const fsld_image_rec* recs,
-                        const int32_t* idx, int B, const void* v, const void* x, void* grad_acc,
-                        double* sq_out, unsigned flags, const double* fx_scale, void* scratch,
+static int run_reducing(int op, int M, int mode, int n_mask, const int16_t* pix, const int8_t* pc,
+                        const fsld_image_rec* recs, const int32_t* idx, int B, const void* v, const void* x,
+                        void* grad_acc, double* sq_out, unsigned flags, const double* fx_scale, void* scratch,
                         size_t scratch_bytes, void* stream) {
     if (!geom_ok(M, mode, n_mask, B)) return FSLD_EINVAL;
-    if (!pix || !recs || !v || !x || !sq_out || !scratch) return FSLD_EINVAL;
+    if ((!pix && !pc) || !recs || !v || !x || !sq_out || !scratch) return FSLD_EINVAL;
     if (op == OP_LOSS_GRAD && !grad_acc) return FSLD_EINVAL;
     const bool det = (flags & FSLD_DETERMINISTIC) != 0;
     if (det && !fx_scale) return FSLD_EINVAL;
@@ -102,35 +107,6 @@ static int run_reducing(int op, int M, int mode, int n_mask, const int16_t* pix,
     if (scratch_bytes < L.total) return FSLD_EINVAL;
     char* scr = reinterpret_cast<char*>(scratch);
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    if (op == OP_LOSS_GRAD && mode == FSLD_MODE_TRI && !det && !(flags & FSLD_TILE_PATH)) {
-        BrickArgs b{};
-        b.M = M;
-        b.c = (M + 1) / 2;
-        b.nb = L.nb;
-        b.nbr = L.nbr;
-        b.n_mask = n_mask;
-        b.B = B;
-        b.bnd = (float)(M / 2 - 1);
-        b.pix2p = reinterpret_cast<const int*>(scr + L.pix2p);
-        b.rowmin = reinterpret_cast<const int*>(scr + L.rowmin);
-        b.rowmax = reinterpret_cast<const int*>(scr + L.rowmax);
-        b.hdr = reinterpret_cast<const GeomHeader*>(scr + L.hdr);
-        b.recs = recs;
-        b.idx = idx;
-        b.v = reinterpret_cast<const float2*>(v);
-        b.x = reinterpret_cast<const float2*>(x);
-        b.acc = reinterpret_cast<float2*>(grad_acc);
-        b.cnt = reinterpret_cast<int*>(scr + L.cnt);
-        b.off = reinterpret_cast<int*>(scr + L.off);
-        b.fill = reinterpret_cast<int*>(scr + L.fill);
-        b.pairs = reinterpret_cast<int*>(scr + L.pairs);
-        b.items = reinterpret_cast<int4*>(scr + L.items);
-        b.ctl = reinterpret_cast<int*>(scr + L.ctl);
-        b.part = reinterpret_cast<double*>(scr + L.part);
-        b.cap_pairs = L.cap_pairs;
-        b.cap_items = L.cap_items;
-        return status_of(launch_brick_loss_grad(b, sq_out, s));
-    }
     SliceArgs a = make_args(M, n_mask, pix, recs, idx);
     const int nblocks = B * a.tiles;
     a.v = reinterpret_cast<const float2*>(v);
@@ -139,6 +115,7 @@ static int run_reducing(int op, int M, int mode, int n_mask, const int16_t* pix,
     a.acc = grad_acc;
     a.partials = reinterpret_cast<double*>(scr + L.part);
     a.fx = fx_scale;
+    a.pc = reinterpret_cast<const char2*>(pc);
     cudaError_t e = launch_slice(op, mode, det, a, nblocks, s);
     if (e != cudaSuccess) return FSLD_ECUDA;
     return status_of(launch_reduce(a.partials, nblocks, sq_out, s));
@@ -147,14 +124,14 @@ static int run_reducing(int op, int M, int mode, int n_mask, const int16_t* pix,
 int fsld_loss_grad(int M, int mode, int n_mask, const int16_t* pix, const fsld_image_rec* recs,
                    const int32_t* idx, int B, const void* v, const void* x, void* grad_acc, double* sq_out,
                    unsigned flags, const double* fx_scale, void* scratch, size_t scratch_bytes, void* stream) {
-    return run_reducing(OP_LOSS_GRAD, M, mode, n_mask, pix, recs, idx, B, v, x, grad_acc, sq_out, flags,
+    return run_reducing(OP_LOSS_GRAD, M, mode, n_mask, pix, nullptr, recs, idx, B, v, x, grad_acc, sq_out, flags,
                         fx_scale, scratch, scratch_bytes, stream);
 }
 
 int fsld_loss(int M, int mode, int n_mask, const int16_t* pix, const fsld_image_rec* recs, const int32_t* idx,
               int B, const void* v, const void* x, double* sq_out, void* scratch, size_t scratch_bytes,
               void* stream) {
-    return run_reducing(OP_LOSS, M, mode, n_mask, pix, recs, idx, B, v, x, nullptr, sq_out, 0u, nullptr,
+    return run_reducing(OP_LOSS, M, mode, n_mask, pix, nullptr, recs, idx, B, v, x, nullptr, sq_out, 0u, nullptr,
                         scratch, scratch_bytes, stream);
 }
 
@@ -269,6 +246,101 @@ int fsld_scatter_sq_tab(int M, int mode, int n_mask, const int16_t* pix, const f
     a.acc = acc;
     a.fx = fx_scale;
     return status_of(launch_slice(OP_DIAG, mode, det, a, B * a.tiles, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+// ---------------------------------------------------------------- brick-sorted dataset layout
+
+int fsld_sorted_count(int M, int n_mask, const int16_t* pix, const fsld_image_rec* recs, int N, int32_t* seg_off,
+                      void* stream) {
+    if (M < 2 || M > 256 || n_mask < 1 || n_mask > 65535 || N < 1 || !pix || !recs || !seg_off) return FSLD_EINVAL;
+    return status_of(launch_sorted_count(M, n_mask, reinterpret_cast<const short2*>(pix), recs, N, seg_off,
+                                         reinterpret_cast<cudaStream_t>(stream)));
+}
+
+int fsld_sorted_fill(int M, int n_mask, const int16_t* pix, const fsld_image_rec* recs, int N, const void* x_in,
+                     void* x_out, int8_t* pc_out, const int32_t* seg_off, int32_t* segs, void* stream) {
+    if (M < 2 || M > 256 || n_mask < 1 || n_mask > 65535 || N < 1 || !pix || !recs || !pc_out || !seg_off || !segs)
+        return FSLD_EINVAL;
+    if (x_in && !x_out) return FSLD_EINVAL;
+    return status_of(launch_sorted_fill(M, n_mask, reinterpret_cast<const short2*>(pix), recs, N,
+                                        reinterpret_cast<const float2*>(x_in), reinterpret_cast<float2*>(x_out),
+                                        reinterpret_cast<char2*>(pc_out), seg_off, reinterpret_cast<int2*>(segs),
+                                        reinterpret_cast<cudaStream_t>(stream)));
+}
+
+int fsld_loss_grad_sorted(int M, int mode, int n_mask, const fsld_image_rec* recs, const int32_t* idx, int B,
+                          const void* v, const void* xs, const int8_t* pc, const int32_t* seg_off, const int32_t* segs,
+                          void* grad_acc, double* sq_out, unsigned flags, const double* fx_scale, void* scratch,
+                          size_t scratch_bytes, void* stream) {
+    if (!geom_ok(M, mode, n_mask, B) || M > 256) return FSLD_EINVAL;
+    if (!recs || !v || !xs || !pc || !grad_acc || !sq_out || !scratch) return FSLD_EINVAL;
+    const bool det = (flags & FSLD_DETERMINISTIC) != 0;
+    if (mode != FSLD_MODE_TRI || det || (flags & FSLD_TILE_PATH) || !seg_off || !segs)
+        return run_reducing(OP_LOSS_GRAD, M, mode, n_mask, nullptr, pc, recs, idx, B, v, xs, grad_acc, sq_out, flags,
+                            fx_scale, scratch, scratch_bytes, stream);
+    const ScratchLayout L = scratch_layout(M, n_mask, B);
+    if (scratch_bytes < L.total) return FSLD_EINVAL;
+    char* scr = reinterpret_cast<char*>(scratch);
+    SortedArgs b{};
+    b.M = M;
+    b.c = (M + 1) / 2;
+    b.nb = L.nb;
+    b.nbr = L.nbr;
+    b.n_mask = n_mask;
+    b.B = B;
+    b.bnd = (float)(M / 2 - 1);
+    b.recs = recs;
+    b.idx = idx;
+    b.v = reinterpret_cast<const float2*>(v);
+    b.xs = reinterpret_cast<const float2*>(xs);
+    b.pc = reinterpret_cast<const char2*>(pc);
+    b.seg_off = seg_off;
+    b.segs = reinterpret_cast<const int2*>(segs);
+    b.acc = reinterpret_cast<float2*>(grad_acc);
+    b.cnt = reinterpret_cast<int*>(scr + L.cnt);
+    b.off = reinterpret_cast<int*>(scr + L.off);
+    b.fill = reinterpret_cast<int*>(scr + L.fill);
+    b.pairs = reinterpret_cast<int2*>(scr + L.pairs);
+    b.items = reinterpret_cast<int4*>(scr + L.items);
+    b.ctl = reinterpret_cast<int*>(scr + L.ctl);
+    b.part = reinterpret_cast<double*>(scr + L.part);
+    b.cap_pairs = L.cap_pairs;
+    b.cap_items = L.cap_items;
+    return status_of(launch_sorted_loss_grad(b, sq_out, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+int fsld_loss_sorted(int M, int mode, int n_mask, const fsld_image_rec* recs, const int32_t* idx, int B,
+                     const void* v, const void* xs, const int8_t* pc, double* sq_out, void* scratch,
+                     size_t scratch_bytes, void* stream) {
+    if (!pc) return FSLD_EINVAL;
+    return run_reducing(OP_LOSS, M, mode, n_mask, nullptr, pc, recs, idx, B, v, xs, nullptr, sq_out, 0u, nullptr,
+                        scratch, scratch_bytes, stream);
+}
+
+int fsld_project_sorted(int M, int mode, int n_mask, const fsld_image_rec* recs, const int32_t* idx, int B,
+                        const void* v, const int8_t* pc, void* out, void* stream) {
+    if (!geom_ok(M, mode, n_mask, B) || !recs || !v || !pc || !out) return FSLD_EINVAL;
+    SliceArgs a = make_args(M, n_mask, nullptr, recs, idx);
+    a.v = reinterpret_cast<const float2*>(v);
+    a.out = reinterpret_cast<float2*>(out);
+    a.pc = reinterpret_cast<const char2*>(pc);
+    a.x_by_idx = 1;
+    return status_of(launch_slice(OP_PROJECT, mode, false, a, B * a.tiles, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+int fsld_backproject_sorted(int M, int mode, int n_mask, const fsld_image_rec* recs, const int32_t* idx, int B,
+                            const void* xs, const int8_t* pc, void* acc, unsigned flags, const double* fx_scale,
+                            void* stream) {
+    if (!geom_ok(M, mode, n_mask, B) || !recs || !xs || !pc || !acc) return FSLD_EINVAL;
+    const bool det = (flags & FSLD_DETERMINISTIC) != 0;
+    if (det && !fx_scale) return FSLD_EINVAL;
+    SliceArgs a = make_args(M, n_mask, nullptr, recs, idx);
+    a.x = reinterpret_cast<const float2*>(xs);
+    a.x_by_idx = 1;
+    a.pc = reinterpret_cast<const char2*>(pc);
+    a.acc = acc;
+    a.fx = fx_scale;
+    return status_of(launch_slice(OP_BACKPROJECT, mode, det, a, B * a.tiles, reinterpret_cast<cudaStream_t>(stream)));
 }
 
 int fsld_fixed_scale(const void* data, int64_t n, double mult, double add, double* fx_scale, void* stream) {

@@ -23,65 +23,69 @@ struct SliceArgs {
     double* partials;      // per-CTA loss partials
     const double* fx;      // fixed-point scale (deterministic)
     const float2* ftab;    // optional (B, n_mask) factor table f = phase*ctf (numba-style calls)
+    const char2* pc;       // optional per-(row, p) pixel coordinates (brick-sorted dataset layout)
 };
 
 // ---------------------------------------------------------------------------
-// Brick-binned path (fsld_brick.cu): the volume is cut into BT^3 bricks in
-// frequency space; every (brick, batch image) pair whose slice plane crosses
-// the brick is binned, and one CTA per work item (brick, <= BC images)
-// gathers from / scatters into a shared-memory copy of the brick (+1 halo),
-// so the adjoint costs one global reduction per brick voxel per item
-// instead of 8 per pixel.
+// Brick-sorted path (fsld_brick.cu).  Poses are fixed for the whole run, so
+// each image's masked pixels are stored once in HBM grouped by the 8^3 volume
+// brick that owns their trilinear footprint (floor corner), with per-pixel
+// (kx, ky) as int8 pairs and a per-image segment list (brick, start, count).
+// Per step the batch's segments are binned by brick (count -> scan -> fill)
+// into work items (brick, <= BC segments); one CTA per item gathers from /
+// scatters into a shared-memory copy of the brick (+1 halo), so the adjoint
+// costs one global reduction per touched brick voxel per item instead of 8
+// per pixel.
 // ---------------------------------------------------------------------------
 constexpr int BT = 8;                 // brick edge (voxels)
 constexpr int BH = BT + 1;            // + halo for the floor+1 corners
 constexpr int BH3 = BH * BH * BH;     // 729
-constexpr int BC = 32;                // images per work item
+constexpr int BC = 32;                // segments (images) per work item
 constexpr int BW = 8;                 // warps per CTA
 constexpr int BTHREADS = BW * 32;
-constexpr int BMAXCAND = 448;         // per-warp candidate table (rows*row length bound)
 constexpr uint32_t kGeomMagic = 0xF51DB200u;
 
 struct GeomHeader {   // at the start of the scratch buffer (256-byte slot)
     uint32_t magic;
     int M, n_mask, pad0;
     const void* pix;
-    unsigned rmax2;   // max kx^2+ky^2 over the mask
-    int pad1[9];
+    int pad1[10];
 };
 
 struct ScratchLayout {
-    size_t hdr, pix2p, rowmin, rowmax, cnt, off, fill, pairs, items, ctl, part, total;
+    size_t hdr, cnt, off, fill, pairs, items, ctl, part, total;
     int nb, nbr, cap_pairs, cap_items, cap_part;
 };
 
 ScratchLayout scratch_layout(int M, int n_mask, int B);
 
-struct BrickArgs {
+struct SortedArgs {
     int M, c, nb, nbr, n_mask, B;
     float bnd;
-    const int* pix2p;       // M*M -> compact pixel index or -1
-    const int* rowmin;      // per py row (index py + c): min px (or large)
-    const int* rowmax;
-    const GeomHeader* hdr;
     const fsld_image_rec* recs;
     const int32_t* idx;
     const float2* v;
-    const float2* x;
+    const float2* xs;        // (N, n_mask) brick-sorted images
+    const char2* pc;         // (N, n_mask) (kx, ky) of each sorted pixel
+    const int32_t* seg_off;  // (N+1) CSR offsets into segs
+    const int2* segs;        // (brick, start | count << 16)
     float2* acc;
     int* cnt;
     int* off;
     int* fill;
-    int* pairs;
-    int4* items;
+    int2* pairs;             // (batch entry b, global segment index)
+    int4* items;             // (brick, first pair, n pairs, 0)
     int* ctl;
     double* part;
     int cap_pairs, cap_items;
 };
 
-cudaError_t launch_geom_prepare(int M, int n_mask, const short2* pix, const ScratchLayout& L, char* scratch,
-                                cudaStream_t s);
-cudaError_t launch_brick_loss_grad(const BrickArgs& a, double* sq_out, cudaStream_t s);
+cudaError_t launch_sorted_count(int M, int n_mask, const short2* pix, const fsld_image_rec* recs, int N,
+                                int32_t* seg_off, cudaStream_t s);
+cudaError_t launch_sorted_fill(int M, int n_mask, const short2* pix, const fsld_image_rec* recs, int N,
+                               const float2* x_in, float2* x_out, char2* pc_out, const int32_t* seg_off,
+                               int2* segs, cudaStream_t s);
+cudaError_t launch_sorted_loss_grad(const SortedArgs& a, double* sq_out, cudaStream_t s);
 
 cudaError_t launch_slice(int op, int mode, bool det, const SliceArgs& a, int nblocks, cudaStream_t s);
 cudaError_t launch_reduce(const double* part, int n, double* out, cudaStream_t s);

@@ -36,12 +36,20 @@ __global__ void __launch_bounds__(kThreads) slice_kernel(SliceArgs a) {
     if (OP == OP_LOSS || OP == OP_LOSS_GRAD || OP == OP_BACKPROJECT)
         xrow = a.x + (size_t)(a.x_by_idx ? row : b) * n;
     float sq = 0.0f;
+    // brick-sorted dataset layout: per-(row, p) coordinates instead of the shared mask table
+    const char2* __restrict__ pcrow = a.pc ? a.pc + (size_t)(a.x_by_idx ? row : b) * n : nullptr;
 
     const int p0 = tile * a.ppt * kThreads + threadIdx.x;
     for (int k = 0; k < a.ppt; ++k) {
         const int p = p0 + k * kThreads;
         if (p >= n) break;
-        const short2 kk = __ldg(a.pix + p);
+        short2 kk;
+        if (pcrow) {
+            const char2 q = pcrow[p];
+            kk = make_short2(q.x, q.y);
+        } else {
+            kk = __ldg(a.pix + p);
+        }
         const int kx = kk.x, ky = kk.y;
         double cx, cy, cz;
         rotate_pixel(rec.rot, (double)kx, (double)ky, bnd, cx, cy, cz);

@@ -46,7 +46,7 @@ class SliceEngine:
     """One dataset resident on one GPU (see module docstring)."""
 
     def __init__(self, M: int, mode: str, mask: np.ndarray, recs: np.ndarray, x=None,
-                 deterministic: bool = False, device=None, tile_path: bool = False):
+                 deterministic: bool = False, device=None, tile_path: bool = False, layout: str | None = None):
         if mode not in ("nn", "tri"):
             raise ValueError("mode must be one of ('nn', 'tri')")
         self.dev = device or require_device()
@@ -63,23 +63,75 @@ class SliceEngine:
         recs = np.ascontiguousarray(recs, dtype=C.REC_DTYPE)
         self.n_images = int(recs.shape[0])
         self.recs = torch.from_numpy(recs.view(np.uint8).copy()).to(self.dev)
+        # dataset layout of x: "sorted" = brick-sorted (fsld_sorted_*; needs M <= 256), "mask" = mask order
+        if layout is None:
+            layout = "sorted" if (self.M <= 256 and self.n_mask <= 65535 and self.n_images > 0) else "mask"
+        if layout not in ("sorted", "mask"):
+            raise ValueError("layout must be 'sorted' or 'mask'")
+        self.layout = layout
+        self.pc = self.seg_off = self.segs = None
+        if layout == "sorted":
+            self._build_sorted_index()
         self.x = None
         self.x_maxabs = 0.0
+        self._scratch = None
         if x is not None:
             self.set_images(x)
-        self._scratch = None
         self._bad = torch.zeros(1, dtype=torch.int32, device=self.dev)
         self._all_idx = None
 
     # ---- data -----------------------------------------------------------
-    def set_images(self, x):
-        """Upload observed images (N, n_mask) as complex64 (DatasetOperator.x, forward.py:527)."""
+    def _build_sorted_index(self):
+        """Per-image brick-sorted pixel order: pc (N, n, 2) int8 and the segment list (once per dataset)."""
+        lib = C.load()
+        N = self.n_images
+        self.seg_off = torch.empty(N + 1, dtype=torch.int32, device=self.dev)
+        C.check(lib.fsld_sorted_count(self.M, self.n_mask, ctypes_ptr(self.pix), ctypes_ptr(self.recs), N,
+                                      ctypes_ptr(self.seg_off), _stream()), "fsld_sorted_count")
+        nseg = int(self.seg_off[N].item())
+        self.segs = torch.empty((max(nseg, 1), 2), dtype=torch.int32, device=self.dev)
+        self.pc = torch.empty((N, self.n_mask, 2), dtype=torch.int8, device=self.dev)
+        C.check(lib.fsld_sorted_fill(self.M, self.n_mask, ctypes_ptr(self.pix), ctypes_ptr(self.recs), N, 0, 0,
+                                     ctypes_ptr(self.pc), ctypes_ptr(self.seg_off), ctypes_ptr(self.segs),
+                                     _stream()), "fsld_sorted_fill")
+
+    def _sort_images(self, xd: torch.Tensor) -> torch.Tensor:
+        """Mask-order images -> brick-sorted order (same permutation as pc; order within a segment may differ
+        between builds, pc is rewritten consistently)."""
+        lib = C.load()
+        xs = torch.empty_like(xd)
+        C.check(lib.fsld_sorted_fill(self.M, self.n_mask, ctypes_ptr(self.pix), ctypes_ptr(self.recs),
+                                     self.n_images, ctypes_ptr(xd), ctypes_ptr(xs), ctypes_ptr(self.pc),
+                                     ctypes_ptr(self.seg_off), ctypes_ptr(self.segs), _stream()), "fsld_sorted_fill")
+        return xs
+
+    def x_masked(self) -> torch.Tensor:
+        """Observed images in mask (reference) pixel order (N, n_mask) complex64."""
+        if self.layout == "mask" or self.x is None:
+            return self.x
+        c = (self.M + 1) // 2
+        lut = torch.full((self.M * self.M,), -1, dtype=torch.int64, device=self.dev)
+        pix = self.pix.long()
+        lut[(pix[:, 1] + c) * self.M + pix[:, 0] + c] = torch.arange(self.n_mask, device=self.dev)
+        pc = self.pc.long()
+        orig = lut[(pc[..., 1] + c) * self.M + pc[..., 0] + c]
+        out = torch.empty_like(self.x)
+        out.scatter_(1, orig, self.x)
+        return out
+
+    def set_images(self, x, sorted_order: bool = False):
+        """Upload observed images (N, n_mask) as complex64 (DatasetOperator.x, forward.py:527).
+
+        Images are given in mask order (reference layout) unless ``sorted_order`` (already in this
+        engine's brick-sorted order, e.g. produced by project_sorted)."""
         if isinstance(x, torch.Tensor):
             xd = x.to(self.dev, torch.complex64).contiguous()
         else:
             xd = torch.from_numpy(np.ascontiguousarray(x, dtype=np.complex64)).to(self.dev)
         if tuple(xd.shape) != (self.n_images, self.n_mask):
             raise ValueError(f"images shape {tuple(xd.shape)} != ({self.n_images}, {self.n_mask})")
+        if self.layout == "sorted" and not sorted_order:
+            xd = self._sort_images(xd)
         self.x = xd
         if xd.numel():
             # per-image max |x| into fsld_image_rec.xmax (bounds the brick fixed-point accumulator)
@@ -155,6 +207,13 @@ class SliceEngine:
             fx = self.fixed_scale(v, HITS_PER_IMAGE * (fx_batch or B), self.x_maxabs)
         sq = torch.empty(1, dtype=torch.float64, device=self.dev)
         scr = self.scratch(B)
+        if self.layout == "sorted":
+            C.check(lib.fsld_loss_grad_sorted(self.M, self.mode_id, self.n_mask, ctypes_ptr(self.recs),
+                                              ctypes_ptr(idx), B, ctypes_ptr(v), ctypes_ptr(self.x),
+                                              ctypes_ptr(self.pc), ctypes_ptr(self.seg_off), ctypes_ptr(self.segs),
+                                              ctypes_ptr(acc), ctypes_ptr(sq), self.flags, ctypes_ptr(fx),
+                                              ctypes_ptr(scr), scr.numel() * 8, _stream()), "fsld_loss_grad_sorted")
+            return sq, acc, fx
         C.check(lib.fsld_loss_grad(self.M, self.mode_id, self.n_mask, ctypes_ptr(self.pix),
                                    ctypes_ptr(self.recs), ctypes_ptr(idx), B, ctypes_ptr(v),
                                    ctypes_ptr(self.x), ctypes_ptr(acc), ctypes_ptr(sq), self.flags,
@@ -170,10 +229,42 @@ class SliceEngine:
         B = idx.numel()
         sq = torch.empty(1, dtype=torch.float64, device=self.dev)
         scr = self.scratch(B)
+        if self.layout == "sorted":
+            C.check(lib.fsld_loss_sorted(self.M, self.mode_id, self.n_mask, ctypes_ptr(self.recs), ctypes_ptr(idx), B,
+                                         ctypes_ptr(v), ctypes_ptr(self.x), ctypes_ptr(self.pc), ctypes_ptr(sq),
+                                         ctypes_ptr(scr), scr.numel() * 8, _stream()), "fsld_loss_sorted")
+            return sq
         C.check(lib.fsld_loss(self.M, self.mode_id, self.n_mask, ctypes_ptr(self.pix), ctypes_ptr(self.recs),
                               ctypes_ptr(idx), B, ctypes_ptr(v), ctypes_ptr(self.x), ctypes_ptr(sq),
                               ctypes_ptr(scr), scr.numel() * 8, _stream()), "fsld_loss")
         return sq
+
+    def project_sorted(self, v, idx, out=None) -> torch.Tensor:
+        """Projections of dataset rows idx in their brick-sorted pixel order (dataset synthesis)."""
+        lib = C.load()
+        v = self._vol(v)
+        idx = self.idx_tensor(idx)
+        if out is None:
+            out = torch.empty((idx.numel(), self.n_mask), dtype=torch.complex64, device=self.dev)
+        C.check(lib.fsld_project_sorted(self.M, self.mode_id, self.n_mask, ctypes_ptr(self.recs), ctypes_ptr(idx),
+                                        idx.numel(), ctypes_ptr(v), ctypes_ptr(self.pc), ctypes_ptr(out), _stream()),
+                "fsld_project_sorted")
+        return out
+
+    def backproject_dataset(self, idx, acc=None, fx=None):
+        """acc += sum_b P^* conj(f) x[idx[b]] over dataset rows (b_vector, forward.py:572-579)."""
+        if self.layout == "mask":
+            return self.backproject(self.x[self.idx_tensor(idx).long()], idx, acc, fx)
+        lib = C.load()
+        idx = self.idx_tensor(idx)
+        acc = self.new_cacc() if acc is None else acc
+        if self.deterministic and fx is None:
+            fx = self.fixed_scale(self.x, HITS_PER_IMAGE * idx.numel(), 0.0)
+        C.check(lib.fsld_backproject_sorted(self.M, self.mode_id, self.n_mask, ctypes_ptr(self.recs),
+                                            ctypes_ptr(idx), idx.numel(), ctypes_ptr(self.x), ctypes_ptr(self.pc),
+                                            ctypes_ptr(acc), self.flags, ctypes_ptr(fx), _stream()),
+                "fsld_backproject_sorted")
+        return acc, fx
 
     def project(self, v, idx) -> torch.Tensor:
         lib = C.load()
@@ -310,6 +401,14 @@ class SliceEngine:
         C.check(lib.fsld_norm2(self.n_voxels, ctypes_ptr(v), ctypes_ptr(out), ctypes_ptr(scr), scr.numel() * 8,
                                _stream()), "fsld_norm2")
         return out
+
+
+def _rows_contiguous(pix: np.ndarray) -> bool:
+    """True if every mask row is one run of consecutive kx in ascending index order (disk masks are)."""
+    ky = pix[:, 1].astype(np.int64)
+    kx = pix[:, 0].astype(np.int64)
+    same = ky[1:] == ky[:-1]
+    return bool(np.all(np.diff(ky) >= 0) and np.all(kx[1:][same] - kx[:-1][same] == 1))
 
 
 def records_for(M: int, quats, shifts=None, ctfs=None) -> np.ndarray:

@@ -282,7 +282,7 @@ class DatasetOperator:
     @property
     def x(self) -> np.ndarray:
         """Masked observed images (N, n_mask), host copy (forward.py:527)."""
-        return _to_host_c128(self.engine.x)
+        return _to_host_c128(self.engine.x_masked())
 
     @property
     def rots(self) -> np.ndarray:
@@ -350,7 +350,7 @@ class DatasetOperator:
     def b_vector(self):
         """sum_i P_i^* C_i x_i over all images (forward.py:572-579)."""
         e = self.engine
-        acc, fx = e.backproject(e.x, e.all_indices())
+        acc, fx = e.backproject_dataset(e.all_indices())
         return _to_host_c128(e.finalize_c(acc, fx, 1.0, 0.0))
 
 

@@ -130,7 +130,11 @@ def build_workload(cfg: Config, seed: int = 0, n_images: int | None = None, dete
     power = 0.0
     for lo in range(0, N, chunk):
         idx = torch.arange(lo, min(lo + chunk, N), dtype=torch.int32, device=eng.dev)
-        x[lo:lo + idx.numel()] = eng.project(vd, idx)
+        # project straight into the engine's dataset layout (brick-sorted for tri)
+        if eng.layout == "sorted":
+            eng.project_sorted(vd, idx, out=x[lo:lo + idx.numel()])
+        else:
+            x[lo:lo + idx.numel()] = eng.project(vd, idx)
         power += float(torch.view_as_real(x[lo:lo + idx.numel()]).pow(2).sum().item())
     sigma = float(np.sqrt(power / (N * mask.size) / cfg.snr))
     g = torch.Generator(device=eng.dev)
@@ -139,5 +143,5 @@ def build_workload(cfg: Config, seed: int = 0, n_images: int | None = None, dete
         hi = min(lo + chunk, N)
         nz = torch.randn((hi - lo, mask.size, 2), generator=g, device=eng.dev, dtype=torch.float32)
         x[lo:hi] += torch.view_as_complex(nz * (sigma / np.sqrt(2.0)))
-    eng.set_images(x)
+    eng.set_images(x, sorted_order=True)
     return Workload(cfg, M, mask, v, quats, shifts, ctfs, eng, sigma)
