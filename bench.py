@@ -224,11 +224,13 @@ def run_b200(args):
                for _ in range(n_steps)]
     stream = _stream()
     flags = C.TILE_PATH if os.environ.get("FSLD_TILE_PATH") else 0
-    # loss_grad: memset(cnt) + count + scan + fill + brick kernel + reduce = 5 kernels; norm2 (2), grad_finalize
-    launches_per_step = 8 if not flags else 5
+    # loss_grad: count + scan + fill + brick kernel + reduce (5 kernels, + cnt memset); fused epilogue (2)
+    launches_per_step = 7 if not flags else 4
+
+    loss = torch.empty(1, dtype=torch.float64, device=dev)
 
     def step(idx, ev_k0=None, ev_k1=None):
-        acc.zero_()
+        # acc is zero on entry (zeroed by the previous step's fused epilogue)
         if ev_k0 is not None:
             ev_k0.record()
         C.check(lib.fsld_loss_grad_sorted(M, eng.mode_id, n, ctypes_ptr(eng.recs), ctypes_ptr(idx), B,
@@ -238,16 +240,16 @@ def run_b200(args):
                 "loss_grad")
         if ev_k1 is not None:
             ev_k1.record()
-        C.check(lib.fsld_norm2(M ** 3, ctypes_ptr(v), ctypes_ptr(nrm), ctypes_ptr(nscr), nscr.numel() * 8, stream),
-                "norm2")
-        if world > 1:
+        if world > 1:  # one packed all-reduce: [grad accumulator | loss hi, lo]
             s32 = sq.float()
             packed[-2:-1].copy_(s32)
             packed[-1:].copy_((sq - s32.double()).float())
             dist.all_reduce(packed)
-        C.check(lib.fsld_grad_finalize(M ** 3, ctypes_ptr(acc), 0, 0, ctypes_ptr(v), scale, lam, ctypes_ptr(grad),
-                                       stream), "finalize")
-        return 0.5 * scale * sq + 0.5 * lam * nrm
+            sq.copy_(packed[-2:-1].double() + packed[-1:].double())
+        C.check(lib.fsld_grad_epilogue(M ** 3, ctypes_ptr(acc), ctypes_ptr(v), scale, lam, ctypes_ptr(grad),
+                                       ctypes_ptr(sq), ctypes_ptr(loss), 0, ctypes_ptr(nscr), nscr.numel() * 8,
+                                       stream), "epilogue")
+        return loss
 
     for i in range(args.warmup):
         step(batches[i])

@@ -263,6 +263,16 @@ int fsld_grad_finalize(int64_t nvox, const void* acc, unsigned flags, const doub
 int fsld_real_finalize(int64_t nvox, const void* acc, unsigned flags, const double* fx_scale,
                        double scale, double add, float* out, void* stream);
 
+/*
+ * Fused loss_and_grad epilogue (optim.py:186-189), one pass over the volume:
+ *   grad = scale * acc + lam * v  (complex64);  acc is zeroed for the next step;
+ *   *loss = 0.5 * scale * (*sq) + 0.5 * lam * ||v||^2  (device doubles; loss / norm2 may be NULL).
+ * scratch: >= 1184 doubles of per-block partials (fixed reduction order).
+ */
+int fsld_grad_epilogue(int64_t nvox, void* acc, const void* v, double scale, double lam, void* grad,
+                       const double* sq, double* loss, double* norm2, void* scratch, size_t scratch_bytes,
+                       void* stream);
+
 /* sum |v|^2 over complex64 M^3 in a fixed order (fp64), for the lam/2 ||v||^2 term. */
 int fsld_norm2(int64_t n, const void* v, double* out, void* scratch, size_t scratch_bytes,
                void* stream);

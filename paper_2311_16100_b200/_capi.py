@@ -77,6 +77,7 @@ SIGNATURES = {
     "fsld_grad_finalize": (I, [I64, P, U, P, P, D, D, P, P]),
     "fsld_real_finalize": (I, [I64, P, U, P, D, D, P, P]),
     "fsld_norm2": (I, [I64, P, P, P, SZ, P]),
+    "fsld_grad_epilogue": (I, [I64, P, P, D, D, P, P, P, P, P, SZ, P]),
 }
 
 _lib = None

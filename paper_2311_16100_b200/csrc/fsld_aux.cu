@@ -124,3 +124,47 @@ cudaError_t launch_norm2(int64_t n, const float2* v, double* out, double* part, 
 }
 
 }  // namespace fsld
+
+namespace fsld {
+
+// Fused loss_and_grad epilogue (optim.py:186-189) in one pass over the volume:
+//   grad = scale * acc + lam * v;  acc <- 0 (ready for the next step);
+//   per-block partials of ||v||^2 (fixed order) -> loss kernel.
+__global__ void __launch_bounds__(256) grad_epilogue_kernel(int64_t n, float2* __restrict__ acc,
+                                                            const float2* __restrict__ v, float scale, float lam,
+                                                            float2* __restrict__ grad, double* part) {
+    __shared__ double smem[32];
+    double s = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const float2 a = acc[i];
+        const float2 w = v[i];
+        grad[i] = make_float2(fmaf(scale, a.x, lam * w.x), fmaf(scale, a.y, lam * w.y));
+        acc[i] = make_float2(0.f, 0.f);
+        s += (double)w.x * w.x + (double)w.y * w.y;
+    }
+    s = block_sum(s, smem);
+    if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+// loss = 0.5 * scale * sq + 0.5 * lam * sum(part)   (fixed reduction order)
+__global__ void __launch_bounds__(1024) loss_kernel(const double* __restrict__ part, int nparts, const double* sq,
+                                                    double scale, double lam, double* loss, double* norm2) {
+    __shared__ double smem[32];
+    double s = 0.0;
+    for (int i = threadIdx.x; i < nparts; i += blockDim.x) s += part[i];
+    s = block_sum(s, smem);
+    if (threadIdx.x == 0) {
+        if (norm2) *norm2 = s;
+        if (loss) *loss = 0.5 * scale * (*sq) + 0.5 * lam * s;
+    }
+}
+
+cudaError_t launch_grad_epilogue(int64_t nvox, float2* acc, const float2* v, double scale, double lam, float2* grad,
+                                 const double* sq, double* loss, double* norm2, double* part, int nparts,
+                                 cudaStream_t s) {
+    grad_epilogue_kernel<<<nparts, 256, 0, s>>>(nvox, acc, v, (float)scale, (float)lam, grad, part);
+    loss_kernel<<<1, 1024, 0, s>>>(part, nparts, sq, scale, lam, loss, norm2);
+    return cudaGetLastError();
+}
+
+}  // namespace fsld

@@ -375,3 +375,15 @@ int fsld_norm2(int64_t n, const void* v, double* out, void* scratch, size_t scra
 }
 
 }  // extern "C"
+
+extern "C" int fsld_grad_epilogue(int64_t nvox, void* acc, const void* v, double scale, double lam, void* grad,
+                                  const double* sq, double* loss, double* norm2, void* scratch, size_t scratch_bytes,
+                                  void* stream) {
+    const int nparts = 148 * 8;
+    if (nvox < 1 || !acc || !v || !grad || !sq || !scratch || scratch_bytes < nparts * sizeof(double))
+        return FSLD_EINVAL;
+    return status_of(launch_grad_epilogue(nvox, reinterpret_cast<float2*>(acc), reinterpret_cast<const float2*>(v),
+                                          scale, lam, reinterpret_cast<float2*>(grad), sq, loss, norm2,
+                                          reinterpret_cast<double*>(scratch), nparts,
+                                          reinterpret_cast<cudaStream_t>(stream)));
+}

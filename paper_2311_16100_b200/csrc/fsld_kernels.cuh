@@ -101,5 +101,8 @@ cudaError_t launch_grad_finalize(int64_t nvox, const void* acc, bool det, const 
 cudaError_t launch_real_finalize(int64_t nvox, const void* acc, bool det, const double* fx, double scale,
                                  double add, float* out, cudaStream_t s);
 cudaError_t launch_norm2(int64_t n, const float2* v, double* out, double* part, int nparts, cudaStream_t s);
+cudaError_t launch_grad_epilogue(int64_t nvox, float2* acc, const float2* v, double scale, double lam, float2* grad,
+                                 const double* sq, double* loss, double* norm2, double* part, int nparts,
+                                 cudaStream_t s);
 
 }  // namespace fsld

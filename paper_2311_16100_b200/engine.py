@@ -369,6 +369,20 @@ class SliceEngine:
                                    ctypes_ptr(idx), idx.numel(), ctypes_ptr(out), _stream()), "fsld_assign_nn")
         return out
 
+    def epilogue(self, acc, v, scale: float, lam: float, sq, grad=None, loss=None):
+        """Fused grad = scale*acc + lam*v, acc <- 0, loss = scale/2 sq + lam/2 ||v||^2 (optim.py:186-189).
+
+        Complex64 accumulators only (the deterministic int64 path uses finalize_c + norm2)."""
+        lib = C.load()
+        v = self._vol(v)
+        grad = torch.empty(self.n_voxels, dtype=torch.complex64, device=self.dev) if grad is None else grad
+        loss = torch.empty(1, dtype=torch.float64, device=self.dev) if loss is None else loss
+        scr = self._norm_scratch()
+        C.check(lib.fsld_grad_epilogue(self.n_voxels, ctypes_ptr(acc), ctypes_ptr(v), float(scale), float(lam),
+                                       ctypes_ptr(grad), ctypes_ptr(sq), ctypes_ptr(loss), 0, ctypes_ptr(scr),
+                                       scr.numel() * 8, _stream()), "fsld_grad_epilogue")
+        return loss, grad
+
     def _norm_scratch(self) -> torch.Tensor:
         if getattr(self, "_nscr", None) is None:
             self._nscr = torch.empty(148 * 8, dtype=torch.float64, device=self.dev)

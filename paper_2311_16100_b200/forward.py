@@ -337,11 +337,14 @@ class DatasetOperator:
         scale = n_total / B
         st["v"].copy_(v_host, non_blocking=True)
         idx = idx_host.to(e.dev, non_blocking=True)
-        st["acc"].zero_()
-        sq, acc, fx = e.loss_grad(st["v"], idx, st["acc"])
-        e.finalize_c(acc, fx, scale, lam, st["v"], out=st["g"])
-        nrm = e.norm2(st["v"])
-        st["out"][0:1].copy_(0.5 * scale * sq + 0.5 * lam * nrm)
+        if e.deterministic:
+            st["acc"].zero_()
+            sq, acc, fx = e.loss_grad(st["v"], idx, st["acc"])
+            e.finalize_c(acc, fx, scale, lam, st["v"], out=st["g"])
+            st["out"][0:1].copy_(0.5 * scale * sq + 0.5 * lam * e.norm2(st["v"]))
+        else:  # accumulator stays zero between calls: the fused epilogue clears it
+            sq, acc, fx = e.loss_grad(st["v"], idx, st["acc"])
+            e.epilogue(acc, st["v"], scale, lam, sq, grad=st["g"], loss=st["out"][0:1])
         grad_host.copy_(st["g"], non_blocking=True)
         st["out_h"].copy_(st["out"], non_blocking=True)
         torch.cuda.current_stream().synchronize()

@@ -81,8 +81,11 @@ def loss_and_grad(op, v, batch, lam: float, n_total: int | None = None):
     if _is_dev(v):
         vd = e._vol(v)
         sq, acc, fx = e.loss_grad(vd, batch)
-        loss = 0.5 * scale * sq[0] + 0.5 * lam * e.norm2(vd)[0]
-        return loss, e.finalize_c(acc, fx, scale, lam, vd)
+        if e.deterministic:
+            loss = 0.5 * scale * sq[0] + 0.5 * lam * e.norm2(vd)[0]
+            return loss, e.finalize_c(acc, fx, scale, lam, vd)
+        loss, grad = e.epilogue(acc, vd, scale, lam, sq)
+        return loss[0], grad
     v = np.asarray(v, dtype=np.complex128).reshape(-1)
     sq, acc, fx = e.loss_grad(_to_dev_c64(v, e.dev), batch)
     g = _to_host_c128(e.finalize_c(acc, fx, 1.0, 0.0))

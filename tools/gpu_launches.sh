@@ -1,8 +1,5 @@
-# tests + smoke + bench + launch list of a short bench (cfg3 on 4096 images)
-python -m pytest tests -m gpu -q -x 2>&1 | tail -15
-python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
-timeout 900 python bench.py --steps 10 --warmup 3 > gpurun_out/bench.log 2>&1; tail -1 gpurun_out/bench.log
+# launch list of a short bench (cfg3 on 4096 images): per-kernel device time shares
 B="python bench.py --images 4096 --steps 3 --warmup 3 --no-cpu-baseline --no-e2e"
 $B > gpurun_out/plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $B > gpurun_out/ncu1.log 2>&1
-tail -2 gpurun_out/ncu1.log
+tail -1 gpurun_out/ncu1.log | cut -c1-200
