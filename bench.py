@@ -307,7 +307,7 @@ def run_b200(args):
                        "parallelism": f"dp{world}", "l2": "flushed between timed steps (512 MB write)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic, "peak_source": src,
-                         "kernel": "fsld slice_kernel<TRI,LOSS_GRAD> (+fixed-order loss reduce)",
+                         "kernel": ("fsld_loss_grad_sorted: bin count/scan/fill + sorted_loss_grad_kernel + loss reduce" if not flags else "fsld slice_kernel<TRI,LOSS_GRAD> (tile path)"),
                          "kernel_ms": t_kern, "algorithmic_bytes_per_launch": abytes},
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clk.summary(),
