@@ -42,7 +42,7 @@ ScratchLayout scratch_layout(int M, int n_mask, int B) {
     L.cnt = o; o = al(o + sizeof(int) * (size_t)L.nbr);
     L.off = o; o = al(o + sizeof(int) * (size_t)(L.nbr + 1));
     L.fill = o; o = al(o + sizeof(int) * (size_t)L.nbr);
-    L.pairs = o; o = al(o + sizeof(int2) * (size_t)L.cap_pairs);
+    L.pairs = o; o = al(o + sizeof(int4) * (size_t)L.cap_pairs);
     L.items = o; o = al(o + sizeof(int4) * (size_t)L.cap_items);
     L.ctl = o; o = al(o + 64);
     L.part = o; o = al(o + sizeof(double) * (size_t)L.cap_part);
@@ -207,7 +207,8 @@ __global__ void __launch_bounds__(128) bin_sorted_kernel(SortedArgs a) {
         const int brick = a.segs[sidx].x;
         if (FILL) {
             const int slot = atomicAdd(a.fill + brick, 1);
-            a.pairs[a.off[brick] + slot] = make_int2(b, sidx);
+            const int2 seg = a.segs[sidx];
+            a.pairs[a.off[brick] + slot] = make_int4(a.idx ? a.idx[b] : b, seg.y & 0xFFFF, seg.y >> 16, 0);
         } else {
             atomicAdd(a.cnt + brick, 1);
         }
@@ -261,225 +262,10 @@ __global__ void __launch_bounds__(1024) brick_scan_kernel(SortedArgs a) {
 
 // ---------------------------------------------------------------- main kernel
 
-// float -> int32 round-to-nearest for |x| < 2^22 via the 1.5*2^23 magic (FFMA + IADD, no F2I).
-constexpr float kMagic = 12582912.0f;
-constexpr int kMagicBits = 0x4B400000;
+#include "fsld_brick_main.cuh"  // the work-item kernel (kept separate: it is the tuning target)
 
-// Upper bound on the pixels one image owns in one brick: lattice points of a
-// plane section of a BT^3 cube (area <= BT^2 sqrt 2, perimeter <= 2 BT (1 + sqrt 2)).
-constexpr int BOWN_MAX = 112;
-constexpr int BBUF = BC * BOWN_MAX;
-
-struct SortedSmem {
-    float2 vb[BH3];                 // v brick + halo
-    int accr[BH3];                  // fixed-point adjoint accumulator (re)
-    int acci[BH3];                  // (im)
-    float2 bval[BBUF];              // pass 1 -> 2: conj(f) r per pixel of the item
-    unsigned char bk[BBUF];         // segment (image) of each pixel of the item
-    char2 bpc[BBUF];                // its (kx, ky), kept for pass 2
-    fsld_image_rec recs[BC];        // records of the item's images
-    float frame[BC][6];             // fp32 rows 0,1 of R
-    int seg_row[BC];                // dataset row of segment k
-    int seg_pos[BC];                // start of segment k in its row (sorted order)
-    int pref[BC + 1];               // exclusive prefix of segment lengths
-    int item;
-    int vmax_bits;
-    double red[BW];
-};
-
-// Item-local flat index e -> segment k (largest k with pref[k] <= e), binary search over <= 32.
-__device__ __forceinline__ int seg_of(const int* pref, int nseg, int e) {
-    int k = 0;
-#pragma unroll
-    for (int s = 16; s >= 1; s >>= 1)
-        if (k + s < nseg && pref[k + s] <= e) k += s;
-    return k;
-}
-
-// Two passes per work item over the item's pixels, flattened across its <= 32
-// segments (all lanes busy):
-//   1. per pixel: gather 8 corners from the smem brick, f = C * phase,
-//      r = f P v - x, |r|^2 -> loss, val = conj(f) r -> smem buffer;
-//   2. with the item's max |val| known, quantise val * w to int32 with a
-//      power-of-two scale (|val w s| <= 2^22; <= BC*12 contributions per voxel
-//      -> |sum| < 2^31) and add with native ATOMS.ADD (order-free, no CAS).
-// The scale follows the residual, not |Pv| or |x|: quantum ~2^-22 of the
-// item's largest contribution.
-__global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArgs a) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    SortedSmem& S = *reinterpret_cast<SortedSmem*>(smem_raw);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int M = a.M, c = a.c, nb = a.nb, n = a.n_mask;
-    const float bnd = a.bnd;
-    double lsum = 0.0;
-
-    for (;;) {
-        if (threadIdx.x == 0) {
-            S.item = atomicAdd(a.ctl + 1, 1);
-            S.vmax_bits = 0;
-        }
-        __syncthreads();
-        const int it = S.item;
-        if (it >= a.ctl[0]) break;
-        const int4 item = a.items[it];
-        const int bid = item.x, pstart = item.y, nseg = item.z;
-        const int bx = bid % nb, by = (bid / nb) % nb, bz = bid / (nb * nb);
-        const int ox = -c + BT * bx, oy = -c + BT * by, oz = -c + BT * bz;
-
-        if (warp == 0) {  // segment table + prefix of lengths (one warp)
-            int len = 0;
-            if (lane < nseg) {
-                const int2 pr = a.pairs[pstart + lane];
-                const int row = a.idx ? a.idx[pr.x] : pr.x;
-                const int2 seg = a.segs[pr.y];
-                S.seg_row[lane] = row;
-                S.seg_pos[lane] = seg.y & 0xFFFF;
-                len = seg.y >> 16;
-            }
-            int incl = len;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int t = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += t;
-            }
-            if (lane < nseg) S.pref[lane] = incl - len;
-            if (lane == 31) S.pref[nseg] = incl;
-        }
-        {   // v brick + halo: issue all loads before the stores
-            constexpr int U = (BH3 + BTHREADS - 1) / BTHREADS;
-            float2 vv[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int l = threadIdx.x + u * BTHREADS;
-                const int lx = l % BH, ly = (l / BH) % BH, lz = l / (BH * BH);
-                const int kx = ox + lx, ky = oy + ly, kz = oz + lz;
-                vv[u] = make_float2(0.f, 0.f);
-                if (l < BH3 && kx < M - c && ky < M - c && kz < M - c) vv[u] = __ldg(a.v + lin_index(kx, ky, kz, M, c));
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int l = threadIdx.x + u * BTHREADS;
-                if (l < BH3) {
-                    S.vb[l] = vv[u];
-                    S.accr[l] = 0;
-                    S.acci[l] = 0;
-                }
-            }
-        }
-        __syncthreads();
-        for (int w = threadIdx.x; w < nseg * 32; w += BTHREADS) {
-            const int k = w >> 5, q = w & 31;
-            reinterpret_cast<uint32_t*>(S.recs + k)[q] = __ldg(reinterpret_cast<const uint32_t*>(a.recs + S.seg_row[k]) + q);
-        }
-        __syncthreads();
-        if (threadIdx.x < nseg * 6) S.frame[threadIdx.x / 6][threadIdx.x % 6] = (float)S.recs[threadIdx.x / 6].rot[threadIdx.x % 6];
-        __syncthreads();
-        const int total = min(S.pref[nseg], BBUF);
-        // item-local pixel e -> segment k table (one byte per pixel)
-        for (int k = warp; k < nseg; k += BW)
-            for (int e = S.pref[k] + lane; e < min(S.pref[k + 1], BBUF); e += 32) S.bk[e] = (unsigned char)k;
-        __syncthreads();
-
-        // ---------------- pass 1 (loads of the next pixel issued before the current one is computed)
-        float sq = 0.f, vmax = 0.f;
-        int kn = 0;
-        char2 kkn = make_char2(0, 0);
-        float2 xvn = make_float2(0.f, 0.f);
-        if ((int)threadIdx.x < total) {
-            kn = S.bk[threadIdx.x];
-            const size_t g = (size_t)S.seg_row[kn] * n + S.seg_pos[kn] + (threadIdx.x - S.pref[kn]);
-            kkn = a.pc[g];
-            xvn = __ldg(a.xs + g);
-        }
-        for (int e = threadIdx.x; e < total; e += BTHREADS) {
-            const int k = kn;
-            const char2 kk = kkn;
-            const float2 xv = xvn;
-            if (e + BTHREADS < total) {
-                kn = S.bk[e + BTHREADS];
-                const size_t g = (size_t)S.seg_row[kn] * n + S.seg_pos[kn] + (e + BTHREADS - S.pref[kn]);
-                kkn = a.pc[g];
-                xvn = __ldg(a.xs + g);
-            }
-            S.bpc[e] = kk;
-            const float* fr = S.frame[k];
-            const int px = kk.x, py = kk.y;
-            float cx, cy, cz, fx, fy, fz;
-            floor_corner((float)px, (float)py, fr, bnd, cx, cy, cz, fx, fy, fz);
-            const int l0 = (((int)fz - oz) * BH + ((int)fy - oy)) * BH + ((int)fx - ox);
-            const float wx = cx - fx, wy = cy - fy, wz = cz - fz;
-            const float ax = 1.f - wx, ay = 1.f - wy, az = 1.f - wz;
-            const float2 f = pixel_factor(S.recs[k], px, py);
-            const float2* vb = S.vb + l0;
-            // trilinear gather (kernels.py:171-176) from the smem brick
-            const float2 WX = make_float2(wx, wx), AX = make_float2(ax, ax);
-            const float2 e0 = __ffma2_rn(WX, vb[1], __fmul2_rn(AX, vb[0]));
-            const float2 e1 = __ffma2_rn(WX, vb[BH + 1], __fmul2_rn(AX, vb[BH]));
-            const float2 e2 = __ffma2_rn(WX, vb[BH * BH + 1], __fmul2_rn(AX, vb[BH * BH]));
-            const float2 e3 = __ffma2_rn(WX, vb[BH * BH + BH + 1], __fmul2_rn(AX, vb[BH * BH + BH]));
-            const float2 q0 = __ffma2_rn(make_float2(wy, wy), e1, __fmul2_rn(make_float2(ay, ay), e0));
-            const float2 q1 = __ffma2_rn(make_float2(wy, wy), e3, __fmul2_rn(make_float2(ay, ay), e2));
-            const float2 pv = __ffma2_rn(make_float2(wz, wz), q1, __fmul2_rn(make_float2(az, az), q0));
-            const float2 prj = cmul(pv, f);
-            const float2 rr = make_float2(prj.x - xv.x, prj.y - xv.y);
-            sq = fmaf(rr.x, rr.x, fmaf(rr.y, rr.y, sq));
-            const float2 val = cmulconj(f, rr);
-            vmax = fmaxf(vmax, fmaxf(fabsf(val.x), fabsf(val.y)));
-            S.bval[e] = val;
-        }
-        for (int o = 16; o > 0; o >>= 1) {
-            sq += __shfl_xor_sync(0xffffffffu, sq, o);
-            vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
-        }
-        if (lane == 0) {
-            lsum += (double)sq;
-            atomicMax(&S.vmax_bits, __float_as_int(vmax));
-        }
-        __syncthreads();
-
-        // ---------------- pass 2: fixed-point adjoint scatter (kernels.py:221-230)
-        const float vm = __int_as_float(S.vmax_bits);
-        const float sc = vm > 0.f ? exp2f(floorf(log2f(4194303.0f / vm))) : 1.0f;
-        const float inv_sc = 1.0f / sc;
-        for (int e = threadIdx.x; e < total; e += BTHREADS) {
-            const int k = S.bk[e];
-            const char2 kk = S.bpc[e];
-            float cx, cy, cz, fx, fy, fz;
-            floor_corner((float)kk.x, (float)kk.y, S.frame[k], bnd, cx, cy, cz, fx, fy, fz);
-            const int l0 = (((int)fz - oz) * BH + ((int)fy - oy)) * BH + ((int)fx - ox);
-            const float wx = cx - fx, wy = cy - fy, wz = cz - fz;
-            const float ax = 1.f - wx, ay = 1.f - wy, az = 1.f - wz;
-            const float2 val = __fmul2_rn(S.bval[e], make_float2(sc, sc));
-            const float zy00 = az * ay, zy10 = az * wy, zy01 = wz * ay, zy11 = wz * wy;
-            const float w8[8] = {zy00 * ax, zy00 * wx, zy10 * ax, zy10 * wx, zy01 * ax, zy01 * wx, zy11 * ax, zy11 * wx};
-            const int off8[8] = {0, 1, BH, BH + 1, BH * BH, BH * BH + 1, BH * BH + BH, BH * BH + BH + 1};
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const float2 y = __ffma2_rn(make_float2(w8[q], w8[q]), val, make_float2(kMagic, kMagic));
-                atomicAdd(S.accr + l0 + off8[q], __float_as_int(y.x) - kMagicBits);
-                atomicAdd(S.acci + l0 + off8[q], __float_as_int(y.y) - kMagicBits);
-            }
-        }
-        __syncthreads();
-        // ---------------- flush: one vector reduction per touched brick voxel
-        for (int l = threadIdx.x; l < BH3; l += BTHREADS) {
-            const int qr = S.accr[l], qi = S.acci[l];
-            if ((qr | qi) == 0) continue;
-            const int lx = l % BH, ly = (l / BH) % BH, lz = l / (BH * BH);
-            const int kx = ox + lx, ky = oy + ly, kz = oz + lz;
-            if (kx >= M - c || ky >= M - c || kz >= M - c) continue;
-            red_f32x2(reinterpret_cast<float*>(a.acc) + 2 * (size_t)lin_index(kx, ky, kz, M, c),
-                      (float)qr * inv_sc, (float)qi * inv_sc);
-        }
-        __syncthreads();
-    }
-    if (lane == 0) S.red[warp] = lsum;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double s = 0.0;
-        for (int w = 0; w < BW; ++w) s += S.red[w];
-        a.part[blockIdx.x] = s;
-    }
+cudaError_t set_phase_profile(unsigned long long* buf) {
+    return cudaMemcpyToSymbol(g_phase_prof, &buf, sizeof(buf));
 }
 
 static int g_sorted_grid = 0;

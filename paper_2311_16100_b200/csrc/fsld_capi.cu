@@ -300,7 +300,7 @@ int fsld_loss_grad_sorted(int M, int mode, int n_mask, const fsld_image_rec* rec
     b.cnt = reinterpret_cast<int*>(scr + L.cnt);
     b.off = reinterpret_cast<int*>(scr + L.off);
     b.fill = reinterpret_cast<int*>(scr + L.fill);
-    b.pairs = reinterpret_cast<int2*>(scr + L.pairs);
+    b.pairs = reinterpret_cast<int4*>(scr + L.pairs);
     b.items = reinterpret_cast<int4*>(scr + L.items);
     b.ctl = reinterpret_cast<int*>(scr + L.ctl);
     b.part = reinterpret_cast<double*>(scr + L.part);
@@ -386,4 +386,10 @@ extern "C" int fsld_grad_epilogue(int64_t nvox, void* acc, const void* v, double
                                           scale, lam, reinterpret_cast<float2*>(grad), sq, loss, norm2,
                                           reinterpret_cast<double*>(scratch), nparts,
                                           reinterpret_cast<cudaStream_t>(stream)));
+}
+
+// Debug: accumulate per-phase cycles of the brick kernel's item loop into buf[0..5]
+// (5 phases + item count, summed over CTAs); NULL disables.  Not part of the stable ABI.
+extern "C" int fsld_debug_phase_profile(unsigned long long* buf) {
+    return status_of(set_phase_profile(buf));
 }

@@ -114,7 +114,8 @@ constexpr double kInvTwoPi = 0.15915494309189535;
 // CTF value at the unrotated pixel (forward.py:93-111 generalised; see
 // fsld_image_rec).  gamma is evaluated in fp64 (it reaches ~470 rad at the
 // mask edge for the physical CTF) and range-reduced before the fp32 sincos.
-__device__ __forceinline__ float ctf_value(const fsld_image_rec& R, int kx, int ky) {
+template <class Rec>
+__device__ __forceinline__ float ctf_value(const Rec& R, int kx, int ky) {
     double k2 = (double)(kx * kx + ky * ky);
     double c2 = (double)(kx * kx - ky * ky);
     double s2 = (double)(2 * kx * ky);
@@ -130,7 +131,8 @@ __device__ __forceinline__ float ctf_value(const fsld_image_rec& R, int kx, int 
 }
 
 // exp(i*pi*(shift . k)) (forward.py:299-303), argument reduced mod 2 in fp64.
-__device__ __forceinline__ float2 shift_phase(const fsld_image_rec& R, int kx, int ky) {
+template <class Rec>
+__device__ __forceinline__ float2 shift_phase(const Rec& R, int kx, int ky) {
     double t = fma(R.shift[0], (double)kx, R.shift[1] * (double)ky);
     t -= 2.0 * rint(0.5 * t);
     float s, c;
@@ -139,7 +141,8 @@ __device__ __forceinline__ float2 shift_phase(const fsld_image_rec& R, int kx, i
 }
 
 // Full per-pixel factor f = C * phase (complex).
-__device__ __forceinline__ float2 pixel_factor(const fsld_image_rec& R, int kx, int ky) {
+template <class Rec>
+__device__ __forceinline__ float2 pixel_factor(const Rec& R, int kx, int ky) {
     float ctf = (R.flags & FSLD_REC_CTF) ? ctf_value(R, kx, ky) : 1.0f;
     if (R.flags & FSLD_REC_SHIFT) {
         float2 p = shift_phase(R, kx, ky);
@@ -148,7 +151,8 @@ __device__ __forceinline__ float2 pixel_factor(const fsld_image_rec& R, int kx, 
     return make_float2(ctf, 0.0f);
 }
 
-__device__ __forceinline__ float ctf_sq(const fsld_image_rec& R, int kx, int ky) {
+template <class Rec>
+__device__ __forceinline__ float ctf_sq(const Rec& R, int kx, int ky) {
     if (!(R.flags & FSLD_REC_CTF)) return 1.0f;
     float c = ctf_value(R, kx, ky);
     return c * c;

@@ -73,7 +73,7 @@ struct SortedArgs {
     int* cnt;
     int* off;
     int* fill;
-    int2* pairs;             // (batch entry b, global segment index)
+    int4* pairs;             // (dataset row, start, count, 0) per binned segment, item-contiguous
     int4* items;             // (brick, first pair, n pairs, 0)
     int* ctl;
     double* part;
@@ -86,6 +86,7 @@ cudaError_t launch_sorted_fill(int M, int n_mask, const short2* pix, const fsld_
                                const float2* x_in, float2* x_out, char2* pc_out, const int32_t* seg_off,
                                int2* segs, cudaStream_t s);
 cudaError_t launch_sorted_loss_grad(const SortedArgs& a, double* sq_out, cudaStream_t s);
+cudaError_t set_phase_profile(unsigned long long* buf);
 
 cudaError_t launch_slice(int op, int mode, bool det, const SliceArgs& a, int nblocks, cudaStream_t s);
 cudaError_t launch_reduce(const double* part, int n, double* out, cudaStream_t s);
