@@ -171,6 +171,8 @@ __global__ void __launch_bounds__(256) sorted_fill_kernel(int M, int n_mask, con
     }
 }
 
+#include "fsld_brick_wave.cuh"
+
 static int smem_optin(const void* fn, size_t bytes) {
     if (bytes <= 48 * 1024) return 0;
     return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) == cudaSuccess ? 0 : -1;
@@ -193,6 +195,7 @@ cudaError_t launch_sorted_fill(int M, int n_mask, const short2* pix, const fsld_
     const size_t smem = sizeof(int) * (size_t)nb * nb * nb;
     if (smem_optin((const void*)sorted_fill_kernel, smem)) return cudaErrorInvalidValue;
     sorted_fill_kernel<<<N, 256, smem, s>>>(M, n_mask, pix, recs, x_in, x_out, pc_out, seg_off, segs);
+    wave_order_kernel<<<N, 256, 0, s>>>(M, n_mask, recs, x_in ? x_out : nullptr, pc_out, seg_off, segs);
     return cudaGetLastError();
 }
 
