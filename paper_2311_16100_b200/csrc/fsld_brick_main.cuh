@@ -22,6 +22,17 @@ __device__ unsigned long long* g_phase_prof = nullptr;
 constexpr int BOWN_MAX = 112;
 constexpr int BBUF = BC * BOWN_MAX;
 
+// The record fields pixel_factor reads (bytes 48..119 of fsld_image_rec, same layout).
+struct FactorRec {
+    double shift[2];
+    double gamma[4];
+    double env;
+    float wsin, wcos;
+    uint32_t flags;
+    float xmax;
+};
+static_assert(sizeof(FactorRec) == 72, "FactorRec mirrors fsld_image_rec bytes 48..119");
+
 struct SortedSmem {
     float2 vb[BH3];                 // v brick + halo
     int accr[BH3];                  // fixed-point adjoint accumulator (re)
@@ -29,32 +40,30 @@ struct SortedSmem {
     float2 bval[BBUF];              // pass 1 -> 2: conj(f) r per pixel of the item
     unsigned char bk[BBUF];         // segment (image) of each pixel of the item
     char2 bpc[BBUF];                // its (kx, ky), kept for pass 2
-    fsld_image_rec recs[BC];        // records of the item's images
+    FactorRec fac[BC];              // CTF / shift parameters of the item's images
     float frame[BC][6];             // fp32 rows 0,1 of R
     int seg_row[BC];                // dataset row of segment k
     int seg_pos[BC];                // start of segment k in its row (sorted order)
     int pref[BC + 1];               // exclusive prefix of segment lengths
+    int4 item_desc;
     int item;
     int vmax_bits;
     double red[BW];
 };
 
-// Item-local flat index e -> segment k (largest k with pref[k] <= e), binary search over <= 32.
-__device__ __forceinline__ int seg_of(const int* pref, int nseg, int e) {
-    int k = 0;
-#pragma unroll
-    for (int s = 16; s >= 1; s >>= 1)
-        if (k + s < nseg && pref[k + s] <= e) k += s;
-    return k;
-}
-
-// Two passes per work item over the item's pixels, flattened across its <= 32
-// segments (all lanes busy):
-//   1. per pixel: gather 8 corners from the smem brick, f = C * phase,
-//      r = f P v - x, |r|^2 -> loss, val = conj(f) r -> smem buffer;
+// Per work item (brick, <= BC image segments):
+//   A  claim the item (thread 0);
+//   B  warp 0: segment table + prefix of lengths; warps 1-7: the brick's 9^3
+//      voxels of v (+halo, zero off the grid) -> smem;
+//   C  frames, CTF/shift records (straight from the global records) and the
+//      pixel -> segment table;
+//   1. per pixel (flattened over the item's segments, all lanes busy):
+//      gather 8 corners from the smem brick, f = C * phase, r = f P v - x,
+//      |r|^2 -> loss, val = conj(f) r -> smem buffer;
 //   2. with the item's max |val| known, quantise val * w to int32 with a
 //      power-of-two scale (|val w s| <= 2^22; <= BC*12 contributions per voxel
-//      -> |sum| < 2^31) and add with native ATOMS.ADD (order-free, no CAS).
+//      -> |sum| < 2^31) and add with native ATOMS.ADD (order-free, no CAS);
+//   3. flush: one red.global.add.v2.f32 per touched brick voxel.
 // The scale follows the residual, not |Pv| or |x|: quantum ~2^-22 of the
 // item's largest contribution.
 __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArgs a) {
@@ -64,23 +73,41 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArg
     const int M = a.M, c = a.c, nb = a.nb, n = a.n_mask;
     const float bnd = a.bnd;
     double lsum = 0.0;
-
+    // Work claiming runs ahead on one thread of the last warp (off warp 0's critical path):
+    // its atomicAdd for item i+2 and descriptor load for item i+1 are issued during item i
+    // and only consumed one iteration later.
+    constexpr int kClaimer = BTHREADS - 32;
+    const int n_items = a.ctl[0];
+    int next_it = 0, claimed = 0;
+    int4 next_item = make_int4(0, 0, 0, 0);
+    if (threadIdx.x == kClaimer) {
+        next_it = atomicAdd(a.ctl + 1, 1);
+        if (next_it < n_items) next_item = a.items[next_it];
+        claimed = atomicAdd(a.ctl + 1, 1);
+    }
     PHASE_INIT();
-    for (;;) {
-        if (threadIdx.x == 0) {
-            S.item = atomicAdd(a.ctl + 1, 1);
-            S.vmax_bits = 0;
-        }
-        __syncthreads();
-        PHASE_MARK(0);
-        const int it = S.item;
-        if (it >= a.ctl[0]) break;
-        const int4 item = a.items[it];
-        const int bid = item.x, pstart = item.y, nseg = item.z;
-        const int bx = bid % nb, by = (bid / nb) % nb, bz = bid / (nb * nb);
-        const int ox = -c + BT * bx, oy = -c + BT * by, oz = -c + BT * bz;
 
-        if (warp == 0) {  // segment table + prefix of lengths (one warp)
+    for (;;) {
+        // ---------------- A
+        if (threadIdx.x == kClaimer) {
+            S.item_desc = next_item;
+            S.item = next_it;
+        }
+        if (threadIdx.x == 0) S.vmax_bits = 0;
+        __syncthreads();
+        const int it = S.item;
+        if (it >= n_items) break;
+        const int4 item = S.item_desc;
+        if (threadIdx.x == kClaimer) {  // consumed next iteration / the one after
+            next_it = claimed;
+            if (next_it < n_items) next_item = a.items[next_it];
+            if (next_it < n_items) claimed = atomicAdd(a.ctl + 1, 1);
+        }
+        const int bid = item.x, pstart = item.y, nseg = item.z;
+        const int ox = -c + BT * (bid % nb), oy = -c + BT * ((bid / nb) % nb), oz = -c + BT * (bid / (nb * nb));
+        PHASE_MARK(0);
+        // ---------------- B
+        if (warp == 0) {
             int len = 0;
             if (lane < nseg) {
                 const int4 pr = a.pairs[pstart + lane];  // (row, start, count)
@@ -96,13 +123,12 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArg
             }
             if (lane < nseg) S.pref[lane] = incl - len;
             if (lane == 31) S.pref[nseg] = incl;
-        }
-        {   // v brick + halo: issue all loads before the stores
-            constexpr int U = (BH3 + BTHREADS - 1) / BTHREADS;
+        } else {
+            constexpr int U = (BH3 + BTHREADS - 32 - 1) / (BTHREADS - 32);
             float2 vv[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                const int l = threadIdx.x + u * BTHREADS;
+                const int l = threadIdx.x - 32 + u * (BTHREADS - 32);
                 const int lx = l % BH, ly = (l / BH) % BH, lz = l / (BH * BH);
                 const int kx = ox + lx, ky = oy + ly, kz = oz + lz;
                 vv[u] = make_float2(0.f, 0.f);
@@ -110,7 +136,7 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArg
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                const int l = threadIdx.x + u * BTHREADS;
+                const int l = threadIdx.x - 32 + u * (BTHREADS - 32);
                 if (l < BH3) {
                     S.vb[l] = vv[u];
                     S.accr[l] = 0;
@@ -120,21 +146,21 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArg
         }
         __syncthreads();
         PHASE_MARK(1);
-        for (int w = threadIdx.x; w < nseg * 32; w += BTHREADS) {
-            const int k = w >> 5, q = w & 31;
-            reinterpret_cast<uint32_t*>(S.recs + k)[q] = __ldg(reinterpret_cast<const uint32_t*>(a.recs + S.seg_row[k]) + q);
+        // ---------------- C
+        for (int w = threadIdx.x; w < nseg * 24; w += BTHREADS) {
+            const int k = w / 24, q = w - 24 * (w / 24);
+            const uint32_t* rec = reinterpret_cast<const uint32_t*>(a.recs + S.seg_row[k]);
+            if (q < 18) {
+                reinterpret_cast<uint32_t*>(S.fac + k)[q] = __ldg(rec + 12 + q);
+            } else {
+                S.frame[k][q - 18] = (float)__ldg(reinterpret_cast<const double*>(rec) + (q - 18));
+            }
         }
-        __syncthreads();
-        PHASE_MARK(2);
-        if (threadIdx.x < nseg * 6) S.frame[threadIdx.x / 6][threadIdx.x % 6] = (float)S.recs[threadIdx.x / 6].rot[threadIdx.x % 6];
-        __syncthreads();
-        PHASE_MARK(3);
         const int total = min(S.pref[nseg], BBUF);
-        // item-local pixel e -> segment k table (one byte per pixel)
         for (int k = warp; k < nseg; k += BW)
             for (int e = S.pref[k] + lane; e < min(S.pref[k + 1], BBUF); e += 32) S.bk[e] = (unsigned char)k;
         __syncthreads();
-        PHASE_MARK(4);
+        PHASE_MARK(2);
 
         // ---------------- pass 1 (loads of the next pixel issued before the current one is computed)
         float sq = 0.f, vmax = 0.f;
@@ -165,7 +191,7 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArg
             const int l0 = (((int)fz - oz) * BH + ((int)fy - oy)) * BH + ((int)fx - ox);
             const float wx = cx - fx, wy = cy - fy, wz = cz - fz;
             const float ax = 1.f - wx, ay = 1.f - wy, az = 1.f - wz;
-            const float2 f = pixel_factor(S.recs[k], px, py);
+            const float2 f = pixel_factor(S.fac[k], px, py);
             const float2* vb = S.vb + l0;
             // trilinear gather (kernels.py:171-176) from the smem brick
             const float2 WX = make_float2(wx, wx), AX = make_float2(ax, ax);
@@ -192,7 +218,7 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArg
             atomicMax(&S.vmax_bits, __float_as_int(vmax));
         }
         __syncthreads();
-        PHASE_MARK(5);
+        PHASE_MARK(3);
 
         // ---------------- pass 2: fixed-point adjoint scatter (kernels.py:221-230)
         const float vm = __int_as_float(S.vmax_bits);
@@ -218,7 +244,7 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArg
             }
         }
         __syncthreads();
-        PHASE_MARK(6);
+        PHASE_MARK(4);
         // ---------------- flush: one vector reduction per touched brick voxel
         for (int l = threadIdx.x; l < BH3; l += BTHREADS) {
             const int qr = S.accr[l], qi = S.acci[l];
@@ -241,4 +267,3 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArg
         a.part[blockIdx.x] = s;
     }
 }
-
