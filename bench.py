@@ -232,6 +232,7 @@ def run_b200(args):
 
     def step(idx, ev_k0=None, ev_k1=None):
         # acc is zero on entry (zeroed by the previous step's fused epilogue)
+        stream = _stream()  # the current torch stream (the capture stream under CUDA-graph capture)
         if ev_k0 is not None:
             ev_k0.record()
         C.check(lib.fsld_loss_grad_sorted(M, eng.mode_id, n, ctypes_ptr(eng.recs), ctypes_ptr(idx), B,
@@ -255,25 +256,46 @@ def run_b200(args):
     for i in range(args.warmup):
         step(batches[i])
     torch.cuda.synchronize()
+    # kernel-only timing (events around the fused loss+grad call, eager)
+    E = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    kev = [(E(), E()) for _ in range(args.steps)]
+    for i in range(args.steps):
+        flush.fill_(float(i))
+        step(batches[args.warmup + i], *kev[i])
+    torch.cuda.synchronize()
+    kern_ms = [a_.elapsed_time(b_) for a_, b_ in kev]
+    # the timed step runs as one CUDA graph replay (N=1; under NCCL the collective stays eager)
+    idx_static = torch.empty(B, dtype=torch.int32, device=dev)
+    graph = None
+    if world == 1 and not os.environ.get("FSLD_NO_GRAPH"):
+        idx_static.copy_(batches[0])
+        step(idx_static)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step(idx_static)
+        torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    E = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
-    ev = [(E(), E(), E(), E()) for _ in range(args.steps)]
+    ev = [(E(), E()) for _ in range(args.steps)]
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         for i in range(args.steps):
             flush.fill_(float(i))  # L2 flush between timed steps (outside the step events)
-            s0, k0, k1, s1 = ev[i]
+            s0, s1 = ev[i]
             s0.record()
-            step(batches[args.warmup + i], k0, k1)
+            if graph is not None:
+                idx_static.copy_(batches[args.warmup + i])
+                graph.replay()
+            else:
+                step(batches[args.warmup + i])
             s1.record()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-    step_ms = [e[0].elapsed_time(e[3]) for e in ev]
-    kern_ms = [e[1].elapsed_time(e[2]) for e in ev]
+    step_ms = [a_.elapsed_time(b_) for a_, b_ in ev]
     t_step = float(np.mean(step_ms))
     t_kern = float(np.mean(kern_ms))
     if world > 1:
@@ -305,7 +327,8 @@ def run_b200(args):
             "dtype": "c64/f32 (fp64 coords, CTF phase)", "data": "synthetic (seeded generators of BASELINE cfg; SURVEY.md 8d)",
             "config": {"workload": cfg.name, "M": M, "n_mask": n, "batch_per_gpu": B,
                        "n_images_per_gpu": eng.n_images, "mode": cfg.mode, "ctf": "physical astigmatic",
-                       "parallelism": f"dp{world}", "l2": "flushed between timed steps (512 MB write)"},
+                       "parallelism": f"dp{world}", "l2": "flushed between timed steps (512 MB write)",
+                       "step": "CUDA graph replay" if world == 1 and not os.environ.get("FSLD_NO_GRAPH") else "eager"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic, "peak_source": src,
                          "kernel": ("fsld_loss_grad_sorted: bin count/scan/fill + sorted_loss_grad_kernel + loss reduce" if not flags else "fsld slice_kernel<TRI,LOSS_GRAD> (tile path)"),

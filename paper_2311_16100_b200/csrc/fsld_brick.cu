@@ -219,10 +219,11 @@ __global__ void __launch_bounds__(128) bin_sorted_kernel(SortedArgs a) {
 }
 
 // Exclusive scan of per-brick pair counts and expansion into work items
-// (brick, first pair, n pairs <= BC).  One CTA of 1024 threads.
+// (brick, first pair, n pairs <= BC).  One CTA of 1024 threads, warp-shuffle
+// scans.  Leaves cnt[] zeroed for the next call (fsld_prepare zeroes it once).
 __global__ void __launch_bounds__(1024) brick_scan_kernel(SortedArgs a) {
-    __shared__ int s_pairs[1024];
-    __shared__ int s_items[1024];
+    __shared__ int wp[32], wi[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int per = (a.nbr + 1023) / 1024;
     const int lo = threadIdx.x * per;
     const int hi = min(lo + per, a.nbr);
@@ -232,21 +233,39 @@ __global__ void __launch_bounds__(1024) brick_scan_kernel(SortedArgs a) {
         np += c;
         ni += (c + BC - 1) / BC;
     }
-    s_pairs[threadIdx.x] = np;
-    s_items[threadIdx.x] = ni;
-    __syncthreads();
-    for (int o = 1; o < 1024; o <<= 1) {  // Hillis-Steele inclusive scan
-        const int vp = threadIdx.x >= o ? s_pairs[threadIdx.x - o] : 0;
-        const int vi = threadIdx.x >= o ? s_items[threadIdx.x - o] : 0;
-        __syncthreads();
-        s_pairs[threadIdx.x] += vp;
-        s_items[threadIdx.x] += vi;
-        __syncthreads();
+    int ip = np, ii = ni;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int tp = __shfl_up_sync(0xffffffffu, ip, o), ti = __shfl_up_sync(0xffffffffu, ii, o);
+        if (lane >= o) {
+            ip += tp;
+            ii += ti;
+        }
     }
-    int pbase = s_pairs[threadIdx.x] - np;
-    int ibase = s_items[threadIdx.x] - ni;
+    if (lane == 31) {
+        wp[warp] = ip;
+        wi[warp] = ii;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        int vp = wp[lane], vi = wi[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int tp = __shfl_up_sync(0xffffffffu, vp, o), ti = __shfl_up_sync(0xffffffffu, vi, o);
+            if (lane >= o) {
+                vp += tp;
+                vi += ti;
+            }
+        }
+        wp[lane] = vp;
+        wi[lane] = vi;
+    }
+    __syncthreads();
+    int pbase = (warp > 0 ? wp[warp - 1] : 0) + ip - np;
+    int ibase = (warp > 0 ? wi[warp - 1] : 0) + ii - ni;
     for (int i = lo; i < hi; ++i) {
         const int c = a.cnt[i];
+        a.cnt[i] = 0;
         a.off[i] = pbase;
         a.fill[i] = 0;
         for (int k = 0; k < c; k += BC) {
@@ -256,10 +275,10 @@ __global__ void __launch_bounds__(1024) brick_scan_kernel(SortedArgs a) {
         pbase += c;
     }
     if (threadIdx.x == 1023) {
-        a.off[a.nbr] = s_pairs[1023];
-        a.ctl[0] = min(s_items[1023], a.cap_items);
+        a.off[a.nbr] = wp[31];
+        a.ctl[0] = min(wi[31], a.cap_items);
         a.ctl[1] = 0;
-        a.ctl[2] = s_pairs[1023] > a.cap_pairs;  // overflow flag (cannot happen for the 4 nb^2 bound)
+        a.ctl[2] = wp[31] > a.cap_pairs;  // overflow flag (cannot happen for the 4 nb^2 bound)
     }
 }
 
@@ -285,8 +304,8 @@ cudaError_t launch_sorted_loss_grad(const SortedArgs& a, double* sq_out, cudaStr
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sorted_loss_grad_kernel, BTHREADS, smem);
         g_sorted_grid = sms * (occ > 0 ? occ : 1);
     }
-    cudaError_t e = cudaMemsetAsync(a.cnt, 0, sizeof(int) * (size_t)a.nbr, s);
-    if (e != cudaSuccess) return e;
+    // cnt[] is zero on entry: zeroed by fsld_prepare, and re-zeroed by every scan
+    cudaError_t e;
     bin_sorted_kernel<false><<<a.B, 128, 0, s>>>(a);
     brick_scan_kernel<<<1, 1024, 0, s>>>(a);
     bin_sorted_kernel<true><<<a.B, 128, 0, s>>>(a);

@@ -85,13 +85,16 @@ int fsld_prepare(int M, int n_mask, const int16_t* pix, void* scratch, size_t sc
     if (M < 2 || M > 1024 || n_mask < 1 || n_mask > M * M || !pix || !scratch) return FSLD_EINVAL;
     const ScratchLayout L = scratch_layout(M, n_mask, 1);
     if (scratch_bytes < L.total) return FSLD_EINVAL;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    // zero everything once (the brick binning relies on cnt[] == 0 on entry)
+    cudaError_t e = cudaMemsetAsync(scratch, 0, scratch_bytes, s);
+    if (e != cudaSuccess) return FSLD_ECUDA;
     GeomHeader h{};
     h.magic = kGeomMagic;
     h.M = M;
     h.n_mask = n_mask;
     h.pix = pix;
-    return status_of(cudaMemcpyAsync(reinterpret_cast<char*>(scratch) + L.hdr, &h, sizeof(h), cudaMemcpyHostToDevice,
-                                     reinterpret_cast<cudaStream_t>(stream)));
+    return status_of(cudaMemcpyAsync(reinterpret_cast<char*>(scratch) + L.hdr, &h, sizeof(h), cudaMemcpyHostToDevice, s));
 }
 
 static int run_reducing(int op, int M, int mode, int n_mask, const int16_t* pix, const int8_t* pc,
