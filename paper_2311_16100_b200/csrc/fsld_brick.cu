@@ -42,7 +42,7 @@ ScratchLayout scratch_layout(int M, int n_mask, int B) {
     L.cnt = o; o = al(o + sizeof(int) * (size_t)L.nbr);
     L.off = o; o = al(o + sizeof(int) * (size_t)(L.nbr + 1));
     L.fill = o; o = al(o + sizeof(int) * (size_t)L.nbr);
-    L.pairs = o; o = al(o + sizeof(int4) * (size_t)L.cap_pairs);
+    L.pairs = o; o = al(o + sizeof(SegRec) * (size_t)L.cap_pairs);
     L.items = o; o = al(o + sizeof(int4) * (size_t)L.cap_items);
     L.ctl = o; o = al(o + 64);
     L.part = o; o = al(o + sizeof(double) * (size_t)L.cap_part);
@@ -201,82 +201,166 @@ cudaError_t launch_sorted_fill(int M, int n_mask, const short2* pix, const fsld_
 
 // ---------------------------------------------------------------- per-step binning
 
+// frac(hi + lo) * 2^64 as a wrapping 64-bit fixed-point "turns" value
+// (double-double input, |hi| < 2^40).  Every step but the last rounding is exact.
+__device__ __forceinline__ unsigned long long frac_fixed64(double hi, double lo) {
+    const double f = hi - rint(hi);               // exact, |f| <= 1/2
+    const double a = f * 4294967296.0;            // exact
+    const double ah = floor(a);                   // exact
+    const double r = (a - ah) + lo * 4294967296.0;  // a - ah exact, in [0, 1)
+    const long long l = __double2ll_rn(r * 4294967296.0);
+    return ((unsigned long long)(long long)ah << 32) + (unsigned long long)l;
+}
+
+// x / (2 pi) in turns, fixed point: double-double product with 1/(2 pi).
+__device__ __forceinline__ unsigned long long turns_of_radians(double x) {
+    constexpr double kInv2PiHi = 0.15915494309189535;     // fl(1 / 2pi)
+    constexpr double kInv2PiLo = -9.839338337591243e-18;  // 1/2pi - fl(1/2pi)
+    const double hi = x * kInv2PiHi;
+    const double lo = fma(x, kInv2PiHi, -hi) + x * kInv2PiLo;
+    return frac_fixed64(hi, lo);
+}
+
+// The per-image part of a SegRec (everything except gofs / count / start),
+// from the 128-byte record (fsld_common.cuh ctf_value / shift_phase restated):
+//   gamma = g0 k2 + g1 c2 + g2 s2 + g3 k2^2 with c2 = kx^2 - ky^2, s2 = 2 kx ky;
+//   the kernel multiplies non-negative monomials (k2, c2 + 2^15, s2 + 2^16, k2^2),
+//   so the offsets go into the constant term.  Shift: t = (s0 kx + s1 ky) / 2 turns,
+//   with kx + 128, ky + 128.
+__device__ void seg_template(const fsld_image_rec& R, SegRec& T) {
+    for (int q = 0; q < 6; ++q) T.frame[q] = (float)R.rot[q];
+    unsigned long long g[4] = {0, 0, 0, 0}, gconst = 0, s[2] = {0, 0}, sconst = 0;
+    T.wsin = 0.f;
+    T.wcos = -1.f;  // no CTF: -(0 sin 0 + (-1) cos 0) = 1
+    T.envl = 0.f;
+    if (R.flags & FSLD_REC_CTF) {
+        for (int q = 0; q < 4; ++q) g[q] = turns_of_radians(R.gamma[q]);
+        gconst = turns_of_radians(-32768.0 * R.gamma[1]) + turns_of_radians(-65536.0 * R.gamma[2]);
+        T.wsin = R.wsin;
+        T.wcos = R.wcos;
+        T.envl = (float)(R.env * 1.4426950408889634);
+    }
+    if (R.flags & FSLD_REC_SHIFT) {
+        for (int q = 0; q < 2; ++q) {
+            s[q] = frac_fixed64(0.5 * R.shift[q], 0.0);
+            sconst += frac_fixed64(-64.0 * R.shift[q], 0.0);
+        }
+    }
+    for (int q = 0; q < 4; ++q) {
+        T.glo[q] = (uint32_t)g[q];
+        T.ghi[q] = (uint32_t)(g[q] >> 32);
+    }
+    for (int q = 0; q < 2; ++q) {
+        T.slo[q] = (uint32_t)s[q];
+        T.shi[q] = (uint32_t)(s[q] >> 32);
+    }
+    // constants: round to the nearest 2^-32 turn
+    T.gc = (uint32_t)((gconst + 0x80000000ull) >> 32);
+    T.sc = (uint32_t)((sconst + 0x80000000ull) >> 32);
+    T.pad[0] = T.pad[1] = T.pad[2] = T.pad[3] = 0;
+}
+
 template <bool FILL>
 __global__ void __launch_bounds__(128) bin_sorted_kernel(SortedArgs a) {
     const int b = blockIdx.x;
     const int row = a.idx ? a.idx[b] : b;
     const int s0 = a.seg_off[row], s1 = a.seg_off[row + 1];
-    for (int sidx = s0 + threadIdx.x; sidx < s1; sidx += blockDim.x) {
-        const int brick = a.segs[sidx].x;
-        if (FILL) {
-            const int slot = atomicAdd(a.fill + brick, 1);
+    if (FILL) {
+        __shared__ SegRec T;
+        if (threadIdx.x == 0) seg_template(a.recs[row], T);
+        __syncthreads();
+        for (int sidx = s0 + threadIdx.x; sidx < s1; sidx += blockDim.x) {
             const int2 seg = a.segs[sidx];
-            a.pairs[a.off[brick] + slot] = make_int4(a.idx ? a.idx[b] : b, seg.y & 0xFFFF, seg.y >> 16, 0);
-        } else {
-            atomicAdd(a.cnt + brick, 1);
+            const int slot = atomicAdd(a.fill + seg.x, 1);
+            SegRec r = T;
+            r.start = (uint32_t)(seg.y & 0xFFFF);
+            r.count = seg.y >> 16;
+            r.row = row;
+            r.gofs = (long long)row * a.n_mask + (seg.y & 0xFFFF);
+            const int4* src = reinterpret_cast<const int4*>(&r);
+            int4* dst = reinterpret_cast<int4*>(a.pairs + a.off[seg.x] + slot);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) dst[q] = src[q];
         }
+    } else {
+        for (int sidx = s0 + threadIdx.x; sidx < s1; sidx += blockDim.x) atomicAdd(a.cnt + a.segs[sidx].x, 1);
     }
 }
 
 // Exclusive scan of per-brick pair counts and expansion into work items
-// (brick, first pair, n pairs <= BC).  One CTA of 1024 threads, warp-shuffle
-// scans.  Leaves cnt[] zeroed for the next call (fsld_prepare zeroes it once).
+// (brick, first pair, n pairs <= BC).  Full items (BC pairs) are listed first
+// and the partial remainders after them, so the persistent kernel's last
+// claims are the small items (shorter tail).  One CTA of 1024 threads,
+// warp-shuffle scans.  Leaves cnt[] zeroed for the next call (fsld_prepare
+// zeroes it once).
 __global__ void __launch_bounds__(1024) brick_scan_kernel(SortedArgs a) {
-    __shared__ int wp[32], wi[32];
+    __shared__ int wp[32], wf[32], wr[32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int per = (a.nbr + 1023) / 1024;
     const int lo = threadIdx.x * per;
     const int hi = min(lo + per, a.nbr);
-    int np = 0, ni = 0;
+    int np = 0, nf = 0, nr = 0;
     for (int i = lo; i < hi; ++i) {
         const int c = a.cnt[i];
         np += c;
-        ni += (c + BC - 1) / BC;
+        nf += c / BC;
+        nr += (c % BC) != 0;
     }
-    int ip = np, ii = ni;
+    int ip = np, jf = nf, jr = nr;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-        const int tp = __shfl_up_sync(0xffffffffu, ip, o), ti = __shfl_up_sync(0xffffffffu, ii, o);
+        const int tp = __shfl_up_sync(0xffffffffu, ip, o), tf = __shfl_up_sync(0xffffffffu, jf, o),
+                  tr = __shfl_up_sync(0xffffffffu, jr, o);
         if (lane >= o) {
             ip += tp;
-            ii += ti;
+            jf += tf;
+            jr += tr;
         }
     }
     if (lane == 31) {
         wp[warp] = ip;
-        wi[warp] = ii;
+        wf[warp] = jf;
+        wr[warp] = jr;
     }
     __syncthreads();
     if (warp == 0) {
-        int vp = wp[lane], vi = wi[lane];
+        int vp = wp[lane], vf = wf[lane], vr = wr[lane];
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const int tp = __shfl_up_sync(0xffffffffu, vp, o), ti = __shfl_up_sync(0xffffffffu, vi, o);
+            const int tp = __shfl_up_sync(0xffffffffu, vp, o), tf = __shfl_up_sync(0xffffffffu, vf, o),
+                      tr = __shfl_up_sync(0xffffffffu, vr, o);
             if (lane >= o) {
                 vp += tp;
-                vi += ti;
+                vf += tf;
+                vr += tr;
             }
         }
         wp[lane] = vp;
-        wi[lane] = vi;
+        wf[lane] = vf;
+        wr[lane] = vr;
     }
     __syncthreads();
+    const int n_full = wf[31];
     int pbase = (warp > 0 ? wp[warp - 1] : 0) + ip - np;
-    int ibase = (warp > 0 ? wi[warp - 1] : 0) + ii - ni;
+    int fbase = (warp > 0 ? wf[warp - 1] : 0) + jf - nf;
+    int rbase = n_full + (warp > 0 ? wr[warp - 1] : 0) + jr - nr;
     for (int i = lo; i < hi; ++i) {
         const int c = a.cnt[i];
         a.cnt[i] = 0;
         a.off[i] = pbase;
         a.fill[i] = 0;
-        for (int k = 0; k < c; k += BC) {
-            if (ibase < a.cap_items) a.items[ibase] = make_int4(i, pbase + k, min(BC, c - k), 0);
-            ++ibase;
+        int k = 0;
+        for (; k + BC <= c; k += BC, ++fbase)
+            if (fbase < a.cap_items) a.items[fbase] = make_int4(i, pbase + k, BC, 0);
+        if (k < c) {
+            if (rbase < a.cap_items) a.items[rbase] = make_int4(i, pbase + k, c - k, 0);
+            ++rbase;
         }
         pbase += c;
     }
     if (threadIdx.x == 1023) {
         a.off[a.nbr] = wp[31];
-        a.ctl[0] = min(wi[31], a.cap_items);
+        a.ctl[0] = min(n_full + wr[31], a.cap_items);
         a.ctl[1] = 0;
         a.ctl[2] = wp[31] > a.cap_pairs;  // overflow flag (cannot happen for the 4 nb^2 bound)
     }

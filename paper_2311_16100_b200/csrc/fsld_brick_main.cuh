@@ -17,65 +17,130 @@ __device__ unsigned long long* g_phase_prof = nullptr;
 #define PHASE_FLUSH() \
     if (ph_on) for (int q = 0; q < 9; ++q) atomicAdd(g_phase_prof + q, ph_acc[q])
 
-// Upper bound on the pixels one image owns in one brick: lattice points of a
-// plane section of a BT^3 cube (area <= BT^2 sqrt 2, perimeter <= 2 BT (1 + sqrt 2)).
-constexpr int BOWN_MAX = 112;
-constexpr int BBUF = BC * BOWN_MAX;
-
-// The record fields pixel_factor reads (bytes 48..119 of fsld_image_rec, same layout).
-struct FactorRec {
-    double shift[2];
-    double gamma[4];
-    double env;
-    float wsin, wcos;
-    uint32_t flags;
-    float xmax;
-};
-static_assert(sizeof(FactorRec) == 72, "FactorRec mirrors fsld_image_rec bytes 48..119");
+constexpr int RB = 1024;                               // pixels per round (pass 1 -> pass 2 buffer)
+constexpr int BU = (BH3 + BTHREADS - 1) / BTHREADS;    // brick voxels per thread (3)
+constexpr int SEG_T = BTHREADS / BC;                   // threads per segment in the bk build (4)
+static_assert(BTHREADS % BC == 0 && BC <= 64, "segment table is built by two warps");
 
 struct SortedSmem {
     float2 vb[BH3];                 // v brick + halo
-    int accr[BH3];                  // fixed-point adjoint accumulator (re)
+    int accr[BH3];                  // fixed-point adjoint accumulator of the current round (re)
     int acci[BH3];                  // (im)
-    float2 bval[BBUF];              // pass 1 -> 2: conj(f) r per pixel of the item
-    unsigned char bk[BBUF];         // segment (image) of each pixel of the item
-    char2 bpc[BBUF];                // its (kx, ky), kept for pass 2
-    FactorRec fac[BC];              // CTF / shift parameters of the item's images
-    float frame[BC][6];             // fp32 rows 0,1 of R
-    int seg_row[BC];                // dataset row of segment k
-    int seg_pos[BC];                // start of segment k in its row (sorted order)
+    float2 facc[BH3];               // float accumulator across rounds
+    float2 bval[RB];                // pass 1 -> 2: conj(f) r
+    float4 bgeo[RB];                // pass 1 -> 2: (wx, wy, wz, local corner index)
+    SegRec seg[BC];                 // the item's segment records (gofs rebased to the flat index)
     int pref[BC + 1];               // exclusive prefix of segment lengths
+    unsigned char bk[RB];           // round pixel -> segment
     int4 item_desc;
     int item;
     int vmax_bits;
+    int wtot[2];                    // per-warp segment-length totals
     double red[BW];
 };
 
+// 64-bit shared load (ptxas pairs adjacent ones into LDS.128, which measured
+// fewer smem wavefronts per warp than separate broadcast LDS.64: ~3.4 vs ~2.7 each).
+__device__ __forceinline__ uint2 lds64(const void* p) {
+    uint2 r;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];"
+                 : "=r"(r.x), "=r"(r.y)
+                 : "r"((uint32_t)__cvta_generic_to_shared(p)));
+    return r;
+}
+
+// The per-pixel fields of a SegRec, in registers.
+struct SegRegs {
+    long long gofs;
+    float fr[6];
+    float wsin, wcos, envl;
+    uint32_t gc, sc, glo[4], ghi[4], slo[2], shi[2];
+};
+
+__device__ __forceinline__ void load_seg(const SegRec& R, SegRegs& Q) {
+    uint2 t = lds64(&R.gofs);
+    Q.gofs = (long long)(((unsigned long long)t.y << 32) | t.x);
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        t = lds64(R.frame + 2 * q);
+        Q.fr[2 * q] = __uint_as_float(t.x);
+        Q.fr[2 * q + 1] = __uint_as_float(t.y);
+    }
+    t = lds64(&R.wsin);
+    Q.wsin = __uint_as_float(t.x);
+    Q.wcos = __uint_as_float(t.y);
+    t = lds64(&R.envl);
+    Q.envl = __uint_as_float(t.x);
+    Q.gc = t.y;
+    Q.sc = lds64(&R.sc).x;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        t = lds64(R.glo + 2 * q);
+        Q.glo[2 * q] = t.x;
+        Q.glo[2 * q + 1] = t.y;
+        t = lds64(R.ghi + 2 * q);
+        Q.ghi[2 * q] = t.x;
+        Q.ghi[2 * q + 1] = t.y;
+    }
+    t = lds64(R.slo);
+    Q.slo[0] = t.x;
+    Q.slo[1] = t.y;
+    t = lds64(R.shi);
+    Q.shi[0] = t.x;
+    Q.shi[1] = t.y;
+}
+
+// hi32(F * u mod 2^64) for F = hi:lo (64-bit fixed-point turns), u < 2^32, wrapping
+__device__ __forceinline__ uint32_t turns_term(uint32_t lo, uint32_t hi, uint32_t u) {
+    return hi * u + __umulhi(lo, u);
+}
+
+// f = CTF(k) * exp(i pi shift.k) for a segment's image (fsld_common.cuh pixel_factor,
+// forward.py:93-111, 299-303): both phases mod 1 turn, exactly, in 32-bit integer
+// arithmetic (error < 6 * 2^-32 turn), then the fp32 sin/cos.
+__device__ __forceinline__ float2 seg_factor(const SegRegs& R, int kx, int ky) {
+    const int kx2 = kx * kx, ky2 = ky * ky;
+    const uint32_t k2 = (uint32_t)(kx2 + ky2);
+    const uint32_t c2 = (uint32_t)(kx2 - ky2 + 32768);
+    const uint32_t s2 = (uint32_t)(2 * kx * ky + 65536);
+    const uint32_t tg = R.gc + turns_term(R.glo[0], R.ghi[0], k2) + turns_term(R.glo[1], R.ghi[1], c2) +
+                        turns_term(R.glo[2], R.ghi[2], s2) + turns_term(R.glo[3], R.ghi[3], k2 * k2);
+    const uint32_t ts = R.sc + turns_term(R.slo[0], R.shi[0], (uint32_t)(kx + 128)) +
+                        turns_term(R.slo[1], R.shi[1], (uint32_t)(ky + 128));
+    constexpr float kTurn = 1.4629180792671596e-09f;  // 2 pi / 2^32
+    float sg, cg, ss, cs;
+    __sincosf((float)(int)tg * kTurn, &sg, &cg);
+    __sincosf((float)(int)ts * kTurn, &ss, &cs);
+    const float ctf = -(R.wsin * sg + R.wcos * cg) * exp2f(-R.envl * (float)k2);
+    return make_float2(ctf * cs, ctf * ss);
+}
+
 // Per work item (brick, <= BC image segments):
-//   A  claim the item (thread 0);
-//   B  warp 0: segment table + prefix of lengths; warps 1-7: the brick's 9^3
-//      voxels of v (+halo, zero off the grid) -> smem;
-//   C  frames, CTF/shift records (straight from the global records) and the
-//      pixel -> segment table;
-//   1. per pixel (flattened over the item's segments, all lanes busy):
-//      gather 8 corners from the smem brick, f = C * phase, r = f P v - x,
-//      |r|^2 -> loss, val = conj(f) r -> smem buffer;
-//   2. with the item's max |val| known, quantise val * w to int32 with a
-//      power-of-two scale (|val w s| <= 2^22; <= BC*12 contributions per voxel
-//      -> |sum| < 2^31) and add with native ATOMS.ADD (order-free, no CAS);
-//   3. flush: one red.global.add.v2.f32 per touched brick voxel.
-// The scale follows the residual, not |Pv| or |x|: quantum ~2^-22 of the
-// item's largest contribution.
+//   setup: claim (run ahead on one thread), the segment records (one 128-B
+//          SegRec each, written by the fill pass), their prefix, the brick's
+//          9^3 voxels of v (+halo, zero off the grid);
+//   rounds of <= RB pixels (flattened over the item's segments):
+//     0. round pixel -> segment byte table (SEG_T threads per segment);
+//     1. gather 8 corners from the smem brick, f = C * phase, r = f P v - x,
+//        |r|^2 -> loss; conj(f) r and the corner geometry -> smem buffers;
+//     2. with the round's max |val| known, quantise val * w to int32 with a
+//        power-of-two scale (|val w s| <= min(2^22, 2^31 / (12 nseg)): <= 12
+//        contributions per voxel per image) and add with native ATOMS.ADD;
+//     (3. multi-round items: fold the int accumulator into a float one)
+//   flush: one red.global.add.v2.f32 per touched brick voxel.
 __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SortedSmem& S = *reinterpret_cast<SortedSmem*>(smem_raw);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int M = a.M, c = a.c, nb = a.nb, n = a.n_mask;
+    const int M = a.M, c = a.c, nb = a.nb;
     const float bnd = a.bnd;
-    double lsum = 0.0;
-    // Work claiming runs ahead on one thread of the last warp (off warp 0's critical path):
-    // its atomicAdd for item i+2 and descriptor load for item i+1 are issued during item i
-    // and only consumed one iteration later.
+    double lsum = 0.0;  // this thread's sum of |r|^2 (fp32 within a round)
+    int lxyz[BU];  // this thread's brick voxels: lx | ly << 4 | lz << 8 (or -1)
+#pragma unroll
+    for (int u = 0; u < BU; ++u) {
+        const int l = threadIdx.x + u * BTHREADS;
+        lxyz[u] = l < BH3 ? (l % BH) | (((l / BH) % BH) << 4) | ((l / (BH * BH)) << 8) : -1;
+    }
     constexpr int kClaimer = BTHREADS - 32;
     const int n_items = a.ctl[0];
     int next_it = 0, claimed = 0;
@@ -88,12 +153,10 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArg
     PHASE_INIT();
 
     for (;;) {
-        // ---------------- A
         if (threadIdx.x == kClaimer) {
             S.item_desc = next_item;
             S.item = next_it;
         }
-        if (threadIdx.x == 0) S.vmax_bits = 0;
         __syncthreads();
         const int it = S.item;
         if (it >= n_items) break;
@@ -105,160 +168,170 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArg
         }
         const int bid = item.x, pstart = item.y, nseg = item.z;
         const int ox = -c + BT * (bid % nb), oy = -c + BT * ((bid / nb) % nb), oz = -c + BT * (bid / (nb * nb));
-        PHASE_MARK(0);
-        // ---------------- B
-        if (warp == 0) {
-            int len = 0;
-            if (lane < nseg) {
-                const int4 pr = a.pairs[pstart + lane];  // (row, start, count)
-                S.seg_row[lane] = pr.x;
-                S.seg_pos[lane] = pr.y;
-                len = pr.z;
-            }
+        // ---------------- setup: segment records, their prefix (warps 0, 1), v brick
+        {
+            const int4* src = reinterpret_cast<const int4*>(a.pairs + pstart);
+            int4* dst = reinterpret_cast<int4*>(S.seg);
+            for (int w = threadIdx.x; w < nseg * 8; w += BTHREADS) dst[w] = __ldg(src + w);
+        }
+        if (warp < 2) {
+            const int k = threadIdx.x;
+            const int len = k < nseg ? __ldg(&a.pairs[pstart + k].count) : 0;
             int incl = len;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const int t = __shfl_up_sync(0xffffffffu, incl, o);
                 if (lane >= o) incl += t;
             }
-            if (lane < nseg) S.pref[lane] = incl - len;
-            if (lane == 31) S.pref[nseg] = incl;
-        } else {
-            constexpr int U = (BH3 + BTHREADS - 32 - 1) / (BTHREADS - 32);
-            float2 vv[U];
+            S.pref[k] = incl - len;  // warp 1 adds warp 0's total below
+            if (lane == 31) S.wtot[warp] = incl;
+        }
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int l = threadIdx.x - 32 + u * (BTHREADS - 32);
-                const int lx = l % BH, ly = (l / BH) % BH, lz = l / (BH * BH);
-                const int kx = ox + lx, ky = oy + ly, kz = oz + lz;
-                vv[u] = make_float2(0.f, 0.f);
-                if (l < BH3 && kx < M - c && ky < M - c && kz < M - c) vv[u] = __ldg(a.v + lin_index(kx, ky, kz, M, c));
+        for (int u = 0; u < BU; ++u) {
+            if (lxyz[u] < 0) continue;
+            const int l = threadIdx.x + u * BTHREADS;
+            const int kx = ox + (lxyz[u] & 15), ky = oy + ((lxyz[u] >> 4) & 15), kz = oz + (lxyz[u] >> 8);
+            S.vb[l] = (kx < M - c && ky < M - c && kz < M - c) ? __ldg(a.v + lin_index(kx, ky, kz, M, c))
+                                                               : make_float2(0.f, 0.f);
+            S.accr[l] = 0;
+            S.acci[l] = 0;
+            S.facc[l] = make_float2(0.f, 0.f);
+        }
+        __syncthreads();
+        if (threadIdx.x < nseg) {  // final prefix; rebase gofs to the flat pixel index
+            const int k = threadIdx.x;
+            const int p = S.pref[k] + (k >= 32 ? S.wtot[0] : 0);
+            __syncwarp(__activemask());
+            S.pref[k] = p;
+            S.seg[k].gofs -= p;
+        }
+        if (threadIdx.x == 0) S.pref[nseg] = S.wtot[0] + (nseg > 32 ? S.wtot[1] : 0);
+        __syncthreads();
+        PHASE_MARK(0);
+        const int total = S.pref[nseg];
+        const bool multi = total > RB;
+
+        for (int r0 = 0; r0 < total; r0 += RB) {
+            const int rn = min(RB, total - r0);
+            {  // round pixel -> segment table: SEG_T threads per segment
+                const int k = threadIdx.x / SEG_T, q = threadIdx.x % SEG_T;
+                if (k < nseg) {
+                    const int e1 = min(S.pref[k + 1], r0 + rn) - r0;
+                    for (int e = max(S.pref[k], r0) - r0 + q; e < e1; e += SEG_T) S.bk[e] = (unsigned char)k;
+                }
             }
+            if (threadIdx.x == 0) S.vmax_bits = 0;
+            __syncthreads();
+            PHASE_MARK(1);
+            // ---------------- pass 1
+            float vmax = 0.f, sq = 0.f;
+#pragma unroll 1
+            for (int e = threadIdx.x; e < rn; e += BTHREADS) {
+                SegRegs R;
+                load_seg(S.seg[S.bk[e]], R);
+                const long long g = R.gofs + (r0 + e);
+                const char2 kk = a.pc[g];
+                const float2 xv = __ldg(a.xs + g);
+                const int px = kk.x, py = kk.y;
+                float cx, cy, cz, fx, fy, fz;
+                floor_corner((float)px, (float)py, R.fr, bnd, cx, cy, cz, fx, fy, fz);
+                const int lyz = ((int)fz - oz) * BH + ((int)fy - oy), lx = (int)fx - ox;
+                const int l0 = lyz * BH + lx;
+                const float wx = cx - fx, wy = cy - fy, wz = cz - fz;
+                const float ax = 1.f - wx, ay = 1.f - wy, az = 1.f - wz;
+                const float2 f = seg_factor(R, px, py);
+                const float2* vb = S.vb + l0;
+                // trilinear gather (kernels.py:171-176) from the smem brick
+                const float2 WX = make_float2(wx, wx), AX = make_float2(ax, ax);
+                const float2 e0 = __ffma2_rn(WX, vb[1], __fmul2_rn(AX, vb[0]));
+                const float2 e1 = __ffma2_rn(WX, vb[BH + 1], __fmul2_rn(AX, vb[BH]));
+                const float2 e2 = __ffma2_rn(WX, vb[BH * BH + 1], __fmul2_rn(AX, vb[BH * BH]));
+                const float2 e3 = __ffma2_rn(WX, vb[BH * BH + BH + 1], __fmul2_rn(AX, vb[BH * BH + BH]));
+                const float2 q0 = __ffma2_rn(make_float2(wy, wy), e1, __fmul2_rn(make_float2(ay, ay), e0));
+                const float2 q1 = __ffma2_rn(make_float2(wy, wy), e3, __fmul2_rn(make_float2(ay, ay), e2));
+                const float2 pv = __ffma2_rn(make_float2(wz, wz), q1, __fmul2_rn(make_float2(az, az), q0));
+                const float2 prj = cmul(pv, f);
+                const float2 rr = make_float2(prj.x - xv.x, prj.y - xv.y);
+                sq = fmaf(rr.x, rr.x, fmaf(rr.y, rr.y, sq));
+                const float2 val = cmulconj(f, rr);
+                vmax = fmaxf(vmax, fmaxf(fabsf(val.x), fabsf(val.y)));
+                S.bval[e] = val;
+                S.bgeo[e] = make_float4(wx, wy, wz, __int_as_float(l0));
+            }
+            lsum += (double)sq;
+            {  // vmax >= 0, so its bit pattern orders like an int
+                const int vb_max = __reduce_max_sync(0xffffffffu, __float_as_int(vmax));
+                if (lane == 0) atomicMax(&S.vmax_bits, vb_max);
+            }
+            __syncthreads();
+            PHASE_MARK(2);
+            // ---------------- pass 2: fixed-point adjoint scatter (kernels.py:221-230)
+            const float vm = __int_as_float(S.vmax_bits);
+            // <= 12 contributions per voxel per image segment -> |sum| < 2^31
+            const float lim = fminf(4194303.0f, 178956970.0f / (float)nseg);
+            const float sc = vm > 0.f ? exp2f(floorf(log2f(lim / vm))) : 1.0f;
+            const float inv_sc = 1.0f / sc;
+            for (int e = threadIdx.x; e < rn; e += BTHREADS) {
+                const float4 geo = S.bgeo[e];
+                const int l0 = __float_as_int(geo.w);
+                const float wx = geo.x, wy = geo.y, wz = geo.z;
+                const float ax = 1.f - wx, ay = 1.f - wy, az = 1.f - wz;
+                const float2 val = __fmul2_rn(S.bval[e], make_float2(sc, sc));
+                const float zy00 = az * ay, zy10 = az * wy, zy01 = wz * ay, zy11 = wz * wy;
+                const float w8[8] = {zy00 * ax, zy00 * wx, zy10 * ax, zy10 * wx, zy01 * ax, zy01 * wx, zy11 * ax, zy11 * wx};
+                const int off8[8] = {0, 1, BH, BH + 1, BH * BH, BH * BH + 1, BH * BH + BH, BH * BH + BH + 1};
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int l = threadIdx.x - 32 + u * (BTHREADS - 32);
-                if (l < BH3) {
-                    S.vb[l] = vv[u];
+                for (int q = 0; q < 8; ++q) {
+                    const float2 y = __ffma2_rn(make_float2(w8[q], w8[q]), val, make_float2(kMagic, kMagic));
+                    atomicAdd(S.accr + l0 + off8[q], __float_as_int(y.x) - kMagicBits);
+                    atomicAdd(S.acci + l0 + off8[q], __float_as_int(y.y) - kMagicBits);
+                }
+            }
+            __syncthreads();
+            PHASE_MARK(3);
+            if (multi) {  // fold this round's fixed-point sums into the float accumulator
+#pragma unroll
+                for (int u = 0; u < BU; ++u) {
+                    if (lxyz[u] < 0) continue;
+                    const int l = threadIdx.x + u * BTHREADS;
+                    const int qr = S.accr[l], qi = S.acci[l];
+                    if ((qr | qi) == 0) continue;
+                    const float2 f = S.facc[l];
+                    S.facc[l] = make_float2(fmaf((float)qr, inv_sc, f.x), fmaf((float)qi, inv_sc, f.y));
                     S.accr[l] = 0;
                     S.acci[l] = 0;
                 }
-            }
-        }
-        __syncthreads();
-        PHASE_MARK(1);
-        // ---------------- C
-        for (int w = threadIdx.x; w < nseg * 24; w += BTHREADS) {
-            const int k = w / 24, q = w - 24 * (w / 24);
-            const uint32_t* rec = reinterpret_cast<const uint32_t*>(a.recs + S.seg_row[k]);
-            if (q < 18) {
-                reinterpret_cast<uint32_t*>(S.fac + k)[q] = __ldg(rec + 12 + q);
-            } else {
-                S.frame[k][q - 18] = (float)__ldg(reinterpret_cast<const double*>(rec) + (q - 18));
-            }
-        }
-        const int total = min(S.pref[nseg], BBUF);
-        for (int k = warp; k < nseg; k += BW)
-            for (int e = S.pref[k] + lane; e < min(S.pref[k + 1], BBUF); e += 32) S.bk[e] = (unsigned char)k;
-        __syncthreads();
-        PHASE_MARK(2);
-
-        // ---------------- pass 1 (loads of the next pixel issued before the current one is computed)
-        float sq = 0.f, vmax = 0.f;
-        int kn = 0;
-        char2 kkn = make_char2(0, 0);
-        float2 xvn = make_float2(0.f, 0.f);
-        if ((int)threadIdx.x < total) {
-            kn = S.bk[threadIdx.x];
-            const size_t g = (size_t)S.seg_row[kn] * n + S.seg_pos[kn] + (threadIdx.x - S.pref[kn]);
-            kkn = a.pc[g];
-            xvn = __ldg(a.xs + g);
-        }
-        for (int e = threadIdx.x; e < total; e += BTHREADS) {
-            const int k = kn;
-            const char2 kk = kkn;
-            const float2 xv = xvn;
-            if (e + BTHREADS < total) {
-                kn = S.bk[e + BTHREADS];
-                const size_t g = (size_t)S.seg_row[kn] * n + S.seg_pos[kn] + (e + BTHREADS - S.pref[kn]);
-                kkn = a.pc[g];
-                xvn = __ldg(a.xs + g);
-            }
-            S.bpc[e] = kk;
-            const float* fr = S.frame[k];
-            const int px = kk.x, py = kk.y;
-            float cx, cy, cz, fx, fy, fz;
-            floor_corner((float)px, (float)py, fr, bnd, cx, cy, cz, fx, fy, fz);
-            const int l0 = (((int)fz - oz) * BH + ((int)fy - oy)) * BH + ((int)fx - ox);
-            const float wx = cx - fx, wy = cy - fy, wz = cz - fz;
-            const float ax = 1.f - wx, ay = 1.f - wy, az = 1.f - wz;
-            const float2 f = pixel_factor(S.fac[k], px, py);
-            const float2* vb = S.vb + l0;
-            // trilinear gather (kernels.py:171-176) from the smem brick
-            const float2 WX = make_float2(wx, wx), AX = make_float2(ax, ax);
-            const float2 e0 = __ffma2_rn(WX, vb[1], __fmul2_rn(AX, vb[0]));
-            const float2 e1 = __ffma2_rn(WX, vb[BH + 1], __fmul2_rn(AX, vb[BH]));
-            const float2 e2 = __ffma2_rn(WX, vb[BH * BH + 1], __fmul2_rn(AX, vb[BH * BH]));
-            const float2 e3 = __ffma2_rn(WX, vb[BH * BH + BH + 1], __fmul2_rn(AX, vb[BH * BH + BH]));
-            const float2 q0 = __ffma2_rn(make_float2(wy, wy), e1, __fmul2_rn(make_float2(ay, ay), e0));
-            const float2 q1 = __ffma2_rn(make_float2(wy, wy), e3, __fmul2_rn(make_float2(ay, ay), e2));
-            const float2 pv = __ffma2_rn(make_float2(wz, wz), q1, __fmul2_rn(make_float2(az, az), q0));
-            const float2 prj = cmul(pv, f);
-            const float2 rr = make_float2(prj.x - xv.x, prj.y - xv.y);
-            sq = fmaf(rr.x, rr.x, fmaf(rr.y, rr.y, sq));
-            const float2 val = cmulconj(f, rr);
-            vmax = fmaxf(vmax, fmaxf(fabsf(val.x), fabsf(val.y)));
-            S.bval[e] = val;
-        }
-        for (int o = 16; o > 0; o >>= 1) {
-            sq += __shfl_xor_sync(0xffffffffu, sq, o);
-            vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
-        }
-        if (lane == 0) {
-            lsum += (double)sq;
-            atomicMax(&S.vmax_bits, __float_as_int(vmax));
-        }
-        __syncthreads();
-        PHASE_MARK(3);
-
-        // ---------------- pass 2: fixed-point adjoint scatter (kernels.py:221-230)
-        const float vm = __int_as_float(S.vmax_bits);
-        const float sc = vm > 0.f ? exp2f(floorf(log2f(4194303.0f / vm))) : 1.0f;
-        const float inv_sc = 1.0f / sc;
-        for (int e = threadIdx.x; e < total; e += BTHREADS) {
-            const int k = S.bk[e];
-            const char2 kk = S.bpc[e];
-            float cx, cy, cz, fx, fy, fz;
-            floor_corner((float)kk.x, (float)kk.y, S.frame[k], bnd, cx, cy, cz, fx, fy, fz);
-            const int l0 = (((int)fz - oz) * BH + ((int)fy - oy)) * BH + ((int)fx - ox);
-            const float wx = cx - fx, wy = cy - fy, wz = cz - fz;
-            const float ax = 1.f - wx, ay = 1.f - wy, az = 1.f - wz;
-            const float2 val = __fmul2_rn(S.bval[e], make_float2(sc, sc));
-            const float zy00 = az * ay, zy10 = az * wy, zy01 = wz * ay, zy11 = wz * wy;
-            const float w8[8] = {zy00 * ax, zy00 * wx, zy10 * ax, zy10 * wx, zy01 * ax, zy01 * wx, zy11 * ax, zy11 * wx};
-            const int off8[8] = {0, 1, BH, BH + 1, BH * BH, BH * BH + 1, BH * BH + BH, BH * BH + BH + 1};
+            } else {  // single round: flush the fixed-point sums directly
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const float2 y = __ffma2_rn(make_float2(w8[q], w8[q]), val, make_float2(kMagic, kMagic));
-                atomicAdd(S.accr + l0 + off8[q], __float_as_int(y.x) - kMagicBits);
-                atomicAdd(S.acci + l0 + off8[q], __float_as_int(y.y) - kMagicBits);
+                for (int u = 0; u < BU; ++u) {
+                    if (lxyz[u] < 0) continue;
+                    const int l = threadIdx.x + u * BTHREADS;
+                    const int qr = S.accr[l], qi = S.acci[l];
+                    if ((qr | qi) == 0) continue;
+                    const int kx = ox + (lxyz[u] & 15), ky = oy + ((lxyz[u] >> 4) & 15), kz = oz + (lxyz[u] >> 8);
+                    if (kx >= M - c || ky >= M - c || kz >= M - c) continue;
+                    red_f32x2(reinterpret_cast<float*>(a.acc) + 2 * (size_t)lin_index(kx, ky, kz, M, c),
+                              (float)qr * inv_sc, (float)qi * inv_sc);
+                }
+            }
+            __syncthreads();
+        }
+        if (multi) {  // flush the float accumulator: one vector reduction per touched voxel
+#pragma unroll
+            for (int u = 0; u < BU; ++u) {
+                if (lxyz[u] < 0) continue;
+                const int l = threadIdx.x + u * BTHREADS;
+                const float2 q = S.facc[l];
+                if (q.x == 0.f && q.y == 0.f) continue;
+                const int kx = ox + (lxyz[u] & 15), ky = oy + ((lxyz[u] >> 4) & 15), kz = oz + (lxyz[u] >> 8);
+                if (kx >= M - c || ky >= M - c || kz >= M - c) continue;
+                red_f32x2(reinterpret_cast<float*>(a.acc) + 2 * (size_t)lin_index(kx, ky, kz, M, c), q.x, q.y);
             }
         }
-        __syncthreads();
-        PHASE_MARK(4);
-        // ---------------- flush: one vector reduction per touched brick voxel
-        for (int l = threadIdx.x; l < BH3; l += BTHREADS) {
-            const int qr = S.accr[l], qi = S.acci[l];
-            if ((qr | qi) == 0) continue;
-            const int lx = l % BH, ly = (l / BH) % BH, lz = l / (BH * BH);
-            const int kx = ox + lx, ky = oy + ly, kz = oz + lz;
-            if (kx >= M - c || ky >= M - c || kz >= M - c) continue;
-            red_f32x2(reinterpret_cast<float*>(a.acc) + 2 * (size_t)lin_index(kx, ky, kz, M, c),
-                      (float)qr * inv_sc, (float)qi * inv_sc);
-        }
-        __syncthreads();
         PHASE_MARK(7);
     }
     PHASE_FLUSH();
+    for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
     if (lane == 0) S.red[warp] = lsum;
     __syncthreads();
     if (threadIdx.x == 0) {

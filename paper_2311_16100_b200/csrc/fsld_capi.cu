@@ -303,7 +303,7 @@ int fsld_loss_grad_sorted(int M, int mode, int n_mask, const fsld_image_rec* rec
     b.cnt = reinterpret_cast<int*>(scr + L.cnt);
     b.off = reinterpret_cast<int*>(scr + L.off);
     b.fill = reinterpret_cast<int*>(scr + L.fill);
-    b.pairs = reinterpret_cast<int4*>(scr + L.pairs);
+    b.pairs = reinterpret_cast<SegRec*>(scr + L.pairs);
     b.items = reinterpret_cast<int4*>(scr + L.items);
     b.ctl = reinterpret_cast<int*>(scr + L.ctl);
     b.part = reinterpret_cast<double*>(scr + L.part);

@@ -40,7 +40,7 @@ struct SliceArgs {
 constexpr int BT = 8;                 // brick edge (voxels)
 constexpr int BH = BT + 1;            // + halo for the floor+1 corners
 constexpr int BH3 = BH * BH * BH;     // 729
-constexpr int BC = 32;                // segments (images) per work item
+constexpr int BC = 64;                // segments (images) per work item
 constexpr int BW = 8;                 // warps per CTA
 constexpr int BTHREADS = BW * 32;
 constexpr uint32_t kGeomMagic = 0xF51DB200u;
@@ -51,6 +51,28 @@ struct GeomHeader {   // at the start of the scratch buffer (256-byte slot)
     const void* pix;
     int pad1[10];
 };
+
+// Per binned (image, brick) segment, written by the per-step fill pass from the
+// image's fsld_image_rec: everything the main kernel needs per pixel, in six
+// 16-byte words.  The CTF defocus phase and the shift phase are carried as
+// 64-bit fixed-point "turns" coefficients (frac(coef / 2pi) * 2^64), so the
+// kernel evaluates gamma mod 2pi exactly with wrapping 32-bit integer
+// multiplies on small non-negative integer monomials of (kx, ky) instead of
+// fp64 arithmetic (see seg_factor in fsld_brick_main.cuh).
+struct __align__(16) SegRec {
+    long long gofs;       // row * n_mask + start (element offset of the segment in xs / pc)
+    int count, row;
+    float frame[6];       // fp32 rotation rows 0, 1 (floor_corner)
+    float wsin, wcos;     // CTF = -(wsin sin(gamma) + wcos cos(gamma)) * 2^(-envl k^2)
+    float envl;
+    uint32_t gc;          // gamma constant term, turns * 2^32
+    uint32_t sc;          // shift constant term, turns * 2^32
+    uint32_t start;
+    uint32_t glo[4], ghi[4];  // gamma: k2, c2 + 2^15, s2 + 2^16, k2^2
+    uint32_t slo[2], shi[2];  // shift: kx + 128, ky + 128
+    uint32_t pad[4];
+};
+static_assert(sizeof(SegRec) == 128, "SegRec is 8 x 16 B");
 
 struct ScratchLayout {
     size_t hdr, cnt, off, fill, pairs, items, ctl, part, total;
@@ -73,7 +95,7 @@ struct SortedArgs {
     int* cnt;
     int* off;
     int* fill;
-    int4* pairs;             // (dataset row, start, count, 0) per binned segment, item-contiguous
+    SegRec* pairs;           // per binned segment, item-contiguous
     int4* items;             // (brick, first pair, n pairs, 0)
     int* ctl;
     double* part;
