@@ -277,6 +277,75 @@ int fsld_grad_epilogue(int64_t nvox, void* acc, const void* v, double scale, dou
 int fsld_norm2(int64_t n, const void* v, double* out, void* scratch, size_t scratch_bytes,
                void* stream);
 
+/*
+ * ---- Algorithm-1 step on the device -------------------
+ *
+ * One preconditioned SGD step of optim.run (optim.py:362-382) without host
+ * round trips:  loss_grad pass (acc, sq) [+ hutch_fold pass (fold)] ->
+ * fsld_precond_step (grad, Hutchinson average, EMA, threshold, direction and
+ * the line-search volume terms, one pass) -> fsld_armijo_terms (one projection
+ * of the direction) -> fsld_armijo_select (closed-form backtracking) ->
+ * fsld_apply_step.  The loss is quadratic in v, so
+ *   batch_loss(v - eta d) - f0 = 1/2 s (eta^2 |q|^2 - 2 eta Re<r, q>)
+ *                              + 1/2 lam (eta^2 ||d||^2 - 2 eta Re<v, d>)
+ * with r = f P v - x and q = f P d over the batch: (1 + backtracks) loss
+ * passes (optim.py:269-306) become one projection.
+ */
+typedef struct fsld_step_params {
+    double scale;        /* N / |batch| (optim.py:183) */
+    double lam;
+    double beta;         /* EMA weight (optim.py:244) */
+    double floor;        /* alpha, or 1e-12 for the unthresholded variant (optim.py:246) */
+    double w_old, w_new; /* d_avg <- w_old d_avg + w_new sample: k_old/k, k_new/k (optim.py:226-229) */
+    double hutch_scale;  /* sample = hutch_scale * fold + lam, hutch_scale = scale / k_new */
+    int estimating;      /* 1: Hutchinson/EMA/threshold from fold; 0: dhat = dhat_fixed (or 1) */
+    int pad;
+} fsld_step_params;
+
+typedef struct fsld_armijo_state {
+    double eta;          /* carried step size, in/out (optim.py:362, 372-376) */
+    double f0;           /* 1/2 s sq + 1/2 lam ||v||^2 of the step */
+    double f_next;       /* accepted loss */
+    double eta_applied;  /* step applied by fsld_apply_step (0 when decrease == 0) */
+    double decrease;     /* ||grad||^2 in the dhat^-1 norm */
+    int backtracks;
+    int status;          /* 0 ok; 1 = more than max_halvings halvings (NumericalError) */
+    int n_steps;         /* steps selected so far (hist row index) */
+    int pad;
+} fsld_armijo_state;
+
+/* One pass over the volume (complex64 acc / v / dir, float32 state):
+ *   grad = scale*acc + lam*v;  acc <- 0
+ *   estimating: sample = hutch_scale*fold + lam; fold <- 0;
+ *               d_avg <- w_old*d_avg + w_new*sample; d <- beta*d + (1-beta)*d_avg;
+ *               dhat = max(|d|, floor)            (optim.py:210-247)
+ *   else        dhat = dhat_fixed[i] (or 1 when NULL: the plain variant)
+ *   dir = grad / dhat                             (optim.py:292)
+ *   out4 = {sum |grad|^2/dhat, ||v||^2, Re<v, dir>, ||dir||^2}  (fp64, fixed order)
+ * grad_out / dhat_out may be NULL.  scratch >= 4 * 1184 doubles. */
+int fsld_precond_step(int64_t nvox, void* acc, const void* v, float* fold, float* d_avg, float* d,
+                      const float* dhat_fixed, const fsld_step_params* params, void* dir, void* grad_out,
+                      float* dhat_out, double* out4, void* scratch, size_t scratch_bytes, void* stream);
+
+/* Line-search terms of the direction d over the batch (r = f P v - x, q = f P d):
+ *   out3 = {sum |r|^2, sum Re(conj(r) q), sum |q|^2}  (fp64, fixed order).
+ * Coordinates from pc (brick-sorted dataset: xs and pc in the sorted layout) or, when pc
+ * is NULL, from the mask table pix. */
+int fsld_armijo_terms(int M, int mode, int n_mask, const int16_t* pix, const int8_t* pc,
+                      const fsld_image_rec* recs, const int32_t* idx, int B, const void* v, const void* d,
+                      const void* xs, double* out3, void* scratch, size_t scratch_bytes, void* stream);
+
+/* Closed-form Armijo backtracking (optim.py:269-306) on the device, one thread:
+ * sq = the step's loss-pass sum |r|^2 (f0), t3 = fsld_armijo_terms, vol4 = fsld_precond_step.
+ * Halves st->eta until delta(eta) <= -c eta decrease (at most max_halvings times); records
+ * (f0, eta, f_next, backtracks, decrease) into hist[5 * st->n_steps ...] when st->n_steps < hist_cap. */
+int fsld_armijo_select(const double* sq, const double* t3, const double* vol4, double scale, double lam,
+                       double c, int max_halvings, fsld_armijo_state* st, double* hist, int hist_cap,
+                       void* stream);
+
+/* v <- v - st->eta_applied * dir  (complex64). */
+int fsld_apply_step(int64_t nvox, void* v, const void* dir, const fsld_armijo_state* st, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -40,6 +40,21 @@ REC_DTYPE = np.dtype([
 ])
 assert REC_DTYPE.itemsize == 128
 
+
+class StepParams(ctypes.Structure):
+    """fsld_step_params (include/fsld_b200.h)."""
+    _fields_ = [("scale", ctypes.c_double), ("lam", ctypes.c_double), ("beta", ctypes.c_double),
+                ("floor", ctypes.c_double), ("w_old", ctypes.c_double), ("w_new", ctypes.c_double),
+                ("hutch_scale", ctypes.c_double), ("estimating", ctypes.c_int), ("pad", ctypes.c_int)]
+
+
+# fsld_armijo_state (include/fsld_b200.h): 56 bytes, lives in device memory
+ARMIJO_DTYPE = np.dtype([
+    ("eta", "<f8"), ("f0", "<f8"), ("f_next", "<f8"), ("eta_applied", "<f8"), ("decrease", "<f8"),
+    ("backtracks", "<i4"), ("status", "<i4"), ("n_steps", "<i4"), ("pad", "<i4"),
+])
+assert ARMIJO_DTYPE.itemsize == 56
+
 P = ctypes.c_void_p
 I = ctypes.c_int
 I64 = ctypes.c_int64
@@ -78,6 +93,10 @@ SIGNATURES = {
     "fsld_real_finalize": (I, [I64, P, U, P, D, D, P, P]),
     "fsld_norm2": (I, [I64, P, P, P, SZ, P]),
     "fsld_grad_epilogue": (I, [I64, P, P, D, D, P, P, P, P, P, SZ, P]),
+    "fsld_precond_step": (I, [I64, P, P, P, P, P, P, P, P, P, P, P, P, SZ, P]),
+    "fsld_armijo_terms": (I, [I, I, I, P, P, P, P, I, P, P, P, P, P, SZ, P]),
+    "fsld_armijo_select": (I, [P, P, P, D, D, D, I, P, P, I, P]),
+    "fsld_apply_step": (I, [I64, P, P, P, P]),
 }
 
 _lib = None

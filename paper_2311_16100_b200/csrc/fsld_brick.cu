@@ -36,7 +36,7 @@ ScratchLayout scratch_layout(int M, int n_mask, int B) {
     L.cap_items = L.nbr + L.cap_pairs / BC + 1;
     int tiles = (n_mask + kThreads * 4 - 1) / (kThreads * 4);
     long long v1parts = (long long)(B > 0 ? B : 1) * (tiles > 0 ? tiles : 1);
-    L.cap_part = (int)(v1parts > 4096 ? v1parts : 4096);
+    L.cap_part = (int)(3 * v1parts > 8192 ? 3 * v1parts : 8192);  // 3 columns (OP_ARMIJO)
     size_t o = 0;
     L.hdr = o; o = al(o + 256);
     L.cnt = o; o = al(o + sizeof(int) * (size_t)L.nbr);

@@ -396,3 +396,62 @@ extern "C" int fsld_grad_epilogue(int64_t nvox, void* acc, const void* v, double
 extern "C" int fsld_debug_phase_profile(unsigned long long* buf) {
     return status_of(set_phase_profile(buf));
 }
+
+// ---------------------------------------------------------------- Algorithm-1 step (fsld_step.cu)
+
+extern "C" int fsld_precond_step(int64_t nvox, void* acc, const void* v, float* fold, float* d_avg, float* d,
+                                 const float* dhat_fixed, const fsld_step_params* params, void* dir,
+                                 void* grad_out, float* dhat_out, double* out4, void* scratch,
+                                 size_t scratch_bytes, void* stream) {
+    const int nparts = 148 * 8;
+    if (nvox < 1 || !acc || !v || !params || !dir || !out4 || !scratch ||
+        scratch_bytes < 4 * nparts * sizeof(double))
+        return FSLD_EINVAL;
+    if (params->estimating && (!fold || !d_avg || !d)) return FSLD_EINVAL;
+    if (params->estimating && !(params->floor > 0.0)) return FSLD_EINVAL;
+    return status_of(launch_precond_step(nvox, reinterpret_cast<float2*>(acc), reinterpret_cast<const float2*>(v),
+                                         fold, d_avg, d, dhat_fixed, *params, reinterpret_cast<float2*>(dir),
+                                         reinterpret_cast<float2*>(grad_out), dhat_out, out4,
+                                         reinterpret_cast<double*>(scratch), nparts,
+                                         reinterpret_cast<cudaStream_t>(stream)));
+}
+
+extern "C" int fsld_armijo_terms(int M, int mode, int n_mask, const int16_t* pix, const int8_t* pc,
+                                 const fsld_image_rec* recs, const int32_t* idx, int B, const void* v,
+                                 const void* d, const void* xs, double* out3, void* scratch, size_t scratch_bytes,
+                                 void* stream) {
+    if (!geom_ok(M, mode, n_mask, B)) return FSLD_EINVAL;
+    if ((!pix && !pc) || !recs || !v || !d || !xs || !out3 || !scratch) return FSLD_EINVAL;
+    const ScratchLayout L = scratch_layout(M, n_mask, B);
+    if (scratch_bytes < L.total) return FSLD_EINVAL;
+    char* scr = reinterpret_cast<char*>(scratch);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    SliceArgs a = make_args(M, n_mask, pix, recs, idx);
+    const int nblocks = B * a.tiles;
+    if (3 * nblocks > L.cap_part) return FSLD_EINVAL;
+    a.v = reinterpret_cast<const float2*>(v);
+    a.v2 = reinterpret_cast<const float2*>(d);
+    a.x = reinterpret_cast<const float2*>(xs);
+    a.x_by_idx = 1;
+    a.partials = reinterpret_cast<double*>(scr + L.part);
+    a.nparts = nblocks;
+    a.pc = reinterpret_cast<const char2*>(pc);
+    cudaError_t e = launch_slice(OP_ARMIJO, mode, false, a, nblocks, s);
+    if (e != cudaSuccess) return FSLD_ECUDA;
+    return status_of(launch_reduce_cols(a.partials, nblocks, 3, out3, s));
+}
+
+extern "C" int fsld_armijo_select(const double* sq, const double* t3, const double* vol4, double scale, double lam,
+                                  double c, int max_halvings, fsld_armijo_state* st, double* hist, int hist_cap,
+                                  void* stream) {
+    if (!sq || !t3 || !vol4 || !st || !(scale > 0.0) || lam < 0.0 || !(c > 0.0 && c < 1.0) || max_halvings < 0)
+        return FSLD_EINVAL;
+    return status_of(launch_armijo_select(sq, t3, vol4, scale, lam, c, max_halvings, st, hist, hist_cap,
+                                          reinterpret_cast<cudaStream_t>(stream)));
+}
+
+extern "C" int fsld_apply_step(int64_t nvox, void* v, const void* dir, const fsld_armijo_state* st, void* stream) {
+    if (nvox < 1 || !v || !dir || !st) return FSLD_EINVAL;
+    return status_of(launch_apply_step(nvox, reinterpret_cast<float2*>(v), reinterpret_cast<const float2*>(dir), st,
+                                       reinterpret_cast<cudaStream_t>(stream)));
+}

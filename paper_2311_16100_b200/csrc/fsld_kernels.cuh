@@ -5,7 +5,7 @@
 
 namespace fsld {
 
-enum Op { OP_PROJECT = 0, OP_LOSS, OP_LOSS_GRAD, OP_BACKPROJECT, OP_HVP, OP_DIAG };
+enum Op { OP_PROJECT = 0, OP_LOSS, OP_LOSS_GRAD, OP_BACKPROJECT, OP_HVP, OP_DIAG, OP_ARMIJO };
 
 struct SliceArgs {
     int M, c2, n_mask;
@@ -24,6 +24,8 @@ struct SliceArgs {
     const double* fx;      // fixed-point scale (deterministic)
     const float2* ftab;    // optional (B, n_mask) factor table f = phase*ctf (numba-style calls)
     const char2* pc;       // optional per-(row, p) pixel coordinates (brick-sorted dataset layout)
+    const float2* v2;      // OP_ARMIJO: the search direction d
+    int nparts;            // OP_ARMIJO: column stride of the 3 partial columns
 };
 
 // ---------------------------------------------------------------------------
@@ -112,6 +114,17 @@ cudaError_t set_phase_profile(unsigned long long* buf);
 
 cudaError_t launch_slice(int op, int mode, bool det, const SliceArgs& a, int nblocks, cudaStream_t s);
 cudaError_t launch_reduce(const double* part, int n, double* out, cudaStream_t s);
+cudaError_t launch_reduce_cols(const double* part, int n, int ncols, double* out, cudaStream_t s);
+
+// Algorithm-1 step kernels (fsld_step.cu)
+cudaError_t launch_precond_step(int64_t nvox, float2* acc, const float2* v, float* fold, float* d_avg, float* d,
+                                const float* dhat_fixed, const fsld_step_params& p, float2* dir, float2* grad_out,
+                                float* dhat_out, double* out4, double* part, int nparts, cudaStream_t s);
+cudaError_t launch_armijo_select(const double* sq, const double* t3, const double* vol4, double scale, double lam,
+                                 double c, int max_halvings, fsld_armijo_state* st, double* hist, int hist_cap,
+                                 cudaStream_t s);
+cudaError_t launch_apply_step(int64_t nvox, float2* v, const float2* dir, const fsld_armijo_state* st,
+                              cudaStream_t s);
 cudaError_t launch_assign_nn(const SliceArgs& a, int nblocks, int32_t* out, cudaStream_t s);
 cudaError_t launch_hutch(int mode, bool det, const SliceArgs& a, int nblocks, const uint32_t* zbits,
                          int words, int k, cudaStream_t s);

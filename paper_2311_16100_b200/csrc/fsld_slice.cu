@@ -11,6 +11,8 @@
 //   OP_BACKPROJECT scatter conj(f) img                 (Projector.backproject_batch)
 //   OP_HVP         scatter C^2 P z                     (DatasetOperator.hvp body)
 //   OP_DIAG        scatter C^2 w^2 (tri) / C^2 (nn)    (scatter_sq_tri / nn bincount)
+//   OP_ARMIJO      sum |r|^2, sum Re(conj(r) q), sum |q|^2 with r = f P v - x,
+//                  q = f P d: the closed-form line-search terms
 // The residual never touches HBM; loss partials are per-CTA fp64 slots
 // reduced in a fixed order; the adjoint scatter uses red.global.add.v2.f32
 // (or int64 fixed point in deterministic mode).
@@ -33,9 +35,9 @@ __global__ void __launch_bounds__(kThreads) slice_kernel(SliceArgs a) {
     const double bnd = a.bnd;
     const double fx = DET ? *a.fx : 0.0;
     const float2* __restrict__ xrow = nullptr;
-    if (OP == OP_LOSS || OP == OP_LOSS_GRAD || OP == OP_BACKPROJECT)
+    if (OP == OP_LOSS || OP == OP_LOSS_GRAD || OP == OP_BACKPROJECT || OP == OP_ARMIJO)
         xrow = a.x + (size_t)(a.x_by_idx ? row : b) * n;
-    float sq = 0.0f;
+    float sq = 0.0f, rq = 0.0f, qq = 0.0f;
     // brick-sorted dataset layout: per-(row, p) coordinates instead of the shared mask table
     const char2* __restrict__ pcrow = a.pc ? a.pc + (size_t)(a.x_by_idx ? row : b) * n : nullptr;
 
@@ -78,7 +80,17 @@ __global__ void __launch_bounds__(kThreads) slice_kernel(SliceArgs a) {
             val = cmulconj(f, __ldg(xrow + p));
         } else {
             const float2 pv = (MODE == FSLD_MODE_TRI) ? tri_gather(a.v, t) : __ldg(a.v + jn);
-            if constexpr (OP == OP_HVP) {
+            if constexpr (OP == OP_ARMIJO) {
+                const float2 pd = (MODE == FSLD_MODE_TRI) ? tri_gather(a.v2, t) : __ldg(a.v2 + jn);
+                const float2 f = frow ? __ldg(frow + p) : pixel_factor(rec, kx, ky);
+                const float2 pr = cmul(pv, f), q = cmul(pd, f);
+                const float2 xv = __ldg(xrow + p);
+                const float2 r = make_float2(pr.x - xv.x, pr.y - xv.y);
+                sq = fmaf(r.x, r.x, fmaf(r.y, r.y, sq));
+                rq = fmaf(r.x, q.x, fmaf(r.y, q.y, rq));
+                qq = fmaf(q.x, q.x, fmaf(q.y, q.y, qq));
+                continue;
+            } else if constexpr (OP == OP_HVP) {
                 const float c2v = ctf_sq(rec, kx, ky);
                 val = make_float2(c2v * pv.x, c2v * pv.y);
             } else {
@@ -110,6 +122,18 @@ __global__ void __launch_bounds__(kThreads) slice_kernel(SliceArgs a) {
     if constexpr (OP == OP_LOSS || OP == OP_LOSS_GRAD) {
         const double s = block_sum((double)sq, red_smem);
         if (threadIdx.x == 0) a.partials[blockIdx.x] = s;
+    }
+    if constexpr (OP == OP_ARMIJO) {
+        const double s0 = block_sum((double)sq, red_smem);
+        __syncthreads();
+        const double s1 = block_sum((double)rq, red_smem);
+        __syncthreads();
+        const double s2 = block_sum((double)qq, red_smem);
+        if (threadIdx.x == 0) {
+            a.partials[blockIdx.x] = s0;
+            a.partials[a.nparts + blockIdx.x] = s1;
+            a.partials[2 * a.nparts + blockIdx.x] = s2;
+        }
     }
 }
 
@@ -154,6 +178,7 @@ static cudaError_t launch_m(int mode, const SliceArgs& a, int nblocks, cudaStrea
 
 cudaError_t launch_slice(int op, int mode, bool det, const SliceArgs& a, int nblocks, cudaStream_t s) {
     switch (op) {
+        case OP_ARMIJO: return launch_m<OP_ARMIJO, false>(mode, a, nblocks, s);
         case OP_PROJECT: return launch_m<OP_PROJECT, false>(mode, a, nblocks, s);
         case OP_LOSS: return launch_m<OP_LOSS, false>(mode, a, nblocks, s);
         case OP_LOSS_GRAD:
@@ -174,6 +199,13 @@ cudaError_t launch_slice(int op, int mode, bool det, const SliceArgs& a, int nbl
 
 cudaError_t launch_reduce(const double* part, int n, double* out, cudaStream_t s) {
     reduce_partials_kernel<<<1, 1024, 0, s>>>(part, n, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_cols(const double* part, int n, int ncols, double* out, cudaStream_t s) {
+    for (int q = 0; q < ncols; ++q) {
+        reduce_partials_kernel<<<1, 1024, 0, s>>>(part + (size_t)q * n, n, out + q);
+    }
     return cudaGetLastError();
 }
 

@@ -15,6 +15,8 @@ sm_100a kernels of libfsld_b200.so.
 """
 from __future__ import annotations
 
+import ctypes
+
 import numpy as np
 import torch
 
@@ -415,6 +417,62 @@ class SliceEngine:
         C.check(lib.fsld_norm2(self.n_voxels, ctypes_ptr(v), ctypes_ptr(out), ctypes_ptr(scr), scr.numel() * 8,
                                _stream()), "fsld_norm2")
         return out
+
+
+    # ---- Algorithm-1 step (fsld_step.cu) ------------------------------------
+    def _step_scratch(self) -> torch.Tensor:
+        if getattr(self, "_sscr", None) is None:
+            self._sscr = torch.empty(4 * 148 * 8, dtype=torch.float64, device=self.dev)
+        return self._sscr
+
+    def precond_step(self, acc, v, params, dir_out, fold=None, d_avg=None, d=None, dhat_fixed=None,
+                     grad_out=None, dhat_out=None, out4=None) -> torch.Tensor:
+        """One pass: grad, Hutchinson average, EMA, threshold, direction; returns the device
+        doubles {decrease, ||v||^2, Re<v, dir>, ||dir||^2} (fsld_precond_step)."""
+        lib = C.load()
+        v = self._vol(v)
+        out4 = torch.empty(4, dtype=torch.float64, device=self.dev) if out4 is None else out4
+        scr = self._step_scratch()
+        C.check(lib.fsld_precond_step(self.n_voxels, ctypes_ptr(acc), ctypes_ptr(v), ctypes_ptr(fold),
+                                      ctypes_ptr(d_avg), ctypes_ptr(d), ctypes_ptr(dhat_fixed), ctypes.byref(params),
+                                      ctypes_ptr(dir_out), ctypes_ptr(grad_out), ctypes_ptr(dhat_out),
+                                      ctypes_ptr(out4), ctypes_ptr(scr), scr.numel() * 8, _stream()),
+                "fsld_precond_step")
+        return out4
+
+    def armijo_terms(self, v, d, idx, out3=None) -> torch.Tensor:
+        """{sum|r|^2, sum Re(conj(r) q), sum|q|^2}, r = f P v - x, q = f P d over the batch (device doubles)."""
+        lib = C.load()
+        v = self._vol(v)
+        d = self._vol(d)
+        idx = self.idx_tensor(idx)
+        B = idx.numel()
+        out3 = torch.empty(3, dtype=torch.float64, device=self.dev) if out3 is None else out3
+        scr = self.scratch(B)
+        pc = self.pc if self.layout == "sorted" else None
+        C.check(lib.fsld_armijo_terms(self.M, self.mode_id, self.n_mask, ctypes_ptr(self.pix), ctypes_ptr(pc),
+                                      ctypes_ptr(self.recs), ctypes_ptr(idx), B, ctypes_ptr(v), ctypes_ptr(d),
+                                      ctypes_ptr(self.x), ctypes_ptr(out3), ctypes_ptr(scr), scr.numel() * 8,
+                                      _stream()), "fsld_armijo_terms")
+        return out3
+
+    def new_armijo_state(self, eta0: float) -> torch.Tensor:
+        st = np.zeros(1, dtype=C.ARMIJO_DTYPE)
+        st["eta"] = eta0
+        return torch.from_numpy(st.view(np.uint8).copy()).to(self.dev)
+
+    def armijo_select(self, sq, t3, vol4, scale: float, lam: float, c: float, st, hist=None,
+                      max_halvings: int = 60) -> None:
+        lib = C.load()
+        cap = 0 if hist is None else hist.numel() // 5
+        C.check(lib.fsld_armijo_select(ctypes_ptr(sq), ctypes_ptr(t3), ctypes_ptr(vol4), float(scale), float(lam),
+                                       float(c), int(max_halvings), ctypes_ptr(st), ctypes_ptr(hist), cap,
+                                       _stream()), "fsld_armijo_select")
+
+    def apply_step(self, v, dir_, st) -> None:
+        """v <- v - eta_applied * dir (in place; v must be this engine's complex64 volume)."""
+        C.check(C.load().fsld_apply_step(self.n_voxels, ctypes_ptr(v), ctypes_ptr(dir_), ctypes_ptr(st), _stream()),
+                "fsld_apply_step")
 
 
 def _rows_contiguous(pix: np.ndarray) -> bool:

@@ -9,7 +9,7 @@ arrays (reference semantics) or torch CUDA tensors (device-resident loop).
 """
 from __future__ import annotations
 
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 import numpy as np
 import torch
@@ -21,10 +21,68 @@ from .grid import shell_counts
 NOTHRESH_FLOOR = 1e-12
 MAX_HALVINGS = 60
 
+VARIANTS = ("plain", "precomputed", "estimated", "estimated_nothresh")
+
 __all__ = [
-    "PreconditionerState", "epoch_batches", "rademacher", "loss_and_grad", "batch_loss",
-    "hutchinson_update", "ema_and_threshold", "threshold_alpha", "armijo_search",
+    "OptimConfig", "PreconditionerState", "RunTrace", "VARIANTS", "epoch_batches", "rademacher",
+    "loss_and_grad", "batch_loss", "hutchinson_update", "ema_and_threshold", "threshold_alpha",
+    "armijo_search", "run",
 ]
+
+
+@dataclass
+class OptimConfig:
+    """Optimizer hyper-parameters (optim.py:60-95), same validation."""
+
+    lam: float
+    batch_size: int
+    epochs: int
+    beta: float = 0.9
+    c: float = 0.5
+    eta0: float = 1.0
+    variant: str = "estimated"
+    seed: int = 0
+    mode: str = "tri"
+    eta_growth: float = 1.0
+
+    def __post_init__(self) -> None:
+        if self.lam < 0:
+            raise ValueError("lam must be non-negative")
+        if self.batch_size < 1:
+            raise ValueError("batch_size must be >= 1")
+        if self.epochs < 1:
+            raise ValueError("epochs must be >= 1")
+        if not 0.0 < self.beta < 1.0:
+            raise ValueError("beta must lie in (0, 1)")
+        if not 0.0 < self.c < 1.0:
+            raise ValueError("c must lie in (0, 1)")
+        if self.eta0 <= 0:
+            raise ValueError("eta0 must be positive")
+        if self.variant not in VARIANTS:
+            raise ValueError(f"variant must be one of {VARIANTS}")
+        if self.mode not in ("nn", "tri"):
+            raise ValueError("mode must be 'nn' or 'tri'")
+        if self.eta_growth < 1.0:
+            raise ValueError("eta_growth must be >= 1")
+
+
+@dataclass
+class RunTrace:
+    """Per-epoch and per-iteration records of one optimizer run (optim.py:117-130)."""
+
+    loss: np.ndarray
+    eta_end: np.ndarray
+    backtracks: np.ndarray
+    precond_rel_err: np.ndarray
+    fsc_history: np.ndarray | None
+    shell_radii: np.ndarray | None
+    accepted_etas: list = field(default_factory=list)
+    armijo_steps: int = 0
+    armijo_violations: int = 0
+    final_dhat: np.ndarray | None = None
+    step_f0: list = field(default_factory=list)      # per step (not in the reference trace)
+    step_f_next: list = field(default_factory=list)
+    step_backtracks: list = field(default_factory=list)
 
 
 @dataclass
@@ -219,3 +277,139 @@ def armijo_search(v, grad, dhat, loss_fn, eta_in: float, c: float, f0=None):
             return eta, v_next, f_next, backtracks
         eta *= 0.5
     raise NumericalError(f"line search exceeded {MAX_HALVINGS} halvings (non-descent direction or numerical breakdown)")
+
+
+def run(config: OptimConfig, stack, v0=None, reference=None, exact_diag_vec=None, probes: str = "reference",
+        op=None):
+    """Algorithm 1 (optim.py:309-393) with every step resident on the GPU.
+
+    Per batch, in stream order and without host synchronisation:
+      [estimating] probe z -> fsld_hutch_fold (one pass, A*A z folded with z)
+      fsld_loss_grad(_sorted)  -> acc, sum|r|^2
+      fsld_precond_step        -> grad, d_avg, d, dhat, direction, line-search volume terms
+      fsld_armijo_terms        -> one projection of the direction
+      fsld_armijo_select       -> closed-form backtracking (eta carried on the device)
+      fsld_apply_step          -> v <- v - eta direction
+    The host reads the per-step record (f0, eta, f_next, backtracks) and the
+    epoch loss once per epoch.  probes="reference" draws z from the
+    reference's numpy stream (parity); probes="device" generates them in-kernel
+    (counter-based, no z bytes moved).  A line search that exceeds 60 halvings
+    raises NumericalError at the end of that epoch (the reference raises at the step).
+    """
+    from .forward import DatasetOperator, FourierVolume
+    from .hessian import exact_diag
+    from .metrics import ShellIndex, fsc, relative_l2
+    from . import _capi as C
+
+    if probes not in ("reference", "device"):
+        raise ValueError("probes must be 'reference' or 'device'")
+    op = DatasetOperator(stack, config.mode) if op is None else op
+    e = op.engine
+    spec = op.spec
+    nvox = spec.n_voxels
+    alpha = threshold_alpha(stack, None, config.lam)
+    n = op.n_images
+    if config.batch_size > n:
+        raise ValueError("batch_size exceeds the number of images")
+    dev = e.dev
+    if v0 is not None:
+        vals = v0.values if hasattr(v0, "values") else v0
+        v = _to_dev_c64(np.asarray(vals) if not _is_dev(vals) else vals, dev).reshape(-1).clone()
+    else:
+        v = torch.zeros(nvox, dtype=torch.complex64, device=dev)
+
+    estimating = config.variant in ("estimated", "estimated_nothresh")
+    thresholded = config.variant != "estimated_nothresh"
+    floor = alpha if thresholded else NOTHRESH_FLOOR
+    d_avg = torch.zeros(nvox, dtype=torch.float32, device=dev)
+    d = torch.ones(nvox, dtype=torch.float32, device=dev)
+    k = 0
+    dhat_fixed = None
+    if config.variant == "precomputed":
+        if exact_diag_vec is None:
+            exact_diag_vec = exact_diag(stack.poses, stack.ctfs, config.lam, config.mode, spec, op.mask)
+        dhat_fixed = torch.from_numpy(np.maximum(exact_diag_vec, alpha).astype(np.float32)).to(dev)
+    z_rng = z_stream(config.seed)
+
+    n_epochs = config.epochs
+    shells = ShellIndex(spec.M, stack.mask_radius, dev) if reference is not None else None
+    trace = RunTrace(
+        loss=np.empty(n_epochs), eta_end=np.empty(n_epochs), backtracks=np.zeros(n_epochs, dtype=np.int64),
+        precond_rel_err=np.full(n_epochs, np.nan),
+        fsc_history=np.empty((n_epochs, stack.mask_radius + 1)) if reference is not None else None,
+        shell_radii=np.arange(stack.mask_radius + 1) if reference is not None else None)
+    ref_vals = None
+    if reference is not None:
+        rv = reference.values if hasattr(reference, "values") else reference
+        ref_vals = torch.as_tensor(np.asarray(rv) if not _is_dev(rv) else rv, device=dev)
+
+    acc = torch.zeros(nvox, dtype=torch.complex64, device=dev)
+    fold = torch.zeros(nvox, dtype=torch.float32, device=dev)
+    dirv = torch.empty(nvox, dtype=torch.complex64, device=dev)
+    dhat_last = torch.empty(nvox, dtype=torch.float32, device=dev)
+    st = e.new_armijo_state(config.eta0)
+    st_f64 = st.view(torch.float64)
+    max_steps = -(-n // config.batch_size)  # batches per epoch
+    hist = torch.zeros(5 * max_steps, dtype=torch.float64, device=dev)
+    lam = float(config.lam)
+    all_idx = e.all_indices()
+    for epoch in range(n_epochs):
+        batches = epoch_batches(n, config.batch_size, config.seed, epoch)
+        st.view(torch.int32)[12] = 0  # n_steps: hist rows restart each epoch
+        for bi, batch in enumerate(batches):
+            idx = e.idx_tensor(batch)
+            nb = idx.numel()
+            scale = n / nb
+            last = epoch == n_epochs - 1 and bi == len(batches) - 1
+            if estimating:
+                if probes == "reference":
+                    zbits, kk = e.pack_probes(rademacher(z_rng, nvox))
+                else:
+                    zbits, kk = e.gen_probes(1, (config.seed << 32) + epoch * 1000003 + bi), 1
+                if e.deterministic:
+                    facc, ffx = e.hutch_fold(zbits, kk, idx)
+                    fold = e.finalize_r(facc, ffx, 1.0, 0.0)
+                else:
+                    e.hutch_fold(zbits, kk, idx, acc=fold)
+            sq, gacc, gfx = e.loss_grad(v, idx, acc=None if e.deterministic else acc)
+            if e.deterministic:
+                gacc = e.finalize_c(gacc, gfx, 1.0, 0.0)
+            params = C.StepParams(scale=scale, lam=lam, beta=float(config.beta), floor=float(floor),
+                                  w_old=k / (k + 1), w_new=1.0 / (k + 1), hutch_scale=scale,
+                                  estimating=1 if estimating else 0)
+            vol4 = e.precond_step(gacc, v, params, dirv, fold=fold if estimating else None,
+                                  d_avg=d_avg if estimating else None, d=d if estimating else None,
+                                  dhat_fixed=dhat_fixed, dhat_out=dhat_last if last else None)
+            if estimating:
+                k += 1
+            t3 = e.armijo_terms(v, dirv, idx)
+            e.armijo_select(sq, t3, vol4, scale, lam, float(config.c), st, hist, MAX_HALVINGS)
+            e.apply_step(v, dirv, st)
+        # ---- epoch end: the only host synchronisation of the epoch
+        rows = hist[: 5 * len(batches)].view(-1, 5).cpu().numpy()
+        stv = st.cpu().numpy().view(C.ARMIJO_DTYPE)[0]
+        if int(stv["status"]) != 0:
+            raise NumericalError(f"line search exceeded {MAX_HALVINGS} halvings "
+                                 "(non-descent direction or numerical breakdown)")
+        for f0, eta_s, f_next, nbt, dec in rows:
+            trace.armijo_steps += 1
+            if not f_next <= f0 - config.c * eta_s * dec:
+                trace.armijo_violations += 1
+            trace.accepted_etas.append(float(eta_s))
+            trace.step_f0.append(float(f0))
+            trace.step_f_next.append(float(f_next))
+            trace.step_backtracks.append(int(nbt))
+            trace.backtracks[epoch] += int(nbt)
+        st_f64[0] *= config.eta_growth
+        sq_all = e.loss(v, all_idx)
+        trace.loss[epoch] = 0.5 * float(sq_all.item()) + 0.5 * lam * float(e.norm2(v).item())
+        trace.eta_end[epoch] = float(st_f64[0].item())
+        if estimating and exact_diag_vec is not None:
+            trace.precond_rel_err[epoch] = relative_l2(d_avg, exact_diag_vec)
+        if reference is not None:
+            trace.fsc_history[epoch] = fsc(v, ref_vals, shells).values
+    if estimating or dhat_fixed is not None:
+        trace.final_dhat = dhat_last.double().cpu().numpy()
+    else:
+        trace.final_dhat = np.ones(nvox)
+    return FourierVolume(_to_host_c128(v), spec), trace

@@ -129,3 +129,40 @@ def test_blob_volume_layout_is_reference_layout():
         zi = neg[2] if neg[2] >= 0 else neg[2] + M
         jn = (zi * M + neg[1] + (M + 1) // 2) * M + neg[0] + (M + 1) // 2
         assert abs(v[jn] - np.conj(v[j])) < 1e-9 * np.abs(v).max()
+
+
+def test_step_abi_structs_match_header():
+    txt = open(os.path.join(ROOT, "include", "fsld_b200.h")).read()
+    assert "typedef struct fsld_step_params" in txt and "typedef struct fsld_armijo_state" in txt
+    assert ctypes.sizeof(C.StepParams) == 7 * 8 + 2 * 4
+    assert C.ARMIJO_DTYPE.itemsize == 56
+
+
+def test_step_entry_points_reject_bad_arguments_without_gpu():
+    lib = C.load()
+    p = C.StepParams(scale=2.0, lam=0.1, beta=0.9, floor=0.0, w_old=0.0, w_new=1.0, hutch_scale=2.0, estimating=1)
+    # estimating needs fold / d_avg / d and a positive floor
+    assert lib.fsld_precond_step(8, 1, 1, 0, 0, 0, 0, ctypes.byref(p), 1, 0, 0, 1, 1, 1 << 16, 0) == C.FSLD_EINVAL
+    p.floor = 1.0
+    assert lib.fsld_precond_step(8, 1, 1, 1, 1, 1, 0, ctypes.byref(p), 1, 0, 0, 1, 1, 16, 0) == C.FSLD_EINVAL
+    assert lib.fsld_precond_step(8, 1, 1, 1, 1, 1, 0, None, 1, 0, 0, 1, 1, 1 << 16, 0) == C.FSLD_EINVAL
+    # empty batch / bad mode -> ValueError semantics
+    assert lib.fsld_armijo_terms(32, C.MODE_TRI, 749, 1, 0, 1, 1, 0, 1, 1, 1, 1, 1, 1 << 20, 0) == C.FSLD_EINVAL
+    assert lib.fsld_armijo_terms(32, 5, 749, 1, 0, 1, 1, 4, 1, 1, 1, 1, 1, 1 << 20, 0) == C.FSLD_EINVAL
+    # c outside (0, 1), negative lam, non-positive scale
+    assert lib.fsld_armijo_select(1, 1, 1, 1.0, 0.1, 1.5, 60, 1, 0, 0, 0) == C.FSLD_EINVAL
+    assert lib.fsld_armijo_select(1, 1, 1, 1.0, -0.1, 0.5, 60, 1, 0, 0, 0) == C.FSLD_EINVAL
+    assert lib.fsld_armijo_select(1, 1, 1, 0.0, 0.1, 0.5, 60, 1, 0, 0, 0) == C.FSLD_EINVAL
+    assert lib.fsld_apply_step(0, 1, 1, 1, 0) == C.FSLD_EINVAL
+
+
+def test_optim_config_validation_matches_reference():
+    from paper_2311_16100_b200.optim import OptimConfig, VARIANTS
+    assert VARIANTS == ("plain", "precomputed", "estimated", "estimated_nothresh")
+    OptimConfig(lam=0.1, batch_size=4, epochs=1)
+    for bad in (dict(lam=-1.0), dict(batch_size=0), dict(epochs=0), dict(beta=1.0), dict(c=0.0),
+                dict(eta0=0.0), dict(variant="x"), dict(mode="cubic"), dict(eta_growth=0.5)):
+        kw = dict(lam=0.1, batch_size=4, epochs=1)
+        kw.update(bad)
+        with pytest.raises(ValueError):
+            OptimConfig(**kw)

@@ -1,0 +1,210 @@
+"""GPU: the device-resident Algorithm-1 step against the reference.
+
+* fsld_armijo_terms + fsld_precond_step give batch_loss(v - eta d) in closed form;
+  checked against explicit batch_loss passes at several eta;
+* fsld_precond_step's grad / dhat / direction against the reference formulas
+  (optim.py:186-189, 210-247, 292-293) evaluated by the oracle;
+* optim.run (device loop) reproduces the reference's 10-step Algorithm-1
+  trajectory of the golden fixtures (made by the reference itself,
+  tests/golden/make_golden.py): identical Armijo step sizes and backtracks,
+  f0 / accepted loss within 1e-4;
+* the plain and precomputed variants against an oracle loop.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+
+import paper_2311_16100_b200 as F
+from paper_2311_16100_b200 import _capi as C
+from paper_2311_16100_b200 import optim as Opt
+from paper_2311_16100_b200.engine import SliceEngine, records_for
+from paper_2311_16100_b200.forward import CtfParams, DatasetOperator
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    return O.relative_l2(np.asarray(a), np.asarray(b))
+
+
+def radial_ctfs(params):
+    return [CtfParams(float(d), float(w), float(b)) for d, w, b in params] if len(params) else None
+
+
+def golden_stack(g, seed):
+    M = int(g["M"])
+    spec = F.GridSpec(M)
+    mask = g["mask"]
+    images = np.zeros((g["x"].shape[0], M * M), dtype=np.complex128)
+    images[:, mask] = g["x"]
+    poses = [F.Pose(q, t) for q, t in zip(g["quats"], g["shifts"])]
+    return F.ImageStack(spec, images, poses, radial_ctfs(g["ctf_params"]), sigma=0.05, seed=seed,
+                        mask_radius=M // 2 - 1, mode=str(g["mode"]))
+
+
+def golden_op(g, layout=None, deterministic=False):
+    M = int(g["M"])
+    recs = records_for(M, g["quats"], g["shifts"], radial_ctfs(g["ctf_params"]))
+    eng = SliceEngine(M, str(g["mode"]), g["mask"], recs, g["x"], deterministic=deterministic, layout=layout)
+    return DatasetOperator.from_engine(eng, F.GridSpec(M))
+
+
+@pytest.mark.parametrize("name", ["dataset_m16_nn.npz", "dataset_m16_tri.npz"])
+@pytest.mark.parametrize("layout", ["sorted", "mask"])
+def test_closed_form_line_search_matches_batch_loss(golden, name, layout):
+    g = golden(name)
+    op = golden_op(g, layout=layout)
+    e = op.engine
+    lam = float(g["lam"])
+    batch = g["batch"]
+    n = op.n_images
+    scale = n / batch.size
+    v = torch.from_numpy(g["v1"].astype(np.complex64)).cuda()
+    sq, acc, _ = e.loss_grad(v, batch)
+    dirv = torch.empty_like(v)
+    dh = torch.from_numpy((1.0 + np.random.default_rng(0).random(v.numel())).astype(np.float32)).cuda()
+    p = C.StepParams(scale=scale, lam=lam, beta=0.9, floor=1.0, w_old=0.0, w_new=1.0, hutch_scale=scale,
+                     estimating=0)
+    vol4 = e.precond_step(acc, v, p, dirv, dhat_fixed=dh).cpu().numpy()
+    t3 = e.armijo_terms(v, dirv, batch).cpu().numpy()
+    sq = float(sq.item())
+    assert abs(t3[0] - sq) / sq < 1e-6
+    f0 = 0.5 * scale * sq + 0.5 * lam * vol4[1]
+    d_h = dirv.cpu().numpy().astype(np.complex128)
+    v_h = g["v1"]
+    for eta in (1.0, 0.25, 1e-3):
+        f_cf = f0 + 0.5 * scale * (eta * eta * t3[2] - 2 * eta * t3[1]) + 0.5 * lam * (eta * eta * vol4[3]
+                                                                                     - 2 * eta * vol4[2])
+        f_ex = F.batch_loss(op, v_h - eta * d_h, batch, lam)
+        assert abs(f_cf - f_ex) / abs(f_ex) < 1e-5, (eta, f_cf, f_ex)
+
+
+@pytest.mark.parametrize("name", ["dataset_m16_nn.npz", "dataset_m16_tri.npz"])
+def test_precond_step_matches_reference_formulas(golden, name):
+    g = golden(name)
+    op = golden_op(g)
+    e = op.engine
+    lam = float(g["lam"])
+    batch = g["batch"]
+    n = op.n_images
+    scale = n / batch.size
+    M3 = int(g["M"]) ** 3
+    rng = np.random.default_rng(5)
+    v_h = g["v1"]
+    v = torch.from_numpy(v_h.astype(np.complex64)).cuda()
+    z = O.rademacher(rng, M3)
+    d_avg0 = rng.random(M3) * 3
+    d0 = rng.random(M3) * 3
+    k_old, beta, alpha = 3, 0.9, 0.7
+    # device step
+    zbits, k = e.pack_probes(z)
+    fold = torch.zeros(M3, dtype=torch.float32, device="cuda")
+    e.hutch_fold(zbits, k, batch, acc=fold)
+    sq, acc, _ = e.loss_grad(v, batch)
+    d_avg = torch.from_numpy(d_avg0.astype(np.float32)).cuda()
+    d = torch.from_numpy(d0.astype(np.float32)).cuda()
+    dirv = torch.empty_like(v)
+    grad = torch.empty_like(v)
+    dhat = torch.empty(M3, dtype=torch.float32, device="cuda")
+    p = C.StepParams(scale=scale, lam=lam, beta=beta, floor=alpha, w_old=k_old / (k_old + 1),
+                     w_new=1.0 / (k_old + 1), hutch_scale=scale, estimating=1)
+    vol4 = e.precond_step(acc, v, p, dirv, fold=fold, d_avg=d_avg, d=d, grad_out=grad, dhat_out=dhat)
+    # reference formulas on the oracle
+    _, oop = _oracle_op(g)
+    st = O.OracleState(M3, alpha)
+    st.d_avg, st.d, st.k = d_avg0.copy(), d0.copy(), k_old
+    O.hutchinson_update(st, oop, z, batch, lam)
+    dh_ref = O.ema_and_threshold(st, beta, alpha, True)
+    _, g_ref = O.loss_and_grad(oop, v_h, batch, lam)
+    dir_ref = g_ref / dh_ref
+    assert rel(grad.cpu().numpy(), g_ref) < 1e-5
+    assert rel(d_avg.cpu().numpy(), st.d_avg) < 1e-5
+    assert rel(dhat.cpu().numpy(), dh_ref) < 1e-5
+    assert rel(dirv.cpu().numpy(), dir_ref) < 1e-5
+    o = vol4.cpu().numpy()
+    dec_ref = float(((g_ref.real ** 2 + g_ref.imag ** 2) / dh_ref).sum())
+    assert abs(o[0] - dec_ref) / dec_ref < 1e-5
+    assert abs(o[1] - float((np.abs(v_h) ** 2).sum())) / float((np.abs(v_h) ** 2).sum()) < 1e-5
+    assert abs(o[2] - float((v_h.conj() * dir_ref).real.sum())) / abs(float((v_h.conj() * dir_ref).real.sum())) < 1e-4
+    assert abs(o[3] - float((np.abs(dir_ref) ** 2).sum())) / float((np.abs(dir_ref) ** 2).sum()) < 1e-5
+    # accumulators were consumed
+    assert float(acc.abs().max()) == 0.0 and float(fold.abs().max()) == 0.0
+
+
+def _oracle_op(g):
+    M = int(g["M"])
+    mode = str(g["mode"])
+    ctfs = radial_ctfs(g["ctf_params"])
+    ctab = None if ctfs is None else O.ctf_table_radial(g["ctf_params"], O.mask_pix(M, g["mask"]), M)
+    return None, O.OracleOperator(M, mode, g["mask"], g["quats"], g["shifts"], ctab, g["x"])
+
+
+@pytest.mark.parametrize("name,seed", [("dataset_m16_nn.npz", 3), ("dataset_m16_tri.npz", 4)])
+def test_device_run_reproduces_reference_trajectory(golden, name, seed):
+    g = golden(name)
+    stack = golden_stack(g, seed)
+    lam = float(g["lam"])
+    assert abs(Opt.threshold_alpha(stack, None, lam) - float(g["alpha"])) <= 1e-12 * float(g["alpha"])
+    cfg = Opt.OptimConfig(lam=lam, batch_size=int(g["batch"].size), epochs=3, seed=seed, mode=str(g["mode"]))
+    vol, tr = Opt.run(cfg, stack)
+    ref = g["sgd_rec"]
+    etas = np.array(tr.accepted_etas[:10])
+    assert np.array_equal(etas, ref[:, 1])  # identical Armijo decisions
+    assert np.array_equal(np.array(tr.step_backtracks[:10]), ref[:, 3].astype(int))
+    f0 = np.array(tr.step_f0[:10])
+    fn = np.array(tr.step_f_next[:10])
+    assert np.max(np.abs(f0 - ref[:, 0]) / np.abs(ref[:, 0])) < 1e-4
+    assert np.max(np.abs(fn - ref[:, 2]) / np.abs(ref[:, 2])) < 1e-4
+    assert tr.armijo_violations == 0 and tr.armijo_steps == 12
+    assert np.all(np.isfinite(tr.loss)) and tr.loss[-1] < tr.loss[0]
+    assert tr.final_dhat.shape == (int(g["M"]) ** 3,) and np.all(tr.final_dhat >= float(g["alpha"]) * (1 - 1e-6))
+
+
+def _oracle_fixed_dhat_loop(oop, n, lam, batch_size, seed, dhat, n_epochs, c=0.5, eta0=1.0):
+    v = np.zeros(oop.M ** 3, dtype=np.complex128)
+    eta = eta0
+    rec = []
+    for epoch in range(n_epochs):
+        for batch in O.epoch_batches(n, batch_size, seed, epoch):
+            f0, grad = O.loss_and_grad(oop, v, batch, lam)
+            eta, v, f_next, nbt = O.armijo_search(v, grad, dhat, lambda w: O.batch_loss(oop, w, batch, lam),
+                                                  eta, c, f0)
+            rec.append((f0, eta, f_next, nbt))
+    return np.array(rec), v
+
+
+@pytest.mark.parametrize("variant", ["plain", "precomputed"])
+def test_device_run_fixed_preconditioner_variants(golden, variant):
+    g = golden("dataset_m16_tri.npz")
+    seed = 4
+    stack = golden_stack(g, seed)
+    lam = float(g["lam"])
+    _, oop = _oracle_op(g)
+    n = oop.n_images
+    alpha = float(g["alpha"])
+    dhat = np.ones(int(g["M"]) ** 3) if variant == "plain" else np.maximum(g["exact_diag"], alpha)
+    rec, v_ref = _oracle_fixed_dhat_loop(oop, n, lam, 24, seed, dhat, 2)
+    cfg = Opt.OptimConfig(lam=lam, batch_size=24, epochs=2, seed=seed, mode="tri", variant=variant)
+    vol, tr = Opt.run(cfg, stack, exact_diag_vec=g["exact_diag"] if variant == "precomputed" else None)
+    assert np.array_equal(np.array(tr.accepted_etas), rec[:, 1])
+    assert np.max(np.abs(np.array(tr.step_f_next) - rec[:, 2]) / np.abs(rec[:, 2])) < 1e-4
+    assert rel(vol.values, v_ref) < 1e-4
+
+
+def test_device_run_deterministic_engine_and_fsc(golden):
+    g = golden("dataset_m16_tri.npz")
+    seed = 4
+    stack = golden_stack(g, seed)
+    lam = float(g["lam"])
+    cfg = Opt.OptimConfig(lam=lam, batch_size=24, epochs=2, seed=seed, mode="tri")
+    _, tr = Opt.run(cfg, stack)
+    opd = golden_op(g, deterministic=True)
+    vol_d, trd = Opt.run(cfg, stack, op=opd, reference=F.FourierVolume(g["v_true"], F.GridSpec(16)))
+    assert trd.accepted_etas == tr.accepted_etas
+    assert np.max(np.abs(trd.loss - tr.loss) / tr.loss) < 1e-4
+    # deterministic engine: bitwise repeatable trajectory
+    vol_d2, trd2 = Opt.run(cfg, stack, op=golden_op(g, deterministic=True))
+    assert np.array_equal(vol_d.values, vol_d2.values)
+    assert trd.fsc_history.shape == (2, 8) and np.all(np.isfinite(trd.fsc_history[:, 1:]))
