@@ -40,6 +40,7 @@ def parse():
     ap.add_argument("--images", type=int, default=0, help="override dataset size (debug)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-algo1", action="store_true", help="skip the full Algorithm-1 step leg")
     ap.add_argument("--lam", type=float, default=1e-3)
     return ap.parse_args()
 
@@ -319,6 +320,9 @@ def run_b200(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(cfg, B, lam)
+    algo1 = None
+    if world == 1 and not args.no_algo1:
+        algo1 = algo1_leg(eng, wl, B, lam, args)
     if rank == 0:
         line = {
             "metric": "image-slices/sec (fused project+CTF+adjoint, loss+grad)",
@@ -340,9 +344,68 @@ def run_b200(args):
             line["e2e"] = e2e
         if cpu is not None:
             line["cpu_baseline"] = cpu
+        if algo1 is not None:
+            line["algorithm1_step"] = algo1
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def algo1_leg(eng, wl, B, lam, args):
+    """One full Algorithm-1 step (optim.run, optim.py:362-382) resident on the device, estimated variant:
+    probe generation + Hutchinson fold + fused loss+grad + precond/direction epilogue + projection of the
+    direction + closed-form Armijo + update.  Reported beside the headline (which is loss+grad only)."""
+    import torch
+
+    from paper_2311_16100_b200 import _capi as C
+
+    M3 = eng.M ** 3
+    dev = eng.dev
+    v = torch.from_numpy((wl.v_true * 0.5).astype(np.complex64)).to(dev)
+    acc = torch.zeros(M3, dtype=torch.complex64, device=dev)
+    fold = torch.zeros(M3, dtype=torch.float32, device=dev)
+    d_avg = torch.zeros(M3, dtype=torch.float32, device=dev)
+    d = torch.ones(M3, dtype=torch.float32, device=dev)
+    dirv = torch.empty(M3, dtype=torch.complex64, device=dev)
+    st = eng.new_armijo_state(1.0)
+    hist = torch.zeros(5 * (args.warmup + args.steps + 1), dtype=torch.float64, device=dev)
+    gen = np.random.default_rng(4321)
+    n = eng.n_images
+    batches = [torch.from_numpy(gen.choice(n, B, replace=False).astype(np.int32)).to(dev)
+               for _ in range(args.warmup + args.steps)]
+    scale = n / B
+    alpha = 1.0
+
+    def one(i, k):
+        idx = batches[i]
+        zb = eng.gen_probes(1, 77 + i)
+        eng.hutch_fold(zb, 1, idx, acc=fold)
+        sq, _, _ = eng.loss_grad(v, idx, acc=acc)
+        p = C.StepParams(scale=scale, lam=lam, beta=0.9, floor=alpha, w_old=k / (k + 1), w_new=1.0 / (k + 1),
+                         hutch_scale=scale, estimating=1)
+        vol4 = eng.precond_step(acc, v, p, dirv, fold=fold, d_avg=d_avg, d=d)
+        qq = eng.proj_energy(dirv, idx)
+        eng.armijo_select(sq, vol4[4:5], qq, vol4, scale, lam, 0.5, st, hist)
+        eng.apply_step(v, dirv, st)
+
+    for i in range(args.warmup):
+        one(i, i)
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for i in range(args.steps):
+        one(args.warmup + i, args.warmup + i)
+    t1.record()
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / args.steps
+    bt = hist.view(-1, 5)[: args.warmup + args.steps, 3].cpu().numpy()
+    return {"ms_per_step": ms, "images_per_s": B / (ms * 1e-3), "batch": B, "probes_per_step": 1,
+            "mean_backtracks": float(bt.mean()),
+            "kernels": "gen_probes, hutch_fold, loss_grad_sorted (5), precond_step (+reduce), "
+                       "proj_energy_sorted (5), armijo_select, apply_step",
+            "note": "eager launches, L2 not flushed; the reference runs (1 + backtracks) extra loss passes "
+                    "per step where this runs one projection of the direction"}
 
 
 def e2e_leg(eng, wl, B, lam, n_total, args, world):

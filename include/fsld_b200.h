@@ -321,13 +321,14 @@ typedef struct fsld_armijo_state {
  *               dhat = max(|d|, floor)            (optim.py:210-247)
  *   else        dhat = dhat_fixed[i] (or 1 when NULL: the plain variant)
  *   dir = grad / dhat                             (optim.py:292)
- *   out4 = {sum |grad|^2/dhat, ||v||^2, Re<v, dir>, ||dir||^2}  (fp64, fixed order)
- * grad_out / dhat_out may be NULL.  scratch >= 4 * 1184 doubles. */
+ *   out5 = {sum |grad|^2/dhat, ||v||^2, Re<v, dir>, ||dir||^2, Re<acc, dir>}  (fp64, fixed order);
+ *   the last is Re<r, A dir> of the line search (acc = A^* r), so only ||A dir||^2 needs a pass.
+ * grad_out / dhat_out may be NULL.  All vectors 16-byte aligned.  scratch >= 5 * 2368 doubles. */
 int fsld_precond_step(int64_t nvox, void* acc, const void* v, float* fold, float* d_avg, float* d,
                       const float* dhat_fixed, const fsld_step_params* params, void* dir, void* grad_out,
-                      float* dhat_out, double* out4, void* scratch, size_t scratch_bytes, void* stream);
+                      float* dhat_out, double* out5, void* scratch, size_t scratch_bytes, void* stream);
 
-/* Line-search terms of the direction d over the batch (r = f P v - x, q = f P d):
+/* Line-search terms of the direction d over the batch (r = f P v - x, q = f P d), tile kernel:
  *   out3 = {sum |r|^2, sum Re(conj(r) q), sum |q|^2}  (fp64, fixed order).
  * Coordinates from pc (brick-sorted dataset: xs and pc in the sorted layout) or, when pc
  * is NULL, from the mask table pix. */
@@ -335,12 +336,19 @@ int fsld_armijo_terms(int M, int mode, int n_mask, const int16_t* pix, const int
                       const fsld_image_rec* recs, const int32_t* idx, int B, const void* v, const void* d,
                       const void* xs, double* out3, void* scratch, size_t scratch_bytes, void* stream);
 
+/* ||A d||^2 = sum_b sum_p C^2 |P d|^2 over the batch on the brick-sorted layout (tri mode):
+ * a gather-only pass (no images) for the closed-form line search.  *out = device double. */
+int fsld_proj_energy_sorted(int M, int mode, int n_mask, const fsld_image_rec* recs, const int32_t* idx, int B,
+                            const void* d, const int8_t* pc, const int32_t* seg_off, const int32_t* segs,
+                            double* out, void* scratch, size_t scratch_bytes, void* stream);
+
 /* Closed-form Armijo backtracking (optim.py:269-306) on the device, one thread:
- * sq = the step's loss-pass sum |r|^2 (f0), t3 = fsld_armijo_terms, vol4 = fsld_precond_step.
- * Halves st->eta until delta(eta) <= -c eta decrease (at most max_halvings times); records
- * (f0, eta, f_next, backtracks, decrease) into hist[5 * st->n_steps ...] when st->n_steps < hist_cap. */
-int fsld_armijo_select(const double* sq, const double* t3, const double* vol4, double scale, double lam,
-                       double c, int max_halvings, fsld_armijo_state* st, double* hist, int hist_cap,
+ * sq = the step's loss-pass sum |r|^2 (f0), rq = Re<r, A d>, qq = ||A d||^2, vol = the first four
+ * outputs of fsld_precond_step.  Halves st->eta until delta(eta) <= -c eta decrease (at most
+ * max_halvings times); records (f0, eta, f_next, backtracks, decrease) into
+ * hist[5 * st->n_steps ...] when st->n_steps < hist_cap. */
+int fsld_armijo_select(const double* sq, const double* rq, const double* qq, const double* vol, double scale,
+                       double lam, double c, int max_halvings, fsld_armijo_state* st, double* hist, int hist_cap,
                        void* stream);
 
 /* v <- v - st->eta_applied * dir  (complex64). */

@@ -95,7 +95,8 @@ SIGNATURES = {
     "fsld_grad_epilogue": (I, [I64, P, P, D, D, P, P, P, P, P, SZ, P]),
     "fsld_precond_step": (I, [I64, P, P, P, P, P, P, P, P, P, P, P, P, SZ, P]),
     "fsld_armijo_terms": (I, [I, I, I, P, P, P, P, I, P, P, P, P, P, SZ, P]),
-    "fsld_armijo_select": (I, [P, P, P, D, D, D, I, P, P, I, P]),
+    "fsld_armijo_select": (I, [P, P, P, P, D, D, D, I, P, P, I, P]),
+    "fsld_proj_energy_sorted": (I, [I, I, I, P, P, I, P, P, P, P, P, P, SZ, P]),
     "fsld_apply_step": (I, [I64, P, P, P, P]),
 }
 

@@ -108,7 +108,20 @@ cudaError_t launch_real_finalize(int64_t nvox, const void* acc, bool det, const 
 __global__ void norm2_kernel(int64_t n, const float2* __restrict__ v, double* part) {
     __shared__ double smem[32];
     double s = 0.0;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n2 = n / 2, stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if ((reinterpret_cast<uintptr_t>(v) & 15) == 0) {
+        for (int64_t i = t0; i < n2; i += stride) {  // two complex per 16-byte load
+            const float4 z = __ldg(reinterpret_cast<const float4*>(v) + i);
+            s += (double)fmaf(z.x, z.x, z.y * z.y) + (double)fmaf(z.z, z.z, z.w * z.w);
+        }
+    } else {
+        for (int64_t i = t0; i < 2 * n2; i += stride) {
+            const float2 z = v[i];
+            s += (double)z.x * z.x + (double)z.y * z.y;
+        }
+    }
+    for (int64_t i = 2 * n2 + t0; i < n; i += stride) {
         const float2 z = v[i];
         s += (double)z.x * z.x + (double)z.y * z.y;
     }
@@ -135,7 +148,20 @@ __global__ void __launch_bounds__(256) grad_epilogue_kernel(int64_t n, float2* _
                                                             float2* __restrict__ grad, double* part) {
     __shared__ double smem[32];
     double s = 0.0;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool vec = ((reinterpret_cast<uintptr_t>(acc) | reinterpret_cast<uintptr_t>(v) |
+                       reinterpret_cast<uintptr_t>(grad)) & 15) == 0;
+    const int64_t n2 = vec ? n / 2 : 0;
+    for (int64_t i = t0; i < n2; i += stride) {  // two voxels per 16-byte access
+        const float4 a = reinterpret_cast<const float4*>(acc)[i];
+        const float4 w = __ldg(reinterpret_cast<const float4*>(v) + i);
+        reinterpret_cast<float4*>(grad)[i] = make_float4(fmaf(scale, a.x, lam * w.x), fmaf(scale, a.y, lam * w.y),
+                                                         fmaf(scale, a.z, lam * w.z), fmaf(scale, a.w, lam * w.w));
+        reinterpret_cast<float4*>(acc)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        s += (double)fmaf(w.x, w.x, w.y * w.y) + (double)fmaf(w.z, w.z, w.w * w.w);
+    }
+    for (int64_t i = 2 * n2 + t0; i < n; i += stride) {
         const float2 a = acc[i];
         const float2 w = v[i];
         grad[i] = make_float2(fmaf(scale, a.x, lam * w.x), fmaf(scale, a.y, lam * w.y));

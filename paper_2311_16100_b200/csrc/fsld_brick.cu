@@ -369,6 +369,7 @@ __global__ void __launch_bounds__(1024) brick_scan_kernel(SortedArgs a) {
 // ---------------------------------------------------------------- main kernel
 
 #include "fsld_brick_main.cuh"  // the work-item kernel (kept separate: it is the tuning target)
+#include "fsld_brick_energy.cuh"
 
 cudaError_t set_phase_profile(unsigned long long* buf) {
     return cudaMemcpyToSymbol(g_phase_prof, &buf, sizeof(buf));
@@ -397,6 +398,29 @@ cudaError_t launch_sorted_loss_grad(const SortedArgs& a, double* sq_out, cudaStr
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     return launch_reduce(a.part, g_sorted_grid, sq_out, s);
+}
+
+static int g_energy_grid = 0;
+
+cudaError_t launch_sorted_energy(const SortedArgs& a, double* out, cudaStream_t s) {
+    const size_t smem = sizeof(EnergySmem);
+    if (g_energy_grid == 0) {
+        cudaError_t e = cudaFuncSetAttribute(sorted_energy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        int dev = 0, sms = 0, occ = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sorted_energy_kernel, BTHREADS, smem);
+        g_energy_grid = sms * (occ > 0 ? occ : 1);
+    }
+    bin_sorted_kernel<false><<<a.B, 128, 0, s>>>(a);
+    brick_scan_kernel<<<1, 1024, 0, s>>>(a);
+    bin_sorted_kernel<true><<<a.B, 128, 0, s>>>(a);
+    sorted_energy_kernel<<<g_energy_grid, BTHREADS, smem, s>>>(a);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return launch_reduce(a.part, g_energy_grid, out, s);
 }
 
 }  // namespace fsld

@@ -43,6 +43,38 @@ SliceArgs make_args(int M, int n_mask, const int16_t* pix, const fsld_image_rec*
     return a;
 }
 
+SortedArgs make_sorted(const ScratchLayout& L, int M, int n_mask, int B, const fsld_image_rec* recs,
+                       const int32_t* idx, const void* v, const void* xs, const int8_t* pc, const int32_t* seg_off,
+                       const int32_t* segs, void* grad_acc, void* scratch) {
+    char* scr = reinterpret_cast<char*>(scratch);
+    SortedArgs b{};
+    b.M = M;
+    b.c = (M + 1) / 2;
+    b.nb = L.nb;
+    b.nbr = L.nbr;
+    b.n_mask = n_mask;
+    b.B = B;
+    b.bnd = (float)(M / 2 - 1);
+    b.recs = recs;
+    b.idx = idx;
+    b.v = reinterpret_cast<const float2*>(v);
+    b.xs = reinterpret_cast<const float2*>(xs);
+    b.pc = reinterpret_cast<const char2*>(pc);
+    b.seg_off = seg_off;
+    b.segs = reinterpret_cast<const int2*>(segs);
+    b.acc = reinterpret_cast<float2*>(grad_acc);
+    b.cnt = reinterpret_cast<int*>(scr + L.cnt);
+    b.off = reinterpret_cast<int*>(scr + L.off);
+    b.fill = reinterpret_cast<int*>(scr + L.fill);
+    b.pairs = reinterpret_cast<SegRec*>(scr + L.pairs);
+    b.items = reinterpret_cast<int4*>(scr + L.items);
+    b.ctl = reinterpret_cast<int*>(scr + L.ctl);
+    b.part = reinterpret_cast<double*>(scr + L.part);
+    b.cap_pairs = L.cap_pairs;
+    b.cap_items = L.cap_items;
+    return b;
+}
+
 }  // namespace
 
 extern "C" {
@@ -283,32 +315,7 @@ int fsld_loss_grad_sorted(int M, int mode, int n_mask, const fsld_image_rec* rec
                             fx_scale, scratch, scratch_bytes, stream);
     const ScratchLayout L = scratch_layout(M, n_mask, B);
     if (scratch_bytes < L.total) return FSLD_EINVAL;
-    char* scr = reinterpret_cast<char*>(scratch);
-    SortedArgs b{};
-    b.M = M;
-    b.c = (M + 1) / 2;
-    b.nb = L.nb;
-    b.nbr = L.nbr;
-    b.n_mask = n_mask;
-    b.B = B;
-    b.bnd = (float)(M / 2 - 1);
-    b.recs = recs;
-    b.idx = idx;
-    b.v = reinterpret_cast<const float2*>(v);
-    b.xs = reinterpret_cast<const float2*>(xs);
-    b.pc = reinterpret_cast<const char2*>(pc);
-    b.seg_off = seg_off;
-    b.segs = reinterpret_cast<const int2*>(segs);
-    b.acc = reinterpret_cast<float2*>(grad_acc);
-    b.cnt = reinterpret_cast<int*>(scr + L.cnt);
-    b.off = reinterpret_cast<int*>(scr + L.off);
-    b.fill = reinterpret_cast<int*>(scr + L.fill);
-    b.pairs = reinterpret_cast<SegRec*>(scr + L.pairs);
-    b.items = reinterpret_cast<int4*>(scr + L.items);
-    b.ctl = reinterpret_cast<int*>(scr + L.ctl);
-    b.part = reinterpret_cast<double*>(scr + L.part);
-    b.cap_pairs = L.cap_pairs;
-    b.cap_items = L.cap_items;
+    const SortedArgs b = make_sorted(L, M, n_mask, B, recs, idx, v, xs, pc, seg_off, segs, grad_acc, scratch);
     return status_of(launch_sorted_loss_grad(b, sq_out, reinterpret_cast<cudaStream_t>(stream)));
 }
 
@@ -403,11 +410,14 @@ extern "C" int fsld_precond_step(int64_t nvox, void* acc, const void* v, float* 
                                  const float* dhat_fixed, const fsld_step_params* params, void* dir,
                                  void* grad_out, float* dhat_out, double* out4, void* scratch,
                                  size_t scratch_bytes, void* stream) {
-    const int nparts = 148 * 8;
+    const int nparts = 148 * 16;
     if (nvox < 1 || !acc || !v || !params || !dir || !out4 || !scratch ||
-        scratch_bytes < 4 * nparts * sizeof(double))
+        scratch_bytes < 5 * nparts * sizeof(double))
         return FSLD_EINVAL;
     if (params->estimating && (!fold || !d_avg || !d)) return FSLD_EINVAL;
+    for (const void* q : {(const void*)acc, v, (const void*)fold, (const void*)d_avg, (const void*)d,
+                          (const void*)dhat_fixed, (const void*)dir, (const void*)grad_out, (const void*)dhat_out})
+        if (reinterpret_cast<uintptr_t>(q) & 15) return FSLD_EINVAL;  // 16-byte vector accesses
     if (params->estimating && !(params->floor > 0.0)) return FSLD_EINVAL;
     return status_of(launch_precond_step(nvox, reinterpret_cast<float2*>(acc), reinterpret_cast<const float2*>(v),
                                          fold, d_avg, d, dhat_fixed, *params, reinterpret_cast<float2*>(dir),
@@ -441,17 +451,31 @@ extern "C" int fsld_armijo_terms(int M, int mode, int n_mask, const int16_t* pix
     return status_of(launch_reduce_cols(a.partials, nblocks, 3, out3, s));
 }
 
-extern "C" int fsld_armijo_select(const double* sq, const double* t3, const double* vol4, double scale, double lam,
-                                  double c, int max_halvings, fsld_armijo_state* st, double* hist, int hist_cap,
-                                  void* stream) {
-    if (!sq || !t3 || !vol4 || !st || !(scale > 0.0) || lam < 0.0 || !(c > 0.0 && c < 1.0) || max_halvings < 0)
+extern "C" int fsld_armijo_select(const double* sq, const double* rq, const double* qq, const double* vol,
+                                  double scale, double lam, double c, int max_halvings, fsld_armijo_state* st,
+                                  double* hist, int hist_cap, void* stream) {
+    if (!sq || !rq || !qq || !vol || !st || !(scale > 0.0) || lam < 0.0 || !(c > 0.0 && c < 1.0) ||
+        max_halvings < 0)
         return FSLD_EINVAL;
-    return status_of(launch_armijo_select(sq, t3, vol4, scale, lam, c, max_halvings, st, hist, hist_cap,
+    return status_of(launch_armijo_select(sq, rq, qq, vol, scale, lam, c, max_halvings, st, hist, hist_cap,
                                           reinterpret_cast<cudaStream_t>(stream)));
+}
+
+extern "C" int fsld_proj_energy_sorted(int M, int mode, int n_mask, const fsld_image_rec* recs, const int32_t* idx,
+                                       int B, const void* d, const int8_t* pc, const int32_t* seg_off,
+                                       const int32_t* segs, double* out, void* scratch, size_t scratch_bytes,
+                                       void* stream) {
+    if (!geom_ok(M, mode, n_mask, B) || M > 256 || mode != FSLD_MODE_TRI) return FSLD_EINVAL;
+    if (!recs || !d || !pc || !seg_off || !segs || !out || !scratch) return FSLD_EINVAL;
+    const ScratchLayout L = scratch_layout(M, n_mask, B);
+    if (scratch_bytes < L.total) return FSLD_EINVAL;
+    const SortedArgs b = make_sorted(L, M, n_mask, B, recs, idx, d, nullptr, pc, seg_off, segs, nullptr, scratch);
+    return status_of(launch_sorted_energy(b, out, reinterpret_cast<cudaStream_t>(stream)));
 }
 
 extern "C" int fsld_apply_step(int64_t nvox, void* v, const void* dir, const fsld_armijo_state* st, void* stream) {
     if (nvox < 1 || !v || !dir || !st) return FSLD_EINVAL;
+    if ((reinterpret_cast<uintptr_t>(v) | reinterpret_cast<uintptr_t>(dir)) & 15) return FSLD_EINVAL;
     return status_of(launch_apply_step(nvox, reinterpret_cast<float2*>(v), reinterpret_cast<const float2*>(dir), st,
                                        reinterpret_cast<cudaStream_t>(stream)));
 }

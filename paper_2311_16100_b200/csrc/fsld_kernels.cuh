@@ -120,9 +120,10 @@ cudaError_t launch_reduce_cols(const double* part, int n, int ncols, double* out
 cudaError_t launch_precond_step(int64_t nvox, float2* acc, const float2* v, float* fold, float* d_avg, float* d,
                                 const float* dhat_fixed, const fsld_step_params& p, float2* dir, float2* grad_out,
                                 float* dhat_out, double* out4, double* part, int nparts, cudaStream_t s);
-cudaError_t launch_armijo_select(const double* sq, const double* t3, const double* vol4, double scale, double lam,
-                                 double c, int max_halvings, fsld_armijo_state* st, double* hist, int hist_cap,
-                                 cudaStream_t s);
+cudaError_t launch_armijo_select(const double* sq, const double* rq, const double* qq, const double* vol,
+                                 double scale, double lam, double c, int max_halvings, fsld_armijo_state* st,
+                                 double* hist, int hist_cap, cudaStream_t s);
+cudaError_t launch_sorted_energy(const SortedArgs& a, double* out, cudaStream_t s);
 cudaError_t launch_apply_step(int64_t nvox, float2* v, const float2* dir, const fsld_armijo_state* st,
                               cudaStream_t s);
 cudaError_t launch_assign_nn(const SliceArgs& a, int nblocks, int32_t* out, cudaStream_t s);

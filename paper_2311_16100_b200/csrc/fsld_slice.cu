@@ -202,10 +202,18 @@ cudaError_t launch_reduce(const double* part, int n, double* out, cudaStream_t s
     return cudaGetLastError();
 }
 
+// One CTA per column of a (ncols, n) partial table: out[q] = sum_i part[q*n + i], fixed order.
+__global__ void __launch_bounds__(1024) reduce_cols_kernel(const double* __restrict__ part, int n, double* out) {
+    __shared__ double smem[32];
+    const double* col = part + (size_t)blockIdx.x * n;
+    double s = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s += col[i];
+    s = block_sum(s, smem);
+    if (threadIdx.x == 0) out[blockIdx.x] = s;
+}
+
 cudaError_t launch_reduce_cols(const double* part, int n, int ncols, double* out, cudaStream_t s) {
-    for (int q = 0; q < ncols; ++q) {
-        reduce_partials_kernel<<<1, 1024, 0, s>>>(part + (size_t)q * n, n, out + q);
-    }
+    reduce_cols_kernel<<<ncols, 1024, 0, s>>>(part, n, out);
     return cudaGetLastError();
 }
 

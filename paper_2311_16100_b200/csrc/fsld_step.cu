@@ -14,8 +14,37 @@
 namespace fsld {
 
 constexpr int kStepThreads = 256;
+constexpr int kStepBlocks = 148 * 16;  // one sweep covers 2.4M voxels at 4 voxels per thread
 
-// Per voxel (optim.py:186-189, 226-229, 244-247, 292-293); fp32 state, fp64 sums.
+struct StepSums {
+    double dec, vv, vd, dd, ad;
+};
+
+// One voxel (optim.py:186-189, 226-229, 244-247, 292-293): fp32 state and arithmetic.
+__device__ __forceinline__ void precond_voxel(const fsld_step_params& p, float scale, float lam, float2 a, float2 w,
+                                              float* fo, float* da, float* dd, float dfix, float2& g, float2& q,
+                                              float& dh, StepSums& S) {
+    g = make_float2(fmaf(scale, a.x, lam * w.x), fmaf(scale, a.y, lam * w.y));
+    if (p.estimating) {
+        const float sample = fmaf((float)p.hutch_scale, *fo, lam);
+        *fo = 0.f;
+        *da = fmaf((float)p.w_old, *da, (float)p.w_new * sample);
+        *dd = fmaf((float)p.beta, *dd, (float)(1.0 - p.beta) * *da);
+        dh = fmaxf(fabsf(*dd), (float)p.floor);
+    } else {
+        dh = dfix;
+    }
+    const float r = __frcp_rn(dh);
+    q = make_float2(g.x * r, g.y * r);
+    S.dec += (double)(fmaf(g.x, g.x, g.y * g.y) * r);
+    S.vv += (double)fmaf(w.x, w.x, w.y * w.y);
+    S.vd += (double)fmaf(w.x, q.x, w.y * q.y);
+    S.dd += (double)fmaf(q.x, q.x, q.y * q.y);
+    S.ad += (double)fmaf(a.x, q.x, a.y * q.y);  // Re<A^* r, d> = Re<r, A d>
+}
+
+// Four voxels per thread with 16-byte loads issued up front (streaming, HBM-bound);
+// fp64 per-thread sums, fixed-order block and grid reductions.
 __global__ void __launch_bounds__(kStepThreads) precond_step_kernel(int64_t n, float2* __restrict__ acc,
                                                                     const float2* __restrict__ v,
                                                                     float* __restrict__ fold,
@@ -26,45 +55,78 @@ __global__ void __launch_bounds__(kStepThreads) precond_step_kernel(int64_t n, f
                                                                     float* __restrict__ dhat_out, double* part,
                                                                     int nparts) {
     __shared__ double smem[32];
-    double s_dec = 0.0, s_vv = 0.0, s_vd = 0.0, s_dd = 0.0;
+    StepSums S{0.0, 0.0, 0.0, 0.0, 0.0};
     const float scale = (float)p.scale, lam = (float)p.lam;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const float2 a = acc[i];
-        const float2 w = v[i];
-        const float2 g = make_float2(fmaf(scale, a.x, lam * w.x), fmaf(scale, a.y, lam * w.y));
-        acc[i] = make_float2(0.f, 0.f);
-        float dh;
+    const int64_t n4 = n / 4, stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (int64_t q4 = t0; q4 < n4; q4 += stride) {
+        const float4 a01 = reinterpret_cast<const float4*>(acc)[2 * q4];
+        const float4 a23 = reinterpret_cast<const float4*>(acc)[2 * q4 + 1];
+        const float4 w01 = __ldg(reinterpret_cast<const float4*>(v) + 2 * q4);
+        const float4 w23 = __ldg(reinterpret_cast<const float4*>(v) + 2 * q4 + 1);
+        float4 fo = make_float4(0.f, 0.f, 0.f, 0.f), da = fo, dd = fo, df = make_float4(1.f, 1.f, 1.f, 1.f);
         if (p.estimating) {
-            const float sample = (float)(p.hutch_scale * (double)fold[i] + p.lam);
-            fold[i] = 0.f;
-            const float da = (float)(p.w_old * (double)d_avg[i] + p.w_new * (double)sample);
-            d_avg[i] = da;
-            const float dd = (float)(p.beta * (double)d[i] + (1.0 - p.beta) * (double)da);
-            d[i] = dd;
-            dh = fmaxf(fabsf(dd), (float)p.floor);
-        } else {
-            dh = dhat_fixed ? dhat_fixed[i] : 1.0f;
+            fo = reinterpret_cast<const float4*>(fold)[q4];
+            da = reinterpret_cast<const float4*>(d_avg)[q4];
+            dd = reinterpret_cast<const float4*>(d)[q4];
+        } else if (dhat_fixed) {
+            df = __ldg(reinterpret_cast<const float4*>(dhat_fixed) + q4);
         }
-        const float2 q = make_float2(g.x / dh, g.y / dh);
+        float2 g[4], q[4];
+        float dh[4];
+        precond_voxel(p, scale, lam, make_float2(a01.x, a01.y), make_float2(w01.x, w01.y), &fo.x, &da.x, &dd.x, df.x,
+                      g[0], q[0], dh[0], S);
+        precond_voxel(p, scale, lam, make_float2(a01.z, a01.w), make_float2(w01.z, w01.w), &fo.y, &da.y, &dd.y, df.y,
+                      g[1], q[1], dh[1], S);
+        precond_voxel(p, scale, lam, make_float2(a23.x, a23.y), make_float2(w23.x, w23.y), &fo.z, &da.z, &dd.z, df.z,
+                      g[2], q[2], dh[2], S);
+        precond_voxel(p, scale, lam, make_float2(a23.z, a23.w), make_float2(w23.z, w23.w), &fo.w, &da.w, &dd.w, df.w,
+                      g[3], q[3], dh[3], S);
+        const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        reinterpret_cast<float4*>(acc)[2 * q4] = z4;
+        reinterpret_cast<float4*>(acc)[2 * q4 + 1] = z4;
+        if (p.estimating) {
+            reinterpret_cast<float4*>(fold)[q4] = z4;
+            reinterpret_cast<float4*>(d_avg)[q4] = da;
+            reinterpret_cast<float4*>(d)[q4] = dd;
+        }
+        reinterpret_cast<float4*>(dir)[2 * q4] = make_float4(q[0].x, q[0].y, q[1].x, q[1].y);
+        reinterpret_cast<float4*>(dir)[2 * q4 + 1] = make_float4(q[2].x, q[2].y, q[3].x, q[3].y);
+        if (grad_out) {
+            reinterpret_cast<float4*>(grad_out)[2 * q4] = make_float4(g[0].x, g[0].y, g[1].x, g[1].y);
+            reinterpret_cast<float4*>(grad_out)[2 * q4 + 1] = make_float4(g[2].x, g[2].y, g[3].x, g[3].y);
+        }
+        if (dhat_out) reinterpret_cast<float4*>(dhat_out)[q4] = make_float4(dh[0], dh[1], dh[2], dh[3]);
+    }
+    for (int64_t i = 4 * n4 + t0; i < n; i += stride) {  // tail (n not a multiple of 4)
+        float fo = p.estimating ? fold[i] : 0.f, da = p.estimating ? d_avg[i] : 0.f, dd = p.estimating ? d[i] : 0.f;
+        float2 g, q;
+        float dh;
+        precond_voxel(p, scale, lam, acc[i], v[i], &fo, &da, &dd, dhat_fixed ? dhat_fixed[i] : 1.f, g, q, dh, S);
+        acc[i] = make_float2(0.f, 0.f);
+        if (p.estimating) {
+            fold[i] = 0.f;
+            d_avg[i] = da;
+            d[i] = dd;
+        }
         dir[i] = q;
         if (grad_out) grad_out[i] = g;
         if (dhat_out) dhat_out[i] = dh;
-        s_dec += ((double)g.x * g.x + (double)g.y * g.y) / (double)dh;
-        s_vv += (double)w.x * w.x + (double)w.y * w.y;
-        s_vd += (double)w.x * q.x + (double)w.y * q.y;
-        s_dd += (double)q.x * q.x + (double)q.y * q.y;
     }
-    double t = block_sum(s_dec, smem);
+    double t = block_sum(S.dec, smem);
     if (threadIdx.x == 0) part[blockIdx.x] = t;
     __syncthreads();
-    t = block_sum(s_vv, smem);
+    t = block_sum(S.vv, smem);
     if (threadIdx.x == 0) part[nparts + blockIdx.x] = t;
     __syncthreads();
-    t = block_sum(s_vd, smem);
+    t = block_sum(S.vd, smem);
     if (threadIdx.x == 0) part[2 * nparts + blockIdx.x] = t;
     __syncthreads();
-    t = block_sum(s_dd, smem);
+    t = block_sum(S.dd, smem);
     if (threadIdx.x == 0) part[3 * nparts + blockIdx.x] = t;
+    __syncthreads();
+    t = block_sum(S.ad, smem);
+    if (threadIdx.x == 0) part[4 * nparts + blockIdx.x] = t;
 }
 
 cudaError_t launch_precond_step(int64_t nvox, float2* acc, const float2* v, float* fold, float* d_avg, float* d,
@@ -74,19 +136,20 @@ cudaError_t launch_precond_step(int64_t nvox, float2* acc, const float2* v, floa
                                                         dhat_out, part, nparts);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    return launch_reduce_cols(part, nparts, 4, out4, s);
+    return launch_reduce_cols(part, nparts, 5, out4, s);
 }
 
 // optim.armijo_search (optim.py:269-306) with the trial losses in closed form:
 //   f(eta) - f0 = 1/2 s (eta^2 qq - 2 eta rq) + 1/2 lam (eta^2 dd - 2 eta vd).
 // The sufficient-decrease test f(eta) <= f0 - c eta dec is evaluated on the
 // difference (no cancellation against f0).
-__global__ void armijo_select_kernel(const double* __restrict__ sq, const double* __restrict__ t3,
-                                     const double* __restrict__ vol4, double scale, double lam, double c,
-                                     int max_halvings, fsld_armijo_state* st, double* hist, int hist_cap) {
+__global__ void armijo_select_kernel(const double* __restrict__ sq, const double* __restrict__ rqp,
+                                     const double* __restrict__ qqp, const double* __restrict__ vol4, double scale,
+                                     double lam, double c, int max_halvings, fsld_armijo_state* st, double* hist,
+                                     int hist_cap) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     const double dec = vol4[0], vv = vol4[1], vd = vol4[2], dd = vol4[3];
-    const double rq = t3[1], qq = t3[2];
+    const double rq = *rqp, qq = *qqp;
     const double f0 = 0.5 * scale * (*sq) + 0.5 * lam * vv;
     double eta = st->eta;
     st->f0 = f0;
@@ -127,10 +190,10 @@ __global__ void armijo_select_kernel(const double* __restrict__ sq, const double
     st->n_steps = k + 1;
 }
 
-cudaError_t launch_armijo_select(const double* sq, const double* t3, const double* vol4, double scale, double lam,
-                                 double c, int max_halvings, fsld_armijo_state* st, double* hist, int hist_cap,
-                                 cudaStream_t s) {
-    armijo_select_kernel<<<1, 32, 0, s>>>(sq, t3, vol4, scale, lam, c, max_halvings, st, hist, hist_cap);
+cudaError_t launch_armijo_select(const double* sq, const double* rq, const double* qq, const double* vol,
+                                 double scale, double lam, double c, int max_halvings, fsld_armijo_state* st,
+                                 double* hist, int hist_cap, cudaStream_t s) {
+    armijo_select_kernel<<<1, 32, 0, s>>>(sq, rq, qq, vol, scale, lam, c, max_halvings, st, hist, hist_cap);
     return cudaGetLastError();
 }
 
@@ -139,7 +202,15 @@ __global__ void __launch_bounds__(kStepThreads) apply_step_kernel(int64_t n, flo
                                                                   const fsld_armijo_state* __restrict__ st) {
     const float eta = (float)st->eta_applied;
     if (eta == 0.0f) return;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n2 = n / 2, stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (int64_t i = t0; i < n2; i += stride) {  // two voxels (16 B) per access
+        const float4 w = reinterpret_cast<const float4*>(v)[i];
+        const float4 q = __ldg(reinterpret_cast<const float4*>(dir) + i);
+        reinterpret_cast<float4*>(v)[i] =
+            make_float4(fmaf(-eta, q.x, w.x), fmaf(-eta, q.y, w.y), fmaf(-eta, q.z, w.z), fmaf(-eta, q.w, w.w));
+    }
+    for (int64_t i = 2 * n2 + t0; i < n; i += stride) {
         const float2 w = v[i], q = dir[i];
         v[i] = make_float2(fmaf(-eta, q.x, w.x), fmaf(-eta, q.y, w.y));
     }
@@ -147,8 +218,8 @@ __global__ void __launch_bounds__(kStepThreads) apply_step_kernel(int64_t n, flo
 
 cudaError_t launch_apply_step(int64_t nvox, float2* v, const float2* dir, const fsld_armijo_state* st,
                               cudaStream_t s) {
-    int blocks = (int)((nvox + kStepThreads - 1) / kStepThreads);
-    blocks = blocks > 148 * 8 ? 148 * 8 : blocks;
+    int blocks = (int)((nvox / 2 + kStepThreads - 1) / kStepThreads);
+    blocks = blocks < 1 ? 1 : (blocks > kStepBlocks ? kStepBlocks : blocks);
     apply_step_kernel<<<blocks, kStepThreads, 0, s>>>(nvox, v, dir, st);
     return cudaGetLastError();
 }

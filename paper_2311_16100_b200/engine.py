@@ -422,16 +422,16 @@ class SliceEngine:
     # ---- Algorithm-1 step (fsld_step.cu) ------------------------------------
     def _step_scratch(self) -> torch.Tensor:
         if getattr(self, "_sscr", None) is None:
-            self._sscr = torch.empty(4 * 148 * 8, dtype=torch.float64, device=self.dev)
+            self._sscr = torch.empty(5 * 148 * 16, dtype=torch.float64, device=self.dev)
         return self._sscr
 
     def precond_step(self, acc, v, params, dir_out, fold=None, d_avg=None, d=None, dhat_fixed=None,
                      grad_out=None, dhat_out=None, out4=None) -> torch.Tensor:
         """One pass: grad, Hutchinson average, EMA, threshold, direction; returns the device
-        doubles {decrease, ||v||^2, Re<v, dir>, ||dir||^2} (fsld_precond_step)."""
+        doubles {decrease, ||v||^2, Re<v, dir>, ||dir||^2, Re<acc, dir>} (fsld_precond_step)."""
         lib = C.load()
         v = self._vol(v)
-        out4 = torch.empty(4, dtype=torch.float64, device=self.dev) if out4 is None else out4
+        out4 = torch.empty(5, dtype=torch.float64, device=self.dev) if out4 is None else out4
         scr = self._step_scratch()
         C.check(lib.fsld_precond_step(self.n_voxels, ctypes_ptr(acc), ctypes_ptr(v), ctypes_ptr(fold),
                                       ctypes_ptr(d_avg), ctypes_ptr(d), ctypes_ptr(dhat_fixed), ctypes.byref(params),
@@ -461,13 +461,34 @@ class SliceEngine:
         st["eta"] = eta0
         return torch.from_numpy(st.view(np.uint8).copy()).to(self.dev)
 
-    def armijo_select(self, sq, t3, vol4, scale: float, lam: float, c: float, st, hist=None,
+    def proj_energy(self, d, idx, out=None) -> torch.Tensor:
+        """||A d||^2 = sum_b sum_p C^2 |P d|^2 over the batch (device double): the brick-sorted
+        gather-only kernel when available, else the tile kernel's third line-search term."""
+        lib = C.load()
+        d = self._vol(d)
+        idx = self.idx_tensor(idx)
+        B = idx.numel()
+        if self.layout == "sorted" and self.mode == "tri":
+            out = torch.empty(1, dtype=torch.float64, device=self.dev) if out is None else out
+            scr = self.scratch(B)
+            C.check(lib.fsld_proj_energy_sorted(self.M, self.mode_id, self.n_mask, ctypes_ptr(self.recs),
+                                                ctypes_ptr(idx), B, ctypes_ptr(d), ctypes_ptr(self.pc),
+                                                ctypes_ptr(self.seg_off), ctypes_ptr(self.segs), ctypes_ptr(out),
+                                                ctypes_ptr(scr), scr.numel() * 8, _stream()),
+                    "fsld_proj_energy_sorted")
+            return out
+        zero = getattr(self, "_zero_vol", None)
+        if zero is None:
+            zero = self._zero_vol = torch.zeros(self.n_voxels, dtype=torch.complex64, device=self.dev)
+        return self.armijo_terms(zero, d, idx)[2:3]
+
+    def armijo_select(self, sq, rq, qq, vol, scale: float, lam: float, c: float, st, hist=None,
                       max_halvings: int = 60) -> None:
         lib = C.load()
         cap = 0 if hist is None else hist.numel() // 5
-        C.check(lib.fsld_armijo_select(ctypes_ptr(sq), ctypes_ptr(t3), ctypes_ptr(vol4), float(scale), float(lam),
-                                       float(c), int(max_halvings), ctypes_ptr(st), ctypes_ptr(hist), cap,
-                                       _stream()), "fsld_armijo_select")
+        C.check(lib.fsld_armijo_select(ctypes_ptr(sq), ctypes_ptr(rq), ctypes_ptr(qq), ctypes_ptr(vol), float(scale),
+                                       float(lam), float(c), int(max_halvings), ctypes_ptr(st), ctypes_ptr(hist),
+                                       cap, _stream()), "fsld_armijo_select")
 
     def apply_step(self, v, dir_, st) -> None:
         """v <- v - eta_applied * dir (in place; v must be this engine's complex64 volume)."""

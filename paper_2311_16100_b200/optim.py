@@ -287,7 +287,8 @@ def run(config: OptimConfig, stack, v0=None, reference=None, exact_diag_vec=None
       [estimating] probe z -> fsld_hutch_fold (one pass, A*A z folded with z)
       fsld_loss_grad(_sorted)  -> acc, sum|r|^2
       fsld_precond_step        -> grad, d_avg, d, dhat, direction, line-search volume terms
-      fsld_armijo_terms        -> one projection of the direction
+                                  (incl. Re<r, A d> = Re<A^* r, d> from the gradient accumulator)
+      fsld_proj_energy_sorted  -> ||A d||^2, one gather-only pass (tile kernel for other layouts)
       fsld_armijo_select       -> closed-form backtracking (eta carried on the device)
       fsld_apply_step          -> v <- v - eta direction
     The host reads the per-step record (f0, eta, f_next, backtracks) and the
@@ -382,8 +383,8 @@ def run(config: OptimConfig, stack, v0=None, reference=None, exact_diag_vec=None
                                   dhat_fixed=dhat_fixed, dhat_out=dhat_last if last else None)
             if estimating:
                 k += 1
-            t3 = e.armijo_terms(v, dirv, idx)
-            e.armijo_select(sq, t3, vol4, scale, lam, float(config.c), st, hist, MAX_HALVINGS)
+            qq = e.proj_energy(dirv, idx)
+            e.armijo_select(sq, vol4[4:5], qq, vol4, scale, lam, float(config.c), st, hist, MAX_HALVINGS)
             e.apply_step(v, dirv, st)
         # ---- epoch end: the only host synchronisation of the epoch
         rows = hist[: 5 * len(batches)].view(-1, 5).cpu().numpy()

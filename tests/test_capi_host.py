@@ -144,15 +144,20 @@ def test_step_entry_points_reject_bad_arguments_without_gpu():
     # estimating needs fold / d_avg / d and a positive floor
     assert lib.fsld_precond_step(8, 1, 1, 0, 0, 0, 0, ctypes.byref(p), 1, 0, 0, 1, 1, 1 << 16, 0) == C.FSLD_EINVAL
     p.floor = 1.0
-    assert lib.fsld_precond_step(8, 1, 1, 1, 1, 1, 0, ctypes.byref(p), 1, 0, 0, 1, 1, 16, 0) == C.FSLD_EINVAL
+    assert lib.fsld_precond_step(8, 16, 16, 16, 16, 16, 0, ctypes.byref(p), 16, 0, 0, 16, 16, 16, 0) == C.FSLD_EINVAL
+    # misaligned vectors
+    assert lib.fsld_precond_step(8, 8, 16, 16, 16, 16, 0, ctypes.byref(p), 16, 0, 0, 16, 16, 1 << 20, 0) == C.FSLD_EINVAL
     assert lib.fsld_precond_step(8, 1, 1, 1, 1, 1, 0, None, 1, 0, 0, 1, 1, 1 << 16, 0) == C.FSLD_EINVAL
     # empty batch / bad mode -> ValueError semantics
     assert lib.fsld_armijo_terms(32, C.MODE_TRI, 749, 1, 0, 1, 1, 0, 1, 1, 1, 1, 1, 1 << 20, 0) == C.FSLD_EINVAL
     assert lib.fsld_armijo_terms(32, 5, 749, 1, 0, 1, 1, 4, 1, 1, 1, 1, 1, 1 << 20, 0) == C.FSLD_EINVAL
     # c outside (0, 1), negative lam, non-positive scale
-    assert lib.fsld_armijo_select(1, 1, 1, 1.0, 0.1, 1.5, 60, 1, 0, 0, 0) == C.FSLD_EINVAL
-    assert lib.fsld_armijo_select(1, 1, 1, 1.0, -0.1, 0.5, 60, 1, 0, 0, 0) == C.FSLD_EINVAL
-    assert lib.fsld_armijo_select(1, 1, 1, 0.0, 0.1, 0.5, 60, 1, 0, 0, 0) == C.FSLD_EINVAL
+    assert lib.fsld_armijo_select(1, 1, 1, 1, 1.0, 0.1, 1.5, 60, 1, 0, 0, 0) == C.FSLD_EINVAL
+    assert lib.fsld_armijo_select(1, 1, 1, 1, 1.0, -0.1, 0.5, 60, 1, 0, 0, 0) == C.FSLD_EINVAL
+    assert lib.fsld_armijo_select(1, 1, 1, 1, 0.0, 0.1, 0.5, 60, 1, 0, 0, 0) == C.FSLD_EINVAL
+    # brick energy pass: tri only, M <= 256
+    assert lib.fsld_proj_energy_sorted(32, C.MODE_NN, 749, 1, 1, 4, 1, 1, 1, 1, 1, 1, 1 << 24, 0) == C.FSLD_EINVAL
+    assert lib.fsld_proj_energy_sorted(512, C.MODE_TRI, 749, 1, 1, 4, 1, 1, 1, 1, 1, 1, 1 << 24, 0) == C.FSLD_EINVAL
     assert lib.fsld_apply_step(0, 1, 1, 1, 0) == C.FSLD_EINVAL
 
 

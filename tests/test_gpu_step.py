@@ -69,8 +69,11 @@ def test_closed_form_line_search_matches_batch_loss(golden, name, layout):
                      estimating=0)
     vol4 = e.precond_step(acc, v, p, dirv, dhat_fixed=dh).cpu().numpy()
     t3 = e.armijo_terms(v, dirv, batch).cpu().numpy()
+    qq = float(e.proj_energy(dirv, batch).item())
     sq = float(sq.item())
     assert abs(t3[0] - sq) / sq < 1e-6
+    assert abs(t3[1] - vol4[4]) / abs(t3[1]) < 1e-5  # Re<r, A d> from the pixels == Re<A^* r, d> from acc
+    assert abs(t3[2] - qq) / t3[2] < 1e-5            # brick gather-only energy == tile projection
     f0 = 0.5 * scale * sq + 0.5 * lam * vol4[1]
     d_h = dirv.cpu().numpy().astype(np.complex128)
     v_h = g["v1"]
@@ -129,6 +132,8 @@ def test_precond_step_matches_reference_formulas(golden, name):
     assert abs(o[1] - float((np.abs(v_h) ** 2).sum())) / float((np.abs(v_h) ** 2).sum()) < 1e-5
     assert abs(o[2] - float((v_h.conj() * dir_ref).real.sum())) / abs(float((v_h.conj() * dir_ref).real.sum())) < 1e-4
     assert abs(o[3] - float((np.abs(dir_ref) ** 2).sum())) / float((np.abs(dir_ref) ** 2).sum()) < 1e-5
+    ad_ref = float(((g_ref - lam * v_h) / scale * dir_ref.conj()).real.sum())
+    assert abs(o[4] - ad_ref) / abs(ad_ref) < 1e-4
     # accumulators were consumed
     assert float(acc.abs().max()) == 0.0 and float(fold.abs().max()) == 0.0
 
