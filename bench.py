@@ -379,8 +379,7 @@ def algo1_leg(eng, wl, B, lam, args):
     def one(i, k):
         idx = batches[i]
         zb = eng.gen_probes(1, 77 + i)
-        eng.hutch_fold(zb, 1, idx, acc=fold)
-        sq, _, _ = eng.loss_grad(v, idx, acc=acc)
+        sq = eng.loss_grad_hutch(v, idx, zb, acc, fold)
         p = C.StepParams(scale=scale, lam=lam, beta=0.9, floor=alpha, w_old=k / (k + 1), w_new=1.0 / (k + 1),
                          hutch_scale=scale, estimating=1)
         vol4 = eng.precond_step(acc, v, p, dirv, fold=fold, d_avg=d_avg, d=d)
@@ -402,7 +401,7 @@ def algo1_leg(eng, wl, B, lam, args):
     bt = hist.view(-1, 5)[: args.warmup + args.steps, 3].cpu().numpy()
     return {"ms_per_step": ms, "images_per_s": B / (ms * 1e-3), "batch": B, "probes_per_step": 1,
             "mean_backtracks": float(bt.mean()),
-            "kernels": "gen_probes, hutch_fold, loss_grad_sorted (5), precond_step (+reduce), "
+            "kernels": "gen_probes, loss_grad_hutch_sorted (5), precond_step (+reduce), "
                        "proj_energy_sorted (5), armijo_select, apply_step",
             "note": "eager launches, L2 not flushed; the reference runs (1 + backtracks) extra loss passes "
                     "per step where this runs one projection of the direction"}

@@ -230,6 +230,18 @@ int fsld_loss_grad_sorted(int M, int mode, int n_mask, const fsld_image_rec* rec
                           const int32_t* seg_off, const int32_t* segs, void* grad_acc, double* sq_out,
                           unsigned flags, const double* fx_scale, void* scratch, size_t scratch_bytes,
                           void* stream);
+/* fsld_loss_grad_sorted fused with the k = 1 Hutchinson probe of the same batch (tri, brick path):
+ *   grad_acc += sum_b P_b^* conj(f_b) r_b,  *sq_out = sum |r|^2          (optim.py:147-162)
+ *   fold[j]  += z_j (sum_b P_b^* C_b^2 P_b z)_j                           (optim.py:210-229 numerator)
+ * z = +-1 from bit 0 of zbits[j] (M^3 words, fsld_pack_probes / fsld_gen_probes with k = 1).
+ * One pass over the batch: the probe rides along with the gradient (one more gather from
+ * shared memory and 8 more shared-memory adds per pixel).  FSLD_DETERMINISTIC / FSLD_TILE_PATH
+ * are rejected (use fsld_loss_grad_sorted + fsld_hutch_fold). */
+int fsld_loss_grad_hutch_sorted(int M, int mode, int n_mask, const fsld_image_rec* recs, const int32_t* idx, int B,
+                                const void* v, const void* xs, const int8_t* pc, const int32_t* seg_off,
+                                const int32_t* segs, const uint32_t* zbits, void* grad_acc, float* fold,
+                                double* sq_out, unsigned flags, void* scratch, size_t scratch_bytes, void* stream);
+
 /* Loss only over a brick-sorted dataset (Armijo trials, optim.py:193-207). */
 int fsld_loss_sorted(int M, int mode, int n_mask, const fsld_image_rec* recs, const int32_t* idx, int B,
                      const void* v, const void* xs, const int8_t* pc, double* sq_out, void* scratch,

@@ -375,29 +375,32 @@ cudaError_t set_phase_profile(unsigned long long* buf) {
     return cudaMemcpyToSymbol(g_phase_prof, &buf, sizeof(buf));
 }
 
-static int g_sorted_grid = 0;
-
-cudaError_t launch_sorted_loss_grad(const SortedArgs& a, double* sq_out, cudaStream_t s) {
-    const size_t smem = sizeof(SortedSmem);
-    if (g_sorted_grid == 0) {
-        cudaError_t e = cudaFuncSetAttribute(sorted_loss_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
+template <bool HUTCH>
+static cudaError_t launch_sorted_main(const SortedArgs& a, double* sq_out, cudaStream_t s) {
+    static int grid = 0;
+    const size_t smem = sizeof(SortedSmemT<HUTCH>);
+    if (grid == 0) {
+        cudaError_t e = cudaFuncSetAttribute(sorted_loss_grad_kernel<HUTCH>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         int dev = 0, sms = 0, occ = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sorted_loss_grad_kernel, BTHREADS, smem);
-        g_sorted_grid = sms * (occ > 0 ? occ : 1);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sorted_loss_grad_kernel<HUTCH>, BTHREADS, smem);
+        grid = sms * (occ > 0 ? occ : 1);
     }
+    sorted_loss_grad_kernel<HUTCH><<<grid, BTHREADS, smem, s>>>(a);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return launch_reduce(a.part, grid, sq_out, s);
+}
+
+cudaError_t launch_sorted_loss_grad(const SortedArgs& a, double* sq_out, cudaStream_t s) {
     // cnt[] is zero on entry: zeroed by fsld_prepare, and re-zeroed by every scan
-    cudaError_t e;
     bin_sorted_kernel<false><<<a.B, 128, 0, s>>>(a);
     brick_scan_kernel<<<1, 1024, 0, s>>>(a);
     bin_sorted_kernel<true><<<a.B, 128, 0, s>>>(a);
-    sorted_loss_grad_kernel<<<g_sorted_grid, BTHREADS, smem, s>>>(a);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    return launch_reduce(a.part, g_sorted_grid, sq_out, s);
+    return a.zbits ? launch_sorted_main<true>(a, sq_out, s) : launch_sorted_main<false>(a, sq_out, s);
 }
 
 static int g_energy_grid = 0;

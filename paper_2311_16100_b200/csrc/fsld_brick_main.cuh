@@ -22,19 +22,22 @@ constexpr int BU = (BH3 + BTHREADS - 1) / BTHREADS;    // brick voxels per threa
 constexpr int SEG_T = BTHREADS / BC;                   // threads per segment in the bk build (4)
 static_assert(BTHREADS % BC == 0 && BC <= 64, "segment table is built by two warps");
 
-struct SortedSmem {
+template <bool HUTCH>
+struct SortedSmemT {
     float2 vb[BH3];                 // v brick + halo
     int accr[BH3];                  // fixed-point adjoint accumulator of the current round (re)
     int acci[BH3];                  // (im)
-    float2 facc[BH3];               // float accumulator across rounds
+    int acch[HUTCH ? BH3 : 1];      // fixed-point Hutchinson accumulator (real)
+    unsigned char zc[HUTCH ? BH3 : 1];  // z signs: bit c = z at corner c of floor voxel l (bit 0 = z_l)
     float2 bval[RB];                // pass 1 -> 2: conj(f) r
     float4 bgeo[RB];                // pass 1 -> 2: (wx, wy, wz, local corner index)
+    float hval[HUTCH ? RB : 1];     // pass 1 -> 2: C^2 P z (also z staging during setup)
     SegRec seg[BC];                 // the item's segment records (gofs rebased to the flat index)
     int pref[BC + 1];               // exclusive prefix of segment lengths
     unsigned char bk[RB];           // round pixel -> segment
     int4 item_desc;
     int item;
-    int vmax_bits;
+    int vmax_bits, hmax_bits;
     int wtot[2];                    // per-warp segment-length totals
     double red[BW];
 };
@@ -118,19 +121,22 @@ __device__ __forceinline__ float2 seg_factor(const SegRegs& R, int kx, int ky) {
 // Per work item (brick, <= BC image segments):
 //   setup: claim (run ahead on one thread), the segment records (one 128-B
 //          SegRec each, written by the fill pass), their prefix, the brick's
-//          9^3 voxels of v (+halo, zero off the grid);
+//          9^3 voxels of v (+halo, zero off the grid) [and the probe's signs];
 //   rounds of <= RB pixels (flattened over the item's segments):
 //     0. round pixel -> segment byte table (SEG_T threads per segment);
 //     1. gather 8 corners from the smem brick, f = C * phase, r = f P v - x,
-//        |r|^2 -> loss; conj(f) r and the corner geometry -> smem buffers;
+//        |r|^2 -> loss; conj(f) r and the corner geometry -> smem buffers
+//        [HUTCH: h = |f|^2 P z from the corner signs -> smem buffer];
 //     2. with the round's max |val| known, quantise val * w to int32 with a
 //        power-of-two scale (|val w s| <= min(2^22, 2^31 / (12 nseg)): <= 12
-//        contributions per voxel per image) and add with native ATOMS.ADD;
-//     (3. multi-round items: fold the int accumulator into a float one)
-//   flush: one red.global.add.v2.f32 per touched brick voxel.
+//        contributions per voxel per image) and add with native ATOMS.ADD
+//        [HUTCH: the same for h w into a real accumulator];
+//     3. flush: one red.global.add.v2.f32 per touched brick voxel
+//        [HUTCH: fold_j += z_j h_j, one red.global.add.f32], accumulators zeroed.
+template <bool HUTCH>
 __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    SortedSmem& S = *reinterpret_cast<SortedSmem*>(smem_raw);
+    SortedSmemT<HUTCH>& S = *reinterpret_cast<SortedSmemT<HUTCH>*>(smem_raw);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int M = a.M, c = a.c, nb = a.nb;
     const float bnd = a.bnd;
@@ -140,6 +146,11 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArg
     for (int u = 0; u < BU; ++u) {
         const int l = threadIdx.x + u * BTHREADS;
         lxyz[u] = l < BH3 ? (l % BH) | (((l / BH) % BH) << 4) | ((l / (BH * BH)) << 8) : -1;
+        if (l < BH3) {  // accumulators start at zero; every round's flush re-zeroes what it reads
+            S.accr[l] = 0;
+            S.acci[l] = 0;
+            if (HUTCH) S.acch[l] = 0;
+        }
     }
     constexpr int kClaimer = BTHREADS - 32;
     const int n_items = a.ctl[0];
@@ -168,7 +179,7 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArg
         }
         const int bid = item.x, pstart = item.y, nseg = item.z;
         const int ox = -c + BT * (bid % nb), oy = -c + BT * ((bid / nb) % nb), oz = -c + BT * (bid / (nb * nb));
-        // ---------------- setup: segment records, their prefix (warps 0, 1), v brick
+        // ---------------- setup: segment records, their prefix (warps 0, 1), v brick [z signs]
         {
             const int4* src = reinterpret_cast<const int4*>(a.pairs + pstart);
             int4* dst = reinterpret_cast<int4*>(S.seg);
@@ -186,30 +197,42 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArg
             S.pref[k] = incl - len;  // warp 1 adds warp 0's total below
             if (lane == 31) S.wtot[warp] = incl;
         }
+        unsigned char* zs = reinterpret_cast<unsigned char*>(S.hval);  // setup staging of the z bits
 #pragma unroll
         for (int u = 0; u < BU; ++u) {
             if (lxyz[u] < 0) continue;
             const int l = threadIdx.x + u * BTHREADS;
             const int kx = ox + (lxyz[u] & 15), ky = oy + ((lxyz[u] >> 4) & 15), kz = oz + (lxyz[u] >> 8);
-            S.vb[l] = (kx < M - c && ky < M - c && kz < M - c) ? __ldg(a.v + lin_index(kx, ky, kz, M, c))
-                                                               : make_float2(0.f, 0.f);
-            S.accr[l] = 0;
-            S.acci[l] = 0;
-            S.facc[l] = make_float2(0.f, 0.f);
+            const bool in = kx < M - c && ky < M - c && kz < M - c;
+            const int j = in ? lin_index(kx, ky, kz, M, c) : 0;
+            S.vb[l] = in ? __ldg(a.v + j) : make_float2(0.f, 0.f);
+            if (HUTCH) zs[l] = in ? (unsigned char)(__ldg(a.zbits + j) & 1u) : 0;
         }
         __syncthreads();
         if (threadIdx.x < nseg) {  // final prefix; rebase gofs to the flat pixel index
             const int k = threadIdx.x;
             const int p = S.pref[k] + (k >= 32 ? S.wtot[0] : 0);
-            __syncwarp(__activemask());
             S.pref[k] = p;
             S.seg[k].gofs -= p;
         }
         if (threadIdx.x == 0) S.pref[nseg] = S.wtot[0] + (nseg > 32 ? S.wtot[1] : 0);
+        if (HUTCH) {  // corner sign masks (x fastest: 000,100,010,110,001,101,011,111)
+#pragma unroll
+            for (int u = 0; u < BU; ++u) {
+                if (lxyz[u] < 0) continue;
+                const int l = threadIdx.x + u * BTHREADS;
+                unsigned m = zs[l];
+                if ((lxyz[u] & 15) < BT && ((lxyz[u] >> 4) & 15) < BT && (lxyz[u] >> 8) < BT) {
+                    m |= (unsigned)zs[l + 1] << 1 | (unsigned)zs[l + BH] << 2 | (unsigned)zs[l + BH + 1] << 3 |
+                         (unsigned)zs[l + BH * BH] << 4 | (unsigned)zs[l + BH * BH + 1] << 5 |
+                         (unsigned)zs[l + BH * BH + BH] << 6 | (unsigned)zs[l + BH * BH + BH + 1] << 7;
+                }
+                S.zc[l] = (unsigned char)m;
+            }
+        }
         __syncthreads();
         PHASE_MARK(0);
         const int total = S.pref[nseg];
-        const bool multi = total > RB;
 
         for (int r0 = 0; r0 < total; r0 += RB) {
             const int rn = min(RB, total - r0);
@@ -220,11 +243,14 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArg
                     for (int e = max(S.pref[k], r0) - r0 + q; e < e1; e += SEG_T) S.bk[e] = (unsigned char)k;
                 }
             }
-            if (threadIdx.x == 0) S.vmax_bits = 0;
+            if (threadIdx.x == 0) {
+                S.vmax_bits = 0;
+                S.hmax_bits = 0;
+            }
             __syncthreads();
             PHASE_MARK(1);
             // ---------------- pass 1
-            float vmax = 0.f, sq = 0.f;
+            float vmax = 0.f, hmax = 0.f, sq = 0.f;
 #pragma unroll 1
             for (int e = threadIdx.x; e < rn; e += BTHREADS) {
                 SegRegs R;
@@ -235,8 +261,7 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArg
                 const int px = kk.x, py = kk.y;
                 float cx, cy, cz, fx, fy, fz;
                 floor_corner((float)px, (float)py, R.fr, bnd, cx, cy, cz, fx, fy, fz);
-                const int lyz = ((int)fz - oz) * BH + ((int)fy - oy), lx = (int)fx - ox;
-                const int l0 = lyz * BH + lx;
+                const int l0 = (((int)fz - oz) * BH + ((int)fy - oy)) * BH + ((int)fx - ox);
                 const float wx = cx - fx, wy = cy - fy, wz = cz - fz;
                 const float ax = 1.f - wx, ay = 1.f - wy, az = 1.f - wz;
                 const float2 f = seg_factor(R, px, py);
@@ -257,20 +282,40 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArg
                 vmax = fmaxf(vmax, fmaxf(fabsf(val.x), fabsf(val.y)));
                 S.bval[e] = val;
                 S.bgeo[e] = make_float4(wx, wy, wz, __int_as_float(l0));
+                if (HUTCH) {  // P z in the same nested order, z = +-1 from the corner sign bits
+                    const unsigned m = S.zc[l0];
+                    auto zf = [m](int b) { return __int_as_float(0xBF800000u ^ (((m >> b) & 1u) << 31)); };
+                    const float z0 = ax * zf(0) + wx * zf(1), z1 = ax * zf(2) + wx * zf(3);
+                    const float z2 = ax * zf(4) + wx * zf(5), z3 = ax * zf(6) + wx * zf(7);
+                    const float pz = az * (ay * z0 + wy * z1) + wz * (ay * z2 + wy * z3);
+                    const float h = fmaf(f.x, f.x, f.y * f.y) * pz;
+                    S.hval[e] = h;
+                    hmax = fmaxf(hmax, fabsf(h));
+                }
             }
             lsum += (double)sq;
-            {  // vmax >= 0, so its bit pattern orders like an int
+            {  // maxima >= 0, so their bit patterns order like ints
                 const int vb_max = __reduce_max_sync(0xffffffffu, __float_as_int(vmax));
                 if (lane == 0) atomicMax(&S.vmax_bits, vb_max);
+                if (HUTCH) {
+                    const int hb_max = __reduce_max_sync(0xffffffffu, __float_as_int(hmax));
+                    if (lane == 0) atomicMax(&S.hmax_bits, hb_max);
+                }
             }
             __syncthreads();
             PHASE_MARK(2);
             // ---------------- pass 2: fixed-point adjoint scatter (kernels.py:221-230)
-            const float vm = __int_as_float(S.vmax_bits);
             // <= 12 contributions per voxel per image segment -> |sum| < 2^31
             const float lim = fminf(4194303.0f, 178956970.0f / (float)nseg);
+            const float vm = __int_as_float(S.vmax_bits);
             const float sc = vm > 0.f ? exp2f(floorf(log2f(lim / vm))) : 1.0f;
             const float inv_sc = 1.0f / sc;
+            float sch = 1.0f, inv_sch = 1.0f;
+            if (HUTCH) {
+                const float hm = __int_as_float(S.hmax_bits);
+                sch = hm > 0.f ? exp2f(floorf(log2f(lim / hm))) : 1.0f;
+                inv_sch = 1.0f / sch;
+            }
             for (int e = threadIdx.x; e < rn; e += BTHREADS) {
                 const float4 geo = S.bgeo[e];
                 const int l0 = __float_as_int(geo.w);
@@ -286,47 +331,37 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArg
                     atomicAdd(S.accr + l0 + off8[q], __float_as_int(y.x) - kMagicBits);
                     atomicAdd(S.acci + l0 + off8[q], __float_as_int(y.y) - kMagicBits);
                 }
+                if (HUTCH) {
+                    const float h = S.hval[e] * sch;
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        atomicAdd(S.acch + l0 + off8[q], __float_as_int(fmaf(w8[q], h, kMagic)) - kMagicBits);
+                }
             }
             __syncthreads();
             PHASE_MARK(3);
-            if (multi) {  // fold this round's fixed-point sums into the float accumulator
-#pragma unroll
-                for (int u = 0; u < BU; ++u) {
-                    if (lxyz[u] < 0) continue;
-                    const int l = threadIdx.x + u * BTHREADS;
-                    const int qr = S.accr[l], qi = S.acci[l];
-                    if ((qr | qi) == 0) continue;
-                    const float2 f = S.facc[l];
-                    S.facc[l] = make_float2(fmaf((float)qr, inv_sc, f.x), fmaf((float)qi, inv_sc, f.y));
-                    S.accr[l] = 0;
-                    S.acci[l] = 0;
-                }
-            } else {  // single round: flush the fixed-point sums directly
-#pragma unroll
-                for (int u = 0; u < BU; ++u) {
-                    if (lxyz[u] < 0) continue;
-                    const int l = threadIdx.x + u * BTHREADS;
-                    const int qr = S.accr[l], qi = S.acci[l];
-                    if ((qr | qi) == 0) continue;
-                    const int kx = ox + (lxyz[u] & 15), ky = oy + ((lxyz[u] >> 4) & 15), kz = oz + (lxyz[u] >> 8);
-                    if (kx >= M - c || ky >= M - c || kz >= M - c) continue;
-                    red_f32x2(reinterpret_cast<float*>(a.acc) + 2 * (size_t)lin_index(kx, ky, kz, M, c),
-                              (float)qr * inv_sc, (float)qi * inv_sc);
-                }
-            }
-            __syncthreads();
-        }
-        if (multi) {  // flush the float accumulator: one vector reduction per touched voxel
+            // ---------------- flush this round: one reduction per touched voxel, accumulators re-zeroed
 #pragma unroll
             for (int u = 0; u < BU; ++u) {
                 if (lxyz[u] < 0) continue;
                 const int l = threadIdx.x + u * BTHREADS;
-                const float2 q = S.facc[l];
-                if (q.x == 0.f && q.y == 0.f) continue;
+                const int qr = S.accr[l], qi = S.acci[l];
+                const int qh = HUTCH ? S.acch[l] : 0;
+                if ((qr | qi | qh) == 0) continue;
+                S.accr[l] = 0;
+                S.acci[l] = 0;
+                if (HUTCH) S.acch[l] = 0;
                 const int kx = ox + (lxyz[u] & 15), ky = oy + ((lxyz[u] >> 4) & 15), kz = oz + (lxyz[u] >> 8);
                 if (kx >= M - c || ky >= M - c || kz >= M - c) continue;
-                red_f32x2(reinterpret_cast<float*>(a.acc) + 2 * (size_t)lin_index(kx, ky, kz, M, c), q.x, q.y);
+                const size_t j = (size_t)lin_index(kx, ky, kz, M, c);
+                if ((qr | qi) != 0)
+                    red_f32x2(reinterpret_cast<float*>(a.acc) + 2 * j, (float)qr * inv_sc, (float)qi * inv_sc);
+                if (HUTCH && qh != 0) {
+                    const float hz = (S.zc[l] & 1u) ? (float)qh * inv_sch : -(float)qh * inv_sch;
+                    atomicAdd(a.fold + j, hz);
+                }
             }
+            __syncthreads();
         }
         PHASE_MARK(7);
     }

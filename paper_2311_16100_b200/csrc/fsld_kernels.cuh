@@ -94,6 +94,8 @@ struct SortedArgs {
     const int32_t* seg_off;  // (N+1) CSR offsets into segs
     const int2* segs;        // (brick, start | count << 16)
     float2* acc;
+    const uint32_t* zbits;   // optional k = 1 Rademacher probe (bit 0 of word j, M^3 words): fused Hutchinson
+    float* fold;             // fold[j] += z_j (sum_b P^* C^2 P z)_j
     int* cnt;
     int* off;
     int* fill;
@@ -109,7 +111,7 @@ cudaError_t launch_sorted_count(int M, int n_mask, const short2* pix, const fsld
 cudaError_t launch_sorted_fill(int M, int n_mask, const short2* pix, const fsld_image_rec* recs, int N,
                                const float2* x_in, float2* x_out, char2* pc_out, const int32_t* seg_off,
                                int2* segs, cudaStream_t s);
-cudaError_t launch_sorted_loss_grad(const SortedArgs& a, double* sq_out, cudaStream_t s);
+cudaError_t launch_sorted_loss_grad(const SortedArgs& a, double* sq_out, cudaStream_t s);  // + hutch if a.zbits
 cudaError_t set_phase_profile(unsigned long long* buf);
 
 cudaError_t launch_slice(int op, int mode, bool det, const SliceArgs& a, int nblocks, cudaStream_t s);

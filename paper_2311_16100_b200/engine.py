@@ -223,6 +223,31 @@ class SliceEngine:
                 "fsld_loss_grad")
         return sq, acc, fx
 
+    def loss_grad_hutch(self, v, idx, zbits, acc, fold):
+        """loss_grad + the k = 1 Hutchinson fold of the same batch (acc, fold accumulate in place).
+
+        One fused brick-path pass when available (tri, brick-sorted layout, not deterministic);
+        otherwise fsld_hutch_fold + loss_grad.  Returns sq (device double)."""
+        lib = C.load()
+        fused = self.layout == "sorted" and self.mode == "tri" and not self.deterministic and \
+            not (self.flags & C.TILE_PATH) and self.M <= 256
+        if not fused:
+            self.hutch_fold(zbits, 1, idx, acc=fold)
+            sq, _, _ = self.loss_grad(v, idx, acc=acc)
+            return sq
+        v = self._vol(v)
+        idx = self.idx_tensor(idx)
+        B = idx.numel()
+        sq = torch.empty(1, dtype=torch.float64, device=self.dev)
+        scr = self.scratch(B)
+        C.check(lib.fsld_loss_grad_hutch_sorted(self.M, self.mode_id, self.n_mask, ctypes_ptr(self.recs),
+                                                ctypes_ptr(idx), B, ctypes_ptr(v), ctypes_ptr(self.x),
+                                                ctypes_ptr(self.pc), ctypes_ptr(self.seg_off), ctypes_ptr(self.segs),
+                                                ctypes_ptr(zbits), ctypes_ptr(acc), ctypes_ptr(fold), ctypes_ptr(sq),
+                                                0, ctypes_ptr(scr), scr.numel() * 8, _stream()),
+                "fsld_loss_grad_hutch_sorted")
+        return sq
+
     def loss(self, v, idx):
         """sum|P v - x|^2 over the batch, device double (optim.py:193-207 data term)."""
         lib = C.load()

@@ -284,8 +284,8 @@ def run(config: OptimConfig, stack, v0=None, reference=None, exact_diag_vec=None
     """Algorithm 1 (optim.py:309-393) with every step resident on the GPU.
 
     Per batch, in stream order and without host synchronisation:
-      [estimating] probe z -> fsld_hutch_fold (one pass, A*A z folded with z)
-      fsld_loss_grad(_sorted)  -> acc, sum|r|^2
+      fsld_loss_grad_hutch_sorted -> acc, sum|r|^2 and (estimating) the probe's fold z*(A*A z),
+                                  one fused pass (else fsld_hutch_fold + fsld_loss_grad)
       fsld_precond_step        -> grad, d_avg, d, dhat, direction, line-search volume terms
                                   (incl. Re<r, A d> = Re<A^* r, d> from the gradient accumulator)
       fsld_proj_energy_sorted  -> ||A d||^2, one gather-only pass (tile kernel for other layouts)
@@ -367,14 +367,17 @@ def run(config: OptimConfig, stack, v0=None, reference=None, exact_diag_vec=None
                     zbits, kk = e.pack_probes(rademacher(z_rng, nvox))
                 else:
                     zbits, kk = e.gen_probes(1, (config.seed << 32) + epoch * 1000003 + bi), 1
-                if e.deterministic:
+            if estimating and not e.deterministic:
+                # one fused pass: gradient accumulator + the probe's Hutchinson fold
+                sq = e.loss_grad_hutch(v, idx, zbits, acc, fold)
+                gacc = acc
+            else:
+                if estimating:
                     facc, ffx = e.hutch_fold(zbits, kk, idx)
                     fold = e.finalize_r(facc, ffx, 1.0, 0.0)
-                else:
-                    e.hutch_fold(zbits, kk, idx, acc=fold)
-            sq, gacc, gfx = e.loss_grad(v, idx, acc=None if e.deterministic else acc)
-            if e.deterministic:
-                gacc = e.finalize_c(gacc, gfx, 1.0, 0.0)
+                sq, gacc, gfx = e.loss_grad(v, idx, acc=None if e.deterministic else acc)
+                if e.deterministic:
+                    gacc = e.finalize_c(gacc, gfx, 1.0, 0.0)
             params = C.StepParams(scale=scale, lam=lam, beta=float(config.beta), floor=float(floor),
                                   w_old=k / (k + 1), w_new=1.0 / (k + 1), hutch_scale=scale,
                                   estimating=1 if estimating else 0)

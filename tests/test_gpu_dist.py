@@ -25,7 +25,7 @@ def test_sharded_step_world1_matches_loss_and_grad_and_probe_fold():
     loss, grad, hs = D.sharded_step(op, v, batch, lam, zbits=zbits, k=k)
     loss_ref, grad_ref = F.loss_and_grad(op, v, torch.from_numpy(batch).cuda(), lam)
     assert abs(float(loss) - float(loss_ref)) / float(loss_ref) < 1e-6
-    assert O.relative_l2(grad.cpu().numpy(), grad_ref.cpu().numpy()) < 1e-6
+    assert O.relative_l2(grad.cpu().numpy(), grad_ref.cpu().numpy()) < 1e-5  # two runs of fp32 atomics: order differs
     from paper_2311_16100_b200.optim import hutchinson_sample
     hs_ref, _ = hutchinson_sample(op, z, batch, lam)
     assert O.relative_l2(hs.cpu().numpy(), hs_ref) < 1e-6

@@ -213,3 +213,37 @@ def test_device_run_deterministic_engine_and_fsc(golden):
     vol_d2, trd2 = Opt.run(cfg, stack, op=golden_op(g, deterministic=True))
     assert np.array_equal(vol_d.values, vol_d2.values)
     assert trd.fsc_history.shape == (2, 8) and np.all(np.isfinite(trd.fsc_history[:, 1:]))
+
+
+@pytest.mark.parametrize("cfgname", ["m32", "m64"])
+def test_fused_loss_grad_hutch_matches_separate_passes_and_oracle(cfgname):
+    from paper_2311_16100_b200 import synth
+    M = 32 if cfgname == "m32" else 64
+    N = 96
+    mask = O.disk_mask(M, M // 2 - 1)
+    q = synth.haar_quaternions(N, 21)
+    sh = synth.normal_shifts(N, 22)
+    ctfs = synth.physical_ctfs(N, 23)
+    pix = O.mask_pix(M, mask)
+    rng = np.random.default_rng(24)
+    x = (rng.standard_normal((N, mask.size)) + 1j * rng.standard_normal((N, mask.size))).astype(np.complex64)
+    recs = records_for(M, q, sh, ctfs)
+    e = SliceEngine(M, "tri", mask, recs, x)
+    assert e.layout == "sorted"
+    v = torch.from_numpy((rng.standard_normal(M ** 3) + 1j * rng.standard_normal(M ** 3)).astype(np.complex64)).cuda()
+    z = O.rademacher(rng, M ** 3)
+    zbits, _ = e.pack_probes(z)
+    batch = rng.permutation(N)[:64]
+    acc1 = torch.zeros(M ** 3, dtype=torch.complex64, device="cuda")
+    fold1 = torch.zeros(M ** 3, dtype=torch.float32, device="cuda")
+    sq1 = e.loss_grad_hutch(v, batch, zbits, acc1, fold1)
+    sq2, acc2, _ = e.loss_grad(v, batch)
+    fold2 = torch.zeros(M ** 3, dtype=torch.float32, device="cuda")
+    e.hutch_fold(zbits, 1, batch, acc=fold2)
+    assert abs(float(sq1) - float(sq2)) / float(sq2) < 1e-6
+    assert rel(acc1.cpu().numpy(), acc2.cpu().numpy()) < 1e-5
+    assert rel(fold1.cpu().numpy(), fold2.cpu().numpy()) < 1e-5
+    # oracle: fold = z * Re(sum_b P^* C^2 P z)  (hvp with lam = 0, scale 1)
+    oop = O.OracleOperator(M, "tri", mask, q, sh, O.ctf_table_physical(synth.ctf_param_array(ctfs), pix, M), None)
+    hz = oop.hvp(z, batch, 0.0, n_total=len(batch))
+    assert rel(fold1.cpu().numpy(), z * hz.real) < 1e-5

@@ -36,6 +36,7 @@ def tm(name, fn, reps=10):
 tm("gen_probes k=1", lambda: e.gen_probes(1, 5))
 tm("hutch_fold k=1 (tile)", lambda: e.hutch_fold(zb, 1, idx, acc=fold))
 tm("loss_grad_sorted", lambda: e.loss_grad(v, idx, acc=acc))
+tm("loss_grad_hutch_sorted", lambda: e.loss_grad_hutch(v, idx, zb, acc, fold))
 vol4 = e.precond_step(acc, v, p, dirv, fold=fold, d_avg=d_avg, d=d)
 tm("precond_step", lambda: e.precond_step(acc, v, p, dirv, fold=fold, d_avg=d_avg, d=d))
 p0 = C.StepParams(scale=8.0, lam=1e-3, beta=0.9, floor=1.0, w_old=0.5, w_new=0.5, hutch_scale=8.0, estimating=0)
