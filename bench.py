@@ -60,7 +60,8 @@ def algorithmic_bytes(M, n_mask, B):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks / throttle reasons sampled during the timed region: NVML every ~0.5 ms (the timed
+    region of a default run is only a few ms), nvidia-smi as the fallback."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -71,10 +72,29 @@ class ClockSampler:
         self.samples = []
         self._stop = threading.Event()
         self._t = None
+        self._nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nvml = (pynvml, pynvml.nvmlDeviceGetHandleByIndex(index))
+        except Exception:
+            self._nvml = None
+
+    def _sample_nvml(self):
+        nv, h = self._nvml
+        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        flag = lambda bit: "Active" if r & bit else "Not Active"  # noqa: E731
+        return [str(sm), str(mx), hex(r), flag(0x8), flag(0x40), flag(0x20), flag(0x4)]
 
     def _run(self):
         while not self._stop.is_set():
             try:
+                if self._nvml is not None:
+                    self.samples.append(self._sample_nvml())
+                    self._stop.wait(0.0005)
+                    continue
                 out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
                                       "--format=csv,noheader,nounits"], capture_output=True, text=True,
                                      timeout=5).stdout.strip()
@@ -83,6 +103,17 @@ class ClockSampler:
             except Exception:
                 pass
             self._stop.wait(0.2)
+
+    def poll_until(self, event):
+        """Sample (NVML) on the calling thread until the CUDA event has completed."""
+        if self._nvml is None:
+            return
+        while not event.query():
+            try:
+                self.samples.append(self._sample_nvml())
+            except Exception:
+                return
+            time.sleep(0.0002)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -101,7 +132,8 @@ class ClockSampler:
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 3 + i and s[3 + i] == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+                "reasons": reasons, "samples": len(self.samples),
+                "source": "nvml" if self._nvml is not None else "nvidia-smi"}
 
 
 # ---------------------------------------------------------------------------
@@ -293,6 +325,7 @@ def run_b200(args):
             else:
                 step(batches[args.warmup + i])
             s1.record()
+        clk.poll_until(ev[-1][1])  # the host is ahead: sample clocks while the GPU runs the timed steps
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
