@@ -351,7 +351,8 @@ def test_device_resident_loss_grad_matches_numpy_api():
     assert rel(g_d.cpu().numpy(), g_np) < 1e-5
 
 
-@pytest.mark.parametrize("M,B", [(8, 50), (16, 300), (36, 200), (64, 512), (128, 512), (256, 128)])
+@pytest.mark.parametrize("M,B", [(8, 50), (16, 300), (33, 64), (36, 200), (64, 512), (65, 100), (128, 512),
+                                 (256, 128)])
 def test_brick_path_processes_every_pixel_exactly_once(M, B):
     """Exact coverage: with v = 0 and x = 1 every processed pixel adds exactly 1 to sum |r|^2."""
     mask = O.disk_mask(M, M // 2 - 1)
@@ -364,7 +365,7 @@ def test_brick_path_processes_every_pixel_exactly_once(M, B):
     assert float(sq) == float(B * mask.size)
 
 
-@pytest.mark.parametrize("M,B", [(16, 40), (36, 64), (64, 256), (128, 512), (256, 64)])
+@pytest.mark.parametrize("M,B", [(16, 40), (33, 64), (36, 64), (64, 256), (65, 96), (128, 512), (256, 64)])
 def test_brick_path_matches_tile_path(M, B):
     """The brick-binned fused loss+grad (default, tri) equals the per-pixel tile kernel: every pixel
     is owned by exactly one brick (incl. clamped rim pixels, M not a multiple of the brick edge)."""
@@ -385,3 +386,29 @@ def test_brick_path_matches_tile_path(M, B):
     a1 = acc1.cpu().numpy()
     a2 = acc2.cpu().numpy()
     assert rel(a1, a2) < 5e-6
+
+
+@pytest.mark.parametrize("M,radius", [(33, 15), (32, 8), (48, 23)])
+def test_odd_sizes_and_small_masks_vs_oracle(M, radius):
+    """Odd M (centre ceil(M/2), grid.py:9-31) and mask radii below M/2-1 on the default (brick) path."""
+    B = 24
+    mask = O.disk_mask(M, radius)
+    pix = O.mask_pix(M, mask)
+    q = synth.haar_quaternions(B, M)
+    sh = synth.normal_shifts(B, M + 1)
+    ctfs = synth.physical_ctfs(B, M + 2)
+    ctab = O.ctf_table_physical(synth.ctf_param_array(ctfs), pix, M)
+    rng = np.random.default_rng(M)
+    v = rng.standard_normal(M ** 3) + 1j * rng.standard_normal(M ** 3)
+    x = rng.standard_normal((B, mask.size)) + 1j * rng.standard_normal((B, mask.size))
+    oop = O.OracleOperator(M, "tri", mask, q, sh, ctab, x)
+    op = gpu_op(M, "tri", mask, q, sh, ctfs, x)
+    assert op.engine.layout == "sorted"
+    batch = rng.permutation(B)[:17]
+    lr, gr = O.loss_and_grad(oop, v, batch, 0.01)
+    lg, gg = F.loss_and_grad(op, v, batch, 0.01)
+    assert abs(lg - lr) / lr < TOL
+    assert rel(gg, gr) < TOL
+    assert rel(op.project(v, batch), oop.project(v, batch)) < TOL
+    # nn indices stay bit-exact at odd M
+    assert np.array_equal(K.assign_nn(oop.rots[batch], pix, M), O.assign_nn(oop.rots[batch], pix, M))
