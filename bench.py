@@ -41,6 +41,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-algo1", action="store_true", help="skip the full Algorithm-1 step leg")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the cfg5 Hutchinson probe sweep leg")
     ap.add_argument("--lam", type=float, default=1e-3)
     return ap.parse_args()
 
@@ -356,6 +357,15 @@ def run_b200(args):
     algo1 = None
     if world == 1 and not args.no_algo1:
         algo1 = algo1_leg(eng, wl, B, lam, args)
+    sweep = None
+    if world == 1 and rank == 0 and not args.no_sweep and args.config == "cfg3":
+        _, n_sw, sw = hutch_sweep(argparse.Namespace(images=0, warmup=2, steps=8))
+        sweep = {"workload": "cfg5_M128_hutch_sweep", "n_images": n_sw, "unit": "probe-images/s",
+                 "kernel": "hutch_kernel (tile, bit-packed probes, Q(c,c') = k - 2 popc(z_c xor z_c'))",
+                 "k": [d["k"] for d in sw], "probe_images_per_s": [d["probe_images_per_s"] for d in sw],
+                 "ms_per_pass": [d["ms_per_pass"] for d in sw],
+                 "probe_bytes_per_probe": sw[0]["probe_bytes_per_probe"],
+                 "rel_l2_vs_exact_M32": [d["rel_l2_vs_exact_M32"] for d in sw]}
     if rank == 0:
         line = {
             "metric": "image-slices/sec (fused project+CTF+adjoint, loss+grad)",
@@ -379,6 +389,8 @@ def run_b200(args):
             line["cpu_baseline"] = cpu
         if algo1 is not None:
             line["algorithm1_step"] = algo1
+        if sweep is not None:
+            line["hutchinson_sweep"] = sweep
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -493,18 +505,14 @@ def main():
 
 
 
-def run_hutch_sweep(args):
-    """cfg5: Hutchinson probe-batching sweep at M=128 (4,096 images, physical CTF), k in {1,4,16,64,256}.
-
-    value = probe-images/s of the folded A*A z pass at k=64; the sweep adds, per k, the probe
-    throughput, probe bytes read per probe (bit-packed: M^3/8 B per probe), and the relative L2 of
-    the estimated diagonal against the exact one at M=32 (same k, 4,096 images).
-    """
+def hutch_sweep(args):
+    """cfg5: Hutchinson probe-batching sweep at M=128 (4,096 images, physical CTF), k in {1,4,16,64,256}:
+    per k the folded A*A z pass time, probe-images/s, probe bytes per probe (bit-packed: M^3/8 B) and
+    the relative L2 of the estimated diagonal against the exact one at M=32 (same k, 4,096 images)."""
     import torch
 
     from paper_2311_16100_b200 import synth
 
-    rank = int(os.environ.get("RANK", "0"))
     cfg = synth.CONFIGS["cfg5"]
     wl = synth.build_workload(cfg, seed=0, n_images=args.images or None)
     eng = wl.engine
@@ -537,6 +545,13 @@ def run_hutch_sweep(args):
         rel = float((est - exact).norm() / exact.norm())
         sweep.append({"k": k, "ms_per_pass": ms, "probe_images_per_s": k * n_img / (ms * 1e-3),
                       "probe_bytes_per_probe": eng.n_voxels / 8.0, "rel_l2_vs_exact_M32": rel})
+    return cfg, n_img, sweep
+
+
+def run_hutch_sweep(args):
+    """bench.py --config cfg5: value = probe-images/s of the folded A*A z pass at k=64, plus the sweep."""
+    rank = int(os.environ.get("RANK", "0"))
+    cfg, n_img, sweep = hutch_sweep(args)
     if rank == 0:
         k64 = next(s for s in sweep if s["k"] == 64)
         print(json.dumps({
