@@ -361,7 +361,7 @@ def run_b200(args):
     if world == 1 and rank == 0 and not args.no_sweep and args.config == "cfg3":
         _, n_sw, sw = hutch_sweep(argparse.Namespace(images=0, warmup=2, steps=8))
         sweep = {"workload": "cfg5_M128_hutch_sweep", "n_images": n_sw, "unit": "probe-images/s",
-                 "kernel": "hutch_kernel (tile, bit-packed probes, Q(c,c') = k - 2 popc(z_c xor z_c'))",
+                 "kernel": "sorted_hutch_kernel (brick-sorted, bit-packed probes in smem, Q(c,c') = k - 2 popc(z_c xor z_c'))",
                  "k": [d["k"] for d in sw], "probe_images_per_s": [d["probe_images_per_s"] for d in sw],
                  "ms_per_pass": [d["ms_per_pass"] for d in sw],
                  "probe_bytes_per_probe": sw[0]["probe_bytes_per_probe"],

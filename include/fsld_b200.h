@@ -348,6 +348,13 @@ int fsld_armijo_terms(int M, int mode, int n_mask, const int16_t* pix, const int
                       const fsld_image_rec* recs, const int32_t* idx, int B, const void* v, const void* d,
                       const void* xs, double* out3, void* scratch, size_t scratch_bytes, void* stream);
 
+/* Hutchinson probe batcher on the brick-sorted layout (tri, k <= 256): same result as
+ * fsld_hutch_fold (float32 fold += sum_p z_p * (sum_b P_b^* C_b^2 P_b z_p)), per brick work item
+ * with the probe words staged in shared memory and a shared fixed-point accumulator. */
+int fsld_hutch_fold_sorted(int M, int mode, int n_mask, const fsld_image_rec* recs, const int32_t* idx, int B,
+                           const int8_t* pc, const int32_t* seg_off, const int32_t* segs, const uint32_t* zbits,
+                           int k, float* fold, void* scratch, size_t scratch_bytes, void* stream);
+
 /* ||A d||^2 = sum_b sum_p C^2 |P d|^2 over the batch on the brick-sorted layout (tri mode):
  * a gather-only pass (no images) for the closed-form line search.  *out = device double. */
 int fsld_proj_energy_sorted(int M, int mode, int n_mask, const fsld_image_rec* recs, const int32_t* idx, int B,

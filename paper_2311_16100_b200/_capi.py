@@ -98,6 +98,7 @@ SIGNATURES = {
     "fsld_armijo_terms": (I, [I, I, I, P, P, P, P, I, P, P, P, P, P, SZ, P]),
     "fsld_armijo_select": (I, [P, P, P, P, D, D, D, I, P, P, I, P]),
     "fsld_proj_energy_sorted": (I, [I, I, I, P, P, I, P, P, P, P, P, P, SZ, P]),
+    "fsld_hutch_fold_sorted": (I, [I, I, I, P, P, I, P, P, P, P, I, P, P, SZ, P]),
     "fsld_apply_step": (I, [I64, P, P, P, P]),
 }
 

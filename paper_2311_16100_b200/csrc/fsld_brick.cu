@@ -370,6 +370,7 @@ __global__ void __launch_bounds__(1024) brick_scan_kernel(SortedArgs a) {
 
 #include "fsld_brick_main.cuh"  // the work-item kernel (kept separate: it is the tuning target)
 #include "fsld_brick_energy.cuh"
+#include "fsld_brick_hutch.cuh"
 
 cudaError_t set_phase_profile(unsigned long long* buf) {
     return cudaMemcpyToSymbol(g_phase_prof, &buf, sizeof(buf));
@@ -424,6 +425,26 @@ cudaError_t launch_sorted_energy(const SortedArgs& a, double* out, cudaStream_t 
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     return launch_reduce(a.part, g_energy_grid, out, s);
+}
+
+cudaError_t launch_sorted_hutch(const SortedArgs& a, int k, cudaStream_t s) {
+    static int grid = 0;
+    const size_t smem = sizeof(HutchSmem);
+    if (grid == 0) {
+        cudaError_t e = cudaFuncSetAttribute(sorted_hutch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        int dev = 0, sms = 0, occ = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sorted_hutch_kernel, BTHREADS, smem);
+        grid = sms * (occ > 0 ? occ : 1);
+    }
+    bin_sorted_kernel<false><<<a.B, 128, 0, s>>>(a);
+    brick_scan_kernel<<<1, 1024, 0, s>>>(a);
+    bin_sorted_kernel<true><<<a.B, 128, 0, s>>>(a);
+    sorted_hutch_kernel<<<grid, BTHREADS, smem, s>>>(a, k, (k + 31) / 32);
+    return cudaGetLastError();
 }
 
 }  // namespace fsld

@@ -1,0 +1,147 @@
+// fsld_brick_hutch.cuh -- Hutchinson probe batcher on the brick-sorted layout (included by fsld_brick.cu).
+//
+// Same estimator as hutch_kernel (fsld_hutch.cu): k bit-packed Rademacher probes folded in one pass,
+//   fold[j] += sum_p z_p[j] (sum_b P_b^* C_b^2 P_b z_p)[j]
+//            = sum_pixels C^2 w_j sum_c' w_c' Q(j, c'),   Q(c, c') = k - 2 popc(bits_c ^ bits_c'),
+// but per work item (brick, <= BC image segments) like the loss+grad kernel: the brick's probe
+// words (9^3 voxels x ceil(k/32) words) are staged in shared memory, the 8 per-pixel corner
+// contributions go to a shared int32 fixed-point accumulator with native ATOMS.ADD, and each
+// touched voxel is flushed once per item.  The contributions are bounded a priori
+// (|C| <= 1, |sum_c' w_c' Q| <= k), so the power-of-two scale is fixed per item and a single
+// pass suffices (no staging buffers).  k <= 256.
+#pragma once
+
+constexpr int kHutchMaxWords = 8;
+
+struct HutchSmem {
+    uint32_t zw[BH3 * kHutchMaxWords];  // probe words of the brick voxels, [l * words + wd]
+    int acc[BH3];
+    SegRec seg[BC];
+    int pref[BC + 1];
+    int wtot[2];
+    unsigned char bk[RB];
+    int4 item_desc;
+};
+
+__global__ void __launch_bounds__(BTHREADS, 4) sorted_hutch_kernel(SortedArgs a, int k, int words) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    HutchSmem& S = *reinterpret_cast<HutchSmem*>(smem_raw);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int M = a.M, c = a.c, nb = a.nb;
+    const float bnd = a.bnd;
+    const int n_items = a.ctl[0];
+    const float kf = (float)k;
+    for (int l = threadIdx.x; l < BH3; l += BTHREADS) S.acc[l] = 0;
+    for (;;) {
+        if (threadIdx.x == 0) {
+            const int it = atomicAdd(a.ctl + 1, 1);
+            S.item_desc = it < n_items ? a.items[it] : make_int4(-1, 0, 0, 0);
+        }
+        __syncthreads();
+        const int4 item = S.item_desc;
+        if (item.x < 0) break;
+        const int bid = item.x, pstart = item.y, nseg = item.z;
+        const int ox = -c + BT * (bid % nb), oy = -c + BT * ((bid / nb) % nb), oz = -c + BT * (bid / (nb * nb));
+        {
+            const int4* src = reinterpret_cast<const int4*>(a.pairs + pstart);
+            int4* dst = reinterpret_cast<int4*>(S.seg);
+            for (int w = threadIdx.x; w < nseg * 8; w += BTHREADS) dst[w] = __ldg(src + w);
+        }
+        if (warp < 2) {
+            const int kk = threadIdx.x;
+            const int len = kk < nseg ? __ldg(&a.pairs[pstart + kk].count) : 0;
+            int incl = len;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += t;
+            }
+            S.pref[kk] = incl - len;
+            if (lane == 31) S.wtot[warp] = incl;
+        }
+        for (int q = threadIdx.x; q < BH3 * words; q += BTHREADS) {
+            const int l = q / words, wd = q - l * words;
+            const int kx = ox + l % BH, ky = oy + (l / BH) % BH, kz = oz + l / (BH * BH);
+            const bool in = kx < M - c && ky < M - c && kz < M - c;
+            S.zw[q] = in ? __ldg(a.zbits + (size_t)lin_index(kx, ky, kz, M, c) * words + wd) : 0u;
+        }
+        __syncthreads();
+        if (threadIdx.x < nseg) {
+            const int kk = threadIdx.x;
+            const int p = S.pref[kk] + (kk >= 32 ? S.wtot[0] : 0);
+            S.pref[kk] = p;
+            S.seg[kk].gofs -= p;
+        }
+        if (threadIdx.x == 0) S.pref[nseg] = S.wtot[0] + (nseg > 32 ? S.wtot[1] : 0);
+        __syncthreads();
+        const int total = S.pref[nseg];
+        // |C^2 w_c S_c| <= k; <= 12 contributions per voxel per image segment -> |sum| < 2^31
+        const float sc = exp2f(floorf(log2f(fminf(4194303.0f, 178956970.0f / (float)nseg) / kf)));
+        for (int r0 = 0; r0 < total; r0 += RB) {
+            const int rn = min(RB, total - r0);
+            {
+                const int kk = threadIdx.x / SEG_T, q = threadIdx.x % SEG_T;
+                if (kk < nseg) {
+                    const int e1 = min(S.pref[kk + 1], r0 + rn) - r0;
+                    for (int e = max(S.pref[kk], r0) - r0 + q; e < e1; e += SEG_T) S.bk[e] = (unsigned char)kk;
+                }
+            }
+            __syncthreads();
+            for (int e = threadIdx.x; e < rn; e += BTHREADS) {
+                const SegRec& R = S.seg[S.bk[e]];
+                const char2 kq = a.pc[R.gofs + (r0 + e)];
+                const int px = kq.x, py = kq.y;
+                float cx, cy, cz, fx, fy, fz;
+                floor_corner((float)px, (float)py, R.frame, bnd, cx, cy, cz, fx, fy, fz);
+                const int l0 = (((int)fz - oz) * BH + ((int)fy - oy)) * BH + ((int)fx - ox);
+                const float wx = cx - fx, wy = cy - fy, wz = cz - fz;
+                const float ax = 1.f - wx, ay = 1.f - wy, az = 1.f - wz;
+                const float zy00 = az * ay, zy10 = az * wy, zy01 = wz * ay, zy11 = wz * wy;
+                const float w[8] = {zy00 * ax, zy00 * wx, zy10 * ax, zy10 * wx, zy01 * ax, zy01 * wx, zy11 * ax, zy11 * wx};
+                const int off8[8] = {0, 1, BH, BH + 1, BH * BH, BH * BH + 1, BH * BH + BH, BH * BH + BH + 1};
+                const float ct = seg_ctf(R, px, py);
+                const float c2v = ct * ct * sc;
+                int d[8][8];
+#pragma unroll
+                for (int p = 0; p < 8; ++p)
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) d[p][q] = 0;
+                for (int wd = 0; wd < words; ++wd) {
+                    uint32_t z[8];
+#pragma unroll
+                    for (int p = 0; p < 8; ++p) z[p] = S.zw[(l0 + off8[p]) * words + wd];
+#pragma unroll
+                    for (int p = 0; p < 8; ++p)
+#pragma unroll
+                        for (int q = p + 1; q < 8; ++q) d[p][q] += __popc(z[p] ^ z[q]);
+                }
+                float wsum = 0.f;
+#pragma unroll
+                for (int p = 0; p < 8; ++p) wsum += w[p];
+#pragma unroll
+                for (int p = 0; p < 8; ++p) {
+                    float s = 0.f;
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        if (q == p) continue;
+                        s = fmaf(w[q], (float)(p < q ? d[p][q] : d[q][p]), s);
+                    }
+                    const float val = c2v * w[p] * fmaf(-2.0f, s, kf * wsum);
+                    atomicAdd(S.acc + l0 + off8[p], __float_as_int(val + kMagic) - kMagicBits);
+                }
+            }
+            __syncthreads();
+        }
+        // flush: one reduction per touched voxel, accumulator re-zeroed for the next item
+        const float inv = 1.0f / sc;
+        for (int l = threadIdx.x; l < BH3; l += BTHREADS) {
+            const int q = S.acc[l];
+            if (q == 0) continue;
+            S.acc[l] = 0;
+            const int kx = ox + l % BH, ky = oy + (l / BH) % BH, kz = oz + l / (BH * BH);
+            if (kx >= M - c || ky >= M - c || kz >= M - c) continue;
+            atomicAdd(a.fold + lin_index(kx, ky, kz, M, c), (float)q * inv);
+        }
+        __syncthreads();
+    }
+}

@@ -477,6 +477,20 @@ extern "C" int fsld_armijo_select(const double* sq, const double* rq, const doub
                                           reinterpret_cast<cudaStream_t>(stream)));
 }
 
+extern "C" int fsld_hutch_fold_sorted(int M, int mode, int n_mask, const fsld_image_rec* recs, const int32_t* idx,
+                                      int B, const int8_t* pc, const int32_t* seg_off, const int32_t* segs,
+                                      const uint32_t* zbits, int k, float* fold, void* scratch, size_t scratch_bytes,
+                                      void* stream) {
+    if (!geom_ok(M, mode, n_mask, B) || M > 256 || mode != FSLD_MODE_TRI || k < 1 || k > 256) return FSLD_EINVAL;
+    if (!recs || !pc || !seg_off || !segs || !zbits || !fold || !scratch) return FSLD_EINVAL;
+    const ScratchLayout L = scratch_layout(M, n_mask, B);
+    if (scratch_bytes < L.total) return FSLD_EINVAL;
+    SortedArgs b = make_sorted(L, M, n_mask, B, recs, idx, nullptr, nullptr, pc, seg_off, segs, nullptr, scratch);
+    b.zbits = zbits;
+    b.fold = fold;
+    return status_of(launch_sorted_hutch(b, k, reinterpret_cast<cudaStream_t>(stream)));
+}
+
 extern "C" int fsld_proj_energy_sorted(int M, int mode, int n_mask, const fsld_image_rec* recs, const int32_t* idx,
                                        int B, const void* d, const int8_t* pc, const int32_t* seg_off,
                                        const int32_t* segs, double* out, void* scratch, size_t scratch_bytes,

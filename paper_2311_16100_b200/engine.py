@@ -369,6 +369,15 @@ class SliceEngine:
         idx = self.idx_tensor(idx)
         B = idx.numel()
         acc = self.new_racc() if acc is None else acc
+        if (self.layout == "sorted" and self.mode == "tri" and not self.deterministic and
+                not (self.flags & C.TILE_PATH) and 1 <= k <= 256):
+            scr = self.scratch(B)
+            C.check(lib.fsld_hutch_fold_sorted(self.M, self.mode_id, self.n_mask, ctypes_ptr(self.recs),
+                                               ctypes_ptr(idx), B, ctypes_ptr(self.pc), ctypes_ptr(self.seg_off),
+                                               ctypes_ptr(self.segs), ctypes_ptr(zbits), int(k), ctypes_ptr(acc),
+                                               ctypes_ptr(scr), scr.numel() * 8, _stream()),
+                    "fsld_hutch_fold_sorted")
+            return acc, fx
         if self.deterministic and fx is None:
             fx = self.fixed_scale(None, HITS_PER_IMAGE * (fx_batch or B) * k, 1.0)
         C.check(lib.fsld_hutch_fold(self.M, self.mode_id, self.n_mask, ctypes_ptr(self.pix),

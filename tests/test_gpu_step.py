@@ -247,3 +247,22 @@ def test_fused_loss_grad_hutch_matches_separate_passes_and_oracle(cfgname):
     oop = O.OracleOperator(M, "tri", mask, q, sh, O.ctf_table_physical(synth.ctf_param_array(ctfs), pix, M), None)
     hz = oop.hvp(z, batch, 0.0, n_total=len(batch))
     assert rel(fold1.cpu().numpy(), z * hz.real) < 1e-5
+
+
+@pytest.mark.parametrize("k", [1, 5, 37, 64, 256])
+def test_brick_probe_batcher_matches_tile_batcher(k):
+    from paper_2311_16100_b200 import synth
+    M, N = 64, 128
+    mask = O.disk_mask(M, M // 2 - 1)
+    q = synth.haar_quaternions(N, 31)
+    sh = synth.normal_shifts(N, 32)
+    ctfs = synth.physical_ctfs(N, 33)
+    recs = records_for(M, q, sh, ctfs)
+    brick = SliceEngine(M, "tri", mask, recs)
+    tile = SliceEngine(M, "tri", mask, recs, tile_path=True)
+    assert brick.layout == "sorted"
+    zb = brick.gen_probes(k, 7 + k)
+    batch = np.random.default_rng(k).permutation(N)[:100]
+    f1, _ = brick.hutch_fold(zb, k, batch)
+    f2, _ = tile.hutch_fold(zb, k, batch)
+    assert rel(f1.cpu().numpy(), f2.cpu().numpy()) < 1e-5
