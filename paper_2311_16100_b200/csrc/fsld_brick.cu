@@ -221,43 +221,43 @@ __device__ __forceinline__ unsigned long long turns_of_radians(double x) {
     return frac_fixed64(hi, lo);
 }
 
-// The per-image part of a SegRec (everything except gofs / count / start),
+// The per-image part of a SegRec (everything except gofs / count / start / row),
 // from the 128-byte record (fsld_common.cuh ctf_value / shift_phase restated):
 //   gamma = g0 k2 + g1 c2 + g2 s2 + g3 k2^2 with c2 = kx^2 - ky^2, s2 = 2 kx ky;
 //   the kernel multiplies non-negative monomials (k2, c2 + 2^15, s2 + 2^16, k2^2),
 //   so the offsets go into the constant term.  Shift: t = (s0 kx + s1 ky) / 2 turns,
 //   with kx + 128, ky + 128.
-__device__ void seg_template(const fsld_image_rec& R, SegRec& T) {
-    for (int q = 0; q < 6; ++q) T.frame[q] = (float)R.rot[q];
-    unsigned long long g[4] = {0, 0, 0, 0}, gconst = 0, s[2] = {0, 0}, sconst = 0;
-    T.wsin = 0.f;
-    T.wcos = -1.f;  // no CTF: -(0 sin 0 + (-1) cos 0) = 1
-    T.envl = 0.f;
-    if (R.flags & FSLD_REC_CTF) {
-        for (int q = 0; q < 4; ++q) g[q] = turns_of_radians(R.gamma[q]);
-        gconst = turns_of_radians(-32768.0 * R.gamma[1]) + turns_of_radians(-65536.0 * R.gamma[2]);
-        T.wsin = R.wsin;
-        T.wcos = R.wcos;
-        T.envl = (float)(R.env * 1.4426950408889634);
+// Computed by one warp, one fixed-point conversion per lane (the conversions are fp64 chains).
+__device__ void seg_template_warp(const fsld_image_rec* __restrict__ rp, SegRec& T) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t flags = rp->flags;
+    const bool ctf = (flags & FSLD_REC_CTF) != 0, shift = (flags & FSLD_REC_SHIFT) != 0;
+    unsigned long long u = 0;
+    if (lane < 6) T.frame[lane] = (float)rp->rot[lane];
+    else if (lane < 10) u = ctf ? turns_of_radians(rp->gamma[lane - 6]) : 0ull;
+    else if (lane == 10) u = ctf ? turns_of_radians(-32768.0 * rp->gamma[1]) : 0ull;
+    else if (lane == 11) u = ctf ? turns_of_radians(-65536.0 * rp->gamma[2]) : 0ull;
+    else if (lane < 14) u = shift ? frac_fixed64(0.5 * rp->shift[lane - 12], 0.0) : 0ull;
+    else if (lane < 16) u = shift ? frac_fixed64(-64.0 * rp->shift[lane - 14], 0.0) : 0ull;
+    const unsigned long long g11 = __shfl_sync(0xffffffffu, u, 11);
+    const unsigned long long s15 = __shfl_sync(0xffffffffu, u, 15);
+    if (lane >= 6 && lane < 10) {
+        T.glo[lane - 6] = (uint32_t)u;
+        T.ghi[lane - 6] = (uint32_t)(u >> 32);
+    } else if (lane == 10) {
+        T.gc = (uint32_t)((u + g11 + 0x80000000ull) >> 32);  // constants: nearest 2^-32 turn
+    } else if (lane == 12 || lane == 13) {
+        T.slo[lane - 12] = (uint32_t)u;
+        T.shi[lane - 12] = (uint32_t)(u >> 32);
+    } else if (lane == 14) {
+        T.sc = (uint32_t)((u + s15 + 0x80000000ull) >> 32);
+    } else if (lane == 16) {
+        T.wsin = ctf ? rp->wsin : 0.f;
+        T.wcos = ctf ? rp->wcos : -1.f;  // no CTF: -(0 sin 0 + (-1) cos 0) = 1
+        T.envl = ctf ? (float)(rp->env * 1.4426950408889634) : 0.f;
+    } else if (lane >= 20 && lane < 24) {
+        T.pad[lane - 20] = 0;
     }
-    if (R.flags & FSLD_REC_SHIFT) {
-        for (int q = 0; q < 2; ++q) {
-            s[q] = frac_fixed64(0.5 * R.shift[q], 0.0);
-            sconst += frac_fixed64(-64.0 * R.shift[q], 0.0);
-        }
-    }
-    for (int q = 0; q < 4; ++q) {
-        T.glo[q] = (uint32_t)g[q];
-        T.ghi[q] = (uint32_t)(g[q] >> 32);
-    }
-    for (int q = 0; q < 2; ++q) {
-        T.slo[q] = (uint32_t)s[q];
-        T.shi[q] = (uint32_t)(s[q] >> 32);
-    }
-    // constants: round to the nearest 2^-32 turn
-    T.gc = (uint32_t)((gconst + 0x80000000ull) >> 32);
-    T.sc = (uint32_t)((sconst + 0x80000000ull) >> 32);
-    T.pad[0] = T.pad[1] = T.pad[2] = T.pad[3] = 0;
 }
 
 template <bool FILL>
@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(128) bin_sorted_kernel(SortedArgs a) {
     const int s0 = a.seg_off[row], s1 = a.seg_off[row + 1];
     if (FILL) {
         __shared__ SegRec T;
-        if (threadIdx.x == 0) seg_template(a.recs[row], T);
+        if (threadIdx.x < 32) seg_template_warp(a.recs + row, T);
         __syncthreads();
         for (int sidx = s0 + threadIdx.x; sidx < s1; sidx += blockDim.x) {
             const int2 seg = a.segs[sidx];
