@@ -31,3 +31,4 @@ def test_c_program_drives_the_abi():
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "capi_demo" in r.stdout
+    print(r.stdout.strip())
