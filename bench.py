@@ -229,9 +229,17 @@ def run_b200(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # FSLD_BENCH_SINGLE_DEVICE=1 (functional check of the multi-rank code path on a 1-GPU box: all
+    # ranks on cuda:0, host-side gloo exchange; never a reported number)
+    single = os.environ.get("FSLD_BENCH_SINGLE_DEVICE") == "1"
+    if single:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if single:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = synth.CONFIGS[args.config]
     wl = synth.build_workload(cfg, seed=0, n_images=args.images or None)
     # cfg1/cfg2 are full-dataset passes in BASELINE; the timed step uses 1024-image batches
