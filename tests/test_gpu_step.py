@@ -266,3 +266,21 @@ def test_brick_probe_batcher_matches_tile_batcher(k):
     f1, _ = brick.hutch_fold(zb, k, batch)
     f2, _ = tile.hutch_fold(zb, k, batch)
     assert rel(f1.cpu().numpy(), f2.cpu().numpy()) < 1e-5
+
+
+@pytest.mark.parametrize("name,seed", [("dataset_m16_nn.npz", 3), ("dataset_m16_tri.npz", 4)])
+def test_device_run_ragged_last_batch_vs_oracle(golden, name, seed):
+    """N = 96 with batch_size 28: every epoch ends with a 12-image batch (scale N/12, optim.py:183)."""
+    from harness import sgd_harness
+    g = golden(name)
+    stack = golden_stack(g, seed)
+    lam = float(g["lam"])
+    _, oop = _oracle_op(g)
+    rec, v_ref, _ = sgd_harness(O, oop, int(g["M"]) ** 3, oop.n_images, lam, float(g["alpha"]), 28, seed, 8)
+    cfg = Opt.OptimConfig(lam=lam, batch_size=28, epochs=2, seed=seed, mode=str(g["mode"]))
+    vol, tr = Opt.run(cfg, stack)
+    assert tr.armijo_steps == 8
+    assert np.array_equal(np.array(tr.accepted_etas), rec[:, 1])
+    assert np.array_equal(np.array(tr.step_backtracks), rec[:, 3].astype(int))
+    assert np.max(np.abs(np.array(tr.step_f0) - rec[:, 0]) / np.abs(rec[:, 0])) < 1e-4
+    assert rel(vol.values, v_ref) < 1e-4

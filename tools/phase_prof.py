@@ -27,7 +27,7 @@ torch.cuda.synchronize()
 lib.fsld_debug_phase_profile(None)
 b = buf.cpu().numpy().astype(np.float64)
 items = b[8]
-names = ["claim", "segs+vbrick", "recs+bk", "pass1", "pass2", "-", "-", "flush"]
+names = ["setup", "bk+round", "pass1", "pass2", "-", "-", "-", "flush"]  # PHASE_MARK ids of fsld_brick_main.cuh
 tot = b[:8].sum()
 print(f"items/launch {items / reps:.0f}  cycles/item {tot / items:.0f}")
 for i, nm in enumerate(names):
