@@ -436,7 +436,7 @@ def algo1_leg(eng, wl, B, lam, args):
         p = C.StepParams(scale=scale, lam=lam, beta=0.9, floor=alpha, w_old=k / (k + 1), w_new=1.0 / (k + 1),
                          hutch_scale=scale, estimating=1)
         vol4 = eng.precond_step(acc, v, p, dirv, fold=fold, d_avg=d_avg, d=d)
-        qq = eng.proj_energy(dirv, idx)
+        qq = eng.proj_energy(dirv, idx, reuse_bins=True)
         eng.armijo_select(sq, vol4[4:5], qq, vol4, scale, lam, 0.5, st, hist)
         eng.apply_step(v, dirv, st)
 

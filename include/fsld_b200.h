@@ -55,6 +55,8 @@ extern "C" {
 /* flags */
 #define FSLD_DETERMINISTIC 1u /* accumulate in int64 fixed point: bitwise repeatable */
 #define FSLD_TILE_PATH 2u     /* force the per-pixel tile kernel (global atomics) instead of bricks */
+#define FSLD_REUSE_BINS 4u    /* reuse the brick work items the previous sorted call on the same scratch
+                                 built for the same (recs, idx, B): skips the per-step binning */
 
 /* fsld_image_rec.flags */
 #define FSLD_REC_CTF 1u
@@ -356,10 +358,13 @@ int fsld_hutch_fold_sorted(int M, int mode, int n_mask, const fsld_image_rec* re
                            int k, float* fold, void* scratch, size_t scratch_bytes, void* stream);
 
 /* ||A d||^2 = sum_b sum_p C^2 |P d|^2 over the batch on the brick-sorted layout (tri mode):
- * a gather-only pass (no images) for the closed-form line search.  *out = device double. */
+ * a gather-only pass (no images) for the closed-form line search.  *out = device double.
+ * flags: 0 or FSLD_REUSE_BINS (the loss+grad call of the same step on this scratch, same recs /
+ * idx pointer / B, with idx unchanged since: the binning is skipped; EINVAL if the host-side
+ * record of the scratch's last binning does not match). */
 int fsld_proj_energy_sorted(int M, int mode, int n_mask, const fsld_image_rec* recs, const int32_t* idx, int B,
                             const void* d, const int8_t* pc, const int32_t* seg_off, const int32_t* segs,
-                            double* out, void* scratch, size_t scratch_bytes, void* stream);
+                            double* out, unsigned flags, void* scratch, size_t scratch_bytes, void* stream);
 
 /* Closed-form Armijo backtracking (optim.py:269-306) on the device, one thread:
  * sq = the step's loss-pass sum |r|^2 (f0), rq = Re<r, A d>, qq = ||A d||^2, vol = the first four

@@ -22,6 +22,7 @@ MODE_NN = 0
 MODE_TRI = 1
 DETERMINISTIC = 1
 TILE_PATH = 2
+REUSE_BINS = 4
 REC_CTF = 1
 REC_SHIFT = 2
 ABI_VERSION = 1
@@ -97,7 +98,7 @@ SIGNATURES = {
     "fsld_precond_step": (I, [I64, P, P, P, P, P, P, P, P, P, P, P, P, SZ, P]),
     "fsld_armijo_terms": (I, [I, I, I, P, P, P, P, I, P, P, P, P, P, SZ, P]),
     "fsld_armijo_select": (I, [P, P, P, P, D, D, D, I, P, P, I, P]),
-    "fsld_proj_energy_sorted": (I, [I, I, I, P, P, I, P, P, P, P, P, P, SZ, P]),
+    "fsld_proj_energy_sorted": (I, [I, I, I, P, P, I, P, P, P, P, P, U, P, SZ, P]),
     "fsld_hutch_fold_sorted": (I, [I, I, I, P, P, I, P, P, P, P, I, P, P, SZ, P]),
     "fsld_apply_step": (I, [I64, P, P, P, P]),
 }

@@ -406,7 +406,7 @@ cudaError_t launch_sorted_loss_grad(const SortedArgs& a, double* sq_out, cudaStr
 
 static int g_energy_grid = 0;
 
-cudaError_t launch_sorted_energy(const SortedArgs& a, double* out, cudaStream_t s) {
+cudaError_t launch_sorted_energy(const SortedArgs& a, double* out, bool rebin, cudaStream_t s) {
     const size_t smem = sizeof(EnergySmem);
     if (g_energy_grid == 0) {
         cudaError_t e = cudaFuncSetAttribute(sorted_energy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -418,9 +418,14 @@ cudaError_t launch_sorted_energy(const SortedArgs& a, double* out, cudaStream_t 
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sorted_energy_kernel, BTHREADS, smem);
         g_energy_grid = sms * (occ > 0 ? occ : 1);
     }
-    bin_sorted_kernel<false><<<a.B, 128, 0, s>>>(a);
-    brick_scan_kernel<<<1, 1024, 0, s>>>(a);
-    bin_sorted_kernel<true><<<a.B, 128, 0, s>>>(a);
+    if (rebin) {
+        bin_sorted_kernel<false><<<a.B, 128, 0, s>>>(a);
+        brick_scan_kernel<<<1, 1024, 0, s>>>(a);
+        bin_sorted_kernel<true><<<a.B, 128, 0, s>>>(a);
+    } else {  // the work items of the previous sorted call on this scratch: only re-arm the claim counter
+        cudaError_t e = cudaMemsetAsync(a.ctl + 1, 0, sizeof(int), s);
+        if (e != cudaSuccess) return e;
+    }
     sorted_energy_kernel<<<g_energy_grid, BTHREADS, smem, s>>>(a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;

@@ -43,6 +43,34 @@ SliceArgs make_args(int M, int n_mask, const int16_t* pix, const fsld_image_rec*
     return a;
 }
 
+// Host-side record of the batch whose work items the last sorted call left in a scratch buffer
+// (FSLD_REUSE_BINS check).  Not thread-safe across host threads sharing one scratch buffer.
+struct BinKey {
+    const void* scratch;
+    const int32_t* idx;
+    const fsld_image_rec* recs;
+    int M, n_mask, B;
+};
+BinKey g_last_bins[8];
+int g_last_bins_next = 0;
+
+void note_bins(const void* scratch, const int32_t* idx, const fsld_image_rec* recs, int M, int n_mask, int B) {
+    for (BinKey& k : g_last_bins)
+        if (k.scratch == scratch) {
+            k = BinKey{scratch, idx, recs, M, n_mask, B};
+            return;
+        }
+    g_last_bins[g_last_bins_next] = BinKey{scratch, idx, recs, M, n_mask, B};
+    g_last_bins_next = (g_last_bins_next + 1) % 8;
+}
+
+bool bins_match(const void* scratch, const int32_t* idx, const fsld_image_rec* recs, int M, int n_mask, int B) {
+    for (const BinKey& k : g_last_bins)
+        if (k.scratch == scratch)
+            return k.idx == idx && k.recs == recs && k.M == M && k.n_mask == n_mask && k.B == B;
+    return false;
+}
+
 SortedArgs make_sorted(const ScratchLayout& L, int M, int n_mask, int B, const fsld_image_rec* recs,
                        const int32_t* idx, const void* v, const void* xs, const int8_t* pc, const int32_t* seg_off,
                        const int32_t* segs, void* grad_acc, void* scratch) {
@@ -316,6 +344,7 @@ int fsld_loss_grad_sorted(int M, int mode, int n_mask, const fsld_image_rec* rec
     const ScratchLayout L = scratch_layout(M, n_mask, B);
     if (scratch_bytes < L.total) return FSLD_EINVAL;
     const SortedArgs b = make_sorted(L, M, n_mask, B, recs, idx, v, xs, pc, seg_off, segs, grad_acc, scratch);
+    note_bins(scratch, idx, recs, M, n_mask, B);
     return status_of(launch_sorted_loss_grad(b, sq_out, reinterpret_cast<cudaStream_t>(stream)));
 }
 
@@ -332,6 +361,7 @@ int fsld_loss_grad_hutch_sorted(int M, int mode, int n_mask, const fsld_image_re
     SortedArgs b = make_sorted(L, M, n_mask, B, recs, idx, v, xs, pc, seg_off, segs, grad_acc, scratch);
     b.zbits = zbits;
     b.fold = fold;
+    note_bins(scratch, idx, recs, M, n_mask, B);
     return status_of(launch_sorted_loss_grad(b, sq_out, reinterpret_cast<cudaStream_t>(stream)));
 }
 
@@ -488,19 +518,24 @@ extern "C" int fsld_hutch_fold_sorted(int M, int mode, int n_mask, const fsld_im
     SortedArgs b = make_sorted(L, M, n_mask, B, recs, idx, nullptr, nullptr, pc, seg_off, segs, nullptr, scratch);
     b.zbits = zbits;
     b.fold = fold;
+    note_bins(scratch, idx, recs, M, n_mask, B);
     return status_of(launch_sorted_hutch(b, k, reinterpret_cast<cudaStream_t>(stream)));
 }
 
 extern "C" int fsld_proj_energy_sorted(int M, int mode, int n_mask, const fsld_image_rec* recs, const int32_t* idx,
                                        int B, const void* d, const int8_t* pc, const int32_t* seg_off,
-                                       const int32_t* segs, double* out, void* scratch, size_t scratch_bytes,
-                                       void* stream) {
+                                       const int32_t* segs, double* out, unsigned flags, void* scratch,
+                                       size_t scratch_bytes, void* stream) {
     if (!geom_ok(M, mode, n_mask, B) || M > 256 || mode != FSLD_MODE_TRI) return FSLD_EINVAL;
     if (!recs || !d || !pc || !seg_off || !segs || !out || !scratch) return FSLD_EINVAL;
+    if (flags & ~FSLD_REUSE_BINS) return FSLD_EINVAL;
     const ScratchLayout L = scratch_layout(M, n_mask, B);
     if (scratch_bytes < L.total) return FSLD_EINVAL;
+    const bool reuse = (flags & FSLD_REUSE_BINS) != 0;
+    if (reuse && !bins_match(scratch, idx, recs, M, n_mask, B)) return FSLD_EINVAL;
     const SortedArgs b = make_sorted(L, M, n_mask, B, recs, idx, d, nullptr, pc, seg_off, segs, nullptr, scratch);
-    return status_of(launch_sorted_energy(b, out, reinterpret_cast<cudaStream_t>(stream)));
+    if (!reuse) note_bins(scratch, idx, recs, M, n_mask, B);
+    return status_of(launch_sorted_energy(b, out, !reuse, reinterpret_cast<cudaStream_t>(stream)));
 }
 
 extern "C" int fsld_apply_step(int64_t nvox, void* v, const void* dir, const fsld_armijo_state* st, void* stream) {

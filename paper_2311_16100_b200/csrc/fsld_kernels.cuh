@@ -125,7 +125,7 @@ cudaError_t launch_precond_step(int64_t nvox, float2* acc, const float2* v, floa
 cudaError_t launch_armijo_select(const double* sq, const double* rq, const double* qq, const double* vol,
                                  double scale, double lam, double c, int max_halvings, fsld_armijo_state* st,
                                  double* hist, int hist_cap, cudaStream_t s);
-cudaError_t launch_sorted_energy(const SortedArgs& a, double* out, cudaStream_t s);
+cudaError_t launch_sorted_energy(const SortedArgs& a, double* out, bool rebin, cudaStream_t s);
 cudaError_t launch_sorted_hutch(const SortedArgs& a, int k, cudaStream_t s);
 cudaError_t launch_apply_step(int64_t nvox, float2* v, const float2* dir, const fsld_armijo_state* st,
                               cudaStream_t s);

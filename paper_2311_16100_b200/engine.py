@@ -223,15 +223,19 @@ class SliceEngine:
                 "fsld_loss_grad")
         return sq, acc, fx
 
+    @property
+    def brick_path(self) -> bool:
+        """Whether loss_grad / loss_grad_hutch / proj_energy run the brick-sorted kernels."""
+        return (self.layout == "sorted" and self.mode == "tri" and not self.deterministic and
+                not (self.flags & C.TILE_PATH) and self.M <= 256)
+
     def loss_grad_hutch(self, v, idx, zbits, acc, fold):
         """loss_grad + the k = 1 Hutchinson fold of the same batch (acc, fold accumulate in place).
 
         One fused brick-path pass when available (tri, brick-sorted layout, not deterministic);
         otherwise fsld_hutch_fold + loss_grad.  Returns sq (device double)."""
         lib = C.load()
-        fused = self.layout == "sorted" and self.mode == "tri" and not self.deterministic and \
-            not (self.flags & C.TILE_PATH) and self.M <= 256
-        if not fused:
+        if not self.brick_path:
             self.hutch_fold(zbits, 1, idx, acc=fold)
             sq, _, _ = self.loss_grad(v, idx, acc=acc)
             return sq
@@ -495,9 +499,11 @@ class SliceEngine:
         st["eta"] = eta0
         return torch.from_numpy(st.view(np.uint8).copy()).to(self.dev)
 
-    def proj_energy(self, d, idx, out=None) -> torch.Tensor:
+    def proj_energy(self, d, idx, out=None, reuse_bins: bool = False) -> torch.Tensor:
         """||A d||^2 = sum_b sum_p C^2 |P d|^2 over the batch (device double): the brick-sorted
-        gather-only kernel when available, else the tile kernel's third line-search term."""
+        gather-only kernel when available, else the tile kernel's third line-search term.
+        reuse_bins: idx is the same (unchanged) device tensor the preceding sorted loss+grad call of
+        this step used, so its work items are reused (FSLD_REUSE_BINS)."""
         lib = C.load()
         d = self._vol(d)
         idx = self.idx_tensor(idx)
@@ -508,8 +514,8 @@ class SliceEngine:
             C.check(lib.fsld_proj_energy_sorted(self.M, self.mode_id, self.n_mask, ctypes_ptr(self.recs),
                                                 ctypes_ptr(idx), B, ctypes_ptr(d), ctypes_ptr(self.pc),
                                                 ctypes_ptr(self.seg_off), ctypes_ptr(self.segs), ctypes_ptr(out),
-                                                ctypes_ptr(scr), scr.numel() * 8, _stream()),
-                    "fsld_proj_energy_sorted")
+                                                C.REUSE_BINS if reuse_bins else 0, ctypes_ptr(scr),
+                                                scr.numel() * 8, _stream()), "fsld_proj_energy_sorted")
             return out
         zero = getattr(self, "_zero_vol", None)
         if zero is None:

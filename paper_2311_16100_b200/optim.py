@@ -386,7 +386,7 @@ def run(config: OptimConfig, stack, v0=None, reference=None, exact_diag_vec=None
                                   dhat_fixed=dhat_fixed, dhat_out=dhat_last if last else None)
             if estimating:
                 k += 1
-            qq = e.proj_energy(dirv, idx)
+            qq = e.proj_energy(dirv, idx, reuse_bins=e.brick_path)  # same batch, same scratch
             e.armijo_select(sq, vol4[4:5], qq, vol4, scale, lam, float(config.c), st, hist, MAX_HALVINGS)
             e.apply_step(v, dirv, st)
         # ---- epoch end: the only host synchronisation of the epoch

@@ -156,8 +156,12 @@ def test_step_entry_points_reject_bad_arguments_without_gpu():
     assert lib.fsld_armijo_select(1, 1, 1, 1, 1.0, -0.1, 0.5, 60, 1, 0, 0, 0) == C.FSLD_EINVAL
     assert lib.fsld_armijo_select(1, 1, 1, 1, 0.0, 0.1, 0.5, 60, 1, 0, 0, 0) == C.FSLD_EINVAL
     # brick energy pass: tri only, M <= 256
-    assert lib.fsld_proj_energy_sorted(32, C.MODE_NN, 749, 1, 1, 4, 1, 1, 1, 1, 1, 1, 1 << 24, 0) == C.FSLD_EINVAL
-    assert lib.fsld_proj_energy_sorted(512, C.MODE_TRI, 749, 1, 1, 4, 1, 1, 1, 1, 1, 1, 1 << 24, 0) == C.FSLD_EINVAL
+    assert lib.fsld_proj_energy_sorted(32, C.MODE_NN, 749, 1, 1, 4, 1, 1, 1, 1, 1, 0, 1, 1 << 24, 0) == C.FSLD_EINVAL
+    assert lib.fsld_proj_energy_sorted(512, C.MODE_TRI, 749, 1, 1, 4, 1, 1, 1, 1, 1, 0, 1, 1 << 24, 0) == C.FSLD_EINVAL
+    # reuse of a binning that was never made on this scratch / unknown flags
+    assert lib.fsld_proj_energy_sorted(32, C.MODE_TRI, 749, 1, 1, 4, 1, 1, 1, 1, 1, C.REUSE_BINS, 1, 1 << 24,
+                                       0) == C.FSLD_EINVAL
+    assert lib.fsld_proj_energy_sorted(32, C.MODE_TRI, 749, 1, 1, 4, 1, 1, 1, 1, 1, 64, 1, 1 << 24, 0) == C.FSLD_EINVAL
     assert lib.fsld_apply_step(0, 1, 1, 1, 0) == C.FSLD_EINVAL
 
 

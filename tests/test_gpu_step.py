@@ -70,6 +70,13 @@ def test_closed_form_line_search_matches_batch_loss(golden, name, layout):
     vol4 = e.precond_step(acc, v, p, dirv, dhat_fixed=dh).cpu().numpy()
     t3 = e.armijo_terms(v, dirv, batch).cpu().numpy()
     qq = float(e.proj_energy(dirv, batch).item())
+    if e.brick_path:  # reusing the loss+grad call's work items gives the same energy
+        bt = e.idx_tensor(batch)
+        e.loss_grad(v, bt)
+        qq2 = float(e.proj_energy(dirv, bt, reuse_bins=True).item())
+        assert abs(qq2 - qq) / qq < 1e-6
+        with pytest.raises(ValueError):  # a different batch tensor was never binned on this scratch
+            e.proj_energy(dirv, e.idx_tensor(batch[::-1].copy()), reuse_bins=True)
     sq = float(sq.item())
     assert abs(t3[0] - sq) / sq < 1e-6
     assert abs(t3[1] - vol4[4]) / abs(t3[1]) < 1e-5  # Re<r, A d> from the pixels == Re<A^* r, d> from acc
