@@ -253,8 +253,12 @@ def run_b200(args):
     scale = n_total / (B * world)
 
     v = torch.from_numpy((wl.v_true * 0.9).astype(np.complex64)).to(dev)
-    packed = torch.zeros(2 * M ** 3 + 2, dtype=torch.float32, device=dev)
-    acc = packed[:2 * M ** 3].view(torch.complex64)
+    acc = torch.zeros(M ** 3, dtype=torch.complex64, device=dev)
+    # N > 1: the all-reduce moves only the voxels a scatter can reach (grid.touched_ball, ~54 % at M=128)
+    from paper_2311_16100_b200.grid import touched_ball
+    ball = torch.from_numpy(touched_ball(M, M // 2 - 1)).to(dev)
+    nball = int(ball.numel())
+    packed = torch.zeros(2 * nball + 2, dtype=torch.float32, device=dev)
     grad = torch.empty(M ** 3, dtype=torch.complex64, device=dev)
     sq = torch.empty(1, dtype=torch.float64, device=dev)
     nrm = torch.empty(1, dtype=torch.float64, device=dev)
@@ -268,7 +272,7 @@ def run_b200(args):
     stream = _stream()
     flags = C.TILE_PATH if os.environ.get("FSLD_TILE_PATH") else 0
     # loss_grad: count + scan + fill + brick kernel + reduce (5 kernels, + cnt memset); fused epilogue (2)
-    launches_per_step = 7 if not flags else 4
+    launches_per_step = (7 if not flags else 4) + (2 if world > 1 else 0)
 
     loss = torch.empty(1, dtype=torch.float64, device=dev)
 
@@ -284,11 +288,15 @@ def run_b200(args):
                 "loss_grad")
         if ev_k1 is not None:
             ev_k1.record()
-        if world > 1:  # one packed all-reduce: [grad accumulator | loss hi, lo]
+        if world > 1:  # one packed all-reduce: [grad accumulator on the touched ball | loss hi, lo]
+            C.check(lib.fsld_ball_gather(nball, ctypes_ptr(ball), ctypes_ptr(acc), ctypes_ptr(packed), 8, stream),
+                    "ball_gather")
             s32 = sq.float()
             packed[-2:-1].copy_(s32)
             packed[-1:].copy_((sq - s32.double()).float())
             dist.all_reduce(packed)
+            C.check(lib.fsld_ball_scatter(nball, ctypes_ptr(ball), ctypes_ptr(packed), ctypes_ptr(acc), 8, stream),
+                    "ball_scatter")
             sq.copy_(packed[-2:-1].double() + packed[-1:].double())
         C.check(lib.fsld_grad_epilogue(M ** 3, ctypes_ptr(acc), ctypes_ptr(v), scale, lam, ctypes_ptr(grad),
                                        ctypes_ptr(sq), ctypes_ptr(loss), 0, ctypes_ptr(nscr), nscr.numel() * 8,
@@ -383,6 +391,7 @@ def run_b200(args):
             "config": {"workload": cfg.name, "M": M, "n_mask": n, "batch_per_gpu": B,
                        "n_images_per_gpu": eng.n_images, "mode": cfg.mode, "ctf": "physical astigmatic",
                        "parallelism": f"dp{world}", "l2": "flushed between timed steps (512 MB write)",
+                       "allreduce_bytes": (8 * nball + 8) if world > 1 else 0,
                        "step": "CUDA graph replay" if world == 1 and not os.environ.get("FSLD_NO_GRAPH") else "eager"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic, "peak_source": src,

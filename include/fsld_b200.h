@@ -378,6 +378,16 @@ int fsld_armijo_select(const double* sq, const double* rq, const double* qq, con
 /* v <- v - st->eta_applied * dir  (complex64). */
 int fsld_apply_step(int64_t nvox, void* v, const void* dir, const fsld_armijo_state* st, void* stream);
 
+/*
+ * Touched-ball compaction for the data-parallel all-reduce: a scatter can only reach
+ * voxels within radius R + 1/2 + sqrt(3) of the origin (mask radius R; Appendix A item 7), ~54 %
+ * of the cube at M=128, so ranks all-reduce the compacted vector.  idx: (n,) int32 voxel indices
+ * (ascending); elements of elem_bytes = 8 (complex64) or 4 (float32).
+ *   gather : dst[i] = src[idx[i]]        scatter: dst[idx[i]] = src[i]   (other dst entries untouched)
+ */
+int fsld_ball_gather(int64_t n, const int32_t* idx, const void* src, void* dst, int elem_bytes, void* stream);
+int fsld_ball_scatter(int64_t n, const int32_t* idx, const void* src, void* dst, int elem_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

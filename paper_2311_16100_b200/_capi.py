@@ -101,6 +101,8 @@ SIGNATURES = {
     "fsld_proj_energy_sorted": (I, [I, I, I, P, P, I, P, P, P, P, P, U, P, SZ, P]),
     "fsld_hutch_fold_sorted": (I, [I, I, I, P, P, I, P, P, P, P, I, P, P, SZ, P]),
     "fsld_apply_step": (I, [I64, P, P, P, P]),
+    "fsld_ball_gather": (I, [I64, P, P, P, I, P]),
+    "fsld_ball_scatter": (I, [I64, P, P, P, I, P]),
 }
 
 _lib = None

@@ -193,4 +193,35 @@ cudaError_t launch_grad_epilogue(int64_t nvox, float2* acc, const float2* v, dou
     return cudaGetLastError();
 }
 
+// Touched-ball compaction for the data-parallel all-reduce: only voxels within
+// radius R + 1/2 + sqrt(3) can receive scatter contributions (Appendix A item 7), ~54 % of the
+// cube at M=128, so the all-reduce moves the compacted vector.  Element-generic (4 or 8 bytes).
+template <typename T>
+__global__ void ball_gather_kernel(int64_t n, const int32_t* __restrict__ idx, const T* __restrict__ src,
+                                   T* __restrict__ dst) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[idx[i]];
+}
+
+template <typename T>
+__global__ void ball_scatter_kernel(int64_t n, const int32_t* __restrict__ idx, const T* __restrict__ src,
+                                    T* __restrict__ dst) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        dst[idx[i]] = src[i];
+}
+
+cudaError_t launch_ball(bool gather, int64_t n, const int32_t* idx, const void* src, void* dst, int elem_bytes,
+                        cudaStream_t s) {
+    int blocks = (int)((n + 255) / 256);
+    blocks = blocks > 148 * 16 ? 148 * 16 : (blocks < 1 ? 1 : blocks);
+    if (elem_bytes == 8) {
+        if (gather) ball_gather_kernel<float2><<<blocks, 256, 0, s>>>(n, idx, (const float2*)src, (float2*)dst);
+        else ball_scatter_kernel<float2><<<blocks, 256, 0, s>>>(n, idx, (const float2*)src, (float2*)dst);
+    } else {
+        if (gather) ball_gather_kernel<float><<<blocks, 256, 0, s>>>(n, idx, (const float*)src, (float*)dst);
+        else ball_scatter_kernel<float><<<blocks, 256, 0, s>>>(n, idx, (const float*)src, (float*)dst);
+    }
+    return cudaGetLastError();
+}
+
 }  // namespace fsld

@@ -544,3 +544,17 @@ extern "C" int fsld_apply_step(int64_t nvox, void* v, const void* dir, const fsl
     return status_of(launch_apply_step(nvox, reinterpret_cast<float2*>(v), reinterpret_cast<const float2*>(dir), st,
                                        reinterpret_cast<cudaStream_t>(stream)));
 }
+
+// ---------------------------------------------------------------- data-parallel all-reduce compaction
+
+extern "C" int fsld_ball_gather(int64_t n, const int32_t* idx, const void* src, void* dst, int elem_bytes,
+                                void* stream) {
+    if (n < 1 || !idx || !src || !dst || (elem_bytes != 4 && elem_bytes != 8)) return FSLD_EINVAL;
+    return status_of(launch_ball(true, n, idx, src, dst, elem_bytes, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+extern "C" int fsld_ball_scatter(int64_t n, const int32_t* idx, const void* src, void* dst, int elem_bytes,
+                                 void* stream) {
+    if (n < 1 || !idx || !src || !dst || (elem_bytes != 4 && elem_bytes != 8)) return FSLD_EINVAL;
+    return status_of(launch_ball(false, n, idx, src, dst, elem_bytes, reinterpret_cast<cudaStream_t>(stream)));
+}

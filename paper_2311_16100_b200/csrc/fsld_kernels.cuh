@@ -116,6 +116,8 @@ cudaError_t set_phase_profile(unsigned long long* buf);
 
 cudaError_t launch_slice(int op, int mode, bool det, const SliceArgs& a, int nblocks, cudaStream_t s);
 cudaError_t launch_reduce(const double* part, int n, double* out, cudaStream_t s);
+cudaError_t launch_ball(bool gather, int64_t n, const int32_t* idx, const void* src, void* dst, int elem_bytes,
+                        cudaStream_t s);
 cudaError_t launch_reduce_cols(const double* part, int n, int ncols, double* out, cudaStream_t s);
 
 // Algorithm-1 step kernels (fsld_step.cu)

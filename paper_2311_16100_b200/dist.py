@@ -7,7 +7,8 @@ share and produces partial sums; ONE all-reduce of a packed buffer
 
     [ grad accumulator (2 M^3) | Hutchinson fold (M^3, optional) | sum|r|^2 (hi, lo) ]
 
-combines them (NCCL over NVLink/NVSwitch on B200, gloo in the CPU tests), and
+combines them (NCCL over NVLink/NVSwitch on B200, gloo in the CPU tests) -- optionally
+compacted to the voxels a scatter can reach (grid.touched_ball, ~54 % of the cube at M=128) -- and
 every rank then applies the same epilogue (scale, lam, running averages), so
 all ranks hold identical gradients / preconditioners.  The global batch
 composition follows the reference's per-epoch permutation (optim.py:133-139),
@@ -44,27 +45,98 @@ def shard_indices(batch, rank: int, world_size: int):
 
 @dataclass
 class PackedBuffer:
-    """One flat tensor viewed as [acc (complex) | hutch (real, optional) | loss (hi, lo)]."""
+    """One flat tensor viewed as [acc (complex) | hutch (real, optional) | loss (hi, lo)].
+
+    With ``ball`` (int32 voxel indices, grid.touched_ball) the accumulators in the flat buffer are
+    the compacted vectors; the per-rank compute writes full-size work accumulators
+    (``work_acc`` / ``work_hutch``) that ``pack`` gathers before and ``unpack`` scatters after the
+    all-reduce (voxels outside the ball are zero on every rank)."""
 
     flat: torch.Tensor
     n_voxels: int
     with_hutch: bool
+    ball: torch.Tensor | None = None
+    _wacc: torch.Tensor | None = None
+    _whutch: torch.Tensor | None = None
 
     @classmethod
-    def new(cls, n_voxels: int, with_hutch: bool, device, dtype=torch.float32) -> "PackedBuffer":
-        size = 2 * n_voxels + (n_voxels if with_hutch else 0) + 2
-        return cls(torch.zeros(size, dtype=dtype, device=device), n_voxels, with_hutch)
+    def new(cls, n_voxels: int, with_hutch: bool, device, dtype=torch.float32, ball=None) -> "PackedBuffer":
+        if ball is not None:
+            ball = torch.as_tensor(np.asarray(ball, dtype=np.int32) if not isinstance(ball, torch.Tensor) else ball,
+                                   device=device).to(torch.int32).contiguous()
+        ne = n_voxels if ball is None else int(ball.numel())
+        size = 2 * ne + (ne if with_hutch else 0) + 2
+        return cls(torch.zeros(size, dtype=dtype, device=device), n_voxels, with_hutch, ball)
+
+    @property
+    def n_elems(self) -> int:
+        return self.n_voxels if self.ball is None else int(self.ball.numel())
+
+    def _cdtype(self):
+        return torch.complex64 if self.flat.dtype == torch.float32 else torch.complex128
 
     @property
     def acc(self) -> torch.Tensor:
-        return self.flat[:2 * self.n_voxels].view(
-            torch.complex64 if self.flat.dtype == torch.float32 else torch.complex128)
+        return self.flat[:2 * self.n_elems].view(self._cdtype())
 
     @property
     def hutch(self) -> torch.Tensor | None:
         if not self.with_hutch:
             return None
-        return self.flat[2 * self.n_voxels:3 * self.n_voxels]
+        return self.flat[2 * self.n_elems:3 * self.n_elems]
+
+    def work_acc(self) -> torch.Tensor:
+        """Full-size accumulator the per-rank compute adds into (the flat view without a ball)."""
+        if self.ball is None:
+            return self.acc
+        if self._wacc is None:
+            self._wacc = torch.zeros(self.n_voxels, dtype=self._cdtype(), device=self.flat.device)
+        return self._wacc
+
+    def work_hutch(self) -> torch.Tensor | None:
+        if self.ball is None or not self.with_hutch:
+            return self.hutch
+        if self._whutch is None:
+            self._whutch = torch.zeros(self.n_voxels, dtype=self.flat.dtype, device=self.flat.device)
+        return self._whutch
+
+    def zero(self) -> None:
+        self.flat.zero_()
+        if self._wacc is not None:
+            self._wacc.zero_()
+        if self._whutch is not None:
+            self._whutch.zero_()
+
+    def _move(self, gather: bool, full: torch.Tensor, compact: torch.Tensor, elem_bytes: int) -> None:
+        if full.is_cuda and full.dtype in (torch.complex64, torch.float32):
+            from . import _capi as C
+            from .engine import _stream, ctypes_ptr
+            fn = C.load().fsld_ball_gather if gather else C.load().fsld_ball_scatter
+            src, dst = (full, compact) if gather else (compact, full)
+            C.check(fn(self.ball.numel(), ctypes_ptr(self.ball), ctypes_ptr(src), ctypes_ptr(dst), elem_bytes,
+                       _stream()), "fsld_ball_gather" if gather else "fsld_ball_scatter")
+        else:  # CPU (gloo tests): plain indexing
+            idx = self.ball.long()
+            if gather:
+                compact.copy_(full[idx])
+            else:
+                full[idx] = compact
+
+    def pack(self) -> None:
+        """Work accumulators -> compacted flat buffer (no-op without a ball)."""
+        if self.ball is None:
+            return
+        self._move(True, self._wacc, self.acc, 8)
+        if self.with_hutch and self._whutch is not None:
+            self._move(True, self._whutch, self.hutch, 4)
+
+    def unpack(self) -> None:
+        """All-reduced compacted buffer -> work accumulators (voxels outside the ball stay zero)."""
+        if self.ball is None:
+            return
+        self._move(False, self._wacc, self.acc, 8)
+        if self.with_hutch and self._whutch is not None:
+            self._move(False, self._whutch, self.hutch, 4)
 
     def set_loss(self, sq: torch.Tensor) -> None:
         """Store a float64 device scalar as (hi, lo) in the buffer's dtype (exact-ish through a sum)."""
@@ -83,9 +155,9 @@ class PackedBuffer:
 def _engine_compute(op, v, sub, buf: PackedBuffer, zbits=None, k=0):
     """Default per-rank compute: fused loss+grad (and probe fold) on this rank's GPU."""
     e = op.engine
-    sq, _, _ = e.loss_grad(v, sub, acc=buf.acc)
+    sq, _, _ = e.loss_grad(v, sub, acc=buf.work_acc())
     if zbits is not None:
-        e.hutch_fold(zbits, k, sub, acc=buf.hutch)
+        e.hutch_fold(zbits, k, sub, acc=buf.work_hutch())
     buf.set_loss(sq)
 
 
@@ -106,19 +178,22 @@ def sharded_step(op, v, batch, lam: float, n_total: int | None = None, buf: Pack
         buf = PackedBuffer.new(v.numel() if isinstance(v, torch.Tensor) else np.asarray(v).size,
                                zbits is not None, dev)
     else:
-        buf.flat.zero_()
+        buf.zero()
     (compute or _engine_compute)(op, v, sub, buf, zbits, k)
+    buf.pack()
     buf.all_reduce(group)
+    buf.unpack()
     sq = buf.loss()
+    acc = buf.work_acc()
     if isinstance(v, torch.Tensor) and v.is_cuda and buf.flat.dtype == torch.float32:
-        loss, grad = op.engine.epilogue(buf.acc, v, scale, lam, sq)
+        loss, grad = op.engine.epilogue(acc, v, scale, lam, sq)
         loss = loss[0]
     else:
         vv = torch.as_tensor(np.asarray(v)) if not isinstance(v, torch.Tensor) else v
-        vv = vv.to(buf.acc.dtype)
-        grad = scale * buf.acc + lam * vv
+        vv = vv.to(acc.dtype)
+        grad = scale * acc + lam * vv
         loss = 0.5 * scale * sq[0] + 0.5 * lam * float((vv.abs() ** 2).sum())
     hs = None
     if buf.with_hutch and k > 0:
-        hs = (scale / k) * buf.hutch.double() + lam
+        hs = (scale / k) * buf.work_hutch().double() + lam
     return loss, grad, hs

@@ -109,3 +109,15 @@ def shell_counts(M: int, mask_radius: int) -> tuple[np.ndarray, np.ndarray]:
     px = np.bincount(pr[pr <= mask_radius], minlength=mask_radius + 1)
     vx = np.bincount(vr[vr <= mask_radius], minlength=mask_radius + 1)
     return px, vx
+
+
+def touched_ball(M: int, mask_radius: int) -> np.ndarray:
+    """Voxel indices (ascending, int32) a scatter can reach: radius < R + 1/2 + sqrt(3).
+
+    A masked pixel has |k| < R + 1/2 (round(|k|) <= R, grid.py:185-189); rotation keeps the
+    radius, the clamp only shortens it (kernels.py:42-60), and the trilinear footprint stays
+    within sqrt(3) of the rotated point.  The data-parallel all-reduce
+    moves only these voxels.
+    """
+    r = np.sqrt((voxel_coords(M).astype(np.float64) ** 2).sum(axis=1))
+    return np.flatnonzero(r < mask_radius + 0.5 + np.sqrt(3.0)).astype(np.int32)

@@ -19,6 +19,7 @@ from conftest import load_golden
 from oracle import oracle as O
 
 from paper_2311_16100_b200 import dist as D
+from paper_2311_16100_b200 import grid as G
 
 
 def _free_port():
@@ -38,16 +39,16 @@ def _oracle_op(g):
 def _oracle_compute(op, v, sub, buf, zbits=None, k=0):
     """Per-rank partial sums with the CPU oracle, written into the packed buffer (float64)."""
     sq, acc = O._resid_pass(op, np.asarray(v), sub, True)
-    buf.acc.copy_(torch.from_numpy(acc))
+    buf.work_acc().copy_(torch.from_numpy(acc))
     if zbits is not None:
         fold = np.zeros(op.M ** 3)
         for z in zbits:  # here: list of +-1 probe vectors
             fold += z * op.backproject(op.project(z, sub), sub).real
-        buf.hutch.copy_(torch.from_numpy(fold))
+        buf.work_hutch().copy_(torch.from_numpy(fold))
     buf.set_loss(torch.tensor([sq], dtype=torch.float64))
 
 
-def _worker(rank, world_size, port, out_path):
+def _worker(rank, world_size, port, out_path, use_ball=False):
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world_size)
     g = load_golden("dataset_m16_tri.npz")
     op = _oracle_op(g)
@@ -57,7 +58,8 @@ def _worker(rank, world_size, port, out_path):
     v = torch.from_numpy(np.asarray(g["v1"], dtype=np.complex128))
     rng = np.random.default_rng(11)
     probes = [rng.integers(0, 2, M ** 3).astype(np.float64) * 2 - 1 for _ in range(3)]
-    buf = D.PackedBuffer.new(M ** 3, True, torch.device("cpu"), dtype=torch.float64)
+    ball = G.touched_ball(M, M // 2 - 1) if use_ball else None
+    buf = D.PackedBuffer.new(M ** 3, True, torch.device("cpu"), dtype=torch.float64, ball=ball)
     loss, grad, hs = D.sharded_step(op, v, batch, lam, buf=buf, zbits=probes, k=len(probes),
                                     compute=_oracle_compute)
     res = {"loss": float(loss), "grad": grad.numpy(), "hs": hs.numpy(), "sub": D.shard_indices(batch, rank, world_size)}
@@ -83,7 +85,8 @@ def test_packed_buffer_loss_split_roundtrip():
     assert abs(float(buf.loss()) - float(sq)) / float(sq) < 1e-12
 
 
-def test_two_rank_gloo_step_equals_single_process():
+@pytest.mark.parametrize("use_ball", [False, True])
+def test_two_rank_gloo_step_equals_single_process(use_ball):
     g = load_golden("dataset_m16_tri.npz")
     op = _oracle_op(g)
     M = op.M
@@ -95,7 +98,7 @@ def test_two_rank_gloo_step_equals_single_process():
     hs_ref = np.mean([z * op.hvp(z, batch, lam).real for z in probes], axis=0)
     with tempfile.TemporaryDirectory() as d:
         out = os.path.join(d, "res")
-        mp.start_processes(_worker, args=(2, _free_port(), out), nprocs=2, start_method="spawn")
+        mp.start_processes(_worker, args=(2, _free_port(), out, use_ball), nprocs=2, start_method="spawn")
         r0 = np.load(out + ".0.npz")
         r1 = np.load(out + ".1.npz")
     assert len(r0["sub"]) + len(r1["sub"]) == batch.size
@@ -104,3 +107,16 @@ def test_two_rank_gloo_step_equals_single_process():
         assert O.relative_l2(r["grad"], grad_ref) < 1e-12
         assert O.relative_l2(r["hs"], hs_ref) < 1e-12
     assert np.array_equal(r0["grad"], r1["grad"])  # identical on every rank
+
+
+def test_touched_ball_contains_every_scatter_target(golden):
+    """Every voxel the oracle's adjoint touches lies inside grid.touched_ball (incl. clamped rim pixels)."""
+    g = golden("dataset_m16_tri.npz")
+    op = _oracle_op(g)
+    M = op.M
+    ball = G.touched_ball(M, M // 2 - 1)
+    ones = np.ones((op.n_images, op.pix.shape[0]), dtype=np.complex128)
+    acc = op.backproject(ones, np.arange(op.n_images))
+    touched = np.flatnonzero(np.abs(acc) > 0)
+    assert np.isin(touched, ball).all()
+    assert ball.size < M ** 3
