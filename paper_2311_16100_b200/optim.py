@@ -280,7 +280,7 @@ def armijo_search(v, grad, dhat, loss_fn, eta_in: float, c: float, f0=None):
 
 
 def run(config: OptimConfig, stack, v0=None, reference=None, exact_diag_vec=None, probes: str = "reference",
-        op=None):
+        op=None, group=None):
     """Algorithm 1 (optim.py:309-393) with every step resident on the GPU.
 
     Per batch, in stream order and without host synchronisation:
@@ -296,6 +296,13 @@ def run(config: OptimConfig, stack, v0=None, reference=None, exact_diag_vec=None
     reference's numpy stream (parity); probes="device" generates them in-kernel
     (counter-based, no z bytes moved).  A line search that exceeds 60 halvings
     raises NumericalError at the end of that epoch (the reference raises at the step).
+
+    Data parallel (torch.distributed initialised, one process per GPU, every rank
+    holding the dataset): each rank takes its contiguous share of every global batch
+    (dist.shard_indices), and per step ONE all-reduce of [gradient accumulator | probe
+    fold | sum|r|^2], compacted to the touched ball, plus one scalar all-reduce of the
+    line-search energy, combine the ranks; the epilogue, the line search and the update
+    then run identically on every rank.
     """
     from .forward import DatasetOperator, FourierVolume
     from .hessian import exact_diag
@@ -344,8 +351,22 @@ def run(config: OptimConfig, stack, v0=None, reference=None, exact_diag_vec=None
         rv = reference.values if hasattr(reference, "values") else reference
         ref_vals = torch.as_tensor(np.asarray(rv) if not _is_dev(rv) else rv, device=dev)
 
-    acc = torch.zeros(nvox, dtype=torch.complex64, device=dev)
-    fold = torch.zeros(nvox, dtype=torch.float32, device=dev)
+    from . import dist as D
+    from .grid import touched_ball
+    rank, ws = D.world()
+    if group is not None:
+        ws = torch.distributed.get_world_size(group)
+        rank = torch.distributed.get_rank(group)
+    if ws > 1 and e.deterministic:
+        raise ValueError("the data-parallel run uses the fp32 accumulators (deterministic engines: one process)")
+    pbuf = None
+    if ws > 1:
+        pbuf = D.PackedBuffer.new(nvox, estimating, dev, ball=touched_ball(spec.M, stack.mask_radius))
+        acc = pbuf.work_acc()
+        fold = pbuf.work_hutch() if estimating else torch.zeros(nvox, dtype=torch.float32, device=dev)
+    else:
+        acc = torch.zeros(nvox, dtype=torch.complex64, device=dev)
+        fold = torch.zeros(nvox, dtype=torch.float32, device=dev)
     dirv = torch.empty(nvox, dtype=torch.complex64, device=dev)
     dhat_last = torch.empty(nvox, dtype=torch.float32, device=dev)
     st = e.new_armijo_state(config.eta0)
@@ -358,16 +379,31 @@ def run(config: OptimConfig, stack, v0=None, reference=None, exact_diag_vec=None
         batches = epoch_batches(n, config.batch_size, config.seed, epoch)
         st.view(torch.int32)[12] = 0  # n_steps: hist rows restart each epoch
         for bi, batch in enumerate(batches):
-            idx = e.idx_tensor(batch)
-            nb = idx.numel()
+            nb = len(batch)
             scale = n / nb
             last = epoch == n_epochs - 1 and bi == len(batches) - 1
+            sub = D.shard_indices(batch, rank, ws) if ws > 1 else batch
+            idx = e.idx_tensor(sub) if len(sub) else None
             if estimating:
                 if probes == "reference":
                     zbits, kk = e.pack_probes(rademacher(z_rng, nvox))
                 else:
                     zbits, kk = e.gen_probes(1, (config.seed << 32) + epoch * 1000003 + bi), 1
-            if estimating and not e.deterministic:
+            if ws > 1:
+                # this rank's share of the batch, then one all-reduce of [acc | fold | sum|r|^2]
+                if idx is not None and estimating:
+                    sq = e.loss_grad_hutch(v, idx, zbits, acc, fold)
+                elif idx is not None:
+                    sq, _, _ = e.loss_grad(v, idx, acc=acc)
+                else:
+                    sq = torch.zeros(1, dtype=torch.float64, device=dev)
+                pbuf.set_loss(sq)
+                pbuf.pack()
+                pbuf.all_reduce(group)
+                pbuf.unpack()
+                sq = pbuf.loss()
+                gacc = acc
+            elif estimating and not e.deterministic:
                 # one fused pass: gradient accumulator + the probe's Hutchinson fold
                 sq = e.loss_grad_hutch(v, idx, zbits, acc, fold)
                 gacc = acc
@@ -386,7 +422,12 @@ def run(config: OptimConfig, stack, v0=None, reference=None, exact_diag_vec=None
                                   dhat_fixed=dhat_fixed, dhat_out=dhat_last if last else None)
             if estimating:
                 k += 1
-            qq = e.proj_energy(dirv, idx, reuse_bins=e.brick_path)  # same batch, same scratch
+            if idx is not None:
+                qq = e.proj_energy(dirv, idx, reuse_bins=e.brick_path)  # same batch, same scratch
+            else:
+                qq = torch.zeros(1, dtype=torch.float64, device=dev)
+            if ws > 1:
+                torch.distributed.all_reduce(qq, group=group)
             e.armijo_select(sq, vol4[4:5], qq, vol4, scale, lam, float(config.c), st, hist, MAX_HALVINGS)
             e.apply_step(v, dirv, st)
         # ---- epoch end: the only host synchronisation of the epoch

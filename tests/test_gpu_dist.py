@@ -50,3 +50,51 @@ def test_sharded_step_with_ball_compaction_matches_full_buffer():
     assert abs(float(l1) - float(l2)) / float(l2) < 1e-6
     assert O.relative_l2(g1.cpu().numpy(), g2.cpu().numpy()) < 1e-5
     assert O.relative_l2(h1.cpu().numpy(), h2.cpu().numpy()) < 1e-5
+
+
+def _run_worker(rank, world_size, port, out_path, name, seed):
+    """One rank of a data-parallel optim.run (functional check: both ranks on cuda:0, gloo exchange)."""
+    import torch.distributed as dist
+    from conftest import load_golden
+    from test_gpu_step import golden_stack
+    from paper_2311_16100_b200 import optim as Opt
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world_size)
+    g = load_golden(name)
+    stack = golden_stack(g, seed)
+    cfg = Opt.OptimConfig(lam=float(g["lam"]), batch_size=int(g["batch"].size), epochs=3, seed=seed,
+                          mode=str(g["mode"]))
+    vol, tr = Opt.run(cfg, stack)
+    np.savez(out_path + f".{rank}.npz", v=vol.values, etas=np.array(tr.accepted_etas),
+             f0=np.array(tr.step_f0), loss=tr.loss)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name,seed", [("dataset_m16_tri.npz", 4)])
+def test_data_parallel_run_matches_single_process(golden, name, seed):
+    """optim.run with world_size 2 (each rank half of every batch, one compacted all-reduce per step)
+    reproduces the single-process device run and the reference trajectory."""
+    import os
+    import socket
+    import tempfile
+    import torch.multiprocessing as mp
+    from test_gpu_step import golden_stack
+    from paper_2311_16100_b200 import optim as Opt
+    g = golden(name)
+    cfg = Opt.OptimConfig(lam=float(g["lam"]), batch_size=int(g["batch"].size), epochs=3, seed=seed,
+                          mode=str(g["mode"]))
+    vol1, tr1 = Opt.run(cfg, golden_stack(g, seed))
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    with tempfile.TemporaryDirectory() as d:
+        out = os.path.join(d, "r")
+        mp.start_processes(_run_worker, args=(2, port, out, name, seed), nprocs=2, start_method="spawn")
+        r0, r1 = np.load(out + ".0.npz"), np.load(out + ".1.npz")
+    assert np.array_equal(r0["etas"], r1["etas"]) and np.array_equal(r0["v"], r1["v"])  # identical ranks
+    assert np.array_equal(r0["etas"], np.array(tr1.accepted_etas))
+    assert np.array_equal(r0["etas"][:10], g["sgd_rec"][:, 1])
+    assert np.max(np.abs(r0["f0"] - np.array(tr1.step_f0)) / np.abs(np.array(tr1.step_f0))) < 1e-5
+    assert O.relative_l2(r0["v"], vol1.values) < 1e-5
