@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "_lib", "libfsld_b200.so")
+LIB_PATH = os.environ.get("FSLD_LIB_PATH") or os.path.join(_PKG, "_lib", "libfsld_b200.so")
 
 FSLD_OK = 0
 FSLD_EINVAL = -1

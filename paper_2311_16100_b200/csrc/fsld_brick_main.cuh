@@ -35,8 +35,8 @@ struct SortedSmemT {
     SegRec seg[BC];                 // the item's segment records (gofs rebased to the flat index)
     int pref[BC + 1];               // exclusive prefix of segment lengths
     unsigned char bk[RB];           // round pixel -> segment
-    int4 item_desc;
-    int item;
+    int4 item_desc;                 // first item of this CTA (prologue)
+    int4 next_desc;                 // the item after the current one ((-1, ..) = none)
     int vmax_bits, hmax_bits;
     int wtot[2];                    // per-warp segment-length totals
     double red[BW];
@@ -118,6 +118,44 @@ __device__ __forceinline__ float2 seg_factor(const SegRegs& R, int kx, int ky) {
     return make_float2(ctf * cs, ctf * ss);
 }
 
+
+// cp.async helpers (sm_80+ LDGSTS): 16-byte copy, and 8-byte copy with zero fill when !valid.
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+                 "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async8_zfill(void* dst, const void* src, bool valid) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+                 "l"(src), "r"(valid ? 8 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// Stage a work item's inputs in shared memory without waiting: its segment records, the brick of
+// v (+halo, zero off the grid) and, for HUTCH, the probe sign of each brick voxel (into S.bk).
+// Issued for the NEXT item right after the current item's last pass 1, so the loads overlap that
+// item's pass 2 and flush (none of S.seg / S.vb / S.bk is read after pass 1).
+template <bool HUTCH>
+__device__ __forceinline__ void stage_item(SortedSmemT<HUTCH>& S, const SortedArgs& a, int4 item, const int* lxyz) {
+    const int M = a.M, c = a.c, nb = a.nb;
+    const int bid = item.x, pstart = item.y, nseg = item.z;
+    const int ox = -c + BT * (bid % nb), oy = -c + BT * ((bid / nb) % nb), oz = -c + BT * (bid / (nb * nb));
+    const int4* src = reinterpret_cast<const int4*>(a.pairs + pstart);
+    int4* dst = reinterpret_cast<int4*>(S.seg);
+    for (int w = threadIdx.x; w < nseg * 8; w += BTHREADS) cp_async16(dst + w, src + w);
+#pragma unroll
+    for (int u = 0; u < BU; ++u) {
+        if (lxyz[u] < 0) continue;
+        const int l = threadIdx.x + u * BTHREADS;
+        const int kx = ox + (lxyz[u] & 15), ky = oy + ((lxyz[u] >> 4) & 15), kz = oz + (lxyz[u] >> 8);
+        const bool in = kx < M - c && ky < M - c && kz < M - c;
+        const int j = in ? lin_index(kx, ky, kz, M, c) : 0;
+        cp_async8_zfill(S.vb + l, a.v + j, in);
+        if (HUTCH) S.bk[l] = in ? (unsigned char)(__ldg(a.zbits + j) & 1u) : 0;
+    }
+}
+
 // Per work item (brick, <= BC image segments):
 //   setup: claim (run ahead on one thread), the segment records (one 128-B
 //          SegRec each, written by the fill pass), their prefix, the brick's
@@ -152,42 +190,34 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArg
             if (HUTCH) S.acch[l] = 0;
         }
     }
+    // work items are claimed one ahead: the claimer thread publishes the item after the current
+    // one in S.next_desc, whose inputs are staged (asynchronously) during the current item
     constexpr int kClaimer = BTHREADS - 32;
     const int n_items = a.ctl[0];
-    int next_it = 0, claimed = 0;
-    int4 next_item = make_int4(0, 0, 0, 0);
+    auto claim = [&]() -> int4 {
+        const int it = atomicAdd(a.ctl + 1, 1);
+        return it < n_items ? a.items[it] : make_int4(-1, 0, 0, 0);
+    };
     if (threadIdx.x == kClaimer) {
-        next_it = atomicAdd(a.ctl + 1, 1);
-        if (next_it < n_items) next_item = a.items[next_it];
-        claimed = atomicAdd(a.ctl + 1, 1);
+        S.item_desc = claim();
+        S.next_desc = claim();
     }
+    __syncthreads();
+    int4 item = S.item_desc;
+    if (item.x >= 0) stage_item(S, a, item, lxyz);
     PHASE_INIT();
 
     for (;;) {
-        if (threadIdx.x == kClaimer) {
-            S.item_desc = next_item;
-            S.item = next_it;
-        }
-        __syncthreads();
-        const int it = S.item;
-        if (it >= n_items) break;
-        const int4 item = S.item_desc;
-        if (threadIdx.x == kClaimer) {  // consumed next iteration / the one after
-            next_it = claimed;
-            if (next_it < n_items) next_item = a.items[next_it];
-            if (next_it < n_items) claimed = atomicAdd(a.ctl + 1, 1);
-        }
-        const int bid = item.x, pstart = item.y, nseg = item.z;
+        if (item.x < 0) break;
+        cp_async_wait_all();
+        __syncthreads();  // (A) this item's inputs are in shared memory
+        const int4 nxt = S.next_desc;
+        const int bid = item.x, nseg = item.z;
         const int ox = -c + BT * (bid % nb), oy = -c + BT * ((bid / nb) % nb), oz = -c + BT * (bid / (nb * nb));
-        // ---------------- setup: segment records, their prefix (warps 0, 1), v brick [z signs]
-        {
-            const int4* src = reinterpret_cast<const int4*>(a.pairs + pstart);
-            int4* dst = reinterpret_cast<int4*>(S.seg);
-            for (int w = threadIdx.x; w < nseg * 8; w += BTHREADS) dst[w] = __ldg(src + w);
-        }
+        // ---------------- setup: segment-length prefix (warps 0, 1) [corner sign masks]
         if (warp < 2) {
             const int k = threadIdx.x;
-            const int len = k < nseg ? __ldg(&a.pairs[pstart + k].count) : 0;
+            const int len = k < nseg ? S.seg[k].count : 0;
             int incl = len;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -197,26 +227,8 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArg
             S.pref[k] = incl - len;  // warp 1 adds warp 0's total below
             if (lane == 31) S.wtot[warp] = incl;
         }
-        unsigned char* zs = reinterpret_cast<unsigned char*>(S.hval);  // setup staging of the z bits
-#pragma unroll
-        for (int u = 0; u < BU; ++u) {
-            if (lxyz[u] < 0) continue;
-            const int l = threadIdx.x + u * BTHREADS;
-            const int kx = ox + (lxyz[u] & 15), ky = oy + ((lxyz[u] >> 4) & 15), kz = oz + (lxyz[u] >> 8);
-            const bool in = kx < M - c && ky < M - c && kz < M - c;
-            const int j = in ? lin_index(kx, ky, kz, M, c) : 0;
-            S.vb[l] = in ? __ldg(a.v + j) : make_float2(0.f, 0.f);
-            if (HUTCH) zs[l] = in ? (unsigned char)(__ldg(a.zbits + j) & 1u) : 0;
-        }
-        __syncthreads();
-        if (threadIdx.x < nseg) {  // final prefix; rebase gofs to the flat pixel index
-            const int k = threadIdx.x;
-            const int p = S.pref[k] + (k >= 32 ? S.wtot[0] : 0);
-            S.pref[k] = p;
-            S.seg[k].gofs -= p;
-        }
-        if (threadIdx.x == 0) S.pref[nseg] = S.wtot[0] + (nseg > 32 ? S.wtot[1] : 0);
-        if (HUTCH) {  // corner sign masks (x fastest: 000,100,010,110,001,101,011,111)
+        if (HUTCH) {  // corner sign masks (x fastest: 000,100,010,110,001,101,011,111) from the staged signs
+            const unsigned char* zs = S.bk;
 #pragma unroll
             for (int u = 0; u < BU; ++u) {
                 if (lxyz[u] < 0) continue;
@@ -230,6 +242,15 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArg
                 S.zc[l] = (unsigned char)m;
             }
         }
+        __syncthreads();  // (B)
+        if (threadIdx.x == kClaimer) S.next_desc = claim();  // everyone has read nxt
+        if (threadIdx.x < nseg) {  // final prefix; rebase gofs to the flat pixel index
+            const int k = threadIdx.x;
+            const int p = S.pref[k] + (k >= 32 ? S.wtot[0] : 0);
+            S.pref[k] = p;
+            S.seg[k].gofs -= p;
+        }
+        if (threadIdx.x == 0) S.pref[nseg] = S.wtot[0] + (nseg > 32 ? S.wtot[1] : 0);
         __syncthreads();
         PHASE_MARK(0);
         const int total = S.pref[nseg];
@@ -304,6 +325,7 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArg
             }
             __syncthreads();
             PHASE_MARK(2);
+            if (r0 + RB >= total && nxt.x >= 0) stage_item(S, a, nxt, lxyz);  // overlaps pass 2 + flush
             // ---------------- pass 2: fixed-point adjoint scatter (kernels.py:221-230)
             // <= 12 contributions per voxel per image segment -> |sum| < 2^31
             const float lim = fminf(4194303.0f, 178956970.0f / (float)nseg);
@@ -364,6 +386,7 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArg
             __syncthreads();
         }
         PHASE_MARK(7);
+        item = nxt;
     }
     PHASE_FLUSH();
     for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
