@@ -6,6 +6,11 @@
 constexpr float kMagic = 12582912.0f;
 constexpr int kMagicBits = 0x4B400000;
 
+// Ablation builds (tools/build_exp.sh <name> -DFSLD_EXP_...; never defined in the product build)
+// remove one part of the work at a time to measure its share: FSLD_EXP_NO_ATOMS (pass-2 shared
+// atomics), FSLD_EXP_ONE_GATHER (7 of the 8 corner gathers), FSLD_EXP_NO_XLOAD (image loads),
+// FSLD_EXP_NO_PASS1, FSLD_EXP_NO_PASS2.  Results are wrong by construction.
+
 // Optional per-phase cycle accounting of the item loop (thread 0 of each CTA), enabled by
 // fsld_debug_phase_profile(); costs one clock64 read per phase when on.
 __device__ unsigned long long* g_phase_prof = nullptr;
@@ -272,13 +277,26 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArg
             PHASE_MARK(1);
             // ---------------- pass 1
             float vmax = 0.f, hmax = 0.f, sq = 0.f;
+#if defined(FSLD_EXP_NO_PASS1)
+            for (int e = threadIdx.x; e < rn; e += BTHREADS) {
+                S.bval[e] = make_float2(1.f, 1.f);
+                S.bgeo[e] = make_float4(0.5f, 0.5f, 0.5f, __int_as_float((e * 37) % 500));
+                vmax = 1.f;
+            }
+            for (int e = threadIdx.x; e < 0; e += BTHREADS) {
+#else
 #pragma unroll 1
             for (int e = threadIdx.x; e < rn; e += BTHREADS) {
+#endif
                 SegRegs R;
                 load_seg(S.seg[S.bk[e]], R);
                 const long long g = R.gofs + (r0 + e);
                 const char2 kk = a.pc[g];
+#if defined(FSLD_EXP_NO_XLOAD)
+                const float2 xv = make_float2((float)(g & 7), 0.f);
+#else
                 const float2 xv = __ldg(a.xs + g);
+#endif
                 const int px = kk.x, py = kk.y;
                 float cx, cy, cz, fx, fy, fz;
                 floor_corner((float)px, (float)py, R.fr, bnd, cx, cy, cz, fx, fy, fz);
@@ -289,10 +307,16 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArg
                 const float2* vb = S.vb + l0;
                 // trilinear gather (kernels.py:171-176) from the smem brick
                 const float2 WX = make_float2(wx, wx), AX = make_float2(ax, ax);
+#if defined(FSLD_EXP_ONE_GATHER)
+                const float2 g0 = vb[0];
+                const float2 e0 = __ffma2_rn(WX, g0, __fmul2_rn(AX, g0)), e1 = __ffma2_rn(AX, g0, __fmul2_rn(WX, g0));
+                const float2 e2 = __ffma2_rn(WX, e0, __fmul2_rn(AX, g0)), e3 = __ffma2_rn(AX, e1, __fmul2_rn(WX, g0));
+#else
                 const float2 e0 = __ffma2_rn(WX, vb[1], __fmul2_rn(AX, vb[0]));
                 const float2 e1 = __ffma2_rn(WX, vb[BH + 1], __fmul2_rn(AX, vb[BH]));
                 const float2 e2 = __ffma2_rn(WX, vb[BH * BH + 1], __fmul2_rn(AX, vb[BH * BH]));
                 const float2 e3 = __ffma2_rn(WX, vb[BH * BH + BH + 1], __fmul2_rn(AX, vb[BH * BH + BH]));
+#endif
                 const float2 q0 = __ffma2_rn(make_float2(wy, wy), e1, __fmul2_rn(make_float2(ay, ay), e0));
                 const float2 q1 = __ffma2_rn(make_float2(wy, wy), e3, __fmul2_rn(make_float2(ay, ay), e2));
                 const float2 pv = __ffma2_rn(make_float2(wz, wz), q1, __fmul2_rn(make_float2(az, az), q0));
@@ -338,7 +362,11 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArg
                 sch = hm > 0.f ? exp2f(floorf(log2f(lim / hm))) : 1.0f;
                 inv_sch = 1.0f / sch;
             }
+#if defined(FSLD_EXP_NO_PASS2)
+            for (int e = threadIdx.x; e < 0; e += BTHREADS) {
+#else
             for (int e = threadIdx.x; e < rn; e += BTHREADS) {
+#endif
                 const float4 geo = S.bgeo[e];
                 const int l0 = __float_as_int(geo.w);
                 const float wx = geo.x, wy = geo.y, wz = geo.z;
@@ -347,12 +375,22 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArg
                 const float zy00 = az * ay, zy10 = az * wy, zy01 = wz * ay, zy11 = wz * wy;
                 const float w8[8] = {zy00 * ax, zy00 * wx, zy10 * ax, zy10 * wx, zy01 * ax, zy01 * wx, zy11 * ax, zy11 * wx};
                 const int off8[8] = {0, 1, BH, BH + 1, BH * BH, BH * BH + 1, BH * BH + BH, BH * BH + BH + 1};
+#if defined(FSLD_EXP_NO_ATOMS)
+                int sink = 0;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const float2 y = __ffma2_rn(make_float2(w8[q], w8[q]), val, make_float2(kMagic, kMagic));
+                    sink += (__float_as_int(y.x) - kMagicBits) ^ (__float_as_int(y.y) - kMagicBits) ^ (l0 + off8[q]);
+                }
+                if (sink == 0x7fffffff) S.accr[0] = sink;
+#else
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
                     const float2 y = __ffma2_rn(make_float2(w8[q], w8[q]), val, make_float2(kMagic, kMagic));
                     atomicAdd(S.accr + l0 + off8[q], __float_as_int(y.x) - kMagicBits);
                     atomicAdd(S.acci + l0 + off8[q], __float_as_int(y.y) - kMagicBits);
                 }
+#endif
                 if (HUTCH) {
                     const float h = S.hval[e] * sch;
 #pragma unroll
