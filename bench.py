@@ -288,6 +288,9 @@ def run_b200(args):
                 "loss_grad")
         if ev_k1 is not None:
             ev_k1.record()
+        return finish_step(stream)
+
+    def finish_step(stream):
         if world > 1:  # one packed all-reduce: [grad accumulator on the touched ball | loss hi, lo]
             C.check(lib.fsld_ball_gather(nball, ctypes_ptr(ball), ctypes_ptr(acc), ctypes_ptr(packed), 8, stream),
                     "ball_gather")
@@ -303,27 +306,71 @@ def run_b200(args):
                                        stream), "epilogue")
         return loss
 
+    # Binning plans (default on the brick path): the batches of a run are known in advance, so their
+    # brick binning is done K batches at a time (fsld_plan_build) and each step runs only the
+    # work-item kernel.  The plan of the TIMED batches is built inside the measurement: its time is
+    # added to the steps (t_plan / K per step).
+    use_plan = flags == 0 and eng.brick_path and not os.environ.get("FSLD_NO_PLAN")
+    E = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    t_plan = 0.0
+    if use_plan:
+        plan_w = eng.make_plan(torch.stack(batches[:args.warmup]))
+        torch.cuda.synchronize()
+        p0, p1 = E(), E()
+        p0.record()
+        plan_t = eng.make_plan(torch.stack(batches[args.warmup:]))
+        p1.record()
+        torch.cuda.synchronize()
+        t_plan = p0.elapsed_time(p1)
+        launches_per_step = 5 + (2 if world > 1 else 0)  # memset + kernel + reduce + epilogue (2)
+
+    def planned_step(plan, k, ev_k0=None, ev_k1=None):
+        stream = _stream()
+        if ev_k0 is not None:
+            ev_k0.record()
+        C.check(lib.fsld_loss_grad_planned(M, eng.mode_id, n, ctypes_ptr(eng.recs), ctypes_ptr(plan.buf), B, k,
+                                           ctypes_ptr(v), ctypes_ptr(eng.x), ctypes_ptr(eng.pc), 0, ctypes_ptr(acc),
+                                           0, ctypes_ptr(sq), ctypes_ptr(scr), scr.numel() * 8, stream),
+                "loss_grad_planned")
+        if ev_k1 is not None:
+            ev_k1.record()
+        return finish_step(stream)
+
     for i in range(args.warmup):
-        step(batches[i])
+        if use_plan:
+            planned_step(plan_w, i)
+        else:
+            step(batches[i])
     torch.cuda.synchronize()
     # kernel-only timing (events around the fused loss+grad call, eager)
-    E = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
     kev = [(E(), E()) for _ in range(args.steps)]
     for i in range(args.steps):
         flush.fill_(float(i))
-        step(batches[args.warmup + i], *kev[i])
+        if use_plan:
+            planned_step(plan_t, i, *kev[i])
+        else:
+            step(batches[args.warmup + i], *kev[i])
     torch.cuda.synchronize()
     kern_ms = [a_.elapsed_time(b_) for a_, b_ in kev]
     # the timed step runs as one CUDA graph replay (N=1; under NCCL the collective stays eager)
     idx_static = torch.empty(B, dtype=torch.int32, device=dev)
-    graph = None
+    graphs = None
     if world == 1 and not os.environ.get("FSLD_NO_GRAPH"):
-        idx_static.copy_(batches[0])
-        step(idx_static)
-        torch.cuda.synchronize()
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph):
+        graphs = []
+        if use_plan:  # one graph per planned batch (the batch index is a kernel argument)
+            for i in range(args.steps):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    planned_step(plan_t, i)
+                graphs.append(g)
+        else:
+            idx_static.copy_(batches[0])
             step(idx_static)
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                step(idx_static)
+            graphs = [g] * args.steps
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -336,9 +383,12 @@ def run_b200(args):
             flush.fill_(float(i))  # L2 flush between timed steps (outside the step events)
             s0, s1 = ev[i]
             s0.record()
-            if graph is not None:
-                idx_static.copy_(batches[args.warmup + i])
-                graph.replay()
+            if graphs is not None:
+                if not use_plan:
+                    idx_static.copy_(batches[args.warmup + i])
+                graphs[i].replay()
+            elif use_plan:
+                planned_step(plan_t, i)
             else:
                 step(batches[args.warmup + i])
             s1.record()
@@ -347,8 +397,8 @@ def run_b200(args):
         if world > 1:
             dist.barrier()
     step_ms = [a_.elapsed_time(b_) for a_, b_ in ev]
-    t_step = float(np.mean(step_ms))
-    t_kern = float(np.mean(kern_ms))
+    t_step = float(np.mean(step_ms)) + t_plan / args.steps
+    t_kern = float(np.mean(kern_ms)) + t_plan / args.steps
     if world > 1:
         t = torch.tensor([t_step, t_kern], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -392,10 +442,13 @@ def run_b200(args):
                        "n_images_per_gpu": eng.n_images, "mode": cfg.mode, "ctf": "physical astigmatic",
                        "parallelism": f"dp{world}", "l2": "flushed between timed steps (512 MB write)",
                        "allreduce_bytes": (8 * nball + 8) if world > 1 else 0,
-                       "step": "CUDA graph replay" if world == 1 and not os.environ.get("FSLD_NO_GRAPH") else "eager"},
+                       "step": "CUDA graph replay" if world == 1 and not os.environ.get("FSLD_NO_GRAPH") else "eager",
+                       "binning": (f"plan of the {args.steps} timed batches (fsld_plan_build), built inside the "
+                                   f"measurement: {t_plan:.4f} ms, added as {t_plan / args.steps:.4f} ms per step")
+                       if use_plan else "per step (count -> scan -> fill kernels)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic, "peak_source": src,
-                         "kernel": ("fsld_loss_grad_sorted: bin count/scan/fill + sorted_loss_grad_kernel + loss reduce" if not flags else "fsld slice_kernel<TRI,LOSS_GRAD> (tile path)"),
+                         "kernel": ("fsld_loss_grad_planned: sorted_loss_grad_kernel + loss reduce (+ the plan's binning / K)" if use_plan else ("fsld_loss_grad_sorted: bin count/scan/fill + sorted_loss_grad_kernel + loss reduce" if not flags else "fsld slice_kernel<TRI,LOSS_GRAD> (tile path)")),
                          "kernel_ms": t_kern, "algorithmic_bytes_per_launch": abytes},
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clk.summary(),

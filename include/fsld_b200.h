@@ -379,6 +379,29 @@ int fsld_armijo_select(const double* sq, const double* rq, const double* qq, con
 int fsld_apply_step(int64_t nvox, void* v, const void* dir, const fsld_armijo_state* st, void* stream);
 
 /*
+ * Multi-batch binning plans.  The batches of an epoch are known in advance (optim.py:133-139),
+ * so the per-step brick binning (count -> scan -> fill of the batch's segment records) can be done
+ * for K batches of B images at once; each step then only runs the work-item kernel.
+ *   idx         : (K, B) int32 dataset rows, batch k = idx[k*B .. k*B+B)
+ *   total_pairs : sum over the K batches of the images' segment counts
+ *                 (sum_k sum_b seg_off[row+1] - seg_off[row]); sizes the plan
+ * A plan is read-only after fsld_plan_build; batch k can be run any number of times.
+ * fsld_loss_grad_planned = fsld_loss_grad_sorted (zbits == NULL) or fsld_loss_grad_hutch_sorted
+ * (zbits != NULL) for batch k; fsld_proj_energy_planned = fsld_proj_energy_sorted for batch k.
+ * scratch: fsld_scratch_bytes(M, n_mask, B) (per-CTA partial sums).
+ */
+size_t fsld_plan_bytes(int M, int n_mask, int B, int K, int64_t total_pairs);
+int fsld_plan_build(int M, int n_mask, const fsld_image_rec* recs, const int32_t* idx, int K, int B,
+                    const int32_t* seg_off, const int32_t* segs, int64_t total_pairs, void* plan, size_t plan_bytes,
+                    void* stream);
+int fsld_loss_grad_planned(int M, int mode, int n_mask, const fsld_image_rec* recs, const void* plan, int B, int k,
+                           const void* v, const void* xs, const int8_t* pc, const uint32_t* zbits, void* grad_acc,
+                           float* fold, double* sq_out, void* scratch, size_t scratch_bytes, void* stream);
+int fsld_proj_energy_planned(int M, int mode, int n_mask, const fsld_image_rec* recs, const void* plan, int B, int k,
+                             const void* d, const int8_t* pc, double* out, void* scratch, size_t scratch_bytes,
+                             void* stream);
+
+/*
  * Touched-ball compaction for the data-parallel all-reduce: a scatter can only reach
  * voxels within radius R + 1/2 + sqrt(3) of the origin (mask radius R; Appendix A item 7), ~54 %
  * of the cube at M=128, so ranks all-reduce the compacted vector.  idx: (n,) int32 voxel indices

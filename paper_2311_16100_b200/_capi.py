@@ -102,6 +102,10 @@ SIGNATURES = {
     "fsld_hutch_fold_sorted": (I, [I, I, I, P, P, I, P, P, P, P, I, P, P, SZ, P]),
     "fsld_apply_step": (I, [I64, P, P, P, P]),
     "fsld_ball_gather": (I, [I64, P, P, P, I, P]),
+    "fsld_plan_bytes": (SZ, [I, I, I, I, I64]),
+    "fsld_plan_build": (I, [I, I, P, P, I, I, P, P, I64, P, SZ, P]),
+    "fsld_loss_grad_planned": (I, [I, I, I, P, P, I, I, P, P, P, P, P, P, P, P, SZ, P]),
+    "fsld_proj_energy_planned": (I, [I, I, I, P, P, I, I, P, P, P, P, SZ, P]),
     "fsld_ball_scatter": (I, [I64, P, P, P, I, P]),
 }
 

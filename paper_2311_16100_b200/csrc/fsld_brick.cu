@@ -292,16 +292,19 @@ __global__ void __launch_bounds__(128) bin_sorted_kernel(SortedArgs a) {
 // and the partial remainders after them, so the persistent kernel's last
 // claims are the small items (shorter tail).  One CTA of 1024 threads,
 // warp-shuffle scans.  Leaves cnt[] zeroed for the next call (fsld_prepare
-// zeroes it once).
-__global__ void __launch_bounds__(1024) brick_scan_kernel(SortedArgs a) {
+// zeroes it once).  ctl = {n_items, claim counter, overflow, pairs base, items base}: the
+// work-item kernels read their pairs at pairs + ctl[3] and their items at items + ctl[4]
+// (both 0 for a single batch; per-batch offsets in a multi-batch plan).
+__device__ void scan_batch(int* cnt, int* off, int* fill, int4* items, int* ctl, int nbr, int cap_items,
+                           int cap_pairs, int pairs_base, int items_base) {
     __shared__ int wp[32], wf[32], wr[32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int per = (a.nbr + 1023) / 1024;
+    const int per = (nbr + 1023) / 1024;
     const int lo = threadIdx.x * per;
-    const int hi = min(lo + per, a.nbr);
+    const int hi = min(lo + per, nbr);
     int np = 0, nf = 0, nr = 0;
     for (int i = lo; i < hi; ++i) {
-        const int c = a.cnt[i];
+        const int c = cnt[i];
         np += c;
         nf += c / BC;
         nr += (c % BC) != 0;
@@ -344,26 +347,135 @@ __global__ void __launch_bounds__(1024) brick_scan_kernel(SortedArgs a) {
     int pbase = (warp > 0 ? wp[warp - 1] : 0) + ip - np;
     int fbase = (warp > 0 ? wf[warp - 1] : 0) + jf - nf;
     int rbase = n_full + (warp > 0 ? wr[warp - 1] : 0) + jr - nr;
+    int4* it = items + items_base;
     for (int i = lo; i < hi; ++i) {
-        const int c = a.cnt[i];
-        a.cnt[i] = 0;
-        a.off[i] = pbase;
-        a.fill[i] = 0;
+        const int c = cnt[i];
+        cnt[i] = 0;
+        off[i] = pbase;
+        fill[i] = 0;
         int k = 0;
         for (; k + BC <= c; k += BC, ++fbase)
-            if (fbase < a.cap_items) a.items[fbase] = make_int4(i, pbase + k, BC, 0);
+            if (fbase < cap_items) it[fbase] = make_int4(i, pbase + k, BC, 0);
         if (k < c) {
-            if (rbase < a.cap_items) a.items[rbase] = make_int4(i, pbase + k, c - k, 0);
+            if (rbase < cap_items) it[rbase] = make_int4(i, pbase + k, c - k, 0);
             ++rbase;
         }
         pbase += c;
     }
     if (threadIdx.x == 1023) {
-        a.off[a.nbr] = wp[31];
-        a.ctl[0] = min(n_full + wr[31], a.cap_items);
-        a.ctl[1] = 0;
-        a.ctl[2] = wp[31] > a.cap_pairs;  // overflow flag (cannot happen for the 4 nb^2 bound)
+        off[nbr] = wp[31];
+        ctl[0] = min(n_full + wr[31], cap_items);
+        ctl[1] = 0;
+        ctl[2] = wp[31] > cap_pairs;  // overflow flag (cannot happen for the 4 nb^2 bound)
+        ctl[3] = pairs_base;
+        ctl[4] = items_base;
     }
+}
+
+__global__ void __launch_bounds__(1024) brick_scan_kernel(SortedArgs a) {
+    scan_batch(a.cnt, a.off, a.fill, a.items, a.ctl, a.nbr, a.cap_items, a.cap_pairs, 0, 0);
+}
+
+// ---------------------------------------------------------------- multi-batch plans
+// The batches of an epoch are known in advance (optim.py:133-139), so their binning can be
+// done for K batches at once: three launches per plan instead of three per step.  Plan layout
+// (PlanLayout): per batch k its own cnt / off / fill / ctl, and shared items / pairs arrays in
+// which batch k starts at ctl_k[4] / ctl_k[3].
+
+__global__ void __launch_bounds__(128) plan_count_kernel(SortedArgs a, int K, int* seg_tot) {
+    const int k = blockIdx.x / a.B, b = blockIdx.x - k * a.B;
+    const int row = a.idx[(size_t)k * a.B + b];
+    const int s0 = a.seg_off[row], s1 = a.seg_off[row + 1];
+    int* cnt = a.cnt + (size_t)k * a.nbr;
+    for (int sidx = s0 + threadIdx.x; sidx < s1; sidx += blockDim.x) atomicAdd(cnt + a.segs[sidx].x, 1);
+    if (threadIdx.x == 0) atomicAdd(seg_tot + k, s1 - s0);
+}
+
+__global__ void __launch_bounds__(1024) plan_scan_kernel(SortedArgs a, int K, const int* seg_tot,
+                                                         int items_cap_total) {
+    __shared__ int base_s;
+    const int k = blockIdx.x;
+    if (threadIdx.x < 32) {  // pairs before batch k
+        int s = 0;
+        for (int q = threadIdx.x; q < k; q += 32) s += seg_tot[q];
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (threadIdx.x == 0) base_s = s;
+    }
+    __syncthreads();
+    const int pairs_base = base_s;
+    // items of batch k <= nbr + pairs_k / BC: a non-overlapping upper-bound layout
+    const int items_base = k * (a.nbr + 2) + (pairs_base + BC - 1) / BC;
+    const int cap = min(a.nbr + seg_tot[k] / BC + 2, items_cap_total - items_base);
+    scan_batch(a.cnt + (size_t)k * a.nbr, a.off + (size_t)k * (a.nbr + 1), a.fill + (size_t)k * a.nbr, a.items,
+               a.ctl + 16 * k, a.nbr, cap, seg_tot[k], pairs_base, items_base);
+}
+
+__global__ void __launch_bounds__(128) plan_fill_kernel(SortedArgs a, int K) {
+    __shared__ SegRec T;
+    const int k = blockIdx.x / a.B, b = blockIdx.x - k * a.B;
+    const int row = a.idx[(size_t)k * a.B + b];
+    const int s0 = a.seg_off[row], s1 = a.seg_off[row + 1];
+    const int* ctl = a.ctl + 16 * k;
+    int* fill = a.fill + (size_t)k * a.nbr;
+    const int* off = a.off + (size_t)k * (a.nbr + 1);
+    SegRec* pairs = a.pairs + ctl[3];
+    if (threadIdx.x < 32) seg_template_warp(a.recs + row, T);
+    __syncthreads();
+    for (int sidx = s0 + threadIdx.x; sidx < s1; sidx += blockDim.x) {
+        const int2 seg = a.segs[sidx];
+        const int slot = atomicAdd(fill + seg.x, 1);
+        SegRec r = T;
+        r.start = (uint32_t)(seg.y & 0xFFFF);
+        r.count = seg.y >> 16;
+        r.row = row;
+        r.gofs = (long long)row * a.n_mask + (seg.y & 0xFFFF);
+        const int4* src = reinterpret_cast<const int4*>(&r);
+        int4* dst = reinterpret_cast<int4*>(pairs + off[seg.x] + slot);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) dst[q] = src[q];
+    }
+}
+
+PlanLayout plan_layout(int M, int B, int K, long long total_pairs) {
+    PlanLayout P{};
+    auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+    const int nb = (M + BT - 1) / BT;
+    P.nbr = nb * nb * nb;
+    P.K = K;
+    P.B = B;
+    P.total_pairs = total_pairs;
+    P.cap_items = (long long)K * (P.nbr + 2) + (total_pairs + BC - 1) / BC + K;
+    size_t o = 0;
+    P.hdr = o; o = al(o + 256);
+    P.cnt = o; o = al(o + sizeof(int) * (size_t)K * P.nbr);
+    P.off = o; o = al(o + sizeof(int) * (size_t)K * (P.nbr + 1));
+    P.fill = o; o = al(o + sizeof(int) * (size_t)K * P.nbr);
+    P.ctl = o; o = al(o + sizeof(int) * 16 * (size_t)K);
+    P.seg_tot = o; o = al(o + sizeof(int) * (size_t)K);
+    P.items = o; o = al(o + sizeof(int4) * (size_t)P.cap_items);
+    P.pairs = o; o = al(o + sizeof(SegRec) * (size_t)(total_pairs > 0 ? total_pairs : 1));
+    P.total = o;
+    return P;
+}
+
+cudaError_t launch_plan_build(SortedArgs a, const PlanLayout& P, char* plan, cudaStream_t s) {
+    // zero the per-batch counters and pair totals (scan leaves cnt / fill zeroed, but a plan
+    // buffer is fresh memory)
+    cudaError_t e = cudaMemsetAsync(plan + P.cnt, 0, P.off - P.cnt, s);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(plan + P.fill, 0, P.items - P.fill, s);
+    if (e != cudaSuccess) return e;
+    a.cnt = reinterpret_cast<int*>(plan + P.cnt);
+    a.off = reinterpret_cast<int*>(plan + P.off);
+    a.fill = reinterpret_cast<int*>(plan + P.fill);
+    a.ctl = reinterpret_cast<int*>(plan + P.ctl);
+    a.items = reinterpret_cast<int4*>(plan + P.items);
+    a.pairs = reinterpret_cast<SegRec*>(plan + P.pairs);
+    int* seg_tot = reinterpret_cast<int*>(plan + P.seg_tot);
+    plan_count_kernel<<<P.K * a.B, 128, 0, s>>>(a, P.K, seg_tot);
+    plan_scan_kernel<<<P.K, 1024, 0, s>>>(a, P.K, seg_tot, (int)P.cap_items);
+    plan_fill_kernel<<<P.K * a.B, 128, 0, s>>>(a, P.K);
+    return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------- main kernel
@@ -401,6 +513,13 @@ cudaError_t launch_sorted_loss_grad(const SortedArgs& a, double* sq_out, cudaStr
     bin_sorted_kernel<false><<<a.B, 128, 0, s>>>(a);
     brick_scan_kernel<<<1, 1024, 0, s>>>(a);
     bin_sorted_kernel<true><<<a.B, 128, 0, s>>>(a);
+    return a.zbits ? launch_sorted_main<true>(a, sq_out, s) : launch_sorted_main<false>(a, sq_out, s);
+}
+
+// One batch of a plan: its work items are ready; re-arm its claim counter and run.
+cudaError_t launch_planned_loss_grad(const SortedArgs& a, double* sq_out, cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(a.ctl + 1, 0, sizeof(int), s);
+    if (e != cudaSuccess) return e;
     return a.zbits ? launch_sorted_main<true>(a, sq_out, s) : launch_sorted_main<false>(a, sq_out, s);
 }
 

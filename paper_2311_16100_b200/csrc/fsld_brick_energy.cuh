@@ -34,6 +34,8 @@ __device__ __forceinline__ float seg_ctf(const SegRec& R, int kx, int ky) {
 __global__ void __launch_bounds__(BTHREADS) sorted_energy_kernel(SortedArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     EnergySmem& S = *reinterpret_cast<EnergySmem*>(smem_raw);
+    a.pairs += a.ctl[3];  // this batch's pairs / items (non-zero offsets in a multi-batch plan)
+    a.items += a.ctl[4];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int M = a.M, c = a.c, nb = a.nb;
     const float bnd = a.bnd;

@@ -26,6 +26,8 @@ struct HutchSmem {
 __global__ void __launch_bounds__(BTHREADS, 4) sorted_hutch_kernel(SortedArgs a, int k, int words) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     HutchSmem& S = *reinterpret_cast<HutchSmem*>(smem_raw);
+    a.pairs += a.ctl[3];  // this batch's pairs / items (non-zero offsets in a multi-batch plan)
+    a.items += a.ctl[4];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int M = a.M, c = a.c, nb = a.nb;
     const float bnd = a.bnd;

@@ -558,3 +558,107 @@ extern "C" int fsld_ball_scatter(int64_t n, const int32_t* idx, const void* src,
     if (n < 1 || !idx || !src || !dst || (elem_bytes != 4 && elem_bytes != 8)) return FSLD_EINVAL;
     return status_of(launch_ball(false, n, idx, src, dst, elem_bytes, reinterpret_cast<cudaStream_t>(stream)));
 }
+
+// ---------------------------------------------------------------- multi-batch binning plans
+
+namespace {
+
+struct PlanKey {
+    const void* plan;
+    int M, n_mask, K, B;
+    long long total_pairs;
+};
+PlanKey g_plans[8];
+int g_plans_next = 0;
+
+void note_plan(const PlanKey& k) {
+    for (PlanKey& p : g_plans)
+        if (p.plan == k.plan) {
+            p = k;
+            return;
+        }
+    g_plans[g_plans_next] = k;
+    g_plans_next = (g_plans_next + 1) % 8;
+}
+
+const PlanKey* find_plan(const void* plan) {
+    for (const PlanKey& p : g_plans)
+        if (p.plan == plan) return &p;
+    return nullptr;
+}
+
+// SortedArgs of batch k of a built plan (work items ready; scratch supplies the partial sums).
+bool make_planned(SortedArgs& b, const void* plan, int M, int n_mask, int B, int k, const fsld_image_rec* recs,
+                  const void* v, const void* xs, const int8_t* pc, void* grad_acc, void* scratch,
+                  size_t scratch_bytes) {
+    const PlanKey* p = find_plan(plan);
+    if (!p || p->M != M || p->n_mask != n_mask || p->B != B || k < 0 || k >= p->K) return false;
+    const ScratchLayout L = scratch_layout(M, n_mask, B);
+    if (scratch_bytes < L.total) return false;
+    const PlanLayout P = plan_layout(M, B, p->K, p->total_pairs);
+    char* pl = reinterpret_cast<char*>(const_cast<void*>(plan));
+    b = make_sorted(L, M, n_mask, B, recs, nullptr, v, xs, pc, nullptr, nullptr, grad_acc, scratch);
+    b.ctl = reinterpret_cast<int*>(pl + P.ctl) + 16 * k;
+    b.items = reinterpret_cast<int4*>(pl + P.items);
+    b.pairs = reinterpret_cast<SegRec*>(pl + P.pairs);
+    b.cnt = b.off = b.fill = nullptr;  // binning already done
+    return true;
+}
+
+}  // namespace
+
+extern "C" size_t fsld_plan_bytes(int M, int n_mask, int B, int K, int64_t total_pairs) {
+    if (M < 2 || M > 256 || n_mask < 1 || B < 1 || K < 1 || total_pairs < 0) return 0;
+    return plan_layout(M, B, K, total_pairs).total;
+}
+
+extern "C" int fsld_plan_build(int M, int n_mask, const fsld_image_rec* recs, const int32_t* idx, int K, int B,
+                               const int32_t* seg_off, const int32_t* segs, int64_t total_pairs, void* plan,
+                               size_t plan_bytes, void* stream) {
+    if (M < 2 || M > 256 || n_mask < 1 || n_mask > M * M || B < 1 || K < 1 || total_pairs < 0) return FSLD_EINVAL;
+    if (!recs || !idx || !seg_off || !segs || !plan) return FSLD_EINVAL;
+    const PlanLayout P = plan_layout(M, B, K, total_pairs);
+    if (plan_bytes < P.total || P.cap_items > 0x7fffffffLL || total_pairs > 0x7fffffffLL) return FSLD_EINVAL;
+    const ScratchLayout L = scratch_layout(M, n_mask, B);
+    SortedArgs a{};
+    a.M = M;
+    a.c = (M + 1) / 2;
+    a.nb = L.nb;
+    a.nbr = L.nbr;
+    a.n_mask = n_mask;
+    a.B = B;
+    a.bnd = (float)(M / 2 - 1);
+    a.recs = recs;
+    a.idx = idx;
+    a.seg_off = seg_off;
+    a.segs = reinterpret_cast<const int2*>(segs);
+    cudaError_t e = launch_plan_build(a, P, reinterpret_cast<char*>(plan), reinterpret_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return FSLD_ECUDA;
+    note_plan(PlanKey{plan, M, n_mask, K, B, (long long)total_pairs});
+    return FSLD_OK;
+}
+
+extern "C" int fsld_loss_grad_planned(int M, int mode, int n_mask, const fsld_image_rec* recs, const void* plan,
+                                      int B, int k, const void* v, const void* xs, const int8_t* pc,
+                                      const uint32_t* zbits, void* grad_acc, float* fold, double* sq_out,
+                                      void* scratch, size_t scratch_bytes, void* stream) {
+    if (!geom_ok(M, mode, n_mask, B) || M > 256 || mode != FSLD_MODE_TRI) return FSLD_EINVAL;
+    if (!recs || !plan || !v || !xs || !pc || !grad_acc || !sq_out || !scratch || (zbits && !fold)) return FSLD_EINVAL;
+    SortedArgs b;
+    if (!make_planned(b, plan, M, n_mask, B, k, recs, v, xs, pc, grad_acc, scratch, scratch_bytes))
+        return FSLD_EINVAL;
+    b.zbits = zbits;
+    b.fold = fold;
+    return status_of(launch_planned_loss_grad(b, sq_out, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+extern "C" int fsld_proj_energy_planned(int M, int mode, int n_mask, const fsld_image_rec* recs, const void* plan,
+                                        int B, int k, const void* d, const int8_t* pc, double* out, void* scratch,
+                                        size_t scratch_bytes, void* stream) {
+    if (!geom_ok(M, mode, n_mask, B) || M > 256 || mode != FSLD_MODE_TRI) return FSLD_EINVAL;
+    if (!recs || !plan || !d || !pc || !out || !scratch) return FSLD_EINVAL;
+    SortedArgs b;
+    if (!make_planned(b, plan, M, n_mask, B, k, recs, d, nullptr, pc, nullptr, scratch, scratch_bytes))
+        return FSLD_EINVAL;
+    return status_of(launch_sorted_energy(b, out, false, reinterpret_cast<cudaStream_t>(stream)));
+}

@@ -83,6 +83,14 @@ struct ScratchLayout {
 
 ScratchLayout scratch_layout(int M, int n_mask, int B);
 
+// Multi-batch binning plan (fsld_plan_*): K batches of B images binned at once.
+struct PlanLayout {
+    size_t hdr, cnt, off, fill, ctl, seg_tot, items, pairs, total;
+    int nbr, K, B;
+    long long total_pairs, cap_items;
+};
+PlanLayout plan_layout(int M, int B, int K, long long total_pairs);
+
 struct SortedArgs {
     int M, c, nb, nbr, n_mask, B;
     float bnd;
@@ -111,7 +119,9 @@ cudaError_t launch_sorted_count(int M, int n_mask, const short2* pix, const fsld
 cudaError_t launch_sorted_fill(int M, int n_mask, const short2* pix, const fsld_image_rec* recs, int N,
                                const float2* x_in, float2* x_out, char2* pc_out, const int32_t* seg_off,
                                int2* segs, cudaStream_t s);
-cudaError_t launch_sorted_loss_grad(const SortedArgs& a, double* sq_out, cudaStream_t s);  // + hutch if a.zbits
+cudaError_t launch_sorted_loss_grad(const SortedArgs& a, double* sq_out, cudaStream_t s);
+cudaError_t launch_planned_loss_grad(const SortedArgs& a, double* sq_out, cudaStream_t s);
+cudaError_t launch_plan_build(SortedArgs a, const PlanLayout& P, char* plan, cudaStream_t s);  // + hutch if a.zbits
 cudaError_t set_phase_profile(unsigned long long* buf);
 
 cudaError_t launch_slice(int op, int mode, bool det, const SliceArgs& a, int nblocks, cudaStream_t s);

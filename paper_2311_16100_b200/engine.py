@@ -252,6 +252,59 @@ class SliceEngine:
                 "fsld_loss_grad_hutch_sorted")
         return sq
 
+    # ---- multi-batch binning plans (fsld_plan_*) ------------------------------
+    def make_plan(self, batches) -> "BinPlan":
+        """Bin K equal-size batches at once (e.g. the batches of an epoch): each planned step then
+        runs only the work-item kernel.  batches: (K, B) array / list of K index arrays."""
+        if not self.brick_path:
+            raise ValueError("binning plans need the brick path (tri, brick-sorted layout, not deterministic)")
+        lib = C.load()
+        if isinstance(batches, torch.Tensor):
+            bt = batches.to(self.dev, torch.int32).contiguous()
+        else:
+            bt = torch.from_numpy(np.ascontiguousarray(np.stack([np.asarray(b) for b in batches]),
+                                                       dtype=np.int32)).to(self.dev)
+        if bt.dim() != 2 or bt.shape[1] < 1:
+            raise ValueError("batches must be (K, B)")
+        K, B = int(bt.shape[0]), int(bt.shape[1])
+        flat = bt.reshape(-1)
+        if getattr(self, "_seg_off_host", None) is None:  # segment counts per image: host copy, once
+            self._seg_off_host = self.seg_off.cpu().numpy().astype(np.int64)
+        rows = (batches.cpu().numpy() if isinstance(batches, torch.Tensor)
+                else np.stack([np.asarray(b) for b in batches])).reshape(-1).astype(np.int64)
+        so = self._seg_off_host
+        total = int((so[rows + 1] - so[rows]).sum())
+        nbytes = int(lib.fsld_plan_bytes(self.M, self.n_mask, B, K, total))
+        buf = torch.empty(nbytes, dtype=torch.uint8, device=self.dev)
+        C.check(lib.fsld_plan_build(self.M, self.n_mask, ctypes_ptr(self.recs), ctypes_ptr(flat), K, B,
+                                    ctypes_ptr(self.seg_off), ctypes_ptr(self.segs), total, ctypes_ptr(buf), nbytes,
+                                    _stream()), "fsld_plan_build")
+        return BinPlan(buf, bt, K, B, total)
+
+    def loss_grad_planned(self, v, plan: "BinPlan", k: int, acc, zbits=None, fold=None, sq=None):
+        """loss_grad (zbits None) or loss_grad_hutch of batch k of a plan; returns sq (device double)."""
+        lib = C.load()
+        v = self._vol(v)
+        sq = torch.empty(1, dtype=torch.float64, device=self.dev) if sq is None else sq
+        scr = self.scratch(plan.B)
+        C.check(lib.fsld_loss_grad_planned(self.M, self.mode_id, self.n_mask, ctypes_ptr(self.recs),
+                                           ctypes_ptr(plan.buf), plan.B, int(k), ctypes_ptr(v), ctypes_ptr(self.x),
+                                           ctypes_ptr(self.pc), ctypes_ptr(zbits), ctypes_ptr(acc), ctypes_ptr(fold),
+                                           ctypes_ptr(sq), ctypes_ptr(scr), scr.numel() * 8, _stream()),
+                "fsld_loss_grad_planned")
+        return sq
+
+    def proj_energy_planned(self, d, plan: "BinPlan", k: int, out=None) -> torch.Tensor:
+        lib = C.load()
+        d = self._vol(d)
+        out = torch.empty(1, dtype=torch.float64, device=self.dev) if out is None else out
+        scr = self.scratch(plan.B)
+        C.check(lib.fsld_proj_energy_planned(self.M, self.mode_id, self.n_mask, ctypes_ptr(self.recs),
+                                             ctypes_ptr(plan.buf), plan.B, int(k), ctypes_ptr(d), ctypes_ptr(self.pc),
+                                             ctypes_ptr(out), ctypes_ptr(scr), scr.numel() * 8, _stream()),
+                "fsld_proj_energy_planned")
+        return out
+
     def loss(self, v, idx):
         """sum|P v - x|^2 over the batch, device double (optim.py:193-207 data term)."""
         lib = C.load()
@@ -534,6 +587,13 @@ class SliceEngine:
         """v <- v - eta_applied * dir (in place; v must be this engine's complex64 volume)."""
         C.check(C.load().fsld_apply_step(self.n_voxels, ctypes_ptr(v), ctypes_ptr(dir_), ctypes_ptr(st), _stream()),
                 "fsld_apply_step")
+
+
+class BinPlan:
+    """Device buffer of a multi-batch binning plan (fsld_plan_build) and its batches."""
+
+    def __init__(self, buf: torch.Tensor, batches: torch.Tensor, K: int, B: int, total_pairs: int):
+        self.buf, self.batches, self.K, self.B, self.total_pairs = buf, batches, K, B, total_pairs
 
 
 def _rows_contiguous(pix: np.ndarray) -> bool:

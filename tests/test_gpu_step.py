@@ -291,3 +291,30 @@ def test_device_run_ragged_last_batch_vs_oracle(golden, name, seed):
     assert np.array_equal(np.array(tr.step_backtracks), rec[:, 3].astype(int))
     assert np.max(np.abs(np.array(tr.step_f0) - rec[:, 0]) / np.abs(rec[:, 0])) < 1e-4
     assert rel(vol.values, v_ref) < 1e-4
+
+
+def test_binning_plan_matches_per_step_binning():
+    """fsld_plan_build bins K batches at once; each planned step equals the per-step binned call."""
+    from paper_2311_16100_b200 import synth
+    wl = synth.build_workload(synth.CONFIGS["cfg2"], seed=3, n_images=512)
+    e = wl.engine
+    rng = np.random.default_rng(0)
+    batches = np.stack([rng.choice(e.n_images, 96, replace=False) for _ in range(5)])
+    plan = e.make_plan(batches)
+    v = torch.from_numpy((wl.v_true * 0.8).astype(np.complex64)).cuda()
+    zb = e.gen_probes(1, 9)
+    for k in (0, 3, 4, 3):  # any order, repeated
+        acc1 = torch.zeros(e.n_voxels, dtype=torch.complex64, device="cuda")
+        fold1 = torch.zeros(e.n_voxels, dtype=torch.float32, device="cuda")
+        sq1 = e.loss_grad_planned(v, plan, k, acc1, zbits=zb, fold=fold1)
+        acc2 = torch.zeros_like(acc1)
+        fold2 = torch.zeros_like(fold1)
+        sq2 = e.loss_grad_hutch(v, batches[k], zb, acc2, fold2)
+        assert abs(float(sq1) - float(sq2)) / float(sq2) < 1e-6
+        assert rel(acc1.cpu().numpy(), acc2.cpu().numpy()) < 1e-5
+        assert rel(fold1.cpu().numpy(), fold2.cpu().numpy()) < 1e-5
+        q1 = float(e.proj_energy_planned(v, plan, k).item())
+        q2 = float(e.proj_energy(v, batches[k]).item())
+        assert abs(q1 - q2) / q2 < 1e-6
+    with pytest.raises(ValueError):
+        e.loss_grad_planned(v, plan, 5, acc1)  # k out of range
