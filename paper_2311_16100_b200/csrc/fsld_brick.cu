@@ -42,7 +42,8 @@ ScratchLayout scratch_layout(int M, int n_mask, int B) {
     L.cnt = o; o = al(o + sizeof(int) * (size_t)L.nbr);
     L.off = o; o = al(o + sizeof(int) * (size_t)(L.nbr + 1));
     L.fill = o; o = al(o + sizeof(int) * (size_t)L.nbr);
-    L.pairs = o; o = al(o + sizeof(SegRec) * (size_t)L.cap_pairs);
+    L.pairs = o; o = al(o + sizeof(PairRec) * (size_t)L.cap_pairs);
+    L.tmpl = o; o = al(o + sizeof(SegRec) * (size_t)(B > 0 ? B : 1));
     L.items = o; o = al(o + sizeof(int4) * (size_t)L.cap_items);
     L.ctl = o; o = al(o + 64);
     L.part = o; o = al(o + sizeof(double) * (size_t)L.cap_part);
@@ -260,29 +261,37 @@ __device__ void seg_template_warp(const fsld_image_rec* __restrict__ rp, SegRec&
     }
 }
 
+// Fill for one batch image (block-cooperative): its SegRec template -> tmpl[tslot] (written by
+// warp 0), and one 16-byte PairRec per segment at its brick's next slot.
+__device__ __forceinline__ void fill_image(const SortedArgs& a, int row, int tslot, int* fill, const int* off,
+                                           PairRec* pairs, SegRec& T) {
+    const int s0 = a.seg_off[row], s1 = a.seg_off[row + 1];
+    if (threadIdx.x < 32) {
+        seg_template_warp(a.recs + row, T);
+        __syncwarp();
+        if (threadIdx.x < 8)
+            reinterpret_cast<int4*>(a.tmpl + tslot)[threadIdx.x] = reinterpret_cast<const int4*>(&T)[threadIdx.x];
+    }
+    for (int sidx = s0 + threadIdx.x; sidx < s1; sidx += blockDim.x) {
+        const int2 seg = a.segs[sidx];
+        const int slot = atomicAdd(fill + seg.x, 1);
+        PairRec r;
+        r.gofs = (long long)row * a.n_mask + (seg.y & 0xFFFF);
+        r.count = seg.y >> 16;
+        r.tslot = tslot;
+        pairs[off[seg.x] + slot] = r;
+    }
+}
+
 template <bool FILL>
 __global__ void __launch_bounds__(128) bin_sorted_kernel(SortedArgs a) {
     const int b = blockIdx.x;
     const int row = a.idx ? a.idx[b] : b;
-    const int s0 = a.seg_off[row], s1 = a.seg_off[row + 1];
     if (FILL) {
         __shared__ SegRec T;
-        if (threadIdx.x < 32) seg_template_warp(a.recs + row, T);
-        __syncthreads();
-        for (int sidx = s0 + threadIdx.x; sidx < s1; sidx += blockDim.x) {
-            const int2 seg = a.segs[sidx];
-            const int slot = atomicAdd(a.fill + seg.x, 1);
-            SegRec r = T;
-            r.start = (uint32_t)(seg.y & 0xFFFF);
-            r.count = seg.y >> 16;
-            r.row = row;
-            r.gofs = (long long)row * a.n_mask + (seg.y & 0xFFFF);
-            const int4* src = reinterpret_cast<const int4*>(&r);
-            int4* dst = reinterpret_cast<int4*>(a.pairs + a.off[seg.x] + slot);
-#pragma unroll
-            for (int q = 0; q < 8; ++q) dst[q] = src[q];
-        }
+        fill_image(a, row, b, a.fill, a.off, a.pairs, T);
     } else {
+        const int s0 = a.seg_off[row], s1 = a.seg_off[row + 1];
         for (int sidx = s0 + threadIdx.x; sidx < s1; sidx += blockDim.x) atomicAdd(a.cnt + a.segs[sidx].x, 1);
     }
 }
@@ -414,26 +423,8 @@ __global__ void __launch_bounds__(128) plan_fill_kernel(SortedArgs a, int K) {
     __shared__ SegRec T;
     const int k = blockIdx.x / a.B, b = blockIdx.x - k * a.B;
     const int row = a.idx[(size_t)k * a.B + b];
-    const int s0 = a.seg_off[row], s1 = a.seg_off[row + 1];
     const int* ctl = a.ctl + 16 * k;
-    int* fill = a.fill + (size_t)k * a.nbr;
-    const int* off = a.off + (size_t)k * (a.nbr + 1);
-    SegRec* pairs = a.pairs + ctl[3];
-    if (threadIdx.x < 32) seg_template_warp(a.recs + row, T);
-    __syncthreads();
-    for (int sidx = s0 + threadIdx.x; sidx < s1; sidx += blockDim.x) {
-        const int2 seg = a.segs[sidx];
-        const int slot = atomicAdd(fill + seg.x, 1);
-        SegRec r = T;
-        r.start = (uint32_t)(seg.y & 0xFFFF);
-        r.count = seg.y >> 16;
-        r.row = row;
-        r.gofs = (long long)row * a.n_mask + (seg.y & 0xFFFF);
-        const int4* src = reinterpret_cast<const int4*>(&r);
-        int4* dst = reinterpret_cast<int4*>(pairs + off[seg.x] + slot);
-#pragma unroll
-        for (int q = 0; q < 8; ++q) dst[q] = src[q];
-    }
+    fill_image(a, row, k * a.B + b, a.fill + (size_t)k * a.nbr, a.off + (size_t)k * (a.nbr + 1), a.pairs + ctl[3], T);
 }
 
 PlanLayout plan_layout(int M, int B, int K, long long total_pairs) {
@@ -453,7 +444,8 @@ PlanLayout plan_layout(int M, int B, int K, long long total_pairs) {
     P.ctl = o; o = al(o + sizeof(int) * 16 * (size_t)K);
     P.seg_tot = o; o = al(o + sizeof(int) * (size_t)K);
     P.items = o; o = al(o + sizeof(int4) * (size_t)P.cap_items);
-    P.pairs = o; o = al(o + sizeof(SegRec) * (size_t)(total_pairs > 0 ? total_pairs : 1));
+    P.pairs = o; o = al(o + sizeof(PairRec) * (size_t)(total_pairs > 0 ? total_pairs : 1));
+    P.tmpl = o; o = al(o + sizeof(SegRec) * (size_t)K * B);
     P.total = o;
     return P;
 }
@@ -470,7 +462,8 @@ cudaError_t launch_plan_build(SortedArgs a, const PlanLayout& P, char* plan, cud
     a.fill = reinterpret_cast<int*>(plan + P.fill);
     a.ctl = reinterpret_cast<int*>(plan + P.ctl);
     a.items = reinterpret_cast<int4*>(plan + P.items);
-    a.pairs = reinterpret_cast<SegRec*>(plan + P.pairs);
+    a.pairs = reinterpret_cast<PairRec*>(plan + P.pairs);
+    a.tmpl = reinterpret_cast<SegRec*>(plan + P.tmpl);
     int* seg_tot = reinterpret_cast<int*>(plan + P.seg_tot);
     plan_count_kernel<<<P.K * a.B, 128, 0, s>>>(a, P.K, seg_tot);
     plan_scan_kernel<<<P.K, 1024, 0, s>>>(a, P.K, seg_tot, (int)P.cap_items);

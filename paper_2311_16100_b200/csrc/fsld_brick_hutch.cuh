@@ -45,9 +45,8 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_hutch_kernel(SortedArgs a,
         const int bid = item.x, pstart = item.y, nseg = item.z;
         const int ox = -c + BT * (bid % nb), oy = -c + BT * ((bid / nb) % nb), oz = -c + BT * (bid / (nb * nb));
         {
-            const int4* src = reinterpret_cast<const int4*>(a.pairs + pstart);
             int4* dst = reinterpret_cast<int4*>(S.seg);
-            for (int w = threadIdx.x; w < nseg * 8; w += BTHREADS) dst[w] = __ldg(src + w);
+            for (int w = threadIdx.x; w < nseg * 8; w += BTHREADS) dst[w] = seg_chunk(a, pstart + (w >> 3), w & 7);
         }
         if (warp < 2) {
             const int kk = threadIdx.x;

@@ -38,6 +38,7 @@ struct SortedSmemT {
     float4 bgeo[RB];                // pass 1 -> 2: (wx, wy, wz, local corner index)
     float hval[HUTCH ? RB : 1];     // pass 1 -> 2: C^2 P z (also z staging during setup)
     SegRec seg[BC];                 // the item's segment records (gofs rebased to the flat index)
+    PairRec prec[BC];               // the next item's pair records (staged first: their tslots address the templates)
     int pref[BC + 1];               // exclusive prefix of segment lengths
     unsigned char bk[RB];           // round pixel -> segment
     int4 item_desc;                 // first item of this CTA (prologue)
@@ -137,18 +138,37 @@ __device__ __forceinline__ void cp_async8_zfill(void* dst, const void* src, bool
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
+// 16-byte chunk q of the SegRec of pair p: chunk 0 from the PairRec (gofs, count), the rest from
+// the image's template (synchronous version, for the kernels that stage an item in place).
+__device__ __forceinline__ int4 seg_chunk(const SortedArgs& a, int p, int q) {
+    const int4 pr = __ldg(reinterpret_cast<const int4*>(a.pairs + p));  // (gofs lo, gofs hi, count, tslot)
+    if (q == 0) return make_int4(pr.x, pr.y, pr.z, 0);
+    return __ldg(reinterpret_cast<const int4*>(a.tmpl + pr.w) + q);
+}
+
 // Stage a work item's inputs in shared memory without waiting: its segment records, the brick of
 // v (+halo, zero off the grid) and, for HUTCH, the probe sign of each brick voxel (into S.bk).
 // Issued for the NEXT item right after the current item's last pass 1, so the loads overlap that
 // item's pass 2 and flush (none of S.seg / S.vb / S.bk is read after pass 1).
 template <bool HUTCH>
+__device__ __forceinline__ void stage_pairs(SortedSmemT<HUTCH>& S, const SortedArgs& a, int4 item) {
+    for (int k = threadIdx.x; k < item.z; k += BTHREADS) cp_async16(S.prec + k, a.pairs + item.y + k);
+}
+
+// second stage (S.prec of `item` complete and visible): segment records = PairRec + template,
+// the v brick, and for HUTCH the probe sign of each brick voxel (into S.bk)
+template <bool HUTCH>
 __device__ __forceinline__ void stage_item(SortedSmemT<HUTCH>& S, const SortedArgs& a, int4 item, const int* lxyz) {
     const int M = a.M, c = a.c, nb = a.nb;
-    const int bid = item.x, pstart = item.y, nseg = item.z;
+    const int bid = item.x, nseg = item.z;
     const int ox = -c + BT * (bid % nb), oy = -c + BT * ((bid / nb) % nb), oz = -c + BT * (bid / (nb * nb));
-    const int4* src = reinterpret_cast<const int4*>(a.pairs + pstart);
     int4* dst = reinterpret_cast<int4*>(S.seg);
-    for (int w = threadIdx.x; w < nseg * 8; w += BTHREADS) cp_async16(dst + w, src + w);
+    for (int w = threadIdx.x; w < nseg * 8; w += BTHREADS) {
+        const int j = w >> 3, q = w & 7;
+        const PairRec& pr = S.prec[j];
+        if (q == 0) dst[w] = make_int4((int)(unsigned)pr.gofs, (int)(pr.gofs >> 32), pr.count, 0);
+        else cp_async16(dst + w, reinterpret_cast<const int4*>(a.tmpl + pr.tslot) + q);
+    }
 #pragma unroll
     for (int u = 0; u < BU; ++u) {
         if (lxyz[u] < 0) continue;
@@ -211,7 +231,12 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArg
     }
     __syncthreads();
     int4 item = S.item_desc;
-    if (item.x >= 0) stage_item(S, a, item, lxyz);
+    if (item.x >= 0) {
+        stage_pairs(S, a, item);
+        cp_async_wait_all();
+        __syncthreads();
+        stage_item(S, a, item, lxyz);
+    }
     PHASE_INIT();
 
     for (;;) {
@@ -251,6 +276,7 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArg
         }
         __syncthreads();  // (B)
         if (threadIdx.x == kClaimer) S.next_desc = claim();  // everyone has read nxt
+        if (nxt.x >= 0) stage_pairs(S, a, nxt);  // S.prec is free: this item's were consumed before (A)
         if (threadIdx.x < nseg) {  // final prefix; rebase gofs to the flat pixel index
             const int k = threadIdx.x;
             const int p = S.pref[k] + (k >= 32 ? S.wtot[0] : 0);
@@ -341,6 +367,7 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArg
                 }
             }
             lsum += (double)sq;
+            if (r0 + RB >= total && nxt.x >= 0) cp_async_wait_all();  // nxt's pair records (stage_pairs)
             {  // maxima >= 0, so their bit patterns order like ints
                 const int vb_max = __reduce_max_sync(0xffffffffu, __float_as_int(vmax));
                 if (lane == 0) atomicMax(&S.vmax_bits, vb_max);

@@ -94,7 +94,8 @@ SortedArgs make_sorted(const ScratchLayout& L, int M, int n_mask, int B, const f
     b.cnt = reinterpret_cast<int*>(scr + L.cnt);
     b.off = reinterpret_cast<int*>(scr + L.off);
     b.fill = reinterpret_cast<int*>(scr + L.fill);
-    b.pairs = reinterpret_cast<SegRec*>(scr + L.pairs);
+    b.pairs = reinterpret_cast<PairRec*>(scr + L.pairs);
+    b.tmpl = reinterpret_cast<SegRec*>(scr + L.tmpl);
     b.items = reinterpret_cast<int4*>(scr + L.items);
     b.ctl = reinterpret_cast<int*>(scr + L.ctl);
     b.part = reinterpret_cast<double*>(scr + L.part);
@@ -600,7 +601,8 @@ bool make_planned(SortedArgs& b, const void* plan, int M, int n_mask, int B, int
     b = make_sorted(L, M, n_mask, B, recs, nullptr, v, xs, pc, nullptr, nullptr, grad_acc, scratch);
     b.ctl = reinterpret_cast<int*>(pl + P.ctl) + 16 * k;
     b.items = reinterpret_cast<int4*>(pl + P.items);
-    b.pairs = reinterpret_cast<SegRec*>(pl + P.pairs);
+    b.pairs = reinterpret_cast<PairRec*>(pl + P.pairs);
+    b.tmpl = reinterpret_cast<SegRec*>(pl + P.tmpl);
     b.cnt = b.off = b.fill = nullptr;  // binning already done
     return true;
 }

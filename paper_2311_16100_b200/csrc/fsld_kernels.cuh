@@ -76,8 +76,17 @@ struct __align__(16) SegRec {
 };
 static_assert(sizeof(SegRec) == 128, "SegRec is 8 x 16 B");
 
+// Per binned segment in global memory (16 B): the brick kernels assemble a SegRec in shared
+// memory from it and the per-image template (the SegRec fields that depend only on the image).
+struct __align__(16) PairRec {
+    long long gofs;  // row * n_mask + start
+    int count;
+    int tslot;       // index of the image's SegRec template in SortedArgs::tmpl
+};
+static_assert(sizeof(PairRec) == 16, "PairRec is one 16-byte word");
+
 struct ScratchLayout {
-    size_t hdr, cnt, off, fill, pairs, items, ctl, part, total;
+    size_t hdr, cnt, off, fill, pairs, tmpl, items, ctl, part, total;
     int nb, nbr, cap_pairs, cap_items, cap_part;
 };
 
@@ -85,7 +94,7 @@ ScratchLayout scratch_layout(int M, int n_mask, int B);
 
 // Multi-batch binning plan (fsld_plan_*): K batches of B images binned at once.
 struct PlanLayout {
-    size_t hdr, cnt, off, fill, ctl, seg_tot, items, pairs, total;
+    size_t hdr, cnt, off, fill, ctl, seg_tot, items, pairs, tmpl, total;
     int nbr, K, B;
     long long total_pairs, cap_items;
 };
@@ -107,7 +116,8 @@ struct SortedArgs {
     int* cnt;
     int* off;
     int* fill;
-    SegRec* pairs;           // per binned segment, item-contiguous
+    PairRec* pairs;          // per binned segment, item-contiguous
+    SegRec* tmpl;            // per batch image: its SegRec template (tslot = batch position)
     int4* items;             // (brick, first pair, n pairs, 0)
     int* ctl;
     double* part;

@@ -253,33 +253,39 @@ class SliceEngine:
         return sq
 
     # ---- multi-batch binning plans (fsld_plan_*) ------------------------------
-    def make_plan(self, batches) -> "BinPlan":
+    def make_plan(self, batches, build: bool = True) -> "BinPlan":
         """Bin K equal-size batches at once (e.g. the batches of an epoch): each planned step then
-        runs only the work-item kernel.  batches: (K, B) array / list of K index arrays."""
+        runs only the work-item kernel.  batches: (K, B) array / list of K index arrays.
+        build=False only sizes and allocates the plan (build it with build_plan)."""
         if not self.brick_path:
             raise ValueError("binning plans need the brick path (tri, brick-sorted layout, not deterministic)")
         lib = C.load()
-        if isinstance(batches, torch.Tensor):
-            bt = batches.to(self.dev, torch.int32).contiguous()
-        else:
-            bt = torch.from_numpy(np.ascontiguousarray(np.stack([np.asarray(b) for b in batches]),
-                                                       dtype=np.int32)).to(self.dev)
-        if bt.dim() != 2 or bt.shape[1] < 1:
+        rows = (batches.cpu().numpy() if isinstance(batches, torch.Tensor)
+                else np.stack([np.asarray(b) for b in batches])).astype(np.int64)
+        if rows.ndim != 2 or rows.shape[1] < 1:
             raise ValueError("batches must be (K, B)")
-        K, B = int(bt.shape[0]), int(bt.shape[1])
-        flat = bt.reshape(-1)
+        if rows.size and (rows.min() < 0 or rows.max() >= self.n_images):
+            raise IndexError("batch index out of range")
+        K, B = rows.shape
         if getattr(self, "_seg_off_host", None) is None:  # segment counts per image: host copy, once
             self._seg_off_host = self.seg_off.cpu().numpy().astype(np.int64)
-        rows = (batches.cpu().numpy() if isinstance(batches, torch.Tensor)
-                else np.stack([np.asarray(b) for b in batches])).reshape(-1).astype(np.int64)
         so = self._seg_off_host
-        total = int((so[rows + 1] - so[rows]).sum())
+        flat = rows.reshape(-1)
+        total = int((so[flat + 1] - so[flat]).sum())
         nbytes = int(lib.fsld_plan_bytes(self.M, self.n_mask, B, K, total))
         buf = torch.empty(nbytes, dtype=torch.uint8, device=self.dev)
-        C.check(lib.fsld_plan_build(self.M, self.n_mask, ctypes_ptr(self.recs), ctypes_ptr(flat), K, B,
-                                    ctypes_ptr(self.seg_off), ctypes_ptr(self.segs), total, ctypes_ptr(buf), nbytes,
-                                    _stream()), "fsld_plan_build")
-        return BinPlan(buf, bt, K, B, total)
+        bt = torch.from_numpy(flat.astype(np.int32)).to(self.dev)
+        plan = BinPlan(buf, bt.view(K, B), K, B, total)
+        if build:
+            self.build_plan(plan)
+        return plan
+
+    def build_plan(self, plan: "BinPlan") -> None:
+        """The device part of make_plan (count -> scan -> fill for all K batches, three launches)."""
+        C.check(C.load().fsld_plan_build(self.M, self.n_mask, ctypes_ptr(self.recs), ctypes_ptr(plan.batches),
+                                         plan.K, plan.B, ctypes_ptr(self.seg_off), ctypes_ptr(self.segs),
+                                         plan.total_pairs, ctypes_ptr(plan.buf), plan.buf.numel(), _stream()),
+                "fsld_plan_build")
 
     def loss_grad_planned(self, v, plan: "BinPlan", k: int, acc, zbits=None, fold=None, sq=None):
         """loss_grad (zbits None) or loss_grad_hutch of batch k of a plan; returns sq (device double)."""
