@@ -378,12 +378,22 @@ def run(config: OptimConfig, stack, v0=None, reference=None, exact_diag_vec=None
     for epoch in range(n_epochs):
         batches = epoch_batches(n, config.batch_size, config.seed, epoch)
         st.view(torch.int32)[12] = 0  # n_steps: hist rows restart each epoch
+        # binning plan of this rank's share of the epoch's full-size batches (one build per epoch;
+        # a short last batch is binned in its own step)
+        subs = [D.shard_indices(b, rank, ws) if ws > 1 else b for b in batches]
+        plan, plan_k = None, {}
+        if e.brick_path:
+            full = [i for i, sb in enumerate(subs) if len(sb) and len(sb) == len(subs[0])]
+            if len(full) > 1:
+                plan = e.make_plan([subs[i] for i in full])
+                plan_k = {i: j for j, i in enumerate(full)}
         for bi, batch in enumerate(batches):
             nb = len(batch)
             scale = n / nb
             last = epoch == n_epochs - 1 and bi == len(batches) - 1
-            sub = D.shard_indices(batch, rank, ws) if ws > 1 else batch
+            sub = subs[bi]
             idx = e.idx_tensor(sub) if len(sub) else None
+            pk = plan_k.get(bi)
             if estimating:
                 if probes == "reference":
                     zbits, kk = e.pack_probes(rademacher(z_rng, nvox))
@@ -391,7 +401,10 @@ def run(config: OptimConfig, stack, v0=None, reference=None, exact_diag_vec=None
                     zbits, kk = e.gen_probes(1, (config.seed << 32) + epoch * 1000003 + bi), 1
             if ws > 1:
                 # this rank's share of the batch, then one all-reduce of [acc | fold | sum|r|^2]
-                if idx is not None and estimating:
+                if pk is not None:
+                    sq = e.loss_grad_planned(v, plan, pk, acc, zbits=zbits if estimating else None,
+                                             fold=fold if estimating else None)
+                elif idx is not None and estimating:
                     sq = e.loss_grad_hutch(v, idx, zbits, acc, fold)
                 elif idx is not None:
                     sq, _, _ = e.loss_grad(v, idx, acc=acc)
@@ -402,6 +415,10 @@ def run(config: OptimConfig, stack, v0=None, reference=None, exact_diag_vec=None
                 pbuf.all_reduce(group)
                 pbuf.unpack()
                 sq = pbuf.loss()
+                gacc = acc
+            elif pk is not None:  # binned with the epoch's plan
+                sq = e.loss_grad_planned(v, plan, pk, acc, zbits=zbits if estimating else None,
+                                         fold=fold if estimating else None)
                 gacc = acc
             elif estimating and not e.deterministic:
                 # one fused pass: gradient accumulator + the probe's Hutchinson fold
@@ -422,7 +439,9 @@ def run(config: OptimConfig, stack, v0=None, reference=None, exact_diag_vec=None
                                   dhat_fixed=dhat_fixed, dhat_out=dhat_last if last else None)
             if estimating:
                 k += 1
-            if idx is not None:
+            if pk is not None:
+                qq = e.proj_energy_planned(dirv, plan, pk)
+            elif idx is not None:
                 qq = e.proj_energy(dirv, idx, reuse_bins=e.brick_path)  # same batch, same scratch
             else:
                 qq = torch.zeros(1, dtype=torch.float64, device=dev)
