@@ -26,7 +26,7 @@ VARIANTS = ("plain", "precomputed", "estimated", "estimated_nothresh")
 __all__ = [
     "OptimConfig", "PreconditionerState", "RunTrace", "VARIANTS", "epoch_batches", "rademacher",
     "loss_and_grad", "batch_loss", "hutchinson_update", "ema_and_threshold", "threshold_alpha",
-    "armijo_search", "run",
+    "armijo_search", "run", "reference_solve",
 ]
 
 
@@ -477,3 +477,68 @@ def run(config: OptimConfig, stack, v0=None, reference=None, exact_diag_vec=None
     else:
         trace.final_dhat = np.ones(nvox)
     return FourierVolume(_to_host_c128(v), spec), trace
+
+
+# The operator runs in fp32 (products, gathers, atomics): a relative residual below ~1e-6 is not
+# reachable, so tighter requests are served at this floor.
+REF_SOLVE_MIN_TOL = 1e-6
+
+
+def reference_solve(stack, lam: float, mode: str, tol: float = 1e-8, max_iter: int = 500, op=None):
+    """Jacobi-preconditioned CG for H v = b (optim.py:396-450) with every H application on the GPU.
+
+    Same recursion, stopping rule (residual recomputed from scratch before accepting, restart if the
+    recursion drifted) and errors as the reference; vectors are complex128 on the device, each H
+    product is one pass of the fsld_hvp kernel over all images.  ``tol`` below REF_SOLVE_MIN_TOL is
+    raised to it (fp32 operator).
+    """
+    from .forward import DatasetOperator, FourierVolume
+    from .hessian import exact_diag
+
+    if lam <= 0:
+        raise ValueError("reference solve needs lam > 0 (positive definite H)")
+    op = DatasetOperator(stack, mode) if op is None else op
+    e = op.engine
+    all_idx = e.all_indices()
+    acc, fx = e.backproject_dataset(all_idx)
+    b = e.finalize_c(acc, fx, 1.0, 0.0).to(torch.complex128)
+    b_norm = float(torch.linalg.vector_norm(b))
+    if b_norm == 0:
+        return FourierVolume.zeros(op.spec)
+    jacobi = torch.from_numpy(exact_diag(stack.poses, stack.ctfs, lam, mode, op.spec, op.mask)).to(e.dev)
+    tol = max(float(tol), REF_SOLVE_MIN_TOL)
+
+    def apply_h(w):
+        a, f = e.hvp_acc(w.to(torch.complex64), all_idx)
+        return e.finalize_c(a, f, 1.0, 0.0).to(torch.complex128) + lam * w
+
+    def rdot(x, y) -> float:
+        return float(torch.vdot(x, y).real)
+
+    v = torch.zeros_like(b)
+    r = b.clone()
+    y = r / jacobi
+    p = y.clone()
+    rho = rdot(r, y)
+    for _ in range(max_iter):
+        hp = apply_h(p)
+        denom = rdot(p, hp)
+        if denom <= 0:
+            raise NumericalError("CG breakdown: non-positive curvature")
+        step = rho / denom
+        v += step * p
+        r -= step * hp
+        if float(torch.linalg.vector_norm(r)) <= tol * b_norm:
+            r = b - apply_h(v)  # certify with a residual recomputed from scratch
+            if float(torch.linalg.vector_norm(r)) <= tol * b_norm:
+                return FourierVolume(v.cpu().numpy(), op.spec)
+            y = r / jacobi
+            p = y.clone()
+            rho = rdot(r, y)
+            continue
+        y = r / jacobi
+        rho_new = rdot(r, y)
+        beta = rho_new / rho
+        rho = rho_new
+        p = y + beta * p
+    raise NumericalError(f"CG did not reach tolerance {tol} in {max_iter} iterations")

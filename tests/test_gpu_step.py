@@ -318,3 +318,20 @@ def test_binning_plan_matches_per_step_binning():
         assert abs(q1 - q2) / q2 < 1e-6
     with pytest.raises(ValueError):
         e.loss_grad_planned(v, plan, 5, acc1)  # k out of range
+
+
+@pytest.mark.parametrize("name,seed", [("dataset_m16_nn.npz", 3), ("dataset_m16_tri.npz", 4)])
+def test_reference_solve_residual_vs_oracle(golden, name, seed):
+    """Device CG (optim.reference_solve, optim.py:396-450): the returned volume solves H v = b to the
+    fp32 floor, checked with the oracle's fp64 operator (H from oracle hvp, b from oracle b_vector)."""
+    g = golden(name)
+    stack = golden_stack(g, seed)
+    lam = float(g["lam"])
+    vol = Opt.reference_solve(stack, lam, str(g["mode"]))
+    _, oop = _oracle_op(g)
+    idx = np.arange(oop.n_images)
+    b = oop.b_vector()
+    res = oop.hvp(vol.values, idx, lam) - b
+    assert np.linalg.norm(res) / np.linalg.norm(b) < 1e-5
+    with pytest.raises(ValueError):
+        Opt.reference_solve(stack, 0.0, str(g["mode"]))
