@@ -167,6 +167,18 @@ def dataset_fixture(M, N, mode, with_ctf, seed, batch):
     return out
 
 
+def io_fixture():
+    """A tiny FSD1 dataset and FSV1 volume written by the reference's own io module (io.py)."""
+    import fsld.io as fio
+    spec = fsld.GridSpec(8)
+    v = fsld.gaussian_blob_phantom(spec, seed=1)
+    poses = fsld.sample_uniform_poses(5, 1.0, 2)
+    ctfs = [fsld.CtfParams(defocus=1.0 + 0.3 * i, amp_contrast=0.1, b_factor=0.2) for i in range(5)]
+    stack = fsld.synthesize_dataset(v, poses, ctfs, sigma=0.05, mode="tri", mask_radius=3, seed=2)
+    fio.write_dataset(stack, os.path.join(HERE, "tiny_m8.fsd1"))
+    fio.write_volume(v, os.path.join(HERE, "tiny_m8.fsv1"))
+
+
 def main():
     np.savez_compressed(os.path.join(HERE, "kernels_m16.npz"), **kernels_fixture(16, 24, 100))
     np.savez_compressed(os.path.join(HERE, "kernels_m8.npz"), **kernels_fixture(8, 12, 200))
@@ -180,4 +192,8 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if "--io-only" in sys.argv:
+        io_fixture()
+    else:
+        main()
+        io_fixture()

@@ -335,3 +335,21 @@ def test_reference_solve_residual_vs_oracle(golden, name, seed):
     assert np.linalg.norm(res) / np.linalg.norm(b) < 1e-5
     with pytest.raises(ValueError):
         Opt.reference_solve(stack, 0.0, str(g["mode"]))
+
+
+def test_streaming_fsd1_loader_matches_host_reader():
+    """io.load_operator streams the complex128 payload chunk-wise into HBM (masked, complex64 on the
+    device) and gives the same operator as DatasetOperator(read_dataset(path))."""
+    import os
+    from conftest import ROOT
+    from paper_2311_16100_b200 import io as fio
+    path = os.path.join(ROOT, "tests", "golden", "tiny_m8.fsd1")
+    op1, hs = fio.load_operator(path, chunk_images=2)
+    st = fio.read_dataset(path)
+    op2 = DatasetOperator(st)
+    assert np.array_equal(op1.x, op2.x)
+    assert np.array_equal(op1.x, st.images[:, op2.mask].astype(np.complex64).astype(np.complex128))
+    v = np.random.default_rng(0).standard_normal(512) + 0j
+    l1, g1 = F.loss_and_grad(op1, v, np.arange(5), 0.1)
+    l2, g2 = F.loss_and_grad(op2, v, np.arange(5), 0.1)
+    assert abs(l1 - l2) <= 1e-6 * abs(l2) and rel(g1, g2) < 1e-6
