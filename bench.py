@@ -162,6 +162,54 @@ def cpu_workload(cfg, n_images, seed=0):
     return op, v
 
 
+def reference_package():
+    """The unmodified reference package installed in baseline/_ref (pip install --target; git-ignored,
+    travels to the GPU box), or None.  Its numba kernels are the reference's own CPU path."""
+    path = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(path, "fsld")):
+        return None
+    if path not in sys.path:
+        sys.path.insert(0, path)
+    try:
+        import fsld  # noqa: F401
+        import fsld.optim  # noqa: F401
+        return fsld
+    except Exception:  # numba missing / broken install: fall back to the C port
+        return None
+
+
+def reference_operator(fsld, cfg, n_images, seed=0):
+    """The reference's own DatasetOperator on the workload's images: poses and images from the same
+    generators as the GPU arm; the reference computes its phase tables itself; its CTF table is the
+    builder-defined physical CTF (the reference's radial ctf_eval cannot express it)."""
+    oop, v = cpu_workload(cfg, n_images, seed)
+    M = cfg.M
+    spec = fsld.GridSpec(M)
+    from paper_2311_16100_b200 import synth
+    q = synth.haar_quaternions(n_images, seed + 1)
+    sh = synth.normal_shifts(n_images, seed + 2) if cfg.shifts else np.zeros((n_images, 2))
+    poses = [fsld.Pose(q=q[i], t=sh[i]) for i in range(n_images)]
+    images = np.zeros((n_images, M * M), dtype=np.complex128)
+    images[:, oop.mask] = oop.x
+    stack = fsld.ImageStack(spec=spec, images=images, poses=poses, ctfs=None, sigma=1.0, seed=seed,
+                            mask_radius=M // 2 - 1, mode=cfg.mode)
+    op = fsld.DatasetOperator(stack)
+    if cfg.ctf:
+        op.ctf_vals = np.ascontiguousarray(oop.ctf_vals)
+    return op, v
+
+
+def time_reference(fsld, op, v, batch, lam, n_total, steps, warmup):
+    from fsld import optim as ref_optim
+    rng = np.random.default_rng(7)
+    for _ in range(warmup):  # the first call JIT-compiles the numba kernels
+        ref_optim.loss_and_grad(op, v, rng.choice(op.n_images, batch, replace=False), lam, n_total)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        ref_optim.loss_and_grad(op, v, rng.choice(op.n_images, batch, replace=False), lam, n_total)
+    return (time.perf_counter() - t0) / steps
+
+
 def time_cpu(op, v, batch, lam, n_total, steps, warmup):
     from oracle import oracle as O
 
@@ -185,19 +233,36 @@ def cpu_model():
 
 
 def run_reference(args):
-    """--impl reference: the reference's CPU path (oracle port, all host threads) on this config."""
+    """--impl reference: the reference's own CPU path (its numba kernels, installed in baseline/_ref,
+    all host threads) on this config; the C oracle port when the install is unavailable."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    from oracle import oracle as O
     from paper_2311_16100_b200 import synth
 
     cfg = synth.CONFIGS[args.config]
     B = cfg.batch
     n_sub = min(cfg.n_images, max(4 * B, 2048))
-    op, v = cpu_workload(cfg, n_sub)
-    threads = O.max_threads()
-    per = time_cpu(op, v * 0.9, B, args.lam, cfg.n_images, args.steps, args.warmup)
+    fsld = reference_package()
+    threads = os.cpu_count() or 1
+    if fsld is not None:
+        import numba
+        numba.set_num_threads(numba.config.NUMBA_NUM_THREADS)
+        threads = numba.get_num_threads()
+        op, v = reference_operator(fsld, cfg, n_sub)
+        per = time_reference(fsld, op, v * 0.9, B, args.lam, cfg.n_images, args.steps, max(args.warmup, 1))
+        kind = "reference"
+        sample = (f"{args.steps} steps x {B} images drawn from a {n_sub}-image host subset, the reference's "
+                  f"fsld.optim.loss_and_grad (numba {numba.__version__}, {threads} threads, {cpu_model()}); "
+                  f"physical CTF table injected as op.ctf_vals")
+    else:
+        from oracle import oracle as O
+        op, v = cpu_workload(cfg, n_sub)
+        threads = O.max_threads()
+        per = time_cpu(op, v * 0.9, B, args.lam, cfg.n_images, args.steps, args.warmup)
+        kind = "port"
+        sample = (f"{args.steps} steps x {B} images drawn from a {n_sub}-image host subset, C oracle "
+                  f"(fp64, OpenMP {threads} threads, {cpu_model()})")
     val = B / per
     line = {
         "impl": "reference", "metric": "image-slices/sec (fused project+CTF+adjoint, loss+grad)",
@@ -206,9 +271,7 @@ def run_reference(args):
         "dtype": "f64", "data": "synthetic (seeded generators of BASELINE cfg; SURVEY.md 8d)",
         "config": {"workload": cfg.name, "M": cfg.M, "batch_per_step": B, "n_images_total": cfg.n_images,
                    "images_sampled_from": n_sub, "mode": cfg.mode},
-        "cpu_baseline": {"value": val, "unit": "images/s", "cores": threads, "kind": "port",
-                         "sample": f"{args.steps} steps x {B} images drawn from a {n_sub}-image host subset, "
-                                   f"C oracle (fp64, OpenMP {threads} threads, {cpu_model()})"},
+        "cpu_baseline": {"value": val, "unit": "images/s", "cores": threads, "kind": kind, "sample": sample},
         "e2e": {"value": val, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -556,12 +619,21 @@ def e2e_leg(eng, wl, B, lam, n_total, args, world):
 
 
 def cpu_baseline(cfg, B, lam):
-    from oracle import oracle as O
-
+    """A bounded sample of the reference's own CPU path (baseline/_ref), else of the C oracle port."""
     n_sub = 2 * B
+    steps = 4
+    fsld = reference_package()
+    if fsld is not None:
+        import numba
+        threads = numba.get_num_threads()
+        op, v = reference_operator(fsld, cfg, n_sub)
+        per = time_reference(fsld, op, v * 0.9, B, lam, cfg.n_images, steps, 1)
+        return {"value": B / per, "unit": "images/s", "cores": threads, "kind": "reference",
+                "sample": f"{steps} loss+grad steps x {B} images from a {n_sub}-image host subset, the reference's "
+                          f"fsld.optim.loss_and_grad (numba {numba.__version__}, {threads} threads, {cpu_model()})"}
+    from oracle import oracle as O
     op, v = cpu_workload(cfg, n_sub)
     threads = O.max_threads()
-    steps = 4
     per = time_cpu(op, v * 0.9, B, lam, cfg.n_images, steps, 1)
     return {"value": B / per, "unit": "images/s", "cores": threads, "kind": "port",
             "sample": f"{steps} loss+grad steps x {B} images from a {n_sub}-image host subset, C oracle "
