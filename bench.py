@@ -514,7 +514,7 @@ def run_b200(args):
                          "frac": achieved / hbm, "traffic": traffic, "peak_source": src,
                          "kernel": ("fsld_loss_grad_planned: sorted_loss_grad_kernel + loss reduce (+ the plan's binning / K)" if use_plan else ("fsld_loss_grad_sorted: bin count/scan/fill + sorted_loss_grad_kernel + loss reduce" if not flags else "fsld slice_kernel<TRI,LOSS_GRAD> (tile path)")),
                          "kernel_ms": t_kern, "algorithmic_bytes_per_launch": abytes},
-            "gpu_launches": launches_per_step * args.steps,
+            "gpu_launches": launches_per_step * args.steps + (5 if use_plan else 0),  # + plan build (2 memsets, 3 kernels)
             "clocks": clk.summary(),
         }
         if e2e is not None:
