@@ -353,3 +353,25 @@ def test_streaming_fsd1_loader_matches_host_reader():
     l1, g1 = F.loss_and_grad(op1, v, np.arange(5), 0.1)
     l2, g2 = F.loss_and_grad(op2, v, np.arange(5), 0.1)
     assert abs(l1 - l2) <= 1e-6 * abs(l2) and rel(g1, g2) < 1e-6
+
+
+@pytest.mark.parametrize("M,N,B,K", [(33, 40, 1, 3), (16, 24, 24, 1), (64, 64, 17, 4), (256, 20, 6, 2)])
+def test_binning_plan_edge_shapes(M, N, B, K):
+    """Plans at odd M, single-image batches, whole-dataset batches and M=256 equal per-step binning."""
+    from paper_2311_16100_b200 import synth
+    mask = O.disk_mask(M, M // 2 - 1)
+    q = synth.haar_quaternions(N, M + 11)
+    recs = records_for(M, q, synth.normal_shifts(N, M + 12), synth.physical_ctfs(N, M + 13))
+    rng = np.random.default_rng(M)
+    x = (rng.standard_normal((N, mask.size)) + 1j * rng.standard_normal((N, mask.size))).astype(np.complex64)
+    e = SliceEngine(M, "tri", mask, recs, x)
+    assert e.brick_path
+    batches = np.stack([rng.choice(N, B, replace=False) for _ in range(K)])
+    plan = e.make_plan(batches)
+    v = torch.from_numpy(synth.gaussian_blob_volume(M, 2).astype(np.complex64)).cuda()
+    for k in range(K):
+        acc1 = torch.zeros(M ** 3, dtype=torch.complex64, device="cuda")
+        sq1 = e.loss_grad_planned(v, plan, k, acc1)
+        sq2, acc2, _ = e.loss_grad(v, batches[k])
+        assert abs(float(sq1) - float(sq2)) <= 1e-6 * abs(float(sq2))
+        assert rel(acc1.cpu().numpy(), acc2.cpu().numpy()) < 1e-5
