@@ -99,6 +99,22 @@ __device__ __forceinline__ void load_seg(const SegRec& R, SegRegs& Q) {
     Q.shi[1] = t.y;
 }
 
+// Fixed-point scale 2^k with k = floor(log2(lim / vm)) exactly (integer exponent / mantissa
+// comparison: no log2 / exp2 / division on the per-round path); inv = 2^-k.  vm = 0 -> 1.
+__device__ __forceinline__ float pow2_scale(float lim, float vm, float& inv) {
+    const int bl = __float_as_int(lim), bv = __float_as_int(vm);
+    const int el = (bl >> 23) & 0xff, ev = (bv >> 23) & 0xff;
+    if (ev == 0 || el == 0) {  // zero or denormal maximum: the slow formula
+        const float sc = vm > 0.f ? exp2f(floorf(log2f(lim / vm))) : 1.0f;
+        inv = 1.0f / sc;
+        return sc;
+    }
+    int k = el - ev - ((bl & 0x7fffff) < (bv & 0x7fffff) ? 1 : 0);
+    k = max(-126, min(126, k));
+    inv = __int_as_float((127 - k) << 23);
+    return __int_as_float((127 + k) << 23);
+}
+
 // hi32(F * u mod 2^64) for F = hi:lo (64-bit fixed-point turns), u < 2^32, wrapping
 __device__ __forceinline__ uint32_t turns_term(uint32_t lo, uint32_t hi, uint32_t u) {
     return hi * u + __umulhi(lo, u);
@@ -287,6 +303,8 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArg
         __syncthreads();
         PHASE_MARK(0);
         const int total = S.pref[nseg];
+        // fixed-point budget: <= 12 contributions per voxel per image segment -> |sum| < 2^31
+        const float lim = fminf(4194303.0f, 178956970.0f / (float)nseg);
 
         for (int r0 = 0; r0 < total; r0 += RB) {
             const int rn = min(RB, total - r0);
@@ -380,16 +398,13 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArg
             PHASE_MARK(2);
             if (r0 + RB >= total && nxt.x >= 0) stage_item(S, a, nxt, lxyz);  // overlaps pass 2 + flush
             // ---------------- pass 2: fixed-point adjoint scatter (kernels.py:221-230)
-            // <= 12 contributions per voxel per image segment -> |sum| < 2^31
-            const float lim = fminf(4194303.0f, 178956970.0f / (float)nseg);
             const float vm = __int_as_float(S.vmax_bits);
-            const float sc = vm > 0.f ? exp2f(floorf(log2f(lim / vm))) : 1.0f;
-            const float inv_sc = 1.0f / sc;
+            float inv_sc;
+            const float sc = pow2_scale(lim, vm, inv_sc);
             float sch = 1.0f, inv_sch = 1.0f;
             if (HUTCH) {
                 const float hm = __int_as_float(S.hmax_bits);
-                sch = hm > 0.f ? exp2f(floorf(log2f(lim / hm))) : 1.0f;
-                inv_sch = 1.0f / sch;
+                sch = pow2_scale(lim, hm, inv_sch);
             }
 #if defined(FSLD_EXP_NO_PASS2)
             for (int e = threadIdx.x; e < 0; e += BTHREADS) {
