@@ -127,7 +127,7 @@ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
 __global__ void gen_probes_kernel(int64_t n, int k, int words, uint64_t seed, uint32_t* __restrict__ zbits) {
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (tid >= n * words) return;
-    const int wd = (int)(tid % words);
+    const int wd = words == 1 ? 0 : (int)((uint32_t)tid % (uint32_t)words);  // n * words < 2^32
     uint32_t bitsv = (uint32_t)splitmix64(seed ^ splitmix64((uint64_t)tid));
     const int valid = k - wd * 32;
     if (valid < 32) bitsv &= (1u << valid) - 1u;

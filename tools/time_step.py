@@ -44,6 +44,9 @@ tm("precond_step (fixed dhat)", lambda: e.precond_step(acc, v, p0, dirv))
 tm("armijo_terms (tile)", lambda: e.armijo_terms(v, dirv, idx))
 tm("proj_energy (brick)", lambda: e.proj_energy(dirv, idx))
 qq = e.proj_energy(dirv, idx)
+plan = e.make_plan(idx.view(1, -1))
+tm("loss_grad_planned (+probe)", lambda: e.loss_grad_planned(v, plan, 0, acc, zbits=zb, fold=fold))
+tm("proj_energy_planned", lambda: e.proj_energy_planned(dirv, plan, 0))
 tm("armijo_select", lambda: e.armijo_select(sq, vol4[4:5], qq, vol4, 8.0, 1e-3, 0.5, st))
 tm("apply_step", lambda: e.apply_step(v, dirv, st))
 tm("norm2", lambda: e.norm2(v))
