@@ -5,6 +5,7 @@
 // the launch geometry and enqueues the kernels on the caller's stream.
 // Never throws, never synchronises.
 #include <cstdio>
+#include <mutex>
 
 #include "fsld_kernels.cuh"
 
@@ -53,8 +54,10 @@ struct BinKey {
 };
 BinKey g_last_bins[8];
 int g_last_bins_next = 0;
+std::mutex g_registry_mu;  // guards the host-side bin / plan records (any host thread may call the ABI)
 
 void note_bins(const void* scratch, const int32_t* idx, const fsld_image_rec* recs, int M, int n_mask, int B) {
+    std::lock_guard<std::mutex> lk(g_registry_mu);
     for (BinKey& k : g_last_bins)
         if (k.scratch == scratch) {
             k = BinKey{scratch, idx, recs, M, n_mask, B};
@@ -65,6 +68,7 @@ void note_bins(const void* scratch, const int32_t* idx, const fsld_image_rec* re
 }
 
 bool bins_match(const void* scratch, const int32_t* idx, const fsld_image_rec* recs, int M, int n_mask, int B) {
+    std::lock_guard<std::mutex> lk(g_registry_mu);
     for (const BinKey& k : g_last_bins)
         if (k.scratch == scratch)
             return k.idx == idx && k.recs == recs && k.M == M && k.n_mask == n_mask && k.B == B;
@@ -573,6 +577,7 @@ PlanKey g_plans[8];
 int g_plans_next = 0;
 
 void note_plan(const PlanKey& k) {
+    std::lock_guard<std::mutex> lk(g_registry_mu);
     for (PlanKey& p : g_plans)
         if (p.plan == k.plan) {
             p = k;
@@ -582,18 +587,24 @@ void note_plan(const PlanKey& k) {
     g_plans_next = (g_plans_next + 1) % 8;
 }
 
-const PlanKey* find_plan(const void* plan) {
+bool find_plan(const void* plan, PlanKey& out) {
+    std::lock_guard<std::mutex> lk(g_registry_mu);
     for (const PlanKey& p : g_plans)
-        if (p.plan == plan) return &p;
-    return nullptr;
+        if (p.plan == plan) {
+            out = p;
+            return true;
+        }
+    return false;
 }
 
 // SortedArgs of batch k of a built plan (work items ready; scratch supplies the partial sums).
 bool make_planned(SortedArgs& b, const void* plan, int M, int n_mask, int B, int k, const fsld_image_rec* recs,
                   const void* v, const void* xs, const int8_t* pc, void* grad_acc, void* scratch,
                   size_t scratch_bytes) {
-    const PlanKey* p = find_plan(plan);
-    if (!p || p->M != M || p->n_mask != n_mask || p->B != B || k < 0 || k >= p->K) return false;
+    PlanKey pk;
+    if (!find_plan(plan, pk)) return false;
+    const PlanKey* p = &pk;
+    if (p->M != M || p->n_mask != n_mask || p->B != B || k < 0 || k >= p->K) return false;
     const ScratchLayout L = scratch_layout(M, n_mask, B);
     if (scratch_bytes < L.total) return false;
     const PlanLayout P = plan_layout(M, B, p->K, p->total_pairs);
