@@ -306,8 +306,36 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArg
         // fixed-point budget: <= 12 contributions per voxel per image segment -> |sum| < 2^31
         const float lim = fminf(4194303.0f, 178956970.0f / (float)nseg);
 
+        // flush of a completed round: one reduction per touched voxel, accumulators re-zeroed.  It runs
+        // at the start of the next round (alongside the bk build; only pass 2 writes the accumulators,
+        // after the next pass-1 barrier), which saves a barrier per round.
+        auto flush_round = [&](float f_inv_sc, float f_inv_sch) {
+#pragma unroll
+            for (int u = 0; u < BU; ++u) {
+                if (lxyz[u] < 0) continue;
+                const int l = threadIdx.x + u * BTHREADS;
+                const int qr = S.accr[l], qi = S.acci[l];
+                const int qh = HUTCH ? S.acch[l] : 0;
+                if ((qr | qi | qh) == 0) continue;
+                S.accr[l] = 0;
+                S.acci[l] = 0;
+                if (HUTCH) S.acch[l] = 0;
+                const int kx = ox + (lxyz[u] & 15), ky = oy + ((lxyz[u] >> 4) & 15), kz = oz + (lxyz[u] >> 8);
+                if (kx >= M - c || ky >= M - c || kz >= M - c) continue;
+                const size_t j = (size_t)lin_index(kx, ky, kz, M, c);
+                if ((qr | qi) != 0)
+                    red_f32x2(reinterpret_cast<float*>(a.acc) + 2 * j, (float)qr * f_inv_sc, (float)qi * f_inv_sc);
+                if (HUTCH && qh != 0) {
+                    const float hz = (S.zc[l] & 1u) ? (float)qh * f_inv_sch : -(float)qh * f_inv_sch;
+                    atomicAdd(a.fold + j, hz);
+                }
+            }
+        };
+        float prev_inv_sc = 1.0f, prev_inv_sch = 1.0f;
+
         for (int r0 = 0; r0 < total; r0 += RB) {
             const int rn = min(RB, total - r0);
+            if (r0 > 0) flush_round(prev_inv_sc, prev_inv_sch);
             {  // round pixel -> segment table: SEG_T threads per segment
                 const int k = threadIdx.x / SEG_T, q = threadIdx.x % SEG_T;
                 if (k < nseg) {
@@ -444,29 +472,10 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArg
             }
             __syncthreads();
             PHASE_MARK(3);
-            // ---------------- flush this round: one reduction per touched voxel, accumulators re-zeroed
-#pragma unroll
-            for (int u = 0; u < BU; ++u) {
-                if (lxyz[u] < 0) continue;
-                const int l = threadIdx.x + u * BTHREADS;
-                const int qr = S.accr[l], qi = S.acci[l];
-                const int qh = HUTCH ? S.acch[l] : 0;
-                if ((qr | qi | qh) == 0) continue;
-                S.accr[l] = 0;
-                S.acci[l] = 0;
-                if (HUTCH) S.acch[l] = 0;
-                const int kx = ox + (lxyz[u] & 15), ky = oy + ((lxyz[u] >> 4) & 15), kz = oz + (lxyz[u] >> 8);
-                if (kx >= M - c || ky >= M - c || kz >= M - c) continue;
-                const size_t j = (size_t)lin_index(kx, ky, kz, M, c);
-                if ((qr | qi) != 0)
-                    red_f32x2(reinterpret_cast<float*>(a.acc) + 2 * j, (float)qr * inv_sc, (float)qi * inv_sc);
-                if (HUTCH && qh != 0) {
-                    const float hz = (S.zc[l] & 1u) ? (float)qh * inv_sch : -(float)qh * inv_sch;
-                    atomicAdd(a.fold + j, hz);
-                }
-            }
-            __syncthreads();
+            prev_inv_sc = inv_sc;
+            prev_inv_sch = inv_sch;
         }
+        flush_round(prev_inv_sc, prev_inv_sch);  // the item's last round (the next item's (A) barrier follows)
         PHASE_MARK(7);
         item = nxt;
     }
