@@ -503,7 +503,8 @@ def run_b200(args):
             "ms_per_step": t_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "c64/f32 (fp64 coords, CTF phase)", "data": "synthetic (seeded generators of BASELINE cfg; SURVEY.md 8d)",
             "config": {"workload": cfg.name, "M": M, "n_mask": n, "batch_per_gpu": B,
-                       "n_images_per_gpu": eng.n_images, "mode": cfg.mode, "ctf": "physical astigmatic",
+                       "n_images_per_gpu": eng.n_images, "mode": cfg.mode,
+                       "ctf": "physical astigmatic" if cfg.ctf else "none", "shifts": bool(cfg.shifts),
                        "parallelism": f"dp{world}", "l2": "flushed between timed steps (512 MB write)",
                        "allreduce_bytes": (8 * nball + 8) if world > 1 else 0,
                        "step": "CUDA graph replay" if world == 1 and not os.environ.get("FSLD_NO_GRAPH") else "eager",
@@ -512,7 +513,7 @@ def run_b200(args):
                        if use_plan else "per step (count -> scan -> fill kernels)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic, "peak_source": src,
-                         "kernel": ("fsld_loss_grad_planned: sorted_loss_grad_kernel + loss reduce (+ the plan's binning / K)" if use_plan else ("fsld_loss_grad_sorted: bin count/scan/fill + sorted_loss_grad_kernel + loss reduce" if not flags else "fsld slice_kernel<TRI,LOSS_GRAD> (tile path)")),
+                         "kernel": ("fsld_loss_grad_planned: sorted_loss_grad_kernel + loss reduce (+ the plan's binning / K)" if use_plan else ("fsld_loss_grad_sorted: bin count/scan/fill + sorted_loss_grad_kernel + loss reduce" if eng.brick_path else f"fsld slice_kernel<{cfg.mode.upper()},LOSS_GRAD> (tile path)")),
                          "kernel_ms": t_kern, "algorithmic_bytes_per_launch": abytes},
             "gpu_launches": launches_per_step * args.steps + (5 if use_plan else 0),  # + plan build (2 memsets, 3 kernels)
             "clocks": clk.summary(),
