@@ -335,7 +335,7 @@ def run_b200(args):
     stream = _stream()
     flags = C.TILE_PATH if os.environ.get("FSLD_TILE_PATH") else 0
     # loss_grad: count + scan + fill + brick kernel + reduce (5 kernels, + cnt memset); fused epilogue (2)
-    launches_per_step = (7 if not flags else 4) + (2 if world > 1 else 0)
+    launches_per_step = (7 if eng.brick_path and not flags else 4) + (2 if world > 1 else 0)
 
     loss = torch.empty(1, dtype=torch.float64, device=dev)
 
