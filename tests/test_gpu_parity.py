@@ -412,3 +412,29 @@ def test_odd_sizes_and_small_masks_vs_oracle(M, radius):
     assert rel(op.project(v, batch), oop.project(v, batch)) < TOL
     # nn indices stay bit-exact at odd M
     assert np.array_equal(K.assign_nn(oop.rots[batch], pix, M), O.assign_nn(oop.rots[batch], pix, M))
+
+
+@pytest.mark.parametrize("M", [128, 256])
+def test_large_defocus_phase_brick_vs_oracle(M):
+    """Stress the fixed-point CTF / shift phases of the brick path: 5 um defocus, 0.5 um astigmatism,
+    10 px shifts (gamma ~ 10^3 - 10^4 rad at the mask edge), checked against the fp64 oracle."""
+    B = 12
+    mask = O.disk_mask(M, M // 2 - 1)
+    pix = O.mask_pix(M, mask)
+    q = synth.haar_quaternions(B, M + 5)
+    rng = np.random.default_rng(M)
+    sh = rng.normal(0.0, 10.0, (B, 2))
+    ctfs = [PhysicalCtf(defocus=float(d), astig=5.0e3, astig_angle=float(a), voltage_kv=300.0, cs_mm=2.7,
+                        amp_contrast=0.07, apix=0.8)
+            for d, a in zip(rng.uniform(3.0e4, 5.0e4, B), rng.uniform(0, np.pi, B))]
+    ctab = O.ctf_table_physical(synth.ctf_param_array(ctfs), pix, M)
+    v = synth.gaussian_blob_volume(M, 3)
+    x = (rng.standard_normal((B, mask.size)) + 1j * rng.standard_normal((B, mask.size)))
+    oop = O.OracleOperator(M, "tri", mask, q, sh, ctab, x)
+    op = gpu_op(M, "tri", mask, q, sh, ctfs, x)
+    assert op.engine.brick_path
+    batch = np.arange(B)
+    lr, gr = O.loss_and_grad(oop, v, batch, 1e-3)
+    lg, gg = F.loss_and_grad(op, v, batch, 1e-3)
+    assert abs(lg - lr) / lr < TOL
+    assert rel(gg, gr) < TOL
