@@ -12,7 +12,7 @@ struct EnergySmem {
     float2 vb[BH3];
     SegRec seg[BC];
     int pref[BC + 1];
-    int wtot[2];
+    int wtot[BC / 32];
     unsigned char bk[RB];
     int4 item_desc;
     double red[BW];
@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(BTHREADS) sorted_energy_kernel(SortedArgs a) {
             int4* dst = reinterpret_cast<int4*>(S.seg);
             for (int w = threadIdx.x; w < nseg * 8; w += BTHREADS) dst[w] = seg_chunk(a, pstart + (w >> 3), w & 7);
         }
-        if (warp < 2) {
+        if (warp < BC / 32) {
             const int k = threadIdx.x;
             const int len = k < nseg ? __ldg(&a.pairs[pstart + k].count) : 0;
             int incl = len;
@@ -75,11 +75,16 @@ __global__ void __launch_bounds__(BTHREADS) sorted_energy_kernel(SortedArgs a) {
         __syncthreads();
         if (threadIdx.x < nseg) {
             const int k = threadIdx.x;
-            const int p = S.pref[k] + (k >= 32 ? S.wtot[0] : 0);
+            int p = S.pref[k];
+            for (int w = 0; w < (k >> 5); ++w) p += S.wtot[w];
             S.pref[k] = p;
             S.seg[k].gofs -= p;
         }
-        if (threadIdx.x == 0) S.pref[nseg] = S.wtot[0] + (nseg > 32 ? S.wtot[1] : 0);
+        if (threadIdx.x == 0) {
+            int t = 0;
+            for (int w = 0; w < BC / 32; ++w) t += S.wtot[w];
+            S.pref[nseg] = t;
+        }
         __syncthreads();
         const int total = S.pref[nseg];
         for (int r0 = 0; r0 < total; r0 += RB) {

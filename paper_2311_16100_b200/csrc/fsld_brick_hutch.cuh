@@ -18,7 +18,7 @@ struct HutchSmem {
     int acc[BH3];
     SegRec seg[BC];
     int pref[BC + 1];
-    int wtot[2];
+    int wtot[BC / 32];
     unsigned char bk[RB];
     int4 item_desc;
 };
@@ -48,7 +48,7 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_hutch_kernel(SortedArgs a,
             int4* dst = reinterpret_cast<int4*>(S.seg);
             for (int w = threadIdx.x; w < nseg * 8; w += BTHREADS) dst[w] = seg_chunk(a, pstart + (w >> 3), w & 7);
         }
-        if (warp < 2) {
+        if (warp < BC / 32) {
             const int kk = threadIdx.x;
             const int len = kk < nseg ? __ldg(&a.pairs[pstart + kk].count) : 0;
             int incl = len;
@@ -69,11 +69,16 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_hutch_kernel(SortedArgs a,
         __syncthreads();
         if (threadIdx.x < nseg) {
             const int kk = threadIdx.x;
-            const int p = S.pref[kk] + (kk >= 32 ? S.wtot[0] : 0);
+            int p = S.pref[kk];
+            for (int w = 0; w < (kk >> 5); ++w) p += S.wtot[w];
             S.pref[kk] = p;
             S.seg[kk].gofs -= p;
         }
-        if (threadIdx.x == 0) S.pref[nseg] = S.wtot[0] + (nseg > 32 ? S.wtot[1] : 0);
+        if (threadIdx.x == 0) {
+            int t = 0;
+            for (int w = 0; w < BC / 32; ++w) t += S.wtot[w];
+            S.pref[nseg] = t;
+        }
         __syncthreads();
         const int total = S.pref[nseg];
         // |C^2 w_c S_c| <= k; <= 12 contributions per voxel per image segment -> |sum| < 2^31

@@ -25,7 +25,7 @@ __device__ unsigned long long* g_phase_prof = nullptr;
 constexpr int RB = 1024;                               // pixels per round (pass 1 -> pass 2 buffer)
 constexpr int BU = (BH3 + BTHREADS - 1) / BTHREADS;    // brick voxels per thread (3)
 constexpr int SEG_T = BTHREADS / BC;                   // threads per segment in the bk build (4)
-static_assert(BTHREADS % BC == 0 && BC <= 64, "segment table is built by two warps");
+static_assert(BTHREADS % BC == 0 && BC % 32 == 0 && BC <= BTHREADS, "segment table: one scan warp per 32 segments");
 
 template <bool HUTCH>
 struct SortedSmemT {
@@ -44,7 +44,7 @@ struct SortedSmemT {
     int4 item_desc;                 // first item of this CTA (prologue)
     int4 next_desc;                 // the item after the current one ((-1, ..) = none)
     int vmax_bits, hmax_bits;
-    int wtot[2];                    // per-warp segment-length totals
+    int wtot[BC / 32];                    // per-warp segment-length totals
     double red[BW];
 };
 
@@ -263,7 +263,7 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArg
         const int bid = item.x, nseg = item.z;
         const int ox = -c + BT * (bid % nb), oy = -c + BT * ((bid / nb) % nb), oz = -c + BT * (bid / (nb * nb));
         // ---------------- setup: segment-length prefix (warps 0, 1) [corner sign masks]
-        if (warp < 2) {
+        if (warp < BC / 32) {
             const int k = threadIdx.x;
             const int len = k < nseg ? S.seg[k].count : 0;
             int incl = len;
@@ -295,11 +295,16 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArg
         if (nxt.x >= 0) stage_pairs(S, a, nxt);  // S.prec is free: this item's were consumed before (A)
         if (threadIdx.x < nseg) {  // final prefix; rebase gofs to the flat pixel index
             const int k = threadIdx.x;
-            const int p = S.pref[k] + (k >= 32 ? S.wtot[0] : 0);
+            int p = S.pref[k];
+            for (int w = 0; w < (k >> 5); ++w) p += S.wtot[w];
             S.pref[k] = p;
             S.seg[k].gofs -= p;
         }
-        if (threadIdx.x == 0) S.pref[nseg] = S.wtot[0] + (nseg > 32 ? S.wtot[1] : 0);
+        if (threadIdx.x == 0) {
+            int t = 0;
+            for (int w = 0; w < BC / 32; ++w) t += S.wtot[w];
+            S.pref[nseg] = t;
+        }
         __syncthreads();
         PHASE_MARK(0);
         const int total = S.pref[nseg];
