@@ -438,3 +438,38 @@ def test_large_defocus_phase_brick_vs_oracle(M):
     lg, gg = F.loss_and_grad(op, v, batch, 1e-3)
     assert abs(lg - lr) / lr < TOL
     assert rel(gg, gr) < TOL
+
+
+from hypothesis import given, settings  # noqa: E402
+from hypothesis import strategies as st  # noqa: E402
+
+
+@settings(max_examples=15, deadline=None)
+@given(M=st.integers(8, 72), B=st.integers(1, 40), seed=st.integers(0, 10 ** 6),
+       radius_frac=st.floats(0.3, 1.0))
+def test_brick_path_randomised_vs_tile_and_coverage(M, B, seed, radius_frac):
+    """Randomised shapes (odd / even M, any mask radius, any batch size): the brick path covers every
+    pixel exactly once and its loss+grad equals the per-pixel tile kernel's."""
+    R = max(1, int(radius_frac * (M // 2 - 1)))
+    mask = O.disk_mask(M, R)
+    rng = np.random.default_rng(seed)
+    q = rng.standard_normal((B, 4))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    sh = rng.normal(0, 2, (B, 2))
+    ctfs = synth.physical_ctfs(B, seed % 1000)
+    recs = records_for(M, q, sh, ctfs)
+    ones = np.ones((B, mask.size), np.complex64)
+    cov = SliceEngine(M, "tri", mask, records_for(M, q), ones)
+    sq, _, _ = cov.loss_grad(torch.zeros(M ** 3, dtype=torch.complex64, device="cuda"), np.arange(B))
+    assert float(sq) == float(B * mask.size)
+    x = torch.from_numpy((rng.standard_normal((B, mask.size)) + 1j * rng.standard_normal((B, mask.size)))
+                         .astype(np.complex64)).cuda()
+    v = torch.from_numpy((rng.standard_normal(M ** 3) + 1j * rng.standard_normal(M ** 3))
+                         .astype(np.complex64)).cuda()
+    brick = SliceEngine(M, "tri", mask, recs, x)
+    tile = SliceEngine(M, "tri", mask, recs, x, tile_path=True)
+    idx = rng.permutation(B)
+    sq1, a1, _ = brick.loss_grad(v, idx)
+    sq2, a2, _ = tile.loss_grad(v, idx)
+    assert abs(float(sq1) - float(sq2)) <= 1e-6 * float(sq2)
+    assert rel(a1.cpu().numpy(), a2.cpu().numpy()) < 1e-5
