@@ -12,15 +12,18 @@
 // are contiguous; per pixel we keep (kx, ky) as int8 (2 B) and per image a
 // segment list (brick, start, count).
 //
-// Per step (all on device, stream-ordered): the batch's segments are counted
-// per brick, scanned into work items (brick, <= BC segments), and filled.  A
-// persistent CTA takes an item, stages the brick's 9^3 voxels of v in shared
-// memory, and its warps walk the item's segments (coalesced loads of x and
-// coordinates): per pixel gather 8 corners from smem -> f = CTF * shift phase
-// -> r = f P v - x -> |r|^2 -> conj(f) r w accumulated into a 9^3 complex smem
-// accumulator (64-bit CAS).  The item ends with one red.global.add.v2.f32 per
-// touched brick voxel.  Every pixel belongs to exactly one segment, so it is
-// processed exactly once.
+// Per step (all on device, stream-ordered; or for K batches at once in a plan):
+// the batch's segments are counted per brick, scanned into work items (brick,
+// <= BC segments) and filled (a 16-byte pair record per segment, a segment-
+// record template per image).  A persistent CTA takes an item, stages the
+// brick's 9^3 voxels of v and the item's segment records in shared memory
+// (the next item's with cp.async while the current one finishes), and walks
+// the item's pixels in rounds: pass 1 gathers 8 corners from shared memory,
+// f = CTF * shift phase, r = f P v - x, |r|^2, and buffers conj(f) r with the
+// corner geometry; pass 2 adds val * w to a shared int32 fixed-point
+// accumulator (scale from the round's max, native ATOMS.ADD); each round is
+// flushed with one red.global.add.v2.f32 per touched brick voxel.  Every pixel
+// belongs to exactly one segment, so it is processed exactly once.
 #include "fsld_kernels.cuh"
 
 namespace fsld {

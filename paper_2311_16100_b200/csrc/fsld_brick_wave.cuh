@@ -2,11 +2,12 @@
 //
 // Within one image, several pixels can share a floor voxel (their 2x2x2
 // footprints coincide).  If two such pixels sit in the same warp when the
-// brick kernel adds their contributions to shared memory, the 64-bit CAS of one
-// of them fails and retries.  Reordering every segment by "wave" -- the rank of
-// a pixel among the pixels of its image with the same floor voxel -- puts
-// pixels with distinct floor voxels next to each other, so a warp-wide CAS
-// almost never collides.  Order is irrelevant to the result (sum), only to speed.
+// brick kernel adds their contributions to shared memory, the two lanes hit
+// the same addresses and their shared atomics serialise.  Reordering every
+// segment by "wave" -- the rank of a pixel among the pixels of its image with
+// the same floor voxel -- puts pixels with distinct floor voxels next to each
+// other.  Order is irrelevant to the result (an order-free integer sum), only
+// to speed.
 #pragma once
 
 __global__ void __launch_bounds__(256) wave_order_kernel(int M, int n_mask, const fsld_image_rec* __restrict__ recs,
