@@ -1,11 +1,13 @@
-"""Loss / gradient / Hutchinson primitives of Algorithm 1 on the B200 path (drop-in for fsld.optim).
+"""Algorithm 1 of the reference on the B200 path (drop-in for fsld.optim).
 
-Same names, signatures and error behaviour as
-/root/reference/pkg/src/fsld/optim.py:98-306.  ``loss_and_grad``,
-``batch_loss`` and ``hutchinson_update`` run one fused sm_100a kernel pass
-over the batch each (fsld_loss_grad / fsld_loss / fsld_hutch_fold); the
-elementwise EMA / threshold / Armijo logic is unchanged and works on numpy
-arrays (reference semantics) or torch CUDA tensors (device-resident loop).
+Same names, signatures and error behaviour as /root/reference/pkg/src/fsld/optim.py:
+``loss_and_grad``, ``batch_loss`` and ``hutchinson_update`` run one fused sm_100a kernel pass over the
+batch each (fsld_loss_grad(_sorted) / fsld_loss / fsld_hutch_fold(_sorted)); ``ema_and_threshold`` and
+``armijo_search`` keep the reference's elementwise logic on numpy arrays (reference semantics) or
+torch CUDA tensors.  ``run`` (optim.py:309-393) keeps every step on the device (fused loss+grad+probe
+pass, fused preconditioner epilogue, closed-form line search, per-epoch binning plans, optional data
+parallelism) and ``reference_solve`` (optim.py:396-450) runs Jacobi-preconditioned CG with the GPU
+Hessian product.
 """
 from __future__ import annotations
 
