@@ -42,6 +42,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-algo1", action="store_true", help="skip the full Algorithm-1 step leg")
     ap.add_argument("--no-sweep", action="store_true", help="skip the cfg5 Hutchinson probe sweep leg")
+    ap.add_argument("--run-epochs", type=int, default=20,
+                    help="cfg3: epochs of the full Algorithm-1 run leg (optim.run; 0 = skip)")
     ap.add_argument("--lam", type=float, default=1e-3)
     return ap.parse_args()
 
@@ -487,6 +489,9 @@ def run_b200(args):
     algo1 = None
     if world == 1 and not args.no_algo1:
         algo1 = algo1_leg(eng, wl, B, lam, args)
+    run = None
+    if world == 1 and args.run_epochs > 0 and args.config == "cfg3" and not args.no_algo1:
+        run = run_leg(eng, wl, B, lam, args.run_epochs)
     sweep = None
     if world == 1 and rank == 0 and not args.no_sweep and args.config == "cfg3":
         _, n_sw, sw = hutch_sweep(argparse.Namespace(images=0, warmup=2, steps=8))
@@ -524,6 +529,8 @@ def run_b200(args):
             line["cpu_baseline"] = cpu
         if algo1 is not None:
             line["algorithm1_step"] = algo1
+        if run is not None:
+            line["algorithm1_run"] = run
         if sweep is not None:
             line["hutchinson_sweep"] = sweep
         print(json.dumps(line), flush=True)
@@ -588,6 +595,56 @@ def algo1_leg(eng, wl, B, lam, args):
                        "(+probe, 3), precond_step (+reduce), proj_energy_planned (3), armijo_select, apply_step",
             "note": "eager launches, L2 not flushed; the reference runs (1 + backtracks) extra loss passes "
                     "per step where this runs one projection of the direction"}
+
+
+def run_leg(eng, wl, B, lam, epochs):
+    """The BASELINE cfg3 run itself: preconditioned SGD (Algorithm 1, estimated variant) over the whole
+    dataset for `epochs` epochs through the public optim.run -- the reference's per-epoch batch
+    permutation (97 full batches of 512 + one of 336 at 50,000 images), one Hutchinson probe per step
+    generated on the device, a binning plan per epoch, closed-form Armijo, and the full-dataset loss
+    at every epoch end.  Wall-clock seconds of the whole call (device-synchronised on both sides,
+    host bookkeeping included)."""
+    import time
+    from types import SimpleNamespace
+
+    import torch
+
+    from paper_2311_16100_b200 import optim
+    from paper_2311_16100_b200.forward import DatasetOperator
+    from paper_2311_16100_b200.grid import GridSpec
+
+    spec = GridSpec(eng.M)
+    stack = SimpleNamespace(spec=spec, mask_radius=eng.M // 2 - 1, n_images=eng.n_images, ctfs=wl.ctfs,
+                            poses=None)
+    op = DatasetOperator.from_engine(eng, spec)
+    conf = optim.OptimConfig(lam=lam, batch_size=B, epochs=epochs, variant="estimated", seed=0)
+    ta = time.perf_counter()
+    alpha = optim.threshold_alpha(stack, None, lam)  # host setup (CTF ring means of every image)
+    t_alpha = time.perf_counter() - ta
+    optim.run(optim.OptimConfig(lam=lam, batch_size=B, epochs=1, variant="estimated", seed=1), stack,
+              probes="device", op=op, alpha=alpha)  # warm-up (allocations, plan sizing)
+    loss0 = 0.5 * float(eng.loss(torch.zeros(eng.M ** 3, dtype=torch.complex64, device=eng.dev),
+                                 eng.all_indices()).item())
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    _, trace = optim.run(conf, stack, probes="device", op=op, alpha=alpha, reference=wl.v_true)
+    torch.cuda.synchronize()
+    sec = time.perf_counter() - t0
+    steps = len(trace.accepted_etas)
+    curve = trace.fsc_history[-1]
+    below = np.flatnonzero(curve < 0.5)
+    return {"epochs": epochs, "steps": steps, "batch": B, "n_images": eng.n_images, "seconds": sec,
+            "ms_per_step": 1e3 * sec / steps, "images_per_s": epochs * eng.n_images / sec,
+            "loss_v0": loss0, "loss_first_epoch": float(trace.loss[0]), "loss_last_epoch": float(trace.loss[-1]),
+            "fsc_0.5_shell_last_epoch": int(below[0]) if below.size else len(curve),
+            "fsc_shells": len(curve),
+            "mean_backtracks": float(np.mean(trace.step_backtracks)),
+            "path": "optim.run(OptimConfig(variant='estimated', batch_size=512), probes='device'): per step "
+                    "probe + planned loss+grad + precond epilogue + direction energy + Armijo + update; "
+                    "per epoch the full-dataset loss, the FSC against the generating volume and one host "
+                    "read of the step records",
+            "timing": "wall clock of the whole call, synchronised, host bookkeeping included; the threshold "
+                      f"alpha (host setup, {t_alpha:.2f} s) computed before the call"}
 
 
 def e2e_leg(eng, wl, B, lam, n_total, args, world):

@@ -252,6 +252,24 @@ def threshold_alpha(stack, shells=None, lam: float = 0.0) -> float:
         pc = pixel_coords(M).astype(np.float64)
         ring = pc[np.round(np.sqrt((pc ** 2).sum(axis=1))) == r]
         csum = 0.0
+        if all(isinstance(c, PhysicalCtf) or hasattr(c, "astig") for c in stack.ctfs):
+            # vectorised over images (same per-element formula as ctf_table_row), summed in image order
+            from .forward import ctf_coefficients
+            co = [ctf_coefficients(c, M) for c in stack.ctfs]
+            g = np.array([t[0] for t in co], dtype=np.float64)
+            env = np.array([t[1] for t in co])[:, None]
+            ws = np.array([t[2] for t in co])[:, None]
+            wc = np.array([t[3] for t in co])[:, None]
+            kx, ky = ring[:, 0][None, :], ring[:, 1][None, :]
+            k2 = kx * kx + ky * ky
+            for lo in range(0, len(co), 4096):
+                s = slice(lo, lo + 4096)
+                gam = (g[s, 0:1] * k2 + g[s, 1:2] * (kx * kx - ky * ky) + g[s, 2:3] * (2 * kx * ky)
+                       + g[s, 3:4] * k2 * k2)
+                row = -(ws[s] * np.sin(gam) + wc[s] * np.cos(gam)) * np.exp(-env[s] * k2)
+                for m in np.mean(row ** 2, axis=1):
+                    csum += float(m)
+            return float(px[r]) / float(vx[r]) * csum + lam
         for c in stack.ctfs:
             if isinstance(c, PhysicalCtf) or hasattr(c, "astig"):
                 csum += float(np.mean(ctf_table_row(c, ring, M) ** 2))
@@ -282,7 +300,7 @@ def armijo_search(v, grad, dhat, loss_fn, eta_in: float, c: float, f0=None):
 
 
 def run(config: OptimConfig, stack, v0=None, reference=None, exact_diag_vec=None, probes: str = "reference",
-        op=None, group=None):
+        op=None, group=None, alpha: float | None = None):
     """Algorithm 1 (optim.py:309-393) with every step resident on the GPU.
 
     Per batch, in stream order and without host synchronisation:
@@ -317,7 +335,8 @@ def run(config: OptimConfig, stack, v0=None, reference=None, exact_diag_vec=None
     e = op.engine
     spec = op.spec
     nvox = spec.n_voxels
-    alpha = threshold_alpha(stack, None, config.lam)
+    if alpha is None:  # (callers that run several times on one dataset may pass it precomputed)
+        alpha = threshold_alpha(stack, None, config.lam)
     n = op.n_images
     if config.batch_size > n:
         raise ValueError("batch_size exceeds the number of images")
