@@ -461,7 +461,7 @@ extern "C" int fsld_precond_step(int64_t nvox, void* acc, const void* v, float* 
                                  const float* dhat_fixed, const fsld_step_params* params, void* dir,
                                  void* grad_out, float* dhat_out, double* out4, void* scratch,
                                  size_t scratch_bytes, void* stream) {
-    const int nparts = 148 * 16;
+    const int nparts = 148 * 4;  // one wave of precond_step_kernel (4 CTAs / SM)
     if (nvox < 1 || !acc || !v || !params || !dir || !out4 || !scratch ||
         scratch_bytes < 5 * nparts * sizeof(double))
         return FSLD_EINVAL;

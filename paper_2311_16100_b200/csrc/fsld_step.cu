@@ -43,9 +43,9 @@ __device__ __forceinline__ void precond_voxel(const fsld_step_params& p, float s
     S.ad += (double)fmaf(a.x, q.x, a.y * q.y);  // Re<A^* r, d> = Re<r, A d>
 }
 
-// Four voxels per thread with 16-byte loads issued up front (streaming, HBM-bound);
+// Two voxels per thread (16-byte volume / accumulator accesses, 8-byte state accesses), 4 CTAs / SM;
 // fp64 per-thread sums, fixed-order block and grid reductions.
-__global__ void __launch_bounds__(kStepThreads) precond_step_kernel(int64_t n, float2* __restrict__ acc,
+__global__ void __launch_bounds__(kStepThreads, 4) precond_step_kernel(int64_t n, float2* __restrict__ acc,
                                                                     const float2* __restrict__ v,
                                                                     float* __restrict__ fold,
                                                                     float* __restrict__ d_avg, float* __restrict__ d,
@@ -54,51 +54,39 @@ __global__ void __launch_bounds__(kStepThreads) precond_step_kernel(int64_t n, f
                                                                     float2* __restrict__ grad_out,
                                                                     float* __restrict__ dhat_out, double* part,
                                                                     int nparts) {
-    __shared__ double smem[32];
+    __shared__ double smem[5][kStepThreads / 32];
     StepSums S{0.0, 0.0, 0.0, 0.0, 0.0};
     const float scale = (float)p.scale, lam = (float)p.lam;
-    const int64_t n4 = n / 4, stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t n4 = n / 2, stride = (int64_t)gridDim.x * blockDim.x;  // voxel pairs
     const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     for (int64_t q4 = t0; q4 < n4; q4 += stride) {
-        const float4 a01 = reinterpret_cast<const float4*>(acc)[2 * q4];
-        const float4 a23 = reinterpret_cast<const float4*>(acc)[2 * q4 + 1];
-        const float4 w01 = __ldg(reinterpret_cast<const float4*>(v) + 2 * q4);
-        const float4 w23 = __ldg(reinterpret_cast<const float4*>(v) + 2 * q4 + 1);
-        float4 fo = make_float4(0.f, 0.f, 0.f, 0.f), da = fo, dd = fo, df = make_float4(1.f, 1.f, 1.f, 1.f);
+        const float4 a01 = reinterpret_cast<const float4*>(acc)[q4];
+        const float4 w01 = __ldg(reinterpret_cast<const float4*>(v) + q4);
+        float2 fo = make_float2(0.f, 0.f), da = fo, dd = fo, df = make_float2(1.f, 1.f);
         if (p.estimating) {
-            fo = reinterpret_cast<const float4*>(fold)[q4];
-            da = reinterpret_cast<const float4*>(d_avg)[q4];
-            dd = reinterpret_cast<const float4*>(d)[q4];
+            fo = reinterpret_cast<const float2*>(fold)[q4];
+            da = reinterpret_cast<const float2*>(d_avg)[q4];
+            dd = reinterpret_cast<const float2*>(d)[q4];
         } else if (dhat_fixed) {
-            df = __ldg(reinterpret_cast<const float4*>(dhat_fixed) + q4);
+            df = __ldg(reinterpret_cast<const float2*>(dhat_fixed) + q4);
         }
-        float2 g[4], q[4];
-        float dh[4];
+        float2 g[2], q[2];
+        float dh[2];
         precond_voxel(p, scale, lam, make_float2(a01.x, a01.y), make_float2(w01.x, w01.y), &fo.x, &da.x, &dd.x, df.x,
                       g[0], q[0], dh[0], S);
         precond_voxel(p, scale, lam, make_float2(a01.z, a01.w), make_float2(w01.z, w01.w), &fo.y, &da.y, &dd.y, df.y,
                       g[1], q[1], dh[1], S);
-        precond_voxel(p, scale, lam, make_float2(a23.x, a23.y), make_float2(w23.x, w23.y), &fo.z, &da.z, &dd.z, df.z,
-                      g[2], q[2], dh[2], S);
-        precond_voxel(p, scale, lam, make_float2(a23.z, a23.w), make_float2(w23.z, w23.w), &fo.w, &da.w, &dd.w, df.w,
-                      g[3], q[3], dh[3], S);
-        const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-        reinterpret_cast<float4*>(acc)[2 * q4] = z4;
-        reinterpret_cast<float4*>(acc)[2 * q4 + 1] = z4;
+        reinterpret_cast<float4*>(acc)[q4] = make_float4(0.f, 0.f, 0.f, 0.f);
         if (p.estimating) {
-            reinterpret_cast<float4*>(fold)[q4] = z4;
-            reinterpret_cast<float4*>(d_avg)[q4] = da;
-            reinterpret_cast<float4*>(d)[q4] = dd;
+            reinterpret_cast<float2*>(fold)[q4] = make_float2(0.f, 0.f);
+            reinterpret_cast<float2*>(d_avg)[q4] = da;
+            reinterpret_cast<float2*>(d)[q4] = dd;
         }
-        reinterpret_cast<float4*>(dir)[2 * q4] = make_float4(q[0].x, q[0].y, q[1].x, q[1].y);
-        reinterpret_cast<float4*>(dir)[2 * q4 + 1] = make_float4(q[2].x, q[2].y, q[3].x, q[3].y);
-        if (grad_out) {
-            reinterpret_cast<float4*>(grad_out)[2 * q4] = make_float4(g[0].x, g[0].y, g[1].x, g[1].y);
-            reinterpret_cast<float4*>(grad_out)[2 * q4 + 1] = make_float4(g[2].x, g[2].y, g[3].x, g[3].y);
-        }
-        if (dhat_out) reinterpret_cast<float4*>(dhat_out)[q4] = make_float4(dh[0], dh[1], dh[2], dh[3]);
+        reinterpret_cast<float4*>(dir)[q4] = make_float4(q[0].x, q[0].y, q[1].x, q[1].y);
+        if (grad_out) reinterpret_cast<float4*>(grad_out)[q4] = make_float4(g[0].x, g[0].y, g[1].x, g[1].y);
+        if (dhat_out) reinterpret_cast<float2*>(dhat_out)[q4] = make_float2(dh[0], dh[1]);
     }
-    for (int64_t i = 4 * n4 + t0; i < n; i += stride) {  // tail (n not a multiple of 4)
+    for (int64_t i = 2 * n4 + t0; i < n; i += stride) {  // tail (n odd)
         float fo = p.estimating ? fold[i] : 0.f, da = p.estimating ? d_avg[i] : 0.f, dd = p.estimating ? d[i] : 0.f;
         float2 g, q;
         float dh;
@@ -113,20 +101,20 @@ __global__ void __launch_bounds__(kStepThreads) precond_step_kernel(int64_t n, f
         if (grad_out) grad_out[i] = g;
         if (dhat_out) dhat_out[i] = dh;
     }
-    double t = block_sum(S.dec, smem);
-    if (threadIdx.x == 0) part[blockIdx.x] = t;
+    // the five block sums with one barrier: warp shuffles, then warp 0 adds the per-warp partials in order
+    double x[5] = {S.dec, S.vv, S.vd, S.dd, S.ad};
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        for (int o = 16; o > 0; o >>= 1) x[k] += __shfl_xor_sync(0xffffffffu, x[k], o);
+        if (lane == 0) smem[k][wid] = x[k];
+    }
     __syncthreads();
-    t = block_sum(S.vv, smem);
-    if (threadIdx.x == 0) part[nparts + blockIdx.x] = t;
-    __syncthreads();
-    t = block_sum(S.vd, smem);
-    if (threadIdx.x == 0) part[2 * nparts + blockIdx.x] = t;
-    __syncthreads();
-    t = block_sum(S.dd, smem);
-    if (threadIdx.x == 0) part[3 * nparts + blockIdx.x] = t;
-    __syncthreads();
-    t = block_sum(S.ad, smem);
-    if (threadIdx.x == 0) part[4 * nparts + blockIdx.x] = t;
+    if (threadIdx.x < 5) {
+        double t = 0.0;
+        for (int w = 0; w < kStepThreads / 32; ++w) t += smem[threadIdx.x][w];
+        part[threadIdx.x * nparts + blockIdx.x] = t;
+    }
 }
 
 cudaError_t launch_precond_step(int64_t nvox, float2* acc, const float2* v, float* fold, float* d_avg, float* d,
