@@ -492,6 +492,9 @@ def run_b200(args):
     run = None
     if world == 1 and args.run_epochs > 0 and args.config == "cfg3" and not args.no_algo1:
         run = run_leg(eng, wl, B, lam, args.run_epochs)
+    nxt = None
+    if world == 1 and args.config == "cfg3" and not args.no_algo1:
+        nxt = next_rows_leg(eng, wl)
     sweep = None
     if world == 1 and rank == 0 and not args.no_sweep and args.config == "cfg3":
         _, n_sw, sw = hutch_sweep(argparse.Namespace(images=0, warmup=2, steps=8))
@@ -531,6 +534,8 @@ def run_b200(args):
             line["algorithm1_step"] = algo1
         if run is not None:
             line["algorithm1_run"] = run
+        if nxt is not None:
+            line["next_rows"] = nxt
         if sweep is not None:
             line["hutchinson_sweep"] = sweep
         print(json.dumps(line), flush=True)
@@ -645,6 +650,74 @@ def run_leg(eng, wl, B, lam, epochs):
                     "read of the step records",
             "timing": "wall clock of the whole call, synchronised, host bookkeeping included; the threshold "
                       f"alpha (host setup, {t_alpha:.2f} s) computed before the call"}
+
+
+def next_rows_leg(eng, wl):
+    """SURVEY 8f rows 3-4 (each with its parity test in tests/): full-dataset passes of the exact
+    diagonal, the b-vector adjoint and one CG Hessian product (reference_solve), the device FSC, and
+    the streaming FSD1 ingest (io.load_operator) -- device time per call with CUDA events (ingest:
+    wall clock from file to device-resident dataset)."""
+    import tempfile
+    import time
+
+    import torch
+
+    from paper_2311_16100_b200 import io as fio
+    from paper_2311_16100_b200.forward import ImageStack, Pose
+    from paper_2311_16100_b200.grid import GridSpec, disk_mask
+    from paper_2311_16100_b200.metrics import ShellIndex, fsc
+
+    idx = eng.all_indices()
+    n = idx.numel()
+    dev = eng.dev
+    z = torch.from_numpy((wl.v_true * 0.5).astype(np.complex64)).to(dev)
+
+    def timed(fn, reps=3):
+        fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            fn()
+        b.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps
+
+    out = {"n_images": n}
+    ms = timed(lambda: eng.exact_diag_acc(idx))
+    out["exact_diag"] = {"ms": ms, "images_per_s": n / (ms * 1e-3), "path": "fsld_exact_diag (hessian.exact_diag)"}
+    ms = timed(lambda: eng.backproject_dataset(idx))
+    out["b_vector"] = {"ms": ms, "images_per_s": n / (ms * 1e-3), "path": "fsld_backproject_sorted (b_vector)"}
+    ms = timed(lambda: eng.hvp_acc(z, idx))
+    out["cg_hessian_product"] = {"ms": ms, "images_per_s": n / (ms * 1e-3),
+                                 "path": "fsld_hvp over all images (one reference_solve CG iteration)"}
+    shells = ShellIndex(eng.M, eng.M // 2 - 1, dev)
+    ref = torch.from_numpy(wl.v_true.astype(np.complex64)).to(dev)
+    ms = timed(lambda: fsc(z, ref, shells))
+    out["fsc"] = {"ms": ms, "path": "metrics.fsc (device shell bincounts, one host read)"}
+    # ingest: a synthetic FSD1 file (the reference's on-disk format: complex128 full M^2 images)
+    M, ni = eng.M, 1024
+    rng = np.random.default_rng(7)
+    mask = disk_mask(GridSpec(M), M // 2 - 1)
+    imgs = np.zeros((ni, M * M), dtype=np.complex128)
+    imgs[:, mask] = rng.standard_normal((ni, mask.size)) + 1j * rng.standard_normal((ni, mask.size))
+    q = rng.standard_normal((ni, 4))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    stack = ImageStack(spec=GridSpec(M), images=imgs, poses=[Pose(q=q[i], t=np.zeros(2)) for i in range(ni)],
+                       ctfs=None, sigma=1.0, seed=7, mask_radius=M // 2 - 1, mode="tri")
+    with tempfile.TemporaryDirectory() as td:
+        path = fio.write_dataset(stack, f"{td}/ingest.fsd1")
+        nbytes = path.stat().st_size
+        fio.load_operator(path)  # warm (page cache, allocations)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        op, _ = fio.load_operator(path)
+        torch.cuda.synchronize()
+        sec = time.perf_counter() - t0
+    out["ingest"] = {"images": ni, "file_bytes": nbytes, "seconds": sec, "gb_per_s": nbytes / sec / 1e9,
+                     "path": "io.load_operator: FSD1 chunks -> pinned -> HBM, complex64 masking and the one-time "
+                             "brick sort on the device (file in the page cache)"}
+    return out
 
 
 def e2e_leg(eng, wl, B, lam, n_total, args, world):

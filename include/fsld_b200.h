@@ -244,6 +244,16 @@ int fsld_loss_grad_hutch_sorted(int M, int mode, int n_mask, const fsld_image_re
                                 const int32_t* segs, const uint32_t* zbits, void* grad_acc, float* fold,
                                 double* sq_out, unsigned flags, void* scratch, size_t scratch_bytes, void* stream);
 
+/* Hessian data term on the brick-sorted layout (tri, fp32 accumulation; replaces fsld_hvp,
+ * forward.py:554-570 / hessian.py:110-118, for datasets laid out by fsld_sorted_fill):
+ *   acc += sum_b P_b^* C_b^2 P_b z,   *sq_out = sum_b ||C_b P_b z||^2 = ||A z||^2
+ * The brick loss+grad pass with zero images: r = f P z, conj(f) r = |f|^2 P z.  The caller applies
+ * the n_total/|B| scale and lam (forward.py:567-570).  Deterministic / tile-path flags are rejected
+ * (use fsld_hvp). */
+int fsld_hvp_sorted(int M, int mode, int n_mask, const fsld_image_rec* recs, const int32_t* idx, int B,
+                    const void* z, const int8_t* pc, const int32_t* seg_off, const int32_t* segs, void* acc,
+                    double* sq_out, unsigned flags, void* scratch, size_t scratch_bytes, void* stream);
+
 /* Loss only over a brick-sorted dataset (Armijo trials, optim.py:193-207). */
 int fsld_loss_sorted(int M, int mode, int n_mask, const fsld_image_rec* recs, const int32_t* idx, int B,
                      const void* v, const void* xs, const int8_t* pc, double* sq_out, void* scratch,

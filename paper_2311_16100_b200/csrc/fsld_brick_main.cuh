@@ -374,7 +374,7 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArg
 #if defined(FSLD_EXP_NO_XLOAD)
                 const float2 xv = make_float2((float)(g & 7), 0.f);
 #else
-                const float2 xv = __ldg(a.xs + g);
+                const float2 xv = a.xs ? __ldg(a.xs + g) : make_float2(0.f, 0.f);  // NULL: Hessian product
 #endif
                 const int px = kk.x, py = kk.y;
                 float cx, cy, cz, fx, fy, fz;

@@ -353,6 +353,20 @@ int fsld_loss_grad_sorted(int M, int mode, int n_mask, const fsld_image_rec* rec
     return status_of(launch_sorted_loss_grad(b, sq_out, reinterpret_cast<cudaStream_t>(stream)));
 }
 
+int fsld_hvp_sorted(int M, int mode, int n_mask, const fsld_image_rec* recs, const int32_t* idx, int B, const void* z,
+                    const int8_t* pc, const int32_t* seg_off, const int32_t* segs, void* acc, double* sq_out,
+                    unsigned flags, void* scratch, size_t scratch_bytes, void* stream) {
+    if (!geom_ok(M, mode, n_mask, B) || M > 256 || mode != FSLD_MODE_TRI) return FSLD_EINVAL;
+    if (flags & (FSLD_DETERMINISTIC | FSLD_TILE_PATH)) return FSLD_EINVAL;
+    if (!recs || !idx || !z || !pc || !seg_off || !segs || !acc || !sq_out || !scratch) return FSLD_EINVAL;
+    const ScratchLayout L = scratch_layout(M, n_mask, B);
+    if (scratch_bytes < L.total) return FSLD_EINVAL;
+    // xs = NULL: the kernel takes the images as zero (r = f P z)
+    const SortedArgs b = make_sorted(L, M, n_mask, B, recs, idx, z, nullptr, pc, seg_off, segs, acc, scratch);
+    note_bins(scratch, idx, recs, M, n_mask, B);
+    return status_of(launch_sorted_loss_grad(b, sq_out, reinterpret_cast<cudaStream_t>(stream)));
+}
+
 int fsld_loss_grad_hutch_sorted(int M, int mode, int n_mask, const fsld_image_rec* recs, const int32_t* idx, int B,
                                 const void* v, const void* xs, const int8_t* pc, const int32_t* seg_off,
                                 const int32_t* segs, const uint32_t* zbits, void* grad_acc, float* fold,

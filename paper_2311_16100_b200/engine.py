@@ -382,12 +382,26 @@ class SliceEngine:
                 "fsld_backproject")
         return acc, fx
 
+    HVP_CHUNK = 4096  # images per brick-path Hessian launch (bounds the binning scratch)
+
     def hvp_acc(self, z, idx, acc=None, fx=None, fx_batch=None):
         lib = C.load()
         z = self._vol(z)
         idx = self.idx_tensor(idx)
         B = idx.numel()
         acc = self.new_cacc() if acc is None else acc
+        if self.brick_path and not self.deterministic:
+            # brick-sorted layout: the loss+grad work-item kernel with zero images, in chunks
+            sq = torch.empty(1, dtype=torch.float64, device=self.dev)
+            for lo in range(0, B, self.HVP_CHUNK):
+                sub = idx[lo:lo + self.HVP_CHUNK]
+                nb = sub.numel()
+                scr = self.scratch(nb)
+                C.check(lib.fsld_hvp_sorted(self.M, self.mode_id, self.n_mask, ctypes_ptr(self.recs), ctypes_ptr(sub),
+                                            nb, ctypes_ptr(z), ctypes_ptr(self.pc), ctypes_ptr(self.seg_off),
+                                            ctypes_ptr(self.segs), ctypes_ptr(acc), ctypes_ptr(sq), 0,
+                                            ctypes_ptr(scr), scr.numel() * 8, _stream()), "fsld_hvp_sorted")
+            return acc, fx
         if self.deterministic and fx is None:
             fx = self.fixed_scale(z, HITS_PER_IMAGE * (fx_batch or B), 0.0)
         C.check(lib.fsld_hvp(self.M, self.mode_id, self.n_mask, ctypes_ptr(self.pix), ctypes_ptr(self.recs),

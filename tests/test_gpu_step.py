@@ -275,6 +275,50 @@ def test_brick_probe_batcher_matches_tile_batcher(k):
     assert rel(f1.cpu().numpy(), f2.cpu().numpy()) < 1e-5
 
 
+@pytest.mark.parametrize("M,N,nb", [(32, 96, 64), (64, 300, 300)])
+def test_brick_hessian_product_matches_tile_and_oracle(M, N, nb):
+    """fsld_hvp_sorted (brick loss+grad kernel with zero images) vs fsld_hvp (tile) and the oracle;
+    its sq_out is ||A z||^2 = the line-search energy of z.  HVP_CHUNK is lowered to 128 so that
+    several launches accumulate into one accumulator."""
+    from paper_2311_16100_b200 import synth
+    mask = O.disk_mask(M, M // 2 - 1)
+    q = synth.haar_quaternions(N, 41)
+    sh = synth.normal_shifts(N, 42)
+    ctfs = synth.physical_ctfs(N, 43)
+    pix = O.mask_pix(M, mask)
+    recs = records_for(M, q, sh, ctfs)
+    brick = SliceEngine(M, "tri", mask, recs)
+    tile = SliceEngine(M, "tri", mask, recs, tile_path=True)
+    assert brick.brick_path and not tile.brick_path
+    rng = np.random.default_rng(44)
+    z = torch.from_numpy((rng.standard_normal(M ** 3) + 1j * rng.standard_normal(M ** 3)).astype(np.complex64)).cuda()
+    batch = rng.permutation(N)[:nb]
+    brick.HVP_CHUNK = 128  # several launches accumulate into one acc
+    h1, _ = brick.hvp_acc(z, batch)
+    h2, _ = tile.hvp_acc(z, batch)
+    assert rel(h1.cpu().numpy(), h2.cpu().numpy()) < 1e-5
+    oop = O.OracleOperator(M, "tri", mask, q, sh, O.ctf_table_physical(synth.ctf_param_array(ctfs), pix, M), None)
+    hz = oop.hvp(z.cpu().numpy().astype(np.complex128), batch, 0.0, n_total=len(batch))
+    assert rel(h1.cpu().numpy(), hz) < 1e-5
+    # ||A z||^2 through the ABI (one launch) against the gather-only energy pass
+    idx = brick.idx_tensor(batch)
+    acc = torch.zeros(M ** 3, dtype=torch.complex64, device="cuda")
+    sq = torch.zeros(1, dtype=torch.float64, device="cuda")
+    scr = brick.scratch(nb)
+    from paper_2311_16100_b200.engine import ctypes_ptr, _stream
+    C.check(C.load().fsld_hvp_sorted(M, brick.mode_id, brick.n_mask, ctypes_ptr(brick.recs), ctypes_ptr(idx), nb,
+                                     ctypes_ptr(z), ctypes_ptr(brick.pc), ctypes_ptr(brick.seg_off),
+                                     ctypes_ptr(brick.segs), ctypes_ptr(acc), ctypes_ptr(sq), 0, ctypes_ptr(scr),
+                                     scr.numel() * 8, _stream()), "fsld_hvp_sorted")
+    en = brick.proj_energy(z, batch)
+    assert abs(float(sq) - float(en)) / float(en) < 1e-5
+    assert rel(acc.cpu().numpy(), hz) < 1e-5
+    assert C.load().fsld_hvp_sorted(M, brick.mode_id, brick.n_mask, ctypes_ptr(brick.recs), ctypes_ptr(idx), nb,
+                                    ctypes_ptr(z), ctypes_ptr(brick.pc), ctypes_ptr(brick.seg_off),
+                                    ctypes_ptr(brick.segs), ctypes_ptr(acc), None, 0, ctypes_ptr(scr),
+                                    scr.numel() * 8, _stream()) == C.FSLD_EINVAL
+
+
 @pytest.mark.parametrize("name,seed", [("dataset_m16_nn.npz", 3), ("dataset_m16_tri.npz", 4)])
 def test_device_run_ragged_last_batch_vs_oracle(golden, name, seed):
     """N = 96 with batch_size 28: every epoch ends with a 12-image batch (scale N/12, optim.py:183)."""
