@@ -32,7 +32,14 @@ def ctypes_ptr(t) -> int:
     return 0 if t is None else int(t.data_ptr())
 
 
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def _stream() -> int:
+    """The current torch stream of the current device as a raw cudaStream_t (the capture stream
+    under CUDA-graph capture); the raw accessor avoids building a Stream object per launch."""
+    if _raw_stream is not None:
+        return int(_raw_stream(torch.cuda.current_device()))
     return int(torch.cuda.current_stream().cuda_stream)
 
 

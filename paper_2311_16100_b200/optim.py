@@ -413,8 +413,9 @@ def run(config: OptimConfig, stack, v0=None, reference=None, exact_diag_vec=None
             scale = n / nb
             last = epoch == n_epochs - 1 and bi == len(batches) - 1
             sub = subs[bi]
-            idx = e.idx_tensor(sub) if len(sub) else None
             pk = plan_k.get(bi)
+            # (planned steps never touch idx: no per-step host->device upload of the batch)
+            idx = e.idx_tensor(sub) if len(sub) and pk is None else None
             if estimating:
                 if probes == "reference":
                     zbits, kk = e.pack_probes(rademacher(z_rng, nvox))
