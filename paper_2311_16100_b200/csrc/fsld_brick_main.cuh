@@ -206,11 +206,12 @@ __device__ __forceinline__ void stage_item(SortedSmemT<HUTCH>& S, const SortedAr
 //     1. gather 8 corners from the smem brick, f = C * phase, r = f P v - x,
 //        |r|^2 -> loss; conj(f) r and the corner geometry -> smem buffers
 //        [HUTCH: h = |f|^2 P z from the corner signs -> smem buffer];
-//     2. with the round's max |val| known, quantise val * w to int32 with a
-//        power-of-two scale (|val w s| <= min(2^22, 2^31 / (12 nseg)): <= 12
-//        contributions per voxel per image) and add with native ATOMS.ADD
-//        [HUTCH: the same for h w into a real accumulator];
-//     3. flush: one red.global.add.v2.f32 per touched brick voxel
+//     2. with the round's max |val| known, quantise val * w to int32 with the
+//        item's power-of-two scale (|val w s| <= min(2^22, 2^31 / (12 nseg)):
+//        <= 12 contributions per voxel per image; a round that needs a smaller
+//        scale first shifts the partial sums down to it) and add with native
+//        ATOMS.ADD [HUTCH: the same for h w into a real accumulator];
+//   flush, once per item: one red.global.add.v2.f32 per touched brick voxel
 //        [HUTCH: fold_j += z_j h_j, one red.global.add.f32], accumulators zeroed.
 template <bool HUTCH>
 __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArgs a) {
@@ -311,9 +312,7 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArg
         // fixed-point budget: <= 12 contributions per voxel per image segment -> |sum| < 2^31
         const float lim = fminf(4194303.0f, 178956970.0f / (float)nseg);
 
-        // flush of a completed round: one reduction per touched voxel, accumulators re-zeroed.  It runs
-        // at the start of the next round (alongside the bk build; only pass 2 writes the accumulators,
-        // after the next pass-1 barrier), which saves a barrier per round.
+        // flush of a completed item: one reduction per touched voxel, accumulators re-zeroed
         auto flush_round = [&](float f_inv_sc, float f_inv_sch) {
 #pragma unroll
             for (int u = 0; u < BU; ++u) {
@@ -336,11 +335,29 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArg
                 }
             }
         };
-        float prev_inv_sc = 1.0f, prev_inv_sch = 1.0f;
+        // One fixed-point scale per item, power of two and non-increasing over its rounds: a round
+        // whose maximum needs a smaller scale first shifts the partial sums down (rounded) to it, so
+        // the accumulators carry the whole item and are flushed once.  The overflow budget holds
+        // for the whole item: <= 12 contributions per voxel per image over all of its rounds.
+        float item_sc = 0.f, item_inv_sc = 1.f, item_sch = 0.f, item_inv_sch = 1.f;
+        auto rescale = [&](int sh, int* acc_a, int* acc_b) {
+#pragma unroll
+            for (int u = 0; u < BU; ++u) {
+                if (lxyz[u] < 0) continue;
+                const int l = threadIdx.x + u * BTHREADS;
+                if (sh >= 31) {
+                    acc_a[l] = 0;
+                    if (acc_b) acc_b[l] = 0;
+                } else {
+                    const long long half = 1ll << (sh - 1);  // rounded (64-bit: no overflow near 2^31)
+                    acc_a[l] = (int)(((long long)acc_a[l] + half) >> sh);
+                    if (acc_b) acc_b[l] = (int)(((long long)acc_b[l] + half) >> sh);
+                }
+            }
+        };
 
         for (int r0 = 0; r0 < total; r0 += RB) {
             const int rn = min(RB, total - r0);
-            if (r0 > 0) flush_round(prev_inv_sc, prev_inv_sch);
             {  // round pixel -> segment table: SEG_T threads per segment
                 const int k = threadIdx.x / SEG_T, q = threadIdx.x % SEG_T;
                 if (k < nseg) {
@@ -431,14 +448,36 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArg
             PHASE_MARK(2);
             if (r0 + RB >= total && nxt.x >= 0) stage_item(S, a, nxt, lxyz);  // overlaps pass 2 + flush
             // ---------------- pass 2: fixed-point adjoint scatter (kernels.py:221-230)
-            const float vm = __int_as_float(S.vmax_bits);
-            float inv_sc;
-            const float sc = pow2_scale(lim, vm, inv_sc);
-            float sch = 1.0f, inv_sch = 1.0f;
-            if (HUTCH) {
-                const float hm = __int_as_float(S.hmax_bits);
-                sch = pow2_scale(lim, hm, inv_sch);
+            {
+                const float vm = __int_as_float(S.vmax_bits);
+                float inv_r;
+                const float sc_r = pow2_scale(lim, vm, inv_r);
+                bool sync = false;
+                if (r0 == 0 || sc_r >= item_sc) {
+                    if (r0 == 0) { item_sc = sc_r; item_inv_sc = inv_r; }
+                } else {  // exponent difference of two powers of two
+                    rescale((__float_as_int(item_sc) - __float_as_int(sc_r)) >> 23, S.accr, S.acci);
+                    item_sc = sc_r;
+                    item_inv_sc = inv_r;
+                    sync = true;
+                }
+                if (HUTCH) {
+                    const float hm = __int_as_float(S.hmax_bits);
+                    float inv_h;
+                    const float sh_r = pow2_scale(lim, hm, inv_h);
+                    if (r0 == 0) {
+                        item_sch = sh_r;
+                        item_inv_sch = inv_h;
+                    } else if (sh_r < item_sch) {
+                        rescale((__float_as_int(item_sch) - __float_as_int(sh_r)) >> 23, S.acch, nullptr);
+                        item_sch = sh_r;
+                        item_inv_sch = inv_h;
+                        sync = true;
+                    }
+                }
+                if (sync) __syncthreads();  // uniform: every thread read the same maxima
             }
+            const float sc = item_sc, sch = item_sch;
 #if defined(FSLD_EXP_NO_PASS2)
             for (int e = threadIdx.x; e < 0; e += BTHREADS) {
 #else
@@ -477,10 +516,8 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArg
             }
             __syncthreads();
             PHASE_MARK(3);
-            prev_inv_sc = inv_sc;
-            prev_inv_sch = inv_sch;
         }
-        flush_round(prev_inv_sc, prev_inv_sch);  // the item's last round (the next item's (A) barrier follows)
+        flush_round(item_inv_sc, item_inv_sch);  // once per item (the next item's (A) barrier follows)
         PHASE_MARK(7);
         item = nxt;
     }
