@@ -42,7 +42,10 @@ struct SliceArgs {
 constexpr int BT = 8;                 // brick edge (voxels)
 constexpr int BH = BT + 1;            // + halo for the floor+1 corners
 constexpr int BH3 = BH * BH * BH;     // 729
-constexpr int BC = 64;                // segments (images) per work item
+#ifndef FSLD_BC
+#define FSLD_BC 64
+#endif
+constexpr int BC = FSLD_BC;           // segments (images) per work item (tools/build_exp.sh -DFSLD_BC=..)
 constexpr int BW = 8;                 // warps per CTA
 constexpr int BTHREADS = BW * 32;
 constexpr uint32_t kGeomMagic = 0xF51DB200u;
