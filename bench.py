@@ -388,9 +388,14 @@ def run_b200(args):
         p1.record()
         torch.cuda.synchronize()
         t_plan = p0.elapsed_time(p1)
-        launches_per_step = 5 + (2 if world > 1 else 0)  # memset + kernel + reduce + epilogue (2)
+        # world 1: grad init + brick kernel + finalize (fused step); N > 1: brick kernel + reduce +
+        # ball gather / scatter + epilogue (2)
+        launches_per_step = 3 if world == 1 else 6
 
-    def planned_step(plan, k, ev_k0=None, ev_k1=None):
+    def planned_step(plan, k, ev_k0=None, ev_k1=None, fused=False):
+        if fused and world == 1:  # the whole step in one call: grad = lam v, brick pass adds s * sum, finalize
+            eng.loss_grad_step_planned(v, plan, k, scale, lam, grad, sq=sq, loss=loss)
+            return loss
         stream = _stream()
         if ev_k0 is not None:
             ev_k0.record()
@@ -427,7 +432,7 @@ def run_b200(args):
             for i in range(args.steps):
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g):
-                    planned_step(plan_t, i)
+                    planned_step(plan_t, i, fused=True)
                 graphs.append(g)
         else:
             idx_static.copy_(batches[0])
@@ -454,7 +459,7 @@ def run_b200(args):
                     idx_static.copy_(batches[args.warmup + i])
                 graphs[i].replay()
             elif use_plan:
-                planned_step(plan_t, i)
+                planned_step(plan_t, i, fused=True)
             else:
                 step(batches[args.warmup + i])
             s1.record()
@@ -515,7 +520,9 @@ def run_b200(args):
                        "ctf": "physical astigmatic" if cfg.ctf else "none", "shifts": bool(cfg.shifts),
                        "parallelism": f"dp{world}", "l2": "flushed between timed steps (512 MB write)",
                        "allreduce_bytes": (8 * nball + 8) if world > 1 else 0,
-                       "step": "CUDA graph replay" if world == 1 and not os.environ.get("FSLD_NO_GRAPH") else "eager",
+                       "step": ("CUDA graph replay" if world == 1 and not os.environ.get("FSLD_NO_GRAPH") else "eager")
+                       + (" of fsld_loss_grad_step_planned (grad = lam v, the brick pass adds scale * its sums into "
+                          "grad, loss finalize)" if use_plan and world == 1 else ""),
                        "binning": (f"plan of the {args.steps} timed batches (fsld_plan_build), built inside the "
                                    f"measurement: {t_plan:.4f} ms, added as {t_plan / args.steps:.4f} ms per step")
                        if use_plan else "per step (count -> scan -> fill kernels)"},

@@ -407,6 +407,17 @@ int fsld_plan_build(int M, int n_mask, const fsld_image_rec* recs, const int32_t
 int fsld_loss_grad_planned(int M, int mode, int n_mask, const fsld_image_rec* recs, const void* plan, int B, int k,
                            const void* v, const void* xs, const int8_t* pc, const uint32_t* zbits, void* grad_acc,
                            float* fold, double* sq_out, void* scratch, size_t scratch_bytes, void* stream);
+/* The complete loss+grad step of batch k of a plan, epilogue fused around the brick pass
+ * (optim.py:165-190 with loss_and_grad's scale / lam applied on the device):
+ *   grad  = scale * sum_b P_b^* conj(f_b) r_b + lam v        (overwritten; v != grad)
+ *   *sq_out = sum |r|^2,   *loss = 0.5 scale sq + 0.5 lam ||v||^2
+ * grad is set to lam v first and the brick pass adds its scaled contributions into it, so no
+ * separate accumulator is read back or cleared.  scratch: fsld_scratch_bytes(M, n_mask, B);
+ * norm_scratch: >= 148 * 8 doubles. */
+int fsld_loss_grad_step_planned(int M, int mode, int n_mask, const fsld_image_rec* recs, const void* plan, int B,
+                                int k, const void* v, const void* xs, const int8_t* pc, double scale, double lam,
+                                void* grad, double* sq_out, double* loss, void* scratch, size_t scratch_bytes,
+                                void* norm_scratch, size_t norm_scratch_bytes, void* stream);
 int fsld_proj_energy_planned(int M, int mode, int n_mask, const fsld_image_rec* recs, const void* plan, int B, int k,
                              const void* d, const int8_t* pc, double* out, void* scratch, size_t scratch_bytes,
                              void* stream);

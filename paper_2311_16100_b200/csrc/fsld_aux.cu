@@ -193,6 +193,60 @@ cudaError_t launch_grad_epilogue(int64_t nvox, float2* acc, const float2* v, dou
     return cudaGetLastError();
 }
 
+// Fused-epilogue form of the loss+grad step: grad = lam v written BEFORE the brick pass, whose flush
+// then adds scale * (its contributions) straight into grad (no accumulator read-back, no zeroing pass);
+// per-block partials of ||v||^2 for the loss.
+__global__ void __launch_bounds__(256) grad_init_kernel(int64_t n, const float2* __restrict__ v, float lam,
+                                                        float2* __restrict__ grad, double* part) {
+    __shared__ double smem[32];
+    double s = 0.0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool vec = ((reinterpret_cast<uintptr_t>(v) | reinterpret_cast<uintptr_t>(grad)) & 15) == 0;
+    const int64_t n2 = vec ? n / 2 : 0;
+    for (int64_t i = t0; i < n2; i += stride) {
+        const float4 w = __ldg(reinterpret_cast<const float4*>(v) + i);
+        reinterpret_cast<float4*>(grad)[i] = make_float4(lam * w.x, lam * w.y, lam * w.z, lam * w.w);
+        s += (double)fmaf(w.x, w.x, w.y * w.y) + (double)fmaf(w.z, w.z, w.w * w.w);
+    }
+    for (int64_t i = 2 * n2 + t0; i < n; i += stride) {
+        const float2 w = v[i];
+        grad[i] = make_float2(lam * w.x, lam * w.y);
+        s += (double)w.x * w.x + (double)w.y * w.y;
+    }
+    s = block_sum(s, smem);
+    if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+// sq = sum(part_sq) (the brick pass's per-CTA |r|^2), loss = 0.5 scale sq + 0.5 lam sum(part_norm)
+__global__ void __launch_bounds__(1024) loss_finalize_kernel(const double* __restrict__ part_sq, int n_sq,
+                                                             const double* __restrict__ part_norm, int n_norm,
+                                                             double scale, double lam, double* sq_out, double* loss) {
+    __shared__ double smem[32];
+    double a = 0.0, b = 0.0;
+    for (int i = threadIdx.x; i < n_sq; i += blockDim.x) a += part_sq[i];
+    a = block_sum(a, smem);
+    __syncthreads();
+    for (int i = threadIdx.x; i < n_norm; i += blockDim.x) b += part_norm[i];
+    b = block_sum(b, smem);
+    if (threadIdx.x == 0) {
+        *sq_out = a;
+        *loss = 0.5 * scale * a + 0.5 * lam * b;
+    }
+}
+
+cudaError_t launch_grad_init(int64_t nvox, const float2* v, double lam, float2* grad, double* part, int nparts,
+                             cudaStream_t s) {
+    grad_init_kernel<<<nparts, 256, 0, s>>>(nvox, v, (float)lam, grad, part);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_loss_finalize(const double* part_sq, int n_sq, const double* part_norm, int n_norm, double scale,
+                                 double lam, double* sq_out, double* loss, cudaStream_t s) {
+    loss_finalize_kernel<<<1, 1024, 0, s>>>(part_sq, n_sq, part_norm, n_norm, scale, lam, sq_out, loss);
+    return cudaGetLastError();
+}
+
 // Touched-ball compaction for the data-parallel all-reduce: only voxels within
 // radius R + 1/2 + sqrt(3) can receive scatter contributions (Appendix A item 7), ~54 % of the
 // cube at M=128, so the all-reduce moves the compacted vector.  Element-generic (4 or 8 bytes).

@@ -485,7 +485,7 @@ cudaError_t set_phase_profile(unsigned long long* buf) {
 }
 
 template <bool HUTCH>
-static cudaError_t launch_sorted_main(const SortedArgs& a, double* sq_out, cudaStream_t s) {
+static cudaError_t launch_sorted_main(const SortedArgs& a, double* sq_out, cudaStream_t s, int* grid_out = nullptr) {
     static int grid = 0;
     const size_t smem = sizeof(SortedSmemT<HUTCH>);
     if (grid == 0) {
@@ -501,6 +501,10 @@ static cudaError_t launch_sorted_main(const SortedArgs& a, double* sq_out, cudaS
     sorted_loss_grad_kernel<HUTCH><<<grid, BTHREADS, smem, s>>>(a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
+    if (grid_out) {  // the caller reduces the per-CTA partials
+        *grid_out = grid;
+        return cudaSuccess;
+    }
     return launch_reduce(a.part, grid, sq_out, s);
 }
 
@@ -517,6 +521,22 @@ cudaError_t launch_planned_loss_grad(const SortedArgs& a, double* sq_out, cudaSt
     cudaError_t e = cudaMemsetAsync(a.ctl + 1, 0, sizeof(int), s);
     if (e != cudaSuccess) return e;
     return a.zbits ? launch_sorted_main<true>(a, sq_out, s) : launch_sorted_main<false>(a, sq_out, s);
+}
+
+// The whole loss+grad step of batch k of a plan with the epilogue fused around the brick pass:
+// grad = lam v (+ ||v||^2 partials), the brick pass adding scale * contributions into grad, and one
+// finalize of sq and the loss.  a.acc = grad, a.v = v.
+cudaError_t launch_planned_loss_grad_step(SortedArgs a, int64_t nvox, double scale, double lam, double* sq_out,
+                                          double* loss, double* norm_part, int n_norm, cudaStream_t s) {
+    cudaError_t e = launch_grad_init(nvox, a.v, lam, a.acc, norm_part, n_norm, s);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(a.ctl + 1, 0, sizeof(int), s);
+    if (e != cudaSuccess) return e;
+    a.out_scale = (float)scale;
+    int grid = 0;
+    e = launch_sorted_main<false>(a, nullptr, s, &grid);
+    if (e != cudaSuccess) return e;
+    return launch_loss_finalize(a.part, grid, norm_part, n_norm, scale, lam, sq_out, loss, s);
 }
 
 static int g_energy_grid = 0;

@@ -327,8 +327,10 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArg
                 const int kx = ox + (lxyz[u] & 15), ky = oy + ((lxyz[u] >> 4) & 15), kz = oz + (lxyz[u] >> 8);
                 if (kx >= M - c || ky >= M - c || kz >= M - c) continue;
                 const size_t j = (size_t)lin_index(kx, ky, kz, M, c);
-                if ((qr | qi) != 0)
-                    red_f32x2(reinterpret_cast<float*>(a.acc) + 2 * j, (float)qr * f_inv_sc, (float)qi * f_inv_sc);
+                if ((qr | qi) != 0) {
+                    const float fs = f_inv_sc * a.out_scale;  // exact for out_scale = 1
+                    red_f32x2(reinterpret_cast<float*>(a.acc) + 2 * j, (float)qr * fs, (float)qi * fs);
+                }
                 if (HUTCH && qh != 0) {
                     const float hz = (S.zc[l] & 1u) ? (float)qh * f_inv_sch : -(float)qh * f_inv_sch;
                     atomicAdd(a.fold + j, hz);

@@ -105,6 +105,7 @@ SortedArgs make_sorted(const ScratchLayout& L, int M, int n_mask, int B, const f
     b.part = reinterpret_cast<double*>(scr + L.part);
     b.cap_pairs = L.cap_pairs;
     b.cap_items = L.cap_items;
+    b.out_scale = 1.0f;
     return b;
 }
 
@@ -677,6 +678,24 @@ extern "C" int fsld_loss_grad_planned(int M, int mode, int n_mask, const fsld_im
     b.zbits = zbits;
     b.fold = fold;
     return status_of(launch_planned_loss_grad(b, sq_out, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+extern "C" int fsld_loss_grad_step_planned(int M, int mode, int n_mask, const fsld_image_rec* recs, const void* plan,
+                                           int B, int k, const void* v, const void* xs, const int8_t* pc,
+                                           double scale, double lam, void* grad, double* sq_out, double* loss,
+                                           void* scratch, size_t scratch_bytes, void* norm_scratch,
+                                           size_t norm_scratch_bytes, void* stream) {
+    const int n_norm = 148 * 8;
+    if (!geom_ok(M, mode, n_mask, B) || M > 256 || mode != FSLD_MODE_TRI) return FSLD_EINVAL;
+    if (!recs || !plan || !v || !xs || !pc || !grad || !sq_out || !loss || !scratch || !norm_scratch ||
+        norm_scratch_bytes < n_norm * sizeof(double) || v == grad)
+        return FSLD_EINVAL;
+    SortedArgs b;
+    if (!make_planned(b, plan, M, n_mask, B, k, recs, v, xs, pc, grad, scratch, scratch_bytes)) return FSLD_EINVAL;
+    const int64_t nvox = (int64_t)M * M * M;
+    return status_of(launch_planned_loss_grad_step(b, nvox, scale, lam, sq_out, loss,
+                                                   reinterpret_cast<double*>(norm_scratch), n_norm,
+                                                   reinterpret_cast<cudaStream_t>(stream)));
 }
 
 extern "C" int fsld_proj_energy_planned(int M, int mode, int n_mask, const fsld_image_rec* recs, const void* plan,

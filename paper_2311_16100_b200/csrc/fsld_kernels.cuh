@@ -125,6 +125,7 @@ struct SortedArgs {
     int* ctl;
     double* part;
     int cap_pairs, cap_items;
+    float out_scale;         // the flush adds out_scale * (sum of contributions) to acc (1 = plain accumulator)
 };
 
 cudaError_t launch_sorted_count(int M, int n_mask, const short2* pix, const fsld_image_rec* recs, int N,
@@ -142,6 +143,12 @@ cudaError_t launch_reduce(const double* part, int n, double* out, cudaStream_t s
 cudaError_t launch_ball(bool gather, int64_t n, const int32_t* idx, const void* src, void* dst, int elem_bytes,
                         cudaStream_t s);
 cudaError_t launch_reduce_cols(const double* part, int n, int ncols, double* out, cudaStream_t s);
+cudaError_t launch_grad_init(int64_t nvox, const float2* v, double lam, float2* grad, double* part, int nparts,
+                             cudaStream_t s);
+cudaError_t launch_loss_finalize(const double* part_sq, int n_sq, const double* part_norm, int n_norm, double scale,
+                                 double lam, double* sq_out, double* loss, cudaStream_t s);
+cudaError_t launch_planned_loss_grad_step(SortedArgs a, int64_t nvox, double scale, double lam, double* sq_out,
+                                          double* loss, double* norm_part, int n_norm, cudaStream_t s);
 
 // Algorithm-1 step kernels (fsld_step.cu)
 cudaError_t launch_precond_step(int64_t nvox, float2* acc, const float2* v, float* fold, float* d_avg, float* d,

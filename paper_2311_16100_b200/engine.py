@@ -307,6 +307,24 @@ class SliceEngine:
                 "fsld_loss_grad_planned")
         return sq
 
+    def loss_grad_step_planned(self, v, plan: "BinPlan", k: int, scale: float, lam: float, grad,
+                               sq=None, loss=None):
+        """The whole loss+grad step of batch k of a plan (fsld_loss_grad_step_planned): grad is
+        overwritten with scale * sum P^* conj(f) r + lam v; returns (loss, sq) device doubles."""
+        lib = C.load()
+        v = self._vol(v)
+        sq = torch.empty(1, dtype=torch.float64, device=self.dev) if sq is None else sq
+        loss = torch.empty(1, dtype=torch.float64, device=self.dev) if loss is None else loss
+        scr = self.scratch(plan.B)
+        nscr = self._norm_scratch()
+        C.check(lib.fsld_loss_grad_step_planned(self.M, self.mode_id, self.n_mask, ctypes_ptr(self.recs),
+                                                ctypes_ptr(plan.buf), plan.B, int(k), ctypes_ptr(v),
+                                                ctypes_ptr(self.x), ctypes_ptr(self.pc), float(scale), float(lam),
+                                                ctypes_ptr(grad), ctypes_ptr(sq), ctypes_ptr(loss), ctypes_ptr(scr),
+                                                scr.numel() * 8, ctypes_ptr(nscr), nscr.numel() * 8, _stream()),
+                "fsld_loss_grad_step_planned")
+        return loss, sq
+
     def proj_energy_planned(self, d, plan: "BinPlan", k: int, out=None) -> torch.Tensor:
         lib = C.load()
         d = self._vol(d)

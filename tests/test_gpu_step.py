@@ -364,6 +364,45 @@ def test_binning_plan_matches_per_step_binning():
         e.loss_grad_planned(v, plan, 5, acc1)  # k out of range
 
 
+def test_fused_epilogue_step_matches_accumulator_path_and_oracle():
+    """fsld_loss_grad_step_planned (grad = lam v, brick pass adding scale * sums into grad, loss
+    finalize) against the accumulator path (planned loss+grad + epilogue) and the oracle's
+    loss_and_grad (optim.py:165-190)."""
+    from paper_2311_16100_b200 import synth
+    M, N, B = 32, 200, 64
+    mask = O.disk_mask(M, M // 2 - 1)
+    q = synth.haar_quaternions(N, 51)
+    sh = synth.normal_shifts(N, 52)
+    ctfs = synth.physical_ctfs(N, 53)
+    pix = O.mask_pix(M, mask)
+    rng = np.random.default_rng(54)
+    x = (rng.standard_normal((N, mask.size)) + 1j * rng.standard_normal((N, mask.size))).astype(np.complex64)
+    e = SliceEngine(M, "tri", mask, records_for(M, q, sh, ctfs), x)
+    assert e.brick_path
+    batches = np.stack([rng.choice(N, B, replace=False) for _ in range(3)])
+    plan = e.make_plan(batches)
+    v_h = synth.gaussian_blob_volume(M, 5).astype(np.complex64)
+    v = torch.from_numpy(v_h).cuda()
+    lam = 0.37
+    oop = O.OracleOperator(M, "tri", mask, q, sh, O.ctf_table_physical(synth.ctf_param_array(ctfs), pix, M),
+                           x.astype(np.complex128))
+    for k in (2, 0):
+        scale = N / B
+        grad = torch.full((M ** 3,), 7.0, dtype=torch.complex64, device="cuda")  # overwritten, not accumulated
+        loss, sq = e.loss_grad_step_planned(v, plan, k, scale, lam, grad)
+        acc = torch.zeros(M ** 3, dtype=torch.complex64, device="cuda")
+        sq2 = e.loss_grad_planned(v, plan, k, acc)
+        loss2, grad2 = e.epilogue(acc, v, scale, lam, sq2)
+        assert abs(float(sq) - float(sq2)) <= 1e-12 * abs(float(sq2))
+        assert abs(float(loss) - float(loss2[0])) <= 1e-7 * abs(float(loss2[0]))
+        assert rel(grad.cpu().numpy(), grad2.cpu().numpy()) < 1e-6
+        l_ref, g_ref = O.loss_and_grad(oop, v_h.astype(np.complex128), batches[k], lam)
+        assert abs(float(loss) - l_ref) / abs(l_ref) < 1e-5
+        assert rel(grad.cpu().numpy(), g_ref) < 1e-5
+    with pytest.raises(ValueError):
+        e.loss_grad_step_planned(v, plan, 0, 1.0, lam, v)  # grad must not alias v
+
+
 @pytest.mark.parametrize("name,seed", [("dataset_m16_nn.npz", 3), ("dataset_m16_tri.npz", 4)])
 def test_reference_solve_residual_vs_oracle(golden, name, seed):
     """Device CG (optim.reference_solve, optim.py:396-450): the returned volume solves H v = b to the
