@@ -815,7 +815,7 @@ def hutch_sweep(args):
             eng.hutch_fold(zb, k, idx, acc=acc)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        reps = max(2, args.steps // 4)
+        reps = max(5, args.steps // 4)
         e0.record()
         for _ in range(reps):
             acc.zero_()
