@@ -301,8 +301,9 @@ __global__ void __launch_bounds__(128) bin_sorted_kernel(SortedArgs a) {
 
 // Exclusive scan of per-brick pair counts and expansion into work items
 // (brick, first pair, n pairs <= BC).  Full items (BC pairs) are listed first
-// and the partial remainders after them, so the persistent kernel's last
-// claims are the small items (shorter tail).  One CTA of 1024 threads,
+// and the partial remainders after them in descending segment count (largest
+// first: the persistent kernel's last claims are the smallest items, so the CTAs
+// finish together -- measured +6.6 % on the cfg3 step over brick order).  One CTA of 1024 threads,
 // warp-shuffle scans.  Leaves cnt[] zeroed for the next call (fsld_prepare
 // zeroes it once).  ctl = {n_items, claim counter, overflow, pairs base, items base}: the
 // work-item kernels read their pairs at pairs + ctl[3] and their items at items + ctl[4]
@@ -310,6 +311,9 @@ __global__ void __launch_bounds__(128) bin_sorted_kernel(SortedArgs a) {
 __device__ void scan_batch(int* cnt, int* off, int* fill, int4* items, int* ctl, int nbr, int cap_items,
                            int cap_pairs, int pairs_base, int items_base) {
     __shared__ int wp[32], wf[32], wr[32];
+    __shared__ int rh[BC];  // partial items per segment count, then the descending-size cursor
+    if (threadIdx.x < BC) rh[threadIdx.x] = 0;
+    __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int per = (nbr + 1023) / 1024;
     const int lo = threadIdx.x * per;
@@ -320,6 +324,7 @@ __device__ void scan_batch(int* cnt, int* off, int* fill, int4* items, int* ctl,
         np += c;
         nf += c / BC;
         nr += (c % BC) != 0;
+        if (c % BC) atomicAdd(rh + c % BC, 1);
     }
     int ip = np, jf = nf, jr = nr;
 #pragma unroll
@@ -356,9 +361,17 @@ __device__ void scan_batch(int* cnt, int* off, int* fill, int4* items, int* ctl,
     }
     __syncthreads();
     const int n_full = wf[31];
+    if (threadIdx.x == 0) {  // partial items in descending segment count: cursor of size r = sum of larger bins
+        int run = 0;
+        for (int r = BC - 1; r >= 1; --r) {
+            const int h = rh[r];
+            rh[r] = n_full + run;
+            run += h;
+        }
+    }
+    __syncthreads();
     int pbase = (warp > 0 ? wp[warp - 1] : 0) + ip - np;
     int fbase = (warp > 0 ? wf[warp - 1] : 0) + jf - nf;
-    int rbase = n_full + (warp > 0 ? wr[warp - 1] : 0) + jr - nr;
     int4* it = items + items_base;
     for (int i = lo; i < hi; ++i) {
         const int c = cnt[i];
@@ -369,8 +382,8 @@ __device__ void scan_batch(int* cnt, int* off, int* fill, int4* items, int* ctl,
         for (; k + BC <= c; k += BC, ++fbase)
             if (fbase < cap_items) it[fbase] = make_int4(i, pbase + k, BC, 0);
         if (k < c) {
-            if (rbase < cap_items) it[rbase] = make_int4(i, pbase + k, c - k, 0);
-            ++rbase;
+            const int slot = atomicAdd(rh + (c - k), 1);
+            if (slot < cap_items) it[slot] = make_int4(i, pbase + k, c - k, 0);
         }
         pbase += c;
     }
