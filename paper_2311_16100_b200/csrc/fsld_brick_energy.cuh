@@ -10,7 +10,8 @@
 
 struct EnergySmem {
     float2 vb[BH3];
-    SegRec seg[BC];
+    int4 segw[BC * SEG_W];  // segment records, SEG_W words apart (fsld_kernels.cuh)
+    __device__ __forceinline__ SegRec& seg(int k) { return *reinterpret_cast<SegRec*>(segw + k * SEG_W); }
     int pref[BC + 1];
     int wtot[BC / 32];
     unsigned char bk[RB];
@@ -52,8 +53,8 @@ __global__ void __launch_bounds__(BTHREADS) sorted_energy_kernel(SortedArgs a) {
         const int bid = item.x, pstart = item.y, nseg = item.z;
         const int ox = -c + BT * (bid % nb), oy = -c + BT * ((bid / nb) % nb), oz = -c + BT * (bid / (nb * nb));
         {
-            int4* dst = reinterpret_cast<int4*>(S.seg);
-            for (int w = threadIdx.x; w < nseg * 8; w += BTHREADS) dst[w] = seg_chunk(a, pstart + (w >> 3), w & 7);
+            for (int w = threadIdx.x; w < nseg * 8; w += BTHREADS)
+                S.segw[(w >> 3) * SEG_W + (w & 7)] = seg_chunk(a, pstart + (w >> 3), w & 7);
         }
         if (warp < BC / 32) {
             const int k = threadIdx.x;
@@ -78,7 +79,7 @@ __global__ void __launch_bounds__(BTHREADS) sorted_energy_kernel(SortedArgs a) {
             int p = S.pref[k];
             for (int w = 0; w < (k >> 5); ++w) p += S.wtot[w];
             S.pref[k] = p;
-            S.seg[k].gofs -= p;
+            S.seg(k).gofs -= p;
         }
         if (threadIdx.x == 0) {
             int t = 0;
@@ -99,7 +100,7 @@ __global__ void __launch_bounds__(BTHREADS) sorted_energy_kernel(SortedArgs a) {
             __syncthreads();
             float en = 0.f;
             for (int e = threadIdx.x; e < rn; e += BTHREADS) {
-                const SegRec& R = S.seg[S.bk[e]];
+                const SegRec& R = S.seg(S.bk[e]);
                 const char2 kk = a.pc[R.gofs + (r0 + e)];
                 const int px = kk.x, py = kk.y;
                 float cx, cy, cz, fx, fy, fz;

@@ -16,7 +16,8 @@ constexpr int kHutchMaxWords = 8;
 struct HutchSmem {
     uint32_t zw[BH3 * kHutchMaxWords];  // probe words of the brick voxels, [l * words + wd]
     int acc[BH3];
-    SegRec seg[BC];
+    int4 segw[BC * SEG_W];  // segment records, SEG_W words apart (fsld_kernels.cuh)
+    __device__ __forceinline__ SegRec& seg(int k) { return *reinterpret_cast<SegRec*>(segw + k * SEG_W); }
     int pref[BC + 1];
     int wtot[BC / 32];
     unsigned char bk[RB];
@@ -45,8 +46,8 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_hutch_kernel(SortedArgs a,
         const int bid = item.x, pstart = item.y, nseg = item.z;
         const int ox = -c + BT * (bid % nb), oy = -c + BT * ((bid / nb) % nb), oz = -c + BT * (bid / (nb * nb));
         {
-            int4* dst = reinterpret_cast<int4*>(S.seg);
-            for (int w = threadIdx.x; w < nseg * 8; w += BTHREADS) dst[w] = seg_chunk(a, pstart + (w >> 3), w & 7);
+            for (int w = threadIdx.x; w < nseg * 8; w += BTHREADS)
+                S.segw[(w >> 3) * SEG_W + (w & 7)] = seg_chunk(a, pstart + (w >> 3), w & 7);
         }
         if (warp < BC / 32) {
             const int kk = threadIdx.x;
@@ -72,7 +73,7 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_hutch_kernel(SortedArgs a,
             int p = S.pref[kk];
             for (int w = 0; w < (kk >> 5); ++w) p += S.wtot[w];
             S.pref[kk] = p;
-            S.seg[kk].gofs -= p;
+            S.seg(kk).gofs -= p;
         }
         if (threadIdx.x == 0) {
             int t = 0;
@@ -94,7 +95,7 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_hutch_kernel(SortedArgs a,
             }
             __syncthreads();
             for (int e = threadIdx.x; e < rn; e += BTHREADS) {
-                const SegRec& R = S.seg[S.bk[e]];
+                const SegRec& R = S.seg(S.bk[e]);
                 const char2 kq = a.pc[R.gofs + (r0 + e)];
                 const int px = kq.x, py = kq.y;
                 float cx, cy, cz, fx, fy, fz;

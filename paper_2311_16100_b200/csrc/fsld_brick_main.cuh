@@ -37,7 +37,8 @@ struct SortedSmemT {
     float2 bval[RB];                // pass 1 -> 2: conj(f) r
     float4 bgeo[RB];                // pass 1 -> 2: (wx, wy, wz, local corner index)
     float hval[HUTCH ? RB : 1];     // pass 1 -> 2: C^2 P z (also z staging during setup)
-    SegRec seg[BC];                 // the item's segment records (gofs rebased to the flat index)
+    int4 segw[BC * SEG_W];          // the item's segment records (gofs rebased to the flat index), SEG_W words apart
+    __device__ __forceinline__ SegRec& seg(int k) { return *reinterpret_cast<SegRec*>(segw + k * SEG_W); }
     PairRec prec[BC];               // the next item's pair records (staged first: their tslots address the templates)
     int pref[BC + 1];               // exclusive prefix of segment lengths
     unsigned char bk[RB];           // round pixel -> segment
@@ -178,12 +179,12 @@ __device__ __forceinline__ void stage_item(SortedSmemT<HUTCH>& S, const SortedAr
     const int M = a.M, c = a.c, nb = a.nb;
     const int bid = item.x, nseg = item.z;
     const int ox = -c + BT * (bid % nb), oy = -c + BT * ((bid / nb) % nb), oz = -c + BT * (bid / (nb * nb));
-    int4* dst = reinterpret_cast<int4*>(S.seg);
+    int4* dst = S.segw;
     for (int w = threadIdx.x; w < nseg * 8; w += BTHREADS) {
         const int j = w >> 3, q = w & 7;
         const PairRec& pr = S.prec[j];
-        if (q == 0) dst[w] = make_int4((int)(unsigned)pr.gofs, (int)(pr.gofs >> 32), pr.count, 0);
-        else cp_async16(dst + w, reinterpret_cast<const int4*>(a.tmpl + pr.tslot) + q);
+        if (q == 0) dst[j * SEG_W] = make_int4((int)(unsigned)pr.gofs, (int)(pr.gofs >> 32), pr.count, 0);
+        else cp_async16(dst + j * SEG_W + q, reinterpret_cast<const int4*>(a.tmpl + pr.tslot) + q);
     }
 #pragma unroll
     for (int u = 0; u < BU; ++u) {
@@ -266,7 +267,7 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArg
         // ---------------- setup: segment-length prefix (warps 0, 1) [corner sign masks]
         if (warp < BC / 32) {
             const int k = threadIdx.x;
-            const int len = k < nseg ? S.seg[k].count : 0;
+            const int len = k < nseg ? S.seg(k).count : 0;
             int incl = len;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -299,7 +300,7 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArg
             int p = S.pref[k];
             for (int w = 0; w < (k >> 5); ++w) p += S.wtot[w];
             S.pref[k] = p;
-            S.seg[k].gofs -= p;
+            S.seg(k).gofs -= p;
         }
         if (threadIdx.x == 0) {
             int t = 0;
@@ -387,7 +388,7 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArg
             for (int e = threadIdx.x; e < rn; e += BTHREADS) {
 #endif
                 SegRegs R;
-                load_seg(S.seg[S.bk[e]], R);
+                load_seg(S.seg(S.bk[e]), R);
                 const long long g = R.gofs + (r0 + e);
                 const char2 kk = a.pc[g];
 #if defined(FSLD_EXP_NO_XLOAD)

@@ -79,6 +79,14 @@ struct __align__(16) SegRec {
 };
 static_assert(sizeof(SegRec) == 128, "SegRec is 8 x 16 B");
 
+// Shared-memory slot of a SegRec in the brick kernels: 8 + FSLD_SEG_PAD 16-byte words.  With a
+// 128-byte stride every segment's copy of a field sits in the same bank, so a warp whose pixels
+// span several segments replays each record load once per segment; the pad staggers them.
+#ifndef FSLD_SEG_PAD
+#define FSLD_SEG_PAD 1
+#endif
+constexpr int SEG_W = 8 + FSLD_SEG_PAD;
+
 // Per binned segment in global memory (16 B): the brick kernels assemble a SegRec in shared
 // memory from it and the per-image template (the SegRec fields that depend only on the image).
 struct __align__(16) PairRec {
