@@ -96,6 +96,10 @@ int fsld_abi_version(void);
 const char* fsld_status_string(int status);
 /* number of visible devices with compute capability 10.x (host call) */
 int fsld_device_count(int* count);
+/* Page-locked host buffers for the host-buffer entry points (fsld_loss_grad_host): cudaHostAlloc
+ * memory, which the copy engines stream at full PCIe rate in both directions at once. */
+int fsld_host_alloc(size_t bytes, void** out);
+int fsld_host_free(void* p);
 
 /*
  * Scratch bytes needed by the reducing entry points for batches of up to B
@@ -418,6 +422,24 @@ int fsld_loss_grad_step_planned(int M, int mode, int n_mask, const fsld_image_re
                                 int k, const void* v, const void* xs, const int8_t* pc, double scale, double lam,
                                 void* grad, double* sq_out, double* loss, void* scratch, size_t scratch_bytes,
                                 void* norm_scratch, size_t norm_scratch_bytes, void* stream);
+/* Host-buffer loss + gradient: the call a host caller makes with numpy-style buffers
+ * (optim.loss_and_grad, optim.py:165-190, whose v / grad are host arrays), tri mode, brick path.
+ * HOST pointers (page-locked, cudaHostAlloc / cudaHostRegister):
+ *   idx_host  : (B,) int32 dataset rows          v_host : M^3 complex64
+ *   grad_host : M^3 complex64, overwritten with  scale * sum_b P_b^* conj(f_b) r_b + lam v
+ *   out_host  : 2 doubles, {sum |r|^2, loss = 0.5 scale sq + 0.5 lam ||v||^2}
+ * DEVICE staging: v_dev, grad_dev (M^3 complex64 each, distinct), idx_dev (B int32);
+ * scratch: fsld_scratch_bytes(M, n_mask, B), prepared.
+ * The volume moves in n_slabs (1..16) z-slabs of brick layers: slab g's host->device copy, its
+ * lam v initialisation, its brick pass and its device->host copy of the finished gradient are
+ * pipelined on two internal copy streams (forked from / joined back into `stream`), so the
+ * PCIe transfers in both directions overlap each other and the kernels.  Everything is enqueued
+ * on `stream`: the outputs are valid once `stream` has been synchronised. */
+int fsld_loss_grad_host(int M, int mode, int n_mask, const fsld_image_rec* recs, const int32_t* idx_host, int B,
+                        const void* v_host, const void* xs, const int8_t* pc, const int32_t* seg_off,
+                        const int32_t* segs, double scale, double lam, void* grad_host, double* out_host,
+                        void* v_dev, void* grad_dev, int32_t* idx_dev, int n_slabs, void* scratch,
+                        size_t scratch_bytes, void* stream);
 int fsld_proj_energy_planned(int M, int mode, int n_mask, const fsld_image_rec* recs, const void* plan, int B, int k,
                              const void* d, const int8_t* pc, double* out, void* scratch, size_t scratch_bytes,
                              void* stream);

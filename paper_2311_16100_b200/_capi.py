@@ -68,6 +68,8 @@ SIGNATURES = {
     "fsld_abi_version": (I, []),
     "fsld_status_string": (ctypes.c_char_p, [I]),
     "fsld_device_count": (I, [P]),
+    "fsld_host_alloc": (I, [SZ, P]),
+    "fsld_host_free": (I, [P]),
     "fsld_scratch_bytes": (SZ, [I, I, I]),
     "fsld_prepare": (I, [I, I, P, P, SZ, P]),
     "fsld_loss_grad": (I, [I, I, I, P, P, P, I, P, P, P, P, U, P, P, SZ, P]),
@@ -90,6 +92,7 @@ SIGNATURES = {
     "fsld_loss_grad_hutch_sorted": (I, [I, I, I, P, P, I, P, P, P, P, P, P, P, P, P, U, P, SZ, P]),
     "fsld_hvp_sorted": (I, [I, I, I, P, P, I, P, P, P, P, P, P, U, P, SZ, P]),
     "fsld_loss_grad_step_planned": (I, [I, I, I, P, P, I, I, P, P, P, D, D, P, P, P, P, SZ, P, SZ, P]),
+    "fsld_loss_grad_host": (I, [I, I, I, P, P, I, P, P, P, P, P, D, D, P, P, P, P, P, I, P, SZ, P]),
     "fsld_project_sorted": (I, [I, I, I, P, P, I, P, P, P, P]),
     "fsld_backproject_sorted": (I, [I, I, I, P, P, I, P, P, P, U, P, P]),
     "fsld_fixed_scale": (I, [P, I64, D, D, P, P]),
@@ -144,3 +147,20 @@ def check(status: int, what: str) -> None:
     if status == FSLD_EINVAL:
         raise ValueError(f"{what}: {msg}")
     raise FsldError(f"{what}: {msg} (status {status})")
+
+
+def host_empty(numel: int, dtype):
+    """A page-locked host tensor backed by fsld_host_alloc (cudaHostAlloc), freed with the tensor.
+
+    The host-buffer step streams these at full PCIe rate in both directions at once; pinned
+    memory from other allocators is accepted too."""
+    import weakref
+
+    import torch
+
+    nbytes = int(numel) * torch.empty((), dtype=dtype).element_size()
+    ptr = ctypes.c_void_p()
+    check(load().fsld_host_alloc(max(nbytes, 1), ctypes.byref(ptr)), "fsld_host_alloc")
+    buf = (ctypes.c_char * max(nbytes, 1)).from_address(ptr.value)
+    weakref.finalize(buf, load().fsld_host_free, ptr.value)
+    return torch.frombuffer(buf, dtype=dtype, count=int(numel))

@@ -50,6 +50,11 @@ ScratchLayout scratch_layout(int M, int n_mask, int B) {
     L.items = o; o = al(o + sizeof(int4) * (size_t)L.cap_items);
     L.ctl = o; o = al(o + 64);
     L.part = o; o = al(o + sizeof(double) * (size_t)L.cap_part);
+    L.gitems = o; o = al(o + sizeof(int4) * (size_t)L.cap_items);
+    L.gctl = o; o = al(o + sizeof(int) * 16 * (size_t)kMaxSlabs);
+    L.gpart = o; o = al(o + sizeof(double) * (size_t)kMaxSlabs * kSlabCtas);
+    L.npart = o; o = al(o + sizeof(double) * (size_t)kMaxSlabs * 2 * kInitParts);
+    L.hout = o; o = al(o + sizeof(double) * 2);
     L.total = o;
     return L;
 }
@@ -497,11 +502,12 @@ cudaError_t set_phase_profile(unsigned long long* buf) {
     return cudaMemcpyToSymbol(g_phase_prof, &buf, sizeof(buf));
 }
 
+// Persistent grid of the brick kernel (SMs x resident CTAs), set up on first use.
 template <bool HUTCH>
-static cudaError_t launch_sorted_main(const SortedArgs& a, double* sq_out, cudaStream_t s, int* grid_out = nullptr) {
+static cudaError_t main_grid(int& out) {
     static int grid = 0;
-    const size_t smem = sizeof(SortedSmemT<HUTCH>);
     if (grid == 0) {
+        const size_t smem = sizeof(SortedSmemT<HUTCH>);
         cudaError_t e = cudaFuncSetAttribute(sorted_loss_grad_kernel<HUTCH>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
@@ -511,6 +517,16 @@ static cudaError_t launch_sorted_main(const SortedArgs& a, double* sq_out, cudaS
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sorted_loss_grad_kernel<HUTCH>, BTHREADS, smem);
         grid = sms * (occ > 0 ? occ : 1);
     }
+    out = grid;
+    return cudaSuccess;
+}
+
+template <bool HUTCH>
+static cudaError_t launch_sorted_main(const SortedArgs& a, double* sq_out, cudaStream_t s, int* grid_out = nullptr) {
+    const size_t smem = sizeof(SortedSmemT<HUTCH>);
+    int grid = 0;
+    cudaError_t e0 = main_grid<HUTCH>(grid);
+    if (e0 != cudaSuccess) return e0;
     sorted_loss_grad_kernel<HUTCH><<<grid, BTHREADS, smem, s>>>(a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
@@ -521,12 +537,101 @@ static cudaError_t launch_sorted_main(const SortedArgs& a, double* sq_out, cudaS
     return launch_reduce(a.part, grid, sq_out, s);
 }
 
-cudaError_t launch_sorted_loss_grad(const SortedArgs& a, double* sq_out, cudaStream_t s) {
+cudaError_t launch_sorted_bin(const SortedArgs& a, cudaStream_t s) {
     // cnt[] is zero on entry: zeroed by fsld_prepare, and re-zeroed by every scan
     bin_sorted_kernel<false><<<a.B, 128, 0, s>>>(a);
     brick_scan_kernel<<<1, 1024, 0, s>>>(a);
     bin_sorted_kernel<true><<<a.B, 128, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sorted_loss_grad(const SortedArgs& a, double* sq_out, cudaStream_t s) {
+    cudaError_t e = launch_sorted_bin(a, s);
+    if (e != cudaSuccess) return e;
     return a.zbits ? launch_sorted_main<true>(a, sq_out, s) : launch_sorted_main<false>(a, sq_out, s);
+}
+
+// The loss+grad brick pass over the items a.ctl describes, per-CTA |r|^2 partials left in
+// a.part[0 .. *grid) for the caller to reduce.
+cudaError_t launch_sorted_pass(const SortedArgs& a, cudaStream_t s, int* grid) {
+    return launch_sorted_main<false>(a, nullptr, s, grid);
+}
+
+// Work items of one binned batch regrouped by z-slab (G slabs of `layers` brick layers each)
+// for the slab-pipelined host step (fsld_loss_grad_host).  Stable: every slab keeps the
+// full-first / largest-first order of scan_batch.  Slab g's items are gitems[gctl_g[4] ..
+// + gctl_g[0]), gctl_g = gctl + 16 g = {n, claim counter 0, 0, pairs base, items base}.
+__global__ void __launch_bounds__(1024) slab_items_kernel(const int4* __restrict__ items, const int* __restrict__ ctl,
+                                                          int nb, int layers, int G, int4* __restrict__ gitems,
+                                                          int* __restrict__ gctl) {
+    extern __shared__ unsigned char slab_of[];  // per item: its slab (one coalesced pass over the items)
+    __shared__ int wsum[32];
+    __shared__ int base_s;
+    items += ctl[4];
+    const int n = ctl[0], nb2 = nb * nb;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) slab_of[i] = (unsigned char)((__ldg(&items[i].x) / nb2) / layers);
+    const int per = (n + 1023) / 1024;
+    const int lo = min((int)threadIdx.x * per, n), hi = min(lo + per, n);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) base_s = 0;
+    __syncthreads();
+    for (int g = 0; g < G; ++g) {
+        int cnt = 0;
+        for (int i = lo; i < hi; ++i) cnt += slab_of[i] == g;
+        int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        if (lane == 31) wsum[warp] = incl;
+        __syncthreads();
+        if (warp == 0) {
+            int t = wsum[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int u = __shfl_up_sync(0xffffffffu, t, o);
+                if (lane >= o) t += u;
+            }
+            wsum[lane] = t;
+        }
+        __syncthreads();
+        int pos = base_s + (warp > 0 ? wsum[warp - 1] : 0) + incl - cnt;
+        for (int i = lo; i < hi; ++i)
+            if (slab_of[i] == g) gitems[pos++] = items[i];
+        __syncthreads();  // base_s and wsum read by everyone
+        if (threadIdx.x == 0) {
+            int* q = gctl + 16 * g;
+            q[0] = wsum[31];
+            q[1] = 0;
+            q[2] = 0;
+            q[3] = ctl[3];
+            q[4] = base_s;
+            base_s += wsum[31];
+        }
+        __syncthreads();
+    }
+}
+
+// Function attributes / grid sizes of the host-step kernels, outside any stream capture.
+cudaError_t prepare_host_step() {
+    static bool done = false;
+    if (done) return cudaSuccess;
+    // the item count is device-side: the slab table is sized for the capacity
+    cudaError_t e = cudaFuncSetAttribute(slab_items_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e != cudaSuccess) return e;
+    int grid = 0;
+    e = main_grid<false>(grid);
+    done = e == cudaSuccess;
+    return e;
+}
+
+cudaError_t launch_slab_items(const SortedArgs& a, int layers, int G, int4* gitems, int* gctl, cudaStream_t s) {
+    cudaError_t e = prepare_host_step();
+    if (e != cudaSuccess) return e;
+    if (a.cap_items > 200 * 1024) return cudaErrorInvalidValue;
+    slab_items_kernel<<<1, 1024, (size_t)a.cap_items, s>>>(a.items, a.ctl, a.nb, layers, G, gitems, gctl);
+    return cudaGetLastError();
 }
 
 // One batch of a plan: its work items are ready; re-arm its claim counter and run.

@@ -4,7 +4,10 @@
 // forward.py:562-563 / optim.py:179-180, bad mode forward.py:280-281), picks
 // the launch geometry and enqueues the kernels on the caller's stream.
 // Never throws, never synchronises.
+#include <algorithm>
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
 #include <mutex>
 
 #include "fsld_kernels.cuh"
@@ -15,7 +18,13 @@ namespace {
 
 constexpr int kPixPerThreadTarget = 4;
 
-int status_of(cudaError_t e) { return e == cudaSuccess ? FSLD_OK : FSLD_ECUDA; }
+// CUDA error -> status; FSLD_DEBUG=1 in the environment prints the CUDA error string to stderr.
+int status_of(cudaError_t e) {
+    if (e == cudaSuccess) return FSLD_OK;
+    static const bool dbg = std::getenv("FSLD_DEBUG") != nullptr;
+    if (dbg) std::fprintf(stderr, "fsld: CUDA error %d (%s)\n", (int)e, cudaGetErrorString(e));
+    return FSLD_ECUDA;
+}
 
 bool geom_ok(int M, int mode, int n_mask, int B) {
     if (M < 2 || M > 1024) return false;
@@ -141,6 +150,14 @@ int fsld_device_count(int* count) {
     *count = good;
     return good > 0 ? FSLD_OK : FSLD_ENODEV;
 }
+
+int fsld_host_alloc(size_t bytes, void** out) {
+    if (!out || bytes == 0) return FSLD_EINVAL;
+    *out = nullptr;
+    return status_of(cudaHostAlloc(out, bytes, cudaHostAllocDefault));
+}
+
+int fsld_host_free(void* p) { return p ? status_of(cudaFreeHost(p)) : FSLD_OK; }
 
 size_t fsld_scratch_bytes(int M, int n_mask, int B) {
     if (M < 2 || M > 1024) return 0;
@@ -707,4 +724,278 @@ extern "C" int fsld_proj_energy_planned(int M, int mode, int n_mask, const fsld_
     if (!make_planned(b, plan, M, n_mask, B, k, recs, d, nullptr, pc, nullptr, scratch, scratch_bytes))
         return FSLD_EINVAL;
     return status_of(launch_sorted_energy(b, out, false, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+// ---------------------------------------------------------------- slab-pipelined host step
+namespace {
+
+// Per-device copy streams and events of fsld_loss_grad_host, created once.
+struct HostPipe {
+    cudaStream_t h2d = nullptr, d2h = nullptr, ks[2] = {nullptr, nullptr};
+    cudaStream_t cap = nullptr;  // graphs are captured here (the caller's stream may be the legacy one)
+    cudaEvent_t fork = nullptr, join = nullptr, eh[kMaxSlabs] = {}, ei[kMaxSlabs] = {}, ek[kMaxSlabs] = {};
+};
+std::mutex g_pipe_mu;  // held while a call enqueues (the events are reused call after call)
+HostPipe g_pipe[16];
+
+cudaError_t pipe_for_device(HostPipe*& out) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= 16) return cudaErrorInvalidDevice;
+    HostPipe& p = g_pipe[dev];
+    if (!p.h2d) {
+        const unsigned fl = cudaEventDisableTiming;
+        if ((e = cudaStreamCreateWithFlags(&p.h2d, cudaStreamNonBlocking)) != cudaSuccess) return e;
+        if ((e = cudaStreamCreateWithFlags(&p.d2h, cudaStreamNonBlocking)) != cudaSuccess) return e;
+        for (int q = 0; q < 2; ++q)
+            if ((e = cudaStreamCreateWithFlags(&p.ks[q], cudaStreamNonBlocking)) != cudaSuccess) return e;
+        if ((e = cudaStreamCreateWithFlags(&p.cap, cudaStreamNonBlocking)) != cudaSuccess) return e;
+        if ((e = cudaEventCreateWithFlags(&p.fork, fl)) != cudaSuccess) return e;
+        if ((e = cudaEventCreateWithFlags(&p.join, fl)) != cudaSuccess) return e;
+        for (int g = 0; g < kMaxSlabs; ++g) {
+            if ((e = cudaEventCreateWithFlags(&p.eh[g], fl)) != cudaSuccess) return e;
+            if ((e = cudaEventCreateWithFlags(&p.ek[g], fl)) != cudaSuccess) return e;
+            if ((e = cudaEventCreateWithFlags(&p.ei[g], fl)) != cudaSuccess) return e;
+        }
+    }
+    out = &p;
+    return cudaSuccess;
+}
+
+// Slab g = kz in [z0, z1) as at most two contiguous plane ranges of the FFT-ordered z axis.
+int slab_pieces(int M, int z0, int z1, int zi0[2], int nz[2]) {
+    int n = 0;
+    if (z0 < 0) {
+        zi0[n] = z0 + M;
+        nz[n++] = (z1 < 0 ? z1 : 0) - z0;
+    }
+    if (z1 > 0) {
+        const int a = z0 > 0 ? z0 : 0;
+        zi0[n] = a;
+        nz[n++] = z1 - a;
+    }
+    return n;
+}
+
+}  // namespace
+
+namespace {
+
+// Everything a host step enqueues depends only on these (the batch rows are copied from a pinned
+// staging buffer owned by the cached graph), so one captured graph per key is replayed.
+struct HostStepKey {
+    int M, n_mask, B, n_slabs;
+    const void *recs, *v_host, *xs, *pc, *seg_off, *segs, *grad_host, *out_host, *v_dev, *grad_dev, *idx_dev,
+        *scratch;
+    double scale, lam;
+    bool operator==(const HostStepKey& o) const { return std::memcmp(this, &o, sizeof(*this)) == 0; }
+};
+
+// Enqueue one slab-pipelined host step on s (also used under stream capture).
+cudaError_t host_step_enqueue(const HostStepKey& k, HostPipe* P, const int32_t* idx_host, cudaStream_t s) {
+    const int M = k.M, n_mask = k.n_mask, B = k.B, n_slabs = k.n_slabs;
+    const double scale = k.scale, lam = k.lam;
+    const fsld_image_rec* recs = reinterpret_cast<const fsld_image_rec*>(k.recs);
+    void* scratch = const_cast<void*>(k.scratch);
+    void* v_dev = const_cast<void*>(k.v_dev);
+    void* grad_dev = const_cast<void*>(k.grad_dev);
+    int32_t* idx_dev = reinterpret_cast<int32_t*>(const_cast<void*>(k.idx_dev));
+    const void* v_host = k.v_host;
+    void* grad_host = const_cast<void*>(k.grad_host);
+    double* out_host = reinterpret_cast<double*>(const_cast<void*>(k.out_host));
+    const ScratchLayout L = scratch_layout(M, n_mask, B);
+    char* scr = reinterpret_cast<char*>(scratch);
+    SortedArgs a = make_sorted(L, M, n_mask, B, recs, idx_dev, v_dev, k.xs, reinterpret_cast<const int8_t*>(k.pc),
+                               reinterpret_cast<const int32_t*>(k.seg_off), reinterpret_cast<const int32_t*>(k.segs),
+                               grad_dev, scratch);
+    a.out_scale = (float)scale;
+    const int c = (M + 1) / 2, nb = L.nb;
+    const int layers = (nb + n_slabs - 1) / n_slabs;
+    const int G = (nb + layers - 1) / layers;
+    const size_t plane = (size_t)M * M * sizeof(float2);
+    int4* gitems = reinterpret_cast<int4*>(scr + L.gitems);
+    int* gctl = reinterpret_cast<int*>(scr + L.gctl);
+    double* gpart = reinterpret_cast<double*>(scr + L.gpart);
+    double* npart = reinterpret_cast<double*>(scr + L.npart);
+    double* hout = reinterpret_cast<double*>(scr + L.hout);
+    const char* vh = reinterpret_cast<const char*>(v_host);
+    char* gh = reinterpret_cast<char*>(grad_host);
+    char* vd = reinterpret_cast<char*>(v_dev);
+    char* gd = reinterpret_cast<char*>(grad_dev);
+
+    cudaError_t e = cudaSuccess;
+#define FSLD_TRY(x) do { if ((e = (x)) != cudaSuccess) return e; } while (0)
+    // fork: the copy streams start after whatever `stream` already holds (v_dev / grad_dev reuse)
+    FSLD_TRY(cudaEventRecord(P->fork, s));
+    FSLD_TRY(cudaStreamWaitEvent(P->h2d, P->fork, 0));
+    FSLD_TRY(cudaStreamWaitEvent(P->d2h, P->fork, 0));
+    int zi0[kMaxSlabs][2], nz[kMaxSlabs][2], np[kMaxSlabs];
+    for (int g = 0; g < G; ++g) {
+        const int z0 = -c + BT * layers * g, z1 = std::min(-c + BT * layers * (g + 1), M - c);
+        np[g] = slab_pieces(M, z0, z1, zi0[g], nz[g]);
+        for (int q = 0; q < np[g]; ++q)
+            FSLD_TRY(cudaMemcpyAsync(vd + zi0[g][q] * plane, vh + zi0[g][q] * plane, nz[g][q] * plane,
+                                     cudaMemcpyHostToDevice, P->h2d));
+        FSLD_TRY(cudaEventRecord(P->eh[g], P->h2d));
+    }
+    // batch rows + per-step binning, regrouped by slab (independent of v: overlaps the first copies)
+    FSLD_TRY(cudaMemcpyAsync(idx_dev, idx_host, sizeof(int32_t) * (size_t)B, cudaMemcpyHostToDevice, s));
+    FSLD_TRY(cudaMemsetAsync(gpart, 0, L.hout - L.gpart, s));
+    FSLD_TRY(launch_sorted_bin(a, s));
+    FSLD_TRY(launch_slab_items(a, layers, G, gitems, gctl, s));
+    auto init = [&](int g) -> cudaError_t {  // grad = lam v on slab g (+ ||v||^2 partials), on `stream`
+        cudaError_t r = cudaStreamWaitEvent(s, P->eh[g], 0);
+        for (int q = 0; q < np[g] && r == cudaSuccess; ++q) {
+            const size_t o = (size_t)zi0[g][q] * M * M;
+            r = launch_grad_init((int64_t)nz[g][q] * M * M, reinterpret_cast<const float2*>(v_dev) + o, lam,
+                                 reinterpret_cast<float2*>(grad_dev) + o, npart + (2 * g + q) * kInitParts,
+                                 kInitParts, s);
+        }
+        return r == cudaSuccess ? cudaEventRecord(P->ei[g], s) : r;
+    };
+    // Slab g's bricks read v up to the first plane of slab g + 1 and flush into it, so pass g
+    // starts after slab g + 1 is copied and initialised.  Passes of neighbouring slabs only meet
+    // in red.global adds, so they run concurrently (two kernel streams: one pass's tail overlaps
+    // the next one's start).  Slab g's gradient is final once passes g - 1 and g are done.
+    a.items = gitems;
+    for (int g = 0; g < G; ++g) FSLD_TRY(init(g));
+    for (int g = 0; g < G; ++g) {
+        cudaStream_t ks = P->ks[g & 1];
+        FSLD_TRY(cudaStreamWaitEvent(ks, P->ei[g + 1 < G ? g + 1 : g], 0));
+        a.ctl = gctl + 16 * g;
+        a.part = gpart + (size_t)g * kSlabCtas;
+        int grid = 0;
+        FSLD_TRY(launch_sorted_pass(a, ks, &grid));
+        if (grid > kSlabCtas) return cudaErrorInvalidConfiguration;
+        FSLD_TRY(cudaEventRecord(P->ek[g], ks));
+        FSLD_TRY(cudaStreamWaitEvent(P->d2h, P->ek[g], 0));
+        if (g > 0) FSLD_TRY(cudaStreamWaitEvent(P->d2h, P->ek[g - 1], 0));
+        for (int q = 0; q < np[g]; ++q)
+            FSLD_TRY(cudaMemcpyAsync(gh + zi0[g][q] * plane, gd + zi0[g][q] * plane, nz[g][q] * plane,
+                                     cudaMemcpyDeviceToHost, P->d2h));
+    }
+    for (int q = 0; q < 2 && q < G; ++q) FSLD_TRY(cudaStreamWaitEvent(s, P->ek[G - 1 - q], 0));
+    FSLD_TRY(cudaEventRecord(P->join, P->d2h));
+    FSLD_TRY(launch_loss_finalize(gpart, G * kSlabCtas, npart, G * 2 * kInitParts, scale, lam, hout, hout + 1, s));
+    FSLD_TRY(cudaMemcpyAsync(out_host, hout, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    FSLD_TRY(cudaStreamWaitEvent(s, P->join, 0));
+#undef FSLD_TRY
+    return cudaSuccess;
+}
+
+struct HostGraph {
+    HostStepKey key{};
+    int dev = -1;
+    cudaGraphExec_t exec = nullptr;
+    int32_t* idx_pinned = nullptr;  // the graph's source of the batch rows
+    cudaEvent_t done = nullptr;     // after the last replay: idx_pinned may be rewritten
+    unsigned long long used = 0;
+};
+HostGraph g_graphs[8];
+unsigned long long g_graph_clock = 0;
+
+void drop_graph(HostGraph& h) {
+    if (h.done) cudaEventSynchronize(h.done), cudaEventDestroy(h.done);
+    if (h.exec) cudaGraphExecDestroy(h.exec);
+    if (h.idx_pinned) cudaFreeHost(h.idx_pinned);
+    h = HostGraph{};
+}
+
+// The cached graph for (device, key), captured on first use (LRU over 8 entries).
+cudaError_t host_graph(const HostStepKey& k, HostPipe* P, HostGraph*& out) {
+    cudaStream_t s = P->cap;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    HostGraph* lru = &g_graphs[0];
+    for (HostGraph& h : g_graphs) {
+        if (h.exec && h.dev == dev && h.key == k) {
+            h.used = ++g_graph_clock;
+            out = &h;
+            return cudaSuccess;
+        }
+        if (h.used < lru->used) lru = &h;
+    }
+    drop_graph(*lru);
+    HostGraph& h = *lru;
+    if ((e = cudaHostAlloc(reinterpret_cast<void**>(&h.idx_pinned), sizeof(int32_t) * (size_t)k.B,
+                           cudaHostAllocDefault)) != cudaSuccess) {
+        h = HostGraph{};
+        return e;
+    }
+    if ((e = cudaEventCreateWithFlags(&h.done, cudaEventDisableTiming)) != cudaSuccess) {
+        drop_graph(h);
+        return e;
+    }
+    cudaGraph_t g = nullptr;
+    e = prepare_host_step();  // lazily initialised launch state (attributes, grid sizes): not under capture
+    if (e == cudaSuccess) e = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
+    if (e == cudaSuccess) {
+        const cudaError_t e1 = host_step_enqueue(k, P, h.idx_pinned, s);
+        e = cudaStreamEndCapture(s, &g);
+        if (e1 != cudaSuccess) e = e1;
+    }
+    if (e == cudaSuccess) e = cudaGraphInstantiate(&h.exec, g, 0);
+    if (g) cudaGraphDestroy(g);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        drop_graph(h);
+        return e;
+    }
+    h.key = k;
+    h.dev = dev;
+    h.used = ++g_graph_clock;
+    out = &h;
+    return cudaSuccess;
+}
+
+}  // namespace
+
+extern "C" int fsld_loss_grad_host(int M, int mode, int n_mask, const fsld_image_rec* recs, const int32_t* idx_host,
+                                   int B, const void* v_host, const void* xs, const int8_t* pc, const int32_t* seg_off,
+                                   const int32_t* segs, double scale, double lam, void* grad_host, double* out_host,
+                                   void* v_dev, void* grad_dev, int32_t* idx_dev, int n_slabs, void* scratch,
+                                   size_t scratch_bytes, void* stream) {
+    if (!geom_ok(M, mode, n_mask, B) || M > 256 || mode != FSLD_MODE_TRI) return FSLD_EINVAL;
+    if (!recs || !idx_host || !v_host || !xs || !pc || !seg_off || !segs || !grad_host || !out_host || !v_dev ||
+        !grad_dev || !idx_dev || !scratch || v_dev == grad_dev || n_slabs < 1 || n_slabs > kMaxSlabs)
+        return FSLD_EINVAL;
+    const ScratchLayout L = scratch_layout(M, n_mask, B);
+    if (scratch_bytes < L.total || L.cap_items > 200 * 1024) return FSLD_EINVAL;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    HostStepKey k;
+    std::memset(&k, 0, sizeof(k));  // padding bytes take part in the key comparison
+    k.M = M;
+    k.n_mask = n_mask;
+    k.B = B;
+    k.n_slabs = n_slabs;
+    k.recs = recs;
+    k.v_host = v_host;
+    k.xs = xs;
+    k.pc = pc;
+    k.seg_off = seg_off;
+    k.segs = segs;
+    k.grad_host = grad_host;
+    k.out_host = out_host;
+    k.v_dev = v_dev;
+    k.grad_dev = grad_dev;
+    k.idx_dev = idx_dev;
+    k.scratch = scratch;
+    k.scale = scale;
+    k.lam = lam;
+    std::lock_guard<std::mutex> lk(g_pipe_mu);
+    HostPipe* P = nullptr;
+    cudaError_t e = pipe_for_device(P);
+    if (e != cudaSuccess) return status_of(e);
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if ((e = cudaStreamIsCapturing(s, &cs)) != cudaSuccess) return status_of(e);
+    if (cs != cudaStreamCaptureStatusNone) return status_of(host_step_enqueue(k, P, idx_host, s));  // caller's graph
+    HostGraph* h = nullptr;
+    if ((e = host_graph(k, P, h)) != cudaSuccess) return status_of(e);
+    if ((e = cudaEventSynchronize(h->done)) != cudaSuccess) return status_of(e);  // previous replay read its rows
+    std::memcpy(h->idx_pinned, idx_host, sizeof(int32_t) * (size_t)B);
+    if ((e = cudaGraphLaunch(h->exec, s)) != cudaSuccess) return status_of(e);
+    note_bins(scratch, idx_dev, recs, M, n_mask, B);
+    return status_of(cudaEventRecord(h->done, s));
 }

@@ -96,8 +96,14 @@ struct __align__(16) PairRec {
 };
 static_assert(sizeof(PairRec) == 16, "PairRec is one 16-byte word");
 
+// Slab-pipelined host step (fsld_loss_grad_host): at most kMaxSlabs z-slabs of brick layers, each
+// with its own work-item list, control block and partial sums.
+constexpr int kMaxSlabs = 16;
+constexpr int kSlabCtas = 148 * 8;     // >= the persistent brick grid (CTAs per SM x SMs)
+constexpr int kInitParts = 148 * 2;    // grad_init partial sums per contiguous volume piece
+
 struct ScratchLayout {
-    size_t hdr, cnt, off, fill, pairs, tmpl, items, ctl, part, total;
+    size_t hdr, cnt, off, fill, pairs, tmpl, items, ctl, part, gitems, gctl, gpart, npart, hout, total;
     int nb, nbr, cap_pairs, cap_items, cap_part;
 };
 
@@ -143,6 +149,10 @@ cudaError_t launch_sorted_fill(int M, int n_mask, const short2* pix, const fsld_
                                int2* segs, cudaStream_t s);
 cudaError_t launch_sorted_loss_grad(const SortedArgs& a, double* sq_out, cudaStream_t s);
 cudaError_t launch_planned_loss_grad(const SortedArgs& a, double* sq_out, cudaStream_t s);
+cudaError_t launch_sorted_bin(const SortedArgs& a, cudaStream_t s);
+cudaError_t launch_slab_items(const SortedArgs& a, int layers, int G, int4* gitems, int* gctl, cudaStream_t s);
+cudaError_t launch_sorted_pass(const SortedArgs& a, cudaStream_t s, int* grid);
+cudaError_t prepare_host_step();
 cudaError_t launch_plan_build(SortedArgs a, const PlanLayout& P, char* plan, cudaStream_t s);  // + hutch if a.zbits
 cudaError_t set_phase_profile(unsigned long long* buf);
 

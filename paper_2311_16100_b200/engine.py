@@ -15,6 +15,7 @@ sm_100a kernels of libfsld_b200.so.
 """
 from __future__ import annotations
 
+import os
 import ctypes
 
 import numpy as np
@@ -324,6 +325,39 @@ class SliceEngine:
                                                 scr.numel() * 8, ctypes_ptr(nscr), nscr.numel() * 8, _stream()),
                 "fsld_loss_grad_step_planned")
         return loss, sq
+
+    HOST_SLABS = int(os.environ.get("FSLD_HOST_SLABS", "8"))  # z-slabs of the pipelined host step
+
+    def loss_grad_host(self, v_host, idx_host, scale: float, lam: float, grad_host, out_host,
+                       stage: dict, n_slabs: int | None = None) -> None:
+        """fsld_loss_grad_host: pinned host v / idx in, pinned host grad and out_host = [sq, loss]
+        written once the current stream is synchronised.  The copies run slab by slab on the
+        library's own copy streams, overlapping each other and the brick passes.  ``stage``
+        holds the device staging tensors "v", "g" (M^3 complex64) and "idx" (>= B int32)."""
+        lib = C.load()
+        if not self.brick_path:
+            raise ValueError("the host step runs the brick path (tri, sorted, non-deterministic)")
+        for t, n in ((v_host, self.n_voxels), (grad_host, self.n_voxels)):
+            if t.device.type != "cpu" or not t.is_pinned() or t.dtype != torch.complex64 or t.numel() != n \
+                    or not t.is_contiguous():
+                raise ValueError("v_host / grad_host must be pinned contiguous complex64 host tensors of M^3")
+        if idx_host.device.type != "cpu" or not idx_host.is_pinned() or idx_host.dtype != torch.int32:
+            raise ValueError("idx_host must be a pinned int32 host tensor")
+        B = int(idx_host.numel())
+        if B == 0:
+            raise ValueError("batch must be nonempty")
+        if int(idx_host.min()) < 0 or int(idx_host.max()) >= self.n_images:
+            raise ValueError("batch index out of range")
+        scr = self.scratch(B)
+        if stage["idx"].numel() < B:
+            stage["idx"] = torch.empty(B, dtype=torch.int32, device=self.dev)
+        C.check(lib.fsld_loss_grad_host(self.M, self.mode_id, self.n_mask, ctypes_ptr(self.recs),
+                                        ctypes_ptr(idx_host), B, ctypes_ptr(v_host), ctypes_ptr(self.x),
+                                        ctypes_ptr(self.pc), ctypes_ptr(self.seg_off), ctypes_ptr(self.segs),
+                                        float(scale), float(lam), ctypes_ptr(grad_host), ctypes_ptr(out_host),
+                                        ctypes_ptr(stage["v"]), ctypes_ptr(stage["g"]), ctypes_ptr(stage["idx"]),
+                                        int(n_slabs or self.HOST_SLABS), ctypes_ptr(scr), scr.numel() * 8,
+                                        _stream()), "fsld_loss_grad_host")
 
     def proj_energy_planned(self, d, plan: "BinPlan", k: int, out=None) -> torch.Tensor:
         lib = C.load()

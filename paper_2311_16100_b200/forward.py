@@ -318,8 +318,9 @@ class DatasetOperator:
 
     def loss_and_grad_host(self, v_host, idx_host, lam: float, grad_host, n_total: int | None = None) -> float:
         """Host-buffer loss_and_grad: pinned complex64 v (M^3) and int32 idx in, grad written to the
-        pinned complex64 ``grad_host``; returns the loss.  All copies are async on the current
-        stream; one synchronisation at the end (for the loss value)."""
+        pinned complex64 ``grad_host``; returns the loss.  All copies are async; one synchronisation
+        at the end (for the loss value).  On the brick path the volume moves in z-slabs through
+        fsld_loss_grad_host (copies overlapped with each other and with the kernels)."""
         e = self.engine
         st = getattr(self, "_host_stage", None)
         if st is None:
@@ -335,6 +336,11 @@ class DatasetOperator:
             raise ValueError("batch must be nonempty")
         n_total = self.n_images if n_total is None else n_total
         scale = n_total / B
+        if e.brick_path:  # slab-pipelined: copies in both directions overlap the brick passes
+            st.setdefault("idx", torch.empty(B, dtype=torch.int32, device=e.dev))
+            e.loss_grad_host(v_host, idx_host, scale, lam, grad_host, st["out_h"], st)
+            torch.cuda.current_stream().synchronize()
+            return float(st["out_h"][1])
         st["v"].copy_(v_host, non_blocking=True)
         idx = idx_host.to(e.dev, non_blocking=True)
         if e.deterministic:

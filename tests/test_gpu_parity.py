@@ -473,3 +473,55 @@ def test_brick_path_randomised_vs_tile_and_coverage(M, B, seed, radius_frac):
     sq2, a2, _ = tile.loss_grad(v, idx)
     assert abs(float(sq1) - float(sq2)) <= 1e-6 * float(sq2)
     assert rel(a1.cpu().numpy(), a2.cpu().numpy()) < 1e-5
+
+
+@pytest.mark.parametrize("M,B,slabs", [(16, 40, 1), (33, 64, 3), (40, 64, 2), (64, 256, 8), (65, 96, 16),
+                                       (128, 512, 8), (128, 300, 5), (128, 64, 16)])
+def test_host_step_pipelined_matches_device_step(M, B, slabs):
+    """fsld_loss_grad_host (z-slab pipelined copies, per-slab work items) equals the device-resident
+    loss_and_grad for any slab count, including M whose brick layers straddle kz = 0 (M=40, 65),
+    and agrees with the fp64 oracle (loss_and_grad, optim.py:165-190) within the fp32 tolerance."""
+    mask = O.disk_mask(M, M // 2 - 1)
+    pix = O.mask_pix(M, mask)
+    n_img = 2 * B
+    q = synth.haar_quaternions(n_img, 11 * M)
+    sh = synth.normal_shifts(n_img, 11 * M + 1)
+    ctfs = synth.physical_ctfs(n_img, 11 * M + 2)
+    rng = np.random.default_rng(M)
+    x = (rng.standard_normal((n_img, mask.size)) + 1j * rng.standard_normal((n_img, mask.size))) * 1e-3
+    op = gpu_op(M, "tri", mask, q, sh, ctfs, x)
+    v = synth.gaussian_blob_volume(M, 2) * (1 + 0.1 * rng.standard_normal(M ** 3))
+    batch = np.sort(rng.choice(n_img, B, replace=False)).astype(np.int32)
+    lam = 2e-3
+    l_ref, g_ref = F.loss_and_grad(op, v, batch, lam)
+    v_h = torch.from_numpy(v.astype(np.complex64)).pin_memory()
+    g_h = torch.zeros(M ** 3, dtype=torch.complex64).pin_memory()
+    idx_h = torch.from_numpy(batch).pin_memory()
+    op.engine.HOST_SLABS = slabs
+    for _ in range(2):  # re-entrant: the second call reuses the staging buffers and events
+        g_h.zero_()
+        l_h = op.loss_and_grad_host(v_h, idx_h, lam, g_h)
+    assert abs(l_h - l_ref) / l_ref < 1e-6
+    assert rel(g_h.numpy(), g_ref) < 1e-6
+    if M <= 65:
+        ctab = O.ctf_table_physical(synth.ctf_param_array(ctfs), pix, M)
+        oop = O.OracleOperator(M, "tri", mask, q, sh, ctab, x)
+        lr, gr = O.loss_and_grad(oop, v, batch, lam)
+        assert abs(l_h - lr) / lr < TOL
+        assert rel(g_h.numpy(), gr) < TOL
+
+
+def test_host_step_rejects_bad_buffers():
+    M, B = 16, 8
+    mask = O.disk_mask(M, M // 2 - 1)
+    q = synth.haar_quaternions(B, 5)
+    op = gpu_op(M, "tri", mask, q, None, None, np.ones((B, mask.size), np.complex64))
+    v_h = torch.zeros(M ** 3, dtype=torch.complex64).pin_memory()
+    g_h = torch.zeros(M ** 3, dtype=torch.complex64).pin_memory()
+    with pytest.raises(ValueError):
+        op.loss_and_grad_host(v_h, torch.zeros(0, dtype=torch.int32).pin_memory(), 0.0, g_h)
+    with pytest.raises(ValueError):
+        op.loss_and_grad_host(v_h, torch.tensor([0, B], dtype=torch.int32).pin_memory(), 0.0, g_h)
+    with pytest.raises(ValueError):
+        op.loss_and_grad_host(v_h, torch.tensor([0, 1], dtype=torch.int32).pin_memory(), 0.0,
+                              torch.zeros(M ** 3, dtype=torch.complex64))
