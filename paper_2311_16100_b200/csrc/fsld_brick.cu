@@ -557,19 +557,19 @@ cudaError_t launch_sorted_pass(const SortedArgs& a, cudaStream_t s, int* grid) {
     return launch_sorted_main<false>(a, nullptr, s, grid);
 }
 
-// Work items of one binned batch regrouped by z-slab (G slabs of `layers` brick layers each)
+// Work items of one binned batch regrouped by z-slab (brick z-layer -> slab from `map`)
 // for the slab-pipelined host step (fsld_loss_grad_host).  Stable: every slab keeps the
 // full-first / largest-first order of scan_batch.  Slab g's items are gitems[gctl_g[4] ..
 // + gctl_g[0]), gctl_g = gctl + 16 g = {n, claim counter 0, 0, pairs base, items base}.
 __global__ void __launch_bounds__(1024) slab_items_kernel(const int4* __restrict__ items, const int* __restrict__ ctl,
-                                                          int nb, int layers, int G, int4* __restrict__ gitems,
+                                                          int nb, SlabMap map, int G, int4* __restrict__ gitems,
                                                           int* __restrict__ gctl) {
     extern __shared__ unsigned char slab_of[];  // per item: its slab (one coalesced pass over the items)
     __shared__ int wsum[32];
     __shared__ int base_s;
     items += ctl[4];
     const int n = ctl[0], nb2 = nb * nb;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) slab_of[i] = (unsigned char)((__ldg(&items[i].x) / nb2) / layers);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) slab_of[i] = map.of_layer[__ldg(&items[i].x) / nb2];
     const int per = (n + 1023) / 1024;
     const int lo = min((int)threadIdx.x * per, n), hi = min(lo + per, n);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -626,11 +626,11 @@ cudaError_t prepare_host_step() {
     return e;
 }
 
-cudaError_t launch_slab_items(const SortedArgs& a, int layers, int G, int4* gitems, int* gctl, cudaStream_t s) {
+cudaError_t launch_slab_items(const SortedArgs& a, const SlabMap& map, int G, int4* gitems, int* gctl, cudaStream_t s) {
     cudaError_t e = prepare_host_step();
     if (e != cudaSuccess) return e;
     if (a.cap_items > 200 * 1024) return cudaErrorInvalidValue;
-    slab_items_kernel<<<1, 1024, (size_t)a.cap_items, s>>>(a.items, a.ctl, a.nb, layers, G, gitems, gctl);
+    slab_items_kernel<<<1, 1024, (size_t)a.cap_items, s>>>(a.items, a.ctl, a.nb, map, G, gitems, gctl);
     return cudaGetLastError();
 }
 

@@ -763,6 +763,26 @@ cudaError_t pipe_for_device(HostPipe*& out) {
     return cudaSuccess;
 }
 
+// Slabs of brick z-layers: first[g] .. first[g+1].  The copies in and out are the critical path, so
+// the two slabs at each end are one layer thick (the first gradient slab is ready, and its copy
+// out starts, early; little work is left after the last copy in) and the middle layers are split
+// evenly into the remaining n_slabs - 4 (uniform slabs for n_slabs < 6 or few layers).
+int slab_layers(int nb, int n_slabs, int* first) {
+    int G = 0;
+    first[0] = 0;
+    if (n_slabs >= 6 && nb >= n_slabs) {
+        const int mid = n_slabs - 4, mid_layers = nb - 4;
+        int l = 0;
+        for (int g = 0; g < 2; ++g) first[++G] = ++l;
+        for (int g = 0; g < mid; ++g) first[++G] = (l += mid_layers / mid + (g < mid_layers % mid ? 1 : 0));
+        for (int g = 0; g < 2; ++g) first[++G] = ++l;
+        return G;
+    }
+    const int layers = (nb + n_slabs - 1) / n_slabs;
+    for (int l = 0; l < nb;) first[++G] = (l = std::min(nb, l + layers));
+    return G;
+}
+
 // Slab g = kz in [z0, z1) as at most two contiguous plane ranges of the FFT-ordered z axis.
 int slab_pieces(int M, int z0, int z1, int zi0[2], int nz[2]) {
     int n = 0;
@@ -811,8 +831,11 @@ cudaError_t host_step_enqueue(const HostStepKey& k, HostPipe* P, const int32_t* 
                                grad_dev, scratch);
     a.out_scale = (float)scale;
     const int c = (M + 1) / 2, nb = L.nb;
-    const int layers = (nb + n_slabs - 1) / n_slabs;
-    const int G = (nb + layers - 1) / layers;
+    int first[kMaxSlabs + 1];
+    const int G = slab_layers(nb, n_slabs, first);
+    SlabMap map{};
+    for (int g = 0; g < G; ++g)
+        for (int l = first[g]; l < first[g + 1]; ++l) map.of_layer[l] = (unsigned char)g;
     const size_t plane = (size_t)M * M * sizeof(float2);
     int4* gitems = reinterpret_cast<int4*>(scr + L.gitems);
     int* gctl = reinterpret_cast<int*>(scr + L.gctl);
@@ -826,24 +849,25 @@ cudaError_t host_step_enqueue(const HostStepKey& k, HostPipe* P, const int32_t* 
 
     cudaError_t e = cudaSuccess;
 #define FSLD_TRY(x) do { if ((e = (x)) != cudaSuccess) return e; } while (0)
+    // batch rows first (2 KB: the binning must not queue behind a volume slab on the copy engine)
+    FSLD_TRY(cudaMemcpyAsync(idx_dev, idx_host, sizeof(int32_t) * (size_t)B, cudaMemcpyHostToDevice, s));
     // fork: the copy streams start after whatever `stream` already holds (v_dev / grad_dev reuse)
     FSLD_TRY(cudaEventRecord(P->fork, s));
     FSLD_TRY(cudaStreamWaitEvent(P->h2d, P->fork, 0));
     FSLD_TRY(cudaStreamWaitEvent(P->d2h, P->fork, 0));
     int zi0[kMaxSlabs][2], nz[kMaxSlabs][2], np[kMaxSlabs];
     for (int g = 0; g < G; ++g) {
-        const int z0 = -c + BT * layers * g, z1 = std::min(-c + BT * layers * (g + 1), M - c);
+        const int z0 = -c + BT * first[g], z1 = std::min(-c + BT * first[g + 1], M - c);
         np[g] = slab_pieces(M, z0, z1, zi0[g], nz[g]);
         for (int q = 0; q < np[g]; ++q)
             FSLD_TRY(cudaMemcpyAsync(vd + zi0[g][q] * plane, vh + zi0[g][q] * plane, nz[g][q] * plane,
                                      cudaMemcpyHostToDevice, P->h2d));
         FSLD_TRY(cudaEventRecord(P->eh[g], P->h2d));
     }
-    // batch rows + per-step binning, regrouped by slab (independent of v: overlaps the first copies)
-    FSLD_TRY(cudaMemcpyAsync(idx_dev, idx_host, sizeof(int32_t) * (size_t)B, cudaMemcpyHostToDevice, s));
+    // per-step binning, regrouped by slab (independent of v: overlaps the first copies)
     FSLD_TRY(cudaMemsetAsync(gpart, 0, L.hout - L.gpart, s));
     FSLD_TRY(launch_sorted_bin(a, s));
-    FSLD_TRY(launch_slab_items(a, layers, G, gitems, gctl, s));
+    FSLD_TRY(launch_slab_items(a, map, G, gitems, gctl, s));
     auto init = [&](int g) -> cudaError_t {  // grad = lam v on slab g (+ ||v||^2 partials), on `stream`
         cudaError_t r = cudaStreamWaitEvent(s, P->eh[g], 0);
         for (int q = 0; q < np[g] && r == cudaSuccess; ++q) {
@@ -990,7 +1014,12 @@ extern "C" int fsld_loss_grad_host(int M, int mode, int n_mask, const fsld_image
     if (e != cudaSuccess) return status_of(e);
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     if ((e = cudaStreamIsCapturing(s, &cs)) != cudaSuccess) return status_of(e);
-    if (cs != cudaStreamCaptureStatusNone) return status_of(host_step_enqueue(k, P, idx_host, s));  // caller's graph
+    static const bool no_graph = [] {  // FSLD_HOST_GRAPH=0: enqueue every call (A/B of the graph replay)
+        const char* v = std::getenv("FSLD_HOST_GRAPH");
+        return v && v[0] == '0';
+    }();
+    if (cs != cudaStreamCaptureStatusNone || no_graph)  // the caller's own capture, or no replay
+        return status_of(host_step_enqueue(k, P, idx_host, s));
     HostGraph* h = nullptr;
     if ((e = host_graph(k, P, h)) != cudaSuccess) return status_of(e);
     if ((e = cudaEventSynchronize(h->done)) != cudaSuccess) return status_of(e);  // previous replay read its rows

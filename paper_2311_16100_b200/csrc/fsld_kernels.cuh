@@ -150,7 +150,10 @@ cudaError_t launch_sorted_fill(int M, int n_mask, const short2* pix, const fsld_
 cudaError_t launch_sorted_loss_grad(const SortedArgs& a, double* sq_out, cudaStream_t s);
 cudaError_t launch_planned_loss_grad(const SortedArgs& a, double* sq_out, cudaStream_t s);
 cudaError_t launch_sorted_bin(const SortedArgs& a, cudaStream_t s);
-cudaError_t launch_slab_items(const SortedArgs& a, int layers, int G, int4* gitems, int* gctl, cudaStream_t s);
+struct SlabMap {                 // brick z-layer -> slab of the host step (nb <= 32 for M <= 256)
+    unsigned char of_layer[32];
+};
+cudaError_t launch_slab_items(const SortedArgs& a, const SlabMap& map, int G, int4* gitems, int* gctl, cudaStream_t s);
 cudaError_t launch_sorted_pass(const SortedArgs& a, cudaStream_t s, int* grid);
 cudaError_t prepare_host_step();
 cudaError_t launch_plan_build(SortedArgs a, const PlanLayout& P, char* plan, cudaStream_t s);  // + hutch if a.zbits

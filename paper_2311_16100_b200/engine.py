@@ -326,7 +326,7 @@ class SliceEngine:
                 "fsld_loss_grad_step_planned")
         return loss, sq
 
-    HOST_SLABS = int(os.environ.get("FSLD_HOST_SLABS", "8"))  # z-slabs of the pipelined host step
+    HOST_SLABS = int(os.environ.get("FSLD_HOST_SLABS", "12"))  # z-slabs of the pipelined host step
 
     def loss_grad_host(self, v_host, idx_host, scale: float, lam: float, grad_host, out_host,
                        stage: dict, n_slabs: int | None = None) -> None:
