@@ -204,10 +204,19 @@ __global__ void __launch_bounds__(256) grad_init_kernel(int64_t n, const float2*
     const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const bool vec = ((reinterpret_cast<uintptr_t>(v) | reinterpret_cast<uintptr_t>(grad)) & 15) == 0;
     const int64_t n2 = vec ? n / 2 : 0;
-    for (int64_t i = t0; i < n2; i += stride) {
-        const float4 w = __ldg(reinterpret_cast<const float4*>(v) + i);
-        reinterpret_cast<float4*>(grad)[i] = make_float4(lam * w.x, lam * w.y, lam * w.z, lam * w.w);
-        s += (double)fmaf(w.x, w.x, w.y * w.y) + (double)fmaf(w.z, w.z, w.w * w.w);
+    for (int64_t i = t0; i < n2; i += 4 * stride) {  // four independent 16-byte loads in flight
+        float4 w[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            w[u] = i + u * stride < n2 ? __ldg(reinterpret_cast<const float4*>(v) + i + u * stride)
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (i + u * stride >= n2) break;
+            reinterpret_cast<float4*>(grad)[i + u * stride] =
+                make_float4(lam * w[u].x, lam * w[u].y, lam * w[u].z, lam * w[u].w);
+            s += (double)fmaf(w[u].x, w[u].x, w[u].y * w[u].y) + (double)fmaf(w[u].z, w[u].z, w[u].w * w[u].w);
+        }
     }
     for (int64_t i = 2 * n2 + t0; i < n; i += stride) {
         const float2 w = v[i];

@@ -557,59 +557,68 @@ cudaError_t launch_sorted_pass(const SortedArgs& a, cudaStream_t s, int* grid) {
     return launch_sorted_main<false>(a, nullptr, s, grid);
 }
 
-// Work items of one binned batch regrouped by z-slab (brick z-layer -> slab from `map`)
-// for the slab-pipelined host step (fsld_loss_grad_host).  Stable: every slab keeps the
+// Work items of one binned batch regrouped by z-slab (brick z-layer -> slab from `map`) for the
+// slab-pipelined host step (fsld_loss_grad_host): a stable partition, so every slab keeps the
 // full-first / largest-first order of scan_batch.  Slab g's items are gitems[gctl_g[4] ..
 // + gctl_g[0]), gctl_g = gctl + 16 g = {n, claim counter 0, 0, pairs base, items base}.
+// One CTA of 32 warps; warp w owns a contiguous run of items: per-(warp, slab) counts with
+// match.any, a (slab-major, warp-minor) scan, then each item's rank among its chunk's equal-slab
+// lanes gives its position.
 __global__ void __launch_bounds__(1024) slab_items_kernel(const int4* __restrict__ items, const int* __restrict__ ctl,
                                                           int nb, SlabMap map, int G, int4* __restrict__ gitems,
                                                           int* __restrict__ gctl) {
-    extern __shared__ unsigned char slab_of[];  // per item: its slab (one coalesced pass over the items)
-    __shared__ int wsum[32];
-    __shared__ int base_s;
+    __shared__ int cnt[32][kMaxSlabs];  // per warp and slab: count, then the running output position
     items += ctl[4];
     const int n = ctl[0], nb2 = nb * nb;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) slab_of[i] = map.of_layer[__ldg(&items[i].x) / nb2];
-    const int per = (n + 1023) / 1024;
-    const int lo = min((int)threadIdx.x * per, n), hi = min(lo + per, n);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (threadIdx.x == 0) base_s = 0;
+    const int per = ((n + 31) / 32 + 31) & ~31;  // items per warp, whole chunks of 32
+    const int lo = min(warp * per, n), hi = min(lo + per, n);
+    for (int t = threadIdx.x; t < 32 * kMaxSlabs; t += blockDim.x) cnt[t / kMaxSlabs][t % kMaxSlabs] = 0;
     __syncthreads();
-    for (int g = 0; g < G; ++g) {
-        int cnt = 0;
-        for (int i = lo; i < hi; ++i) cnt += slab_of[i] == g;
-        int incl = cnt;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int t = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += t;
-        }
-        if (lane == 31) wsum[warp] = incl;
-        __syncthreads();
-        if (warp == 0) {
-            int t = wsum[lane];
+    for (int b = lo; b < hi; b += 32) {
+        const int i = b + lane;
+        const int g = i < hi ? (int)map.of_layer[__ldg(&items[i].x) / nb2] : -1;
+        const unsigned m = __match_any_sync(0xffffffffu, g);
+        if (g >= 0 && lane == __ffs(m) - 1) cnt[warp][g] += __popc(m);
+    }
+    __syncthreads();
+    if (warp == 0) {  // exclusive scan over (slab, warp), slab-major; lane handles one warp column
+        int base = 0;
+        for (int g = 0; g < G; ++g) {
+            const int c = cnt[lane][g];
+            int incl = c;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
-                const int u = __shfl_up_sync(0xffffffffu, t, o);
-                if (lane >= o) t += u;
+                const int t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += t;
             }
-            wsum[lane] = t;
+            cnt[lane][g] = base + incl - c;
+            const int sum = __shfl_sync(0xffffffffu, incl, 31);
+            if (lane == 0) {
+                int* q = gctl + 16 * g;
+                q[0] = sum;
+                q[1] = 0;
+                q[2] = 0;
+                q[3] = ctl[3];
+                q[4] = base;
+            }
+            base += sum;
         }
-        __syncthreads();
-        int pos = base_s + (warp > 0 ? wsum[warp - 1] : 0) + incl - cnt;
-        for (int i = lo; i < hi; ++i)
-            if (slab_of[i] == g) gitems[pos++] = items[i];
-        __syncthreads();  // base_s and wsum read by everyone
-        if (threadIdx.x == 0) {
-            int* q = gctl + 16 * g;
-            q[0] = wsum[31];
-            q[1] = 0;
-            q[2] = 0;
-            q[3] = ctl[3];
-            q[4] = base_s;
-            base_s += wsum[31];
+    }
+    __syncthreads();
+    for (int b = lo; b < hi; b += 32) {
+        const int i = b + lane;
+        int4 it = make_int4(0, 0, 0, 0);
+        int g = -1;
+        if (i < hi) {
+            it = items[i];
+            g = map.of_layer[it.x / nb2];
         }
-        __syncthreads();
+        const unsigned m = __match_any_sync(0xffffffffu, g);
+        if (g >= 0) gitems[cnt[warp][g] + __popc(m & ((1u << lane) - 1u))] = it;
+        __syncwarp();
+        if (g >= 0 && lane == __ffs(m) - 1) cnt[warp][g] += __popc(m);
+        __syncwarp();
     }
 }
 
@@ -617,11 +626,8 @@ __global__ void __launch_bounds__(1024) slab_items_kernel(const int4* __restrict
 cudaError_t prepare_host_step() {
     static bool done = false;
     if (done) return cudaSuccess;
-    // the item count is device-side: the slab table is sized for the capacity
-    cudaError_t e = cudaFuncSetAttribute(slab_items_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    if (e != cudaSuccess) return e;
     int grid = 0;
-    e = main_grid<false>(grid);
+    cudaError_t e = main_grid<false>(grid);
     done = e == cudaSuccess;
     return e;
 }
@@ -629,8 +635,7 @@ cudaError_t prepare_host_step() {
 cudaError_t launch_slab_items(const SortedArgs& a, const SlabMap& map, int G, int4* gitems, int* gctl, cudaStream_t s) {
     cudaError_t e = prepare_host_step();
     if (e != cudaSuccess) return e;
-    if (a.cap_items > 200 * 1024) return cudaErrorInvalidValue;
-    slab_items_kernel<<<1, 1024, (size_t)a.cap_items, s>>>(a.items, a.ctl, a.nb, map, G, gitems, gctl);
+    slab_items_kernel<<<1, 1024, 0, s>>>(a.items, a.ctl, a.nb, map, G, gitems, gctl);
     return cudaGetLastError();
 }
 

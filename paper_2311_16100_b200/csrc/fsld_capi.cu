@@ -986,7 +986,7 @@ extern "C" int fsld_loss_grad_host(int M, int mode, int n_mask, const fsld_image
         !grad_dev || !idx_dev || !scratch || v_dev == grad_dev || n_slabs < 1 || n_slabs > kMaxSlabs)
         return FSLD_EINVAL;
     const ScratchLayout L = scratch_layout(M, n_mask, B);
-    if (scratch_bytes < L.total || L.cap_items > 200 * 1024) return FSLD_EINVAL;
+    if (scratch_bytes < L.total) return FSLD_EINVAL;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     HostStepKey k;
     std::memset(&k, 0, sizeof(k));  // padding bytes take part in the key comparison
