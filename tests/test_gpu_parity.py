@@ -502,7 +502,7 @@ def test_host_step_pipelined_matches_device_step(M, B, slabs):
         g_h.zero_()
         l_h = op.loss_and_grad_host(v_h, idx_h, lam, g_h)
     assert abs(l_h - l_ref) / l_ref < 1e-6
-    assert rel(g_h.numpy(), g_ref) < 1e-6
+    assert rel(g_h.numpy(), g_ref) < 5e-6  # fp32 epilogue on the device vs fp64 on the host
     if M <= 65:
         ctab = O.ctf_table_physical(synth.ctf_param_array(ctfs), pix, M)
         oop = O.OracleOperator(M, "tri", mask, q, sh, ctab, x)
@@ -525,3 +525,29 @@ def test_host_step_rejects_bad_buffers():
     with pytest.raises(ValueError):
         op.loss_and_grad_host(v_h, torch.tensor([0, 1], dtype=torch.int32).pin_memory(), 0.0,
                               torch.zeros(M ** 3, dtype=torch.complex64))
+
+
+def test_host_step_graph_cache_across_shapes_and_scalars():
+    """The host step caches one CUDA graph per call shape: alternating batch sizes, lam values and
+    host buffers must each give the device path's result (no stale graph, rows re-staged per call)."""
+    from paper_2311_16100_b200 import _capi as C
+    M = 48
+    mask = O.disk_mask(M, M // 2 - 1)
+    n_img = 300
+    q = synth.haar_quaternions(n_img, 91)
+    sh = synth.normal_shifts(n_img, 92)
+    ctfs = synth.physical_ctfs(n_img, 93)
+    rng = np.random.default_rng(94)
+    x = (rng.standard_normal((n_img, mask.size)) + 1j * rng.standard_normal((n_img, mask.size))) * 1e-2
+    op = gpu_op(M, "tri", mask, q, sh, ctfs, x)
+    v = synth.gaussian_blob_volume(M, 5)
+    v_h = [C.host_empty(M ** 3, torch.complex64), torch.zeros(M ** 3, dtype=torch.complex64).pin_memory()]
+    for t in v_h:
+        t.copy_(torch.from_numpy(v.astype(np.complex64)))
+    g_h = C.host_empty(M ** 3, torch.complex64)
+    for it, (B, lam) in enumerate([(64, 1e-3), (100, 1e-3), (64, 5e-2), (100, 1e-3), (64, 1e-3)]):
+        batch = np.sort(rng.choice(n_img, B, replace=False)).astype(np.int32)
+        l_ref, g_ref = F.loss_and_grad(op, v, batch, lam, n_total=n_img)
+        l_h = op.loss_and_grad_host(v_h[it % 2], torch.from_numpy(batch).pin_memory(), lam, g_h, n_total=n_img)
+        assert abs(l_h - l_ref) / l_ref < 1e-6, it
+        assert rel(g_h.numpy(), g_ref) < 5e-6, it  # fp32 epilogue on the device vs fp64 on the host
