@@ -10,10 +10,17 @@
 // to speed.
 #pragma once
 
+#ifndef FSLD_BANK_ORDER  // 1: order segments by (rank within bank, bank); 0: by wave (same floor voxel rank)
+#define FSLD_BANK_ORDER 1
+#endif
+
 __global__ void __launch_bounds__(256) wave_order_kernel(int M, int n_mask, const fsld_image_rec* __restrict__ recs,
                                                          float2* xs, char2* pc, const int32_t* __restrict__ seg_off,
                                                          const int2* __restrict__ segs) {
     __shared__ int cnt[BW][BT * BT * BT];
+#if FSLD_BANK_ORDER
+    __shared__ int hist[BW][128];
+#endif
     __shared__ float frs[6];
     const int i = blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -34,7 +41,7 @@ __global__ void __launch_bounds__(256) wave_order_kernel(int M, int n_mask, cons
         const int ox = -c + BT * (bid % nb), oy = -c + BT * ((bid / nb) % nb), oz = -c + BT * (bid / (nb * nb));
         char2 kk[U];
         float2 xv[U];
-        int lv[U], wv[U];
+        int lv[U], wv[U], l9[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int e = lane + 32 * u;
@@ -46,10 +53,66 @@ __global__ void __launch_bounds__(256) wave_order_kernel(int M, int n_mask, cons
                 float cx, cy, cz, fx, fy, fz;
                 floor_corner((float)kk[u].x, (float)kk[u].y, fr, bnd, cx, cy, cz, fx, fy, fz);
                 lv[u] = (((int)fz - oz) * BT + ((int)fy - oy)) * BT + ((int)fx - ox);
+                l9[u] = (((int)fz - oz) * BH + ((int)fy - oy)) * BH + ((int)fx - ox);
                 wv[u] = min(atomicAdd(&cnt[warp][lv[u]], 1), 3);
             }
         }
         __syncwarp();
+#if FSLD_BANK_ORDER
+        // counting sort of the segment by (rank among the segment's pixels in the same shared-memory
+        // bank, bank): bank = 9-stride brick index of the floor voxel mod 32.  Every run of 32
+        // consecutive pixels then takes at most one pixel per bank from each rank level, so a
+        // warp's corner gathers (LDS.64) and scatters (ATOMS) see few bank conflicts; pixels with
+        // the same floor voxel share a bank and land on different rank levels (the wave order's
+        // property is kept).
+        for (int q = lane; q < 128; q += 32) hist[warp][q] = 0;
+        __syncwarp();
+        int key[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {  // rank within the bank: cnt[warp][bank] reused as counters
+            key[u] = -1;
+            if (wv[u] >= 0) {
+                const int bank = l9[u] & 31;
+                key[u] = min(atomicAdd(&cnt[warp][BT * BT * BT - 32 + bank], 1), 3) * 32 + bank;
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (key[u] >= 0) atomicAdd(&hist[warp][key[u]], 1);
+        __syncwarp();
+        {  // exclusive scan of the 128 counters, four per lane
+            int h[4], t = 0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                h[j] = hist[warp][4 * lane + j];
+                t += h[j];
+            }
+            int incl = t;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            int b = incl - t;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                hist[warp][4 * lane + j] = b;
+                b += h[j];
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (key[u] < 0) continue;
+            const int pos = atomicAdd(&hist[warp][key[u]], 1);
+            pc[row + start + pos] = kk[u];
+            if (xs) xs[row + start + pos] = xv[u];
+            cnt[warp][lv[u]] = 0;
+        }
+        __syncwarp();
+        if (lane < 32) cnt[warp][BT * BT * BT - 32 + lane] = 0;  // bank counters (after every lv reset)
+#else
         // counting sort of the segment by wave, stable in (u, lane) order
         int base[4];
         int run = 0;
@@ -75,6 +138,7 @@ __global__ void __launch_bounds__(256) wave_order_kernel(int M, int n_mask, cons
                 cnt[warp][lv[u]] = 0;
             }
         }
+#endif
         __syncwarp();
     }
 }
