@@ -22,7 +22,15 @@ __device__ unsigned long long* g_phase_prof = nullptr;
 #define PHASE_FLUSH() \
     if (ph_on) for (int q = 0; q < 9; ++q) atomicAdd(g_phase_prof + q, ph_acc[q])
 
-constexpr int RB = 1024;                               // pixels per round (pass 1 -> pass 2 buffer)
+constexpr int RB = 1024;                               // pixels per round (hutch / energy kernels)
+// Pixels per round of the loss+grad kernel (pass 1 -> pass 2 buffer): 1,280 fills the shared memory
+// of 4 CTAs/SM (fewer rounds per item: +1.3 % over 1,024); the probe-carrying variant keeps 1,024
+// (its extra buffers would drop it to 3 CTAs/SM).
+#ifndef FSLD_RB_MAIN
+#define FSLD_RB_MAIN 1280
+#endif
+template <bool HUTCH>
+constexpr int rb_main() { return HUTCH ? 1024 : FSLD_RB_MAIN; }
 constexpr int BU = (BH3 + BTHREADS - 1) / BTHREADS;    // brick voxels per thread (3)
 constexpr int SEG_T = BTHREADS / BC;                   // threads per segment in the bk build (4)
 static_assert(BTHREADS % BC == 0 && BC % 32 == 0 && BC <= BTHREADS, "segment table: one scan warp per 32 segments");
@@ -34,14 +42,14 @@ struct SortedSmemT {
     int acci[BH3];                  // (im)
     int acch[HUTCH ? BH3 : 1];      // fixed-point Hutchinson accumulator (real)
     unsigned char zc[HUTCH ? BH3 : 1];  // z signs: bit c = z at corner c of floor voxel l (bit 0 = z_l)
-    float2 bval[RB];                // pass 1 -> 2: conj(f) r
-    float4 bgeo[RB];                // pass 1 -> 2: (wx, wy, wz, local corner index)
-    float hval[HUTCH ? RB : 1];     // pass 1 -> 2: C^2 P z (also z staging during setup)
+    float2 bval[rb_main<HUTCH>()];             // pass 1 -> 2: conj(f) r
+    float4 bgeo[rb_main<HUTCH>()];             // pass 1 -> 2: (wx, wy, wz, local corner index)
+    float hval[HUTCH ? rb_main<HUTCH>() : 1];  // pass 1 -> 2: C^2 P z (also z staging during setup)
     int4 segw[BC * SEG_W];          // the item's segment records (gofs rebased to the flat index), SEG_W words apart
     __device__ __forceinline__ SegRec& seg(int k) { return *reinterpret_cast<SegRec*>(segw + k * SEG_W); }
     PairRec prec[BC];               // the next item's pair records (staged first: their tslots address the templates)
     int pref[BC + 1];               // exclusive prefix of segment lengths
-    unsigned char bk[RB];           // round pixel -> segment
+    unsigned char bk[rb_main<HUTCH>()];  // round pixel -> segment
     int4 item_desc;                 // first item of this CTA (prologue)
     int4 next_desc;                 // the item after the current one ((-1, ..) = none)
     int vmax_bits, hmax_bits;
@@ -359,8 +367,9 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArg
             }
         };
 
-        for (int r0 = 0; r0 < total; r0 += RB) {
-            const int rn = min(RB, total - r0);
+        constexpr int RBK = rb_main<HUTCH>();
+        for (int r0 = 0; r0 < total; r0 += RBK) {
+            const int rn = min(RBK, total - r0);
             {  // round pixel -> segment table: SEG_T threads per segment
                 const int k = threadIdx.x / SEG_T, q = threadIdx.x % SEG_T;
                 if (k < nseg) {
@@ -438,7 +447,7 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArg
                 }
             }
             lsum += (double)sq;
-            if (r0 + RB >= total && nxt.x >= 0) cp_async_wait_all();  // nxt's pair records (stage_pairs)
+            if (r0 + RBK >= total && nxt.x >= 0) cp_async_wait_all();  // nxt's pair records (stage_pairs)
             {  // maxima >= 0, so their bit patterns order like ints
                 const int vb_max = __reduce_max_sync(0xffffffffu, __float_as_int(vmax));
                 if (lane == 0) atomicMax(&S.vmax_bits, vb_max);
@@ -449,7 +458,7 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArg
             }
             __syncthreads();
             PHASE_MARK(2);
-            if (r0 + RB >= total && nxt.x >= 0) stage_item(S, a, nxt, lxyz);  // overlaps pass 2 + flush
+            if (r0 + RBK >= total && nxt.x >= 0) stage_item(S, a, nxt, lxyz);  // overlaps pass 2 + flush
             // ---------------- pass 2: fixed-point adjoint scatter (kernels.py:221-230)
             {
                 const float vm = __int_as_float(S.vmax_bits);
