@@ -492,8 +492,11 @@ def run_b200(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(cfg, B, lam)
     algo1 = None
-    if world == 1 and not args.no_algo1:
+    if world == 1 and not args.no_algo1 and eng.brick_path:  # the device step runs on binning plans
         algo1 = algo1_leg(eng, wl, B, lam, args)
+    elif world == 1 and not args.no_algo1:
+        algo1 = {"skipped": f"{cfg.mode} mode runs the per-pixel tile path; the device Algorithm-1 leg uses "
+                            "brick binning plans (tri)"}
     run = None
     if world == 1 and args.run_epochs > 0 and args.config == "cfg3" and not args.no_algo1:
         run = run_leg(eng, wl, B, lam, args.run_epochs)
@@ -760,9 +763,11 @@ def e2e_leg(eng, wl, B, lam, n_total, args, world):
     ms = t0.elapsed_time(t1) / args.steps
     return {"value": world * B / (ms * 1e-3), "unit": "images/s", "ms_per_step": ms,
             "h2d_bytes_per_step": 8 * M ** 3 + 4 * B, "d2h_bytes_per_step": 8 * M ** 3 + 16,
-            "path": "DatasetOperator.loss_and_grad_host -> fsld_loss_grad_host (pinned host v / idx in, pinned "
-                    "host grad + loss out; z-slab pipeline: copies in both directions overlap each other and "
-                    "the brick passes; one cached CUDA graph per call shape)",
+            "path": ("DatasetOperator.loss_and_grad_host -> fsld_loss_grad_host (pinned host v / idx in, pinned "
+                     "host grad + loss out; z-slab pipeline: copies in both directions overlap each other and "
+                     "the brick passes; one cached CUDA graph per call shape)" if eng.brick_path else
+                     "DatasetOperator.loss_and_grad_host (pinned host v / idx in, tile-path loss+grad, pinned host "
+                     "grad + loss out)"),
             "host_buffers": "fsld_host_alloc (cudaHostAlloc)"}
 
 
