@@ -12,7 +12,8 @@ from paper_2311_16100_b200 import synth  # noqa: E402
 from paper_2311_16100_b200.forward import DatasetOperator  # noqa: E402
 
 slabs = [int(s) for s in (sys.argv[1] if len(sys.argv) > 1 else "1,4,6,8,10,12,16").split(",")]
-wl = synth.build_workload(synth.CONFIGS["cfg3"], seed=0, n_images=8192)
+N_IMG = int(os.environ.get("FSLD_AB_IMAGES", "8192"))
+wl = synth.build_workload(synth.CONFIGS["cfg3"], seed=0, n_images=N_IMG)
 op = DatasetOperator.from_engine(wl.engine)
 M, B = 128, 512
 v_h = C.host_empty(M ** 3, torch.complex64)
@@ -22,7 +23,7 @@ gen = np.random.default_rng(3)
 idx = []
 for _ in range(16):
     t = C.host_empty(B, torch.int32)
-    t.copy_(torch.from_numpy(gen.choice(8192, B, replace=False).astype(np.int32)))
+    t.copy_(torch.from_numpy(gen.choice(N_IMG, B, replace=False).astype(np.int32)))
     idx.append(t)
 res = {n: [] for n in slabs}
 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
