@@ -8,13 +8,17 @@
 // staged in shared memory and each pixel's 8 corners are read from there.
 #pragma once
 
+#ifndef FSLD_RB_ENERGY  // pixels per round (the pixel -> segment table)
+#define FSLD_RB_ENERGY 4096
+#endif
+
 struct EnergySmem {
     float2 vb[BH3];
     int4 segw[BC * SEG_W];  // segment records, SEG_W words apart (fsld_kernels.cuh)
     __device__ __forceinline__ SegRec& seg(int k) { return *reinterpret_cast<SegRec*>(segw + k * SEG_W); }
     int pref[BC + 1];
     int wtot[BC / 32];
-    unsigned char bk[RB];
+    unsigned char bk[FSLD_RB_ENERGY];
     int4 item_desc;
     double red[BW];
 };
@@ -88,8 +92,8 @@ __global__ void __launch_bounds__(BTHREADS) sorted_energy_kernel(SortedArgs a) {
         }
         __syncthreads();
         const int total = S.pref[nseg];
-        for (int r0 = 0; r0 < total; r0 += RB) {
-            const int rn = min(RB, total - r0);
+        for (int r0 = 0; r0 < total; r0 += FSLD_RB_ENERGY) {
+            const int rn = min(FSLD_RB_ENERGY, total - r0);
             {
                 const int k = threadIdx.x / SEG_T, q = threadIdx.x % SEG_T;
                 if (k < nseg) {

@@ -11,6 +11,10 @@
 // pass suffices (no staging buffers).  k <= 256.
 #pragma once
 
+#ifndef FSLD_RB_HUTCH  // pixels per round (the pixel -> segment table)
+#define FSLD_RB_HUTCH 4096
+#endif
+
 constexpr int kHutchMaxWords = 8;
 
 struct HutchSmem {
@@ -20,7 +24,7 @@ struct HutchSmem {
     __device__ __forceinline__ SegRec& seg(int k) { return *reinterpret_cast<SegRec*>(segw + k * SEG_W); }
     int pref[BC + 1];
     int wtot[BC / 32];
-    unsigned char bk[RB];
+    unsigned char bk[FSLD_RB_HUTCH];
     int4 item_desc;
 };
 
@@ -84,8 +88,8 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_hutch_kernel(SortedArgs a,
         const int total = S.pref[nseg];
         // |C^2 w_c S_c| <= k; <= 12 contributions per voxel per image segment -> |sum| < 2^31
         const float sc = exp2f(floorf(log2f(fminf(4194303.0f, 178956970.0f / (float)nseg) / kf)));
-        for (int r0 = 0; r0 < total; r0 += RB) {
-            const int rn = min(RB, total - r0);
+        for (int r0 = 0; r0 < total; r0 += FSLD_RB_HUTCH) {
+            const int rn = min(FSLD_RB_HUTCH, total - r0);
             {
                 const int kk = threadIdx.x / SEG_T, q = threadIdx.x % SEG_T;
                 if (kk < nseg) {
