@@ -10,6 +10,9 @@
 // to speed.
 #pragma once
 
+#ifndef FSLD_BANK_LEVELS  // rank levels of the bank order (ranks beyond the last share it)
+#define FSLD_BANK_LEVELS 8
+#endif
 #ifndef FSLD_BANK_ORDER  // 1: order segments by (rank within bank, bank); 0: by wave (same floor voxel rank)
 #define FSLD_BANK_ORDER 1
 #endif
@@ -19,7 +22,7 @@ __global__ void __launch_bounds__(256) wave_order_kernel(int M, int n_mask, cons
                                                          const int2* __restrict__ segs) {
     __shared__ int cnt[BW][BT * BT * BT];
 #if FSLD_BANK_ORDER
-    __shared__ int hist[BW][128];
+    __shared__ int hist[BW][32 * FSLD_BANK_LEVELS];
 #endif
     __shared__ float frs[6];
     const int i = blockIdx.x;
@@ -65,7 +68,7 @@ __global__ void __launch_bounds__(256) wave_order_kernel(int M, int n_mask, cons
         // warp's corner gathers (LDS.64) and scatters (ATOMS) see few bank conflicts; pixels with
         // the same floor voxel share a bank and land on different rank levels (the wave order's
         // property is kept).
-        for (int q = lane; q < 128; q += 32) hist[warp][q] = 0;
+        for (int q = lane; q < 32 * FSLD_BANK_LEVELS; q += 32) hist[warp][q] = 0;
         __syncwarp();
         int key[U];
 #pragma unroll
@@ -73,7 +76,7 @@ __global__ void __launch_bounds__(256) wave_order_kernel(int M, int n_mask, cons
             key[u] = -1;
             if (wv[u] >= 0) {
                 const int bank = l9[u] & 31;
-                key[u] = min(atomicAdd(&cnt[warp][BT * BT * BT - 32 + bank], 1), 3) * 32 + bank;
+                key[u] = min(atomicAdd(&cnt[warp][BT * BT * BT - 32 + bank], 1), FSLD_BANK_LEVELS - 1) * 32 + bank;
             }
         }
         __syncwarp();
@@ -81,11 +84,12 @@ __global__ void __launch_bounds__(256) wave_order_kernel(int M, int n_mask, cons
         for (int u = 0; u < U; ++u)
             if (key[u] >= 0) atomicAdd(&hist[warp][key[u]], 1);
         __syncwarp();
-        {  // exclusive scan of the 128 counters, four per lane
-            int h[4], t = 0;
+        {  // exclusive scan of the 32 * FSLD_BANK_LEVELS counters, FSLD_BANK_LEVELS per lane
+            constexpr int NL = FSLD_BANK_LEVELS;
+            int h[NL], t = 0;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                h[j] = hist[warp][4 * lane + j];
+            for (int j = 0; j < NL; ++j) {
+                h[j] = hist[warp][NL * lane + j];
                 t += h[j];
             }
             int incl = t;
@@ -96,8 +100,8 @@ __global__ void __launch_bounds__(256) wave_order_kernel(int M, int n_mask, cons
             }
             int b = incl - t;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                hist[warp][4 * lane + j] = b;
+            for (int j = 0; j < NL; ++j) {
+                hist[warp][NL * lane + j] = b;
                 b += h[j];
             }
         }
