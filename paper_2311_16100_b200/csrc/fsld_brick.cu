@@ -24,6 +24,8 @@
 // accumulator (scale from the round's max, native ATOMS.ADD); each round is
 // flushed with one red.global.add.v2.f32 per touched brick voxel.  Every pixel
 // belongs to exactly one segment, so it is processed exactly once.
+#include <mutex>
+
 #include "fsld_kernels.cuh"
 
 namespace fsld {
@@ -502,23 +504,38 @@ cudaError_t set_phase_profile(unsigned long long* buf) {
     return cudaMemcpyToSymbol(g_phase_prof, &buf, sizeof(buf));
 }
 
-// Persistent grid of the brick kernel (SMs x resident CTAs), set up on first use.
+// Persistent grid (SMs x resident CTAs) of a brick kernel and its >48 KB dynamic shared-memory
+// opt-in, per device: the attribute belongs to a device context, so every device a process uses
+// is set up on its own first launch (std::call_once per device and kernel).
+constexpr int kMaxDevices = 16;
+struct GridCache {
+    std::once_flag once[kMaxDevices];
+    int grid[kMaxDevices] = {};
+    cudaError_t err[kMaxDevices] = {};
+};
+
+template <typename Kern>
+static cudaError_t persistent_grid(GridCache& C, Kern kern, size_t smem, int& out) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+    std::call_once(C.once[dev], [&] {
+        cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        int sms = 0, occ = 0;
+        if (r == cudaSuccess) r = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (r == cudaSuccess) r = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, BTHREADS, smem);
+        C.grid[dev] = sms * (occ > 0 ? occ : 1);
+        C.err[dev] = r;
+    });
+    out = C.grid[dev];
+    return C.err[dev];
+}
+
 template <bool HUTCH>
 static cudaError_t main_grid(int& out) {
-    static int grid = 0;
-    if (grid == 0) {
-        const size_t smem = sizeof(SortedSmemT<HUTCH>);
-        cudaError_t e = cudaFuncSetAttribute(sorted_loss_grad_kernel<HUTCH>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        int dev = 0, sms = 0, occ = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sorted_loss_grad_kernel<HUTCH>, BTHREADS, smem);
-        grid = sms * (occ > 0 ? occ : 1);
-    }
-    out = grid;
-    return cudaSuccess;
+    static GridCache cache;
+    return persistent_grid(cache, sorted_loss_grad_kernel<HUTCH>, sizeof(SortedSmemT<HUTCH>), out);
 }
 
 template <bool HUTCH>
@@ -622,18 +639,17 @@ __global__ void __launch_bounds__(1024) slab_items_kernel(const int4* __restrict
     }
 }
 
-// Function attributes / grid sizes of the host-step kernels, outside any stream capture.
-cudaError_t prepare_host_step() {
-    static bool done = false;
-    if (done) return cudaSuccess;
+// Function attributes / grid size of the host-step kernel on the current device (outside any
+// stream capture); also the grid the slab passes will use (<= kSlabCtas, checked before launch).
+cudaError_t prepare_host_step(int* grid_out) {
     int grid = 0;
     cudaError_t e = main_grid<false>(grid);
-    done = e == cudaSuccess;
+    if (grid_out) *grid_out = grid;
     return e;
 }
 
 cudaError_t launch_slab_items(const SortedArgs& a, const SlabMap& map, int G, int4* gitems, int* gctl, cudaStream_t s) {
-    cudaError_t e = prepare_host_step();
+    cudaError_t e = prepare_host_step(nullptr);
     if (e != cudaSuccess) return e;
     slab_items_kernel<<<1, 1024, 0, s>>>(a.items, a.ctl, a.nb, map, G, gitems, gctl);
     return cudaGetLastError();
@@ -662,20 +678,12 @@ cudaError_t launch_planned_loss_grad_step(SortedArgs a, int64_t nvox, double sca
     return launch_loss_finalize(a.part, grid, norm_part, n_norm, scale, lam, sq_out, loss, s);
 }
 
-static int g_energy_grid = 0;
-
 cudaError_t launch_sorted_energy(const SortedArgs& a, double* out, bool rebin, cudaStream_t s) {
+    static GridCache cache;
     const size_t smem = sizeof(EnergySmem);
-    if (g_energy_grid == 0) {
-        cudaError_t e = cudaFuncSetAttribute(sorted_energy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
-        if (e != cudaSuccess) return e;
-        int dev = 0, sms = 0, occ = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sorted_energy_kernel, BTHREADS, smem);
-        g_energy_grid = sms * (occ > 0 ? occ : 1);
-    }
+    int grid = 0;
+    cudaError_t e0 = persistent_grid(cache, sorted_energy_kernel, smem, grid);
+    if (e0 != cudaSuccess) return e0;
     if (rebin) {
         bin_sorted_kernel<false><<<a.B, 128, 0, s>>>(a);
         brick_scan_kernel<<<1, 1024, 0, s>>>(a);
@@ -684,25 +692,18 @@ cudaError_t launch_sorted_energy(const SortedArgs& a, double* out, bool rebin, c
         cudaError_t e = cudaMemsetAsync(a.ctl + 1, 0, sizeof(int), s);
         if (e != cudaSuccess) return e;
     }
-    sorted_energy_kernel<<<g_energy_grid, BTHREADS, smem, s>>>(a);
+    sorted_energy_kernel<<<grid, BTHREADS, smem, s>>>(a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    return launch_reduce(a.part, g_energy_grid, out, s);
+    return launch_reduce(a.part, grid, out, s);
 }
 
 cudaError_t launch_sorted_hutch(const SortedArgs& a, int k, cudaStream_t s) {
-    static int grid = 0;
+    static GridCache cache;
     const size_t smem = sizeof(HutchSmem);
-    if (grid == 0) {
-        cudaError_t e = cudaFuncSetAttribute(sorted_hutch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
-        if (e != cudaSuccess) return e;
-        int dev = 0, sms = 0, occ = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sorted_hutch_kernel, BTHREADS, smem);
-        grid = sms * (occ > 0 ? occ : 1);
-    }
+    int grid = 0;
+    cudaError_t e0 = persistent_grid(cache, sorted_hutch_kernel, smem, grid);
+    if (e0 != cudaSuccess) return e0;
     bin_sorted_kernel<false><<<a.B, 128, 0, s>>>(a);
     brick_scan_kernel<<<1, 1024, 0, s>>>(a);
     bin_sorted_kernel<true><<<a.B, 128, 0, s>>>(a);

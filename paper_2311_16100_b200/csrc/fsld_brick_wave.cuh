@@ -23,6 +23,7 @@ __global__ void __launch_bounds__(256) wave_order_kernel(int M, int n_mask, cons
     __shared__ int cnt[BW][BT * BT * BT];
 #if FSLD_BANK_ORDER
     __shared__ int hist[BW][32 * FSLD_BANK_LEVELS];
+    __shared__ int bank_cnt[BW][32];  // per-bank rank counters (own array: cnt still holds voxel counts)
 #endif
     __shared__ float frs[6];
     const int i = blockIdx.x;
@@ -31,12 +32,18 @@ __global__ void __launch_bounds__(256) wave_order_kernel(int M, int n_mask, cons
     const float bnd = (float)(M / 2 - 1);
     if (threadIdx.x < 6) frs[threadIdx.x] = (float)recs[i].rot[threadIdx.x];
     for (int q = lane; q < BT * BT * BT; q += 32) cnt[warp][q] = 0;
+#if FSLD_BANK_ORDER
+    bank_cnt[warp][lane] = 0;
+#endif
     __syncthreads();
     float fr[6];
 #pragma unroll
     for (int q = 0; q < 6; ++q) fr[q] = frs[q];
     const size_t row = (size_t)i * n_mask;
-    constexpr int U = 4;  // 4 x 32 >= BOWN_MAX pixels per segment
+    // Up to U x 32 = 128 pixels of a segment are reordered; a larger segment (the biggest plane
+    // section of an 8^3 brick holds ~91 pixels, more only with many clamped rim pixels) keeps
+    // pixels 128.. in place -- any order is correct, only speed depends on it.
+    constexpr int U = 4;
     for (int s = seg_off[i] + warp; s < seg_off[i + 1]; s += BW) {
         const int2 seg = segs[s];
         const int start = seg.y & 0xFFFF, len = seg.y >> 16;
@@ -72,11 +79,11 @@ __global__ void __launch_bounds__(256) wave_order_kernel(int M, int n_mask, cons
         __syncwarp();
         int key[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {  // rank within the bank: cnt[warp][bank] reused as counters
+        for (int u = 0; u < U; ++u) {  // rank within the bank
             key[u] = -1;
             if (wv[u] >= 0) {
                 const int bank = l9[u] & 31;
-                key[u] = min(atomicAdd(&cnt[warp][BT * BT * BT - 32 + bank], 1), FSLD_BANK_LEVELS - 1) * 32 + bank;
+                key[u] = min(atomicAdd(&bank_cnt[warp][bank], 1), FSLD_BANK_LEVELS - 1) * 32 + bank;
             }
         }
         __syncwarp();
@@ -115,7 +122,7 @@ __global__ void __launch_bounds__(256) wave_order_kernel(int M, int n_mask, cons
             cnt[warp][lv[u]] = 0;
         }
         __syncwarp();
-        if (lane < 32) cnt[warp][BT * BT * BT - 32 + lane] = 0;  // bank counters (after every lv reset)
+        bank_cnt[warp][lane] = 0;
 #else
         // counting sort of the segment by wave, stable in (u, lane) order
         int base[4];

@@ -849,6 +849,11 @@ cudaError_t host_step_enqueue(const HostStepKey& k, HostPipe* P, const int32_t* 
 
     cudaError_t e = cudaSuccess;
 #define FSLD_TRY(x) do { if ((e = (x)) != cudaSuccess) return e; } while (0)
+    // the slab passes' per-CTA partials live in kSlabCtas-sized slots: refuse an oversized grid
+    // before anything is enqueued (nothing half-written)
+    int grid_max = 0;
+    FSLD_TRY(prepare_host_step(&grid_max));
+    if (grid_max > kSlabCtas) return cudaErrorInvalidConfiguration;
     // batch rows first (2 KB: the binning must not queue behind a volume slab on the copy engine)
     FSLD_TRY(cudaMemcpyAsync(idx_dev, idx_host, sizeof(int32_t) * (size_t)B, cudaMemcpyHostToDevice, s));
     // fork: the copy streams start after whatever `stream` already holds (v_dev / grad_dev reuse)
@@ -891,7 +896,6 @@ cudaError_t host_step_enqueue(const HostStepKey& k, HostPipe* P, const int32_t* 
         a.part = gpart + (size_t)g * kSlabCtas;
         int grid = 0;
         FSLD_TRY(launch_sorted_pass(a, ks, &grid));
-        if (grid > kSlabCtas) return cudaErrorInvalidConfiguration;
         FSLD_TRY(cudaEventRecord(P->ek[g], ks));
         FSLD_TRY(cudaStreamWaitEvent(P->d2h, P->ek[g], 0));
         if (g > 0) FSLD_TRY(cudaStreamWaitEvent(P->d2h, P->ek[g - 1], 0));
@@ -953,7 +957,7 @@ cudaError_t host_graph(const HostStepKey& k, HostPipe* P, HostGraph*& out) {
         return e;
     }
     cudaGraph_t g = nullptr;
-    e = prepare_host_step();  // lazily initialised launch state (attributes, grid sizes): not under capture
+    e = prepare_host_step(nullptr);  // lazily initialised launch state (attributes, grid sizes): not under capture
     if (e == cudaSuccess) e = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
     if (e == cudaSuccess) {
         const cudaError_t e1 = host_step_enqueue(k, P, h.idx_pinned, s);

@@ -155,7 +155,7 @@ struct SlabMap {                 // brick z-layer -> slab of the host step (nb <
 };
 cudaError_t launch_slab_items(const SortedArgs& a, const SlabMap& map, int G, int4* gitems, int* gctl, cudaStream_t s);
 cudaError_t launch_sorted_pass(const SortedArgs& a, cudaStream_t s, int* grid);
-cudaError_t prepare_host_step();
+cudaError_t prepare_host_step(int* grid_out);  // per device; grid of the slab passes
 cudaError_t launch_plan_build(SortedArgs a, const PlanLayout& P, char* plan, cudaStream_t s);  // + hutch if a.zbits
 cudaError_t set_phase_profile(unsigned long long* buf);
 
