@@ -347,7 +347,7 @@ def run_b200(args):
         if ev_k0 is not None:
             ev_k0.record()
         C.check(lib.fsld_loss_grad_sorted(M, eng.mode_id, n, ctypes_ptr(eng.recs), ctypes_ptr(idx), B,
-                                          ctypes_ptr(v), ctypes_ptr(eng.x), ctypes_ptr(eng.pc),
+                                          ctypes_ptr(v), ctypes_ptr(eng.x), ctypes_ptr(eng.pc), ctypes_ptr(eng.ptab),
                                           ctypes_ptr(eng.seg_off), ctypes_ptr(eng.segs), ctypes_ptr(acc),
                                           ctypes_ptr(sq), flags, 0, ctypes_ptr(scr), scr.numel() * 8, stream),
                 "loss_grad")
@@ -400,7 +400,8 @@ def run_b200(args):
         if ev_k0 is not None:
             ev_k0.record()
         C.check(lib.fsld_loss_grad_planned(M, eng.mode_id, n, ctypes_ptr(eng.recs), ctypes_ptr(plan.buf), B, k,
-                                           ctypes_ptr(v), ctypes_ptr(eng.x), ctypes_ptr(eng.pc), 0, ctypes_ptr(acc),
+                                           ctypes_ptr(v), ctypes_ptr(eng.x), ctypes_ptr(eng.pc), ctypes_ptr(eng.ptab),
+                                           0, ctypes_ptr(acc),
                                            0, ctypes_ptr(sq), ctypes_ptr(scr), scr.numel() * 8, stream),
                 "loss_grad_planned")
         if ev_k1 is not None:

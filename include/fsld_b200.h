@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define FSLD_ABI_VERSION 1
+#define FSLD_ABI_VERSION 2
 
 /* status codes */
 #define FSLD_OK 0
@@ -227,12 +227,29 @@ int fsld_sorted_fill(int M, int n_mask, const int16_t* pix, const fsld_image_rec
                      const void* x_in, void* x_out, int8_t* pc_out, const int32_t* seg_off,
                      int32_t* segs, void* stream);
 
+/*
+ * Per-pixel invariants of a brick-sorted dataset (poses, shifts and CTFs are fixed for a
+ * refinement run; the reference likewise keeps per-(image, pixel) phase and CTF tables,
+ * forward.py:524-527).  ptab: fsld_sorted_tables_bytes(N, n_mask) bytes (24 per pixel + a
+ * header), 256-byte aligned, opaque; per pixel in the sorted order:
+ *   f = C * phase (fp32 complex, evaluated in fp64; forward.py:93-111, 299-312), and the
+ *   trilinear footprint of the clamped rotated pixel (fp64, kernels.py:42-60, 147-170) in
+ *   the frame of its brick: weights (wx, wy, wz) as fp32 and the corner index in the 9^3 brick.
+ * Passing ptab to the brick entry points below selects the table-driven brick kernel
+ * (24 bytes loaded per pixel instead of evaluating geometry, CTF and phase per pixel);
+ * ptab = NULL runs the compute path from pc and the records.  Rebuild after changing poses
+ * or CTFs (the images themselves are not part of the table).
+ */
+size_t fsld_sorted_tables_bytes(int N, int n_mask);
+int fsld_sorted_tables(int M, int n_mask, const fsld_image_rec* recs, int N, const int8_t* pc,
+                       const int32_t* seg_off, const int32_t* segs, void* ptab, void* stream);
+
 /* Fused loss + gradient over a brick-sorted dataset (optim.py:147-190 hot loop):
  * tri mode runs the brick kernel (smem-staged bricks, one global reduction per
  * touched voxel per work item); nn / deterministic / FSLD_TILE_PATH fall back to
  * the per-pixel tile kernel reading coordinates from pc. */
 int fsld_loss_grad_sorted(int M, int mode, int n_mask, const fsld_image_rec* recs, const int32_t* idx,
-                          int B, const void* v, const void* xs, const int8_t* pc,
+                          int B, const void* v, const void* xs, const int8_t* pc, const void* ptab,
                           const int32_t* seg_off, const int32_t* segs, void* grad_acc, double* sq_out,
                           unsigned flags, const double* fx_scale, void* scratch, size_t scratch_bytes,
                           void* stream);
@@ -255,7 +272,7 @@ int fsld_loss_grad_hutch_sorted(int M, int mode, int n_mask, const fsld_image_re
  * the n_total/|B| scale and lam (forward.py:567-570).  Deterministic / tile-path flags are rejected
  * (use fsld_hvp). */
 int fsld_hvp_sorted(int M, int mode, int n_mask, const fsld_image_rec* recs, const int32_t* idx, int B,
-                    const void* z, const int8_t* pc, const int32_t* seg_off, const int32_t* segs, void* acc,
+                    const void* z, const int8_t* pc, const void* ptab, const int32_t* seg_off, const int32_t* segs, void* acc,
                     double* sq_out, unsigned flags, void* scratch, size_t scratch_bytes, void* stream);
 
 /* Loss only over a brick-sorted dataset (Armijo trials, optim.py:193-207). */
@@ -409,7 +426,8 @@ int fsld_plan_build(int M, int n_mask, const fsld_image_rec* recs, const int32_t
                     const int32_t* seg_off, const int32_t* segs, int64_t total_pairs, void* plan, size_t plan_bytes,
                     void* stream);
 int fsld_loss_grad_planned(int M, int mode, int n_mask, const fsld_image_rec* recs, const void* plan, int B, int k,
-                           const void* v, const void* xs, const int8_t* pc, const uint32_t* zbits, void* grad_acc,
+                           const void* v, const void* xs, const int8_t* pc, const void* ptab, const uint32_t* zbits,
+                           void* grad_acc,
                            float* fold, double* sq_out, void* scratch, size_t scratch_bytes, void* stream);
 /* The complete loss+grad step of batch k of a plan, epilogue fused around the brick pass
  * (optim.py:165-190 with loss_and_grad's scale / lam applied on the device):
@@ -419,7 +437,8 @@ int fsld_loss_grad_planned(int M, int mode, int n_mask, const fsld_image_rec* re
  * separate accumulator is read back or cleared.  scratch: fsld_scratch_bytes(M, n_mask, B);
  * norm_scratch: >= 148 * 8 doubles. */
 int fsld_loss_grad_step_planned(int M, int mode, int n_mask, const fsld_image_rec* recs, const void* plan, int B,
-                                int k, const void* v, const void* xs, const int8_t* pc, double scale, double lam,
+                                int k, const void* v, const void* xs, const int8_t* pc, const void* ptab, double scale,
+                                double lam,
                                 void* grad, double* sq_out, double* loss, void* scratch, size_t scratch_bytes,
                                 void* norm_scratch, size_t norm_scratch_bytes, void* stream);
 /* Host-buffer loss + gradient: the call a host caller makes with numpy-style buffers
@@ -436,8 +455,8 @@ int fsld_loss_grad_step_planned(int M, int mode, int n_mask, const fsld_image_re
  * PCIe transfers in both directions overlap each other and the kernels.  Everything is enqueued
  * on `stream`: the outputs are valid once `stream` has been synchronised. */
 int fsld_loss_grad_host(int M, int mode, int n_mask, const fsld_image_rec* recs, const int32_t* idx_host, int B,
-                        const void* v_host, const void* xs, const int8_t* pc, const int32_t* seg_off,
-                        const int32_t* segs, double scale, double lam, void* grad_host, double* out_host,
+                        const void* v_host, const void* xs, const int8_t* pc, const void* ptab,
+                        const int32_t* seg_off, const int32_t* segs, double scale, double lam, void* grad_host, double* out_host,
                         void* v_dev, void* grad_dev, int32_t* idx_dev, int n_slabs, void* scratch,
                         size_t scratch_bytes, void* stream);
 int fsld_proj_energy_planned(int M, int mode, int n_mask, const fsld_image_rec* recs, const void* plan, int B, int k,

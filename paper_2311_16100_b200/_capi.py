@@ -25,7 +25,7 @@ TILE_PATH = 2
 REUSE_BINS = 4
 REC_CTF = 1
 REC_SHIFT = 2
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 # fsld_image_rec (include/fsld_b200.h): 128 bytes
 REC_DTYPE = np.dtype([
@@ -87,12 +87,14 @@ SIGNATURES = {
     "fsld_scatter_sq_tab": (I, [I, I, I, P, P, I, P, P, U, P, P]),
     "fsld_sorted_count": (I, [I, I, P, P, I, P, P]),
     "fsld_sorted_fill": (I, [I, I, P, P, I, P, P, P, P, P, P]),
-    "fsld_loss_grad_sorted": (I, [I, I, I, P, P, I, P, P, P, P, P, P, P, U, P, P, SZ, P]),
+    "fsld_sorted_tables": (I, [I, I, P, I, P, P, P, P, P]),
+    "fsld_sorted_tables_bytes": (SZ, [I, I]),
+    "fsld_loss_grad_sorted": (I, [I, I, I, P, P, I, P, P, P, P, P, P, P, P, U, P, P, SZ, P]),
     "fsld_loss_sorted": (I, [I, I, I, P, P, I, P, P, P, P, P, SZ, P]),
     "fsld_loss_grad_hutch_sorted": (I, [I, I, I, P, P, I, P, P, P, P, P, P, P, P, P, U, P, SZ, P]),
-    "fsld_hvp_sorted": (I, [I, I, I, P, P, I, P, P, P, P, P, P, U, P, SZ, P]),
-    "fsld_loss_grad_step_planned": (I, [I, I, I, P, P, I, I, P, P, P, D, D, P, P, P, P, SZ, P, SZ, P]),
-    "fsld_loss_grad_host": (I, [I, I, I, P, P, I, P, P, P, P, P, D, D, P, P, P, P, P, I, P, SZ, P]),
+    "fsld_hvp_sorted": (I, [I, I, I, P, P, I, P, P, P, P, P, P, P, U, P, SZ, P]),
+    "fsld_loss_grad_step_planned": (I, [I, I, I, P, P, I, I, P, P, P, P, D, D, P, P, P, P, SZ, P, SZ, P]),
+    "fsld_loss_grad_host": (I, [I, I, I, P, P, I, P, P, P, P, P, P, D, D, P, P, P, P, P, I, P, SZ, P]),
     "fsld_project_sorted": (I, [I, I, I, P, P, I, P, P, P, P]),
     "fsld_backproject_sorted": (I, [I, I, I, P, P, I, P, P, P, U, P, P]),
     "fsld_fixed_scale": (I, [P, I64, D, D, P, P]),
@@ -109,7 +111,7 @@ SIGNATURES = {
     "fsld_ball_gather": (I, [I64, P, P, P, I, P]),
     "fsld_plan_bytes": (SZ, [I, I, I, I, I64]),
     "fsld_plan_build": (I, [I, I, P, P, I, I, P, P, I64, P, SZ, P]),
-    "fsld_loss_grad_planned": (I, [I, I, I, P, P, I, I, P, P, P, P, P, P, P, P, SZ, P]),
+    "fsld_loss_grad_planned": (I, [I, I, I, P, P, I, I, P, P, P, P, P, P, P, P, P, SZ, P]),
     "fsld_proj_energy_planned": (I, [I, I, I, P, P, I, I, P, P, P, P, SZ, P]),
     "fsld_ball_scatter": (I, [I64, P, P, P, I, P]),
 }

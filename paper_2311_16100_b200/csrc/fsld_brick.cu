@@ -96,8 +96,8 @@ __global__ void __launch_bounds__(256) sorted_count_kernel(int M, int n_mask, co
     __syncthreads();
     for (int p = threadIdx.x; p < n_mask; p += blockDim.x) atomicAdd(hist + owner_brick(pix[p], fr, bnd, c, nb), 1);
     __syncthreads();
-    int cnt = 0;
-    for (int b = threadIdx.x; b < nbr; b += blockDim.x) cnt += hist[b] > 0;
+    int cnt = 0;  // segments: a brick's pixels in runs of at most kSegMax
+    for (int b = threadIdx.x; b < nbr; b += blockDim.x) cnt += (hist[b] + kSegMax - 1) / kSegMax;
     atomicAdd(&nseg, cnt);
     __syncthreads();
     if (threadIdx.x == 0) seg_off[i + 1] = nseg;
@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(256) sorted_fill_kernel(int M, int n_mask, con
     int s = 0, g = 0;
     for (int b = lo; b < hi; ++b) {
         s += word[b];
-        g += word[b] > 0;
+        g += (word[b] + kSegMax - 1) / kSegMax;
     }
     tsum[threadIdx.x] = s;
     tseg[threadIdx.x] = g;
@@ -168,7 +168,8 @@ __global__ void __launch_bounds__(256) sorted_fill_kernel(int M, int n_mask, con
     for (int b = lo; b < hi; ++b) {
         const int cnt = word[b];
         word[b] = start | (cnt << 16);
-        if (cnt > 0) segs[sbase + ord++] = make_int2(b, start | (cnt << 16));
+        for (int q = 0; q < cnt; q += kSegMax)  // runs of <= kSegMax pixels (the brick kernels' bound)
+            segs[sbase + ord++] = make_int2(b, (start + q) | (min(kSegMax, cnt - q) << 16));
         start += cnt;
     }
     __syncthreads();
@@ -183,6 +184,7 @@ __global__ void __launch_bounds__(256) sorted_fill_kernel(int M, int n_mask, con
 }
 
 #include "fsld_brick_wave.cuh"
+#include "fsld_brick_tables.cuh"
 
 static int smem_optin(const void* fn, size_t bytes) {
     if (bytes <= 48 * 1024) return 0;
@@ -207,6 +209,15 @@ cudaError_t launch_sorted_fill(int M, int n_mask, const short2* pix, const fsld_
     if (smem_optin((const void*)sorted_fill_kernel, smem)) return cudaErrorInvalidValue;
     sorted_fill_kernel<<<N, 256, smem, s>>>(M, n_mask, pix, recs, x_in, x_out, pc_out, seg_off, segs);
     wave_order_kernel<<<N, 256, 0, s>>>(M, n_mask, recs, x_in ? x_out : nullptr, pc_out, seg_off, segs);
+    return cudaGetLastError();
+}
+
+size_t sorted_tables_bytes(long long npx) { return tables_bytes(npx); }
+
+cudaError_t launch_sorted_tables(int M, int n_mask, const fsld_image_rec* recs, int N, const char2* pc,
+                                 const int32_t* seg_off, const int2* segs, void* ptab, cudaStream_t s) {
+    if (N < 1) return cudaSuccess;
+    sorted_tables_kernel<<<N, 256, 0, s>>>(M, n_mask, recs, pc, seg_off, segs, ptab, (long long)N * n_mask);
     return cudaGetLastError();
 }
 
@@ -499,6 +510,7 @@ cudaError_t launch_plan_build(SortedArgs a, const PlanLayout& P, char* plan, cud
 #include "fsld_brick_main.cuh"  // the work-item kernel (kept separate: it is the tuning target)
 #include "fsld_brick_energy.cuh"
 #include "fsld_brick_hutch.cuh"
+#include "fsld_brick_v3.cuh"
 
 cudaError_t set_phase_profile(unsigned long long* buf) {
     return cudaMemcpyToSymbol(g_phase_prof, &buf, sizeof(buf));
@@ -538,13 +550,24 @@ static cudaError_t main_grid(int& out) {
     return persistent_grid(cache, sorted_loss_grad_kernel<HUTCH>, sizeof(SortedSmemT<HUTCH>), out);
 }
 
+static cudaError_t v3_grid(int& out) {
+    static GridCache cache;
+    return persistent_grid(cache, brick_loss_grad_kernel, sizeof(BrickSmem3), out);
+}
+
 template <bool HUTCH>
 static cudaError_t launch_sorted_main(const SortedArgs& a, double* sq_out, cudaStream_t s, int* grid_out = nullptr) {
-    const size_t smem = sizeof(SortedSmemT<HUTCH>);
     int grid = 0;
-    cudaError_t e0 = main_grid<HUTCH>(grid);
-    if (e0 != cudaSuccess) return e0;
-    sorted_loss_grad_kernel<HUTCH><<<grid, BTHREADS, smem, s>>>(a);
+    if (!HUTCH && a.ptab) {  // the table-driven kernel (per-pixel f and footprint from the dataset tables)
+        cudaError_t e0 = v3_grid(grid);
+        if (e0 != cudaSuccess) return e0;
+        brick_loss_grad_kernel<<<grid, BTHREADS, sizeof(BrickSmem3), s>>>(a);
+    } else {
+        const size_t smem = sizeof(SortedSmemT<HUTCH>);
+        cudaError_t e0 = main_grid<HUTCH>(grid);
+        if (e0 != cudaSuccess) return e0;
+        sorted_loss_grad_kernel<HUTCH><<<grid, BTHREADS, smem, s>>>(a);
+    }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     if (grid_out) {  // the caller reduces the per-CTA partials
@@ -642,9 +665,10 @@ __global__ void __launch_bounds__(1024) slab_items_kernel(const int4* __restrict
 // Function attributes / grid size of the host-step kernel on the current device (outside any
 // stream capture); also the grid the slab passes will use (<= kSlabCtas, checked before launch).
 cudaError_t prepare_host_step(int* grid_out) {
-    int grid = 0;
+    int grid = 0, grid3 = 0;
     cudaError_t e = main_grid<false>(grid);
-    if (grid_out) *grid_out = grid;
+    if (e == cudaSuccess) e = v3_grid(grid3);
+    if (grid_out) *grid_out = grid > grid3 ? grid : grid3;
     return e;
 }
 

@@ -397,7 +397,12 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArg
             for (int e = threadIdx.x; e < rn; e += BTHREADS) {
 #endif
                 SegRegs R;
+#if defined(FSLD_EXP_NO_SEGREC)
+                load_seg(S.seg(0), R);
+                R.gofs = S.seg(S.bk[e]).gofs;
+#else
                 load_seg(S.seg(S.bk[e]), R);
+#endif
                 const long long g = R.gofs + (r0 + e);
                 const char2 kk = a.pc[g];
 #if defined(FSLD_EXP_NO_XLOAD)
@@ -411,7 +416,11 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArg
                 const int l0 = (((int)fz - oz) * BH + ((int)fy - oy)) * BH + ((int)fx - ox);
                 const float wx = cx - fx, wy = cy - fy, wz = cz - fz;
                 const float ax = 1.f - wx, ay = 1.f - wy, az = 1.f - wz;
+#if defined(FSLD_EXP_NO_FACTOR)
+                const float2 f = __ldg(a.xs + g + 7);
+#else
                 const float2 f = seg_factor(R, px, py);
+#endif
                 const float2* vb = S.vb + l0;
                 // trilinear gather (kernels.py:171-176) from the smem brick
                 const float2 WX = make_float2(wx, wx), AX = make_float2(ax, ax);

@@ -1,0 +1,291 @@
+// fsld_brick_v3.cuh -- the table-driven brick kernel of the fused loss+gradient (included by fsld_brick.cu).
+//
+// Same work items, shared-memory brick and fixed-point adjoint as sorted_loss_grad_kernel
+// (fsld_brick_main.cuh), with pass 1 rebuilt around the dataset's per-pixel tables
+// (fsld_brick_tables.cuh):
+//   * no per-pixel segment record, no geometry / CTF / phase arithmetic: f = C * phase (8 B) and
+//     the trilinear footprint (16 B) come from the dataset tables next to the 8-byte image value,
+//     so pass 1 is the 8-corner gather, the residual and conj(f) r;
+//   * the pixel -> segment byte table is built once per work item (not per round), so a thread
+//     can address any pixel of the item: each thread's next pixel is loaded while the current
+//     one is computed, and the first pixel of the next round is loaded before the round's
+//     barrier, so it arrives during pass 2 (the per-pixel HBM latency was the top stall of
+//     the compute path);
+//   * pass 2 (fixed-point scatter, kernels.py:221-230) is unchanged.
+#pragma once
+
+#ifndef FSLD_RB3
+#define FSLD_RB3 1280
+#endif
+constexpr int RB3 = FSLD_RB3;
+constexpr int BK3 = BC * kSegMax;  // pixels per work item (<= BC segments of <= kSegMax pixels)
+
+struct BrickSmem3 {
+    float2 vb[BH3];         // v brick + halo
+    int accr[BH3];          // fixed-point adjoint accumulator (re)
+    int acci[BH3];          // (im)
+    float2 bval[RB3];       // pass 1 -> 2: conj(f) r
+    float4 bgeo[RB3];       // pass 1 -> 2: (wx, wy, wz, l0)
+    unsigned char bk[BK3];  // item pixel -> segment
+    PairRec prec[BC];       // the item's pair records (gofs, count)
+    long long sg[BC];       // segment start rebased to the item's flat pixel index: gofs - pref
+    int pref[BC + 1];       // exclusive prefix of segment lengths
+    int4 item_desc, next_desc;
+    int vmax2[2];           // round maximum |conj(f) r| bits, by round parity
+    int wtot[BC / 32];
+    double red[BW];
+};
+
+// L2 prefetch of [p, p + bytes) (TMA bulk prefetch: 16-byte granules, rounded outwards; the
+// callers' arrays carry >= 16 bytes of slack past their end).
+__device__ __forceinline__ void l2_prefetch(const void* p, size_t bytes) {
+    const uintptr_t a0 = reinterpret_cast<uintptr_t>(p) & ~uintptr_t(15);
+    const uintptr_t a1 = (reinterpret_cast<uintptr_t>(p) + bytes + 15) & ~uintptr_t(15);
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((uint32_t)(a1 - a0)) : "memory");
+}
+
+struct Pix3 {  // one pixel's inputs in registers
+    float2 x, f;
+    float4 geo;  // wx, wy, wz, l0 (int bits)
+};
+
+__device__ __forceinline__ void load_pix3(const SortedArgs& a, const float2* tf, const float4* tg, long long g,
+                                          bool has_x, Pix3& p) {
+    p.f = __ldg(tf + g);
+    p.geo = __ldg(tg + g);
+    p.x = has_x ? __ldg(a.xs + g) : make_float2(0.f, 0.f);
+}
+
+// Per work item (brick, <= BC image segments), as sorted_loss_grad_kernel; per round of RB3 pixels:
+//   pass 1: image value + PixTab, 8-corner gather from the smem brick, r = f P v - x, |r|^2,
+//           conj(f) r -> bval, the footprint -> bgeo (the next pixel's loads in flight);
+//   pass 2: fixed-point scatter of val * w (item scale, power of two, non-increasing).
+__global__ void __launch_bounds__(BTHREADS, 4) brick_loss_grad_kernel(SortedArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    BrickSmem3& S = *reinterpret_cast<BrickSmem3*>(smem_raw);
+    a.pairs += a.ctl[3];
+    a.items += a.ctl[4];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int M = a.M, c = a.c, nb = a.nb;
+    const bool has_x = a.xs != nullptr;
+    const float2* tf = tab_f(a.ptab);
+    const float4* tg = tab_geo(a.ptab, reinterpret_cast<const TabHeader*>(a.ptab)->npx);
+    double lsum = 0.0;
+    int rpar = 0;  // round parity counter (continues across items)
+    int lxyz[BU];
+#pragma unroll
+    for (int u = 0; u < BU; ++u) {
+        const int l = threadIdx.x + u * BTHREADS;
+        lxyz[u] = l < BH3 ? (l % BH) | (((l / BH) % BH) << 4) | ((l / (BH * BH)) << 8) : -1;
+        if (l < BH3) {
+            S.accr[l] = 0;
+            S.acci[l] = 0;
+        }
+    }
+    constexpr int kClaimer = BTHREADS - 32;
+    const int n_items = a.ctl[0];
+    auto claim = [&]() -> int4 {
+        const int it = atomicAdd(a.ctl + 1, 1);
+        return it < n_items ? a.items[it] : make_int4(-1, 0, 0, 0);
+    };
+    auto stage_item3 = [&](int4 item) {  // pair records + v brick (+ halo, zero off the grid), async
+        for (int k = threadIdx.x; k < item.z; k += BTHREADS) cp_async16(S.prec + k, a.pairs + item.y + k);
+        const int bid = item.x;
+        const int ox = -c + BT * (bid % nb), oy = -c + BT * ((bid / nb) % nb), oz = -c + BT * (bid / (nb * nb));
+#pragma unroll
+        for (int u = 0; u < BU; ++u) {
+            if (lxyz[u] < 0) continue;
+            const int l = threadIdx.x + u * BTHREADS;
+            const int kx = ox + (lxyz[u] & 15), ky = oy + ((lxyz[u] >> 4) & 15), kz = oz + (lxyz[u] >> 8);
+            const bool in = kx < M - c && ky < M - c && kz < M - c;
+            const int j = in ? lin_index(kx, ky, kz, M, c) : 0;
+            cp_async8_zfill(S.vb + l, a.v + j, in);
+        }
+    };
+    if (threadIdx.x == kClaimer) {
+        S.item_desc = claim();
+        S.next_desc = claim();
+    }
+    if (threadIdx.x < 2) S.vmax2[threadIdx.x] = 0;
+    __syncthreads();
+    int4 item = S.item_desc;
+    if (item.x >= 0) stage_item3(item);
+
+    for (;;) {
+        if (item.x < 0) break;
+        cp_async_wait_all();
+        __syncthreads();  // (A) this item's pair records and v brick are in shared memory
+        const int4 nxt = S.next_desc;
+        const int bid = item.x, nseg = item.z;
+        const int ox = -c + BT * (bid % nb), oy = -c + BT * ((bid / nb) % nb), oz = -c + BT * (bid / (nb * nb));
+        if (warp < BC / 32) {  // segment-length prefix
+            const int k = threadIdx.x;
+            const int len = k < nseg ? S.prec[k].count : 0;
+            int incl = len;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += t;
+            }
+            S.pref[k] = incl - len;
+            if (lane == 31) S.wtot[warp] = incl;
+        }
+        __syncthreads();  // (B)
+        if (threadIdx.x == kClaimer) S.next_desc = claim();
+        if (threadIdx.x < nseg) {
+            const int k = threadIdx.x;
+            int p = S.pref[k];
+            for (int w = 0; w < (k >> 5); ++w) p += S.wtot[w];
+            S.pref[k] = p;
+            S.sg[k] = S.prec[k].gofs - p;
+        }
+        if (threadIdx.x == 0) {
+            int t = 0;
+            for (int w = 0; w < BC / 32; ++w) t += S.wtot[w];
+            S.pref[nseg] = t;
+        }
+        __syncthreads();
+        {  // item pixel -> segment table: SEG_T threads per segment
+            const int k = threadIdx.x / SEG_T, q = threadIdx.x % SEG_T;
+            if (k < nseg)
+                for (int e = S.pref[k] + q; e < S.pref[k + 1]; e += SEG_T) S.bk[e] = (unsigned char)k;
+        }
+        __syncthreads();
+        const int total = S.pref[nseg];
+        const float lim = (float)min(4194303, 178956970 / nseg);
+        float item_sc = 0.f, item_inv_sc = 1.f;
+        // this thread's first pixel of the item (register buffers A / B alternate: no moves of
+        // in-flight load destinations, so a load is waited for only where its pixel is computed)
+        Pix3 pa, pb;
+        bool next_in_b = false;  // the next round's first pixel was loaded into pb
+        if ((int)threadIdx.x < total) load_pix3(a, tf, tg, S.sg[S.bk[threadIdx.x]] + threadIdx.x, has_x, pa);
+        for (int r0 = 0; r0 < total; r0 += RB3, ++rpar) {
+            const int r1 = min(r0 + RB3, total);
+            const int par = rpar & 1;
+            // ---------------- pass 1 (flattened over the round; the next pixel's loads in flight)
+            float vmax = 0.f, sq = 0.f;
+            auto compute = [&](const Pix3& cur, int e) {
+                const float wx = cur.geo.x, wy = cur.geo.y, wz = cur.geo.z;
+                const int l0 = __float_as_int(cur.geo.w);
+                const float ax = 1.f - wx, ay = 1.f - wy, az = 1.f - wz;
+                const float2 f = cur.f;
+                const float2* vb = S.vb + l0;
+                const float2 WX = make_float2(wx, wx), AX = make_float2(ax, ax);
+                const float2 e0 = __ffma2_rn(WX, vb[1], __fmul2_rn(AX, vb[0]));
+                const float2 e1 = __ffma2_rn(WX, vb[BH + 1], __fmul2_rn(AX, vb[BH]));
+                const float2 e2 = __ffma2_rn(WX, vb[BH * BH + 1], __fmul2_rn(AX, vb[BH * BH]));
+                const float2 e3 = __ffma2_rn(WX, vb[BH * BH + BH + 1], __fmul2_rn(AX, vb[BH * BH + BH]));
+                const float2 q0 = __ffma2_rn(make_float2(wy, wy), e1, __fmul2_rn(make_float2(ay, ay), e0));
+                const float2 q1 = __ffma2_rn(make_float2(wy, wy), e3, __fmul2_rn(make_float2(ay, ay), e2));
+                const float2 pv = __ffma2_rn(make_float2(wz, wz), q1, __fmul2_rn(make_float2(az, az), q0));
+                const float2 prj = cmul(pv, f);
+                const float2 rr = make_float2(prj.x - cur.x.x, prj.y - cur.x.y);
+                sq = fmaf(rr.x, rr.x, fmaf(rr.y, rr.y, sq));
+                const float2 val = cmulconj(f, rr);
+                vmax = fmaxf(vmax, fmaxf(fabsf(val.x), fabsf(val.y)));
+                S.bval[e - r0] = val;
+                S.bgeo[e - r0] = cur.geo;
+            };
+            // target of the load issued before computing pixel e: the thread's next pixel of this
+            // round, else its first pixel of the next round
+            auto next_of = [&](int e) { return e + BTHREADS < r1 ? e + BTHREADS : (r1 < total ? r1 + (int)threadIdx.x : total); };
+            if (next_in_b) pa = pb;  // (arrived during the previous round's pass 2)
+            for (int e = r0 + threadIdx.x; e < r1;) {
+                const int n1 = next_of(e);
+                if (n1 < total) load_pix3(a, tf, tg, S.sg[S.bk[n1]] + n1, has_x, pb);
+                compute(pa, e);
+                if (e + BTHREADS >= r1) {
+                    next_in_b = true;
+                    break;
+                }
+                e += BTHREADS;
+                const int n2 = next_of(e);
+                if (n2 < total) load_pix3(a, tf, tg, S.sg[S.bk[n2]] + n2, has_x, pa);
+                compute(pb, e);
+                next_in_b = false;
+                e += BTHREADS;
+            }
+            lsum += (double)sq;
+            {
+                const int vb_max = __reduce_max_sync(0xffffffffu, __float_as_int(vmax));
+                if (lane == 0) atomicMax(&S.vmax2[par], vb_max);
+            }
+            __syncthreads();
+            if (r1 >= total && nxt.x >= 0) stage_item3(nxt);  // overlaps pass 2 + flush
+            // ---------------- pass 2: fixed-point adjoint scatter (kernels.py:221-230)
+            {
+                const float vm = __int_as_float(S.vmax2[par]);
+                float inv_r;
+                const float sc_r = pow2_scale(lim, vm, inv_r);
+                if (r0 == 0 || sc_r >= item_sc) {
+                    if (r0 == 0) {
+                        item_sc = sc_r;
+                        item_inv_sc = inv_r;
+                    }
+                } else {  // a smaller scale: shift the partial sums down (rounded) first
+                    const int sh = (__float_as_int(item_sc) - __float_as_int(sc_r)) >> 23;
+#pragma unroll
+                    for (int u = 0; u < BU; ++u) {
+                        if (lxyz[u] < 0) continue;
+                        const int l = threadIdx.x + u * BTHREADS;
+                        if (sh >= 31) {
+                            S.accr[l] = 0;
+                            S.acci[l] = 0;
+                        } else {
+                            const long long half = 1ll << (sh - 1);
+                            S.accr[l] = (int)(((long long)S.accr[l] + half) >> sh);
+                            S.acci[l] = (int)(((long long)S.acci[l] + half) >> sh);
+                        }
+                    }
+                    item_sc = sc_r;
+                    item_inv_sc = inv_r;
+                    __syncthreads();
+                }
+            }
+            const float sc = item_sc;
+            const int rn = r1 - r0;
+            for (int e = threadIdx.x; e < rn; e += BTHREADS) {
+                const float4 geo = S.bgeo[e];
+                const int l0 = __float_as_int(geo.w);
+                const float wx = geo.x, wy = geo.y, wz = geo.z;
+                const float ax = 1.f - wx, ay = 1.f - wy, az = 1.f - wz;
+                const float2 val = __fmul2_rn(S.bval[e], make_float2(sc, sc));
+                const float zy00 = az * ay, zy10 = az * wy, zy01 = wz * ay, zy11 = wz * wy;
+                const float w8[8] = {zy00 * ax, zy00 * wx, zy10 * ax, zy10 * wx, zy01 * ax, zy01 * wx, zy11 * ax, zy11 * wx};
+                const int off8[8] = {0, 1, BH, BH + 1, BH * BH, BH * BH + 1, BH * BH + BH, BH * BH + BH + 1};
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const float2 y = __ffma2_rn(make_float2(w8[q], w8[q]), val, make_float2(kMagic, kMagic));
+                    atomicAdd(S.accr + l0 + off8[q], __float_as_int(y.x) - kMagicBits);
+                    atomicAdd(S.acci + l0 + off8[q], __float_as_int(y.y) - kMagicBits);
+                }
+            }
+            if (threadIdx.x == 0) S.vmax2[par ^ 1] = 0;  // the next round's slot (unused since this round's barrier)
+            __syncthreads();
+        }
+        // flush of the item: one reduction per touched voxel, accumulators re-zeroed
+#pragma unroll
+        for (int u = 0; u < BU; ++u) {
+            if (lxyz[u] < 0) continue;
+            const int l = threadIdx.x + u * BTHREADS;
+            const int qr = S.accr[l], qi = S.acci[l];
+            if ((qr | qi) == 0) continue;
+            S.accr[l] = 0;
+            S.acci[l] = 0;
+            const int kx = ox + (lxyz[u] & 15), ky = oy + ((lxyz[u] >> 4) & 15), kz = oz + (lxyz[u] >> 8);
+            if (kx >= M - c || ky >= M - c || kz >= M - c) continue;
+            const size_t j = (size_t)lin_index(kx, ky, kz, M, c);
+            const float fs = item_inv_sc * a.out_scale;
+            red_f32x2(reinterpret_cast<float*>(a.acc) + 2 * j, (float)qr * fs, (float)qi * fs);
+        }
+        item = nxt;
+    }
+    for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+    if (lane == 0) S.red[warp] = lsum;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int w = 0; w < BW; ++w) s += S.red[w];
+        a.part[blockIdx.x] = s;
+    }
+}

@@ -40,10 +40,7 @@ __global__ void __launch_bounds__(256) wave_order_kernel(int M, int n_mask, cons
 #pragma unroll
     for (int q = 0; q < 6; ++q) fr[q] = frs[q];
     const size_t row = (size_t)i * n_mask;
-    // Up to U x 32 = 128 pixels of a segment are reordered; a larger segment (the biggest plane
-    // section of an 8^3 brick holds ~91 pixels, more only with many clamped rim pixels) keeps
-    // pixels 128.. in place -- any order is correct, only speed depends on it.
-    constexpr int U = 4;
+    constexpr int U = kSegMax / 32;  // segments hold <= kSegMax pixels (fsld_sorted_fill splits longer runs)
     for (int s = seg_off[i] + warp; s < seg_off[i + 1]; s += BW) {
         const int2 seg = segs[s];
         const int start = seg.y & 0xFFFF, len = seg.y >> 16;

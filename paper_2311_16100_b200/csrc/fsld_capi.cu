@@ -86,9 +86,10 @@ bool bins_match(const void* scratch, const int32_t* idx, const fsld_image_rec* r
 
 SortedArgs make_sorted(const ScratchLayout& L, int M, int n_mask, int B, const fsld_image_rec* recs,
                        const int32_t* idx, const void* v, const void* xs, const int8_t* pc, const int32_t* seg_off,
-                       const int32_t* segs, void* grad_acc, void* scratch) {
+                       const int32_t* segs, void* grad_acc, void* scratch, const void* ptab = nullptr) {
     char* scr = reinterpret_cast<char*>(scratch);
     SortedArgs b{};
+    b.ptab = ptab;
     b.M = M;
     b.c = (M + 1) / 2;
     b.nb = L.nb;
@@ -354,8 +355,24 @@ int fsld_sorted_fill(int M, int n_mask, const int16_t* pix, const fsld_image_rec
                                         reinterpret_cast<cudaStream_t>(stream)));
 }
 
+size_t fsld_sorted_tables_bytes(int N, int n_mask) {
+    if (N < 1 || n_mask < 1) return 0;
+    return sorted_tables_bytes((long long)N * n_mask);
+}
+
+int fsld_sorted_tables(int M, int n_mask, const fsld_image_rec* recs, int N, const int8_t* pc, const int32_t* seg_off,
+                       const int32_t* segs, void* ptab, void* stream) {
+    if (M < 2 || M > 256 || n_mask < 1 || n_mask > 65535 || N < 1 || !recs || !pc || !seg_off || !segs || !ptab)
+        return FSLD_EINVAL;
+    if (reinterpret_cast<uintptr_t>(ptab) & 255) return FSLD_EINVAL;
+    return status_of(launch_sorted_tables(M, n_mask, recs, N, reinterpret_cast<const char2*>(pc), seg_off,
+                                          reinterpret_cast<const int2*>(segs), ptab,
+                                          reinterpret_cast<cudaStream_t>(stream)));
+}
+
 int fsld_loss_grad_sorted(int M, int mode, int n_mask, const fsld_image_rec* recs, const int32_t* idx, int B,
-                          const void* v, const void* xs, const int8_t* pc, const int32_t* seg_off, const int32_t* segs,
+                          const void* v, const void* xs, const int8_t* pc, const void* ptab, const int32_t* seg_off,
+                          const int32_t* segs,
                           void* grad_acc, double* sq_out, unsigned flags, const double* fx_scale, void* scratch,
                           size_t scratch_bytes, void* stream) {
     if (!geom_ok(M, mode, n_mask, B) || M > 256) return FSLD_EINVAL;
@@ -366,13 +383,13 @@ int fsld_loss_grad_sorted(int M, int mode, int n_mask, const fsld_image_rec* rec
                             fx_scale, scratch, scratch_bytes, stream);
     const ScratchLayout L = scratch_layout(M, n_mask, B);
     if (scratch_bytes < L.total) return FSLD_EINVAL;
-    const SortedArgs b = make_sorted(L, M, n_mask, B, recs, idx, v, xs, pc, seg_off, segs, grad_acc, scratch);
+    const SortedArgs b = make_sorted(L, M, n_mask, B, recs, idx, v, xs, pc, seg_off, segs, grad_acc, scratch, ptab);
     note_bins(scratch, idx, recs, M, n_mask, B);
     return status_of(launch_sorted_loss_grad(b, sq_out, reinterpret_cast<cudaStream_t>(stream)));
 }
 
 int fsld_hvp_sorted(int M, int mode, int n_mask, const fsld_image_rec* recs, const int32_t* idx, int B, const void* z,
-                    const int8_t* pc, const int32_t* seg_off, const int32_t* segs, void* acc, double* sq_out,
+                    const int8_t* pc, const void* ptab, const int32_t* seg_off, const int32_t* segs, void* acc, double* sq_out,
                     unsigned flags, void* scratch, size_t scratch_bytes, void* stream) {
     if (!geom_ok(M, mode, n_mask, B) || M > 256 || mode != FSLD_MODE_TRI) return FSLD_EINVAL;
     if (flags & (FSLD_DETERMINISTIC | FSLD_TILE_PATH)) return FSLD_EINVAL;
@@ -380,7 +397,7 @@ int fsld_hvp_sorted(int M, int mode, int n_mask, const fsld_image_rec* recs, con
     const ScratchLayout L = scratch_layout(M, n_mask, B);
     if (scratch_bytes < L.total) return FSLD_EINVAL;
     // xs = NULL: the kernel takes the images as zero (r = f P z)
-    const SortedArgs b = make_sorted(L, M, n_mask, B, recs, idx, z, nullptr, pc, seg_off, segs, acc, scratch);
+    const SortedArgs b = make_sorted(L, M, n_mask, B, recs, idx, z, nullptr, pc, seg_off, segs, acc, scratch, ptab);
     note_bins(scratch, idx, recs, M, n_mask, B);
     return status_of(launch_sorted_loss_grad(b, sq_out, reinterpret_cast<cudaStream_t>(stream)));
 }
@@ -632,7 +649,7 @@ bool find_plan(const void* plan, PlanKey& out) {
 // SortedArgs of batch k of a built plan (work items ready; scratch supplies the partial sums).
 bool make_planned(SortedArgs& b, const void* plan, int M, int n_mask, int B, int k, const fsld_image_rec* recs,
                   const void* v, const void* xs, const int8_t* pc, void* grad_acc, void* scratch,
-                  size_t scratch_bytes) {
+                  size_t scratch_bytes, const void* ptab = nullptr) {
     PlanKey pk;
     if (!find_plan(plan, pk)) return false;
     const PlanKey* p = &pk;
@@ -641,7 +658,7 @@ bool make_planned(SortedArgs& b, const void* plan, int M, int n_mask, int B, int
     if (scratch_bytes < L.total) return false;
     const PlanLayout P = plan_layout(M, B, p->K, p->total_pairs);
     char* pl = reinterpret_cast<char*>(const_cast<void*>(plan));
-    b = make_sorted(L, M, n_mask, B, recs, nullptr, v, xs, pc, nullptr, nullptr, grad_acc, scratch);
+    b = make_sorted(L, M, n_mask, B, recs, nullptr, v, xs, pc, nullptr, nullptr, grad_acc, scratch, ptab);
     b.ctl = reinterpret_cast<int*>(pl + P.ctl) + 16 * k;
     b.items = reinterpret_cast<int4*>(pl + P.items);
     b.pairs = reinterpret_cast<PairRec*>(pl + P.pairs);
@@ -685,12 +702,12 @@ extern "C" int fsld_plan_build(int M, int n_mask, const fsld_image_rec* recs, co
 
 extern "C" int fsld_loss_grad_planned(int M, int mode, int n_mask, const fsld_image_rec* recs, const void* plan,
                                       int B, int k, const void* v, const void* xs, const int8_t* pc,
-                                      const uint32_t* zbits, void* grad_acc, float* fold, double* sq_out,
+                                      const void* ptab, const uint32_t* zbits, void* grad_acc, float* fold, double* sq_out,
                                       void* scratch, size_t scratch_bytes, void* stream) {
     if (!geom_ok(M, mode, n_mask, B) || M > 256 || mode != FSLD_MODE_TRI) return FSLD_EINVAL;
     if (!recs || !plan || !v || !xs || !pc || !grad_acc || !sq_out || !scratch || (zbits && !fold)) return FSLD_EINVAL;
     SortedArgs b;
-    if (!make_planned(b, plan, M, n_mask, B, k, recs, v, xs, pc, grad_acc, scratch, scratch_bytes))
+    if (!make_planned(b, plan, M, n_mask, B, k, recs, v, xs, pc, grad_acc, scratch, scratch_bytes, ptab))
         return FSLD_EINVAL;
     b.zbits = zbits;
     b.fold = fold;
@@ -699,7 +716,7 @@ extern "C" int fsld_loss_grad_planned(int M, int mode, int n_mask, const fsld_im
 
 extern "C" int fsld_loss_grad_step_planned(int M, int mode, int n_mask, const fsld_image_rec* recs, const void* plan,
                                            int B, int k, const void* v, const void* xs, const int8_t* pc,
-                                           double scale, double lam, void* grad, double* sq_out, double* loss,
+                                           const void* ptab, double scale, double lam, void* grad, double* sq_out, double* loss,
                                            void* scratch, size_t scratch_bytes, void* norm_scratch,
                                            size_t norm_scratch_bytes, void* stream) {
     const int n_norm = 148 * 8;
@@ -708,7 +725,8 @@ extern "C" int fsld_loss_grad_step_planned(int M, int mode, int n_mask, const fs
         norm_scratch_bytes < n_norm * sizeof(double) || v == grad)
         return FSLD_EINVAL;
     SortedArgs b;
-    if (!make_planned(b, plan, M, n_mask, B, k, recs, v, xs, pc, grad, scratch, scratch_bytes)) return FSLD_EINVAL;
+    if (!make_planned(b, plan, M, n_mask, B, k, recs, v, xs, pc, grad, scratch, scratch_bytes, ptab))
+        return FSLD_EINVAL;
     const int64_t nvox = (int64_t)M * M * M;
     return status_of(launch_planned_loss_grad_step(b, nvox, scale, lam, sq_out, loss,
                                                    reinterpret_cast<double*>(norm_scratch), n_norm,
@@ -806,8 +824,8 @@ namespace {
 // staging buffer owned by the cached graph), so one captured graph per key is replayed.
 struct HostStepKey {
     int M, n_mask, B, n_slabs;
-    const void *recs, *v_host, *xs, *pc, *seg_off, *segs, *grad_host, *out_host, *v_dev, *grad_dev, *idx_dev,
-        *scratch;
+    const void *recs, *v_host, *xs, *pc, *ptab, *seg_off, *segs, *grad_host, *out_host, *v_dev, *grad_dev,
+        *idx_dev, *scratch;
     double scale, lam;
     bool operator==(const HostStepKey& o) const { return std::memcmp(this, &o, sizeof(*this)) == 0; }
 };
@@ -828,7 +846,7 @@ cudaError_t host_step_enqueue(const HostStepKey& k, HostPipe* P, const int32_t* 
     char* scr = reinterpret_cast<char*>(scratch);
     SortedArgs a = make_sorted(L, M, n_mask, B, recs, idx_dev, v_dev, k.xs, reinterpret_cast<const int8_t*>(k.pc),
                                reinterpret_cast<const int32_t*>(k.seg_off), reinterpret_cast<const int32_t*>(k.segs),
-                               grad_dev, scratch);
+                               grad_dev, scratch, k.ptab);
     a.out_scale = (float)scale;
     const int c = (M + 1) / 2, nb = L.nb;
     int first[kMaxSlabs + 1];
@@ -981,7 +999,8 @@ cudaError_t host_graph(const HostStepKey& k, HostPipe* P, HostGraph*& out) {
 }  // namespace
 
 extern "C" int fsld_loss_grad_host(int M, int mode, int n_mask, const fsld_image_rec* recs, const int32_t* idx_host,
-                                   int B, const void* v_host, const void* xs, const int8_t* pc, const int32_t* seg_off,
+                                   int B, const void* v_host, const void* xs, const int8_t* pc, const void* ptab,
+                                   const int32_t* seg_off,
                                    const int32_t* segs, double scale, double lam, void* grad_host, double* out_host,
                                    void* v_dev, void* grad_dev, int32_t* idx_dev, int n_slabs, void* scratch,
                                    size_t scratch_bytes, void* stream) {
@@ -1002,6 +1021,7 @@ extern "C" int fsld_loss_grad_host(int M, int mode, int n_mask, const fsld_image
     k.v_host = v_host;
     k.xs = xs;
     k.pc = pc;
+    k.ptab = ptab;
     k.seg_off = seg_off;
     k.segs = segs;
     k.grad_host = grad_host;

@@ -56,7 +56,8 @@ class SliceEngine:
     """One dataset resident on one GPU (see module docstring)."""
 
     def __init__(self, M: int, mode: str, mask: np.ndarray, recs: np.ndarray, x=None,
-                 deterministic: bool = False, device=None, tile_path: bool = False, layout: str | None = None):
+                 deterministic: bool = False, device=None, tile_path: bool = False, layout: str | None = None,
+                 tables: bool = True):
         if mode not in ("nn", "tri"):
             raise ValueError("mode must be one of ('nn', 'tri')")
         self.dev = device or require_device()
@@ -79,7 +80,9 @@ class SliceEngine:
         if layout not in ("sorted", "mask"):
             raise ValueError("layout must be 'sorted' or 'mask'")
         self.layout = layout
-        self.pc = self.seg_off = self.segs = None
+        self.pc = self.seg_off = self.segs = self.ptab = None
+        # per-pixel tables (f, trilinear footprint; 24 B per pixel) of the sorted layout: the table-driven brick kernel
+        self.use_tables = bool(tables) and not os.environ.get("FSLD_NO_TABLES")
         if layout == "sorted":
             self._build_sorted_index()
         self.x = None
@@ -104,6 +107,20 @@ class SliceEngine:
         C.check(lib.fsld_sorted_fill(self.M, self.n_mask, ctypes_ptr(self.pix), ctypes_ptr(self.recs), N, 0, 0,
                                      ctypes_ptr(self.pc), ctypes_ptr(self.seg_off), ctypes_ptr(self.segs),
                                      _stream()), "fsld_sorted_fill")
+        self._build_tables()
+
+    def _build_tables(self):
+        """fsld_sorted_tables: per-pixel f = C * phase and trilinear footprint in the sorted order
+        (24 B per pixel; rebuilt whenever the sorted order pc is rewritten)."""
+        if not self.use_tables or self.layout != "sorted":
+            self.ptab = None
+            return
+        if self.ptab is None:
+            nbytes = int(C.load().fsld_sorted_tables_bytes(self.n_images, self.n_mask))
+            self.ptab = torch.empty(nbytes, dtype=torch.uint8, device=self.dev)  # 256-B aligned (caching allocator)
+        C.check(C.load().fsld_sorted_tables(self.M, self.n_mask, ctypes_ptr(self.recs), self.n_images,
+                                            ctypes_ptr(self.pc), ctypes_ptr(self.seg_off), ctypes_ptr(self.segs),
+                                            ctypes_ptr(self.ptab), _stream()), "fsld_sorted_tables")
 
     def _sort_images(self, xd: torch.Tensor) -> torch.Tensor:
         """Mask-order images -> brick-sorted order (same permutation as pc; order within a segment may differ
@@ -113,6 +130,7 @@ class SliceEngine:
         C.check(lib.fsld_sorted_fill(self.M, self.n_mask, ctypes_ptr(self.pix), ctypes_ptr(self.recs),
                                      self.n_images, ctypes_ptr(xd), ctypes_ptr(xs), ctypes_ptr(self.pc),
                                      ctypes_ptr(self.seg_off), ctypes_ptr(self.segs), _stream()), "fsld_sorted_fill")
+        self._build_tables()  # pc was rewritten (order within a segment may differ between builds)
         return xs
 
     def x_masked(self) -> torch.Tensor:
@@ -220,8 +238,9 @@ class SliceEngine:
         if self.layout == "sorted":
             C.check(lib.fsld_loss_grad_sorted(self.M, self.mode_id, self.n_mask, ctypes_ptr(self.recs),
                                               ctypes_ptr(idx), B, ctypes_ptr(v), ctypes_ptr(self.x),
-                                              ctypes_ptr(self.pc), ctypes_ptr(self.seg_off), ctypes_ptr(self.segs),
-                                              ctypes_ptr(acc), ctypes_ptr(sq), self.flags, ctypes_ptr(fx),
+                                              ctypes_ptr(self.pc), ctypes_ptr(self.ptab), ctypes_ptr(self.seg_off),
+                                              ctypes_ptr(self.segs), ctypes_ptr(acc), ctypes_ptr(sq), self.flags,
+                                              ctypes_ptr(fx),
                                               ctypes_ptr(scr), scr.numel() * 8, _stream()), "fsld_loss_grad_sorted")
             return sq, acc, fx
         C.check(lib.fsld_loss_grad(self.M, self.mode_id, self.n_mask, ctypes_ptr(self.pix),
@@ -303,7 +322,8 @@ class SliceEngine:
         scr = self.scratch(plan.B)
         C.check(lib.fsld_loss_grad_planned(self.M, self.mode_id, self.n_mask, ctypes_ptr(self.recs),
                                            ctypes_ptr(plan.buf), plan.B, int(k), ctypes_ptr(v), ctypes_ptr(self.x),
-                                           ctypes_ptr(self.pc), ctypes_ptr(zbits), ctypes_ptr(acc), ctypes_ptr(fold),
+                                           ctypes_ptr(self.pc), ctypes_ptr(self.ptab), ctypes_ptr(zbits),
+                                           ctypes_ptr(acc), ctypes_ptr(fold),
                                            ctypes_ptr(sq), ctypes_ptr(scr), scr.numel() * 8, _stream()),
                 "fsld_loss_grad_planned")
         return sq
@@ -320,7 +340,8 @@ class SliceEngine:
         nscr = self._norm_scratch()
         C.check(lib.fsld_loss_grad_step_planned(self.M, self.mode_id, self.n_mask, ctypes_ptr(self.recs),
                                                 ctypes_ptr(plan.buf), plan.B, int(k), ctypes_ptr(v),
-                                                ctypes_ptr(self.x), ctypes_ptr(self.pc), float(scale), float(lam),
+                                                ctypes_ptr(self.x), ctypes_ptr(self.pc), ctypes_ptr(self.ptab),
+                                                float(scale), float(lam),
                                                 ctypes_ptr(grad), ctypes_ptr(sq), ctypes_ptr(loss), ctypes_ptr(scr),
                                                 scr.numel() * 8, ctypes_ptr(nscr), nscr.numel() * 8, _stream()),
                 "fsld_loss_grad_step_planned")
@@ -353,7 +374,8 @@ class SliceEngine:
             stage["idx"] = torch.empty(B, dtype=torch.int32, device=self.dev)
         C.check(lib.fsld_loss_grad_host(self.M, self.mode_id, self.n_mask, ctypes_ptr(self.recs),
                                         ctypes_ptr(idx_host), B, ctypes_ptr(v_host), ctypes_ptr(self.x),
-                                        ctypes_ptr(self.pc), ctypes_ptr(self.seg_off), ctypes_ptr(self.segs),
+                                        ctypes_ptr(self.pc), ctypes_ptr(self.ptab), ctypes_ptr(self.seg_off),
+                                        ctypes_ptr(self.segs),
                                         float(scale), float(lam), ctypes_ptr(grad_host), ctypes_ptr(out_host),
                                         ctypes_ptr(stage["v"]), ctypes_ptr(stage["g"]), ctypes_ptr(stage["idx"]),
                                         int(n_slabs or self.HOST_SLABS), ctypes_ptr(scr), scr.numel() * 8,
@@ -457,7 +479,8 @@ class SliceEngine:
                 nb = sub.numel()
                 scr = self.scratch(nb)
                 C.check(lib.fsld_hvp_sorted(self.M, self.mode_id, self.n_mask, ctypes_ptr(self.recs), ctypes_ptr(sub),
-                                            nb, ctypes_ptr(z), ctypes_ptr(self.pc), ctypes_ptr(self.seg_off),
+                                            nb, ctypes_ptr(z), ctypes_ptr(self.pc), ctypes_ptr(self.ptab),
+                                            ctypes_ptr(self.seg_off),
                                             ctypes_ptr(self.segs), ctypes_ptr(acc), ctypes_ptr(sq), 0,
                                             ctypes_ptr(scr), scr.numel() * 8, _stream()), "fsld_hvp_sorted")
             return acc, fx

@@ -4,7 +4,8 @@
  *
  *  1. adjointness of the slice operator: <y, P v> == <P^* y, v>  (fsld_project / fsld_backproject);
  *  2. brick-sorted fused loss+grad (fsld_sorted_count/fill + fsld_loss_grad_sorted) against the
- *     per-pixel tile kernel (fsld_loss_grad) on the same batch.
+ *     per-pixel tile kernel (fsld_loss_grad) on the same batch, on both brick kernels: the
+ *     compute path (ptab = NULL) and the table-driven one (fsld_sorted_tables).
  * Prints one line and exits 0 on success.  Built and run by tests/test_gpu_capi_c.py.
  */
 #include <cuda_runtime.h>
@@ -79,7 +80,7 @@ int main(void) {
     CK(cudaMalloc(&d_py, 8 * ni));
     CK(cudaMalloc(&d_acc, 8 * nv));
     CK(cudaMalloc(&d_acc2, 8 * nv));
-    CK(cudaMalloc(&d_sq, 2 * sizeof(double)));
+    CK(cudaMalloc(&d_sq, 3 * sizeof(double)));
     CK(cudaMemcpy(d_pix, pix, sizeof(int16_t) * 2 * n, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(d_recs, recs, sizeof(fsld_image_rec) * B, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(d_v, v, 8 * nv, cudaMemcpyHostToDevice));
@@ -120,20 +121,32 @@ int main(void) {
     CK(cudaMemset(d_acc2, 0, 8 * nv));
     CK(fsld_loss_grad(M, FSLD_MODE_TRI, n, d_pix, d_recs, NULL, B, d_v, d_y, d_acc, (double*)d_sq, 0u, NULL, d_scr,
                       scr_bytes, NULL));
-    CK(fsld_loss_grad_sorted(M, FSLD_MODE_TRI, n, d_recs, NULL, B, d_v, d_xs, d_pc, d_seg_off, d_segs, d_acc2,
+    CK(fsld_loss_grad_sorted(M, FSLD_MODE_TRI, n, d_recs, NULL, B, d_v, d_xs, d_pc, NULL, d_seg_off, d_segs, d_acc2,
                              (double*)d_sq + 1, 0u, NULL, d_scr, scr_bytes, NULL));
-    double sq[2];
+    void* d_ptab = NULL;
+    void* d_acc3 = NULL;
+    CK(cudaMalloc(&d_ptab, fsld_sorted_tables_bytes(B, n)));
+    CK(cudaMalloc(&d_acc3, 8 * nv));
+    CK(cudaMemset(d_acc3, 0, 8 * nv));
+    CK(fsld_sorted_tables(M, n, d_recs, B, d_pc, d_seg_off, d_segs, d_ptab, NULL));
+    CK(fsld_loss_grad_sorted(M, FSLD_MODE_TRI, n, d_recs, NULL, B, d_v, d_xs, d_pc, d_ptab, d_seg_off, d_segs,
+                             d_acc3, (double*)d_sq + 2, 0u, NULL, d_scr, scr_bytes, NULL));
+    double sq[3];
     float* g1 = malloc(8 * nv);
     float* g2 = malloc(8 * nv);
+    float* g3 = malloc(8 * nv);
     CK(cudaMemcpy(sq, d_sq, sizeof(sq), cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(g1, d_acc, 8 * nv, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(g2, d_acc2, 8 * nv, cudaMemcpyDeviceToHost));
-    double num = 0, den = 0;
+    CK(cudaMemcpy(g3, d_acc3, 8 * nv, cudaMemcpyDeviceToHost));
+    double num = 0, num3 = 0, den = 0;
     for (size_t i = 0; i < 2 * nv; ++i) {
         num += ((double)g1[i] - g2[i]) * ((double)g1[i] - g2[i]);
+        num3 += ((double)g1[i] - g3[i]) * ((double)g1[i] - g3[i]);
         den += (double)g1[i] * g1[i];
     }
-    const double grel = sqrt(num / den), srel = fabs(sq[0] - sq[1]) / sq[0];
+    const double grel = fmax(sqrt(num / den), sqrt(num3 / den));
+    const double srel = fmax(fabs(sq[0] - sq[1]), fabs(sq[0] - sq[2])) / sq[0];
     const int bad = fsld_loss_grad(M, 7, n, d_pix, d_recs, NULL, B, d_v, d_y, d_acc, (double*)d_sq, 0u, NULL, d_scr,
                                    scr_bytes, NULL) != FSLD_EINVAL;
     printf("capi_demo M=%d n_mask=%d B=%d segments=%d adjointness=%.3e sq_rel=%.3e grad_rel=%.3e\n", M, n, B, nseg,

@@ -184,6 +184,6 @@ def test_plan_entry_points_reject_bad_arguments_without_gpu():
     assert lib.fsld_plan_bytes(128, 12645, 512, 0, 10 ** 6) == 0
     assert lib.fsld_plan_build(128, 12645, 1, 1, 4, 8, 1, 1, 100, 1, 16, 0) == C.FSLD_EINVAL  # plan too small
     # a plan pointer that was never built on this process
-    assert lib.fsld_loss_grad_planned(128, C.MODE_TRI, 12645, 1, 12345, 8, 0, 1, 1, 1, 0, 1, 0, 1, 1, 1 << 30,
+    assert lib.fsld_loss_grad_planned(128, C.MODE_TRI, 12645, 1, 12345, 8, 0, 1, 1, 1, 0, 0, 1, 0, 1, 1, 1 << 30,
                                       0) == C.FSLD_EINVAL
     assert lib.fsld_proj_energy_planned(128, C.MODE_TRI, 12645, 1, 12345, 8, 0, 1, 1, 1, 1, 1 << 30, 0) == C.FSLD_EINVAL

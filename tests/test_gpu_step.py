@@ -307,14 +307,14 @@ def test_brick_hessian_product_matches_tile_and_oracle(M, N, nb):
     scr = brick.scratch(nb)
     from paper_2311_16100_b200.engine import ctypes_ptr, _stream
     C.check(C.load().fsld_hvp_sorted(M, brick.mode_id, brick.n_mask, ctypes_ptr(brick.recs), ctypes_ptr(idx), nb,
-                                     ctypes_ptr(z), ctypes_ptr(brick.pc), ctypes_ptr(brick.seg_off),
+                                     ctypes_ptr(z), ctypes_ptr(brick.pc), ctypes_ptr(brick.ptab), ctypes_ptr(brick.seg_off),
                                      ctypes_ptr(brick.segs), ctypes_ptr(acc), ctypes_ptr(sq), 0, ctypes_ptr(scr),
                                      scr.numel() * 8, _stream()), "fsld_hvp_sorted")
     en = brick.proj_energy(z, batch)
     assert abs(float(sq) - float(en)) / float(en) < 1e-5
     assert rel(acc.cpu().numpy(), hz) < 1e-5
     assert C.load().fsld_hvp_sorted(M, brick.mode_id, brick.n_mask, ctypes_ptr(brick.recs), ctypes_ptr(idx), nb,
-                                    ctypes_ptr(z), ctypes_ptr(brick.pc), ctypes_ptr(brick.seg_off),
+                                    ctypes_ptr(z), ctypes_ptr(brick.pc), ctypes_ptr(brick.ptab), ctypes_ptr(brick.seg_off),
                                     ctypes_ptr(brick.segs), ctypes_ptr(acc), None, 0, ctypes_ptr(scr),
                                     scr.numel() * 8, _stream()) == C.FSLD_EINVAL
 

@@ -28,7 +28,7 @@ for flags, name in ((0, "brick"), (C.TILE_PATH, "tile")):
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
         st = lib.fsld_loss_grad_sorted(M, 1, eng.n_mask, ctypes_ptr(eng.recs), ctypes_ptr(idx), B, ctypes_ptr(v),
-                                       ctypes_ptr(eng.x), ctypes_ptr(eng.pc), ctypes_ptr(eng.seg_off),
+                                       ctypes_ptr(eng.x), ctypes_ptr(eng.pc), ctypes_ptr(eng.ptab), ctypes_ptr(eng.seg_off),
                                        ctypes_ptr(eng.segs), ctypes_ptr(acc), ctypes_ptr(sq), flags, 0,
                                        ctypes_ptr(scr), scr.numel() * 8, _stream())
         e1.record()
