@@ -15,17 +15,19 @@
 #pragma once
 
 #ifndef FSLD_RB3
-#define FSLD_RB3 1280
+#define FSLD_RB3 1024
 #endif
 constexpr int RB3 = FSLD_RB3;
+#ifndef FSLD_V3_MINB
+#define FSLD_V3_MINB 5
+#endif
 constexpr int BK3 = BC * kSegMax;  // pixels per work item (<= BC segments of <= kSegMax pixels)
 
 struct BrickSmem3 {
     float2 vb[BH3];         // v brick + halo
     int accr[BH3];          // fixed-point adjoint accumulator (re)
     int acci[BH3];          // (im)
-    float2 bval[RB3];       // pass 1 -> 2: conj(f) r
-    float4 bgeo[RB3];       // pass 1 -> 2: (wx, wy, wz, l0)
+    uint4 brec[RB3];        // pass 1 -> 2: conj(f) r (2 x fp32) + the packed footprint (geo_pack)
     unsigned char bk[BK3];  // item pixel -> segment
     PairRec prec[BC];       // the item's pair records (gofs, count)
     long long sg[BC];       // segment start rebased to the item's flat pixel index: gofs - pref
@@ -35,6 +37,18 @@ struct BrickSmem3 {
     int wtot[BC / 32];
     double red[BW];
 };
+
+// The footprint in 8 bytes for the pass-1 -> pass-2 buffer: corner index (10 bits) and the three
+// weights as 18-bit fixed point (round to nearest; |error| <= 2^-19 on the adjoint's weights).
+__device__ __forceinline__ uint32_t q18(float w) {
+    const uint32_t q = (uint32_t)(__float_as_int(fmaf(w, 262144.0f, kMagic)) - kMagicBits);
+    return min(q, 262143u);
+}
+__device__ __forceinline__ uint2 geo_pack(float4 g) {
+    const uint32_t qx = q18(g.x), qy = q18(g.y), qz = q18(g.z);
+    return make_uint2((uint32_t)__float_as_int(g.w) | (qx << 10) | (qy << 28), (qy >> 4) | (qz << 14));
+}
+__device__ __forceinline__ float w18(uint32_t q) { return __int_as_float(0x3F800000u | (q << 5)) - 1.0f; }
 
 // L2 prefetch of [p, p + bytes) (TMA bulk prefetch: 16-byte granules, rounded outwards; the
 // callers' arrays carry >= 16 bytes of slack past their end).
@@ -58,9 +72,9 @@ __device__ __forceinline__ void load_pix3(const SortedArgs& a, const float2* tf,
 
 // Per work item (brick, <= BC image segments), as sorted_loss_grad_kernel; per round of RB3 pixels:
 //   pass 1: image value + PixTab, 8-corner gather from the smem brick, r = f P v - x, |r|^2,
-//           conj(f) r -> bval, the footprint -> bgeo (the next pixel's loads in flight);
+//           conj(f) r and the packed footprint -> brec (the next pixel's loads in flight);
 //   pass 2: fixed-point scatter of val * w (item scale, power of two, non-increasing).
-__global__ void __launch_bounds__(BTHREADS, 4) brick_loss_grad_kernel(SortedArgs a) {
+__global__ void __launch_bounds__(BTHREADS, FSLD_V3_MINB) brick_loss_grad_kernel(SortedArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     BrickSmem3& S = *reinterpret_cast<BrickSmem3*>(smem_raw);
     a.pairs += a.ctl[3];
@@ -183,8 +197,8 @@ __global__ void __launch_bounds__(BTHREADS, 4) brick_loss_grad_kernel(SortedArgs
                 sq = fmaf(rr.x, rr.x, fmaf(rr.y, rr.y, sq));
                 const float2 val = cmulconj(f, rr);
                 vmax = fmaxf(vmax, fmaxf(fabsf(val.x), fabsf(val.y)));
-                S.bval[e - r0] = val;
-                S.bgeo[e - r0] = cur.geo;
+                const uint2 gp = geo_pack(cur.geo);
+                S.brec[e - r0] = make_uint4(__float_as_uint(val.x), __float_as_uint(val.y), gp.x, gp.y);
             };
             // target of the load issued before computing pixel e: the thread's next pixel of this
             // round, else its first pixel of the next round
@@ -245,11 +259,13 @@ __global__ void __launch_bounds__(BTHREADS, 4) brick_loss_grad_kernel(SortedArgs
             const float sc = item_sc;
             const int rn = r1 - r0;
             for (int e = threadIdx.x; e < rn; e += BTHREADS) {
-                const float4 geo = S.bgeo[e];
-                const int l0 = __float_as_int(geo.w);
-                const float wx = geo.x, wy = geo.y, wz = geo.z;
+                const uint4 rec = S.brec[e];
+                const int l0 = (int)(rec.z & 1023u);
+                const float wx = w18((rec.z >> 10) & 262143u);
+                const float wy = w18(__funnelshift_r(rec.z, rec.w, 28) & 262143u);
+                const float wz = w18(rec.w >> 14);
                 const float ax = 1.f - wx, ay = 1.f - wy, az = 1.f - wz;
-                const float2 val = __fmul2_rn(S.bval[e], make_float2(sc, sc));
+                const float2 val = __fmul2_rn(make_float2(__uint_as_float(rec.x), __uint_as_float(rec.y)), make_float2(sc, sc));
                 const float zy00 = az * ay, zy10 = az * wy, zy01 = wz * ay, zy11 = wz * wy;
                 const float w8[8] = {zy00 * ax, zy00 * wx, zy10 * ax, zy10 * wx, zy01 * ax, zy01 * wx, zy11 * ax, zy11 * wx};
                 const int off8[8] = {0, 1, BH, BH + 1, BH * BH, BH * BH + 1, BH * BH + BH, BH * BH + BH + 1};
