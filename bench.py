@@ -234,6 +234,11 @@ def cpu_model():
     return "unknown"
 
 
+def op_n_mask(op):
+    """n_mask of a reference / oracle operator."""
+    return op.n_mask if hasattr(op, "n_mask") else op.x.shape[1]
+
+
 def run_reference(args):
     """--impl reference: the reference's own CPU path (its numba kernels, installed in baseline/_ref,
     all host threads) on this config; the C oracle port when the install is unavailable."""
@@ -271,8 +276,8 @@ def run_reference(args):
         "value": val, "unit": "images/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": per * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded generators of BASELINE cfg; SURVEY.md 8d)",
-        "config": {"workload": cfg.name, "M": cfg.M, "batch_per_step": B, "n_images_total": cfg.n_images,
-                   "images_sampled_from": n_sub, "mode": cfg.mode},
+        "config": bench_config(cfg, cfg.M, int(op_n_mask(op)), B, args.gpus),
+        "details": {"images_sampled_from": n_sub},
         "cpu_baseline": {"value": val, "unit": "images/s", "cores": threads, "kind": kind, "sample": sample},
         "e2e": {"value": val, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -282,6 +287,13 @@ def run_reference(args):
 # ---------------------------------------------------------------------------
 # B200 arm
 # ---------------------------------------------------------------------------
+
+def bench_config(cfg, M, n_mask, B, world):
+    """The workload identity, the same keys in both arms (B200 and --impl reference)."""
+    return {"workload": cfg.name, "M": M, "n_mask": n_mask, "mode": cfg.mode, "batch_per_gpu": B,
+            "n_images": cfg.n_images, "ctf": "physical astigmatic" if cfg.ctf else "none",
+            "shifts": bool(cfg.shifts), "parallelism": f"dp{world}"}
+
 
 def run_b200(args):
     import torch
@@ -300,13 +312,23 @@ def run_b200(args):
     if single:
         local = 0
     torch.cuda.set_device(local)
-    if world > 1:
+    # the data-parallel step (ball gather, packed all-reduce, scatter); FSLD_BENCH_FORCE_DP=1 runs it
+    # on a one-rank NCCL group (functional check of the captured collective on a 1-GPU box)
+    dp = world > 1 or os.environ.get("FSLD_BENCH_FORCE_DP") == "1"
+    if dp and world == 1:  # a one-rank group: rendezvous defaults
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29531")
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", "1")
+    if dp:
         if single:
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = synth.CONFIGS[args.config]
-    wl = synth.build_workload(cfg, seed=0, n_images=args.images or None)
+    # images sharded across ranks (rank r holds images [r N/W, (r+1) N/W) of the N-image dataset);
+    # every rank takes a batch of B of its own images per step (weak scaling, B per GPU)
+    wl = synth.build_workload(cfg, seed=0, n_images=args.images or None, shard=(rank, world))
     # cfg1/cfg2 are full-dataset passes in BASELINE; the timed step uses 1024-image batches
     B = min(cfg.batch if args.config not in ("cfg1", "cfg2") else 1024, wl.engine.n_images)
     eng = wl.engine
@@ -314,7 +336,7 @@ def run_b200(args):
     lib = C.load()
     dev = eng.dev
     lam = args.lam
-    n_total = eng.n_images * world
+    n_total = wl.n_total
     scale = n_total / (B * world)
 
     v = torch.from_numpy((wl.v_true * 0.9).astype(np.complex64)).to(dev)
@@ -337,7 +359,7 @@ def run_b200(args):
     stream = _stream()
     flags = C.TILE_PATH if os.environ.get("FSLD_TILE_PATH") else 0
     # loss_grad: count + scan + fill + brick kernel + reduce (5 kernels, + cnt memset); fused epilogue (2)
-    launches_per_step = (7 if eng.brick_path and not flags else 4) + (2 if world > 1 else 0)
+    launches_per_step = (7 if eng.brick_path and not flags else 4) + (2 if dp else 0)
 
     loss = torch.empty(1, dtype=torch.float64, device=dev)
 
@@ -356,7 +378,7 @@ def run_b200(args):
         return finish_step(stream)
 
     def finish_step(stream):
-        if world > 1:  # one packed all-reduce: [grad accumulator on the touched ball | loss hi, lo]
+        if dp:  # one packed all-reduce: [grad accumulator on the touched ball | loss hi, lo]
             C.check(lib.fsld_ball_gather(nball, ctypes_ptr(ball), ctypes_ptr(acc), ctypes_ptr(packed), 8, stream),
                     "ball_gather")
             s32 = sq.float()
@@ -390,10 +412,10 @@ def run_b200(args):
         t_plan = p0.elapsed_time(p1)
         # world 1: grad init + brick kernel + finalize (fused step); N > 1: brick kernel + reduce +
         # ball gather / scatter + epilogue (2)
-        launches_per_step = 3 if world == 1 else 6
+        launches_per_step = 3 if not dp else 6
 
     def planned_step(plan, k, ev_k0=None, ev_k1=None, fused=False):
-        if fused and world == 1:  # the whole step in one call: grad = lam v, brick pass adds s * sum, finalize
+        if fused and not dp:  # the whole step in one call: grad = lam v, brick pass adds s * sum, finalize
             eng.loss_grad_step_planned(v, plan, k, scale, lam, grad, sq=sq, loss=loss)
             return loss
         stream = _stream()
@@ -424,17 +446,26 @@ def run_b200(args):
             step(batches[args.warmup + i], *kev[i])
     torch.cuda.synchronize()
     kern_ms = [a_.elapsed_time(b_) for a_, b_ in kev]
-    # the timed step runs as one CUDA graph replay (N=1; under NCCL the collective stays eager)
+    # the timed step runs as one CUDA graph replay; for N > 1 over NCCL the graph holds the whole
+    # step -- brick pass, ball gather, the packed all-reduce, ball scatter, epilogue (the gloo
+    # exchange of the single-device functional check cannot be captured and stays eager)
     idx_static = torch.empty(B, dtype=torch.int32, device=dev)
     graphs = None
-    if world == 1 and not os.environ.get("FSLD_NO_GRAPH"):
+    graph_note = "eager"
+    if not (dp and single) and not os.environ.get("FSLD_NO_GRAPH"):
         graphs = []
         if use_plan:  # one graph per planned batch (the batch index is a kernel argument)
-            for i in range(args.steps):
-                g = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(g):
-                    planned_step(plan_t, i, fused=True)
-                graphs.append(g)
+            try:
+                for i in range(args.steps):
+                    g = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(g):
+                        planned_step(plan_t, i, fused=True)
+                    graphs.append(g)
+                graph_note = "CUDA graph replay"
+            except Exception as exc:  # (a collective that refuses capture: fall back to eager steps)
+                graphs = None
+                graph_note = f"eager (graph capture failed: {type(exc).__name__})"
+                torch.cuda.synchronize()
         else:
             idx_static.copy_(batches[0])
             step(idx_static)
@@ -443,6 +474,7 @@ def run_b200(args):
             with torch.cuda.graph(g):
                 step(idx_static)
             graphs = [g] * args.steps
+            graph_note = "CUDA graph replay"
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -485,10 +517,11 @@ def run_b200(args):
     hbm, src = peaks()
     abytes = algorithmic_bytes(M, n, B)
     achieved = abytes / (t_kern * 1e-3) / 1e9
+    kname = "brick_loss_grad_kernel" if eng.ptab is not None else "sorted_loss_grad_kernel"
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
-        traffic = json.load(open(tp)).get(cfg.name)
+        traffic = json.load(open(tp)).get(f"{cfg.name}/{kname}")
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(cfg, B, lam)
@@ -518,21 +551,29 @@ def run_b200(args):
             "metric": "image-slices/sec (fused project+CTF+adjoint, loss+grad)",
             "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": t_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "c64/f32 (fp64 coords, CTF phase)", "data": "synthetic (seeded generators of BASELINE cfg; SURVEY.md 8d)",
-            "config": {"workload": cfg.name, "M": M, "n_mask": n, "batch_per_gpu": B,
-                       "n_images_per_gpu": eng.n_images, "mode": cfg.mode,
-                       "ctf": "physical astigmatic" if cfg.ctf else "none", "shifts": bool(cfg.shifts),
-                       "parallelism": f"dp{world}", "l2": "flushed between timed steps (512 MB write)",
-                       "allreduce_bytes": (8 * nball + 8) if world > 1 else 0,
-                       "step": ("CUDA graph replay" if world == 1 and not os.environ.get("FSLD_NO_GRAPH") else "eager")
-                       + (" of fsld_loss_grad_step_planned (grad = lam v, the brick pass adds scale * its sums into "
-                          "grad, loss finalize)" if use_plan and world == 1 else ""),
-                       "binning": (f"plan of the {args.steps} timed batches (fsld_plan_build), built inside the "
-                                   f"measurement: {t_plan:.4f} ms, added as {t_plan / args.steps:.4f} ms per step")
-                       if use_plan else "per step (count -> scan -> fill kernels)"},
+            "dtype": "f32",
+            "data": "synthetic (seeded generators of BASELINE cfg; SURVEY.md 8d)",
+            "config": bench_config(cfg, M, n, B, world),
+            "details": {
+                "arithmetic": ("complex64 images / volume / gradient, fp32 gather and residual; per-pixel CTF*phase and "
+                               "trilinear footprint evaluated once in fp64 (dataset tables, stored fp32); int32 "
+                               "fixed-point shared-memory adjoint, fp32 global reduction; fp64 loss sums"
+                               if eng.ptab is not None else
+                               "complex64 images / volume / gradient, fp32 coordinates, CTF and shift phases as exact "
+                               "64-bit fixed-point turns; int32 fixed-point shared-memory adjoint; fp64 loss sums"),
+                "n_images_per_gpu": eng.n_images, "l2": "flushed between timed steps (512 MB write)",
+                "allreduce_bytes": (8 * nball + 8) if dp else 0,
+                "collectives_per_step": 1 if dp else 0,
+                "step": graph_note + (" of fsld_loss_grad_step_planned (grad = lam v, the brick pass adds scale * its "
+                                      "sums into grad, loss finalize)" if use_plan and not dp else
+                                      " of brick pass + ball gather + all_reduce([grad acc | sq]) + ball scatter + "
+                                      "epilogue" if dp else ""),
+                "binning": (f"plan of the {args.steps} timed batches (fsld_plan_build), built inside the "
+                            f"measurement: {t_plan:.4f} ms, added as {t_plan / args.steps:.4f} ms per step")
+                if use_plan else "per step (count -> scan -> fill kernels)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic, "peak_source": src,
-                         "kernel": ("fsld_loss_grad_planned: sorted_loss_grad_kernel + loss reduce (+ the plan's binning / K)" if use_plan else ("fsld_loss_grad_sorted: bin count/scan/fill + sorted_loss_grad_kernel + loss reduce" if eng.brick_path else f"fsld slice_kernel<{cfg.mode.upper()},LOSS_GRAD> (tile path)")),
+                         "kernel": (f"fsld_loss_grad_planned: {kname} + loss reduce (+ the plan's binning / K)" if use_plan else ("fsld_loss_grad_sorted: bin count/scan/fill + sorted_loss_grad_kernel + loss reduce" if eng.brick_path else f"fsld slice_kernel<{cfg.mode.upper()},LOSS_GRAD> (tile path)")),
                          "kernel_ms": t_kern, "algorithmic_bytes_per_launch": abytes},
             "gpu_launches": launches_per_step * args.steps + (5 if use_plan else 0),  # + plan build (2 memsets, 3 kernels)
             "clocks": clk.summary(),
@@ -550,7 +591,7 @@ def run_b200(args):
         if sweep is not None:
             line["hutchinson_sweep"] = sweep
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dp:
         dist.destroy_process_group()
 
 
@@ -794,8 +835,30 @@ def cpu_baseline(cfg, B, lam):
                       f"(fp64, OpenMP {threads} threads, {cpu_model()})"}
 
 
+def self_launch(args) -> int | None:
+    """`python bench.py --gpus N` without a torchrun environment: re-run this script under
+    torch.distributed.run with N local ranks (one per GPU, NCCL over NVLink), 127.0.0.1 rendezvous.
+    Returns the launcher's exit code, or None when this process is already a rank (or N == 1)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    # NCCL's communicator init lines (one per rank) stay visible on stderr
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd, env=env).returncode
+
+
 def main():
     args = parse()
+    rc = self_launch(args)
+    if rc is not None:
+        sys.exit(rc)
     if args.impl == "reference":
         run_reference(args)
     elif args.config == "cfg5":

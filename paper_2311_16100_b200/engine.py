@@ -115,8 +115,12 @@ class SliceEngine:
         if not self.use_tables or self.layout != "sorted":
             self.ptab = None
             return
+        nbytes = int(C.load().fsld_sorted_tables_bytes(self.n_images, self.n_mask))
         if self.ptab is None:
-            nbytes = int(C.load().fsld_sorted_tables_bytes(self.n_images, self.n_mask))
+            free, _ = torch.cuda.mem_get_info(self.dev)
+            if nbytes > free // 2:  # large datasets (e.g. cfg4's 200k images) keep the compute path
+                self.use_tables = False
+                return
             self.ptab = torch.empty(nbytes, dtype=torch.uint8, device=self.dev)  # 256-B aligned (caching allocator)
         C.check(C.load().fsld_sorted_tables(self.M, self.n_mask, ctypes_ptr(self.recs), self.n_images,
                                             ctypes_ptr(self.pc), ctypes_ptr(self.seg_off), ctypes_ptr(self.segs),

@@ -111,18 +111,25 @@ class Workload:
     ctfs: list | None
     engine: SliceEngine         # device-resident dataset (x filled)
     sigma: float
+    n_total: int = 0            # images of the whole (unsharded) dataset
 
 
 def build_workload(cfg: Config, seed: int = 0, n_images: int | None = None, deterministic: bool = False,
-                   chunk: int = 4096) -> Workload:
-    """Generate the config's dataset directly in HBM with the product projection kernel."""
+                   chunk: int = 4096, shard: tuple[int, int] = (0, 1)) -> Workload:
+    """Generate the config's dataset directly in HBM with the product projection kernel.
+
+    shard=(r, W): only images [r N/W, (r+1) N/W) of the N-image dataset (same poses / shifts /
+    CTFs as the unsharded one; the noise stream is per shard)."""
     M = cfg.M
-    N = n_images or cfg.n_images
+    N_all = n_images or cfg.n_images
+    r, W = shard
+    lo, hi = (r * N_all) // W, ((r + 1) * N_all) // W
     mask = disk_mask(M, M // 2 - 1)
     v = gaussian_blob_volume(M, seed)
-    quats = haar_quaternions(N, seed + 1)
-    shifts = normal_shifts(N, seed + 2) if cfg.shifts else None
-    ctfs = physical_ctfs(N, seed + 3) if cfg.ctf else None
+    quats = haar_quaternions(N_all, seed + 1)[lo:hi]
+    shifts = normal_shifts(N_all, seed + 2)[lo:hi] if cfg.shifts else None
+    ctfs = physical_ctfs(N_all, seed + 3)[lo:hi] if cfg.ctf else None
+    N = hi - lo
     recs = records_for(M, quats, shifts, ctfs)
     eng = SliceEngine(M, cfg.mode, mask, recs, None, deterministic=deterministic)
     vd = torch.from_numpy(v.astype(np.complex64)).to(eng.dev)
@@ -138,10 +145,10 @@ def build_workload(cfg: Config, seed: int = 0, n_images: int | None = None, dete
         power += float(torch.view_as_real(x[lo:lo + idx.numel()]).pow(2).sum().item())
     sigma = float(np.sqrt(power / (N * mask.size) / cfg.snr))
     g = torch.Generator(device=eng.dev)
-    g.manual_seed(seed + 100)
+    g.manual_seed(seed + 100 + 7919 * r)
     for lo in range(0, N, chunk):
         hi = min(lo + chunk, N)
         nz = torch.randn((hi - lo, mask.size, 2), generator=g, device=eng.dev, dtype=torch.float32)
         x[lo:hi] += torch.view_as_complex(nz * (sigma / np.sqrt(2.0)))
     eng.set_images(x, sorted_order=True)
-    return Workload(cfg, M, mask, v, quats, shifts, ctfs, eng, sigma)
+    return Workload(cfg, M, mask, v, quats, shifts, ctfs, eng, sigma, N_all)
