@@ -464,6 +464,20 @@ int fsld_proj_energy_planned(int M, int mode, int n_mask, const fsld_image_rec* 
                              void* stream);
 
 /*
+ * Per-epoch metric and ingest on the device.
+ * fsld_fsc: Fourier shell correlation of complex64 volumes u, v (metrics.py:38-63):
+ *   out[r] = sum_{shell r} Re(u conj(v)),  out[R+1+r] = sum |u|^2,  out[2(R+1)+r] = sum |v|^2
+ *   for r = 0..max_radius (rounded |k|), fp64; the caller forms num / sqrt(pu pv).
+ *   scratch: fsld_fsc_scratch_bytes(M, max_radius) (per-CTA partial rows, added in a fixed order).
+ * fsld_mask_images: x[i, p] = (complex64) images[i, mask[p]] for N full M^2 complex128 images
+ *   (the FSD1 payload, io.py:91-125) -> the compact masked rows of the dataset (forward.py:527).
+ */
+size_t fsld_fsc_scratch_bytes(int M, int max_radius);
+int fsld_fsc(int M, int max_radius, const void* u, const void* v, double* out, void* scratch, size_t scratch_bytes,
+             void* stream);
+int fsld_mask_images(int M, int n_mask, const int32_t* mask, int N, const void* images, void* x, void* stream);
+
+/*
  * Touched-ball compaction for the data-parallel all-reduce: a scatter can only reach
  * voxels within radius R + 1/2 + sqrt(3) of the origin (mask radius R; Appendix A item 7), ~54 %
  * of the cube at M=128, so ranks all-reduce the compacted vector.  idx: (n,) int32 voxel indices

@@ -89,6 +89,9 @@ SIGNATURES = {
     "fsld_sorted_fill": (I, [I, I, P, P, I, P, P, P, P, P, P]),
     "fsld_sorted_tables": (I, [I, I, P, I, P, P, P, P, P]),
     "fsld_sorted_tables_bytes": (SZ, [I, I]),
+    "fsld_fsc_scratch_bytes": (SZ, [I, I]),
+    "fsld_fsc": (I, [I, I, P, P, P, P, SZ, P]),
+    "fsld_mask_images": (I, [I, I, P, I, P, P, P]),
     "fsld_loss_grad_sorted": (I, [I, I, I, P, P, I, P, P, P, P, P, P, P, P, U, P, P, SZ, P]),
     "fsld_loss_sorted": (I, [I, I, I, P, P, I, P, P, P, P, P, SZ, P]),
     "fsld_loss_grad_hutch_sorted": (I, [I, I, I, P, P, I, P, P, P, P, P, P, P, P, P, U, P, SZ, P]),

@@ -592,6 +592,27 @@ extern "C" int fsld_proj_energy_sorted(int M, int mode, int n_mask, const fsld_i
     return status_of(launch_sorted_energy(b, out, !reuse, reinterpret_cast<cudaStream_t>(stream)));
 }
 
+// ---------------------------------------------------------------- metrics and ingest
+
+extern "C" size_t fsld_fsc_scratch_bytes(int M, int max_radius) {
+    if (M < 2 || max_radius < 0) return 0;
+    return sizeof(double) * (size_t)fsc_grid() * 3 * (max_radius + 1);
+}
+
+extern "C" int fsld_fsc(int M, int max_radius, const void* u, const void* v, double* out, void* scratch,
+                        size_t scratch_bytes, void* stream) {
+    if (M < 2 || M > 1024 || max_radius < 0 || max_radius > M || !u || !v || !out || !scratch) return FSLD_EINVAL;
+    if (scratch_bytes < fsld_fsc_scratch_bytes(M, max_radius)) return FSLD_EINVAL;
+    return status_of(launch_fsc(M, max_radius, reinterpret_cast<const float2*>(u), reinterpret_cast<const float2*>(v),
+                                reinterpret_cast<double*>(scratch), out, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+extern "C" int fsld_mask_images(int M, int n_mask, const int32_t* mask, int N, const void* images, void* x,
+                                void* stream) {
+    if (M < 2 || n_mask < 1 || n_mask > M * M || N < 0 || !mask || (N > 0 && (!images || !x))) return FSLD_EINVAL;
+    return status_of(launch_mask_images(M, n_mask, mask, N, images, x, reinterpret_cast<cudaStream_t>(stream)));
+}
+
 extern "C" int fsld_apply_step(int64_t nvox, void* v, const void* dir, const fsld_armijo_state* st, void* stream) {
     if (nvox < 1 || !v || !dir || !st) return FSLD_EINVAL;
     if ((reinterpret_cast<uintptr_t>(v) | reinterpret_cast<uintptr_t>(dir)) & 15) return FSLD_EINVAL;

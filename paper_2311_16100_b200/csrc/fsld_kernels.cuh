@@ -198,6 +198,10 @@ cudaError_t launch_grad_finalize(int64_t nvox, const void* acc, bool det, const 
                                  const float2* v, double scale, double lam, float2* out, cudaStream_t s);
 cudaError_t launch_real_finalize(int64_t nvox, const void* acc, bool det, const double* fx, double scale,
                                  double add, float* out, cudaStream_t s);
+int fsc_grid();
+cudaError_t launch_fsc(int M, int R, const float2* u, const float2* v, double* part, double* out, cudaStream_t s);
+cudaError_t launch_mask_images(int M, int n_mask, const int32_t* mask, int N, const void* in, void* out,
+                               cudaStream_t s);
 cudaError_t launch_norm2(int64_t n, const float2* v, double* out, double* part, int nparts, cudaStream_t s);
 cudaError_t launch_grad_epilogue(int64_t nvox, float2* acc, const float2* v, double scale, double lam, float2* grad,
                                  const double* sq, double* loss, double* norm2, double* part, int nparts,

@@ -30,8 +30,8 @@ PASS_CHUNK = 1024  # forward.py:39 (kept for API parity; the GPU path needs no c
 
 __all__ = [
     "MODES", "Pose", "CtfParams", "PhysicalCtf", "FourierVolume", "ImageStack", "quat_to_matrix",
-    "sample_uniform_poses", "ctf_eval", "ctf_coefficients", "Projector", "DatasetOperator",
-    "project", "backproject",
+    "sample_uniform_poses", "sample_preferred_poses", "ctf_eval", "ctf_coefficients", "Projector", "DatasetOperator",
+    "project", "backproject", "synthesize_dataset", "gaussian_blob_phantom",
 ]
 
 
@@ -208,6 +208,48 @@ def sample_uniform_poses(n: int, shift_bound: float, seed: int) -> list:
     return [Pose(q=qs[i], t=ts[i]) for i in range(n)]
 
 
+def _qmul(a, b) -> np.ndarray:
+    """Hamilton product of (w, x, y, z) quaternions."""
+    return np.array([a[0] * b[0] - a[1] * b[1] - a[2] * b[2] - a[3] * b[3],
+                     a[0] * b[1] + a[1] * b[0] + a[2] * b[3] - a[3] * b[2],
+                     a[0] * b[2] - a[1] * b[3] + a[2] * b[0] + a[3] * b[1],
+                     a[0] * b[3] + a[1] * b[2] - a[2] * b[1] + a[3] * b[0]])
+
+
+def sample_preferred_poses(n: int, shift_bound: float, seed: int, concentration: float) -> list:
+    """Poses whose slice normals cluster around +z (forward.py:209-258): direction
+    normalize(concentration z + N(0, I)), uniform in-plane spin, uniform shifts; concentration 0
+    is the uniform sampler.  The pose quaternion maps z to the direction under R^T."""
+    if concentration == 0:
+        return sample_uniform_poses(n, shift_bound, seed)
+    if n < 1:
+        raise ValueError("need n >= 1 poses")
+    if shift_bound < 0 or concentration < 0:
+        raise ValueError("shift_bound and concentration must be non-negative")
+    rng = np.random.default_rng(seed)
+    dirs = rng.standard_normal((n, 3))
+    dirs[:, 2] += concentration
+    dirs /= np.linalg.norm(dirs, axis=1, keepdims=True)
+    psis = rng.uniform(0.0, 2.0 * np.pi, n)
+    ts = rng.uniform(-shift_bound, shift_bound, size=(n, 2)) if shift_bound > 0 else np.zeros((n, 2))
+    out = []
+    for d, psi, t in zip(dirs, psis, ts):
+        cz = float(d[2])
+        if cz > 1.0 - 1e-12:
+            qa = np.array([1.0, 0.0, 0.0, 0.0])
+        elif cz < -1.0 + 1e-12:
+            qa = np.array([0.0, 1.0, 0.0, 0.0])
+        else:  # rotation about z x d by the angle between them
+            ax = np.array([-d[1], d[0], 0.0])
+            ax /= np.linalg.norm(ax)
+            h = 0.5 * np.arccos(cz)
+            qa = np.concatenate([[np.cos(h)], np.sin(h) * ax])
+        q = _qmul(qa, np.array([np.cos(0.5 * psi), 0.0, 0.0, np.sin(0.5 * psi)]))
+        q[1:] = -q[1:]
+        out.append(Pose(q=q / np.linalg.norm(q), t=t))
+    return out
+
+
 # ---------------------------------------------------------------------------
 # numpy <-> device helpers
 # ---------------------------------------------------------------------------
@@ -286,7 +328,72 @@ class DatasetOperator:
 
     @property
     def rots(self) -> np.ndarray:
-        return np.ascontiguousarray([quat_to_matrix(q) for q in self._quats])
+        """(N, 3, 3) rotations (forward.py:524); rows 0-1 from the records for engine-built operators."""
+        if self._quats is not None:
+            return np.ascontiguousarray([quat_to_matrix(q) for q in self._quats])
+        r = self._host_records()["rot"].reshape(-1, 2, 3)
+        return np.ascontiguousarray(np.concatenate([r, np.cross(r[:, 0], r[:, 1])[:, None, :]], axis=1))
+
+    # -- the reference's per-(image, pixel) tables (forward.py:523-526) -----------------------
+    # Here phase and CTF live in the 128-byte per-image records (and, on the brick path, in the
+    # dataset's per-pixel f tables); these host views are built on first access (10 GB of
+    # complex128 at cfg3, like the reference's own tables) and are read-only: the kernels never
+    # read them, so an assigned table could not take effect and is refused.
+    @property
+    def projector(self) -> "Projector":
+        if getattr(self, "_projector", None) is None:
+            self._projector = Projector(self.spec, self.mask, self.mode)
+        return self._projector
+
+    def _host_records(self) -> np.ndarray:
+        from . import _capi as C
+        return self.engine.recs.cpu().numpy().view(C.REC_DTYPE).reshape(-1)
+
+    @property
+    def phases(self) -> np.ndarray:
+        """(N, n_mask) complex128 shift phases exp(-2 pi i k.t / M) (forward.py:299-303, 525)."""
+        if getattr(self, "_phases", None) is None:
+            if self.stack is not None and getattr(self.stack, "poses", None) is not None:
+                self._phases = self.projector.phase_batch(self.stack.poses)
+            else:  # records: phase = exp(i pi (shift0 kx + shift1 ky)), shift = -2 t / M
+                sh = self._host_records()["shift"]
+                self._phases = np.exp(1j * np.pi * (sh @ self.projector.pix.T))
+        return self._phases
+
+    @phases.setter
+    def phases(self, table):
+        self._refuse("phases", table, self.phases)
+
+    @property
+    def ctf_vals(self) -> np.ndarray:
+        """(N, n_mask) float64 CTF values at the unrotated pixels (forward.py:305-312, 526)."""
+        if getattr(self, "_ctf_vals", None) is None:
+            if self.stack is not None and getattr(self.stack, "poses", None) is not None:
+                self._ctf_vals = self.projector.ctf_batch(self.stack.ctfs, self.n_images)
+            else:  # records: C = -(wsin sin g + wcos cos g) exp(-env k^2) where the CTF flag is set
+                from . import _capi as C
+                r = self._host_records()
+                kx, ky = self.projector.pix[:, 0], self.projector.pix[:, 1]
+                k2 = kx * kx + ky * ky
+                g = r["gamma"]
+                gam = (g[:, 0:1] * k2 + g[:, 1:2] * (kx * kx - ky * ky) + g[:, 2:3] * (2 * kx * ky)
+                       + g[:, 3:4] * k2 * k2)
+                c = -(r["wsin"][:, None].astype(np.float64) * np.sin(gam)
+                      + r["wcos"][:, None].astype(np.float64) * np.cos(gam)) * np.exp(-r["env"][:, None] * k2)
+                self._ctf_vals = np.where((r["flags"] & C.REC_CTF)[:, None] != 0, c, 1.0)
+        return self._ctf_vals
+
+    @ctf_vals.setter
+    def ctf_vals(self, table):
+        self._refuse("ctf_vals", table, self.ctf_vals)
+
+    def _refuse(self, name, table, current):
+        t = np.asarray(table)
+        if t.shape == current.shape and np.allclose(t, current, rtol=1e-12, atol=1e-12):
+            return  # (the same values: nothing to change)
+        raise ValueError(f"DatasetOperator.{name} is derived from the stack's poses / CTF models and evaluated "
+                         "inside the kernels; an arbitrary table cannot be injected (build the ImageStack with "
+                         "the CTF models, e.g. PhysicalCtf, instead)")
 
     def all_indices(self) -> np.ndarray:
         return np.arange(self.n_images)
@@ -465,3 +572,70 @@ def backproject(img, pose, ctf=None, mode: str = "tri", mask=None, spec=None):
     e = _single_stack(spec, mask, mode, pose, ctf)
     acc, fx = e.backproject(_to_dev_c64(img[np.asarray(mask)][None, :], e.dev), [0])
     return FourierVolume(_to_host_c128(e.finalize_c(acc, fx, 1.0, 0.0)), spec)
+
+
+# ---------------------------------------------------------------------------
+# synthetic data (forward.py:411-506)
+# ---------------------------------------------------------------------------
+
+def _noise_for_image(seed: int, index: int, n: int, sigma: float) -> np.ndarray:
+    """The reference's per-image noise stream (forward.py:411-424): SeedSequence(seed, (100, i)),
+    complex Gaussian with sigma / sqrt(2) per part, independent of generation order."""
+    rng = np.random.default_rng(np.random.SeedSequence(entropy=seed, spawn_key=(100, index)))
+    re_im = rng.standard_normal((2, n))
+    return (sigma / np.sqrt(2.0)) * (re_im[0] + 1j * re_im[1])
+
+
+def synthesize_dataset(v, poses, ctfs, sigma: float, mode: str = "tri", mask_radius: int | None = None,
+                       seed: int = 0, chunk: int = 4096) -> ImageStack:
+    """Noisy projections of v for the given poses / CTFs (forward.py:427-470).
+
+    The clean projections run on the GPU (the product slice kernel, mask order); the noise is the
+    reference's per-image stream, so a dataset differs from the reference's only by the fp32
+    projection (relative ~1e-7)."""
+    if sigma < 0:
+        raise ValueError("sigma must be non-negative")
+    if mode not in MODES:
+        raise ValueError(f"mode must be one of {MODES}")
+    spec = v.spec
+    if mask_radius is None:
+        mask_radius = spec.max_mask_radius
+    mask = disk_mask(spec, mask_radius)
+    n_img = len(poses)
+    if ctfs is not None and len(ctfs) != n_img:
+        raise ValueError("ctfs length must match poses")
+    quats = np.array([p.q for p in poses], dtype=np.float64)
+    shifts = np.array([p.t for p in poses], dtype=np.float64)
+    eng = SliceEngine(spec.M, mode, mask, records_for(spec.M, quats, shifts, ctfs), None, layout="mask")
+    vd = _to_dev_c64(v.values, eng.dev)
+    images = np.zeros((n_img, spec.n_pixels), dtype=np.complex128)
+    for lo in range(0, n_img, chunk):
+        hi = min(lo + chunk, n_img)
+        clean = _to_host_c128(eng.project(vd, np.arange(lo, hi)))
+        if sigma > 0:
+            for b in range(hi - lo):
+                clean[b] += _noise_for_image(seed, lo + b, mask.size, sigma)
+        images[lo:hi, mask] = clean
+    return ImageStack(spec=spec, images=images, poses=list(poses), ctfs=list(ctfs) if ctfs is not None else None,
+                      sigma=float(sigma), seed=int(seed), mask_radius=int(mask_radius), mode=mode)
+
+
+def gaussian_blob_phantom(spec, n_blobs: int = 8, seed: int = 0, widths=(0.35, 1.2)) -> FourierVolume:
+    """Anisotropic Gaussian blobs written analytically in the Fourier domain (forward.py:473-506):
+    a exp(-2 pi^2 k^T S k / M^2) exp(-2 pi i k.mu / M) per blob, S = R diag(sig^2) R^T with a Haar
+    rotation, sig ~ U[widths], mu ~ U[-M/6, M/6]^3, a ~ U[0.5, 1.5] (one seeded stream)."""
+    rng = np.random.default_rng(seed)
+    M = spec.M
+    k = spec.voxel_coords().astype(np.float64)
+    out = np.zeros(spec.n_voxels, dtype=np.complex128)
+    for _ in range(n_blobs):
+        q = rng.standard_normal(4)
+        q /= np.linalg.norm(q)
+        R = quat_to_matrix(q)
+        sig = rng.uniform(widths[0], widths[1], size=3)
+        S = (R * sig ** 2) @ R.T
+        mu = rng.uniform(-M / 6.0, M / 6.0, size=3)
+        amp = rng.uniform(0.5, 1.5)
+        quad = np.einsum("vi,ij,vj->v", k, S, k)
+        out += amp * np.exp(-2.0 * np.pi ** 2 * quad / M ** 2) * np.exp(-2j * np.pi * (k @ mu) / M)
+    return FourierVolume(out, spec)

@@ -53,6 +53,14 @@ class GridSpec:
     def voxel_coords(self) -> np.ndarray:
         return voxel_coords(self.M)
 
+    def pixel_radii(self) -> np.ndarray:
+        """|k| per pixel in linear-index order (grid.py:136-141)."""
+        return np.sqrt((pixel_coords(self.M).astype(np.float64) ** 2).sum(axis=1))
+
+    def voxel_radii(self) -> np.ndarray:
+        """|k| per voxel in linear-index order (grid.py:143-148)."""
+        return np.sqrt((voxel_coords(self.M).astype(np.float64) ** 2).sum(axis=1))
+
 
 @lru_cache(maxsize=16)
 def _pix(M: int) -> np.ndarray:
@@ -121,3 +129,59 @@ def touched_ball(M: int, mask_radius: int) -> np.ndarray:
     """
     r = np.sqrt((voxel_coords(M).astype(np.float64) ** 2).sum(axis=1))
     return np.flatnonzero(r < mask_radius + 0.5 + np.sqrt(3.0)).astype(np.int32)
+
+
+@dataclass
+class ShellTable:
+    """Shell (rounded-radius) membership and populations of one grid (grid.py:200-238).
+
+    ``shell_of_pixel`` / ``shell_of_voxel``: shell index per grid point in linear-index order, -1
+    beyond ``max_radius``; ``px_count[r]`` / ``vx_count[r]``: 2D / 3D shell populations.
+    """
+
+    spec: GridSpec
+    max_radius: int
+    px_count: np.ndarray
+    vx_count: np.ndarray
+    shell_of_pixel: np.ndarray
+    shell_of_voxel: np.ndarray
+
+    @property
+    def radii(self) -> np.ndarray:
+        return np.arange(self.max_radius + 1)
+
+    def n_masked_pixels(self) -> int:
+        return int(self.px_count.sum())
+
+    def n_masked_voxels(self) -> int:
+        return int(self.vx_count.sum())
+
+    def _check(self, r: int) -> None:
+        if not 0 <= r <= self.max_radius:
+            raise ValueError(f"radius {r} outside table range {self.max_radius}")
+
+    def shell_ratio(self, r: int) -> float:
+        """P_x(r) / P_v(r)."""
+        self._check(r)
+        if self.vx_count[r] == 0:
+            raise ValueError(f"empty 3D shell at radius {r}")
+        return float(self.px_count[r]) / float(self.vx_count[r])
+
+    def pixel_voxel_ratio(self, r: int) -> float:
+        """|disk(r)| / |ball(r)| (the condition-number bound's p(r))."""
+        self._check(r)
+        return float(self.px_count[: r + 1].sum()) / float(self.vx_count[: r + 1].sum())
+
+
+def shell_table(spec: GridSpec, mask_radius: int) -> ShellTable:
+    """ShellTable of the points with rounded radius <= mask_radius (grid.py:241-257)."""
+    if not 1 <= mask_radius <= spec.max_mask_radius:
+        raise ValueError(f"mask_radius must be in [1, {spec.max_mask_radius}] for M={spec.M}, got {mask_radius}")
+    ps = np.round(spec.pixel_radii()).astype(np.int64)
+    vs = np.round(spec.voxel_radii()).astype(np.int64)
+    sp = np.where(ps <= mask_radius, ps, -1).astype(np.int32)
+    sv = np.where(vs <= mask_radius, vs, -1).astype(np.int32)
+    return ShellTable(spec=spec, max_radius=int(mask_radius),
+                      px_count=np.bincount(sp[sp >= 0], minlength=mask_radius + 1),
+                      vx_count=np.bincount(sv[sv >= 0], minlength=mask_radius + 1),
+                      shell_of_pixel=sp, shell_of_voxel=sv)

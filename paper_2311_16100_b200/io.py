@@ -161,6 +161,16 @@ class _HeaderStack:
         return len(self.poses)
 
 
+def file_digest(path) -> str:
+    """64-bit blake2b content digest of a file as 16 hex characters (io.py:152-158)."""
+    import hashlib
+    h = hashlib.blake2b(digest_size=8)
+    with open(path, "rb") as f:
+        for chunk in iter(lambda: f.read(1 << 20), b""):
+            h.update(chunk)
+    return h.hexdigest()
+
+
 def load_operator(path, mode: str | None = None, chunk_images: int = 1024, deterministic: bool = False):
     """Stream an FSD1 file into a device-resident DatasetOperator.
 
@@ -191,7 +201,10 @@ def load_operator(path, mode: str | None = None, chunk_images: int = 1024, deter
                           deterministic=deterministic)
         dev = eng.dev
         x = torch.empty((N, mask.size), dtype=torch.complex64, device=dev)
-        mask_d = torch.from_numpy(mask).to(dev)
+        mask_d = torch.from_numpy(mask.astype(np.int32)).to(dev)
+        from . import _capi as C
+        from .engine import _stream, ctypes_ptr
+        lib = C.load()
         pin = torch.empty(chunk_images * M * M * 16, dtype=torch.uint8).pin_memory()
         for i0 in range(0, N, chunk_images):
             n = min(chunk_images, N - i0)
@@ -201,8 +214,9 @@ def load_operator(path, mode: str | None = None, chunk_images: int = 1024, deter
             if got != nbytes:
                 raise DataError(f"{path}: truncated payload")
             raw = pin[:nbytes].to(dev, non_blocking=True)
-            imgs = raw.view(torch.complex128).view(n, M * M)
-            x[i0:i0 + n] = imgs[:, mask_d].to(torch.complex64)
+            # x[i0:i0+n] = (complex64) images[:, mask] (fsld_mask_images kernel)
+            C.check(lib.fsld_mask_images(M, mask.size, ctypes_ptr(mask_d), n, ctypes_ptr(raw),
+                                         ctypes_ptr(x[i0:i0 + n]), _stream()), "fsld_mask_images")
             torch.cuda.current_stream().synchronize()  # the pinned chunk is reused
         eng.set_images(x)
         op = DatasetOperator.from_engine(eng, hstack.spec)
