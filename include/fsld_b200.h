@@ -390,9 +390,10 @@ int fsld_hutch_fold_sorted(int M, int mode, int n_mask, const fsld_image_rec* re
 
 /* ||A d||^2 = sum_b sum_p C^2 |P d|^2 over the batch on the brick-sorted layout (tri mode):
  * a gather-only pass (no images) for the closed-form line search.  *out = device double.
- * flags: 0 or FSLD_REUSE_BINS (the loss+grad call of the same step on this scratch, same recs /
- * idx pointer / B, with idx unchanged since: the binning is skipped; EINVAL if the host-side
- * record of the scratch's last binning does not match). */
+ * flags: 0 or FSLD_REUSE_BINS: reuse the work items the last sorted call on this scratch binned
+ * (the loss+grad call of the same step).  EINVAL if that call was for another recs / idx pointer /
+ * B; the rows themselves are compared on the device with the copy the binning stored, and if the
+ * caller rewrote idx in place since, the batch is binned again (never stale work items). */
 int fsld_proj_energy_sorted(int M, int mode, int n_mask, const fsld_image_rec* recs, const int32_t* idx, int B,
                             const void* d, const int8_t* pc, const int32_t* seg_off, const int32_t* segs,
                             double* out, unsigned flags, void* scratch, size_t scratch_bytes, void* stream);
@@ -453,7 +454,10 @@ int fsld_loss_grad_step_planned(int M, int mode, int n_mask, const fsld_image_re
  * lam v initialisation, its brick pass and its device->host copy of the finished gradient are
  * pipelined on two internal copy streams (forked from / joined back into `stream`), so the
  * PCIe transfers in both directions overlap each other and the kernels.  Everything is enqueued
- * on `stream`: the outputs are valid once `stream` has been synchronised. */
+ * on `stream`: the outputs are valid once `stream` has been synchronised.
+ * Host-side blocking: the step of a given call shape is one cached CUDA graph whose batch rows come
+ * from a pinned staging buffer it owns, so a call first waits (host) until the previous replay of
+ * the same shape has read its rows; calls from several host threads are serialised. */
 int fsld_loss_grad_host(int M, int mode, int n_mask, const fsld_image_rec* recs, const int32_t* idx_host, int B,
                         const void* v_host, const void* xs, const int8_t* pc, const void* ptab,
                         const int32_t* seg_off, const int32_t* segs, double scale, double lam, void* grad_host, double* out_host,

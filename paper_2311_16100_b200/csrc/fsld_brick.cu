@@ -57,6 +57,8 @@ ScratchLayout scratch_layout(int M, int n_mask, int B) {
     L.gpart = o; o = al(o + sizeof(double) * (size_t)kMaxSlabs * kSlabCtas);
     L.npart = o; o = al(o + sizeof(double) * (size_t)kMaxSlabs * 2 * kInitParts);
     L.hout = o; o = al(o + sizeof(double) * 2);
+    L.bidx = o; o = al(o + sizeof(int32_t) * (size_t)(B > 0 ? B : 1));
+    L.gate = o; o = al(o + sizeof(int));
     L.total = o;
     return L;
 }
@@ -306,8 +308,10 @@ __device__ __forceinline__ void fill_image(const SortedArgs& a, int row, int tsl
 
 template <bool FILL>
 __global__ void __launch_bounds__(128) bin_sorted_kernel(SortedArgs a) {
+    if (a.gate && *a.gate == 0) return;  // reuse: the items in scratch are this batch's already
     const int b = blockIdx.x;
     const int row = a.idx ? a.idx[b] : b;
+    if (!FILL && threadIdx.x == 0 && a.bidx) a.bidx[b] = row;  // what these work items were binned for
     if (FILL) {
         __shared__ SegRec T;
         fill_image(a, row, b, a.fill, a.off, a.pairs, T);
@@ -416,6 +420,7 @@ __device__ void scan_batch(int* cnt, int* off, int* fill, int4* items, int* ctl,
 }
 
 __global__ void __launch_bounds__(1024) brick_scan_kernel(SortedArgs a) {
+    if (a.gate && *a.gate == 0) return;
     scan_batch(a.cnt, a.off, a.fill, a.items, a.ctl, a.nbr, a.cap_items, a.cap_pairs, 0, 0);
 }
 
@@ -702,6 +707,17 @@ cudaError_t launch_planned_loss_grad_step(SortedArgs a, int64_t nvox, double sca
     return launch_loss_finalize(a.part, grid, norm_part, n_norm, scale, lam, sq_out, loss, s);
 }
 
+// FSLD_REUSE_BINS: the work items left in scratch are reused only if they were binned for this very
+// batch -- the rows are compared on the device with the copy the count pass stored (bidx); any
+// difference (or another batch size) opens the gate and the three binning kernels run again.
+__global__ void __launch_bounds__(1024) bins_check_kernel(const int32_t* __restrict__ idx, const int32_t* __restrict__ bidx,
+                                                          int B, int* gate) {
+    int diff = 0;
+    for (int b = threadIdx.x; b < B; b += blockDim.x) diff |= (idx ? idx[b] : b) != bidx[b];
+    diff = __syncthreads_or(diff);
+    if (threadIdx.x == 0) *gate = diff;
+}
+
 cudaError_t launch_sorted_energy(const SortedArgs& a, double* out, bool rebin, cudaStream_t s) {
     static GridCache cache;
     const size_t smem = sizeof(EnergySmem);
@@ -712,9 +728,13 @@ cudaError_t launch_sorted_energy(const SortedArgs& a, double* out, bool rebin, c
         bin_sorted_kernel<false><<<a.B, 128, 0, s>>>(a);
         brick_scan_kernel<<<1, 1024, 0, s>>>(a);
         bin_sorted_kernel<true><<<a.B, 128, 0, s>>>(a);
-    } else {  // the work items of the previous sorted call on this scratch: only re-arm the claim counter
-        cudaError_t e = cudaMemsetAsync(a.ctl + 1, 0, sizeof(int), s);
+    } else {  // the work items of the previous sorted call on this scratch, if its rows are these
+        cudaError_t e = cudaMemsetAsync(a.ctl + 1, 0, sizeof(int), s);  // re-arm the claim counter
         if (e != cudaSuccess) return e;
+        bins_check_kernel<<<1, 1024, 0, s>>>(a.idx, a.bidx, a.B, a.gate);
+        bin_sorted_kernel<false><<<a.B, 128, 0, s>>>(a);  // (gated: no-ops unless the rows differ)
+        brick_scan_kernel<<<1, 1024, 0, s>>>(a);
+        bin_sorted_kernel<true><<<a.B, 128, 0, s>>>(a);
     }
     sorted_energy_kernel<<<grid, BTHREADS, smem, s>>>(a);
     cudaError_t e = cudaGetLastError();

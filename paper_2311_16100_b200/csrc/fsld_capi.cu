@@ -113,6 +113,8 @@ SortedArgs make_sorted(const ScratchLayout& L, int M, int n_mask, int B, const f
     b.items = reinterpret_cast<int4*>(scr + L.items);
     b.ctl = reinterpret_cast<int*>(scr + L.ctl);
     b.part = reinterpret_cast<double*>(scr + L.part);
+    b.bidx = reinterpret_cast<int32_t*>(scr + L.bidx);
+    b.gate = nullptr;
     b.cap_pairs = L.cap_pairs;
     b.cap_items = L.cap_items;
     b.out_scale = 1.0f;
@@ -587,7 +589,8 @@ extern "C" int fsld_proj_energy_sorted(int M, int mode, int n_mask, const fsld_i
     if (scratch_bytes < L.total) return FSLD_EINVAL;
     const bool reuse = (flags & FSLD_REUSE_BINS) != 0;
     if (reuse && !bins_match(scratch, idx, recs, M, n_mask, B)) return FSLD_EINVAL;
-    const SortedArgs b = make_sorted(L, M, n_mask, B, recs, idx, d, nullptr, pc, seg_off, segs, nullptr, scratch);
+    SortedArgs b = make_sorted(L, M, n_mask, B, recs, idx, d, nullptr, pc, seg_off, segs, nullptr, scratch);
+    if (reuse) b.gate = reinterpret_cast<int*>(reinterpret_cast<char*>(scratch) + L.gate);
     if (!reuse) note_bins(scratch, idx, recs, M, n_mask, B);
     return status_of(launch_sorted_energy(b, out, !reuse, reinterpret_cast<cudaStream_t>(stream)));
 }

@@ -104,7 +104,7 @@ constexpr int kSlabCtas = 148 * 8;     // >= the persistent brick grid (CTAs per
 constexpr int kInitParts = 148 * 2;    // grad_init partial sums per contiguous volume piece
 
 struct ScratchLayout {
-    size_t hdr, cnt, off, fill, pairs, tmpl, items, ctl, part, gitems, gctl, gpart, npart, hout, total;
+    size_t hdr, cnt, off, fill, pairs, tmpl, items, ctl, part, gitems, gctl, gpart, npart, hout, bidx, gate, total;
     int nb, nbr, cap_pairs, cap_items, cap_part;
 };
 
@@ -140,6 +140,8 @@ struct SortedArgs {
     int4* items;             // (brick, first pair, n pairs, 0)
     int* ctl;
     double* part;
+    int32_t* bidx;           // the batch rows the work items in scratch were binned for (reuse check)
+    int* gate;               // non-NULL: the binning kernels run only if *gate != 0 (set by the check)
     int cap_pairs, cap_items;
     float out_scale;         // the flush adds out_scale * (sum of contributions) to acc (1 = plain accumulator)
 };

@@ -234,15 +234,25 @@ def ema_and_threshold(state, beta: float, alpha: float, thresholded: bool = True
 def threshold_alpha(stack, shells=None, lam: float = 0.0) -> float:
     """alpha = P_x(R)/P_v(R) * sum_i |C_i(R)|^2 + lam (optim.py:250-266).
 
-    Radial CTFs are evaluated at R like the reference; for the astigmatic
-    PhysicalCtf (not radial) |C_i(R)|^2 is the mean over the masked pixels of
+    ``shells`` (a ShellTable, as the reference passes) supplies P_x(R)/P_v(R) and must have
+    max_radius == the stack's mask radius (ValueError otherwise, like the reference); None builds
+    the populations from the grid.  Radial CTFs are evaluated at R like the reference; for the
+    astigmatic PhysicalCtf (not radial) |C_i(R)|^2 is the mean over the masked pixels of
     shell R (builder-defined).
     """
     M = stack.spec.M
     r = stack.mask_radius
-    px, vx = shell_counts(M, r)
-    if vx[r] == 0:
-        raise ValueError(f"empty 3D shell at radius {r}")
+    if shells is not None:
+        if shells.max_radius != r:
+            raise ValueError("shell table radius must match the stack mask radius")
+        if shells.vx_count[r] == 0:
+            raise ValueError(f"empty 3D shell at radius {r}")
+        ratio = shells.shell_ratio(r)
+    else:
+        px, vx = shell_counts(M, r)
+        if vx[r] == 0:
+            raise ValueError(f"empty 3D shell at radius {r}")
+        ratio = float(px[r]) / float(vx[r])
     if stack.ctfs is None:
         csum = float(stack.n_images)
     else:
@@ -269,13 +279,13 @@ def threshold_alpha(stack, shells=None, lam: float = 0.0) -> float:
                 row = -(ws[s] * np.sin(gam) + wc[s] * np.cos(gam)) * np.exp(-env[s] * k2)
                 for m in np.mean(row ** 2, axis=1):
                     csum += float(m)
-            return float(px[r]) / float(vx[r]) * csum + lam
+            return ratio * csum + lam
         for c in stack.ctfs:
             if isinstance(c, PhysicalCtf) or hasattr(c, "astig"):
                 csum += float(np.mean(ctf_table_row(c, ring, M) ** 2))
             else:
                 csum += ctf_eval(c, r, M // 2) ** 2
-    return float(px[r]) / float(vx[r]) * csum + lam
+    return ratio * csum + lam
 
 
 def armijo_search(v, grad, dhat, loss_fn, eta_in: float, c: float, f0=None):

@@ -68,3 +68,21 @@ def test_fsld_shim_resolves_to_this_package():
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300,
                        env=dict(os.environ, PYTHONPATH=os.path.join(ROOT, "pkg", "src")), cwd="/tmp")
     assert r.returncode == 0 and r.stdout.strip() == "ok", r.stderr[-2000:]
+
+
+@needs_ref
+def test_threshold_alpha_uses_the_shell_table_like_the_reference(ref, golden):
+    g = golden("dataset_m16_tri.npz")
+    M = int(g["M"])
+    R = M // 2 - 1
+    images = np.zeros((g["x"].shape[0], M * M), complex)
+    images[:, g["mask"]] = g["x"]
+    rstack = ref.ImageStack(ref.GridSpec(M), images, [ref.Pose(q, t) for q, t in zip(g["quats"], g["shifts"])],
+                            [ref.CtfParams(*map(float, p)) for p in g["ctf_params"]], 0.05, 4, R, "tri")
+    stack = F.ImageStack(F.GridSpec(M), images, [F.Pose(q, t) for q, t in zip(g["quats"], g["shifts"])],
+                         [F.CtfParams(*map(float, p)) for p in g["ctf_params"]], 0.05, 4, R, "tri")
+    a_ref = ref.optim.threshold_alpha(rstack, ref.shell_table(ref.GridSpec(M), R), 0.01)
+    assert abs(F.threshold_alpha(stack, F.shell_table(F.GridSpec(M), R), 0.01) - a_ref) <= 1e-14 * a_ref
+    assert abs(F.threshold_alpha(stack, None, 0.01) - a_ref) <= 1e-14 * a_ref
+    with pytest.raises(ValueError):
+        F.threshold_alpha(stack, F.shell_table(F.GridSpec(M), R - 1), 0.01)

@@ -458,3 +458,25 @@ def test_binning_plan_edge_shapes(M, N, B, K):
         sq2, acc2, _ = e.loss_grad(v, batches[k])
         assert abs(float(sq1) - float(sq2)) <= 1e-6 * abs(float(sq2))
         assert rel(acc1.cpu().numpy(), acc2.cpu().numpy()) < 1e-5
+
+
+def test_reuse_bins_rebins_when_rows_were_rewritten_in_place(golden):
+    """FSLD_REUSE_BINS is checked by content on the device: the same idx tensor rewritten in place
+    after the loss+grad call must give the new batch's energy, not the stale work items'."""
+    g = golden("dataset_m16_tri.npz")
+    op = golden_op(g)
+    e = op.engine
+    assert e.brick_path
+    rng = np.random.default_rng(3)
+    b1 = rng.permutation(e.n_images)[:24]
+    b2 = rng.permutation(e.n_images)[:24]
+    d = torch.from_numpy((g["v1"] * 0.3).astype(np.complex64)).cuda()
+    bt = e.idx_tensor(b1)
+    e.loss_grad(d, bt)
+    q_same = float(e.proj_energy(d, bt, reuse_bins=True).item())
+    assert abs(q_same - float(e.proj_energy(d, b1).item())) <= 1e-6 * q_same
+    e.loss_grad(d, bt)
+    bt.copy_(torch.from_numpy(b2.astype(np.int32)).cuda())  # same pointer, new rows
+    q_new = float(e.proj_energy(d, bt, reuse_bins=True).item())
+    q_ref = float(e.proj_energy(d, b2).item())
+    assert abs(q_new - q_ref) <= 1e-6 * q_ref
