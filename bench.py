@@ -517,7 +517,8 @@ def run_b200(args):
     hbm, src = peaks()
     abytes = algorithmic_bytes(M, n, B)
     achieved = abytes / (t_kern * 1e-3) / 1e9
-    kname = "brick_loss_grad_kernel" if eng.ptab is not None else "sorted_loss_grad_kernel"
+    kname = ("brick_loss_grad_kernel" if eng.table_path else "sorted_loss_grad_kernel" if eng.brick_path
+             else f"slice_kernel<{cfg.mode.upper()},LOSS_GRAD>")
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
@@ -558,7 +559,7 @@ def run_b200(args):
                 "arithmetic": ("complex64 images / volume / gradient, fp32 gather and residual; per-pixel CTF*phase and "
                                "trilinear footprint evaluated once in fp64 (dataset tables, stored fp32); int32 "
                                "fixed-point shared-memory adjoint, fp32 global reduction; fp64 loss sums"
-                               if eng.ptab is not None else
+                               if eng.table_path else
                                "complex64 images / volume / gradient, fp32 coordinates, CTF and shift phases as exact "
                                "64-bit fixed-point turns; int32 fixed-point shared-memory adjoint; fp64 loss sums"),
                 "n_images_per_gpu": eng.n_images, "l2": "flushed between timed steps (512 MB write)",
@@ -573,7 +574,7 @@ def run_b200(args):
                 if use_plan else "per step (count -> scan -> fill kernels)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic, "peak_source": src,
-                         "kernel": (f"fsld_loss_grad_planned: {kname} + loss reduce (+ the plan's binning / K)" if use_plan else ("fsld_loss_grad_sorted: bin count/scan/fill + sorted_loss_grad_kernel + loss reduce" if eng.brick_path else f"fsld slice_kernel<{cfg.mode.upper()},LOSS_GRAD> (tile path)")),
+                         "kernel": (f"fsld_loss_grad_planned: {kname} + loss reduce (+ the plan's binning / K)" if use_plan else (f"fsld_loss_grad_sorted: bin count/scan/fill + {kname} + loss reduce" if eng.brick_path else f"fsld {kname} (tile path)")),
                          "kernel_ms": t_kern, "algorithmic_bytes_per_launch": abytes},
             "gpu_launches": launches_per_step * args.steps + (5 if use_plan else 0),  # + plan build (2 memsets, 3 kernels)
             "clocks": clk.summary(),

@@ -55,6 +55,9 @@ extern "C" {
 /* flags */
 #define FSLD_DETERMINISTIC 1u /* accumulate in int64 fixed point: bitwise repeatable */
 #define FSLD_TILE_PATH 2u     /* force the per-pixel tile kernel (global atomics) instead of bricks */
+#define FSLD_NN_BRICK 8u      /* nn mode with dataset tables: the brick kernel instead of the per-pixel
+                                 tile kernel (one global RED per pixel is cheaper for nn at every
+                                 measured M, so the tile kernel is the default there) */
 #define FSLD_REUSE_BINS 4u    /* reuse the brick work items the previous sorted call on the same scratch
                                  built for the same (recs, idx, B): skips the per-step binning */
 
@@ -237,11 +240,14 @@ int fsld_sorted_fill(int M, int n_mask, const int16_t* pix, const fsld_image_rec
  *   the frame of its brick: weights (wx, wy, wz) as fp32 and the corner index in the 9^3 brick.
  * Passing ptab to the brick entry points below selects the table-driven brick kernel
  * (24 bytes loaded per pixel instead of evaluating geometry, CTF and phase per pixel);
- * ptab = NULL runs the compute path from pc and the records.  Rebuild after changing poses
+ * ptab = NULL runs the compute path from pc and the records.  mode FSLD_MODE_NN stores the
+ * reference's nearest-neighbour voxel (bit-exact, kernels.py:69-120) instead of the trilinear
+ * footprint: fsld_loss_grad_sorted with FSLD_NN_BRICK / fsld_hvp_sorted then run the brick kernel
+ * in nn mode (one gather, one complex shared-memory add per pixel).  Rebuild after changing poses
  * or CTFs (the images themselves are not part of the table).
  */
 size_t fsld_sorted_tables_bytes(int N, int n_mask);
-int fsld_sorted_tables(int M, int n_mask, const fsld_image_rec* recs, int N, const int8_t* pc,
+int fsld_sorted_tables(int M, int mode, int n_mask, const fsld_image_rec* recs, int N, const int8_t* pc,
                        const int32_t* seg_off, const int32_t* segs, void* ptab, void* stream);
 
 /* Fused loss + gradient over a brick-sorted dataset (optim.py:147-190 hot loop):

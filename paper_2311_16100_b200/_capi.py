@@ -22,6 +22,7 @@ MODE_NN = 0
 MODE_TRI = 1
 DETERMINISTIC = 1
 TILE_PATH = 2
+NN_BRICK = 8
 REUSE_BINS = 4
 REC_CTF = 1
 REC_SHIFT = 2
@@ -87,7 +88,7 @@ SIGNATURES = {
     "fsld_scatter_sq_tab": (I, [I, I, I, P, P, I, P, P, U, P, P]),
     "fsld_sorted_count": (I, [I, I, P, P, I, P, P]),
     "fsld_sorted_fill": (I, [I, I, P, P, I, P, P, P, P, P, P]),
-    "fsld_sorted_tables": (I, [I, I, P, I, P, P, P, P, P]),
+    "fsld_sorted_tables": (I, [I, I, I, P, I, P, P, P, P, P]),
     "fsld_sorted_tables_bytes": (SZ, [I, I]),
     "fsld_fsc_scratch_bytes": (SZ, [I, I]),
     "fsld_fsc": (I, [I, I, P, P, P, P, SZ, P]),

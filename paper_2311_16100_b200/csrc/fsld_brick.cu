@@ -216,10 +216,11 @@ cudaError_t launch_sorted_fill(int M, int n_mask, const short2* pix, const fsld_
 
 size_t sorted_tables_bytes(long long npx) { return tables_bytes(npx); }
 
-cudaError_t launch_sorted_tables(int M, int n_mask, const fsld_image_rec* recs, int N, const char2* pc,
+cudaError_t launch_sorted_tables(int M, int n_mask, int mode, const fsld_image_rec* recs, int N, const char2* pc,
                                  const int32_t* seg_off, const int2* segs, void* ptab, cudaStream_t s) {
     if (N < 1) return cudaSuccess;
-    sorted_tables_kernel<<<N, 256, 0, s>>>(M, n_mask, recs, pc, seg_off, segs, ptab, (long long)N * n_mask);
+    sorted_tables_kernel<<<N, 256, 0, s>>>(M, n_mask, mode == FSLD_MODE_NN, recs, pc, seg_off, segs, ptab,
+                                           (long long)N * n_mask);
     return cudaGetLastError();
 }
 
@@ -555,18 +556,20 @@ static cudaError_t main_grid(int& out) {
     return persistent_grid(cache, sorted_loss_grad_kernel<HUTCH>, sizeof(SortedSmemT<HUTCH>), out);
 }
 
+template <bool NN>
 static cudaError_t v3_grid(int& out) {
     static GridCache cache;
-    return persistent_grid(cache, brick_loss_grad_kernel, sizeof(BrickSmem3), out);
+    return persistent_grid(cache, brick_loss_grad_kernel<NN>, sizeof(BrickSmem3), out);
 }
 
 template <bool HUTCH>
 static cudaError_t launch_sorted_main(const SortedArgs& a, double* sq_out, cudaStream_t s, int* grid_out = nullptr) {
     int grid = 0;
     if (!HUTCH && a.ptab) {  // the table-driven kernel (per-pixel f and footprint from the dataset tables)
-        cudaError_t e0 = v3_grid(grid);
+        cudaError_t e0 = a.nn ? v3_grid<true>(grid) : v3_grid<false>(grid);
         if (e0 != cudaSuccess) return e0;
-        brick_loss_grad_kernel<<<grid, BTHREADS, sizeof(BrickSmem3), s>>>(a);
+        if (a.nn) brick_loss_grad_kernel<true><<<grid, BTHREADS, sizeof(BrickSmem3), s>>>(a);
+        else brick_loss_grad_kernel<false><<<grid, BTHREADS, sizeof(BrickSmem3), s>>>(a);
     } else {
         const size_t smem = sizeof(SortedSmemT<HUTCH>);
         cudaError_t e0 = main_grid<HUTCH>(grid);
@@ -672,7 +675,7 @@ __global__ void __launch_bounds__(1024) slab_items_kernel(const int4* __restrict
 cudaError_t prepare_host_step(int* grid_out) {
     int grid = 0, grid3 = 0;
     cudaError_t e = main_grid<false>(grid);
-    if (e == cudaSuccess) e = v3_grid(grid3);
+    if (e == cudaSuccess) e = v3_grid<false>(grid3);
     if (grid_out) *grid_out = grid > grid3 ? grid : grid3;
     return e;
 }
@@ -731,10 +734,12 @@ cudaError_t launch_sorted_energy(const SortedArgs& a, double* out, bool rebin, c
     } else {  // the work items of the previous sorted call on this scratch, if its rows are these
         cudaError_t e = cudaMemsetAsync(a.ctl + 1, 0, sizeof(int), s);  // re-arm the claim counter
         if (e != cudaSuccess) return e;
-        bins_check_kernel<<<1, 1024, 0, s>>>(a.idx, a.bidx, a.B, a.gate);
-        bin_sorted_kernel<false><<<a.B, 128, 0, s>>>(a);  // (gated: no-ops unless the rows differ)
-        brick_scan_kernel<<<1, 1024, 0, s>>>(a);
-        bin_sorted_kernel<true><<<a.B, 128, 0, s>>>(a);
+        if (a.gate) {  // (binning plans carry their own work items: nothing to check)
+            bins_check_kernel<<<1, 1024, 0, s>>>(a.idx, a.bidx, a.B, a.gate);
+            bin_sorted_kernel<false><<<a.B, 128, 0, s>>>(a);  // (gated: no-ops unless the rows differ)
+            brick_scan_kernel<<<1, 1024, 0, s>>>(a);
+            bin_sorted_kernel<true><<<a.B, 128, 0, s>>>(a);
+        }
     }
     sorted_energy_kernel<<<grid, BTHREADS, smem, s>>>(a);
     cudaError_t e = cudaGetLastError();

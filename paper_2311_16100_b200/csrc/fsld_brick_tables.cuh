@@ -45,7 +45,8 @@ __device__ __forceinline__ float geo_weight(double w) {
 }
 
 // One CTA per image, one warp per segment (lanes over its pixels).
-__global__ void __launch_bounds__(256) sorted_tables_kernel(int M, int n_mask, const fsld_image_rec* __restrict__ recs,
+__global__ void __launch_bounds__(256) sorted_tables_kernel(int M, int n_mask, int nn,
+                                                            const fsld_image_rec* __restrict__ recs,
                                                             const char2* __restrict__ pc,
                                                             const int32_t* __restrict__ seg_off,
                                                             const int2* __restrict__ segs, void* __restrict__ ptab,
@@ -79,8 +80,16 @@ __global__ void __launch_bounds__(256) sorted_tables_kernel(int M, int n_mask, c
             const int lz = min(max((int)floor(cz) - oz, 0), BT - 1);
             const size_t g = row + start + e;
             tf[g] = pixel_factor(R, (int)k.x, (int)k.y);
-            tg[g] = make_float4(geo_weight(cx - (double)(ox + lx)), geo_weight(cy - (double)(oy + ly)),
-                                geo_weight(cz - (double)(oz + lz)), __int_as_float((lz * BH + ly) * BH + lx));
+            if (nn) {  // the nn voxel j -> (kx, ky, kz) -> the brick frame
+                const int j = nn_index(cx, cy, cz, M, c);
+                const int x = j % M, y = (j / M) % M, zi = j / (M * M);
+                const int nx = min(max(x - c - ox, 0), BH - 1), ny = min(max(y - c - oy, 0), BH - 1);
+                const int nz = min(max((zi < M - c ? zi : zi - M) - oz, 0), BH - 1);
+                tg[g] = make_float4(0.f, 0.f, 0.f, __int_as_float((nz * BH + ny) * BH + nx));
+            } else {
+                tg[g] = make_float4(geo_weight(cx - (double)(ox + lx)), geo_weight(cy - (double)(oy + ly)),
+                                    geo_weight(cz - (double)(oz + lz)), __int_as_float((lz * BH + ly) * BH + lx));
+            }
         }
     }
 }

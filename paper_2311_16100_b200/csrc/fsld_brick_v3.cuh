@@ -74,6 +74,9 @@ __device__ __forceinline__ void load_pix3(const SortedArgs& a, const float2* tf,
 //   pass 1: image value + PixTab, 8-corner gather from the smem brick, r = f P v - x, |r|^2,
 //           conj(f) r and the packed footprint -> brec (the next pixel's loads in flight);
 //   pass 2: fixed-point scatter of val * w (item scale, power of two, non-increasing).
+// NN: nearest-neighbour slicing (kernels.py:180-190, 233-248): one gather and one complex scatter
+// (two ATOMS) per pixel at the nn voxel the table holds.
+template <bool NN>
 __global__ void __launch_bounds__(BTHREADS, FSLD_V3_MINB) brick_loss_grad_kernel(SortedArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     BrickSmem3& S = *reinterpret_cast<BrickSmem3*>(smem_raw);
@@ -184,14 +187,19 @@ __global__ void __launch_bounds__(BTHREADS, FSLD_V3_MINB) brick_loss_grad_kernel
                 const float ax = 1.f - wx, ay = 1.f - wy, az = 1.f - wz;
                 const float2 f = cur.f;
                 const float2* vb = S.vb + l0;
-                const float2 WX = make_float2(wx, wx), AX = make_float2(ax, ax);
-                const float2 e0 = __ffma2_rn(WX, vb[1], __fmul2_rn(AX, vb[0]));
-                const float2 e1 = __ffma2_rn(WX, vb[BH + 1], __fmul2_rn(AX, vb[BH]));
-                const float2 e2 = __ffma2_rn(WX, vb[BH * BH + 1], __fmul2_rn(AX, vb[BH * BH]));
-                const float2 e3 = __ffma2_rn(WX, vb[BH * BH + BH + 1], __fmul2_rn(AX, vb[BH * BH + BH]));
-                const float2 q0 = __ffma2_rn(make_float2(wy, wy), e1, __fmul2_rn(make_float2(ay, ay), e0));
-                const float2 q1 = __ffma2_rn(make_float2(wy, wy), e3, __fmul2_rn(make_float2(ay, ay), e2));
-                const float2 pv = __ffma2_rn(make_float2(wz, wz), q1, __fmul2_rn(make_float2(az, az), q0));
+                float2 pv;
+                if (NN) {
+                    pv = vb[0];
+                } else {
+                    const float2 WX = make_float2(wx, wx), AX = make_float2(ax, ax);
+                    const float2 e0 = __ffma2_rn(WX, vb[1], __fmul2_rn(AX, vb[0]));
+                    const float2 e1 = __ffma2_rn(WX, vb[BH + 1], __fmul2_rn(AX, vb[BH]));
+                    const float2 e2 = __ffma2_rn(WX, vb[BH * BH + 1], __fmul2_rn(AX, vb[BH * BH]));
+                    const float2 e3 = __ffma2_rn(WX, vb[BH * BH + BH + 1], __fmul2_rn(AX, vb[BH * BH + BH]));
+                    const float2 q0 = __ffma2_rn(make_float2(wy, wy), e1, __fmul2_rn(make_float2(ay, ay), e0));
+                    const float2 q1 = __ffma2_rn(make_float2(wy, wy), e3, __fmul2_rn(make_float2(ay, ay), e2));
+                    pv = __ffma2_rn(make_float2(wz, wz), q1, __fmul2_rn(make_float2(az, az), q0));
+                }
                 const float2 prj = cmul(pv, f);
                 const float2 rr = make_float2(prj.x - cur.x.x, prj.y - cur.x.y);
                 sq = fmaf(rr.x, rr.x, fmaf(rr.y, rr.y, sq));
@@ -261,6 +269,13 @@ __global__ void __launch_bounds__(BTHREADS, FSLD_V3_MINB) brick_loss_grad_kernel
             for (int e = threadIdx.x; e < rn; e += BTHREADS) {
                 const uint4 rec = S.brec[e];
                 const int l0 = (int)(rec.z & 1023u);
+                if (NN) {  // one complex contribution at the nn voxel
+                    const float2 y = __ffma2_rn(make_float2(__uint_as_float(rec.x), __uint_as_float(rec.y)),
+                                                make_float2(sc, sc), make_float2(kMagic, kMagic));
+                    atomicAdd(S.accr + l0, __float_as_int(y.x) - kMagicBits);
+                    atomicAdd(S.acci + l0, __float_as_int(y.y) - kMagicBits);
+                    continue;
+                }
                 const float wx = w18((rec.z >> 10) & 262143u);
                 const float wy = w18(__funnelshift_r(rec.z, rec.w, 28) & 262143u);
                 const float wz = w18(rec.w >> 14);

@@ -362,12 +362,13 @@ size_t fsld_sorted_tables_bytes(int N, int n_mask) {
     return sorted_tables_bytes((long long)N * n_mask);
 }
 
-int fsld_sorted_tables(int M, int n_mask, const fsld_image_rec* recs, int N, const int8_t* pc, const int32_t* seg_off,
-                       const int32_t* segs, void* ptab, void* stream) {
+int fsld_sorted_tables(int M, int mode, int n_mask, const fsld_image_rec* recs, int N, const int8_t* pc,
+                       const int32_t* seg_off, const int32_t* segs, void* ptab, void* stream) {
     if (M < 2 || M > 256 || n_mask < 1 || n_mask > 65535 || N < 1 || !recs || !pc || !seg_off || !segs || !ptab)
         return FSLD_EINVAL;
+    if (mode != FSLD_MODE_NN && mode != FSLD_MODE_TRI) return FSLD_EINVAL;
     if (reinterpret_cast<uintptr_t>(ptab) & 255) return FSLD_EINVAL;
-    return status_of(launch_sorted_tables(M, n_mask, recs, N, reinterpret_cast<const char2*>(pc), seg_off,
+    return status_of(launch_sorted_tables(M, n_mask, mode, recs, N, reinterpret_cast<const char2*>(pc), seg_off,
                                           reinterpret_cast<const int2*>(segs), ptab,
                                           reinterpret_cast<cudaStream_t>(stream)));
 }
@@ -380,12 +381,16 @@ int fsld_loss_grad_sorted(int M, int mode, int n_mask, const fsld_image_rec* rec
     if (!geom_ok(M, mode, n_mask, B) || M > 256) return FSLD_EINVAL;
     if (!recs || !v || !xs || !pc || !grad_acc || !sq_out || !scratch) return FSLD_EINVAL;
     const bool det = (flags & FSLD_DETERMINISTIC) != 0;
-    if (mode != FSLD_MODE_TRI || det || (flags & FSLD_TILE_PATH) || !seg_off || !segs)
+    // brick kernels: trilinear (tables or compute path); nearest-neighbour with tables on request
+    const bool brick = (mode == FSLD_MODE_TRI || (ptab && (flags & FSLD_NN_BRICK))) && !det &&
+                       !(flags & FSLD_TILE_PATH) && seg_off && segs;
+    if (!brick)
         return run_reducing(OP_LOSS_GRAD, M, mode, n_mask, nullptr, pc, recs, idx, B, v, xs, grad_acc, sq_out, flags,
                             fx_scale, scratch, scratch_bytes, stream);
     const ScratchLayout L = scratch_layout(M, n_mask, B);
     if (scratch_bytes < L.total) return FSLD_EINVAL;
-    const SortedArgs b = make_sorted(L, M, n_mask, B, recs, idx, v, xs, pc, seg_off, segs, grad_acc, scratch, ptab);
+    SortedArgs b = make_sorted(L, M, n_mask, B, recs, idx, v, xs, pc, seg_off, segs, grad_acc, scratch, ptab);
+    b.nn = mode == FSLD_MODE_NN;
     note_bins(scratch, idx, recs, M, n_mask, B);
     return status_of(launch_sorted_loss_grad(b, sq_out, reinterpret_cast<cudaStream_t>(stream)));
 }
@@ -393,13 +398,14 @@ int fsld_loss_grad_sorted(int M, int mode, int n_mask, const fsld_image_rec* rec
 int fsld_hvp_sorted(int M, int mode, int n_mask, const fsld_image_rec* recs, const int32_t* idx, int B, const void* z,
                     const int8_t* pc, const void* ptab, const int32_t* seg_off, const int32_t* segs, void* acc, double* sq_out,
                     unsigned flags, void* scratch, size_t scratch_bytes, void* stream) {
-    if (!geom_ok(M, mode, n_mask, B) || M > 256 || mode != FSLD_MODE_TRI) return FSLD_EINVAL;
+    if (!geom_ok(M, mode, n_mask, B) || M > 256 || (mode != FSLD_MODE_TRI && !ptab)) return FSLD_EINVAL;
     if (flags & (FSLD_DETERMINISTIC | FSLD_TILE_PATH)) return FSLD_EINVAL;
     if (!recs || !idx || !z || !pc || !seg_off || !segs || !acc || !sq_out || !scratch) return FSLD_EINVAL;
     const ScratchLayout L = scratch_layout(M, n_mask, B);
     if (scratch_bytes < L.total) return FSLD_EINVAL;
     // xs = NULL: the kernel takes the images as zero (r = f P z)
-    const SortedArgs b = make_sorted(L, M, n_mask, B, recs, idx, z, nullptr, pc, seg_off, segs, acc, scratch, ptab);
+    SortedArgs b = make_sorted(L, M, n_mask, B, recs, idx, z, nullptr, pc, seg_off, segs, acc, scratch, ptab);
+    b.nn = mode == FSLD_MODE_NN;
     note_bins(scratch, idx, recs, M, n_mask, B);
     return status_of(launch_sorted_loss_grad(b, sq_out, reinterpret_cast<cudaStream_t>(stream)));
 }

@@ -127,6 +127,7 @@ struct SortedArgs {
     const float2* xs;        // (N, n_mask) brick-sorted images
     const char2* pc;         // (N, n_mask) (kx, ky) of each sorted pixel
     const void* ptab;        // optional (N, n_mask) PixTab (f, footprint): the table-driven brick kernel
+    int nn;                  // nearest-neighbour slicing (table-driven kernel only; 0 = trilinear)
     const int32_t* seg_off;  // (N+1) CSR offsets into segs
     const int2* segs;        // (brick, start | count << 16)
     float2* acc;
@@ -152,7 +153,7 @@ cudaError_t launch_sorted_fill(int M, int n_mask, const short2* pix, const fsld_
                                const float2* x_in, float2* x_out, char2* pc_out, const int32_t* seg_off,
                                int2* segs, cudaStream_t s);
 size_t sorted_tables_bytes(long long npx);
-cudaError_t launch_sorted_tables(int M, int n_mask, const fsld_image_rec* recs, int N, const char2* pc,
+cudaError_t launch_sorted_tables(int M, int n_mask, int mode, const fsld_image_rec* recs, int N, const char2* pc,
                                  const int32_t* seg_off, const int2* segs, void* ptab, cudaStream_t s);
 cudaError_t launch_sorted_loss_grad(const SortedArgs& a, double* sq_out, cudaStream_t s);
 cudaError_t launch_planned_loss_grad(const SortedArgs& a, double* sq_out, cudaStream_t s);

@@ -57,7 +57,7 @@ class SliceEngine:
 
     def __init__(self, M: int, mode: str, mask: np.ndarray, recs: np.ndarray, x=None,
                  deterministic: bool = False, device=None, tile_path: bool = False, layout: str | None = None,
-                 tables: bool = True):
+                 tables: bool = True, nn_brick: bool = False):
         if mode not in ("nn", "tri"):
             raise ValueError("mode must be one of ('nn', 'tri')")
         self.dev = device or require_device()
@@ -68,7 +68,8 @@ class SliceEngine:
         self.n_mask = int(self.mask.size)
         self.n_voxels = self.M ** 3
         self.deterministic = bool(deterministic)
-        self.flags = (C.DETERMINISTIC if self.deterministic else 0) | (C.TILE_PATH if tile_path else 0)
+        self.flags = ((C.DETERMINISTIC if self.deterministic else 0) | (C.TILE_PATH if tile_path else 0)
+                      | (C.NN_BRICK if nn_brick else 0))
         pix = pixel_coords(self.M)[self.mask].astype(np.int16)
         self.pix = torch.from_numpy(np.ascontiguousarray(pix)).to(self.dev)
         recs = np.ascontiguousarray(recs, dtype=C.REC_DTYPE)
@@ -122,7 +123,7 @@ class SliceEngine:
                 self.use_tables = False
                 return
             self.ptab = torch.empty(nbytes, dtype=torch.uint8, device=self.dev)  # 256-B aligned (caching allocator)
-        C.check(C.load().fsld_sorted_tables(self.M, self.n_mask, ctypes_ptr(self.recs), self.n_images,
+        C.check(C.load().fsld_sorted_tables(self.M, self.mode_id, self.n_mask, ctypes_ptr(self.recs), self.n_images,
                                             ctypes_ptr(self.pc), ctypes_ptr(self.seg_off), ctypes_ptr(self.segs),
                                             ctypes_ptr(self.ptab), _stream()), "fsld_sorted_tables")
 
@@ -259,6 +260,12 @@ class SliceEngine:
         """Whether loss_grad / loss_grad_hutch / proj_energy run the brick-sorted kernels."""
         return (self.layout == "sorted" and self.mode == "tri" and not self.deterministic and
                 not (self.flags & C.TILE_PATH) and self.M <= 256)
+
+    @property
+    def table_path(self) -> bool:
+        """Whether loss_grad / hvp run the table-driven brick kernel (tri or nn; dataset tables built)."""
+        return (self.layout == "sorted" and self.ptab is not None and not self.deterministic and
+                not (self.flags & C.TILE_PATH) and (self.mode == "tri" or bool(self.flags & C.NN_BRICK)))
 
     def loss_grad_hutch(self, v, idx, zbits, acc, fold):
         """loss_grad + the k = 1 Hutchinson fold of the same batch (acc, fold accumulate in place).
@@ -475,7 +482,7 @@ class SliceEngine:
         idx = self.idx_tensor(idx)
         B = idx.numel()
         acc = self.new_cacc() if acc is None else acc
-        if self.brick_path and not self.deterministic:
+        if (self.brick_path or self.table_path) and not self.deterministic:
             # brick-sorted layout: the loss+grad work-item kernel with zero images, in chunks
             sq = torch.empty(1, dtype=torch.float64, device=self.dev)
             for lo in range(0, B, self.HVP_CHUNK):

@@ -128,7 +128,7 @@ int main(void) {
     CK(cudaMalloc(&d_ptab, fsld_sorted_tables_bytes(B, n)));
     CK(cudaMalloc(&d_acc3, 8 * nv));
     CK(cudaMemset(d_acc3, 0, 8 * nv));
-    CK(fsld_sorted_tables(M, n, d_recs, B, d_pc, d_seg_off, d_segs, d_ptab, NULL));
+    CK(fsld_sorted_tables(M, FSLD_MODE_TRI, n, d_recs, B, d_pc, d_seg_off, d_segs, d_ptab, NULL));
     CK(fsld_loss_grad_sorted(M, FSLD_MODE_TRI, n, d_recs, NULL, B, d_v, d_xs, d_pc, d_ptab, d_seg_off, d_segs,
                              d_acc3, (double*)d_sq + 2, 0u, NULL, d_scr, scr_bytes, NULL));
     double sq[3];
