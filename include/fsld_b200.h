@@ -488,6 +488,15 @@ int fsld_fsc(int M, int max_radius, const void* u, const void* v, double* out, v
 int fsld_mask_images(int M, int n_mask, const int32_t* mask, int N, const void* images, void* x, void* stream);
 
 /*
+ * Host-side casts for the numpy (reference-signature) calls: dst = (float) src / (double) src over
+ * n reals (2 per complex), OpenMP threads (threads <= 0: up to 16), non-temporal stores so a
+ * page-locked staging buffer is not left dirty in the CPU caches before the copy engine reads it.
+ * Host pointers; no stream, synchronous.
+ */
+int fsld_host_cast_f64_to_f32(const double* src, float* dst, int64_t n, int threads);
+int fsld_host_cast_f32_to_f64(const float* src, double* dst, int64_t n, int threads);
+
+/*
  * Touched-ball compaction for the data-parallel all-reduce: a scatter can only reach
  * voxels within radius R + 1/2 + sqrt(3) of the origin (mask radius R; Appendix A item 7), ~54 %
  * of the cube at M=128, so ranks all-reduce the compacted vector.  idx: (n,) int32 voxel indices

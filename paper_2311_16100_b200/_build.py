@@ -24,6 +24,7 @@ NVCC_FLAGS = [
     "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
     "--expt-relaxed-constexpr",
     "-cudart", "static",
+    "-Xcompiler", "-fopenmp",
 ]
 
 
@@ -61,7 +62,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         subprocess.run(cmd, check=True)
         objs.append(obj)
     tmp = LIB + ".tmp"
-    subprocess.run([nvcc(), *NVCC_FLAGS, "-shared", "-o", tmp, *objs], check=True)
+    subprocess.run([nvcc(), *NVCC_FLAGS, "-shared", "-o", tmp, *objs, "-lgomp"], check=True)
     os.replace(tmp, LIB)
     for o in objs:
         os.remove(o)

@@ -463,6 +463,40 @@ class DatasetOperator:
         torch.cuda.current_stream().synchronize()
         return float(st["out_h"][0])
 
+    def loss_and_grad_numpy(self, v, batch, lam: float, n_total: int | None = None):
+        """optim.loss_and_grad with the reference's argument types (numpy complex128 v in, (float,
+        complex128 gradient) out; optim.py:165-190) on the brick path: v is cast into a pinned
+        complex64 buffer (fsld_host_cast_*: OpenMP threads, streaming stores), fsld_loss_grad_host
+        moves it slab by slab while the brick passes run and streams the complex64 gradient
+        (scale * sum + lam v, formed on the device) back, and the gradient is cast into a fresh
+        complex128 array.  Accuracy: the fp32 path (1e-7 relative
+        from the complex64 v and gradient)."""
+        from . import _capi as C
+
+        e = self.engine
+        n = e.n_voxels
+        st = getattr(self, "_np_stage", None)
+        if st is None:  # cudaHostAlloc staging (the copy engines stream it at full PCIe rate)
+            v64 = C.host_empty(n, torch.complex64)
+            g64 = C.host_empty(n, torch.complex64)
+            st = self._np_stage = {"v": v64, "g": g64, "idx": torch.empty(0, dtype=torch.int32)}
+        b = np.asarray(batch).reshape(-1)
+        if b.size == 0:
+            raise ValueError("batch must be nonempty")
+        if st["idx"].numel() != b.size:
+            st["idx"] = torch.empty(b.size, dtype=torch.int32).pin_memory()
+        st["idx"].numpy()[:] = b
+        lib = C.load()
+        vin = np.ascontiguousarray(v, dtype=np.complex128).reshape(-1)
+        if vin.size != n:
+            raise ValueError(f"volume has {vin.size} entries, expected {n}")
+        # streaming-store casts (fsld_hostio): the staged volume is clean in DRAM for the copy engine
+        C.check(lib.fsld_host_cast_f64_to_f32(vin.ctypes.data, st["v"].data_ptr(), 2 * n, 0), "host cast")
+        loss = self.loss_and_grad_host(st["v"], st["idx"], lam, st["g"], n_total)
+        grad = np.empty(n, dtype=np.complex128)
+        C.check(lib.fsld_host_cast_f32_to_f64(st["g"].data_ptr(), grad.ctypes.data, 2 * n, 0), "host cast")
+        return loss, grad
+
     def b_vector(self):
         """sum_i P_i^* C_i x_i over all images (forward.py:572-579)."""
         e = self.engine

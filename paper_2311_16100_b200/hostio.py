@@ -1,0 +1,43 @@
+"""Host-side staging of the numpy (reference-signature) calls: pinned buffers and threaded casts.
+
+The reference's callers hand ``loss_and_grad`` a numpy complex128 volume and expect a numpy
+complex128 gradient (optim.py:165-190).  The device works in complex64, so each call casts v into a
+page-locked complex64 buffer (the copy engines then stream it at full PCIe rate) and casts the
+pinned complex64 gradient back into a fresh complex128 array.  numpy's casting loops release the
+GIL, so the casts are split over a thread pool (one chunk per core).
+"""
+from __future__ import annotations
+
+import os
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+
+_POOL = None
+_WORKERS = max(1, min(16, os.cpu_count() or 1))
+_MIN_CHUNK = 1 << 16  # elements per task (smaller arrays cast on the calling thread)
+
+
+def _pool() -> ThreadPoolExecutor:
+    global _POOL
+    if _POOL is None:
+        _POOL = ThreadPoolExecutor(max_workers=_WORKERS, thread_name_prefix="fsld-cast")
+    return _POOL
+
+
+def cast_into(dst: np.ndarray, src: np.ndarray) -> np.ndarray:
+    """dst[...] = src (any numeric cast), flat, in parallel chunks."""
+    d = dst.reshape(-1)
+    s = np.asarray(src).reshape(-1)
+    if d.size != s.size:
+        raise ValueError(f"size mismatch {s.size} -> {d.size}")
+    n = d.size
+    k = min(_WORKERS, max(1, n // _MIN_CHUNK))
+    if k == 1:
+        np.copyto(d, s, casting="unsafe")
+        return dst
+    step = -(-n // k)
+    futs = [_pool().submit(np.copyto, d[i:i + step], s[i:i + step], casting="unsafe") for i in range(0, n, step)]
+    for f in futs:
+        f.result()
+    return dst

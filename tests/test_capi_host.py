@@ -187,3 +187,20 @@ def test_plan_entry_points_reject_bad_arguments_without_gpu():
     assert lib.fsld_loss_grad_planned(128, C.MODE_TRI, 12645, 1, 12345, 8, 0, 1, 1, 1, 0, 0, 1, 0, 1, 1, 1 << 30,
                                       0) == C.FSLD_EINVAL
     assert lib.fsld_proj_energy_planned(128, C.MODE_TRI, 12645, 1, 12345, 8, 0, 1, 1, 1, 1, 1 << 30, 0) == C.FSLD_EINVAL
+
+
+def test_host_casts_are_exact_roundings_any_alignment():
+    """fsld_host_cast_* (the numpy call path's staging casts) equal numpy's casts, aligned or not."""
+    lib = C.load()
+    rng = np.random.default_rng(0)
+    for n in (0, 1, 7, 1001, 1 << 16):
+        a = rng.standard_normal(2 * n + 3)
+        for off in (0, 1):
+            src = a[off:off + 2 * n]
+            dst = np.zeros(2 * n + 4, np.float32)[off:off + 2 * n]
+            assert lib.fsld_host_cast_f64_to_f32(src.ctypes.data, dst.ctypes.data, 2 * n, 0) == 0
+            assert np.array_equal(dst, src.astype(np.float32))
+            back = np.zeros(2 * n + 2, np.float64)[off:off + 2 * n]
+            assert lib.fsld_host_cast_f32_to_f64(dst.ctypes.data, back.ctypes.data, 2 * n, 3) == 0
+            assert np.array_equal(back, dst.astype(np.float64))
+    assert lib.fsld_host_cast_f64_to_f32(None, None, -1, 0) == C.FSLD_EINVAL
