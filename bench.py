@@ -701,8 +701,9 @@ def run_leg(eng, wl, B, lam, epochs):
                     "probe + planned loss+grad + precond epilogue + direction energy + Armijo + update; "
                     "per epoch the full-dataset loss, the FSC against the generating volume and one host "
                     "read of the step records",
-            "timing": "wall clock of the whole call, synchronised, host bookkeeping included; the threshold "
-                      f"alpha (host setup, {t_alpha:.2f} s) computed before the call"}
+            "timing": "wall clock of the whole call, synchronised, host bookkeeping included",
+            "setup_seconds": {"threshold_alpha": t_alpha,
+                              "note": "per-image CTF ring power on the device (fsld_ctf_ring_power), before the call"}}
 
 
 def next_rows_leg(eng, wl):

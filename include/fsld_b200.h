@@ -463,7 +463,11 @@ int fsld_loss_grad_step_planned(int M, int mode, int n_mask, const fsld_image_re
  * on `stream`: the outputs are valid once `stream` has been synchronised.
  * Host-side blocking: the step of a given call shape is one cached CUDA graph whose batch rows come
  * from a pinned staging buffer it owns, so a call first waits (host) until the previous replay of
- * the same shape has read its rows; calls from several host threads are serialised. */
+ * the same shape has read its rows; calls from several host threads are serialised.
+ * Buffer lifetime: a cached graph's copies hold v_host / grad_host / out_host as captured.
+ * fsld_host_free drops the graphs that use the buffer it frees; before freeing host buffers that
+ * came from another allocator, call fsld_host_step_reset() (drops every cached graph). */
+int fsld_host_step_reset(void);
 int fsld_loss_grad_host(int M, int mode, int n_mask, const fsld_image_rec* recs, const int32_t* idx_host, int B,
                         const void* v_host, const void* xs, const int8_t* pc, const void* ptab,
                         const int32_t* seg_off, const int32_t* segs, double scale, double lam, void* grad_host, double* out_host,
@@ -483,18 +487,21 @@ int fsld_proj_energy_planned(int M, int mode, int n_mask, const fsld_image_rec* 
  *   (the FSD1 payload, io.py:91-125) -> the compact masked rows of the dataset (forward.py:527).
  */
 size_t fsld_fsc_scratch_bytes(int M, int max_radius);
+/* out[i] = mean over the n_ring pixels (kx, ky) of ring of C_i(k)^2 (fp64; 1 without a CTF): the
+ * per-image term of threshold_alpha for a non-radial CTF (optim.py:250-266). */
+int fsld_ctf_ring_power(const fsld_image_rec* recs, int N, const int16_t* ring, int n_ring, double* out, void* stream);
 int fsld_fsc(int M, int max_radius, const void* u, const void* v, double* out, void* scratch, size_t scratch_bytes,
              void* stream);
 int fsld_mask_images(int M, int n_mask, const int32_t* mask, int N, const void* images, void* x, void* stream);
 
 /*
  * Host-side casts for the numpy (reference-signature) calls: dst = (float) src / (double) src over
- * n reals (2 per complex), OpenMP threads (threads <= 0: up to 16), non-temporal stores so a
- * page-locked staging buffer is not left dirty in the CPU caches before the copy engine reads it.
- * Host pointers; no stream, synchronous.
+ * n reals (2 per complex) with non-temporal stores, so a page-locked staging buffer is not left
+ * dirty in the CPU caches before the copy engine reads it.  Host pointers; synchronous; thread-safe
+ * (callers split large ranges over their own threads).
  */
-int fsld_host_cast_f64_to_f32(const double* src, float* dst, int64_t n, int threads);
-int fsld_host_cast_f32_to_f64(const float* src, double* dst, int64_t n, int threads);
+int fsld_host_cast_f64_to_f32(const double* src, float* dst, int64_t n);
+int fsld_host_cast_f32_to_f64(const float* src, double* dst, int64_t n);
 
 /*
  * Touched-ball compaction for the data-parallel all-reduce: a scatter can only reach

@@ -24,7 +24,6 @@ NVCC_FLAGS = [
     "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
     "--expt-relaxed-constexpr",
     "-cudart", "static",
-    "-Xcompiler", "-fopenmp",
 ]
 
 
@@ -62,7 +61,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         subprocess.run(cmd, check=True)
         objs.append(obj)
     tmp = LIB + ".tmp"
-    subprocess.run([nvcc(), *NVCC_FLAGS, "-shared", "-o", tmp, *objs, "-lgomp"], check=True)
+    subprocess.run([nvcc(), *NVCC_FLAGS, "-shared", "-o", tmp, *objs], check=True)
     os.replace(tmp, LIB)
     for o in objs:
         os.remove(o)

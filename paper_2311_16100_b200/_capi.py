@@ -91,8 +91,10 @@ SIGNATURES = {
     "fsld_sorted_tables": (I, [I, I, I, P, I, P, P, P, P, P]),
     "fsld_sorted_tables_bytes": (SZ, [I, I]),
     "fsld_fsc_scratch_bytes": (SZ, [I, I]),
-    "fsld_host_cast_f64_to_f32": (I, [P, P, I64, I]),
-    "fsld_host_cast_f32_to_f64": (I, [P, P, I64, I]),
+    "fsld_host_step_reset": (I, []),
+    "fsld_ctf_ring_power": (I, [P, I, P, I, P, P]),
+    "fsld_host_cast_f64_to_f32": (I, [P, P, I64]),
+    "fsld_host_cast_f32_to_f64": (I, [P, P, I64]),
     "fsld_fsc": (I, [I, I, P, P, P, P, SZ, P]),
     "fsld_mask_images": (I, [I, I, P, I, P, P, P]),
     "fsld_loss_grad_sorted": (I, [I, I, I, P, P, I, P, P, P, P, P, P, P, P, U, P, P, SZ, P]),

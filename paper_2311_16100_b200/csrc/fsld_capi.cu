@@ -123,6 +123,10 @@ SortedArgs make_sorted(const ScratchLayout& L, int M, int n_mask, int B, const f
 
 }  // namespace
 
+namespace {
+void drop_host_graphs_using(const void* p);  // (fsld_loss_grad_host's graph cache, below)
+}  // namespace
+
 extern "C" {
 
 int fsld_abi_version(void) { return FSLD_ABI_VERSION; }
@@ -160,7 +164,11 @@ int fsld_host_alloc(size_t bytes, void** out) {
     return status_of(cudaHostAlloc(out, bytes, cudaHostAllocDefault));
 }
 
-int fsld_host_free(void* p) { return p ? status_of(cudaFreeHost(p)) : FSLD_OK; }
+int fsld_host_free(void* p) {
+    if (!p) return FSLD_OK;
+    drop_host_graphs_using(p);  // a replay must never touch a freed (and maybe re-allocated) buffer
+    return status_of(cudaFreeHost(p));
+}
 
 size_t fsld_scratch_bytes(int M, int n_mask, int B) {
     if (M < 2 || M > 1024) return 0;
@@ -616,6 +624,13 @@ extern "C" int fsld_fsc(int M, int max_radius, const void* u, const void* v, dou
                                 reinterpret_cast<double*>(scratch), out, reinterpret_cast<cudaStream_t>(stream)));
 }
 
+extern "C" int fsld_ctf_ring_power(const fsld_image_rec* recs, int N, const int16_t* ring, int n_ring, double* out,
+                                   void* stream) {
+    if (N < 0 || n_ring < 1 || (N > 0 && (!recs || !ring || !out))) return FSLD_EINVAL;
+    return status_of(launch_ctf_ring_power(recs, N, reinterpret_cast<const short2*>(ring), n_ring, out,
+                                           reinterpret_cast<cudaStream_t>(stream)));
+}
+
 extern "C" int fsld_mask_images(int M, int n_mask, const int32_t* mask, int N, const void* images, void* x,
                                 void* stream) {
     if (M < 2 || n_mask < 1 || n_mask > M * M || N < 0 || !mask || (N > 0 && (!images || !x))) return FSLD_EINVAL;
@@ -1026,7 +1041,20 @@ cudaError_t host_graph(const HostStepKey& k, HostPipe* P, HostGraph*& out) {
     return cudaSuccess;
 }
 
+// Every cached graph whose copies read or write host buffer p (its memcpy nodes hold the address
+// as it was when captured): dropped before p is freed, and on fsld_host_step_reset().
+void drop_host_graphs_using(const void* p) {
+    std::lock_guard<std::mutex> lk(g_pipe_mu);
+    for (HostGraph& h : g_graphs)
+        if (h.exec && (!p || h.key.v_host == p || h.key.grad_host == p || h.key.out_host == p)) drop_graph(h);
+}
+
 }  // namespace
+
+extern "C" int fsld_host_step_reset(void) {
+    drop_host_graphs_using(nullptr);
+    return FSLD_OK;
+}
 
 extern "C" int fsld_loss_grad_host(int M, int mode, int n_mask, const fsld_image_rec* recs, const int32_t* idx_host,
                                    int B, const void* v_host, const void* xs, const int8_t* pc, const void* ptab,

@@ -77,4 +77,37 @@ cudaError_t launch_mask_images(int M, int n_mask, const int32_t* mask, int N, co
     return cudaGetLastError();
 }
 
+// Mean over the pixels of one ring (rounded radius R) of each image's squared CTF, fp64 throughout
+// (threshold_alpha's sum_i |C_i(R)|^2 for a non-radial CTF; optim.py:250-266): one CTA per image.
+__global__ void __launch_bounds__(128) ctf_ring_power_kernel(const fsld_image_rec* __restrict__ recs, int N,
+                                                             const short2* __restrict__ ring, int n_ring,
+                                                             double* __restrict__ out) {
+    __shared__ double red[4];
+    const int i = blockIdx.x;
+    const fsld_image_rec& R = recs[i];
+    double s = 0.0;
+    for (int p = threadIdx.x; p < n_ring; p += blockDim.x) {
+        double c2 = 1.0;
+        if (R.flags & FSLD_REC_CTF) {
+            const double kx = ring[p].x, ky = ring[p].y, k2 = kx * kx + ky * ky;
+            const double g = R.gamma[0] * k2 + R.gamma[1] * (kx * kx - ky * ky) + R.gamma[2] * (2.0 * kx * ky) +
+                             R.gamma[3] * k2 * k2;
+            const double c = -((double)R.wsin * sin(g) + (double)R.wcos * cos(g)) * exp(-R.env * k2);
+            c2 = c * c;
+        }
+        s += c2;
+    }
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) out[i] = (red[0] + red[1] + red[2] + red[3]) / (double)n_ring;
+}
+
+cudaError_t launch_ctf_ring_power(const fsld_image_rec* recs, int N, const short2* ring, int n_ring, double* out,
+                                  cudaStream_t s) {
+    if (N < 1) return cudaSuccess;
+    ctf_ring_power_kernel<<<N, 128, 0, s>>>(recs, N, ring, n_ring, out);
+    return cudaGetLastError();
+}
+
 }  // namespace fsld

@@ -726,14 +726,15 @@ def records_for(M: int, quats, shifts=None, ctfs=None) -> np.ndarray:
     ctfs: None, or a sequence of CtfParams-like (defocus, amp_contrast,
     b_factor) / PhysicalCtf objects (see forward.ctf_coefficients).
     """
-    from .forward import ctf_coefficients, quat_to_matrix
+    from .forward import ctf_coefficients
 
     quats = np.asarray(quats, dtype=np.float64).reshape(-1, 4)
     N = quats.shape[0]
     recs = np.zeros(N, dtype=C.REC_DTYPE)
-    for i in range(N):
-        R = quat_to_matrix(quats[i])
-        recs["rot"][i] = (R[0, 0], R[0, 1], R[0, 2], R[1, 0], R[1, 1], R[1, 2])
+    # rows 0-1 of quat_to_matrix, vectorised with the same per-element fp64 expressions (bit-identical)
+    w, x, y, z = (quats[:, i] for i in range(4))
+    recs["rot"] = np.stack([1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y),
+                            2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)], axis=1)
     if shifts is not None:
         t = np.asarray(shifts, dtype=np.float64).reshape(N, 2)
         recs["shift"] = -2.0 * t / M
@@ -741,11 +742,10 @@ def records_for(M: int, quats, shifts=None, ctfs=None) -> np.ndarray:
     if ctfs is not None:
         if len(ctfs) != N:
             raise ValueError("ctfs length must match poses")
-        for i, c in enumerate(ctfs):
-            g, env, ws, wc = ctf_coefficients(c, M)
-            recs["gamma"][i] = g
-            recs["env"][i] = env
-            recs["wsin"][i] = ws
-            recs["wcos"][i] = wc
+        co = [ctf_coefficients(c, M) for c in ctfs]
+        recs["gamma"] = np.array([t[0] for t in co], dtype=np.float64).reshape(N, 4)
+        recs["env"] = np.array([t[1] for t in co], dtype=np.float64)
+        recs["wsin"] = np.array([t[2] for t in co], dtype=np.float32)
+        recs["wcos"] = np.array([t[3] for t in co], dtype=np.float32)
         recs["flags"] |= np.uint32(C.REC_CTF)
     return recs

@@ -466,12 +466,13 @@ class DatasetOperator:
     def loss_and_grad_numpy(self, v, batch, lam: float, n_total: int | None = None):
         """optim.loss_and_grad with the reference's argument types (numpy complex128 v in, (float,
         complex128 gradient) out; optim.py:165-190) on the brick path: v is cast into a pinned
-        complex64 buffer (fsld_host_cast_*: OpenMP threads, streaming stores), fsld_loss_grad_host
+        complex64 buffer (fsld_host_cast_*: streaming stores, host thread pool), fsld_loss_grad_host
         moves it slab by slab while the brick passes run and streams the complex64 gradient
         (scale * sum + lam v, formed on the device) back, and the gradient is cast into a fresh
         complex128 array.  Accuracy: the fp32 path (1e-7 relative
         from the complex64 v and gradient)."""
         from . import _capi as C
+        from .hostio import cast_native
 
         e = self.engine
         n = e.n_voxels
@@ -490,11 +491,12 @@ class DatasetOperator:
         vin = np.ascontiguousarray(v, dtype=np.complex128).reshape(-1)
         if vin.size != n:
             raise ValueError(f"volume has {vin.size} entries, expected {n}")
-        # streaming-store casts (fsld_hostio): the staged volume is clean in DRAM for the copy engine
-        C.check(lib.fsld_host_cast_f64_to_f32(vin.ctypes.data, st["v"].data_ptr(), 2 * n, 0), "host cast")
+        # streaming-store casts on the host thread pool: the staged volume is clean in DRAM for the
+        # copy engine
+        cast_native(lib.fsld_host_cast_f64_to_f32, vin.ctypes.data, st["v"].data_ptr(), 2 * n, 8, 4)
         loss = self.loss_and_grad_host(st["v"], st["idx"], lam, st["g"], n_total)
         grad = np.empty(n, dtype=np.complex128)
-        C.check(lib.fsld_host_cast_f32_to_f64(st["g"].data_ptr(), grad.ctypes.data, 2 * n, 0), "host cast")
+        cast_native(lib.fsld_host_cast_f32_to_f64, st["g"].data_ptr(), grad.ctypes.data, 2 * n, 4, 8)
         return loss, grad
 
     def b_vector(self):

@@ -41,3 +41,19 @@ def cast_into(dst: np.ndarray, src: np.ndarray) -> np.ndarray:
     for f in futs:
         f.result()
     return dst
+
+
+def cast_native(fn, src_ptr: int, dst_ptr: int, n: int, src_item: int, dst_item: int) -> None:
+    """Run a fsld_host_cast_* over n reals split into 16-byte-aligned chunks on the thread pool
+    (ctypes releases the GIL for the foreign call, so the chunks run in parallel)."""
+    k = min(_WORKERS, max(1, n // (4 * _MIN_CHUNK)))
+    step = (-(-n // k) + 3) & ~3  # multiple of 4 reals: each chunk start stays 16-byte aligned
+    jobs = [(i, min(step, n - i)) for i in range(0, n, step)]
+    if len(jobs) == 1:
+        if fn(src_ptr, dst_ptr, n) != 0:
+            raise ValueError("host cast failed")
+        return
+    futs = [_pool().submit(fn, src_ptr + i * src_item, dst_ptr + i * dst_item, m) for i, m in jobs]
+    for f in futs:
+        if f.result() != 0:
+            raise ValueError("host cast failed")

@@ -267,7 +267,10 @@ def threshold_alpha(stack, shells=None, lam: float = 0.0) -> float:
         ring = pc[np.round(np.sqrt((pc ** 2).sum(axis=1))) == r]
         csum = 0.0
         if all(isinstance(c, PhysicalCtf) or hasattr(c, "astig") for c in stack.ctfs):
-            # vectorised over images (same per-element formula as ctf_table_row), summed in image order
+            if torch.cuda.is_available():  # fsld_ctf_ring_power: one CTA per image, fp64
+                csum = _ring_power_device(stack.ctfs, ring, M)
+                return ratio * csum + lam
+            # (no device: the same per-element formula vectorised on the host, summed in image order)
             from .forward import ctf_coefficients
             co = [ctf_coefficients(c, M) for c in stack.ctfs]
             g = np.array([t[0] for t in co], dtype=np.float64)
@@ -290,6 +293,25 @@ def threshold_alpha(stack, shells=None, lam: float = 0.0) -> float:
             else:
                 csum += ctf_eval(c, r, M // 2) ** 2
     return ratio * csum + lam
+
+
+def _ring_power_device(ctfs, ring: np.ndarray, M: int) -> float:
+    """sum_i mean_{k in ring} C_i(k)^2 on the device (fsld_ctf_ring_power), summed in image order."""
+    from . import _capi as C
+    from .engine import _stream, ctypes_ptr, records_for
+
+    n = len(ctfs)
+    recs = records_for(M, np.tile([1.0, 0.0, 0.0, 0.0], (n, 1)), None, ctfs)  # the CTF fields only
+    dev = torch.device("cuda", torch.cuda.current_device())
+    rd = torch.from_numpy(recs.view(np.uint8).copy()).to(dev)
+    rg = torch.from_numpy(np.ascontiguousarray(ring, dtype=np.int16)).to(dev)
+    out = torch.empty(n, dtype=torch.float64, device=dev)
+    C.check(C.load().fsld_ctf_ring_power(ctypes_ptr(rd), n, ctypes_ptr(rg), rg.shape[0], ctypes_ptr(out), _stream()),
+            "fsld_ctf_ring_power")
+    csum = 0.0
+    for m in out.cpu().numpy():
+        csum += float(m)
+    return csum
 
 
 def armijo_search(v, grad, dhat, loss_fn, eta_in: float, c: float, f0=None):

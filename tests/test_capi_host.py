@@ -190,7 +190,8 @@ def test_plan_entry_points_reject_bad_arguments_without_gpu():
 
 
 def test_host_casts_are_exact_roundings_any_alignment():
-    """fsld_host_cast_* (the numpy call path's staging casts) equal numpy's casts, aligned or not."""
+    """fsld_host_cast_* (the numpy call path's staging casts) equal numpy's casts, aligned or not, and
+    the thread-pool split (hostio.cast_native) covers the whole range."""
     lib = C.load()
     rng = np.random.default_rng(0)
     for n in (0, 1, 7, 1001, 1 << 16):
@@ -198,9 +199,14 @@ def test_host_casts_are_exact_roundings_any_alignment():
         for off in (0, 1):
             src = a[off:off + 2 * n]
             dst = np.zeros(2 * n + 4, np.float32)[off:off + 2 * n]
-            assert lib.fsld_host_cast_f64_to_f32(src.ctypes.data, dst.ctypes.data, 2 * n, 0) == 0
+            assert lib.fsld_host_cast_f64_to_f32(src.ctypes.data, dst.ctypes.data, 2 * n) == 0
             assert np.array_equal(dst, src.astype(np.float32))
             back = np.zeros(2 * n + 2, np.float64)[off:off + 2 * n]
-            assert lib.fsld_host_cast_f32_to_f64(dst.ctypes.data, back.ctypes.data, 2 * n, 3) == 0
+            assert lib.fsld_host_cast_f32_to_f64(dst.ctypes.data, back.ctypes.data, 2 * n) == 0
             assert np.array_equal(back, dst.astype(np.float64))
-    assert lib.fsld_host_cast_f64_to_f32(None, None, -1, 0) == C.FSLD_EINVAL
+    assert lib.fsld_host_cast_f64_to_f32(None, None, -1) == C.FSLD_EINVAL
+    from paper_2311_16100_b200.hostio import cast_native
+    big = rng.standard_normal(2 * 300001)
+    out = np.zeros(2 * 300001, np.float32)
+    cast_native(lib.fsld_host_cast_f64_to_f32, big.ctypes.data, out.ctypes.data, big.size, 8, 4)
+    assert np.array_equal(out, big.astype(np.float32))

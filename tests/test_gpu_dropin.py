@@ -163,3 +163,18 @@ def test_fsc_kernel_matches_oracle():
     from paper_2311_16100_b200.metrics import ShellIndex
     got2 = F.fsc(torch.from_numpy(u).cuda(), torch.from_numpy(v).cuda(), ShellIndex(M, R, "cuda"))
     assert np.max(np.abs(got2.values[defined] - ref[defined])) < 1e-12
+
+
+def test_threshold_alpha_device_ring_power_matches_host():
+    """threshold_alpha's per-image ring mean of C^2 (non-radial CTF) on the device equals the host
+    evaluation of the same formula (optim.py:250-266)."""
+    from unittest import mock
+    from paper_2311_16100_b200 import optim as Opt, synth
+    M, n = 128, 3000
+    spec = F.GridSpec(M)
+    stack = F.ImageStack.__new__(F.ImageStack)
+    stack.spec, stack.mask_radius, stack.ctfs, stack.poses = spec, M // 2 - 1, synth.physical_ctfs(n, 5), [None] * n
+    a_dev = Opt.threshold_alpha(stack, F.shell_table(spec, M // 2 - 1), 1e-3)
+    with mock.patch("torch.cuda.is_available", return_value=False):
+        a_host = Opt.threshold_alpha(stack, F.shell_table(spec, M // 2 - 1), 1e-3)
+    assert abs(a_dev - a_host) <= 1e-7 * a_host  # (records carry wsin / wcos in fp32)

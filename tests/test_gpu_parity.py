@@ -551,3 +551,19 @@ def test_host_step_graph_cache_across_shapes_and_scalars():
         l_h = op.loss_and_grad_host(v_h[it % 2], torch.from_numpy(batch).pin_memory(), lam, g_h, n_total=n_img)
         assert abs(l_h - l_ref) / l_ref < 1e-6, it
         assert rel(g_h.numpy(), g_ref) < 5e-6, it  # fp32 epilogue on the device vs fp64 on the host
+
+
+def test_host_step_graph_cache_survives_freed_and_reused_buffers(golden):
+    """The numpy call path stages through pinned buffers (fsld_host_alloc) that die with their
+    operator; a later operator can get the same addresses.  Cached host-step graphs that captured
+    a freed buffer must be dropped (fsld_host_free), never replayed."""
+    import gc
+    g = golden("dataset_m16_tri.npz")
+    lam = float(g["lam"])
+    for _ in range(4):
+        op, _ = golden_ops(g)
+        loss, grad = F.loss_and_grad(op, g["v1"], g["batch"], lam)
+        assert abs(loss - float(g["loss1_batch"])) / float(g["loss1_batch"]) < TOL
+        assert rel(grad, g["grad1_batch"]) < TOL
+        del op
+        gc.collect()
