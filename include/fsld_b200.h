@@ -267,7 +267,8 @@ int fsld_loss_grad_sorted(int M, int mode, int n_mask, const fsld_image_rec* rec
  * shared memory and 8 more shared-memory adds per pixel).  FSLD_DETERMINISTIC / FSLD_TILE_PATH
  * are rejected (use fsld_loss_grad_sorted + fsld_hutch_fold). */
 int fsld_loss_grad_hutch_sorted(int M, int mode, int n_mask, const fsld_image_rec* recs, const int32_t* idx, int B,
-                                const void* v, const void* xs, const int8_t* pc, const int32_t* seg_off,
+                                const void* v, const void* xs, const int8_t* pc, const void* ptab,
+                                const int32_t* seg_off,
                                 const int32_t* segs, const uint32_t* zbits, void* grad_acc, float* fold,
                                 double* sq_out, unsigned flags, void* scratch, size_t scratch_bytes, void* stream);
 

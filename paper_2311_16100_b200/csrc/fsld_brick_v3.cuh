@@ -23,11 +23,17 @@ constexpr int RB3 = FSLD_RB3;
 #endif
 constexpr int BK3 = BC * kSegMax;  // pixels per work item (<= BC segments of <= kSegMax pixels)
 
-struct BrickSmem3 {
+template <bool HUTCH>
+struct BrickSmem3T {
     float2 vb[BH3];         // v brick + halo
     int accr[BH3];          // fixed-point adjoint accumulator (re)
     int acci[BH3];          // (im)
     uint4 brec[RB3];        // pass 1 -> 2: conj(f) r (2 x fp32) + the packed footprint (geo_pack)
+    int acch[HUTCH ? BH3 : 1];            // fixed-point Hutchinson accumulator
+    float hval[HUTCH ? RB3 : 1];          // pass 1 -> 2: h = |f|^2 P z
+    unsigned char zs[HUTCH ? BH3 : 1];    // the probe's sign bit per brick voxel (staged)
+    unsigned char zc[HUTCH ? BH3 : 1];    // corner sign masks (bit c = z at corner c of floor voxel l)
+    int hmax2[HUTCH ? 2 : 1];
     unsigned char bk[BK3];  // item pixel -> segment
     PairRec prec[BC];       // the item's pair records (gofs, count)
     long long sg[BC];       // segment start rebased to the item's flat pixel index: gofs - pref
@@ -37,6 +43,7 @@ struct BrickSmem3 {
     int wtot[BC / 32];
     double red[BW];
 };
+using BrickSmem3 = BrickSmem3T<false>;
 
 // The footprint in 8 bytes for the pass-1 -> pass-2 buffer: corner index (10 bits) and the three
 // weights as 18-bit fixed point (round to nearest; |error| <= 2^-19 on the adjoint's weights).
@@ -76,10 +83,14 @@ __device__ __forceinline__ void load_pix3(const SortedArgs& a, const float2* tf,
 //   pass 2: fixed-point scatter of val * w (item scale, power of two, non-increasing).
 // NN: nearest-neighbour slicing (kernels.py:180-190, 233-248): one gather and one complex scatter
 // (two ATOMS) per pixel at the nn voxel the table holds.
-template <bool NN>
-__global__ void __launch_bounds__(BTHREADS, FSLD_V3_MINB) brick_loss_grad_kernel(SortedArgs a) {
+// HUTCH (trilinear): the k = 1 Rademacher probe rides along (optim.py:210-229 numerator): P z from
+// the corner signs of the staged probe bits, h = |f|^2 P z, 8 more fixed-point shared adds, and
+// fold_j += z_j (sum P^* C^2 P z)_j at the flush.
+template <bool NN, bool HUTCH>
+__global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss_grad_kernel(SortedArgs a) {
+    static_assert(!(NN && HUTCH), "the fused probe is trilinear only");
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    BrickSmem3& S = *reinterpret_cast<BrickSmem3*>(smem_raw);
+    BrickSmem3T<HUTCH>& S = *reinterpret_cast<BrickSmem3T<HUTCH>*>(smem_raw);
     a.pairs += a.ctl[3];
     a.items += a.ctl[4];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -97,6 +108,7 @@ __global__ void __launch_bounds__(BTHREADS, FSLD_V3_MINB) brick_loss_grad_kernel
         if (l < BH3) {
             S.accr[l] = 0;
             S.acci[l] = 0;
+            if (HUTCH) S.acch[l] = 0;
         }
     }
     constexpr int kClaimer = BTHREADS - 32;
@@ -117,13 +129,17 @@ __global__ void __launch_bounds__(BTHREADS, FSLD_V3_MINB) brick_loss_grad_kernel
             const bool in = kx < M - c && ky < M - c && kz < M - c;
             const int j = in ? lin_index(kx, ky, kz, M, c) : 0;
             cp_async8_zfill(S.vb + l, a.v + j, in);
+            if (HUTCH) S.zs[l] = in ? (unsigned char)(__ldg(a.zbits + j) & 1u) : 0;
         }
     };
     if (threadIdx.x == kClaimer) {
         S.item_desc = claim();
         S.next_desc = claim();
     }
-    if (threadIdx.x < 2) S.vmax2[threadIdx.x] = 0;
+    if (threadIdx.x < 2) {
+        S.vmax2[threadIdx.x] = 0;
+        if (HUTCH) S.hmax2[threadIdx.x] = 0;
+    }
     __syncthreads();
     int4 item = S.item_desc;
     if (item.x >= 0) stage_item3(item);
@@ -146,6 +162,19 @@ __global__ void __launch_bounds__(BTHREADS, FSLD_V3_MINB) brick_loss_grad_kernel
             }
             S.pref[k] = incl - len;
             if (lane == 31) S.wtot[warp] = incl;
+        }
+        if (HUTCH) {  // corner sign masks (x fastest: 000,100,010,110,001,101,011,111) of the floor voxels
+#pragma unroll
+            for (int u = 0; u < BU; ++u) {
+                if (lxyz[u] < 0) continue;
+                const int l = threadIdx.x + u * BTHREADS;
+                unsigned m = S.zs[l];
+                if ((lxyz[u] & 15) < BT && ((lxyz[u] >> 4) & 15) < BT && (lxyz[u] >> 8) < BT)
+                    m |= (unsigned)S.zs[l + 1] << 1 | (unsigned)S.zs[l + BH] << 2 | (unsigned)S.zs[l + BH + 1] << 3 |
+                         (unsigned)S.zs[l + BH * BH] << 4 | (unsigned)S.zs[l + BH * BH + 1] << 5 |
+                         (unsigned)S.zs[l + BH * BH + BH] << 6 | (unsigned)S.zs[l + BH * BH + BH + 1] << 7;
+                S.zc[l] = (unsigned char)m;
+            }
         }
         __syncthreads();  // (B)
         if (threadIdx.x == kClaimer) S.next_desc = claim();
@@ -170,7 +199,7 @@ __global__ void __launch_bounds__(BTHREADS, FSLD_V3_MINB) brick_loss_grad_kernel
         __syncthreads();
         const int total = S.pref[nseg];
         const float lim = (float)min(4194303, 178956970 / nseg);
-        float item_sc = 0.f, item_inv_sc = 1.f;
+        float item_sc = 0.f, item_inv_sc = 1.f, item_sch = 0.f, item_inv_sch = 1.f;
         // this thread's first pixel of the item (register buffers A / B alternate: no moves of
         // in-flight load destinations, so a load is waited for only where its pixel is computed)
         Pix3 pa, pb;
@@ -180,7 +209,7 @@ __global__ void __launch_bounds__(BTHREADS, FSLD_V3_MINB) brick_loss_grad_kernel
             const int r1 = min(r0 + RB3, total);
             const int par = rpar & 1;
             // ---------------- pass 1 (flattened over the round; the next pixel's loads in flight)
-            float vmax = 0.f, sq = 0.f;
+            float vmax = 0.f, hmax = 0.f, sq = 0.f;
             auto compute = [&](const Pix3& cur, int e) {
                 const float wx = cur.geo.x, wy = cur.geo.y, wz = cur.geo.z;
                 const int l0 = __float_as_int(cur.geo.w);
@@ -207,6 +236,16 @@ __global__ void __launch_bounds__(BTHREADS, FSLD_V3_MINB) brick_loss_grad_kernel
                 vmax = fmaxf(vmax, fmaxf(fabsf(val.x), fabsf(val.y)));
                 const uint2 gp = geo_pack(cur.geo);
                 S.brec[e - r0] = make_uint4(__float_as_uint(val.x), __float_as_uint(val.y), gp.x, gp.y);
+                if (HUTCH) {  // P z in the same nested order, z = +-1 from the corner sign bits
+                    const unsigned m = S.zc[l0];
+                    auto zf = [m](int b) { return __int_as_float(0xBF800000u ^ (((m >> b) & 1u) << 31)); };
+                    const float z0 = ax * zf(0) + wx * zf(1), z1 = ax * zf(2) + wx * zf(3);
+                    const float z2 = ax * zf(4) + wx * zf(5), z3 = ax * zf(6) + wx * zf(7);
+                    const float pz = az * (ay * z0 + wy * z1) + wz * (ay * z2 + wy * z3);
+                    const float h = fmaf(f.x, f.x, f.y * f.y) * pz;
+                    S.hval[e - r0] = h;
+                    hmax = fmaxf(hmax, fabsf(h));
+                }
             };
             // target of the load issued before computing pixel e: the thread's next pixel of this
             // round, else its first pixel of the next round
@@ -231,38 +270,58 @@ __global__ void __launch_bounds__(BTHREADS, FSLD_V3_MINB) brick_loss_grad_kernel
             {
                 const int vb_max = __reduce_max_sync(0xffffffffu, __float_as_int(vmax));
                 if (lane == 0) atomicMax(&S.vmax2[par], vb_max);
+                if (HUTCH) {
+                    const int hb_max = __reduce_max_sync(0xffffffffu, __float_as_int(hmax));
+                    if (lane == 0) atomicMax(&S.hmax2[par], hb_max);
+                }
             }
             __syncthreads();
             if (r1 >= total && nxt.x >= 0) stage_item3(nxt);  // overlaps pass 2 + flush
             // ---------------- pass 2: fixed-point adjoint scatter (kernels.py:221-230)
             {
-                const float vm = __int_as_float(S.vmax2[par]);
-                float inv_r;
-                const float sc_r = pow2_scale(lim, vm, inv_r);
-                if (r0 == 0 || sc_r >= item_sc) {
-                    if (r0 == 0) {
-                        item_sc = sc_r;
-                        item_inv_sc = inv_r;
-                    }
-                } else {  // a smaller scale: shift the partial sums down (rounded) first
-                    const int sh = (__float_as_int(item_sc) - __float_as_int(sc_r)) >> 23;
+                // one power-of-two scale per item and accumulator, non-increasing over its rounds: a
+                // round that needs a smaller one first shifts the partial sums down (rounded)
+                auto shift_down = [&](int sh, int* acc_a, int* acc_b) {
 #pragma unroll
                     for (int u = 0; u < BU; ++u) {
                         if (lxyz[u] < 0) continue;
                         const int l = threadIdx.x + u * BTHREADS;
                         if (sh >= 31) {
-                            S.accr[l] = 0;
-                            S.acci[l] = 0;
+                            acc_a[l] = 0;
+                            if (acc_b) acc_b[l] = 0;
                         } else {
                             const long long half = 1ll << (sh - 1);
-                            S.accr[l] = (int)(((long long)S.accr[l] + half) >> sh);
-                            S.acci[l] = (int)(((long long)S.acci[l] + half) >> sh);
+                            acc_a[l] = (int)(((long long)acc_a[l] + half) >> sh);
+                            if (acc_b) acc_b[l] = (int)(((long long)acc_b[l] + half) >> sh);
                         }
                     }
+                };
+                bool sync = false;
+                float inv_r;
+                const float sc_r = pow2_scale(lim, __int_as_float(S.vmax2[par]), inv_r);
+                if (r0 == 0) {
                     item_sc = sc_r;
                     item_inv_sc = inv_r;
-                    __syncthreads();
+                } else if (sc_r < item_sc) {
+                    shift_down((__float_as_int(item_sc) - __float_as_int(sc_r)) >> 23, S.accr, S.acci);
+                    item_sc = sc_r;
+                    item_inv_sc = inv_r;
+                    sync = true;
                 }
+                if (HUTCH) {
+                    float inv_h;
+                    const float sh_r = pow2_scale(lim, __int_as_float(S.hmax2[par]), inv_h);
+                    if (r0 == 0) {
+                        item_sch = sh_r;
+                        item_inv_sch = inv_h;
+                    } else if (sh_r < item_sch) {
+                        shift_down((__float_as_int(item_sch) - __float_as_int(sh_r)) >> 23, S.acch, nullptr);
+                        item_sch = sh_r;
+                        item_inv_sch = inv_h;
+                        sync = true;
+                    }
+                }
+                if (sync) __syncthreads();  // (uniform: every thread read the same maxima)
             }
             const float sc = item_sc;
             const int rn = r1 - r0;
@@ -290,8 +349,17 @@ __global__ void __launch_bounds__(BTHREADS, FSLD_V3_MINB) brick_loss_grad_kernel
                     atomicAdd(S.accr + l0 + off8[q], __float_as_int(y.x) - kMagicBits);
                     atomicAdd(S.acci + l0 + off8[q], __float_as_int(y.y) - kMagicBits);
                 }
+                if (HUTCH) {
+                    const float h = S.hval[e] * item_sch;
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        atomicAdd(S.acch + l0 + off8[q], __float_as_int(fmaf(w8[q], h, kMagic)) - kMagicBits);
+                }
             }
-            if (threadIdx.x == 0) S.vmax2[par ^ 1] = 0;  // the next round's slot (unused since this round's barrier)
+            if (threadIdx.x == 0) {  // the next round's slots (unused since this round's barrier)
+                S.vmax2[par ^ 1] = 0;
+                if (HUTCH) S.hmax2[par ^ 1] = 0;
+            }
             __syncthreads();
         }
         // flush of the item: one reduction per touched voxel, accumulators re-zeroed
@@ -300,14 +368,22 @@ __global__ void __launch_bounds__(BTHREADS, FSLD_V3_MINB) brick_loss_grad_kernel
             if (lxyz[u] < 0) continue;
             const int l = threadIdx.x + u * BTHREADS;
             const int qr = S.accr[l], qi = S.acci[l];
-            if ((qr | qi) == 0) continue;
+            const int qh = HUTCH ? S.acch[l] : 0;
+            if ((qr | qi | qh) == 0) continue;
             S.accr[l] = 0;
             S.acci[l] = 0;
+            if (HUTCH) S.acch[l] = 0;
             const int kx = ox + (lxyz[u] & 15), ky = oy + ((lxyz[u] >> 4) & 15), kz = oz + (lxyz[u] >> 8);
             if (kx >= M - c || ky >= M - c || kz >= M - c) continue;
             const size_t j = (size_t)lin_index(kx, ky, kz, M, c);
-            const float fs = item_inv_sc * a.out_scale;
-            red_f32x2(reinterpret_cast<float*>(a.acc) + 2 * j, (float)qr * fs, (float)qi * fs);
+            if ((qr | qi) != 0) {
+                const float fs = item_inv_sc * a.out_scale;
+                red_f32x2(reinterpret_cast<float*>(a.acc) + 2 * j, (float)qr * fs, (float)qi * fs);
+            }
+            if (HUTCH && qh != 0) {  // fold_j += z_j h_j
+                const float hz = (S.zc[l] & 1u) ? (float)qh * item_inv_sch : -(float)qh * item_inv_sch;
+                atomicAdd(a.fold + j, hz);
+            }
         }
         item = nxt;
     }

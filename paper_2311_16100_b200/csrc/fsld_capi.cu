@@ -419,7 +419,8 @@ int fsld_hvp_sorted(int M, int mode, int n_mask, const fsld_image_rec* recs, con
 }
 
 int fsld_loss_grad_hutch_sorted(int M, int mode, int n_mask, const fsld_image_rec* recs, const int32_t* idx, int B,
-                                const void* v, const void* xs, const int8_t* pc, const int32_t* seg_off,
+                                const void* v, const void* xs, const int8_t* pc, const void* ptab,
+                                const int32_t* seg_off,
                                 const int32_t* segs, const uint32_t* zbits, void* grad_acc, float* fold,
                                 double* sq_out, unsigned flags, void* scratch, size_t scratch_bytes, void* stream) {
     if (!geom_ok(M, mode, n_mask, B) || M > 256 || mode != FSLD_MODE_TRI) return FSLD_EINVAL;
@@ -428,7 +429,7 @@ int fsld_loss_grad_hutch_sorted(int M, int mode, int n_mask, const fsld_image_re
         return FSLD_EINVAL;
     const ScratchLayout L = scratch_layout(M, n_mask, B);
     if (scratch_bytes < L.total) return FSLD_EINVAL;
-    SortedArgs b = make_sorted(L, M, n_mask, B, recs, idx, v, xs, pc, seg_off, segs, grad_acc, scratch);
+    SortedArgs b = make_sorted(L, M, n_mask, B, recs, idx, v, xs, pc, seg_off, segs, grad_acc, scratch, ptab);
     b.zbits = zbits;
     b.fold = fold;
     note_bins(scratch, idx, recs, M, n_mask, B);

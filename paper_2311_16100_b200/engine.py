@@ -284,8 +284,8 @@ class SliceEngine:
         scr = self.scratch(B)
         C.check(lib.fsld_loss_grad_hutch_sorted(self.M, self.mode_id, self.n_mask, ctypes_ptr(self.recs),
                                                 ctypes_ptr(idx), B, ctypes_ptr(v), ctypes_ptr(self.x),
-                                                ctypes_ptr(self.pc), ctypes_ptr(self.seg_off), ctypes_ptr(self.segs),
-                                                ctypes_ptr(zbits), ctypes_ptr(acc), ctypes_ptr(fold), ctypes_ptr(sq),
+                                                ctypes_ptr(self.pc), ctypes_ptr(self.ptab), ctypes_ptr(self.seg_off),
+                                                ctypes_ptr(self.segs), ctypes_ptr(zbits), ctypes_ptr(acc), ctypes_ptr(fold), ctypes_ptr(sq),
                                                 0, ctypes_ptr(scr), scr.numel() * 8, _stream()),
                 "fsld_loss_grad_hutch_sorted")
         return sq
