@@ -701,6 +701,23 @@ cudaError_t launch_planned_loss_grad(const SortedArgs& a, double* sq_out, cudaSt
 // finalize of sq and the loss.  a.acc = grad, a.v = v.
 cudaError_t launch_planned_loss_grad_step(SortedArgs a, int64_t nvox, double scale, double lam, double* sq_out,
                                           double* loss, double* norm_part, int n_norm, cudaStream_t s) {
+    if (a.ptab && !a.nn) {  // the table-driven kernel does the whole step in one launch
+        int grid = 0;
+        cudaError_t e = v3_grid<false, false>(grid);
+        if (e != cudaSuccess) return e;
+        if (grid > n_norm) return cudaErrorInvalidValue;
+        e = cudaMemsetAsync(a.ctl + 1, 0, sizeof(int), s);  // re-arm the claim counter (any earlier use)
+        if (e != cudaSuccess) return e;
+        a.out_scale = (float)scale;
+        a.fuse = 1;
+        a.flam = (float)lam;
+        a.fscale = scale;
+        a.fnorm = norm_part;
+        a.fsq = sq_out;
+        a.floss = loss;
+        brick_loss_grad_kernel<false, false><<<grid, BTHREADS, sizeof(BrickSmem3), s>>>(a);
+        return cudaGetLastError();
+    }
     cudaError_t e = launch_grad_init(nvox, a.v, lam, a.acc, norm_part, n_norm, s);
     if (e != cudaSuccess) return e;
     e = cudaMemsetAsync(a.ctl + 1, 0, sizeof(int), s);

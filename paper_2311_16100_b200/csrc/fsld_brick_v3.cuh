@@ -143,6 +143,27 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
     __syncthreads();
     int4 item = S.item_desc;
     if (item.x >= 0) stage_item3(item);
+    bool init_seen = !a.fuse;
+    if (a.fuse) {  // this CTA's slice of acc = lam v, ||v||^2 partial; then count the slice as written
+        const int64_t n = (int64_t)M * M * M;
+        const int64_t lo = n * blockIdx.x / gridDim.x, hi = n * (blockIdx.x + 1) / gridDim.x;
+        double s2 = 0.0;
+        for (int64_t j = lo + threadIdx.x; j < hi; j += BTHREADS) {
+            const float2 w = __ldg(a.v + j);
+            a.acc[j] = make_float2(a.flam * w.x, a.flam * w.y);
+            s2 += (double)fmaf(w.x, w.x, w.y * w.y);
+        }
+        for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+        if (lane == 0) S.red[warp] = s2;
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int w = 0; w < BW; ++w) t += S.red[w];
+            a.fnorm[blockIdx.x] = t;
+            atomicAdd(a.ctl + 6, 1);
+        }
+    }
 
     for (;;) {
         if (item.x < 0) break;
@@ -362,6 +383,13 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
             }
             __syncthreads();
         }
+        if (!init_seen) {  // (fused step) every CTA's slice of acc = lam v is in place before the first add
+            if (threadIdx.x == 0)
+                while (*reinterpret_cast<volatile int*>(a.ctl + 6) < (int)gridDim.x) __nanosleep(64);
+            __syncthreads();
+            __threadfence();
+            init_seen = true;
+        }
         // flush of the item: one reduction per touched voxel, accumulators re-zeroed
 #pragma unroll
         for (int u = 0; u < BU; ++u) {
@@ -394,5 +422,31 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
         double s = 0.0;
         for (int w = 0; w < BW; ++w) s += S.red[w];
         a.part[blockIdx.x] = s;
+    }
+    if (a.fuse) {  // the last CTA: sq and the loss in a fixed order, counters re-armed for the next step
+        __shared__ bool last;
+        if (threadIdx.x == 0) {
+            __threadfence();
+            last = atomicAdd(a.ctl + 7, 1) == (int)gridDim.x - 1;
+        }
+        __syncthreads();
+        if (last && warp == 0) {
+            __threadfence();
+            double q = 0.0, v2 = 0.0;
+            for (int b = lane; b < (int)gridDim.x; b += 32) {
+                q += reinterpret_cast<volatile double*>(a.part)[b];
+                v2 += reinterpret_cast<volatile double*>(a.fnorm)[b];
+            }
+            for (int o = 16; o > 0; o >>= 1) {
+                q += __shfl_xor_sync(0xffffffffu, q, o);
+                v2 += __shfl_xor_sync(0xffffffffu, v2, o);
+            }
+            if (lane == 0) {
+                *a.fsq = q;
+                *a.floss = 0.5 * a.fscale * q + 0.5 * (double)a.flam * v2;
+                a.ctl[6] = 0;
+                a.ctl[7] = 0;
+            }
+        }
     }
 }
