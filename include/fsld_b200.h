@@ -474,6 +474,15 @@ int fsld_loss_grad_host(int M, int mode, int n_mask, const fsld_image_rec* recs,
                         const int32_t* seg_off, const int32_t* segs, double scale, double lam, void* grad_host, double* out_host,
                         void* v_dev, void* grad_dev, int32_t* idx_dev, int n_slabs, void* scratch,
                         size_t scratch_bytes, void* stream);
+/* fsld_loss_grad_host with the gradient delivered as complex128 (the reference's dtype, optim.py:190):
+ * grad_host_c128 is a page-locked M^3 complex128 host buffer; each finished slab is cast on the device
+ * into grad_dev128 (device staging, M^3 complex128) and copied out from there, so the host never casts
+ * the gradient.  v_host stays complex64. */
+int fsld_loss_grad_host_c128(int M, int mode, int n_mask, const fsld_image_rec* recs, const int32_t* idx_host, int B,
+                             const void* v_host, const void* xs, const int8_t* pc, const void* ptab,
+                             const int32_t* seg_off, const int32_t* segs, double scale, double lam,
+                             void* grad_host_c128, double* out_host, void* v_dev, void* grad_dev, void* grad_dev128,
+                             int32_t* idx_dev, int n_slabs, void* scratch, size_t scratch_bytes, void* stream);
 int fsld_proj_energy_planned(int M, int mode, int n_mask, const fsld_image_rec* recs, const void* plan, int B, int k,
                              const void* d, const int8_t* pc, double* out, void* scratch, size_t scratch_bytes,
                              void* stream);

@@ -871,7 +871,7 @@ namespace {
 struct HostStepKey {
     int M, n_mask, B, n_slabs;
     const void *recs, *v_host, *xs, *pc, *ptab, *seg_off, *segs, *grad_host, *out_host, *v_dev, *grad_dev,
-        *idx_dev, *scratch;
+        *idx_dev, *scratch, *grad_dev128;  // grad_dev128 != NULL: grad_host is complex128
     double scale, lam;
     bool operator==(const HostStepKey& o) const { return std::memcmp(this, &o, sizeof(*this)) == 0; }
 };
@@ -963,9 +963,18 @@ cudaError_t host_step_enqueue(const HostStepKey& k, HostPipe* P, const int32_t* 
         FSLD_TRY(cudaEventRecord(P->ek[g], ks));
         FSLD_TRY(cudaStreamWaitEvent(P->d2h, P->ek[g], 0));
         if (g > 0) FSLD_TRY(cudaStreamWaitEvent(P->d2h, P->ek[g - 1], 0));
-        for (int q = 0; q < np[g]; ++q)
-            FSLD_TRY(cudaMemcpyAsync(gh + zi0[g][q] * plane, gd + zi0[g][q] * plane, nz[g][q] * plane,
-                                     cudaMemcpyDeviceToHost, P->d2h));
+        for (int q = 0; q < np[g]; ++q) {
+            if (k.grad_dev128) {  // complex128 out: cast the finished slab on the device, copy 16 B / voxel
+                char* g128 = reinterpret_cast<char*>(const_cast<void*>(k.grad_dev128));
+                FSLD_TRY(launch_cast_c64_c128((int64_t)nz[g][q] * M * M, gd + zi0[g][q] * plane,
+                                              g128 + 2 * zi0[g][q] * plane, P->d2h));
+                FSLD_TRY(cudaMemcpyAsync(gh + 2 * zi0[g][q] * plane, g128 + 2 * zi0[g][q] * plane,
+                                         2 * nz[g][q] * plane, cudaMemcpyDeviceToHost, P->d2h));
+            } else {
+                FSLD_TRY(cudaMemcpyAsync(gh + zi0[g][q] * plane, gd + zi0[g][q] * plane, nz[g][q] * plane,
+                                         cudaMemcpyDeviceToHost, P->d2h));
+            }
+        }
     }
     for (int q = 0; q < 2 && q < G; ++q) FSLD_TRY(cudaStreamWaitEvent(s, P->ek[G - 1 - q], 0));
     FSLD_TRY(cudaEventRecord(P->join, P->d2h));
@@ -1057,12 +1066,11 @@ extern "C" int fsld_host_step_reset(void) {
     return FSLD_OK;
 }
 
-extern "C" int fsld_loss_grad_host(int M, int mode, int n_mask, const fsld_image_rec* recs, const int32_t* idx_host,
-                                   int B, const void* v_host, const void* xs, const int8_t* pc, const void* ptab,
-                                   const int32_t* seg_off,
-                                   const int32_t* segs, double scale, double lam, void* grad_host, double* out_host,
-                                   void* v_dev, void* grad_dev, int32_t* idx_dev, int n_slabs, void* scratch,
-                                   size_t scratch_bytes, void* stream) {
+static int loss_grad_host_impl(int M, int mode, int n_mask, const fsld_image_rec* recs, const int32_t* idx_host,
+                               int B, const void* v_host, const void* xs, const int8_t* pc, const void* ptab,
+                               const int32_t* seg_off, const int32_t* segs, double scale, double lam,
+                               void* grad_host, double* out_host, void* v_dev, void* grad_dev, int32_t* idx_dev,
+                               int n_slabs, void* scratch, size_t scratch_bytes, void* stream, void* grad_dev128) {
     if (!geom_ok(M, mode, n_mask, B) || M > 256 || mode != FSLD_MODE_TRI) return FSLD_EINVAL;
     if (!recs || !idx_host || !v_host || !xs || !pc || !seg_off || !segs || !grad_host || !out_host || !v_dev ||
         !grad_dev || !idx_dev || !scratch || v_dev == grad_dev || n_slabs < 1 || n_slabs > kMaxSlabs)
@@ -1087,6 +1095,7 @@ extern "C" int fsld_loss_grad_host(int M, int mode, int n_mask, const fsld_image
     k.out_host = out_host;
     k.v_dev = v_dev;
     k.grad_dev = grad_dev;
+    k.grad_dev128 = grad_dev128;
     k.idx_dev = idx_dev;
     k.scratch = scratch;
     k.scale = scale;
@@ -1110,4 +1119,27 @@ extern "C" int fsld_loss_grad_host(int M, int mode, int n_mask, const fsld_image
     if ((e = cudaGraphLaunch(h->exec, s)) != cudaSuccess) return status_of(e);
     note_bins(scratch, idx_dev, recs, M, n_mask, B);
     return status_of(cudaEventRecord(h->done, s));
+}
+
+extern "C" int fsld_loss_grad_host(int M, int mode, int n_mask, const fsld_image_rec* recs, const int32_t* idx_host,
+                                   int B, const void* v_host, const void* xs, const int8_t* pc, const void* ptab,
+                                   const int32_t* seg_off, const int32_t* segs, double scale, double lam,
+                                   void* grad_host, double* out_host, void* v_dev, void* grad_dev, int32_t* idx_dev,
+                                   int n_slabs, void* scratch, size_t scratch_bytes, void* stream) {
+    return loss_grad_host_impl(M, mode, n_mask, recs, idx_host, B, v_host, xs, pc, ptab, seg_off, segs, scale, lam,
+                               grad_host, out_host, v_dev, grad_dev, idx_dev, n_slabs, scratch, scratch_bytes, stream,
+                               nullptr);
+}
+
+extern "C" int fsld_loss_grad_host_c128(int M, int mode, int n_mask, const fsld_image_rec* recs,
+                                        const int32_t* idx_host, int B, const void* v_host, const void* xs,
+                                        const int8_t* pc, const void* ptab, const int32_t* seg_off,
+                                        const int32_t* segs, double scale, double lam, void* grad_host_c128,
+                                        double* out_host, void* v_dev, void* grad_dev, void* grad_dev128,
+                                        int32_t* idx_dev, int n_slabs, void* scratch, size_t scratch_bytes,
+                                        void* stream) {
+    if (!grad_dev128 || grad_dev128 == v_dev || grad_dev128 == grad_dev) return FSLD_EINVAL;
+    return loss_grad_host_impl(M, mode, n_mask, recs, idx_host, B, v_host, xs, pc, ptab, seg_off, segs, scale, lam,
+                               grad_host_c128, out_host, v_dev, grad_dev, idx_dev, n_slabs, scratch, scratch_bytes,
+                               stream, grad_dev128);
 }

@@ -110,4 +110,21 @@ cudaError_t launch_ctf_ring_power(const fsld_image_rec* recs, int N, const short
     return cudaGetLastError();
 }
 
+// complex64 -> complex128 (the numpy call path's gradient: cast on the device, copied out as complex128
+// straight into the caller's array, so the host never casts it)
+__global__ void cast_c64_c128_kernel(int64_t n, const float2* __restrict__ src, double2* __restrict__ dst) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const float2 z = src[i];
+        dst[i] = make_double2((double)z.x, (double)z.y);
+    }
+}
+
+cudaError_t launch_cast_c64_c128(int64_t n, const void* src, void* dst, cudaStream_t s) {
+    if (n < 1) return cudaSuccess;
+    const int64_t blocks = (n + 255) / 256;
+    cast_c64_c128_kernel<<<(int)(blocks < 148 * 16 ? blocks : 148 * 16), 256, 0, s>>>(
+        n, reinterpret_cast<const float2*>(src), reinterpret_cast<double2*>(dst));
+    return cudaGetLastError();
+}
+
 }  // namespace fsld

@@ -362,6 +362,8 @@ class SliceEngine:
 
     def loss_grad_host(self, v_host, idx_host, scale: float, lam: float, grad_host, out_host,
                        stage: dict, n_slabs: int | None = None) -> None:
+        """(grad_host complex128: fsld_loss_grad_host_c128, the gradient cast on the device; ``stage``
+        then also holds "g128", an M^3 complex128 device staging tensor)"""
         """fsld_loss_grad_host: pinned host v / idx in, pinned host grad and out_host = [sq, loss]
         written once the current stream is synchronised.  The copies run slab by slab on the
         library's own copy streams, overlapping each other and the brick passes.  ``stage``
@@ -369,10 +371,12 @@ class SliceEngine:
         lib = C.load()
         if not self.brick_path:
             raise ValueError("the host step runs the brick path (tri, sorted, non-deterministic)")
+        c128 = grad_host.dtype == torch.complex128
         for t, n in ((v_host, self.n_voxels), (grad_host, self.n_voxels)):
-            if t.device.type != "cpu" or not t.is_pinned() or t.dtype != torch.complex64 or t.numel() != n \
-                    or not t.is_contiguous():
-                raise ValueError("v_host / grad_host must be pinned contiguous complex64 host tensors of M^3")
+            if t.device.type != "cpu" or not t.is_pinned() or t.numel() != n or not t.is_contiguous() or \
+                    t.dtype != (torch.complex128 if (t is grad_host and c128) else torch.complex64):
+                raise ValueError("v_host / grad_host must be pinned contiguous host tensors of M^3 (v complex64, "
+                                 "grad complex64 or complex128)")
         if idx_host.device.type != "cpu" or not idx_host.is_pinned() or idx_host.dtype != torch.int32:
             raise ValueError("idx_host must be a pinned int32 host tensor")
         B = int(idx_host.numel())
@@ -383,6 +387,17 @@ class SliceEngine:
         scr = self.scratch(B)
         if stage["idx"].numel() < B:
             stage["idx"] = torch.empty(B, dtype=torch.int32, device=self.dev)
+        if c128:
+            if stage.get("g128") is None:
+                stage["g128"] = torch.empty(self.n_voxels, dtype=torch.complex128, device=self.dev)
+            C.check(lib.fsld_loss_grad_host_c128(
+                self.M, self.mode_id, self.n_mask, ctypes_ptr(self.recs), ctypes_ptr(idx_host), B, ctypes_ptr(v_host),
+                ctypes_ptr(self.x), ctypes_ptr(self.pc), ctypes_ptr(self.ptab), ctypes_ptr(self.seg_off),
+                ctypes_ptr(self.segs), float(scale), float(lam), ctypes_ptr(grad_host), ctypes_ptr(out_host),
+                ctypes_ptr(stage["v"]), ctypes_ptr(stage["g"]), ctypes_ptr(stage["g128"]), ctypes_ptr(stage["idx"]),
+                int(n_slabs or self.HOST_SLABS), ctypes_ptr(scr), scr.numel() * 8, _stream()),
+                "fsld_loss_grad_host_c128")
+            return
         C.check(lib.fsld_loss_grad_host(self.M, self.mode_id, self.n_mask, ctypes_ptr(self.recs),
                                         ctypes_ptr(idx_host), B, ctypes_ptr(v_host), ctypes_ptr(self.x),
                                         ctypes_ptr(self.pc), ctypes_ptr(self.ptab), ctypes_ptr(self.seg_off),

@@ -466,21 +466,20 @@ class DatasetOperator:
     def loss_and_grad_numpy(self, v, batch, lam: float, n_total: int | None = None):
         """optim.loss_and_grad with the reference's argument types (numpy complex128 v in, (float,
         complex128 gradient) out; optim.py:165-190) on the brick path: v is cast into a pinned
-        complex64 buffer (fsld_host_cast_*: streaming stores, host thread pool), fsld_loss_grad_host
-        moves it slab by slab while the brick passes run and streams the complex64 gradient
-        (scale * sum + lam v, formed on the device) back, and the gradient is cast into a fresh
-        complex128 array.  Accuracy: the fp32 path (1e-7 relative
-        from the complex64 v and gradient)."""
+        complex64 buffer (fsld_host_cast_*: streaming stores, host thread pool), fsld_loss_grad_host_c128
+        moves it slab by slab while the brick passes run, forms scale * sum + lam v on the device, casts
+        each finished slab to complex128 there and copies it straight into the returned array (a
+        recycled page-locked buffer).  Accuracy: the fp32 path (1e-7 relative)."""
         from . import _capi as C
-        from .hostio import cast_native
+        from .hostio import PinnedArrays, cast_native
 
         e = self.engine
         n = e.n_voxels
         st = getattr(self, "_np_stage", None)
         if st is None:  # cudaHostAlloc staging (the copy engines stream it at full PCIe rate)
-            v64 = C.host_empty(n, torch.complex64)
-            g64 = C.host_empty(n, torch.complex64)
-            st = self._np_stage = {"v": v64, "g": g64, "idx": torch.empty(0, dtype=torch.int32)}
+            st = self._np_stage = {"v": C.host_empty(n, torch.complex64), "g": C.host_empty(n, torch.complex64),
+                                   "idx": torch.empty(0, dtype=torch.int32),
+                                   "out": PinnedArrays(n, torch.complex128)}
         b = np.asarray(batch).reshape(-1)
         if b.size == 0:
             raise ValueError("batch must be nonempty")
@@ -491,10 +490,14 @@ class DatasetOperator:
         vin = np.ascontiguousarray(v, dtype=np.complex128).reshape(-1)
         if vin.size != n:
             raise ValueError(f"volume has {vin.size} entries, expected {n}")
-        # streaming-store casts on the host thread pool: the staged volume is clean in DRAM for the
-        # copy engine
+        # streaming-store cast on the host thread pool: the staged volume is clean in DRAM for the copy engine
         cast_native(lib.fsld_host_cast_f64_to_f32, vin.ctypes.data, st["v"].data_ptr(), 2 * n, 8, 4)
-        loss = self.loss_and_grad_host(st["v"], st["idx"], lam, st["g"], n_total)
+        out = st["out"].get()
+        if out is not None:  # complex128 straight from the device into a recycled pinned array
+            grad, gt = out
+            loss = self.loss_and_grad_host(st["v"], st["idx"], lam, gt, n_total)
+            return loss, grad
+        loss = self.loss_and_grad_host(st["v"], st["idx"], lam, st["g"], n_total)  # (many results held)
         grad = np.empty(n, dtype=np.complex128)
         cast_native(lib.fsld_host_cast_f32_to_f64, st["g"].data_ptr(), grad.ctypes.data, 2 * n, 4, 8)
         return loss, grad

@@ -57,3 +57,31 @@ def cast_native(fn, src_ptr: int, dst_ptr: int, n: int, src_item: int, dst_item:
     for f in futs:
         if f.result() != 0:
             raise ValueError("host cast failed")
+
+
+class PinnedArrays:
+    """Recycled page-locked numpy arrays for results handed to the caller (the numpy call path's
+    complex128 gradients).  The copy engine writes them directly (no host cast, no first-touch page
+    faults of a fresh array); an array goes back to the pool when the caller drops it."""
+
+    def __init__(self, n: int, dtype, keep: int = 8):
+        self.n, self.dtype, self.keep = int(n), dtype, keep
+        self.free: list = []
+        self.live = 0
+
+    def get(self):
+        """(numpy array, backing pinned tensor) -- None when `keep` arrays are already out."""
+        import weakref
+
+        import torch
+        from . import _capi as C
+        if self.free:
+            t = self.free.pop()
+        elif self.live < self.keep:
+            t = C.host_empty(self.n, self.dtype)
+            self.live += 1
+        else:
+            return None
+        arr = t.numpy()
+        weakref.finalize(arr, self.free.append, t)
+        return arr, t
