@@ -72,9 +72,16 @@ struct Pix3 {  // one pixel's inputs in registers
 
 __device__ __forceinline__ void load_pix3(const SortedArgs& a, const float2* tf, const float4* tg, long long g,
                                           bool has_x, Pix3& p) {
+#ifdef FSLD_EXP_NO_LOADS  // ablation (results wrong by construction): no pixel stream from HBM
+    const float t = (float)(g & 1023) * 1e-3f;
+    p.f = make_float2(t, 1.f - t);
+    p.geo = make_float4(t, 0.5f * t, 1.f - t, __int_as_float((int)(g & 511)));
+    p.x = make_float2(t, t);
+#else
     p.f = __ldg(tf + g);
     p.geo = __ldg(tg + g);
     p.x = has_x ? __ldg(a.xs + g) : make_float2(0.f, 0.f);
+#endif
 }
 
 // Per work item (brick, <= BC image segments), as sorted_loss_grad_kernel; per round of RB3 pixels:
@@ -242,10 +249,16 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
                     pv = vb[0];
                 } else {
                     const float2 WX = make_float2(wx, wx), AX = make_float2(ax, ax);
+#ifdef FSLD_EXP_ONE_GATHER  // ablation (results wrong by construction): one corner gather per pixel
+                    const float2 g0 = vb[0];
+                    const float2 e0 = __ffma2_rn(WX, g0, __fmul2_rn(AX, g0));
+                    const float2 e1 = __fmul2_rn(AX, e0), e2 = __fmul2_rn(WX, e0), e3 = __fmul2_rn(WX, e1);
+#else
                     const float2 e0 = __ffma2_rn(WX, vb[1], __fmul2_rn(AX, vb[0]));
                     const float2 e1 = __ffma2_rn(WX, vb[BH + 1], __fmul2_rn(AX, vb[BH]));
                     const float2 e2 = __ffma2_rn(WX, vb[BH * BH + 1], __fmul2_rn(AX, vb[BH * BH]));
                     const float2 e3 = __ffma2_rn(WX, vb[BH * BH + BH + 1], __fmul2_rn(AX, vb[BH * BH + BH]));
+#endif
                     const float2 q0 = __ffma2_rn(make_float2(wy, wy), e1, __fmul2_rn(make_float2(ay, ay), e0));
                     const float2 q1 = __ffma2_rn(make_float2(wy, wy), e3, __fmul2_rn(make_float2(ay, ay), e2));
                     pv = __ffma2_rn(make_float2(wz, wz), q1, __fmul2_rn(make_float2(az, az), q0));
@@ -345,7 +358,11 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
                 if (sync) __syncthreads();  // (uniform: every thread read the same maxima)
             }
             const float sc = item_sc;
+#ifdef FSLD_EXP_NO_PASS2  // ablation (results wrong by construction): no pass 2
+            const int rn = 0;
+#else
             const int rn = r1 - r0;
+#endif
             for (int e = threadIdx.x; e < rn; e += BTHREADS) {
                 const uint4 rec = S.brec[e];
                 const int l0 = (int)(rec.z & 1023u);
@@ -367,8 +384,12 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
                     const float2 y = __ffma2_rn(make_float2(w8[q], w8[q]), val, make_float2(kMagic, kMagic));
+#ifdef FSLD_EXP_NO_ATOMS  // ablation (results wrong by construction): one shared add per pixel
+                    if (q == 0) atomicAdd(S.accr + l0, (__float_as_int(y.x) - kMagicBits) ^ (__float_as_int(y.y) - kMagicBits));
+#else
                     atomicAdd(S.accr + l0 + off8[q], __float_as_int(y.x) - kMagicBits);
                     atomicAdd(S.acci + l0 + off8[q], __float_as_int(y.y) - kMagicBits);
+#endif
                 }
                 if (HUTCH) {
                     const float h = S.hval[e] * item_sch;

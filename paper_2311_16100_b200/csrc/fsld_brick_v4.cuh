@@ -1,0 +1,489 @@
+// fsld_brick_v4.cuh -- the TMA-staged, bank-slotted brick kernel of the fused loss+gradient
+// (included by fsld_brick.cu).  Trilinear slicing (kernels.py:138-177) and its adjoint
+// (kernels.py:193-230) with the CTF / shift factor and the residual fused in (optim.py:147-190).
+//
+// Same work items, dataset tables (fsld_brick_tables.cuh) and fixed-point adjoint as the
+// table-driven kernel (fsld_brick_v3.cuh); what changes is how pixels reach the threads and the
+// order of the shared-memory scatter:
+//   * rounds are whole segments (a segment belongs to round floor(P / RB4), P its padded start in
+//     the item), staged into shared memory by cp.async.bulk (TMA, one copy per segment and array:
+//     image values, f, footprints) one round ahead, double buffered and tracked by an mbarrier per
+//     buffer -- no per-pixel global load, address arithmetic or pixel -> segment lookup, and the
+//     HBM latency is hidden by the copy engine instead of by register prefetch.  8-byte arrays are
+//     copied as their 16-byte aligned superset (a segment is padded to an even start and length);
+//     a per-round bit mask (built with the item's metadata) marks the real pixels;
+//   * pass 1 (gather, residual, conj(f) r) writes conj(f) r in place over the image value (the
+//     footprint stays where it was staged) and files the pixel under (rank, bank) with bank =
+//     corner index mod 16: a warp-aggregated rank (match.any) and one conflict-free ATOMS per
+//     (warp, bank);
+//   * pass 2 walks the slots level by level: a warp instruction covers two levels, lanes 0-15 one
+//     and lanes 16-31 the next, each half with 16 distinct banks mod 16.  The fixed-point
+//     accumulator is (re, im) interleaved, and the half-warps add opposite components first, so
+//     the first half hits even banks and the second odd banks: every one of the 16 ATOMS per pixel
+//     is conflict-free (measured: 1.0 cycle per ATOMS against 2.9 for the pixel order of the
+//     round-1 / v3 kernels, tools/micro/smem_tput.cu).  Ranks past LCAP4 go to an overflow list.
+#pragma once
+
+#ifndef FSLD_RB4
+#define FSLD_RB4 512
+#endif
+#ifndef FSLD_LCAP4
+#define FSLD_LCAP4 64
+#endif
+#ifndef FSLD_V4_MINB
+#define FSLD_V4_MINB 3
+#endif
+constexpr int RB4 = FSLD_RB4;                     // round positions (segments are assigned by start)
+constexpr int SEGP4 = kSegMax + 2;                // padded length bound of one segment
+constexpr int CAP4 = RB4 + SEGP4 - 2;             // positions one round can span
+constexpr int NB4 = 16;                           // bank keys
+constexpr int LCAP4 = FSLD_LCAP4;                 // slotted levels per bank
+constexpr int MAXR4 = (BC * SEGP4) / RB4 + 2;     // rounds per item (+1)
+constexpr int MW4 = (CAP4 + 31) / 32;             // mask words per round
+constexpr int IT4 = (CAP4 + BTHREADS - 1) / BTHREADS;  // pass-1 positions per thread
+static_assert((RB4 & (RB4 - 1)) == 0 && RB4 >= 2 * SEGP4, "RB4: power of two, >= two segments");
+
+struct ItemMeta4 {
+    long long g[BC];   // segment offsets in the dataset order (xs / table index)
+    int n[BC];         // pixels
+    int P[BC + 1];     // exclusive prefix of the padded lengths ((g & 1) + n rounded up to even)
+    int rs[MAXR4 + 1]; // first segment of each round
+    unsigned rbytes[MAXR4];      // bytes the round's bulk copies deliver (expect_tx)
+    unsigned mask[MAXR4][MW4];   // real pixels of each round (position bits)
+    int tailk;         // segment whose image values end at the array end (copied by hand), or -1
+    int nseg, nrounds, bid;
+};
+
+struct __align__(16) BrickSmem4 {
+    float4 geo[2][CAP4];      // staged footprints; pass 1 overwrites with (conj(f) r, packed footprint)
+    float2 xs[2][CAP4];       // staged image values
+    float2 fs[2][CAP4];       // staged f = C * phase
+    float2 vb[2][BH3];        // v brick + halo, by item parity
+    int2 acc[BH3];            // fixed-point adjoint accumulator, (re, im) interleaved
+    unsigned short sidx[NB4 * LCAP4];  // slot (level, bank) -> position
+    unsigned short olist[CAP4];        // overflow positions (rank >= LCAP4)
+    ItemMeta4 meta[3];        // current item, the next, and the one after (built one item ahead)
+    unsigned long long full[2];  // mbarriers: round staged in buffer b
+    int bcnt[2][NB4];         // per-bank pixel counts, by round parity
+    int ocnt[2];
+    int vmax2[2];
+    int claim;
+    double red[BW];
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(unsigned long long* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "W4_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra W4_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// Work-item metadata (one warp): the pair records, padded lengths and their prefix, round starts.
+__device__ __forceinline__ void build_meta4(const SortedArgs& a, int4 item, ItemMeta4& m, int lane, long long npx) {
+    if (item.x < 0) {
+        if (lane == 0) m.bid = -1;
+        __syncwarp();
+        return;
+    }
+    const int nseg = item.z;
+    const bool has_x = a.xs != nullptr;
+    for (int w = lane; w < MAXR4 * MW4; w += 32) (&m.mask[0][0])[w] = 0u;
+    if (lane < MAXR4) m.rbytes[lane] = 0u;
+    if (lane == 0) m.tailk = -1;
+    __syncwarp();
+    int carry = 0, rprev = -1;
+#pragma unroll
+    for (int half = 0; half < BC / 32; ++half) {
+        const int k = half * 32 + lane;
+        long long g = 0;
+        int n = 0, len = 0;
+        if (k < nseg) {
+            const int4 pr = __ldg(reinterpret_cast<const int4*>(a.pairs + item.y + k));  // gofs lo, hi, count, tslot
+            g = (long long)(((unsigned long long)(unsigned)pr.y << 32) | (unsigned)pr.x);
+            n = pr.z;
+            len = ((int)(g & 1) + n + 1) & ~1;
+        }
+        int incl = len;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        const int P = carry + incl - len;
+        const int rk = k < nseg ? P / RB4 : 0x7fffffff;
+        int rp = __shfl_up_sync(0xffffffffu, rk, 1);
+        if (lane == 0) rp = rprev;
+        if (k < nseg) {
+            m.g[k] = g;
+            m.n[k] = n;
+            m.P[k] = P;
+            if (rk != rp) m.rs[rk] = k;
+            const int h = (int)(g & 1);
+            int xlen = len;
+            if (has_x && g - h + len > npx) {  // the dataset's last segment: no 16-byte superset past the end
+                xlen = len - 2;
+                m.tailk = k;
+            }
+            atomicAdd(&m.rbytes[rk], (has_x ? 8u * (uint32_t)xlen : 0u) + 8u * (uint32_t)len + 16u * (uint32_t)n);
+        }
+        rprev = __shfl_sync(0xffffffffu, rk, 31);
+        carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    __syncwarp();
+    for (int k = lane; k < nseg; k += 32) {  // the real pixels of each segment in its round's mask
+        const int rk = m.P[k] / RB4;
+        const int lo = m.P[k] - m.P[m.rs[rk]] + (int)(m.g[k] & 1), hi = lo + m.n[k];
+        for (int w = lo >> 5; w <= (hi - 1) >> 5; ++w) {
+            const int a0 = max(lo - 32 * w, 0), a1 = min(hi - 32 * w, 32);
+            const unsigned bits = (a1 - a0 == 32) ? 0xffffffffu : (((1u << (a1 - a0)) - 1u) << a0);
+            atomicOr(&m.mask[rk][w], bits);
+        }
+    }
+    if (lane == 0) {
+        m.P[nseg] = carry;
+        const int nr = m.P[nseg - 1] / RB4 + 1;
+        m.rs[nr] = nseg;
+        m.nrounds = nr;
+        m.nseg = nseg;
+        m.bid = item.x;
+    }
+    __syncwarp();
+}
+
+// Stage round r of item m into buffer b: thread 0 arms the mbarrier with the round's byte count
+// (and copies by hand the image values of the dataset's final segment that a 16-byte superset
+// would overrun), thread t < segments issues segment s0 + t's three bulk copies (a copy may land
+// before the expect_tx: the transaction count of the phase goes negative, never complete).
+__device__ __forceinline__ void issue_round4(const SortedArgs& a, BrickSmem4& S, const ItemMeta4& m, int r, int b,
+                                             const float2* tf, const float4* tg) {
+    const int s0 = m.rs[r], s1 = m.rs[r + 1];
+    const int base = m.P[s0];
+    const bool has_x = a.xs != nullptr;
+    if (threadIdx.x == 0) {
+        const int k = m.tailk;
+        if (k >= s0 && k < s1) {
+            const long long g = m.g[k];
+            const int n = m.n[k], h = (int)(g & 1), p = m.P[k] - base, len = m.P[k + 1] - m.P[k];
+            for (int q = len - 2; q < len; ++q)
+                if (q - h >= 0 && q - h < n) S.xs[b][p + q] = __ldg(a.xs + g + (q - h));
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive_tx(&S.full[b], m.rbytes[r]);
+    }
+    const int k = s0 + (int)threadIdx.x;
+    if (k < s1) {
+        const long long g = m.g[k];
+        const int n = m.n[k], h = (int)(g & 1), p = m.P[k] - base, len = m.P[k + 1] - m.P[k];
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        bulk_g2s(&S.fs[b][p], tf + (g - h), 8u * (uint32_t)len, &S.full[b]);
+        bulk_g2s(&S.geo[b][p + h], tg + g, 16u * (uint32_t)n, &S.full[b]);
+        if (has_x) {
+            const int xlen = k == m.tailk ? len - 2 : len;
+            if (xlen > 0) bulk_g2s(&S.xs[b][p], a.xs + (g - h), 8u * (uint32_t)xlen, &S.full[b]);
+        }
+    }
+}
+
+template <int DUMMY>
+__global__ void __launch_bounds__(BTHREADS, FSLD_V4_MINB) brick_loss_grad_v4_kernel(SortedArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    BrickSmem4& S = *reinterpret_cast<BrickSmem4*>(smem_raw);
+    a.pairs += a.ctl[3];
+    a.items += a.ctl[4];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int M = a.M, c = a.c, nb = a.nb;
+    const bool has_x = a.xs != nullptr;
+    const TabHeader* th = reinterpret_cast<const TabHeader*>(a.ptab);
+    const long long npx = th->npx;
+    const float2* tf = tab_f(a.ptab);
+    const float4* tg = tab_geo(a.ptab, npx);
+    const int n_items = a.ctl[0];
+    int lxyz[BU];
+#pragma unroll
+    for (int u = 0; u < BU; ++u) {
+        const int l = threadIdx.x + u * BTHREADS;
+        lxyz[u] = l < BH3 ? (l % BH) | (((l / BH) % BH) << 4) | ((l / (BH * BH)) << 8) : -1;
+        if (l < BH3) S.acc[l] = make_int2(0, 0);
+    }
+    auto claim = [&]() -> int4 {  // one warp (all lanes get the item)
+        int it = 0;
+        if (lane == 0) it = atomicAdd(a.ctl + 1, 1);
+        it = __shfl_sync(0xffffffffu, it, 0);
+        return it < n_items ? __ldg(a.items + it) : make_int4(-1, 0, 0, 0);
+    };
+    auto stage_vb = [&](int bid, int vpar) {  // the brick's 9^3 voxels (zero off the grid), cp.async
+        const int ox = -c + BT * (bid % nb), oy = -c + BT * ((bid / nb) % nb), oz = -c + BT * (bid / (nb * nb));
+#pragma unroll
+        for (int u = 0; u < BU; ++u) {
+            if (lxyz[u] < 0) continue;
+            const int l = threadIdx.x + u * BTHREADS;
+            const int kx = ox + (lxyz[u] & 15), ky = oy + ((lxyz[u] >> 4) & 15), kz = oz + (lxyz[u] >> 8);
+            const bool in = kx < M - c && ky < M - c && kz < M - c;
+            const int j = in ? lin_index(kx, ky, kz, M, c) : 0;
+            cp_async8_zfill(&S.vb[vpar][l], a.v + j, in);
+        }
+    };
+    if (threadIdx.x == 0) {
+        mbar_init(&S.full[0], 1);
+        mbar_init(&S.full[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (threadIdx.x < 2 * NB4) S.bcnt[threadIdx.x / NB4][threadIdx.x % NB4] = 0;
+    if (threadIdx.x < 2) {
+        S.ocnt[threadIdx.x] = 0;
+        S.vmax2[threadIdx.x] = 0;
+    }
+    if (warp == BW - 1) {
+        build_meta4(a, claim(), S.meta[0], lane, npx);
+        build_meta4(a, claim(), S.meta[1], lane, npx);
+    }
+    __syncthreads();
+    bool init_seen = !a.fuse;
+    if (S.meta[0].bid >= 0) {
+        stage_vb(S.meta[0].bid, 0);
+        issue_round4(a, S, S.meta[0], 0, 0, tf, tg);
+    }
+    if (a.fuse) {  // this CTA's slice of acc = lam v, ||v||^2 partial; then count the slice as written
+        const int64_t n = (int64_t)M * M * M;
+        const int64_t lo = n * blockIdx.x / gridDim.x, hi = n * (blockIdx.x + 1) / gridDim.x;
+        double s2 = 0.0;
+        for (int64_t j = lo + threadIdx.x; j < hi; j += BTHREADS) {
+            const float2 w = __ldg(a.v + j);
+            a.acc[j] = make_float2(a.flam * w.x, a.flam * w.y);
+            s2 += (double)fmaf(w.x, w.x, w.y * w.y);
+        }
+        for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+        if (lane == 0) S.red[warp] = s2;
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int w = 0; w < BW; ++w) t += S.red[w];
+            a.fnorm[blockIdx.x] = t;
+            atomicAdd(a.ctl + 6, 1);
+        }
+    }
+    cp_async_wait_all();
+    __syncthreads();
+
+    double lsum = 0.0;
+    int iq = 0, r = 0, vpar = 0;  // current item slot, its round, its vb buffer
+    unsigned j = 0;               // round counter (stage buffer j & 1, mbarrier phase (j >> 1) & 1)
+    float item_sc = 0.f, item_inv_sc = 1.f;
+    const int h = lane >> 4, bk = lane & 15;
+    while (S.meta[iq].bid >= 0) {
+        const ItemMeta4& m = S.meta[iq];
+        const int buf = j & 1, par = j & 1;
+        const bool last = r + 1 == m.nrounds;
+        const int nq = iq == 2 ? 0 : iq + 1;
+        // ---- prefetch: the next round into the other buffer; at an item's first round, the item
+        // after the next one; at its last round, the next item's brick
+        if (!last) issue_round4(a, S, m, r + 1, buf ^ 1, tf, tg);
+        else if (S.meta[nq].bid >= 0) issue_round4(a, S, S.meta[nq], 0, buf ^ 1, tf, tg);
+        if (r == 0 && warp == BW - 1) build_meta4(a, claim(), S.meta[nq == 2 ? 0 : nq + 1], lane, npx);
+        if (last && S.meta[nq].bid >= 0) stage_vb(S.meta[nq].bid, vpar ^ 1);
+        const int bid = m.bid, nseg = m.nseg;
+        const int L = m.P[m.rs[r + 1]] - m.P[m.rs[r]];
+        mbar_wait(&S.full[buf], (j >> 1) & 1);
+        // ---------------- pass 1: gather, residual, record in place, (rank, bank) slot
+        float vmax = 0.f, sq = 0.f;
+        const float2* vb = S.vb[vpar];
+#pragma unroll
+        for (int it = 0; it < IT4; ++it) {
+            const int e = threadIdx.x + it * BTHREADS;
+            const bool valid = e < L && ((m.mask[r][e >> 5] >> (e & 31)) & 1u);
+            int key = -1;
+            if (valid) {
+                const float4 gg = S.geo[buf][e];
+                const float2 f = S.fs[buf][e];
+                const float2 x = has_x ? S.xs[buf][e] : make_float2(0.f, 0.f);
+                const float wx = gg.x, wy = gg.y, wz = gg.z;
+                const int l0 = __float_as_int(gg.w);
+                const float ax = 1.f - wx, ay = 1.f - wy, az = 1.f - wz;
+                const float2* q = vb + l0;
+                const float2 WX = make_float2(wx, wx), AX = make_float2(ax, ax);
+                const float2 e0 = __ffma2_rn(WX, q[1], __fmul2_rn(AX, q[0]));
+                const float2 e1 = __ffma2_rn(WX, q[BH + 1], __fmul2_rn(AX, q[BH]));
+                const float2 e2 = __ffma2_rn(WX, q[BH * BH + 1], __fmul2_rn(AX, q[BH * BH]));
+                const float2 e3 = __ffma2_rn(WX, q[BH * BH + BH + 1], __fmul2_rn(AX, q[BH * BH + BH]));
+                const float2 q0 = __ffma2_rn(make_float2(wy, wy), e1, __fmul2_rn(make_float2(ay, ay), e0));
+                const float2 q1 = __ffma2_rn(make_float2(wy, wy), e3, __fmul2_rn(make_float2(ay, ay), e2));
+                const float2 pv = __ffma2_rn(make_float2(wz, wz), q1, __fmul2_rn(make_float2(az, az), q0));
+                const float2 prj = cmul(pv, f);
+                const float2 rr = make_float2(prj.x - x.x, prj.y - x.y);
+                sq = fmaf(rr.x, rr.x, fmaf(rr.y, rr.y, sq));
+                const float2 val = cmulconj(f, rr);
+                vmax = fmaxf(vmax, fmaxf(fabsf(val.x), fabsf(val.y)));
+                S.xs[buf][e] = val;  // the record: conj(f) r over the image value, the footprint kept
+                key = l0 & (NB4 - 1);
+            }
+            // warp-aggregated rank among this round's pixels of the same bank key
+            const unsigned peers = __match_any_sync(0xffffffffu, key);
+            const int leader = __ffs(peers) - 1;
+            int base = 0;
+            if (key >= 0 && lane == leader) base = atomicAdd(&S.bcnt[par][key], __popc(peers));
+            base = __shfl_sync(0xffffffffu, base, leader);
+            if (key >= 0) {
+                const int rank = base + __popc(peers & ((1u << lane) - 1u));
+                if (rank < LCAP4) S.sidx[rank * NB4 + key] = (unsigned short)e;
+                else S.olist[atomicAdd(&S.ocnt[par], 1)] = (unsigned short)e;
+            }
+        }
+        lsum += (double)sq;
+        {
+            const int vb_max = __reduce_max_sync(0xffffffffu, __float_as_int(vmax));
+            if (lane == 0) atomicMax(&S.vmax2[par], vb_max);
+        }
+        __syncthreads();  // (B1) records, slots, counts and the round maximum complete
+        {
+            const float lim = (float)min(4194303, 178956970 / nseg);
+            float inv_r;
+            const float sc_r = pow2_scale(lim, __int_as_float(S.vmax2[par]), inv_r);
+            if (r == 0) {
+                item_sc = sc_r;
+                item_inv_sc = inv_r;
+            } else if (sc_r < item_sc) {  // shift the partial sums down (rounded) to the new scale
+                const int sh = (__float_as_int(item_sc) - __float_as_int(sc_r)) >> 23;
+#pragma unroll
+                for (int u = 0; u < BU; ++u) {
+                    if (lxyz[u] < 0) continue;
+                    const int l = threadIdx.x + u * BTHREADS;
+                    int2 q = S.acc[l];
+                    if (sh >= 31) {
+                        q = make_int2(0, 0);
+                    } else {
+                        const long long half = 1ll << (sh - 1);
+                        q.x = (int)(((long long)q.x + half) >> sh);
+                        q.y = (int)(((long long)q.y + half) >> sh);
+                    }
+                    S.acc[l] = q;
+                }
+                item_sc = sc_r;
+                item_inv_sc = inv_r;
+                __syncthreads();  // (uniform: every thread read the same maximum)
+            }
+        }
+        // ---------------- pass 2: slot order, conflict-free fixed-point scatter (kernels.py:221-230)
+        {
+            const float sc = item_sc;
+            int* accw = reinterpret_cast<int*>(S.acc);
+            auto scatter = [&](int e, int hh) {
+                const float2 val = S.xs[buf][e];
+                const float4 gg = S.geo[buf][e];
+                const int l0 = __float_as_int(gg.w);
+                const float wx = gg.x, wy = gg.y, wz = gg.z;
+                const float ax = 1.f - wx, ay = 1.f - wy, az = 1.f - wz;
+                const float va = (hh ? val.y : val.x) * sc, vbv = (hh ? val.x : val.y) * sc;
+                const float zy00 = az * ay, zy10 = az * wy, zy01 = wz * ay, zy11 = wz * wy;
+                const float w8[8] = {zy00 * ax, zy00 * wx, zy10 * ax, zy10 * wx, zy01 * ax, zy01 * wx, zy11 * ax, zy11 * wx};
+                constexpr int off8[8] = {0, 1, BH, BH + 1, BH * BH, BH * BH + 1, BH * BH + BH, BH * BH + BH + 1};
+                int* pa = accw + 2 * l0 + hh;
+                int* pb = accw + 2 * l0 + (hh ^ 1);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const float2 y = __ffma2_rn(make_float2(w8[q], w8[q]), make_float2(va, vbv), make_float2(kMagic, kMagic));
+                    atomicAdd(pa + 2 * off8[q], __float_as_int(y.x) - kMagicBits);
+                    atomicAdd(pb + 2 * off8[q], __float_as_int(y.y) - kMagicBits);
+                }
+            };
+            const int cb = min(S.bcnt[par][bk], LCAP4);
+            const int lv = __reduce_max_sync(0xffffffffu, cb);
+            for (int p2 = warp; 2 * p2 < lv; p2 += BW) {
+                const int lev = 2 * p2 + h;
+                if (lev < cb) scatter(S.sidx[lev * NB4 + bk], h);
+            }
+            const int no = S.ocnt[par];
+            for (int t = threadIdx.x; t < no; t += BTHREADS) scatter(S.olist[t], 0);
+            if (threadIdx.x < NB4) S.bcnt[par ^ 1][threadIdx.x] = 0;  // the next round's slots
+            if (threadIdx.x == 0) {
+                S.vmax2[par ^ 1] = 0;
+                S.ocnt[par ^ 1] = 0;
+            }
+        }
+        if (last) cp_async_wait_all();  // (the next item's brick)
+        // order this round's in-place records (generic proxy) before the bulk copy that will refill
+        // the buffer two rounds on (async proxy)
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();                // (B2) pass 2 done: slots, counts and this buffer are free
+        if (last) {
+            if (!init_seen) {  // (fused step) every CTA's slice of acc = lam v is in place before the first add
+                if (threadIdx.x == 0)
+                    while (*reinterpret_cast<volatile int*>(a.ctl + 6) < (int)gridDim.x) __nanosleep(64);
+                __syncthreads();
+                __threadfence();
+                init_seen = true;
+            }
+            const int ox = -c + BT * (bid % nb), oy = -c + BT * ((bid / nb) % nb), oz = -c + BT * (bid / (nb * nb));
+            const float fs = item_inv_sc * a.out_scale;
+#pragma unroll
+            for (int u = 0; u < BU; ++u) {
+                if (lxyz[u] < 0) continue;
+                const int l = threadIdx.x + u * BTHREADS;
+                const int2 q = S.acc[l];
+                if ((q.x | q.y) == 0) continue;
+                S.acc[l] = make_int2(0, 0);
+                const int kx = ox + (lxyz[u] & 15), ky = oy + ((lxyz[u] >> 4) & 15), kz = oz + (lxyz[u] >> 8);
+                if (kx >= M - c || ky >= M - c || kz >= M - c) continue;
+                const size_t jv = (size_t)lin_index(kx, ky, kz, M, c);
+                red_f32x2(reinterpret_cast<float*>(a.acc) + 2 * jv, (float)q.x * fs, (float)q.y * fs);
+            }
+            iq = nq;
+            vpar ^= 1;
+            r = 0;
+        } else {
+            ++r;
+        }
+        ++j;
+    }
+    for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+    if (lane == 0) S.red[warp] = lsum;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int w = 0; w < BW; ++w) s += S.red[w];
+        a.part[blockIdx.x] = s;
+    }
+    if (a.fuse) {  // the last CTA: sq and the loss in a fixed order, counters re-armed for the next step
+        __shared__ bool last_cta;
+        if (threadIdx.x == 0) {
+            __threadfence();
+            last_cta = atomicAdd(a.ctl + 7, 1) == (int)gridDim.x - 1;
+        }
+        __syncthreads();
+        if (last_cta && warp == 0) {
+            __threadfence();
+            double q = 0.0, v2 = 0.0;
+            for (int b = lane; b < (int)gridDim.x; b += 32) {
+                q += reinterpret_cast<volatile double*>(a.part)[b];
+                v2 += reinterpret_cast<volatile double*>(a.fnorm)[b];
+            }
+            for (int o = 16; o > 0; o >>= 1) {
+                q += __shfl_xor_sync(0xffffffffu, q, o);
+                v2 += __shfl_xor_sync(0xffffffffu, v2, o);
+            }
+            if (lane == 0) {
+                *a.fsq = q;
+                *a.floss = 0.5 * a.fscale * q + 0.5 * (double)a.flam * v2;
+                a.ctl[6] = 0;
+                a.ctl[7] = 0;
+            }
+        }
+    }
+}
