@@ -749,6 +749,35 @@ def next_rows_leg(eng, wl):
     ref = torch.from_numpy(wl.v_true.astype(np.complex64)).to(dev)
     ms = timed(lambda: fsc(z, ref, shells))
     out["fsc"] = {"ms": ms, "path": "metrics.fsc (device shell bincounts, one host read)"}
+    # deterministic mode (FSLD_DETERMINISTIC) on the brick kernel: one B=512 loss+grad, against the
+    # same call without the flag (both eager, binning included)
+    if eng.ptab is not None and eng.mode == "tri":
+        from paper_2311_16100_b200 import _capi as C
+        from paper_2311_16100_b200.engine import ctypes_ptr, _stream
+
+        lib = C.load()
+        bsel = idx[:512].contiguous()
+        v5 = torch.from_numpy((wl.v_true * 0.9).astype(np.complex64)).to(dev)
+        acc64 = torch.zeros((eng.n_voxels, 2), dtype=torch.int64, device=dev)
+        accf = torch.zeros(eng.n_voxels, dtype=torch.complex64, device=dev)
+        fx = eng.fixed_scale(v5, 16 * 512, eng.x_maxabs)
+        sqd = torch.empty(1, dtype=torch.float64, device=dev)
+        scr = eng.scratch(512)
+
+        def lg(flags, acc):
+            C.check(lib.fsld_loss_grad_sorted(eng.M, eng.mode_id, eng.n_mask, ctypes_ptr(eng.recs), ctypes_ptr(bsel),
+                                              512, ctypes_ptr(v5), ctypes_ptr(eng.x), ctypes_ptr(eng.pc),
+                                              ctypes_ptr(eng.ptab), ctypes_ptr(eng.seg_off), ctypes_ptr(eng.segs),
+                                              ctypes_ptr(acc), ctypes_ptr(sqd), flags, ctypes_ptr(fx),
+                                              ctypes_ptr(scr), scr.numel() * 8, _stream()), "loss_grad_sorted")
+
+        ms_d = timed(lambda: lg(C.DETERMINISTIC, acc64))
+        ms_p = timed(lambda: lg(0, accf))
+        out["deterministic_loss_grad"] = {
+            "ms": ms_d, "images_per_s": 512 / (ms_d * 1e-3), "plain_ms": ms_p,
+            "path": "fsld_loss_grad_sorted(FSLD_DETERMINISTIC), B=512: brick-ordered items, per-brick segment "
+                    "sort, int64 fixed-point flush, per-item loss partials (bitwise independent of grid / batch "
+                    "order, tests/test_gpu_det.py); plain_ms = the same call without the flag"}
     # ingest: a synthetic FSD1 file (the reference's on-disk format: complex128 full M^2 images)
     M, ni = eng.M, 1024
     rng = np.random.default_rng(7)

@@ -44,6 +44,7 @@ ScratchLayout scratch_layout(int M, int n_mask, int B) {
     int tiles = (n_mask + kThreads * 4 - 1) / (kThreads * 4);
     long long v1parts = (long long)(B > 0 ? B : 1) * (tiles > 0 ? tiles : 1);
     L.cap_part = (int)(3 * v1parts > 8192 ? 3 * v1parts : 8192);  // 3 columns (OP_ARMIJO)
+    if (L.cap_part < L.cap_items) L.cap_part = L.cap_items;         // per-item loss partials (deterministic)
     size_t o = 0;
     L.hdr = o; o = al(o + 256);
     L.cnt = o; o = al(o + sizeof(int) * (size_t)L.nbr);
@@ -334,7 +335,7 @@ __global__ void __launch_bounds__(128) bin_sorted_kernel(SortedArgs a) {
 // work-item kernels read their pairs at pairs + ctl[3] and their items at items + ctl[4]
 // (both 0 for a single batch; per-batch offsets in a multi-batch plan).
 __device__ void scan_batch(int* cnt, int* off, int* fill, int4* items, int* ctl, int nbr, int cap_items,
-                           int cap_pairs, int pairs_base, int items_base) {
+                           int cap_pairs, int pairs_base, int items_base, bool det = false) {
     __shared__ int wp[32], wf[32], wr[32];
     __shared__ int rh[BC];  // partial items per segment count, then the descending-size cursor
     if (threadIdx.x < BC) rh[threadIdx.x] = 0;
@@ -397,6 +398,7 @@ __device__ void scan_batch(int* cnt, int* off, int* fill, int4* items, int* ctl,
     __syncthreads();
     int pbase = (warp > 0 ? wp[warp - 1] : 0) + ip - np;
     int fbase = (warp > 0 ? wf[warp - 1] : 0) + jf - nf;
+    int rbase = n_full + (warp > 0 ? wr[warp - 1] : 0) + jr - nr;  // (det: partial items in brick order)
     int4* it = items + items_base;
     for (int i = lo; i < hi; ++i) {
         const int c = cnt[i];
@@ -407,7 +409,7 @@ __device__ void scan_batch(int* cnt, int* off, int* fill, int4* items, int* ctl,
         for (; k + BC <= c; k += BC, ++fbase)
             if (fbase < cap_items) it[fbase] = make_int4(i, pbase + k, BC, 0);
         if (k < c) {
-            const int slot = atomicAdd(rh + (c - k), 1);
+            const int slot = det ? rbase++ : atomicAdd(rh + (c - k), 1);
             if (slot < cap_items) it[slot] = make_int4(i, pbase + k, c - k, 0);
         }
         pbase += c;
@@ -424,7 +426,68 @@ __device__ void scan_batch(int* cnt, int* off, int* fill, int4* items, int* ctl,
 
 __global__ void __launch_bounds__(1024) brick_scan_kernel(SortedArgs a) {
     if (a.gate && *a.gate == 0) return;
-    scan_batch(a.cnt, a.off, a.fill, a.items, a.ctl, a.nbr, a.cap_items, a.cap_pairs, 0, 0);
+    scan_batch(a.cnt, a.off, a.fill, a.items, a.ctl, a.nbr, a.cap_items, a.cap_pairs, 0, 0, a.det != 0);
+}
+
+// Deterministic mode: each brick's pair records sorted by dataset offset (the fill pass places them
+// in atomic order), one CTA per brick, bitonic in shared memory (<= 2 x kDetMaxBatch records).
+__global__ void __launch_bounds__(256) sort_pairs_kernel(const int* __restrict__ off, PairRec* pairs, int* ctl) {
+    __shared__ long long key[2 * kDetMaxBatch];
+    __shared__ int2 val[2 * kDetMaxBatch];
+    const int i = blockIdx.x, lo = off[i], n = off[i + 1] - lo;
+    if (n <= 1) return;
+    if (n > 2 * kDetMaxBatch) {  // cannot happen for <= 2 segments per image and brick; flagged, left unsorted
+        if (threadIdx.x == 0) atomicOr(ctl + 2, 2);
+        return;
+    }
+    int P = 1;
+    while (P < n) P <<= 1;
+    for (int t = threadIdx.x; t < P; t += blockDim.x) {
+        if (t < n) {
+            const PairRec r = pairs[lo + t];
+            key[t] = r.gofs;
+            val[t] = make_int2(r.count, r.tslot);
+        } else {
+            key[t] = 0x7fffffffffffffffll;
+        }
+    }
+    __syncthreads();
+    for (int k = 2; k <= P; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int t = threadIdx.x; t < P; t += blockDim.x) {
+                const int u = t ^ j;
+                if (u > t) {
+                    const bool up = (t & k) == 0;
+                    if ((key[t] > key[u]) == up) {
+                        const long long kk = key[t];
+                        key[t] = key[u];
+                        key[u] = kk;
+                        const int2 vv = val[t];
+                        val[t] = val[u];
+                        val[u] = vv;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    for (int t = threadIdx.x; t < n; t += blockDim.x) {
+        PairRec r;
+        r.gofs = key[t];
+        r.count = val[t].x;
+        r.tslot = val[t].y;
+        pairs[lo + t] = r;
+    }
+}
+
+// Deterministic mode: the loss partials of the work items (one per item, in item order) -> *out.
+__global__ void __launch_bounds__(1024) reduce_items_kernel(const double* __restrict__ part, const int* __restrict__ ctl,
+                                                            double* out) {
+    __shared__ double red[32];
+    const int n = ctl[0];
+    double s = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s += part[i];
+    const double t = block_sum(s, red);
+    if (threadIdx.x == 0) *out = t;
 }
 
 // ---------------------------------------------------------------- multi-batch plans
@@ -562,7 +625,7 @@ static cudaError_t main_grid(int& out) {
 template <bool NN, bool HUTCH>
 static cudaError_t v3_grid(int& out) {
     static GridCache cache;
-    return persistent_grid(cache, brick_loss_grad_kernel<NN, HUTCH>, sizeof(BrickSmem3T<HUTCH>), out);
+    return persistent_grid(cache, brick_loss_grad_kernel<NN, HUTCH, false>, sizeof(BrickSmem3T<HUTCH>), out);
 }
 
 static cudaError_t v4_grid(int& out) {
@@ -593,9 +656,9 @@ static cudaError_t launch_sorted_main(const SortedArgs& a, double* sq_out, cudaS
         cudaError_t e0 = HUTCH ? v3_grid<false, true>(grid) : a.nn ? v3_grid<true, false>(grid)
                                                                   : v3_grid<false, false>(grid);
         if (e0 != cudaSuccess) return e0;
-        if (HUTCH) brick_loss_grad_kernel<false, true><<<grid, BTHREADS, sizeof(BrickSmem3T<true>), s>>>(a);
-        else if (a.nn) brick_loss_grad_kernel<true, false><<<grid, BTHREADS, sizeof(BrickSmem3), s>>>(a);
-        else brick_loss_grad_kernel<false, false><<<grid, BTHREADS, sizeof(BrickSmem3), s>>>(a);
+        if (HUTCH) brick_loss_grad_kernel<false, true, false><<<grid, BTHREADS, sizeof(BrickSmem3T<true>), s>>>(a);
+        else if (a.nn) brick_loss_grad_kernel<true, false, false><<<grid, BTHREADS, sizeof(BrickSmem3), s>>>(a);
+        else brick_loss_grad_kernel<false, false, false><<<grid, BTHREADS, sizeof(BrickSmem3), s>>>(a);
     } else {
         const size_t smem = sizeof(SortedSmemT<HUTCH>);
         cudaError_t e0 = main_grid<HUTCH>(grid);
@@ -616,6 +679,29 @@ cudaError_t launch_sorted_bin(const SortedArgs& a, cudaStream_t s) {
     bin_sorted_kernel<false><<<a.B, 128, 0, s>>>(a);
     brick_scan_kernel<<<1, 1024, 0, s>>>(a);
     bin_sorted_kernel<true><<<a.B, 128, 0, s>>>(a);
+    if (a.det) sort_pairs_kernel<<<a.nbr, 256, 0, s>>>(a.off, a.pairs, a.ctl);
+    return cudaGetLastError();
+}
+
+// Deterministic loss+grad on the table-driven kernel: bitwise the same gradient (int64 pairs at
+// scale *a.fxp, accumulated in a.acc) and loss for any launch grid and any order of the batch.
+cudaError_t launch_sorted_loss_grad_det(const SortedArgs& a0, double* sq_out, cudaStream_t s) {
+    SortedArgs a = a0;
+    a.det = 1;
+    cudaError_t e = launch_sorted_bin(a, s);
+    if (e != cudaSuccess) return e;
+    static GridCache cache;
+    int grid = 0;
+    e = persistent_grid(cache, brick_loss_grad_kernel<false, false, true>, sizeof(BrickSmem3), grid);
+    if (e != cudaSuccess) return e;
+    if (const char* g = getenv("FSLD_DET_GRID")) {  // (tests: the result must not depend on the grid)
+        const int want = atoi(g);
+        if (want > 0 && want < grid) grid = want;
+    }
+    brick_loss_grad_kernel<false, false, true><<<grid, BTHREADS, sizeof(BrickSmem3), s>>>(a);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    reduce_items_kernel<<<1, 1024, 0, s>>>(a.part, a.ctl, sq_out);
     return cudaGetLastError();
 }
 
@@ -744,7 +830,7 @@ cudaError_t launch_planned_loss_grad_step(SortedArgs a, int64_t nvox, double sca
         a.fsq = sq_out;
         a.floss = loss;
         if (v4) brick_loss_grad_v4_kernel<0><<<grid, BTHREADS, sizeof(BrickSmem4), s>>>(a);
-        else brick_loss_grad_kernel<false, false><<<grid, BTHREADS, sizeof(BrickSmem3), s>>>(a);
+        else brick_loss_grad_kernel<false, false, false><<<grid, BTHREADS, sizeof(BrickSmem3), s>>>(a);
         return cudaGetLastError();
     }
     cudaError_t e = launch_grad_init(nvox, a.v, lam, a.acc, norm_part, n_norm, s);

@@ -93,9 +93,14 @@ __device__ __forceinline__ void load_pix3(const SortedArgs& a, const float2* tf,
 // HUTCH (trilinear): the k = 1 Rademacher probe rides along (optim.py:210-229 numerator): P z from
 // the corner signs of the staged probe bits, h = |f|^2 P z, 8 more fixed-point shared adds, and
 // fold_j += z_j (sum P^* C^2 P z)_j at the flush.
-template <bool NN, bool HUTCH>
+// DET (deterministic mode, trilinear, no probe): the item's int32 sums go to the int64 fixed-point
+// accumulator at the caller's scale *a.fxp (exact power-of-two shifts, order-free RED.ADD.64), and
+// the loss is summed per item (a.part[item index], the items in brick order) -- bitwise the same
+// for any grid, any claim order and any batch order.
+template <bool NN, bool HUTCH, bool DET>
 __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss_grad_kernel(SortedArgs a) {
     static_assert(!(NN && HUTCH), "the fused probe is trilinear only");
+    static_assert(!(DET && (NN || HUTCH)), "deterministic mode: trilinear loss+grad");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     BrickSmem3T<HUTCH>& S = *reinterpret_cast<BrickSmem3T<HUTCH>*>(smem_raw);
     a.pairs += a.ctl[3];
@@ -120,10 +125,15 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
     }
     constexpr int kClaimer = BTHREADS - 32;
     const int n_items = a.ctl[0];
-    auto claim = [&]() -> int4 {
+    auto claim = [&]() -> int4 {  // (w = the item's index)
         const int it = atomicAdd(a.ctl + 1, 1);
-        return it < n_items ? a.items[it] : make_int4(-1, 0, 0, 0);
+        if (it >= n_items) return make_int4(-1, 0, 0, 0);
+        int4 r = a.items[it];
+        r.w = it;
+        return r;
     };
+    // deterministic mode: exponent of the int64 fixed-point scale (a power of two)
+    const int efx = DET ? (int)((__double_as_longlong(*a.fxp) >> 52) & 0x7ff) - 1023 : 0;
     auto stage_item3 = [&](int4 item) {  // pair records + v brick (+ halo, zero off the grid), async
         for (int k = threadIdx.x; k < item.z; k += BTHREADS) cp_async16(S.prec + k, a.pairs + item.y + k);
         const int bid = item.x;
@@ -227,6 +237,7 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
         __syncthreads();
         const int total = S.pref[nseg];
         const float lim = (float)min(4194303, 178956970 / nseg);
+        double item_lsum = 0.0;  // (DET: the item's loss partial)
         float item_sc = 0.f, item_inv_sc = 1.f, item_sch = 0.f, item_inv_sch = 1.f;
         // this thread's first pixel of the item (register buffers A / B alternate: no moves of
         // in-flight load destinations, so a load is waited for only where its pixel is computed)
@@ -300,7 +311,8 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
                 next_in_b = false;
                 e += BTHREADS;
             }
-            lsum += (double)sq;
+            if (DET) item_lsum += (double)sq;
+            else lsum += (double)sq;
             {
                 const int vb_max = __reduce_max_sync(0xffffffffu, __float_as_int(vmax));
                 if (lane == 0) atomicMax(&S.vmax2[par], vb_max);
@@ -411,6 +423,26 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
             __threadfence();
             init_seen = true;
         }
+        if (DET) {  // the item's loss partial, in a fixed order
+            for (int o = 16; o > 0; o >>= 1) item_lsum += __shfl_xor_sync(0xffffffffu, item_lsum, o);
+            if (lane == 0) S.red[warp] = item_lsum;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                double t = 0.0;
+                for (int w = 0; w < BW; ++w) t += S.red[w];
+                a.part[item.w] = t;
+            }
+        }
+        // item value q at scale 2^esc -> q * 2^(efx - esc) at the deterministic scale (exact left
+        // shift; a right shift rounds, for items whose values are below the scale's resolution)
+        const int dsh = DET ? efx - (((__float_as_int(item_sc) >> 23) & 0xff) - 127) : 0;
+        auto to_fixed = [dsh](int q) -> unsigned long long {
+            long long r;
+            if (dsh >= 0) r = (long long)q << min(dsh, 62);
+            else if (dsh > -63) r = ((long long)q + (1ll << ((-dsh - 1) & 63))) >> ((-dsh) & 63);
+            else r = 0;
+            return (unsigned long long)r;
+        };
         // flush of the item: one reduction per touched voxel, accumulators re-zeroed
 #pragma unroll
         for (int u = 0; u < BU; ++u) {
@@ -425,7 +457,11 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
             const int kx = ox + (lxyz[u] & 15), ky = oy + ((lxyz[u] >> 4) & 15), kz = oz + (lxyz[u] >> 8);
             if (kx >= M - c || ky >= M - c || kz >= M - c) continue;
             const size_t j = (size_t)lin_index(kx, ky, kz, M, c);
-            if ((qr | qi) != 0) {
+            if (DET) {
+                unsigned long long* q64 = reinterpret_cast<unsigned long long*>(a.acc) + 2 * j;
+                if (qr) atomicAdd(q64, to_fixed(qr));
+                if (qi) atomicAdd(q64 + 1, to_fixed(qi));
+            } else if ((qr | qi) != 0) {
                 const float fs = item_inv_sc * a.out_scale;
                 red_f32x2(reinterpret_cast<float*>(a.acc) + 2 * j, (float)qr * fs, (float)qi * fs);
             }
@@ -436,37 +472,39 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
         }
         item = nxt;
     }
-    for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
-    if (lane == 0) S.red[warp] = lsum;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double s = 0.0;
-        for (int w = 0; w < BW; ++w) s += S.red[w];
-        a.part[blockIdx.x] = s;
-    }
-    if (a.fuse) {  // the last CTA: sq and the loss in a fixed order, counters re-armed for the next step
-        __shared__ bool last;
-        if (threadIdx.x == 0) {
-            __threadfence();
-            last = atomicAdd(a.ctl + 7, 1) == (int)gridDim.x - 1;
-        }
+    if constexpr (!DET) {  // (deterministic mode: the loss partials are per item, a.part[item index])
+        for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+        if (lane == 0) S.red[warp] = lsum;
         __syncthreads();
-        if (last && warp == 0) {
-            __threadfence();
-            double q = 0.0, v2 = 0.0;
-            for (int b = lane; b < (int)gridDim.x; b += 32) {
-                q += reinterpret_cast<volatile double*>(a.part)[b];
-                v2 += reinterpret_cast<volatile double*>(a.fnorm)[b];
+        if (threadIdx.x == 0) {
+            double s = 0.0;
+            for (int w = 0; w < BW; ++w) s += S.red[w];
+            a.part[blockIdx.x] = s;
+        }
+        if (a.fuse) {  // the last CTA: sq and the loss in a fixed order, counters re-armed for the next step
+            __shared__ bool last;
+            if (threadIdx.x == 0) {
+                __threadfence();
+                last = atomicAdd(a.ctl + 7, 1) == (int)gridDim.x - 1;
             }
-            for (int o = 16; o > 0; o >>= 1) {
-                q += __shfl_xor_sync(0xffffffffu, q, o);
-                v2 += __shfl_xor_sync(0xffffffffu, v2, o);
-            }
-            if (lane == 0) {
-                *a.fsq = q;
-                *a.floss = 0.5 * a.fscale * q + 0.5 * (double)a.flam * v2;
-                a.ctl[6] = 0;
-                a.ctl[7] = 0;
+            __syncthreads();
+            if (last && warp == 0) {
+                __threadfence();
+                double q = 0.0, v2 = 0.0;
+                for (int b = lane; b < (int)gridDim.x; b += 32) {
+                    q += reinterpret_cast<volatile double*>(a.part)[b];
+                    v2 += reinterpret_cast<volatile double*>(a.fnorm)[b];
+                }
+                for (int o = 16; o > 0; o >>= 1) {
+                    q += __shfl_xor_sync(0xffffffffu, q, o);
+                    v2 += __shfl_xor_sync(0xffffffffu, v2, o);
+                }
+                if (lane == 0) {
+                    *a.fsq = q;
+                    *a.floss = 0.5 * a.fscale * q + 0.5 * (double)a.flam * v2;
+                    a.ctl[6] = 0;
+                    a.ctl[7] = 0;
+                }
             }
         }
     }

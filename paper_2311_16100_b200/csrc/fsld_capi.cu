@@ -76,6 +76,12 @@ void note_bins(const void* scratch, const int32_t* idx, const fsld_image_rec* re
     g_last_bins_next = (g_last_bins_next + 1) % 8;
 }
 
+void forget_bins(const void* scratch) {
+    std::lock_guard<std::mutex> lk(g_registry_mu);
+    for (BinKey& k : g_last_bins)
+        if (k.scratch == scratch) k = BinKey{};
+}
+
 bool bins_match(const void* scratch, const int32_t* idx, const fsld_image_rec* recs, int M, int n_mask, int B) {
     std::lock_guard<std::mutex> lk(g_registry_mu);
     for (const BinKey& k : g_last_bins)
@@ -389,6 +395,16 @@ int fsld_loss_grad_sorted(int M, int mode, int n_mask, const fsld_image_rec* rec
     if (!geom_ok(M, mode, n_mask, B) || M > 256) return FSLD_EINVAL;
     if (!recs || !v || !xs || !pc || !grad_acc || !sq_out || !scratch) return FSLD_EINVAL;
     const bool det = (flags & FSLD_DETERMINISTIC) != 0;
+    if (det && !fx_scale) return FSLD_EINVAL;
+    // deterministic mode on the table-driven brick kernel (trilinear, tables built, B <= 1024)
+    if (det && mode == FSLD_MODE_TRI && ptab && seg_off && segs && B <= kDetMaxBatch && !(flags & FSLD_TILE_PATH)) {
+        const ScratchLayout L = scratch_layout(M, n_mask, B);
+        if (scratch_bytes < L.total) return FSLD_EINVAL;
+        SortedArgs b = make_sorted(L, M, n_mask, B, recs, idx, v, xs, pc, seg_off, segs, grad_acc, scratch, ptab);
+        b.fxp = fx_scale;
+        forget_bins(scratch);  // (these work items are in the deterministic order: not reused by FSLD_REUSE_BINS)
+        return status_of(launch_sorted_loss_grad_det(b, sq_out, reinterpret_cast<cudaStream_t>(stream)));
+    }
     // brick kernels: trilinear (tables or compute path); nearest-neighbour with tables on request
     const bool brick = (mode == FSLD_MODE_TRI || (ptab && (flags & FSLD_NN_BRICK))) && !det &&
                        !(flags & FSLD_TILE_PATH) && seg_off && segs;

@@ -150,6 +150,11 @@ struct SortedArgs {
     // the last CTA to finish (ctl[7]) forms *fsq / *floss and re-arms both counters -- the whole
     // step in one kernel launch (+ the claim-counter reset)
     int fuse;
+    // deterministic mode (table-driven kernel): work items in brick order with their segments
+    // sorted by dataset offset, the flush converts each item's int32 sums to int64 fixed point at
+    // the caller's scale *fxp (order-free integer adds), and the loss is summed per item in item order
+    int det;
+    const double* fxp;
     float flam;
     double fscale;
     double* fnorm;
@@ -166,6 +171,8 @@ size_t sorted_tables_bytes(long long npx);
 cudaError_t launch_sorted_tables(int M, int n_mask, int mode, const fsld_image_rec* recs, int N, const char2* pc,
                                  const int32_t* seg_off, const int2* segs, void* ptab, cudaStream_t s);
 cudaError_t launch_sorted_loss_grad(const SortedArgs& a, double* sq_out, cudaStream_t s);
+cudaError_t launch_sorted_loss_grad_det(const SortedArgs& a, double* sq_out, cudaStream_t s);
+constexpr int kDetMaxBatch = 1024;  // deterministic brick path: <= 2 segments per image and brick -> 2048 per sort
 cudaError_t launch_planned_loss_grad(const SortedArgs& a, double* sq_out, cudaStream_t s);
 cudaError_t launch_sorted_bin(const SortedArgs& a, cudaStream_t s);
 struct SlabMap {                 // brick z-layer -> slab of the host step (nb <= 32 for M <= 256)
