@@ -43,6 +43,19 @@ def shard_indices(batch, rank: int, world_size: int):
     return batch[bounds[rank]:bounds[rank + 1]]
 
 
+def image_range(n_images: int, rank: int, world_size: int) -> tuple[int, int]:
+    """The contiguous image range [lo, hi) a rank holds when the dataset itself is sharded."""
+    bounds = np.linspace(0, n_images, world_size + 1).round().astype(int)
+    return int(bounds[rank]), int(bounds[rank + 1])
+
+
+def local_batch(batch, lo: int, hi: int):
+    """The images of a global batch that fall in [lo, hi), as indices local to that range (the
+    rank's share of the batch when each rank holds only its image range)."""
+    b = np.asarray(batch)
+    return b[(b >= lo) & (b < hi)] - lo
+
+
 @dataclass
 class PackedBuffer:
     """One flat tensor viewed as [acc (complex) | hutch (real, optional) | loss (hi, lo)].
@@ -162,17 +175,21 @@ def _engine_compute(op, v, sub, buf: PackedBuffer, zbits=None, k=0):
 
 
 def sharded_step(op, v, batch, lam: float, n_total: int | None = None, buf: PackedBuffer | None = None,
-                 zbits=None, k: int = 0, compute=None, group=None):
+                 zbits=None, k: int = 0, compute=None, group=None, image_range: tuple[int, int] | None = None):
     """One data-parallel loss / gradient (/ Hutchinson fold) evaluation over a GLOBAL batch.
 
     Returns (loss, grad, hutch_sample) identical on every rank, where
     hutch_sample = n_total/|batch|/k * sum_p z_p * (A^*A z_p) + lam (None without probes).
+    image_range=(lo, hi): the dataset itself is sharded -- ``op`` holds only images [lo, hi) and
+    the rank computes the batch's images of that range (n_total is then required).
     """
     rank, ws = world()
     batch = np.asarray(batch)
+    if image_range is not None and n_total is None:
+        raise ValueError("a sharded dataset needs n_total (the number of images over all ranks)")
     n_total = op.n_images if n_total is None else n_total
     scale = n_total / batch.size
-    sub = shard_indices(batch, rank, ws)
+    sub = shard_indices(batch, rank, ws) if image_range is None else local_batch(batch, *image_range)
     dev = v.device if isinstance(v, torch.Tensor) else torch.device("cpu")
     if buf is None:
         buf = PackedBuffer.new(v.numel() if isinstance(v, torch.Tensor) else np.asarray(v).size,

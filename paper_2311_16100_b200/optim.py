@@ -336,7 +336,7 @@ def armijo_search(v, grad, dhat, loss_fn, eta_in: float, c: float, f0=None):
 
 
 def run(config: OptimConfig, stack, v0=None, reference=None, exact_diag_vec=None, probes: str = "reference",
-        op=None, group=None, alpha: float | None = None):
+        op=None, group=None, alpha: float | None = None, shard_dataset: bool = False):
     """Algorithm 1 (optim.py:309-393) with every step resident on the GPU.
 
     Per batch, in stream order and without host synchronisation:
@@ -358,22 +358,43 @@ def run(config: OptimConfig, stack, v0=None, reference=None, exact_diag_vec=None
     (dist.shard_indices), and per step ONE all-reduce of [gradient accumulator | probe
     fold | sum|r|^2], compacted to the touched ball, plus one scalar all-reduce of the
     line-search energy, combine the ranks; the epilogue, the line search and the update
-    then run identically on every rank.
+    then run identically on every rank.  With ``shard_dataset=True`` each rank
+    holds only its contiguous range of the images (1/world of the dataset in HBM) and takes
+    from every global batch the images of its range; the per-epoch full-dataset loss adds one
+    scalar all-reduce.  The batches, probes and the summed objective are the same, so the
+    trajectory matches the replicated run up to fp32 summation order.
     """
-    from .forward import DatasetOperator, FourierVolume
+    from .forward import DatasetOperator, FourierVolume, ImageStack
     from .hessian import exact_diag
     from .metrics import ShellIndex, fsc, relative_l2
     from . import _capi as C
 
     if probes not in ("reference", "device"):
         raise ValueError("probes must be 'reference' or 'device'")
+    from . import dist as D
+    rank, ws = D.world()
+    if group is not None:
+        ws = torch.distributed.get_world_size(group)
+        rank = torch.distributed.get_rank(group)
+    n = stack.n_images
+    lo, hi = 0, n  # the images this rank holds
+    if shard_dataset and ws > 1:
+        if op is not None:
+            raise ValueError("shard_dataset builds the rank's operator itself (op must be None)")
+        lo, hi = D.image_range(n, rank, ws)
+        if hi <= lo:
+            raise ValueError("shard_dataset needs at least one image per rank")
+        sub = ImageStack(spec=stack.spec, images=stack.images[lo:hi], poses=list(stack.poses[lo:hi]),
+                         ctfs=None if stack.ctfs is None else list(stack.ctfs[lo:hi]), sigma=stack.sigma,
+                         seed=stack.seed, mask_radius=stack.mask_radius, mode=stack.mode)
+        op = DatasetOperator(sub, config.mode)
+    sharded = hi - lo < n
     op = DatasetOperator(stack, config.mode) if op is None else op
     e = op.engine
     spec = op.spec
     nvox = spec.n_voxels
     if alpha is None:  # (callers that run several times on one dataset may pass it precomputed)
         alpha = threshold_alpha(stack, None, config.lam)
-    n = op.n_images
     if config.batch_size > n:
         raise ValueError("batch_size exceeds the number of images")
     dev = e.dev
@@ -408,12 +429,7 @@ def run(config: OptimConfig, stack, v0=None, reference=None, exact_diag_vec=None
         rv = reference.values if hasattr(reference, "values") else reference
         ref_vals = torch.as_tensor(np.asarray(rv) if not _is_dev(rv) else rv, device=dev)
 
-    from . import dist as D
     from .grid import touched_ball
-    rank, ws = D.world()
-    if group is not None:
-        ws = torch.distributed.get_world_size(group)
-        rank = torch.distributed.get_rank(group)
     if ws > 1 and e.deterministic:
         raise ValueError("the data-parallel run uses the fp32 accumulators (deterministic engines: one process)")
     pbuf = None
@@ -437,7 +453,10 @@ def run(config: OptimConfig, stack, v0=None, reference=None, exact_diag_vec=None
         st.view(torch.int32)[12] = 0  # n_steps: hist rows restart each epoch
         # binning plan of this rank's share of the epoch's full-size batches (one build per epoch;
         # a short last batch is binned in its own step)
-        subs = [D.shard_indices(b, rank, ws) if ws > 1 else b for b in batches]
+        if sharded:  # the batch's images in this rank's range, as local indices
+            subs = [D.local_batch(b, lo, hi) for b in batches]
+        else:
+            subs = [D.shard_indices(b, rank, ws) if ws > 1 else b for b in batches]
         plan, plan_k = None, {}
         if e.brick_path:
             full = [i for i, sb in enumerate(subs) if len(sb) and len(sb) == len(subs[0])]
@@ -524,6 +543,8 @@ def run(config: OptimConfig, stack, v0=None, reference=None, exact_diag_vec=None
             trace.backtracks[epoch] += int(nbt)
         st_f64[0] *= config.eta_growth
         sq_all = e.loss(v, all_idx)
+        if sharded:
+            torch.distributed.all_reduce(sq_all, group=group)
         trace.loss[epoch] = 0.5 * float(sq_all.item()) + 0.5 * lam * float(e.norm2(v).item())
         trace.eta_end[epoch] = float(st_f64[0].item())
         if estimating and exact_diag_vec is not None:

@@ -68,6 +68,53 @@ def _worker(rank, world_size, port, out_path, use_ball=False):
     dist.destroy_process_group()
 
 
+def _range_worker(rank, world_size, port, out_path):
+    """Each rank holds only its image range of the dataset (oracle operator over those rows)."""
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world_size)
+    g = load_golden("dataset_m16_tri.npz")
+    M = int(g["M"])
+    n = g["quats"].shape[0]
+    lo, hi = D.image_range(n, rank, world_size)
+    ctab = O.ctf_table_radial(g["ctf_params"], O.mask_pix(M, g["mask"]), M) if g["ctf_params"].shape[0] else None
+    op = O.OracleOperator(M, str(g["mode"]), g["mask"], g["quats"][lo:hi], g["shifts"][lo:hi],
+                          None if ctab is None else ctab[lo:hi], g["x"][lo:hi])
+    buf = D.PackedBuffer.new(M ** 3, False, torch.device("cpu"), dtype=torch.float64)
+    loss, grad, _ = D.sharded_step(op, torch.from_numpy(np.asarray(g["v1"], dtype=np.complex128)),
+                                   np.asarray(g["batch"]), float(g["lam"]), n_total=n, buf=buf,
+                                   compute=_oracle_compute, image_range=(lo, hi))
+    np.savez(out_path + f".{rank}.npz", loss=float(loss), grad=grad.numpy(),
+             sub=D.local_batch(g["batch"], lo, hi) + lo)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_image_range_partition_and_local_batch():
+    b = np.random.default_rng(0).permutation(101)[:40]
+    for ws in (1, 2, 3, 8):
+        ranges = [D.image_range(101, r, ws) for r in range(ws)]
+        assert ranges[0][0] == 0 and ranges[-1][1] == 101
+        assert all(ranges[r][1] == ranges[r + 1][0] for r in range(ws - 1))
+        parts = [D.local_batch(b, lo, hi) + lo for lo, hi in ranges]
+        assert np.array_equal(np.sort(np.concatenate(parts)), np.sort(b))
+
+
+def test_two_rank_gloo_sharded_dataset_equals_single_process():
+    """optim.run(shard_dataset=True)'s exchange: each rank holds half of the images, takes the
+    batch's images of its range, one packed all-reduce -> the single-process full-batch result."""
+    g = load_golden("dataset_m16_tri.npz")
+    op = _oracle_op(g)
+    batch = np.asarray(g["batch"])
+    loss_ref, grad_ref = O.loss_and_grad(op, g["v1"], batch, float(g["lam"]))
+    with tempfile.TemporaryDirectory() as d:
+        out = os.path.join(d, "res")
+        mp.start_processes(_range_worker, args=(2, _free_port(), out), nprocs=2, start_method="spawn")
+        r0, r1 = np.load(out + ".0.npz"), np.load(out + ".1.npz")
+    assert np.array_equal(np.sort(np.concatenate([r0["sub"], r1["sub"]])), np.sort(batch))
+    for r in (r0, r1):
+        assert abs(float(r["loss"]) - loss_ref) / loss_ref < 1e-12
+        assert O.relative_l2(r["grad"], grad_ref) < 1e-12
+
+
 def test_shard_indices_partition():
     b = np.arange(37)[::-1]
     for ws in (1, 2, 3, 8):

@@ -52,7 +52,7 @@ def test_sharded_step_with_ball_compaction_matches_full_buffer():
     assert O.relative_l2(h1.cpu().numpy(), h2.cpu().numpy()) < 1e-5
 
 
-def _run_worker(rank, world_size, port, out_path, name, seed):
+def _run_worker(rank, world_size, port, out_path, name, seed, shard=False):
     """One rank of a data-parallel optim.run (functional check: both ranks on cuda:0, gloo exchange)."""
     import torch.distributed as dist
     from conftest import load_golden
@@ -64,16 +64,17 @@ def _run_worker(rank, world_size, port, out_path, name, seed):
     stack = golden_stack(g, seed)
     cfg = Opt.OptimConfig(lam=float(g["lam"]), batch_size=int(g["batch"].size), epochs=3, seed=seed,
                           mode=str(g["mode"]))
-    vol, tr = Opt.run(cfg, stack)
+    vol, tr = Opt.run(cfg, stack, shard_dataset=shard)
     np.savez(out_path + f".{rank}.npz", v=vol.values, etas=np.array(tr.accepted_etas),
              f0=np.array(tr.step_f0), loss=tr.loss)
     dist.barrier()
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name,seed", [("dataset_m16_tri.npz", 4)])
-def test_data_parallel_run_matches_single_process(golden, name, seed):
-    """optim.run with world_size 2 (each rank half of every batch, one compacted all-reduce per step)
+@pytest.mark.parametrize("name,seed,shard", [("dataset_m16_tri.npz", 4, False), ("dataset_m16_tri.npz", 4, True)])
+def test_data_parallel_run_matches_single_process(golden, name, seed, shard):
+    """optim.run with world_size 2 (each rank half of every batch, one compacted all-reduce per step;
+    shard: each rank holds only half of the images and takes the batch images of its range)
     reproduces the single-process device run and the reference trajectory."""
     import os
     import socket
@@ -91,7 +92,7 @@ def test_data_parallel_run_matches_single_process(golden, name, seed):
     s.close()
     with tempfile.TemporaryDirectory() as d:
         out = os.path.join(d, "r")
-        mp.start_processes(_run_worker, args=(2, port, out, name, seed), nprocs=2, start_method="spawn")
+        mp.start_processes(_run_worker, args=(2, port, out, name, seed, shard), nprocs=2, start_method="spawn")
         r0, r1 = np.load(out + ".0.npz"), np.load(out + ".1.npz")
     assert np.array_equal(r0["etas"], r1["etas"]) and np.array_equal(r0["v"], r1["v"])  # identical ranks
     assert np.array_equal(r0["etas"], np.array(tr1.accepted_etas))
