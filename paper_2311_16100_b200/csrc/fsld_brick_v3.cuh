@@ -39,6 +39,7 @@ struct BrickSmem3T {
     long long sg[BC];       // segment start rebased to the item's flat pixel index: gofs - pref
     int pref[BC + 1];       // exclusive prefix of segment lengths
     int4 item_desc, next_desc;
+    int4 item_geo, next_geo;  // (ox, oy, oz, lim bits) of the item's brick, computed once by the claimer
     int vmax2[2];           // round maximum |conj(f) r| bits, by round parity
     int wtot[BC / 32];
     double red[BW];
@@ -112,11 +113,12 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
     const float4* tg = tab_geo(a.ptab, reinterpret_cast<const TabHeader*>(a.ptab)->npx);
     double lsum = 0.0;
     int rpar = 0;  // round parity counter (continues across items)
-    int lxyz[BU];
+    int lxyz[BU], cj[BU];  // brick voxel (lx, ly, lz) and the in-plane part of its lin_index
 #pragma unroll
     for (int u = 0; u < BU; ++u) {
         const int l = threadIdx.x + u * BTHREADS;
         lxyz[u] = l < BH3 ? (l % BH) | (((l / BH) % BH) << 4) | ((l / (BH * BH)) << 8) : -1;
+        cj[u] = ((l / BH) % BH + c) * M + l % BH + c;
         if (l < BH3) {
             S.accr[l] = 0;
             S.acci[l] = 0;
@@ -125,33 +127,41 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
     }
     constexpr int kClaimer = BTHREADS - 32;
     const int n_items = a.ctl[0];
-    auto claim = [&]() -> int4 {  // (w = the item's index)
+    auto claim = [&](int4& geo) -> int4 {  // (w = the item's index; geo = brick origin and fixed-point bound)
         const int it = atomicAdd(a.ctl + 1, 1);
         if (it >= n_items) return make_int4(-1, 0, 0, 0);
         int4 r = a.items[it];
         r.w = it;
+        const int bid = r.x;
+        geo = make_int4(-c + BT * (bid % nb), -c + BT * ((bid / nb) % nb), -c + BT * (bid / (nb * nb)),
+                        __float_as_int((float)min(4194303, 178956970 / r.z)));
         return r;
+    };
+    // lin_index(ox + lx, oy + ly, oz + lz) = zi M^2 + (oy M + ox) + cj (kernels.py:63-66), or -1 off the grid
+    auto voxel_j = [&](const int4& geo, int u) -> int {
+        const int lx = lxyz[u] & 15, ly = (lxyz[u] >> 4) & 15, lz = lxyz[u] >> 8;
+        if (lx >= M - c - geo.x || ly >= M - c - geo.y || lz >= M - c - geo.z) return -1;
+        const int kz = geo.z + lz;
+        return (kz < 0 ? kz + M : kz) * M * M + geo.y * M + geo.x + cj[u];
     };
     // deterministic mode: exponent of the int64 fixed-point scale (a power of two)
     const int efx = DET ? (int)((__double_as_longlong(*a.fxp) >> 52) & 0x7ff) - 1023 : 0;
-    auto stage_item3 = [&](int4 item) {  // pair records + v brick (+ halo, zero off the grid), async
+    auto stage_item3 = [&](int4 item, int4 geo) {  // pair records + v brick (+ halo, zero off the grid), async
         for (int k = threadIdx.x; k < item.z; k += BTHREADS) cp_async16(S.prec + k, a.pairs + item.y + k);
-        const int bid = item.x;
-        const int ox = -c + BT * (bid % nb), oy = -c + BT * ((bid / nb) % nb), oz = -c + BT * (bid / (nb * nb));
 #pragma unroll
         for (int u = 0; u < BU; ++u) {
             if (lxyz[u] < 0) continue;
             const int l = threadIdx.x + u * BTHREADS;
-            const int kx = ox + (lxyz[u] & 15), ky = oy + ((lxyz[u] >> 4) & 15), kz = oz + (lxyz[u] >> 8);
-            const bool in = kx < M - c && ky < M - c && kz < M - c;
-            const int j = in ? lin_index(kx, ky, kz, M, c) : 0;
+            const int jv = voxel_j(geo, u);
+            const bool in = jv >= 0;
+            const int j = in ? jv : 0;
             cp_async8_zfill(S.vb + l, a.v + j, in);
             if (HUTCH) S.zs[l] = in ? (unsigned char)(__ldg(a.zbits + j) & 1u) : 0;
         }
     };
     if (threadIdx.x == kClaimer) {
-        S.item_desc = claim();
-        S.next_desc = claim();
+        S.item_desc = claim(S.item_geo);
+        S.next_desc = claim(S.next_geo);
     }
     if (threadIdx.x < 2) {
         S.vmax2[threadIdx.x] = 0;
@@ -159,7 +169,8 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
     }
     __syncthreads();
     int4 item = S.item_desc;
-    if (item.x >= 0) stage_item3(item);
+    int4 igeo = S.item_geo;
+    if (item.x >= 0) stage_item3(item, igeo);
     bool init_seen = !a.fuse;
     if (a.fuse) {  // this CTA's slice of acc = lam v, ||v||^2 partial; then count the slice as written
         const int64_t n = (int64_t)M * M * M;
@@ -186,9 +197,8 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
         if (item.x < 0) break;
         cp_async_wait_all();
         __syncthreads();  // (A) this item's pair records and v brick are in shared memory
-        const int4 nxt = S.next_desc;
-        const int bid = item.x, nseg = item.z;
-        const int ox = -c + BT * (bid % nb), oy = -c + BT * ((bid / nb) % nb), oz = -c + BT * (bid / (nb * nb));
+        const int4 nxt = S.next_desc, ngeo = S.next_geo;
+        const int nseg = item.z;
         if (warp < BC / 32) {  // segment-length prefix
             const int k = threadIdx.x;
             const int len = k < nseg ? S.prec[k].count : 0;
@@ -215,7 +225,7 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
             }
         }
         __syncthreads();  // (B)
-        if (threadIdx.x == kClaimer) S.next_desc = claim();
+        if (threadIdx.x == kClaimer) S.next_desc = claim(S.next_geo);
         if (threadIdx.x < nseg) {
             const int k = threadIdx.x;
             int p = S.pref[k];
@@ -236,7 +246,7 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
         }
         __syncthreads();
         const int total = S.pref[nseg];
-        const float lim = (float)min(4194303, 178956970 / nseg);
+        const float lim = __int_as_float(igeo.w);
         double item_lsum = 0.0;  // (DET: the item's loss partial)
         float item_sc = 0.f, item_inv_sc = 1.f, item_sch = 0.f, item_inv_sch = 1.f;
         // this thread's first pixel of the item (register buffers A / B alternate: no moves of
@@ -322,7 +332,7 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
                 }
             }
             __syncthreads();
-            if (r1 >= total && nxt.x >= 0) stage_item3(nxt);  // overlaps pass 2 + flush
+            if (r1 >= total && nxt.x >= 0) stage_item3(nxt, ngeo);  // overlaps pass 2 + flush
             // ---------------- pass 2: fixed-point adjoint scatter (kernels.py:221-230)
             {
                 // one power-of-two scale per item and accumulator, non-increasing over its rounds: a
@@ -390,8 +400,12 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
                 const float wz = w18(rec.w >> 14);
                 const float ax = 1.f - wx, ay = 1.f - wy, az = 1.f - wz;
                 const float2 val = __fmul2_rn(make_float2(__uint_as_float(rec.x), __uint_as_float(rec.y)), make_float2(sc, sc));
-                const float zy00 = az * ay, zy10 = az * wy, zy01 = wz * ay, zy11 = wz * wy;
-                const float w8[8] = {zy00 * ax, zy00 * wx, zy10 * ax, zy10 * wx, zy01 * ax, zy01 * wx, zy11 * ax, zy11 * wx};
+                // the 8 corner weights as packed products (bitwise the scalar ones)
+                const float2 AW = make_float2(ax, wx), YW = make_float2(ay, wy);
+                const float2 z0 = __fmul2_rn(make_float2(az, az), YW), z1 = __fmul2_rn(make_float2(wz, wz), YW);
+                const float2 w01 = __fmul2_rn(make_float2(z0.x, z0.x), AW), w23 = __fmul2_rn(make_float2(z0.y, z0.y), AW);
+                const float2 w45 = __fmul2_rn(make_float2(z1.x, z1.x), AW), w67 = __fmul2_rn(make_float2(z1.y, z1.y), AW);
+                const float w8[8] = {w01.x, w01.y, w23.x, w23.y, w45.x, w45.y, w67.x, w67.y};
                 const int off8[8] = {0, 1, BH, BH + 1, BH * BH, BH * BH + 1, BH * BH + BH, BH * BH + BH + 1};
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
@@ -454,9 +468,9 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
             S.accr[l] = 0;
             S.acci[l] = 0;
             if (HUTCH) S.acch[l] = 0;
-            const int kx = ox + (lxyz[u] & 15), ky = oy + ((lxyz[u] >> 4) & 15), kz = oz + (lxyz[u] >> 8);
-            if (kx >= M - c || ky >= M - c || kz >= M - c) continue;
-            const size_t j = (size_t)lin_index(kx, ky, kz, M, c);
+            const int jv = voxel_j(igeo, u);
+            if (jv < 0) continue;
+            const size_t j = (size_t)jv;
             if (DET) {
                 unsigned long long* q64 = reinterpret_cast<unsigned long long*>(a.acc) + 2 * j;
                 if (qr) atomicAdd(q64, to_fixed(qr));
@@ -471,6 +485,7 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
             }
         }
         item = nxt;
+        igeo = ngeo;
     }
     if constexpr (!DET) {  // (deterministic mode: the loss partials are per item, a.part[item index])
         for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
