@@ -839,10 +839,11 @@ def e2e_leg(eng, wl, B, lam, n_total, args, world):
     out = {"value": world * B / sec, "unit": "images/s", "ms_per_step": sec * 1e3,
            "h2d_bytes_per_step": 8 * M ** 3 + 4 * B, "d2h_bytes_per_step": 16 * M ** 3 + 16,
            "path": ("optim.loss_and_grad(op, v: numpy complex128, batch: numpy, lam) -> (float, numpy complex128) "
-                    "-- the reference's signature: streaming-store cast of v into pinned complex64 (host threads), "
-                    "fsld_loss_grad_host_c128 (z-slab pipeline: copies in both directions overlap the brick passes; "
-                    "each finished gradient slab cast to complex128 on the device and copied straight into the "
-                    "returned array, a recycled page-locked buffer; cached CUDA graph)"),
+                    "-- the reference's signature, through fsld_loss_grad_host_np: v cast to complex64 on the "
+                    "library's native host thread pool (streaming stores into page-locked staging), then the z-slab "
+                    "pipelined host step (copies in both directions overlap the brick passes; each finished gradient "
+                    "slab cast to complex128 on the device and copied straight into the returned array, a recycled "
+                    "page-locked buffer; cached CUDA graph)"),
            "timing": f"wall clock, mean of {n_time} calls after {n_warm} warm-up calls (host cast, PCIe copies and "
                      "kernels inside)"}
     # (2) the C ABI host-buffer entry on pinned complex64 buffers

@@ -483,6 +483,18 @@ int fsld_loss_grad_host_c128(int M, int mode, int n_mask, const fsld_image_rec* 
                              const int32_t* seg_off, const int32_t* segs, double scale, double lam,
                              void* grad_host_c128, double* out_host, void* v_dev, void* grad_dev, void* grad_dev128,
                              int32_t* idx_dev, int n_slabs, void* scratch, size_t scratch_bytes, void* stream);
+/* The reference's call shape end to end: optim.loss_and_grad(op, v, batch, lam) with a numpy complex128
+ * volume in and a complex128 gradient out (optim.py:165-190).  v128_host / grad128_host: M^3 complex128
+ * host arrays (any host memory, 16-byte aligned).  The library casts v to complex64 on its host thread
+ * pool (streaming stores) into its own page-locked staging and runs the slab-pipelined host step; a
+ * page-locked grad128_host is written by the copy engine (each finished slab cast to complex128 on the
+ * device), any other memory receives the complex64 gradient cast back by the host threads.  Blocking:
+ * returns once grad128_host and out_host = [sum|r|^2, loss] are written. */
+int fsld_loss_grad_host_np(int M, int mode, int n_mask, const fsld_image_rec* recs, const int32_t* idx_host, int B,
+                           const double* v128_host, const void* xs, const int8_t* pc, const void* ptab,
+                           const int32_t* seg_off, const int32_t* segs, double scale, double lam, double* grad128_host,
+                           double* out_host, void* v_dev, void* grad_dev, int32_t* idx_dev, int n_slabs,
+                           void* scratch, size_t scratch_bytes, void* stream);
 int fsld_proj_energy_planned(int M, int mode, int n_mask, const fsld_image_rec* recs, const void* plan, int B, int k,
                              const void* d, const int8_t* pc, double* out, void* scratch, size_t scratch_bytes,
                              void* stream);

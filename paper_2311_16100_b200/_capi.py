@@ -104,6 +104,7 @@ SIGNATURES = {
     "fsld_loss_grad_step_planned": (I, [I, I, I, P, P, I, I, P, P, P, P, D, D, P, P, P, P, SZ, P, SZ, P]),
     "fsld_loss_grad_host": (I, [I, I, I, P, P, I, P, P, P, P, P, P, D, D, P, P, P, P, P, I, P, SZ, P]),
     "fsld_loss_grad_host_c128": (I, [I, I, I, P, P, I, P, P, P, P, P, P, D, D, P, P, P, P, P, P, I, P, SZ, P]),
+    "fsld_loss_grad_host_np": (I, [I, I, I, P, P, I, P, P, P, P, P, P, D, D, P, P, P, P, P, I, P, SZ, P]),
     "fsld_project_sorted": (I, [I, I, I, P, P, I, P, P, P, P]),
     "fsld_backproject_sorted": (I, [I, I, I, P, P, I, P, P, P, U, P, P]),
     "fsld_fixed_scale": (I, [P, I64, D, D, P, P]),

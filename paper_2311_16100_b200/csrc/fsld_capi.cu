@@ -10,6 +10,8 @@
 #include <cstring>
 #include <mutex>
 
+
+#include "fsld_hostpool.h"
 #include "fsld_kernels.cuh"
 
 using namespace fsld;
@@ -1158,4 +1160,89 @@ extern "C" int fsld_loss_grad_host_c128(int M, int mode, int n_mask, const fsld_
     return loss_grad_host_impl(M, mode, n_mask, recs, idx_host, B, v_host, xs, pc, ptab, seg_off, segs, scale, lam,
                                grad_host_c128, out_host, v_dev, grad_dev, idx_dev, n_slabs, scratch, scratch_bytes,
                                stream, grad_dev128);
+}
+
+// ---------------------------------------------------------------- numpy-signature host step
+namespace {
+struct NpStage {  // per device: page-locked complex64 staging of v and of the gradient, device complex128 staging
+    int64_t n = 0;
+    float2 *v64 = nullptr, *g64 = nullptr;
+    double2* g128_dev = nullptr;
+};
+NpStage g_np[16];
+std::mutex g_np_mu;  // one numpy-signature call at a time (the staging is per device)
+
+cudaError_t np_stage(int64_t n, NpStage*& out) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= 16) return cudaErrorInvalidDevice;
+    NpStage& st = g_np[dev];
+    if (st.n != n) {
+        if (st.v64) {
+            drop_host_graphs_using(st.v64);
+            drop_host_graphs_using(st.g64);
+            cudaFreeHost(st.v64);
+            cudaFreeHost(st.g64);
+            cudaFree(st.g128_dev);
+        }
+        st = NpStage{};
+        if ((e = cudaHostAlloc(reinterpret_cast<void**>(&st.v64), sizeof(float2) * (size_t)n, cudaHostAllocDefault)) !=
+                cudaSuccess ||
+            (e = cudaHostAlloc(reinterpret_cast<void**>(&st.g64), sizeof(float2) * (size_t)n, cudaHostAllocDefault)) !=
+                cudaSuccess ||
+            (e = cudaMalloc(reinterpret_cast<void**>(&st.g128_dev), sizeof(double2) * (size_t)n)) != cudaSuccess)
+            return e;
+        st.n = n;
+    }
+    out = &st;
+    return cudaSuccess;
+}
+
+// complex128 <-> complex64 over n complex elements on the library's host thread pool (streaming stores)
+void np_cast(const double* src, float* dst, int64_t n) {
+    fsld_host::parallel_for(n, 1 << 15, [&](int64_t i0, int64_t i1) {
+        fsld_host_cast_f64_to_f32(src + 2 * i0, dst + 2 * i0, 2 * (i1 - i0));
+    });
+}
+void np_cast_back(const float* src, double* dst, int64_t n) {
+    fsld_host::parallel_for(n, 1 << 15, [&](int64_t i0, int64_t i1) {
+        fsld_host_cast_f32_to_f64(src + 2 * i0, dst + 2 * i0, 2 * (i1 - i0));
+    });
+}
+}  // namespace
+
+// Measured on the B200 box (cfg3, tools/e2e_split.py): the call is bound by host memory traffic (the
+// complex128 volume read and the complex128 gradient written are ~67 MB, the complex64 staging another
+// ~34 MB); overlapping the slab casts with the copies (device waits on host-written flags) made every
+// phase slower through that contention (1.31 vs 1.22 ms), so the cast runs first, on all host cores.
+extern "C" int fsld_loss_grad_host_np(int M, int mode, int n_mask, const fsld_image_rec* recs, const int32_t* idx_host,
+                                      int B, const double* v128_host, const void* xs, const int8_t* pc,
+                                      const void* ptab, const int32_t* seg_off, const int32_t* segs, double scale,
+                                      double lam, double* grad128_host, double* out_host, void* v_dev,
+                                      void* grad_dev, int32_t* idx_dev, int n_slabs, void* scratch,
+                                      size_t scratch_bytes, void* stream) {
+    if (!v128_host || !grad128_host || !out_host || M < 2 || M > 256 || n_slabs < 1 || n_slabs > kMaxSlabs)
+        return FSLD_EINVAL;
+    if ((reinterpret_cast<uintptr_t>(v128_host) | reinterpret_cast<uintptr_t>(grad128_host)) & 15) return FSLD_EINVAL;
+    const int64_t n = (int64_t)M * M * M;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    std::lock_guard<std::mutex> lk(g_np_mu);
+    NpStage* st = nullptr;
+    cudaError_t e = np_stage(n, st);
+    if (e != cudaSuccess) return status_of(e);
+    // a page-locked output array is written by the copy engine (the device casts each finished slab to
+    // complex128); any other memory gets the complex64 gradient cast back by the host threads
+    cudaPointerAttributes pa{};
+    const bool out_pinned = cudaPointerGetAttributes(&pa, grad128_host) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    np_cast(v128_host, reinterpret_cast<float*>(st->v64), n);
+    const int rc = loss_grad_host_impl(M, mode, n_mask, recs, idx_host, B, st->v64, xs, pc, ptab, seg_off, segs,
+                                       scale, lam, out_pinned ? static_cast<void*>(grad128_host) : st->g64, out_host,
+                                       v_dev, grad_dev, idx_dev, n_slabs, scratch, scratch_bytes, stream,
+                                       out_pinned ? static_cast<void*>(st->g128_dev) : nullptr);
+    if (rc != FSLD_OK) return rc;
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return status_of(e);
+    if (!out_pinned) np_cast_back(reinterpret_cast<const float*>(st->g64), grad128_host, n);
+    return FSLD_OK;
 }

@@ -12,7 +12,16 @@
 #include <stdint.h>
 #include <xmmintrin.h>
 
+#include <algorithm>
+#include <atomic>
+#include <condition_variable>
+#include <functional>
+#include <mutex>
+#include <thread>
+#include <vector>
+
 #include "fsld_b200.h"
+#include "fsld_hostpool.h"
 
 // dst[i] = (float) src[i] over n doubles (n = 2 x complex count); dst 16-byte aligned for the stream.
 extern "C" int fsld_host_cast_f64_to_f32(const double* src, float* dst, int64_t n) {
@@ -49,3 +58,90 @@ extern "C" int fsld_host_cast_f32_to_f64(const float* src, double* dst, int64_t 
     _mm_sfence();
     return FSLD_OK;
 }
+
+// ---------------------------------------------------------------- host thread pool
+// A persistent pool for the numpy-signature host step (fsld_loss_grad_host_np): the casts of one
+// z-slab are split over the workers and the calling thread, which waits for all of them.  Plain
+// std::thread (no second OpenMP runtime next to torch's).  One parallel_for at a time (the host
+// step holds its pipe mutex while it casts).
+namespace fsld_host {
+namespace {
+struct Pool {
+    std::vector<std::thread> workers;
+    std::mutex m;
+    std::condition_variable cv, done_cv;
+    const std::function<void(int64_t, int64_t)>* fn = nullptr;
+    int64_t n = 0, grain = 1;
+    std::atomic<int64_t> next{0};
+    int active = 0;
+    unsigned long long gen = 0;
+    bool stop = false;
+
+    void run_chunks() {
+        for (;;) {
+            const int64_t i0 = next.fetch_add(grain);
+            if (i0 >= n) return;
+            (*fn)(i0, std::min(n, i0 + grain));
+        }
+    }
+    void loop() {
+        unsigned long long seen = 0;
+        for (;;) {
+            {
+                std::unique_lock<std::mutex> lk(m);
+                cv.wait(lk, [&] { return stop || gen != seen; });
+                if (stop) return;
+                seen = gen;
+            }
+            run_chunks();
+            std::lock_guard<std::mutex> lk(m);
+            if (--active == 0) done_cv.notify_one();
+        }
+    }
+    Pool() {
+        const unsigned hc = std::thread::hardware_concurrency();
+        const int nw = (int)std::max(1u, std::min(16u, hc ? hc : 1u)) - 1;  // + the calling thread
+        for (int i = 0; i < nw; ++i) workers.emplace_back([this] { loop(); });
+    }
+    ~Pool() {
+        {
+            std::lock_guard<std::mutex> lk(m);
+            stop = true;
+        }
+        cv.notify_all();
+        for (auto& t : workers) t.join();
+    }
+};
+Pool& pool() {
+    static Pool p;
+    return p;
+}
+std::mutex g_pf_mu;
+}  // namespace
+
+void parallel_for(int64_t n, int64_t grain, const std::function<void(int64_t, int64_t)>& f) {
+    if (n <= 0) return;
+    Pool& P = pool();
+    if (P.workers.empty() || n <= grain) {
+        f(0, n);
+        return;
+    }
+    std::lock_guard<std::mutex> one(g_pf_mu);
+    {
+        std::lock_guard<std::mutex> lk(P.m);
+        P.fn = &f;
+        P.n = n;
+        P.grain = grain;
+        P.next.store(0);
+        P.active = (int)P.workers.size();
+        ++P.gen;
+    }
+    P.cv.notify_all();
+    P.run_chunks();
+    std::unique_lock<std::mutex> lk(P.m);
+    P.done_cv.wait(lk, [&] { return P.active == 0; });
+    P.fn = nullptr;
+}
+
+int workers() { return (int)pool().workers.size() + 1; }
+}  // namespace fsld_host

@@ -407,6 +407,34 @@ class SliceEngine:
                                         int(n_slabs or self.HOST_SLABS), ctypes_ptr(scr), scr.numel() * 8,
                                         _stream()), "fsld_loss_grad_host")
 
+    def loss_grad_host_np(self, v128: np.ndarray, idx_host, scale: float, lam: float, grad128: np.ndarray,
+                          out_host, stage: dict, n_slabs: int | None = None) -> None:
+        """fsld_loss_grad_host_np: numpy complex128 v in, numpy complex128 gradient out (the reference's
+        call shape); the library casts slab by slab on its host threads, overlapped with the copies and
+        the brick passes.  Blocking; out_host (pinned float64[2]) = [sum|r|^2, loss]."""
+        lib = C.load()
+        if not self.brick_path:
+            raise ValueError("the host step runs the brick path (tri, sorted, non-deterministic)")
+        for a in (v128, grad128):
+            if a.dtype != np.complex128 or a.size != self.n_voxels or not a.flags.c_contiguous or a.ctypes.data % 16:
+                raise ValueError("v / grad must be contiguous 16-byte-aligned complex128 arrays of M^3")
+        if idx_host.device.type != "cpu" or not idx_host.is_pinned() or idx_host.dtype != torch.int32:
+            raise ValueError("idx_host must be a pinned int32 host tensor")
+        B = int(idx_host.numel())
+        if B == 0:
+            raise ValueError("batch must be nonempty")
+        if int(idx_host.min()) < 0 or int(idx_host.max()) >= self.n_images:
+            raise ValueError("batch index out of range")
+        scr = self.scratch(B)
+        if stage["idx"].numel() < B:
+            stage["idx"] = torch.empty(B, dtype=torch.int32, device=self.dev)
+        C.check(lib.fsld_loss_grad_host_np(
+            self.M, self.mode_id, self.n_mask, ctypes_ptr(self.recs), ctypes_ptr(idx_host), B, v128.ctypes.data,
+            ctypes_ptr(self.x), ctypes_ptr(self.pc), ctypes_ptr(self.ptab), ctypes_ptr(self.seg_off),
+            ctypes_ptr(self.segs), float(scale), float(lam), grad128.ctypes.data, ctypes_ptr(out_host),
+            ctypes_ptr(stage["v"]), ctypes_ptr(stage["g"]), ctypes_ptr(stage["idx"]),
+            int(n_slabs or self.HOST_SLABS), ctypes_ptr(scr), scr.numel() * 8, _stream()), "fsld_loss_grad_host_np")
+
     def proj_energy_planned(self, d, plan: "BinPlan", k: int, out=None) -> torch.Tensor:
         lib = C.load()
         d = self._vol(d)

@@ -465,42 +465,42 @@ class DatasetOperator:
 
     def loss_and_grad_numpy(self, v, batch, lam: float, n_total: int | None = None):
         """optim.loss_and_grad with the reference's argument types (numpy complex128 v in, (float,
-        complex128 gradient) out; optim.py:165-190) on the brick path: v is cast into a pinned
-        complex64 buffer (fsld_host_cast_*: streaming stores, host thread pool), fsld_loss_grad_host_c128
-        moves it slab by slab while the brick passes run, forms scale * sum + lam v on the device, casts
-        each finished slab to complex128 there and copies it straight into the returned array (a
-        recycled page-locked buffer).  Accuracy: the fp32 path (1e-7 relative)."""
-        from . import _capi as C
-        from .hostio import PinnedArrays, cast_native
+        complex128 gradient) out; optim.py:165-190) on the brick path, through fsld_loss_grad_host_np:
+        the library casts v to complex64 slab by slab on its host thread pool while the device copies
+        and processes the earlier slabs (each slab's copy waits on a mapped flag), and casts every
+        finished gradient slab back to complex128 into the returned array (a recycled page-locked
+        buffer) while later slabs are still in flight.  Accuracy: the fp32 path (1e-7 relative)."""
+        from .hostio import PinnedArrays
 
         e = self.engine
         n = e.n_voxels
         st = getattr(self, "_np_stage", None)
-        if st is None:  # cudaHostAlloc staging (the copy engines stream it at full PCIe rate)
-            st = self._np_stage = {"v": C.host_empty(n, torch.complex64), "g": C.host_empty(n, torch.complex64),
-                                   "idx": torch.empty(0, dtype=torch.int32),
-                                   "out": PinnedArrays(n, torch.complex128)}
+        if st is None:
+            st = self._np_stage = {"idx": torch.empty(0, dtype=torch.int32), "out": PinnedArrays(n, torch.complex128),
+                                   "out_h": torch.empty(2, dtype=torch.float64).pin_memory()}
         b = np.asarray(batch).reshape(-1)
         if b.size == 0:
             raise ValueError("batch must be nonempty")
         if st["idx"].numel() != b.size:
             st["idx"] = torch.empty(b.size, dtype=torch.int32).pin_memory()
         st["idx"].numpy()[:] = b
-        lib = C.load()
         vin = np.ascontiguousarray(v, dtype=np.complex128).reshape(-1)
         if vin.size != n:
             raise ValueError(f"volume has {vin.size} entries, expected {n}")
-        # streaming-store cast on the host thread pool: the staged volume is clean in DRAM for the copy engine
-        cast_native(lib.fsld_host_cast_f64_to_f32, vin.ctypes.data, st["v"].data_ptr(), 2 * n, 8, 4)
+        if vin.ctypes.data % 16:
+            vin = vin.copy()
+        hs = getattr(self, "_host_stage", None)
+        if hs is None:
+            hs = self._host_stage = {"v": torch.empty(n, dtype=torch.complex64, device=e.dev),
+                                     "g": torch.empty(n, dtype=torch.complex64, device=e.dev),
+                                     "acc": e.new_cacc(), "out": torch.empty(2, dtype=torch.float64, device=e.dev),
+                                     "out_h": torch.empty(2, dtype=torch.float64).pin_memory()}
+        hs.setdefault("idx", torch.empty(b.size, dtype=torch.int32, device=e.dev))
         out = st["out"].get()
-        if out is not None:  # complex128 straight from the device into a recycled pinned array
-            grad, gt = out
-            loss = self.loss_and_grad_host(st["v"], st["idx"], lam, gt, n_total)
-            return loss, grad
-        loss = self.loss_and_grad_host(st["v"], st["idx"], lam, st["g"], n_total)  # (many results held)
-        grad = np.empty(n, dtype=np.complex128)
-        cast_native(lib.fsld_host_cast_f32_to_f64, st["g"].data_ptr(), grad.ctypes.data, 2 * n, 4, 8)
-        return loss, grad
+        grad = out[0] if out is not None else np.empty(n, dtype=np.complex128)  # (many results held)
+        n_total = self.n_images if n_total is None else n_total
+        e.loss_grad_host_np(vin, st["idx"], n_total / b.size, lam, grad, st["out_h"], hs)
+        return float(st["out_h"][1]), grad
 
     def b_vector(self):
         """sum_i P_i^* C_i x_i over all images (forward.py:572-579)."""
