@@ -15,11 +15,19 @@
 #pragma once
 
 #ifndef FSLD_RB3
+#if FSLD_V3_FULLW
+#define FSLD_RB3 768
+#else
 #define FSLD_RB3 1024
 #endif
+#endif
 constexpr int RB3 = FSLD_RB3;
-#ifndef FSLD_V3_MINB
+#ifndef FSLD_V3_MINB  // CTAs per SM the registers are budgeted for (FULLW: 64 registers, 4 CTAs; 5 spills)
+#if FSLD_V3_FULLW
+#define FSLD_V3_MINB 4
+#else
 #define FSLD_V3_MINB 5
+#endif
 #endif
 constexpr int BK3 = BC * kSegMax;  // pixels per work item (<= BC segments of <= kSegMax pixels)
 
@@ -28,7 +36,12 @@ struct BrickSmem3T {
     float2 vb[BH3];         // v brick + halo
     int accr[BH3];          // fixed-point adjoint accumulator (re)
     int acci[BH3];          // (im)
+#if FSLD_V3_FULLW
+    float2 bval[RB3];       // pass 1 -> 2: conj(f) r
+    float4 bgeo[RB3];       // pass 1 -> 2: the footprint as read from the table (fp32 weights, corner index)
+#else
     uint4 brec[RB3];        // pass 1 -> 2: conj(f) r (2 x fp32) + the packed footprint (geo_pack)
+#endif
     int acch[HUTCH ? BH3 : 1];            // fixed-point Hutchinson accumulator
     float hval[HUTCH ? RB3 : 1];          // pass 1 -> 2: h = |f|^2 P z
     unsigned char zs[HUTCH ? BH3 : 1];    // the probe's sign bit per brick voxel (staged)
@@ -134,7 +147,7 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
         r.w = it;
         const int bid = r.x;
         geo = make_int4(-c + BT * (bid % nb), -c + BT * ((bid / nb) % nb), -c + BT * (bid / (nb * nb)),
-                        __float_as_int((float)min(4194303, 178956970 / r.z)));
+                        __float_as_int(fixed_lim<NN>(r.z)));
         return r;
     };
     // lin_index(ox + lx, oy + ly, oz + lz) = zi M^2 + (oy M + ox) + cj (kernels.py:63-66), or -1 off the grid
@@ -246,7 +259,11 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
         }
         __syncthreads();
         const int total = S.pref[nseg];
+#ifdef FSLD_EXP_LIM_DIV  // experiment: a looser fixed-point scale (precision headroom of an a-priori bound)
+        const float lim = __int_as_float(igeo.w) * (1.0f / FSLD_EXP_LIM_DIV);
+#else
         const float lim = __int_as_float(igeo.w);
+#endif
         double item_lsum = 0.0;  // (DET: the item's loss partial)
         float item_sc = 0.f, item_inv_sc = 1.f, item_sch = 0.f, item_inv_sch = 1.f;
         // this thread's first pixel of the item (register buffers A / B alternate: no moves of
@@ -289,8 +306,13 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
                 sq = fmaf(rr.x, rr.x, fmaf(rr.y, rr.y, sq));
                 const float2 val = cmulconj(f, rr);
                 vmax = fmaxf(vmax, fmaxf(fabsf(val.x), fabsf(val.y)));
+#if FSLD_V3_FULLW
+                S.bval[e - r0] = val;
+                S.bgeo[e - r0] = cur.geo;
+#else
                 const uint2 gp = geo_pack(cur.geo);
                 S.brec[e - r0] = make_uint4(__float_as_uint(val.x), __float_as_uint(val.y), gp.x, gp.y);
+#endif
                 if (HUTCH) {  // P z in the same nested order, z = +-1 from the corner sign bits
                     const unsigned m = S.zc[l0];
                     auto zf = [m](int b) { return __int_as_float(0xBF800000u ^ (((m >> b) & 1u) << 31)); };
@@ -386,6 +408,17 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
             const int rn = r1 - r0;
 #endif
             for (int e = threadIdx.x; e < rn; e += BTHREADS) {
+#if FSLD_V3_FULLW
+                const float4 gq = S.bgeo[e];
+                const int l0 = __float_as_int(gq.w);
+                const float2 val = __fmul2_rn(S.bval[e], make_float2(sc, sc));
+                if (NN) {  // one complex contribution at the nn voxel
+                    atomicAdd(S.accr + l0, __float2int_rn(val.x));
+                    atomicAdd(S.acci + l0, __float2int_rn(val.y));
+                    continue;
+                }
+                const float wx = gq.x, wy = gq.y, wz = gq.z;
+#else
                 const uint4 rec = S.brec[e];
                 const int l0 = (int)(rec.z & 1023u);
                 if (NN) {  // one complex contribution at the nn voxel
@@ -398,8 +431,9 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
                 const float wx = w18((rec.z >> 10) & 262143u);
                 const float wy = w18(__funnelshift_r(rec.z, rec.w, 28) & 262143u);
                 const float wz = w18(rec.w >> 14);
-                const float ax = 1.f - wx, ay = 1.f - wy, az = 1.f - wz;
                 const float2 val = __fmul2_rn(make_float2(__uint_as_float(rec.x), __uint_as_float(rec.y)), make_float2(sc, sc));
+#endif
+                const float ax = 1.f - wx, ay = 1.f - wy, az = 1.f - wz;
                 // the 8 corner weights as packed products (bitwise the scalar ones)
                 const float2 AW = make_float2(ax, wx), YW = make_float2(ay, wy);
                 const float2 z0 = __fmul2_rn(make_float2(az, az), YW), z1 = __fmul2_rn(make_float2(wz, wz), YW);
@@ -409,19 +443,29 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
                 const int off8[8] = {0, 1, BH, BH + 1, BH * BH, BH * BH + 1, BH * BH + BH, BH * BH + BH + 1};
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
-                    const float2 y = __ffma2_rn(make_float2(w8[q], w8[q]), val, make_float2(kMagic, kMagic));
-#ifdef FSLD_EXP_NO_ATOMS  // ablation (results wrong by construction): one shared add per pixel
-                    if (q == 0) atomicAdd(S.accr + l0, (__float_as_int(y.x) - kMagicBits) ^ (__float_as_int(y.y) - kMagicBits));
+#if FSLD_V3_FULLW
+                    const float2 y = __fmul2_rn(make_float2(w8[q], w8[q]), val);
+                    const int qr = __float2int_rn(y.x), qi = __float2int_rn(y.y);
 #else
-                    atomicAdd(S.accr + l0 + off8[q], __float_as_int(y.x) - kMagicBits);
-                    atomicAdd(S.acci + l0 + off8[q], __float_as_int(y.y) - kMagicBits);
+                    const float2 y = __ffma2_rn(make_float2(w8[q], w8[q]), val, make_float2(kMagic, kMagic));
+                    const int qr = __float_as_int(y.x) - kMagicBits, qi = __float_as_int(y.y) - kMagicBits;
+#endif
+#ifdef FSLD_EXP_NO_ATOMS  // ablation (results wrong by construction): one shared add per pixel
+                    if (q == 0) atomicAdd(S.accr + l0, qr ^ qi);
+#else
+                    atomicAdd(S.accr + l0 + off8[q], qr);
+                    atomicAdd(S.acci + l0 + off8[q], qi);
 #endif
                 }
                 if (HUTCH) {
                     const float h = S.hval[e] * item_sch;
 #pragma unroll
                     for (int q = 0; q < 8; ++q)
+#if FSLD_V3_FULLW
+                        atomicAdd(S.acch + l0 + off8[q], __float2int_rn(w8[q] * h));
+#else
                         atomicAdd(S.acch + l0 + off8[q], __float_as_int(fmaf(w8[q], h, kMagic)) - kMagicBits);
+#endif
                 }
             }
             if (threadIdx.x == 0) {  // the next round's slots (unused since this round's barrier)
