@@ -582,7 +582,6 @@ cudaError_t launch_plan_build(SortedArgs a, const PlanLayout& P, char* plan, cud
 #include "fsld_brick_energy.cuh"
 #include "fsld_brick_hutch.cuh"
 #include "fsld_brick_v3.cuh"
-#include "fsld_brick_v4.cuh"
 
 cudaError_t set_phase_profile(unsigned long long* buf) {
     return cudaMemcpyToSymbol(g_phase_prof, &buf, sizeof(buf));
@@ -628,31 +627,10 @@ static cudaError_t v3_grid(int& out) {
     return persistent_grid(cache, brick_loss_grad_kernel<NN, HUTCH, false>, sizeof(BrickSmem3T<HUTCH>), out);
 }
 
-static cudaError_t v4_grid(int& out) {
-    static GridCache cache;
-    return persistent_grid(cache, brick_loss_grad_v4_kernel<0>, sizeof(BrickSmem4), out);
-}
-
-// The plain trilinear loss+grad pass over the dataset tables runs the table-driven kernel
-// (fsld_brick_v3.cuh).  FSLD_KERNEL=v4 in the environment selects the TMA-staged, bank-slotted
-// variant (fsld_brick_v4.cuh): parity-green and conflict-free in its shared atomics, but measured
-// slower at every configuration -- kept for A/B measurements.
-static bool use_v4() {
-    static const bool v4 = [] {
-        const char* k = getenv("FSLD_KERNEL");
-        return k && strcmp(k, "v4") == 0;
-    }();
-    return v4;
-}
-
 template <bool HUTCH>
 static cudaError_t launch_sorted_main(const SortedArgs& a, double* sq_out, cudaStream_t s, int* grid_out = nullptr) {
     int grid = 0;
-    if (!HUTCH && a.ptab && !a.nn && use_v4()) {
-        cudaError_t e0 = v4_grid(grid);
-        if (e0 != cudaSuccess) return e0;
-        brick_loss_grad_v4_kernel<0><<<grid, BTHREADS, sizeof(BrickSmem4), s>>>(a);
-    } else if (a.ptab && (!HUTCH || !a.nn)) {  // the table-driven kernel (per-pixel f and footprint from the tables)
+    if (a.ptab && (!HUTCH || !a.nn)) {  // the table-driven kernel (per-pixel f and footprint from the tables)
         cudaError_t e0 = HUTCH ? v3_grid<false, true>(grid) : a.nn ? v3_grid<true, false>(grid)
                                                                   : v3_grid<false, false>(grid);
         if (e0 != cudaSuccess) return e0;
@@ -789,8 +767,6 @@ cudaError_t prepare_host_step(int* grid_out) {
     cudaError_t e = main_grid<false>(grid);
     if (e == cudaSuccess) e = v3_grid<false, false>(grid3);
     if (grid3 > grid) grid = grid3;
-    if (e == cudaSuccess) e = v4_grid(grid3);
-    if (grid3 > grid) grid = grid3;
     if (grid_out) *grid_out = grid;
     return e;
 }
@@ -815,9 +791,8 @@ cudaError_t launch_planned_loss_grad(const SortedArgs& a, double* sq_out, cudaSt
 cudaError_t launch_planned_loss_grad_step(SortedArgs a, int64_t nvox, double scale, double lam, double* sq_out,
                                           double* loss, double* norm_part, int n_norm, cudaStream_t s) {
     if (a.ptab && !a.nn) {  // the table-driven kernels do the whole step in one launch
-        const bool v4 = use_v4();
         int grid = 0;
-        cudaError_t e = v4 ? v4_grid(grid) : v3_grid<false, false>(grid);
+        cudaError_t e = v3_grid<false, false>(grid);
         if (e != cudaSuccess) return e;
         if (grid > n_norm) return cudaErrorInvalidValue;
         e = cudaMemsetAsync(a.ctl + 1, 0, sizeof(int), s);  // re-arm the claim counter (any earlier use)
@@ -829,8 +804,7 @@ cudaError_t launch_planned_loss_grad_step(SortedArgs a, int64_t nvox, double sca
         a.fnorm = norm_part;
         a.fsq = sq_out;
         a.floss = loss;
-        if (v4) brick_loss_grad_v4_kernel<0><<<grid, BTHREADS, sizeof(BrickSmem4), s>>>(a);
-        else brick_loss_grad_kernel<false, false, false><<<grid, BTHREADS, sizeof(BrickSmem3), s>>>(a);
+        brick_loss_grad_kernel<false, false, false><<<grid, BTHREADS, sizeof(BrickSmem3), s>>>(a);
         return cudaGetLastError();
     }
     cudaError_t e = launch_grad_init(nvox, a.v, lam, a.acc, norm_part, n_norm, s);

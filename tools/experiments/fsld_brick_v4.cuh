@@ -1,3 +1,6 @@
+// EXPERIMENT, not compiled into the library: the TMA-staged, bank-slotted variant of the table-driven
+// kernel measured in round 2 (profiles/r02_kernel_anatomy.md section 3).  It was included by fsld_brick.cu
+// and selected with FSLD_KERNEL=v4; it predates the cvt.rni / fp32-footprint scatter (FSLD_V3_FULLW).
 // fsld_brick_v4.cuh -- the TMA-staged, bank-slotted brick kernel of the fused loss+gradient
 // (included by fsld_brick.cu).  Trilinear slicing (kernels.py:138-177) and its adjoint
 // (kernels.py:193-230) with the CTF / shift factor and the residual fused in (optim.py:147-190).
