@@ -85,3 +85,24 @@ def test_det_brick_vs_oracle_and_plain(data):
     # and the numpy-level result is bitwise repeatable
     ld2, gd2 = F.loss_and_grad(opd, v1, batch[::-1].copy(), lam)
     assert ld2 == ld and np.array_equal(gd2.view(np.uint64), gd.view(np.uint64))
+
+
+def test_numpy_signature_call_pinned_and_pageable_outputs(data):
+    """optim.loss_and_grad(op, numpy complex128 v, ...) -> fsld_loss_grad_host_np: the recycled page-locked
+    output arrays (device-side complex128 cast) and, once more than the pool's arrays are held, plain
+    numpy arrays (complex64 gradient cast back on the host threads) -- both equal the device step."""
+    from paper_2311_16100_b200 import optim as Opt
+    d, _, plain = data
+    op = DatasetOperator.from_engine(plain)
+    lam = 1e-3
+    v = (0.9 * d.v_true).astype(np.complex128)
+    batch = np.random.default_rng(8).permutation(1024)[:512]
+    ref_l, ref_g = O.loss_and_grad(d.oop, v.astype(np.complex64).astype(np.complex128), batch, lam)
+    held = []
+    for i in range(10):  # the pool keeps 8 page-locked arrays: calls 9 and 10 return pageable ones
+        l, g = Opt.loss_and_grad(op, v, batch, lam)
+        assert g.dtype == np.complex128 and g.shape == (d.M ** 3,)
+        assert abs(l - ref_l) / ref_l < TOL
+        assert O.relative_l2(g, ref_g) < TOL
+        held.append(g)
+    assert O.relative_l2(held[-1], held[0]) < 1e-6
