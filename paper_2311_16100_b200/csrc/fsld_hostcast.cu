@@ -13,6 +13,7 @@
 #include <xmmintrin.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <atomic>
 #include <condition_variable>
 #include <functional>
@@ -100,7 +101,12 @@ struct Pool {
     }
     Pool() {
         const unsigned hc = std::thread::hardware_concurrency();
-        const int nw = (int)std::max(1u, std::min(16u, hc ? hc : 1u)) - 1;  // + the calling thread
+        unsigned want = std::min(16u, hc ? hc : 1u);
+        if (const char* e = std::getenv("FSLD_HOST_THREADS")) {  // (A/B: threads of the host casts)
+            const int v = std::atoi(e);
+            if (v >= 1 && v <= 256) want = (unsigned)v;
+        }
+        const int nw = (int)std::max(1u, want) - 1;  // + the calling thread
         for (int i = 0; i < nw; ++i) workers.emplace_back([this] { loop(); });
     }
     ~Pool() {
