@@ -567,3 +567,31 @@ def test_host_step_graph_cache_survives_freed_and_reused_buffers(golden):
         assert rel(grad, g["grad1_batch"]) < TOL
         del op
         gc.collect()
+
+
+@pytest.mark.parametrize("mode,nn_brick", [("tri", False), ("nn", True)])
+def test_fixed_point_budget_identical_planes(mode, nn_brick):
+    """Worst case of the brick kernel's int32 budget (fixed_lim): 256 images with ONE pose, so every
+    brick's work items hold 64 segments of the same plane and every voxel collects 64 copies of the
+    largest per-image weight sum, with large-amplitude images.  No int32 overflow: the loss and the
+    gradient still match the oracle."""
+    from paper_2311_16100_b200.engine import SliceEngine
+    M, N = 32, 256
+    mask = O.disk_mask(M, M // 2 - 1)
+    pix = O.mask_pix(M, mask)
+    q = np.tile(synth.haar_quaternions(1, 5), (N, 1))
+    sh = np.zeros((N, 2))
+    v = synth.gaussian_blob_volume(M, 6) * 1e3
+    oop = O.OracleOperator(M, mode, mask, q, sh, None, None)
+    rng = np.random.default_rng(7)
+    x = oop.project(v, np.arange(N)) * 3.0 + 50.0 * (rng.standard_normal((N, pix.shape[0])) +
+                                                     1j * rng.standard_normal((N, pix.shape[0])))
+    oop.x = np.ascontiguousarray(x)
+    eng = SliceEngine(M, mode, mask, records_for(M, q, None, None), x, nn_brick=nn_brick)
+    assert eng.table_path
+    op = DatasetOperator.from_engine(eng)
+    batch = np.arange(N)
+    lg, gg = F.loss_and_grad(op, v, batch, 1e-3)
+    lr, gr = O.loss_and_grad(oop, v, batch, 1e-3)
+    assert abs(lg - lr) / lr < TOL
+    assert rel(gg, gr) < TOL
