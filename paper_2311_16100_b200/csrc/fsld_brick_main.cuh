@@ -14,6 +14,9 @@ constexpr int kMagicBits = 0x4B400000;
 #ifndef FSLD_V3_FULLW
 #define FSLD_V3_FULLW 1
 #endif
+#ifndef FSLD_V3_F2I  // the cvt.rni rounding and the weight-sum bound (independent of the buffer layout;
+#define FSLD_V3_F2I 1  // measured: either change alone already needs > 48 registers, i.e. 4 CTAs/SM)
+#endif
 // Fixed-point bound of an item of nseg segments: the largest |contribution| after scaling.  FULLW:
 // one image's pixels put a trilinear weight sum of at most 1.28 on any voxel (measured over 2e5 random
 // poses and offsets; bound 2 used) and at most 3 pixels share an nn voxel (bound 4), so a voxel's
@@ -21,7 +24,7 @@ constexpr int kMagicBits = 0x4B400000;
 // Round 1: |q| < 2^22 for the magic-number rounding and 12 contributions per voxel and segment.
 template <bool NN>
 __device__ __forceinline__ float fixed_lim(int nseg) {
-#if FSLD_V3_FULLW
+#if FSLD_V3_F2I
     return __fdiv_rn(NN ? 536870912.0f : 1073741824.0f, (float)nseg);
 #else
     return (float)min(4194303, 178956970 / nseg);
@@ -545,7 +548,7 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArg
 #else
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
-#if FSLD_V3_FULLW
+#if FSLD_V3_F2I
                     const float2 y = __fmul2_rn(make_float2(w8[q], w8[q]), val);
                     atomicAdd(S.accr + l0 + off8[q], __float2int_rn(y.x));
                     atomicAdd(S.acci + l0 + off8[q], __float2int_rn(y.y));
@@ -560,7 +563,7 @@ __global__ void __launch_bounds__(BTHREADS, 4) sorted_loss_grad_kernel(SortedArg
                     const float h = S.hval[e] * sch;
 #pragma unroll
                     for (int q = 0; q < 8; ++q)
-#if FSLD_V3_FULLW
+#if FSLD_V3_F2I
                         atomicAdd(S.acch + l0 + off8[q], __float2int_rn(w8[q] * h));
 #else
                         atomicAdd(S.acch + l0 + off8[q], __float_as_int(fmaf(w8[q], h, kMagic)) - kMagicBits);

@@ -412,27 +412,26 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
                 const float4 gq = S.bgeo[e];
                 const int l0 = __float_as_int(gq.w);
                 const float2 val = __fmul2_rn(S.bval[e], make_float2(sc, sc));
-                if (NN) {  // one complex contribution at the nn voxel
-                    atomicAdd(S.accr + l0, __float2int_rn(val.x));
-                    atomicAdd(S.acci + l0, __float2int_rn(val.y));
-                    continue;
-                }
                 const float wx = gq.x, wy = gq.y, wz = gq.z;
 #else
                 const uint4 rec = S.brec[e];
                 const int l0 = (int)(rec.z & 1023u);
-                if (NN) {  // one complex contribution at the nn voxel
-                    const float2 y = __ffma2_rn(make_float2(__uint_as_float(rec.x), __uint_as_float(rec.y)),
-                                                make_float2(sc, sc), make_float2(kMagic, kMagic));
-                    atomicAdd(S.accr + l0, __float_as_int(y.x) - kMagicBits);
-                    atomicAdd(S.acci + l0, __float_as_int(y.y) - kMagicBits);
-                    continue;
-                }
                 const float wx = w18((rec.z >> 10) & 262143u);
                 const float wy = w18(__funnelshift_r(rec.z, rec.w, 28) & 262143u);
                 const float wz = w18(rec.w >> 14);
                 const float2 val = __fmul2_rn(make_float2(__uint_as_float(rec.x), __uint_as_float(rec.y)), make_float2(sc, sc));
 #endif
+                if (NN) {  // one complex contribution at the nn voxel
+#if FSLD_V3_F2I
+                    atomicAdd(S.accr + l0, __float2int_rn(val.x));
+                    atomicAdd(S.acci + l0, __float2int_rn(val.y));
+#else
+                    const float2 y = __fadd2_rn(val, make_float2(kMagic, kMagic));
+                    atomicAdd(S.accr + l0, __float_as_int(y.x) - kMagicBits);
+                    atomicAdd(S.acci + l0, __float_as_int(y.y) - kMagicBits);
+#endif
+                    continue;
+                }
                 const float ax = 1.f - wx, ay = 1.f - wy, az = 1.f - wz;
                 // the 8 corner weights as packed products (bitwise the scalar ones)
                 const float2 AW = make_float2(ax, wx), YW = make_float2(ay, wy);
@@ -443,7 +442,7 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
                 const int off8[8] = {0, 1, BH, BH + 1, BH * BH, BH * BH + 1, BH * BH + BH, BH * BH + BH + 1};
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
-#if FSLD_V3_FULLW
+#if FSLD_V3_F2I
                     const float2 y = __fmul2_rn(make_float2(w8[q], w8[q]), val);
                     const int qr = __float2int_rn(y.x), qi = __float2int_rn(y.y);
 #else
@@ -461,7 +460,7 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
                     const float h = S.hval[e] * item_sch;
 #pragma unroll
                     for (int q = 0; q < 8; ++q)
-#if FSLD_V3_FULLW
+#if FSLD_V3_F2I
                         atomicAdd(S.acch + l0 + off8[q], __float2int_rn(w8[q] * h));
 #else
                         atomicAdd(S.acch + l0 + off8[q], __float_as_int(fmaf(w8[q], h, kMagic)) - kMagicBits);
