@@ -22,13 +22,9 @@
 #endif
 #endif
 constexpr int RB3 = FSLD_RB3;
-#ifndef FSLD_V3_MINB  // CTAs per SM the registers are budgeted for (FULLW: 64 registers, 4 CTAs; 5 spills)
-#if FSLD_V3_FULLW
-#define FSLD_V3_MINB 4
-#else
-#define FSLD_V3_MINB 5
-#endif
-#endif
+#ifndef FSLD_V3_MINB  // CTAs per SM the registers are budgeted for: 4 (64 registers).  5 (48) fits
+#define FSLD_V3_MINB 4   // without spills since the work-item state lives in shared memory, but measured
+#endif                   // 141 vs 130.5 us (the 48-register schedule loses the loads' overlap)
 constexpr int BK3 = BC * kSegMax;  // pixels per work item (<= BC segments of <= kSegMax pixels)
 
 template <bool HUTCH>
@@ -51,8 +47,10 @@ struct BrickSmem3T {
     PairRec prec[BC];       // the item's pair records (gofs, count)
     long long sg[BC];       // segment start rebased to the item's flat pixel index: gofs - pref
     int pref[BC + 1];       // exclusive prefix of segment lengths
-    int4 item_desc, next_desc;
-    int4 item_geo, next_geo;  // (ox, oy, oz, lim bits) of the item's brick, computed once by the claimer
+    // work items: the current one, the next, and the one after (claimed one item ahead) -- in shared
+    // memory rather than registers (uniform per CTA, read a few times per item); ring_geo = (ox, oy,
+    // oz, lim bits) of the brick, computed once by the claimer
+    int4 ring_desc[3], ring_geo[3];
     int vmax2[2];           // round maximum |conj(f) r| bits, by round parity
     int wtot[BC / 32];
     double red[BW];
@@ -126,12 +124,11 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
     const float4* tg = tab_geo(a.ptab, reinterpret_cast<const TabHeader*>(a.ptab)->npx);
     double lsum = 0.0;
     int rpar = 0;  // round parity counter (continues across items)
-    int lxyz[BU], cj[BU];  // brick voxel (lx, ly, lz) and the in-plane part of its lin_index
+    int lxyz[BU];  // brick voxel (lx, ly, lz)
 #pragma unroll
     for (int u = 0; u < BU; ++u) {
         const int l = threadIdx.x + u * BTHREADS;
         lxyz[u] = l < BH3 ? (l % BH) | (((l / BH) % BH) << 4) | ((l / (BH * BH)) << 8) : -1;
-        cj[u] = ((l / BH) % BH + c) * M + l % BH + c;
         if (l < BH3) {
             S.accr[l] = 0;
             S.acci[l] = 0;
@@ -150,16 +147,17 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
                         __float_as_int(fixed_lim<NN>(r.z)));
         return r;
     };
-    // lin_index(ox + lx, oy + ly, oz + lz) = zi M^2 + (oy M + ox) + cj (kernels.py:63-66), or -1 off the grid
+    // lin_index(ox + lx, oy + ly, oz + lz) (kernels.py:63-66), or -1 off the grid
     auto voxel_j = [&](const int4& geo, int u) -> int {
         const int lx = lxyz[u] & 15, ly = (lxyz[u] >> 4) & 15, lz = lxyz[u] >> 8;
         if (lx >= M - c - geo.x || ly >= M - c - geo.y || lz >= M - c - geo.z) return -1;
         const int kz = geo.z + lz;
-        return (kz < 0 ? kz + M : kz) * M * M + geo.y * M + geo.x + cj[u];
+        return ((kz < 0 ? kz + M : kz) * M + geo.y + ly + c) * M + geo.x + lx + c;
     };
     // deterministic mode: exponent of the int64 fixed-point scale (a power of two)
     const int efx = DET ? (int)((__double_as_longlong(*a.fxp) >> 52) & 0x7ff) - 1023 : 0;
-    auto stage_item3 = [&](int4 item, int4 geo) {  // pair records + v brick (+ halo, zero off the grid), async
+    auto stage_item3 = [&](int slot) {  // pair records + v brick (+ halo, zero off the grid), async
+        const int4 item = S.ring_desc[slot], geo = S.ring_geo[slot];
         for (int k = threadIdx.x; k < item.z; k += BTHREADS) cp_async16(S.prec + k, a.pairs + item.y + k);
 #pragma unroll
         for (int u = 0; u < BU; ++u) {
@@ -173,17 +171,16 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
         }
     };
     if (threadIdx.x == kClaimer) {
-        S.item_desc = claim(S.item_geo);
-        S.next_desc = claim(S.next_geo);
+        S.ring_desc[0] = claim(S.ring_geo[0]);
+        S.ring_desc[1] = claim(S.ring_geo[1]);
     }
     if (threadIdx.x < 2) {
         S.vmax2[threadIdx.x] = 0;
         if (HUTCH) S.hmax2[threadIdx.x] = 0;
     }
     __syncthreads();
-    int4 item = S.item_desc;
-    int4 igeo = S.item_geo;
-    if (item.x >= 0) stage_item3(item, igeo);
+    int cur = 0;  // ring slot of the current item
+    if (S.ring_desc[0].x >= 0) stage_item3(0);
     bool init_seen = !a.fuse;
     if (a.fuse) {  // this CTA's slice of acc = lam v, ||v||^2 partial; then count the slice as written
         const int64_t n = (int64_t)M * M * M;
@@ -207,11 +204,11 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
     }
 
     for (;;) {
-        if (item.x < 0) break;
+        if (S.ring_desc[cur].x < 0) break;
         cp_async_wait_all();
         __syncthreads();  // (A) this item's pair records and v brick are in shared memory
-        const int4 nxt = S.next_desc, ngeo = S.next_geo;
-        const int nseg = item.z;
+        const int nxs = cur == 2 ? 0 : cur + 1;  // ring slot of the next item
+        const int nseg = S.ring_desc[cur].z;
         if (warp < BC / 32) {  // segment-length prefix
             const int k = threadIdx.x;
             const int len = k < nseg ? S.prec[k].count : 0;
@@ -238,7 +235,10 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
             }
         }
         __syncthreads();  // (B)
-        if (threadIdx.x == kClaimer) S.next_desc = claim(S.next_geo);
+        if (threadIdx.x == kClaimer) {  // the item after the next one, into the finished item's slot
+            const int s2 = nxs == 2 ? 0 : nxs + 1;
+            S.ring_desc[s2] = claim(S.ring_geo[s2]);
+        }
         if (threadIdx.x < nseg) {
             const int k = threadIdx.x;
             int p = S.pref[k];
@@ -260,9 +260,9 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
         __syncthreads();
         const int total = S.pref[nseg];
 #ifdef FSLD_EXP_LIM_DIV  // experiment: a looser fixed-point scale (precision headroom of an a-priori bound)
-        const float lim = __int_as_float(igeo.w) * (1.0f / FSLD_EXP_LIM_DIV);
+        const float lim = __int_as_float(S.ring_geo[cur].w) * (1.0f / FSLD_EXP_LIM_DIV);
 #else
-        const float lim = __int_as_float(igeo.w);
+        const float lim = __int_as_float(S.ring_geo[cur].w);
 #endif
         double item_lsum = 0.0;  // (DET: the item's loss partial)
         float item_sc = 0.f, item_inv_sc = 1.f, item_sch = 0.f, item_inv_sch = 1.f;
@@ -354,7 +354,7 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
                 }
             }
             __syncthreads();
-            if (r1 >= total && nxt.x >= 0) stage_item3(nxt, ngeo);  // overlaps pass 2 + flush
+            if (r1 >= total && S.ring_desc[nxs].x >= 0) stage_item3(nxs);  // overlaps pass 2 + flush
             // ---------------- pass 2: fixed-point adjoint scatter (kernels.py:221-230)
             {
                 // one power-of-two scale per item and accumulator, non-increasing over its rounds: a
@@ -487,7 +487,7 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
             if (threadIdx.x == 0) {
                 double t = 0.0;
                 for (int w = 0; w < BW; ++w) t += S.red[w];
-                a.part[item.w] = t;
+                a.part[S.ring_desc[cur].w] = t;
             }
         }
         // item value q at scale 2^esc -> q * 2^(efx - esc) at the deterministic scale (exact left
@@ -501,6 +501,7 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
             return (unsigned long long)r;
         };
         // flush of the item: one reduction per touched voxel, accumulators re-zeroed
+        const int4 igeo = S.ring_geo[cur];
 #pragma unroll
         for (int u = 0; u < BU; ++u) {
             if (lxyz[u] < 0) continue;
@@ -527,8 +528,7 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
                 atomicAdd(a.fold + j, hz);
             }
         }
-        item = nxt;
-        igeo = ngeo;
+        cur = nxs;
     }
     if constexpr (!DET) {  // (deterministic mode: the loss partials are per item, a.part[item index])
         for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
