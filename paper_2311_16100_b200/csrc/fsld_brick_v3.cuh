@@ -124,11 +124,15 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
     const float4* tg = tab_geo(a.ptab, reinterpret_cast<const TabHeader*>(a.ptab)->npx);
     double lsum = 0.0;
     int rpar = 0;  // round parity counter (continues across items)
-    int lxyz[BU];  // brick voxel (lx, ly, lz)
+    // brick voxel l = threadIdx.x + u * BTHREADS as (lx | ly << 4 | lz << 8), or -1 past the brick
+    // (recomputed where used: no long-lived registers)
+    auto lxyz = [](int u) -> int {
+        const int l = (int)threadIdx.x + u * BTHREADS;
+        return l < BH3 ? (l % BH) | (((l / BH) % BH) << 4) | ((l / (BH * BH)) << 8) : -1;
+    };
 #pragma unroll
     for (int u = 0; u < BU; ++u) {
         const int l = threadIdx.x + u * BTHREADS;
-        lxyz[u] = l < BH3 ? (l % BH) | (((l / BH) % BH) << 4) | ((l / (BH * BH)) << 8) : -1;
         if (l < BH3) {
             S.accr[l] = 0;
             S.acci[l] = 0;
@@ -149,7 +153,7 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
     };
     // lin_index(ox + lx, oy + ly, oz + lz) (kernels.py:63-66), or -1 off the grid
     auto voxel_j = [&](const int4& geo, int u) -> int {
-        const int lx = lxyz[u] & 15, ly = (lxyz[u] >> 4) & 15, lz = lxyz[u] >> 8;
+        const int lx = lxyz(u) & 15, ly = (lxyz(u) >> 4) & 15, lz = lxyz(u) >> 8;
         if (lx >= M - c - geo.x || ly >= M - c - geo.y || lz >= M - c - geo.z) return -1;
         const int kz = geo.z + lz;
         return ((kz < 0 ? kz + M : kz) * M + geo.y + ly + c) * M + geo.x + lx + c;
@@ -161,7 +165,7 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
         for (int k = threadIdx.x; k < item.z; k += BTHREADS) cp_async16(S.prec + k, a.pairs + item.y + k);
 #pragma unroll
         for (int u = 0; u < BU; ++u) {
-            if (lxyz[u] < 0) continue;
+            if (lxyz(u) < 0) continue;
             const int l = threadIdx.x + u * BTHREADS;
             const int jv = voxel_j(geo, u);
             const bool in = jv >= 0;
@@ -224,10 +228,10 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
         if (HUTCH) {  // corner sign masks (x fastest: 000,100,010,110,001,101,011,111) of the floor voxels
 #pragma unroll
             for (int u = 0; u < BU; ++u) {
-                if (lxyz[u] < 0) continue;
+                if (lxyz(u) < 0) continue;
                 const int l = threadIdx.x + u * BTHREADS;
                 unsigned m = S.zs[l];
-                if ((lxyz[u] & 15) < BT && ((lxyz[u] >> 4) & 15) < BT && (lxyz[u] >> 8) < BT)
+                if ((lxyz(u) & 15) < BT && ((lxyz(u) >> 4) & 15) < BT && (lxyz(u) >> 8) < BT)
                     m |= (unsigned)S.zs[l + 1] << 1 | (unsigned)S.zs[l + BH] << 2 | (unsigned)S.zs[l + BH + 1] << 3 |
                          (unsigned)S.zs[l + BH * BH] << 4 | (unsigned)S.zs[l + BH * BH + 1] << 5 |
                          (unsigned)S.zs[l + BH * BH + BH] << 6 | (unsigned)S.zs[l + BH * BH + BH + 1] << 7;
@@ -362,7 +366,7 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
                 auto shift_down = [&](int sh, int* acc_a, int* acc_b) {
 #pragma unroll
                     for (int u = 0; u < BU; ++u) {
-                        if (lxyz[u] < 0) continue;
+                        if (lxyz(u) < 0) continue;
                         const int l = threadIdx.x + u * BTHREADS;
                         if (sh >= 31) {
                             acc_a[l] = 0;
@@ -504,7 +508,7 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
         const int4 igeo = S.ring_geo[cur];
 #pragma unroll
         for (int u = 0; u < BU; ++u) {
-            if (lxyz[u] < 0) continue;
+            if (lxyz(u) < 0) continue;
             const int l = threadIdx.x + u * BTHREADS;
             const int qr = S.accr[l], qi = S.acci[l];
             const int qh = HUTCH ? S.acch[l] : 0;
