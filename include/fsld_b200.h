@@ -286,6 +286,12 @@ int fsld_hvp_sorted(int M, int mode, int n_mask, const fsld_image_rec* recs, con
 int fsld_loss_sorted(int M, int mode, int n_mask, const fsld_image_rec* recs, const int32_t* idx, int B,
                      const void* v, const void* xs, const int8_t* pc, double* sq_out, void* scratch,
                      size_t scratch_bytes, void* stream);
+/* fsld_loss_sorted over a table-built dataset (ptab from fsld_sorted_tables; seg_off / segs the
+ * dataset's segment list): the brick binning and the table-driven kernel's projection pass alone
+ * (optim.py:193-207 data term); ptab = NULL or nn mode fall back to fsld_loss_sorted. */
+int fsld_loss_sorted_tab(int M, int mode, int n_mask, const fsld_image_rec* recs, const int32_t* idx, int B,
+                         const void* v, const void* xs, const int8_t* pc, const void* ptab, const int32_t* seg_off,
+                         const int32_t* segs, double* sq_out, void* scratch, size_t scratch_bytes, void* stream);
 /* Projection of dataset rows idx into their sorted pixel order: out (B, n_mask). */
 int fsld_project_sorted(int M, int mode, int n_mask, const fsld_image_rec* recs, const int32_t* idx, int B,
                         const void* v, const int8_t* pc, void* out, void* stream);

@@ -99,6 +99,7 @@ SIGNATURES = {
     "fsld_mask_images": (I, [I, I, P, I, P, P, P]),
     "fsld_loss_grad_sorted": (I, [I, I, I, P, P, I, P, P, P, P, P, P, P, P, U, P, P, SZ, P]),
     "fsld_loss_sorted": (I, [I, I, I, P, P, I, P, P, P, P, P, SZ, P]),
+    "fsld_loss_sorted_tab": (I, [I, I, I, P, P, I, P, P, P, P, P, P, P, P, SZ, P]),
     "fsld_loss_grad_hutch_sorted": (I, [I, I, I, P, P, I, P, P, P, P, P, P, P, P, P, P, U, P, SZ, P]),
     "fsld_hvp_sorted": (I, [I, I, I, P, P, I, P, P, P, P, P, P, P, U, P, SZ, P]),
     "fsld_loss_grad_step_planned": (I, [I, I, I, P, P, I, I, P, P, P, P, D, D, P, P, P, P, SZ, P, SZ, P]),

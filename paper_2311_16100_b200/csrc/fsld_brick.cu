@@ -661,6 +661,21 @@ cudaError_t launch_sorted_bin(const SortedArgs& a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+// sum |f P v - x|^2 over a batch of a table-built dataset (trilinear): binning + the table-driven
+// kernel's projection pass alone (GATHER) + the fixed-order reduce.
+cudaError_t launch_sorted_loss_tab(const SortedArgs& a, double* sq_out, cudaStream_t s) {
+    cudaError_t e = launch_sorted_bin(a, s);
+    if (e != cudaSuccess) return e;
+    static GridCache cache;
+    int grid = 0;
+    e = persistent_grid(cache, brick_loss_grad_kernel<false, false, false, true>, sizeof(BrickSmem3), grid);
+    if (e != cudaSuccess) return e;
+    brick_loss_grad_kernel<false, false, false, true><<<grid, BTHREADS, sizeof(BrickSmem3), s>>>(a);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return launch_reduce(a.part, grid, sq_out, s);
+}
+
 // Deterministic loss+grad on the table-driven kernel: bitwise the same gradient (int64 pairs at
 // scale *a.fxp, accumulated in a.acc) and loss for any launch grid and any order of the batch.
 cudaError_t launch_sorted_loss_grad_det(const SortedArgs& a0, double* sq_out, cudaStream_t s) {

@@ -109,10 +109,14 @@ __device__ __forceinline__ void load_pix3(const SortedArgs& a, const float2* tf,
 // accumulator at the caller's scale *a.fxp (exact power-of-two shifts, order-free RED.ADD.64), and
 // the loss is summed per item (a.part[item index], the items in brick order) -- bitwise the same
 // for any grid, any claim order and any batch order.
-template <bool NN, bool HUTCH, bool DET>
+// GATHER: the projection pass alone -- sum |f P v - x|^2 over the work items (optim.py:193-207, the
+// batch_loss data term; the full-dataset loss of each optim.run epoch), no round buffer, no scatter,
+// no flush; an item's pixels in one sweep.
+template <bool NN, bool HUTCH, bool DET, bool GATHER = false>
 __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss_grad_kernel(SortedArgs a) {
     static_assert(!(NN && HUTCH), "the fused probe is trilinear only");
     static_assert(!(DET && (NN || HUTCH)), "deterministic mode: trilinear loss+grad");
+    static_assert(!(GATHER && (HUTCH || DET)), "the gather-only pass carries no probe and no fixed point");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     BrickSmem3T<HUTCH>& S = *reinterpret_cast<BrickSmem3T<HUTCH>*>(smem_raw);
     a.pairs += a.ctl[3];
@@ -275,8 +279,8 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
         Pix3 pa, pb;
         bool next_in_b = false;  // the next round's first pixel was loaded into pb
         if ((int)threadIdx.x < total) load_pix3(a, tf, tg, S.sg[S.bk[threadIdx.x]] + threadIdx.x, has_x, pa);
-        for (int r0 = 0; r0 < total; r0 += RB3, ++rpar) {
-            const int r1 = min(r0 + RB3, total);
+        for (int r0 = 0; r0 < total; r0 += (GATHER ? total : RB3), ++rpar) {
+            const int r1 = GATHER ? total : min(r0 + RB3, total);
             const int par = rpar & 1;
             // ---------------- pass 1 (flattened over the round; the next pixel's loads in flight)
             float vmax = 0.f, hmax = 0.f, sq = 0.f;
@@ -308,6 +312,7 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
                 const float2 prj = cmul(pv, f);
                 const float2 rr = make_float2(prj.x - cur.x.x, prj.y - cur.x.y);
                 sq = fmaf(rr.x, rr.x, fmaf(rr.y, rr.y, sq));
+                if constexpr (GATHER) return;
                 const float2 val = cmulconj(f, rr);
                 vmax = fmaxf(vmax, fmaxf(fabsf(val.x), fabsf(val.y)));
 #if FSLD_V3_FULLW
@@ -359,6 +364,7 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
             }
             __syncthreads();
             if (r1 >= total && S.ring_desc[nxs].x >= 0) stage_item3(nxs);  // overlaps pass 2 + flush
+            if constexpr (GATHER) continue;
             // ---------------- pass 2: fixed-point adjoint scatter (kernels.py:221-230)
             {
                 // one power-of-two scale per item and accumulator, non-increasing over its rounds: a
@@ -507,7 +513,7 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
         // flush of the item: one reduction per touched voxel, accumulators re-zeroed
         const int4 igeo = S.ring_geo[cur];
 #pragma unroll
-        for (int u = 0; u < BU; ++u) {
+        for (int u = 0; u < (GATHER ? 0 : BU); ++u) {
             if (lxyz(u) < 0) continue;
             const int l = threadIdx.x + u * BTHREADS;
             const int qr = S.accr[l], qi = S.acci[l];

@@ -462,6 +462,20 @@ int fsld_loss_sorted(int M, int mode, int n_mask, const fsld_image_rec* recs, co
                         scratch, scratch_bytes, stream);
 }
 
+int fsld_loss_sorted_tab(int M, int mode, int n_mask, const fsld_image_rec* recs, const int32_t* idx, int B,
+                         const void* v, const void* xs, const int8_t* pc, const void* ptab, const int32_t* seg_off,
+                         const int32_t* segs, double* sq_out, void* scratch, size_t scratch_bytes, void* stream) {
+    if (!ptab || mode != FSLD_MODE_TRI || !seg_off || !segs)  // (no tables / nn: the tile kernel)
+        return fsld_loss_sorted(M, mode, n_mask, recs, idx, B, v, xs, pc, sq_out, scratch, scratch_bytes, stream);
+    if (!geom_ok(M, mode, n_mask, B) || M > 256 || !recs || !v || !xs || !pc || !sq_out || !scratch)
+        return FSLD_EINVAL;
+    const ScratchLayout L = scratch_layout(M, n_mask, B);
+    if (scratch_bytes < L.total) return FSLD_EINVAL;
+    SortedArgs b = make_sorted(L, M, n_mask, B, recs, idx, v, xs, pc, seg_off, segs, nullptr, scratch, ptab);
+    forget_bins(scratch);  // (these work items replace whatever the scratch held)
+    return status_of(launch_sorted_loss_tab(b, sq_out, reinterpret_cast<cudaStream_t>(stream)));
+}
+
 int fsld_project_sorted(int M, int mode, int n_mask, const fsld_image_rec* recs, const int32_t* idx, int B,
                         const void* v, const int8_t* pc, void* out, void* stream) {
     if (!geom_ok(M, mode, n_mask, B) || !recs || !v || !pc || !out) return FSLD_EINVAL;

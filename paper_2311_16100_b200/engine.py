@@ -454,6 +454,13 @@ class SliceEngine:
         B = idx.numel()
         sq = torch.empty(1, dtype=torch.float64, device=self.dev)
         scr = self.scratch(B)
+        if self.layout == "sorted" and self.table_path and self.mode == "tri":  # brick projection pass
+            C.check(lib.fsld_loss_sorted_tab(self.M, self.mode_id, self.n_mask, ctypes_ptr(self.recs), ctypes_ptr(idx),
+                                             B, ctypes_ptr(v), ctypes_ptr(self.x), ctypes_ptr(self.pc),
+                                             ctypes_ptr(self.ptab), ctypes_ptr(self.seg_off), ctypes_ptr(self.segs),
+                                             ctypes_ptr(sq), ctypes_ptr(scr), scr.numel() * 8, _stream()),
+                    "fsld_loss_sorted_tab")
+            return sq
         if self.layout == "sorted":
             C.check(lib.fsld_loss_sorted(self.M, self.mode_id, self.n_mask, ctypes_ptr(self.recs), ctypes_ptr(idx), B,
                                          ctypes_ptr(v), ctypes_ptr(self.x), ctypes_ptr(self.pc), ctypes_ptr(sq),
