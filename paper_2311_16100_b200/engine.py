@@ -490,6 +490,15 @@ class SliceEngine:
         lib = C.load()
         idx = self.idx_tensor(idx)
         acc = self.new_cacc() if acc is None else acc
+        if self.table_path and self.mode == "tri":
+            # the brick kernel with v = 0: its accumulator collects sum P^* conj(f) (0 - x) = -b
+            zero = getattr(self, "_zero_vol", None)
+            if zero is None:
+                zero = self._zero_vol = torch.zeros(self.n_voxels, dtype=torch.complex64, device=self.dev)
+            neg = torch.zeros(self.n_voxels, dtype=torch.complex64, device=self.dev)
+            self.loss_grad(zero, idx, acc=neg)
+            acc.sub_(neg)
+            return acc, fx
         if self.deterministic and fx is None:
             fx = self.fixed_scale(self.x, HITS_PER_IMAGE * idx.numel(), 0.0)
         C.check(lib.fsld_backproject_sorted(self.M, self.mode_id, self.n_mask, ctypes_ptr(self.recs),
