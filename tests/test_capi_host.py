@@ -56,6 +56,18 @@ def test_invalid_arguments_rejected_without_gpu():
     assert st == C.FSLD_EINVAL  # deterministic without a fixed-point scale
     with pytest.raises(ValueError):
         C.check(C.FSLD_EINVAL, "x")
+    # numpy-signature host step: missing / misaligned host arrays are refused before any device work
+    args = (128, C.MODE_TRI, 12645, 1, 1, 512)
+    tail = (1, 1, 1, 1, 1, 1.0, 1e-3)
+    st = lib.fsld_loss_grad_host_np(*args, 0, *tail, 16, 16, 16, 16, 16, 12, 16, 1 << 30, 0)
+    assert st == C.FSLD_EINVAL  # v = NULL
+    st = lib.fsld_loss_grad_host_np(*args, 24, *tail, 8, 16, 16, 16, 16, 12, 16, 1 << 30, 0)
+    assert st == C.FSLD_EINVAL  # gradient not 16-byte aligned
+    st = lib.fsld_loss_grad_host_np(*args, 16, *tail, 16, 16, 16, 16, 16, 99, 16, 1 << 30, 0)
+    assert st == C.FSLD_EINVAL  # n_slabs out of range
+    # table loss pass: an empty batch is refused
+    st = lib.fsld_loss_sorted_tab(128, C.MODE_TRI, 12645, 1, 1, 0, 1, 1, 1, 1, 1, 1, 1, 1, 1 << 30, 0)
+    assert st == C.FSLD_EINVAL
 
 
 def test_scratch_bytes_grows_with_batch():
