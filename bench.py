@@ -739,7 +739,36 @@ def next_rows_leg(eng, wl):
 
     out = {"n_images": n}
     ms = timed(lambda: eng.exact_diag_acc(idx))
-    out["exact_diag"] = {"ms": ms, "images_per_s": n / (ms * 1e-3), "path": "fsld_exact_diag (hessian.exact_diag)"}
+    brick_diag = eng.layout == "sorted" and eng.ptab is not None and eng.mode == "tri"
+    out["exact_diag"] = {"ms": ms, "images_per_s": n / (ms * 1e-3),
+                         "path": ("fsld_exact_diag_sorted_tab (table-driven brick kernel, DIAG pass; "
+                                  "hessian.exact_diag)" if brick_diag else "fsld_exact_diag (hessian.exact_diag)")}
+    if brick_diag:  # the deterministic call hessian.exact_diag makes, and the tile kernel it replaced
+        from paper_2311_16100_b200 import _capi as C
+        from paper_2311_16100_b200.engine import HITS_PER_IMAGE, ctypes_ptr, _stream
+
+        lib = C.load()
+        acc64 = torch.zeros(eng.n_voxels, dtype=torch.int64, device=dev)
+        accf = torch.zeros(eng.n_voxels, dtype=torch.float32, device=dev)
+        fxd = eng.fixed_scale(None, HITS_PER_IMAGE * n, 1.0)
+        scr = eng.scratch(1024)
+
+        def diag_det():
+            for lo in range(0, n, 1024):
+                sub = idx[lo:lo + 1024]
+                C.check(lib.fsld_exact_diag_sorted_tab(eng.M, eng.mode_id, eng.n_mask, ctypes_ptr(eng.recs),
+                                                       ctypes_ptr(sub), sub.numel(), ctypes_ptr(eng.pc),
+                                                       ctypes_ptr(eng.ptab), ctypes_ptr(eng.seg_off),
+                                                       ctypes_ptr(eng.segs), ctypes_ptr(acc64), C.DETERMINISTIC,
+                                                       ctypes_ptr(fxd), ctypes_ptr(scr), scr.numel() * 8, _stream()),
+                        "exact_diag_sorted_tab")
+
+        def diag_tile():
+            C.check(lib.fsld_exact_diag(eng.M, eng.mode_id, eng.n_mask, ctypes_ptr(eng.pix), ctypes_ptr(eng.recs),
+                                        ctypes_ptr(idx), n, ctypes_ptr(accf), 0, None, _stream()), "exact_diag")
+
+        out["exact_diag"]["deterministic_ms"] = timed(diag_det)
+        out["exact_diag"]["tile_kernel_ms"] = timed(diag_tile)
     ms = timed(lambda: eng.backproject_dataset(idx))
     out["b_vector"] = {"ms": ms, "images_per_s": n / (ms * 1e-3), "path": "fsld_backproject_sorted (b_vector)"}
     ms = timed(lambda: eng.hvp_acc(z, idx))

@@ -191,6 +191,17 @@ int fsld_exact_diag(int M, int mode, int n_mask, const int16_t* pix,
                     const fsld_image_rec* recs, const int32_t* idx, int B,
                     void* acc, unsigned flags, const double* fx_scale, void* stream);
 
+/* fsld_exact_diag on the table-driven brick kernel (trilinear; the dataset's sorted layout and
+ * tables, fsld_sorted_tables): acc[j] += sum_b,p C^2 w_pj^2 for the B images idx (no volume, no
+ * images read).  acc is fp32, or with FSLD_DETERMINISTIC int64 at *fx_scale -- then bitwise the
+ * same for any launch grid and batch order, and B <= 1024 per call.  scratch as fsld_scratch_bytes(B).
+ * Replaces kernels.scatter_sq_tri (kernels.py:251-294) as called by hessian.exact_diag
+ * (hessian.py:62-107). */
+int fsld_exact_diag_sorted_tab(int M, int mode, int n_mask, const fsld_image_rec* recs, const int32_t* idx, int B,
+                               const int8_t* pc, const void* ptab, const int32_t* seg_off, const int32_t* segs,
+                               void* acc, unsigned flags, const double* fx_scale, void* scratch, size_t scratch_bytes,
+                               void* stream);
+
 /* Nearest-neighbour voxel index per (image, pixel), int32 (B, n_mask); bit-exact with
  * kernels.assign_nn (kernels.py:123-135). */
 int fsld_assign_nn(int M, int n_mask, const int16_t* pix, const fsld_image_rec* recs,

@@ -82,6 +82,7 @@ SIGNATURES = {
     "fsld_pack_probes": (I, [I64, I, P, P, P, P]),
     "fsld_gen_probes": (I, [I64, I, ctypes.c_uint64, P, P]),
     "fsld_exact_diag": (I, [I, I, I, P, P, P, I, P, U, P, P]),
+    "fsld_exact_diag_sorted_tab": (I, [I, I, I, P, P, I, P, P, P, P, P, U, P, P, SZ, P]),
     "fsld_assign_nn": (I, [I, I, P, P, P, I, P, P]),
     "fsld_project_tab": (I, [I, I, I, P, P, I, P, P, P, P]),
     "fsld_backproject_tab": (I, [I, I, I, P, P, I, P, P, P, U, P, P]),

@@ -676,6 +676,32 @@ cudaError_t launch_sorted_loss_tab(const SortedArgs& a, double* sq_out, cudaStre
     return launch_reduce(a.part, grid, sq_out, s);
 }
 
+// Exact Hessian diagonal (data term) of a batch of a table-built dataset, trilinear: binning + the
+// table-driven kernel's DIAG pass (a.fold += sum C^2 w^2; DET: int64 at *a.fxp, bitwise the same for
+// any grid and batch order, B <= kDetMaxBatch).
+cudaError_t launch_sorted_diag(const SortedArgs& a0, cudaStream_t s) {
+    SortedArgs a = a0;
+    cudaError_t e = launch_sorted_bin(a, s);
+    if (e != cudaSuccess) return e;
+    int grid = 0;
+    if (a.det) {
+        static GridCache cache;
+        e = persistent_grid(cache, brick_loss_grad_kernel<false, false, true, false, true>, sizeof(BrickSmem3T<true>), grid);
+        if (e != cudaSuccess) return e;
+        if (const char* g = getenv("FSLD_DET_GRID")) {
+            const int want = atoi(g);
+            if (want > 0 && want < grid) grid = want;
+        }
+        brick_loss_grad_kernel<false, false, true, false, true><<<grid, BTHREADS, sizeof(BrickSmem3T<true>), s>>>(a);
+    } else {
+        static GridCache cache;
+        e = persistent_grid(cache, brick_loss_grad_kernel<false, false, false, false, true>, sizeof(BrickSmem3T<true>), grid);
+        if (e != cudaSuccess) return e;
+        brick_loss_grad_kernel<false, false, false, false, true><<<grid, BTHREADS, sizeof(BrickSmem3T<true>), s>>>(a);
+    }
+    return cudaGetLastError();
+}
+
 // Deterministic loss+grad on the table-driven kernel: bitwise the same gradient (int64 pairs at
 // scale *a.fxp, accumulated in a.acc) and loss for any launch grid and any order of the batch.
 cudaError_t launch_sorted_loss_grad_det(const SortedArgs& a0, double* sq_out, cudaStream_t s) {

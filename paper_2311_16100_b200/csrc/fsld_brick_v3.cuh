@@ -112,18 +112,24 @@ __device__ __forceinline__ void load_pix3(const SortedArgs& a, const float2* tf,
 // GATHER: the projection pass alone -- sum |f P v - x|^2 over the work items (optim.py:193-207, the
 // batch_loss data term; the full-dataset loss of each optim.run epoch), no round buffer, no scatter,
 // no flush; an item's pixels in one sweep.
-template <bool NN, bool HUTCH, bool DET, bool GATHER = false>
-__global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss_grad_kernel(SortedArgs a) {
+// DIAG: the exact Hessian diagonal's data term, fold_j += sum_p C_p^2 w_pj^2 (kernels.py:251-294,
+// hessian.py:62-107): no volume, no gathers, no images -- |f|^2 from the table and the squared
+// footprint weights scattered into the real fixed-point accumulator: a.fold (fp32), or with DET
+// int64 at the scale *a.fxp like the deterministic gradient.
+template <bool NN, bool HUTCH, bool DET, bool GATHER = false, bool DIAG = false>
+__global__ void __launch_bounds__(BTHREADS, (HUTCH || DIAG) ? 4 : FSLD_V3_MINB) brick_loss_grad_kernel(SortedArgs a) {
     static_assert(!(NN && HUTCH), "the fused probe is trilinear only");
     static_assert(!(DET && (NN || HUTCH)), "deterministic mode: trilinear loss+grad");
     static_assert(!(GATHER && (HUTCH || DET)), "the gather-only pass carries no probe and no fixed point");
+    static_assert(!(DIAG && (NN || HUTCH || GATHER)), "the exact diagonal is its own trilinear pass");
+    constexpr bool RACC = HUTCH || DIAG;  // the real accumulator (probe fold / diagonal)
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    BrickSmem3T<HUTCH>& S = *reinterpret_cast<BrickSmem3T<HUTCH>*>(smem_raw);
+    BrickSmem3T<RACC>& S = *reinterpret_cast<BrickSmem3T<RACC>*>(smem_raw);
     a.pairs += a.ctl[3];
     a.items += a.ctl[4];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int M = a.M, c = a.c, nb = a.nb;
-    const bool has_x = a.xs != nullptr;
+    const bool has_x = !DIAG && a.xs != nullptr;
     const float2* tf = tab_f(a.ptab);
     const float4* tg = tab_geo(a.ptab, reinterpret_cast<const TabHeader*>(a.ptab)->npx);
     double lsum = 0.0;
@@ -140,7 +146,7 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
         if (l < BH3) {
             S.accr[l] = 0;
             S.acci[l] = 0;
-            if (HUTCH) S.acch[l] = 0;
+            if (RACC) S.acch[l] = 0;
         }
     }
     constexpr int kClaimer = BTHREADS - 32;
@@ -174,7 +180,7 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
             const int jv = voxel_j(geo, u);
             const bool in = jv >= 0;
             const int j = in ? jv : 0;
-            cp_async8_zfill(S.vb + l, a.v + j, in);
+            if (!DIAG) cp_async8_zfill(S.vb + l, a.v + j, in);
             if (HUTCH) S.zs[l] = in ? (unsigned char)(__ldg(a.zbits + j) & 1u) : 0;
         }
     };
@@ -184,7 +190,7 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
     }
     if (threadIdx.x < 2) {
         S.vmax2[threadIdx.x] = 0;
-        if (HUTCH) S.hmax2[threadIdx.x] = 0;
+        if (RACC) S.hmax2[threadIdx.x] = 0;
     }
     __syncthreads();
     int cur = 0;  // ring slot of the current item
@@ -289,6 +295,18 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
                 const int l0 = __float_as_int(cur.geo.w);
                 const float ax = 1.f - wx, ay = 1.f - wy, az = 1.f - wz;
                 const float2 f = cur.f;
+                if constexpr (DIAG) {  // |f|^2 = C^2 (the phase has modulus 1) and the footprint
+                    const float h = fmaf(f.x, f.x, f.y * f.y);
+                    S.hval[e - r0] = h;
+                    hmax = fmaxf(hmax, h);
+#if FSLD_V3_FULLW
+                    S.bgeo[e - r0] = cur.geo;
+#else
+                    const uint2 gp = geo_pack(cur.geo);
+                    S.brec[e - r0] = make_uint4(0u, 0u, gp.x, gp.y);
+#endif
+                    return;
+                }
                 const float2* vb = S.vb + l0;
                 float2 pv;
                 if (NN) {
@@ -357,7 +375,7 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
             {
                 const int vb_max = __reduce_max_sync(0xffffffffu, __float_as_int(vmax));
                 if (lane == 0) atomicMax(&S.vmax2[par], vb_max);
-                if (HUTCH) {
+                if (RACC) {
                     const int hb_max = __reduce_max_sync(0xffffffffu, __float_as_int(hmax));
                     if (lane == 0) atomicMax(&S.hmax2[par], hb_max);
                 }
@@ -396,7 +414,7 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
                     item_inv_sc = inv_r;
                     sync = true;
                 }
-                if (HUTCH) {
+                if (RACC) {
                     float inv_h;
                     const float sh_r = pow2_scale(lim, __int_as_float(S.hmax2[par]), inv_h);
                     if (r0 == 0) {
@@ -450,8 +468,13 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
                 const float2 w45 = __fmul2_rn(make_float2(z1.x, z1.x), AW), w67 = __fmul2_rn(make_float2(z1.y, z1.y), AW);
                 const float w8[8] = {w01.x, w01.y, w23.x, w23.y, w45.x, w45.y, w67.x, w67.y};
                 const int off8[8] = {0, 1, BH, BH + 1, BH * BH, BH * BH + 1, BH * BH + BH, BH * BH + BH + 1};
+                if constexpr (DIAG) {  // C^2 w^2 per corner
+                    const float h = S.hval[e] * item_sch;
 #pragma unroll
-                for (int q = 0; q < 8; ++q) {
+                    for (int q = 0; q < 8; ++q) atomicAdd(S.acch + l0 + off8[q], __float2int_rn(w8[q] * w8[q] * h));
+                }
+#pragma unroll
+                for (int q = 0; q < (DIAG ? 0 : 8); ++q) {
 #if FSLD_V3_F2I
                     const float2 y = __fmul2_rn(make_float2(w8[q], w8[q]), val);
                     const int qr = __float2int_rn(y.x), qi = __float2int_rn(y.y);
@@ -479,7 +502,7 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
             }
             if (threadIdx.x == 0) {  // the next round's slots (unused since this round's barrier)
                 S.vmax2[par ^ 1] = 0;
-                if (HUTCH) S.hmax2[par ^ 1] = 0;
+                if (RACC) S.hmax2[par ^ 1] = 0;
             }
             __syncthreads();
         }
@@ -502,7 +525,7 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
         }
         // item value q at scale 2^esc -> q * 2^(efx - esc) at the deterministic scale (exact left
         // shift; a right shift rounds, for items whose values are below the scale's resolution)
-        const int dsh = DET ? efx - (((__float_as_int(item_sc) >> 23) & 0xff) - 127) : 0;
+        const int dsh = DET ? efx - (((__float_as_int(DIAG ? item_sch : item_sc) >> 23) & 0xff) - 127) : 0;
         auto to_fixed = [dsh](int q) -> unsigned long long {
             long long r;
             if (dsh >= 0) r = (long long)q << min(dsh, 62);
@@ -517,11 +540,11 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
             if (lxyz(u) < 0) continue;
             const int l = threadIdx.x + u * BTHREADS;
             const int qr = S.accr[l], qi = S.acci[l];
-            const int qh = HUTCH ? S.acch[l] : 0;
+            const int qh = RACC ? S.acch[l] : 0;
             if ((qr | qi | qh) == 0) continue;
             S.accr[l] = 0;
             S.acci[l] = 0;
-            if (HUTCH) S.acch[l] = 0;
+            if (RACC) S.acch[l] = 0;
             const int jv = voxel_j(igeo, u);
             if (jv < 0) continue;
             const size_t j = (size_t)jv;
@@ -533,6 +556,8 @@ __global__ void __launch_bounds__(BTHREADS, HUTCH ? 4 : FSLD_V3_MINB) brick_loss
                 const float fs = item_inv_sc * a.out_scale;
                 red_f32x2(reinterpret_cast<float*>(a.acc) + 2 * j, (float)qr * fs, (float)qi * fs);
             }
+            if (DIAG && DET) atomicAdd(reinterpret_cast<unsigned long long*>(a.fold) + j, to_fixed(qh));
+            else if (DIAG) atomicAdd(a.fold + j, (float)qh * item_inv_sch);  // diag_j += sum C^2 w^2
             if (HUTCH && qh != 0) {  // fold_j += z_j h_j
                 const float hz = (S.zc[l] & 1u) ? (float)qh * item_inv_sch : -(float)qh * item_inv_sch;
                 atomicAdd(a.fold + j, hz);

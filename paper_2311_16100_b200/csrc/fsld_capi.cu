@@ -476,6 +476,24 @@ int fsld_loss_sorted_tab(int M, int mode, int n_mask, const fsld_image_rec* recs
     return status_of(launch_sorted_loss_tab(b, sq_out, reinterpret_cast<cudaStream_t>(stream)));
 }
 
+int fsld_exact_diag_sorted_tab(int M, int mode, int n_mask, const fsld_image_rec* recs, const int32_t* idx, int B,
+                               const int8_t* pc, const void* ptab, const int32_t* seg_off, const int32_t* segs,
+                               void* acc, unsigned flags, const double* fx_scale, void* scratch, size_t scratch_bytes,
+                               void* stream) {
+    if (!geom_ok(M, mode, n_mask, B) || M > 256 || mode != FSLD_MODE_TRI) return FSLD_EINVAL;
+    if (!recs || !pc || !ptab || !seg_off || !segs || !acc || !scratch) return FSLD_EINVAL;
+    const bool det = (flags & FSLD_DETERMINISTIC) != 0;
+    if (det && (!fx_scale || B > kDetMaxBatch)) return FSLD_EINVAL;
+    const ScratchLayout L = scratch_layout(M, n_mask, B);
+    if (scratch_bytes < L.total) return FSLD_EINVAL;
+    SortedArgs b = make_sorted(L, M, n_mask, B, recs, idx, nullptr, nullptr, pc, seg_off, segs, nullptr, scratch, ptab);
+    b.fold = reinterpret_cast<float*>(acc);
+    b.det = det ? 1 : 0;
+    b.fxp = fx_scale;
+    forget_bins(scratch);
+    return status_of(launch_sorted_diag(b, reinterpret_cast<cudaStream_t>(stream)));
+}
+
 int fsld_project_sorted(int M, int mode, int n_mask, const fsld_image_rec* recs, const int32_t* idx, int B,
                         const void* v, const int8_t* pc, void* out, void* stream) {
     if (!geom_ok(M, mode, n_mask, B) || !recs || !v || !pc || !out) return FSLD_EINVAL;

@@ -173,6 +173,7 @@ cudaError_t launch_sorted_tables(int M, int n_mask, int mode, const fsld_image_r
 cudaError_t launch_sorted_loss_grad(const SortedArgs& a, double* sq_out, cudaStream_t s);
 cudaError_t launch_sorted_loss_grad_det(const SortedArgs& a, double* sq_out, cudaStream_t s);
 cudaError_t launch_sorted_loss_tab(const SortedArgs& a, double* sq_out, cudaStream_t s);
+cudaError_t launch_sorted_diag(const SortedArgs& a, cudaStream_t s);
 constexpr int kDetMaxBatch = 1024;  // deterministic brick path: <= 2 segments per image and brick -> 2048 per sort
 cudaError_t launch_planned_loss_grad(const SortedArgs& a, double* sq_out, cudaStream_t s);
 cudaError_t launch_sorted_bin(const SortedArgs& a, cudaStream_t s);

@@ -621,6 +621,20 @@ class SliceEngine:
         acc = self.new_racc() if acc is None else acc
         if self.deterministic and fx is None:
             fx = self.fixed_scale(None, HITS_PER_IMAGE * (fx_batch or B), 1.0)
+        if (self.layout == "sorted" and self.ptab is not None and self.mode == "tri" and
+                not (self.flags & C.TILE_PATH)):
+            # the table-driven brick kernel's DIAG pass (deterministic: <= 1024 images per call)
+            chunk = 1024 if self.deterministic else self.HVP_CHUNK
+            for lo in range(0, B, chunk):
+                sub = idx[lo:lo + chunk]
+                nb = sub.numel()
+                scr = self.scratch(nb)
+                C.check(lib.fsld_exact_diag_sorted_tab(self.M, self.mode_id, self.n_mask, ctypes_ptr(self.recs),
+                                                       ctypes_ptr(sub), nb, ctypes_ptr(self.pc), ctypes_ptr(self.ptab),
+                                                       ctypes_ptr(self.seg_off), ctypes_ptr(self.segs), ctypes_ptr(acc),
+                                                       self.flags, ctypes_ptr(fx), ctypes_ptr(scr), scr.numel() * 8,
+                                                       _stream()), "fsld_exact_diag_sorted_tab")
+            return acc, fx
         C.check(lib.fsld_exact_diag(self.M, self.mode_id, self.n_mask, ctypes_ptr(self.pix),
                                     ctypes_ptr(self.recs), ctypes_ptr(idx), B, ctypes_ptr(acc), self.flags,
                                     ctypes_ptr(fx), _stream()), "fsld_exact_diag")

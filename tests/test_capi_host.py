@@ -68,6 +68,13 @@ def test_invalid_arguments_rejected_without_gpu():
     # table loss pass: an empty batch is refused
     st = lib.fsld_loss_sorted_tab(128, C.MODE_TRI, 12645, 1, 1, 0, 1, 1, 1, 1, 1, 1, 1, 1, 1 << 30, 0)
     assert st == C.FSLD_EINVAL
+    # brick exact diagonal: nn mode, missing tables, deterministic without a scale or with B > 1024
+    dg = lib.fsld_exact_diag_sorted_tab
+    assert dg(128, C.MODE_NN, 12645, 1, 1, 8, 1, 1, 1, 1, 1, 0, 0, 1, 1 << 30, 0) == C.FSLD_EINVAL
+    assert dg(128, C.MODE_TRI, 12645, 1, 1, 8, 1, 0, 1, 1, 1, 0, 0, 1, 1 << 30, 0) == C.FSLD_EINVAL
+    assert dg(128, C.MODE_TRI, 12645, 1, 1, 8, 1, 1, 1, 1, 1, C.DETERMINISTIC, 0, 1, 1 << 30, 0) == C.FSLD_EINVAL
+    assert dg(128, C.MODE_TRI, 12645, 1, 1, 2048, 1, 1, 1, 1, 1, C.DETERMINISTIC, 1, 1, 1 << 40, 0) == C.FSLD_EINVAL
+    assert dg(128, C.MODE_TRI, 12645, 1, 1, 8, 1, 1, 1, 1, 1, 0, 0, 1, 16, 0) == C.FSLD_EINVAL  # scratch too small
 
 
 def test_scratch_bytes_grows_with_batch():
