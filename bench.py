@@ -414,7 +414,37 @@ def run_b200(args):
         # ball gather / scatter + epilogue (2)
         launches_per_step = 3 if not dp else 6
 
+    # N > 1 on NVSwitch: the exchange rides on the brick pass (each item's flush is a multimem.red into
+    # every rank's copy of the accumulator, dist.NvlsGroup) instead of the all-reduce after it;
+    # FSLD_COMM=nccl keeps the packed NCCL all-reduce
+    nvg, comm_note = None, "nccl"
+    if dp and use_plan and eng.table_path and not single and os.environ.get("FSLD_COMM", "nvls") == "nvls":
+        from paper_2311_16100_b200.dist import NvlsGroup, nvls_available
+
+        ok = [nvls_available(local)]
+        if world > 1:
+            oks = [None] * world
+            dist.all_gather_object(oks, ok[0])
+            ok = oks
+        if all(ok):
+            try:
+                nvg = NvlsGroup(M ** 3)
+                comm_note = "nvls"
+            except Exception as exc:  # (every rank raises together: NvlsGroup agrees on each phase)
+                comm_note = f"nccl (NVLS set-up failed: {exc})"
+        else:
+            comm_note = "nccl (no multicast support reported)"
+    sq_tot = torch.empty(1, dtype=torch.float64, device=dev)
+    if nvg is not None:
+        launches_per_step = 6  # barrier, brick kernel, loss reduce, barrier, epilogue (2)
+
     def planned_step(plan, k, ev_k0=None, ev_k1=None, fused=False):
+        if nvg is not None:
+            from paper_2311_16100_b200.dist import nvls_planned_step
+
+            nvls_planned_step(eng, nvg, plan, k, v, scale, lam, grad, sq, sq_tot, loss, nscr,
+                              events=(ev_k0, ev_k1) if ev_k0 is not None else None)
+            return loss
         if fused and not dp:  # the whole step in one call: grad = lam v, brick pass adds s * sum, finalize
             eng.loss_grad_step_planned(v, plan, k, scale, lam, grad, sq=sq, loss=loss)
             return loss
@@ -563,10 +593,15 @@ def run_b200(args):
                                "complex64 images / volume / gradient, fp32 coordinates, CTF and shift phases as exact "
                                "64-bit fixed-point turns; int32 fixed-point shared-memory adjoint; fp64 loss sums"),
                 "n_images_per_gpu": eng.n_images, "l2": "flushed between timed steps (512 MB write)",
-                "allreduce_bytes": (8 * nball + 8) if dp else 0,
-                "collectives_per_step": 1 if dp else 0,
+                "allreduce_bytes": (8 * nball + 8) if dp and nvg is None else 0,
+                "collectives_per_step": 1 if dp and nvg is None else 0,
+                "exchange": (("NVLS: per-item multimem.red.add.v2.f32 flush into the multicast accumulator "
+                              "(every rank's copy), 2 barrier kernels per step, |r|^2 slots summed in rank order")
+                             if nvg is not None else comm_note if dp else "none (one GPU)"),
                 "step": graph_note + (" of fsld_loss_grad_step_planned (grad = lam v, the brick pass adds scale * its "
                                       "sums into grad, loss finalize)" if use_plan and not dp else
+                                      " of barrier + brick pass flushing into the NVLS multicast accumulator + "
+                                      "barrier + epilogue" if nvg is not None else
                                       " of brick pass + ball gather + all_reduce([grad acc | sq]) + ball scatter + "
                                       "epilogue" if dp else ""),
                 "binning": (f"plan of the {args.steps} timed batches (fsld_plan_build), built inside the "
@@ -592,6 +627,9 @@ def run_b200(args):
         if sweep is not None:
             line["hutchinson_sweep"] = sweep
         print(json.dumps(line), flush=True)
+    if nvg is not None:
+        nvg.check()
+        nvg.close()
     if dp:
         dist.destroy_process_group()
 

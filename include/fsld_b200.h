@@ -552,6 +552,50 @@ int fsld_host_cast_f32_to_f64(const float* src, double* dst, int64_t n);
 int fsld_ball_gather(int64_t n, const int32_t* idx, const void* src, void* dst, int elem_bytes, void* stream);
 int fsld_ball_scatter(int64_t n, const int32_t* idx, const void* src, void* dst, int elem_bytes, void* stream);
 
+/*
+ * Data-parallel gradient exchange through NVSwitch multicast (NVLS), fused into the brick pass.
+ * The loss is a sum over images (optim.py:186-189; the per-rank partial sums of a sharded dataset
+ * add), so every rank maps one multicast object over its own copy of the gradient accumulator and
+ * the brick kernel's per-item flush reduces into the multicast address (multimem.red): NVSwitch
+ * applies each flush to every copy while the pass runs, and after fsld_nvls_barrier each rank's copy
+ * holds the sum over all ranks -- no all-reduce after the pass.  Replaces the NCCL all-reduce of
+ * the touched-ball vector (fsld_ball_gather / fsld_ball_scatter) on NVSwitch systems.
+ *   rank 0       : fsld_nvls_create -> size, fd (a POSIX fd for n_ranks > 1, else -1)
+ *   rank r > 0   : receive the fd (fsld_fd_listen before rank 0 sends, fsld_fd_send, fsld_fd_recv),
+ *                  fsld_nvls_import(fd, n_ranks, r, data_bytes, size)
+ *   every rank   : fsld_nvls_add_device (current device) ; [all ranks] ; fsld_nvls_bind -> uc, mc
+ *   per step     : fsld_nvls_barrier(NULL, NULL)  -- every copy zeroed by its rank's epilogue
+ *                  fsld_loss_grad_planned_mc(..., mc, ...)  -- the pass, flushing into the multicast
+ *                  fsld_nvls_barrier(sq, sq_total)  -- all flushes landed; |r|^2 summed in rank order
+ *                  fsld_grad_epilogue on uc (grad = scale uc + lam v, uc <- 0)
+ * data_bytes: the accumulator (M^3 complex64); the bound range also holds the barrier word and the
+ * per-rank |r|^2 slots at fsld_nvls_ctl_offset(data_bytes).  A barrier that waits > 20 s for a peer
+ * gives up and fsld_nvls_status returns FSLD_ECUDA.  fsld_nvls_supported: the driver reports
+ * multicast support for the device AND creates a one-device multicast object (0 without a driver,
+ * on systems without NVSwitch multicast, or where the fabric's multicast service is not reachable).
+ */
+typedef struct fsld_nvls fsld_nvls;
+int fsld_nvls_supported(int device);
+size_t fsld_nvls_ctl_offset(size_t data_bytes);
+int fsld_nvls_create(int n_ranks, size_t data_bytes, size_t* size_out, int* fd_out, fsld_nvls** out);
+int fsld_nvls_import(int fd, int n_ranks, int rank, size_t data_bytes, size_t size, fsld_nvls** out);
+int fsld_nvls_add_device(fsld_nvls* g);
+int fsld_nvls_bind(fsld_nvls* g, void** uc_ptr, void** mc_ptr);
+int fsld_nvls_barrier(fsld_nvls* g, const double* sq_in, double* sq_out, void* stream);
+int fsld_nvls_status(fsld_nvls* g);
+int fsld_nvls_destroy(fsld_nvls* g);
+/* fd passing between processes of one node: SCM_RIGHTS over an abstract unix socket `name`.
+ * fsld_fd_listen binds (before the sender connects); fsld_fd_recv accepts one fd and closes the
+ * socket; fsld_fd_send connects (retrying for ~10 s) and sends. */
+int fsld_fd_listen(const char* name, int* sock_out);
+int fsld_fd_recv(int sock, int* fd_out);
+int fsld_fd_send(const char* name, int fd);
+/* fsld_loss_grad_planned (trilinear, tables, no probe) with grad_acc a MULTICAST address from
+ * fsld_nvls_bind: the flush reduces into every rank's copy.  sq_out: this rank's |r|^2. */
+int fsld_loss_grad_planned_mc(int M, int mode, int n_mask, const fsld_image_rec* recs, const void* plan, int B, int k,
+                              const void* v, const void* xs, const int8_t* pc, const void* ptab, void* grad_acc_mc,
+                              double* sq_out, void* scratch, size_t scratch_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

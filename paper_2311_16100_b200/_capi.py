@@ -124,6 +124,19 @@ SIGNATURES = {
     "fsld_plan_bytes": (SZ, [I, I, I, I, I64]),
     "fsld_plan_build": (I, [I, I, P, P, I, I, P, P, I64, P, SZ, P]),
     "fsld_loss_grad_planned": (I, [I, I, I, P, P, I, I, P, P, P, P, P, P, P, P, P, SZ, P]),
+    "fsld_loss_grad_planned_mc": (I, [I, I, I, P, P, I, I, P, P, P, P, P, P, P, SZ, P]),
+    "fsld_nvls_supported": (I, [I]),
+    "fsld_nvls_ctl_offset": (SZ, [SZ]),
+    "fsld_nvls_create": (I, [I, SZ, P, P, P]),
+    "fsld_nvls_import": (I, [I, I, I, SZ, SZ, P]),
+    "fsld_nvls_add_device": (I, [P]),
+    "fsld_nvls_bind": (I, [P, P, P]),
+    "fsld_nvls_barrier": (I, [P, P, P, P]),
+    "fsld_nvls_status": (I, [P]),
+    "fsld_nvls_destroy": (I, [P]),
+    "fsld_fd_listen": (I, [ctypes.c_char_p, P]),
+    "fsld_fd_recv": (I, [I, P]),
+    "fsld_fd_send": (I, [ctypes.c_char_p, I]),
     "fsld_proj_energy_planned": (I, [I, I, I, P, P, I, I, P, P, P, P, SZ, P]),
     "fsld_ball_scatter": (I, [I64, P, P, P, I, P]),
 }

@@ -554,7 +554,8 @@ __global__ void __launch_bounds__(BTHREADS, (HUTCH || DIAG) ? 4 : FSLD_V3_MINB) 
                 if (qi) atomicAdd(q64 + 1, to_fixed(qi));
             } else if ((qr | qi) != 0) {
                 const float fs = item_inv_sc * a.out_scale;
-                red_f32x2(reinterpret_cast<float*>(a.acc) + 2 * j, (float)qr * fs, (float)qi * fs);
+                if (a.mc) red_mc_f32x2(reinterpret_cast<float*>(a.acc) + 2 * j, (float)qr * fs, (float)qi * fs);
+                else red_f32x2(reinterpret_cast<float*>(a.acc) + 2 * j, (float)qr * fs, (float)qi * fs);
             }
             if (DIAG && DET) atomicAdd(reinterpret_cast<unsigned long long*>(a.fold) + j, to_fixed(qh));
             else if (DIAG) atomicAdd(a.fold + j, (float)qh * item_inv_sch);  // diag_j += sum C^2 w^2

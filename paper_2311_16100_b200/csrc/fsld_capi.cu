@@ -810,6 +810,19 @@ extern "C" int fsld_loss_grad_planned(int M, int mode, int n_mask, const fsld_im
     return status_of(launch_planned_loss_grad(b, sq_out, reinterpret_cast<cudaStream_t>(stream)));
 }
 
+extern "C" int fsld_loss_grad_planned_mc(int M, int mode, int n_mask, const fsld_image_rec* recs, const void* plan,
+                                         int B, int k, const void* v, const void* xs, const int8_t* pc,
+                                         const void* ptab, void* grad_acc_mc, double* sq_out, void* scratch,
+                                         size_t scratch_bytes, void* stream) {
+    if (!geom_ok(M, mode, n_mask, B) || M > 256 || mode != FSLD_MODE_TRI) return FSLD_EINVAL;
+    if (!recs || !plan || !v || !xs || !pc || !ptab || !grad_acc_mc || !sq_out || !scratch) return FSLD_EINVAL;
+    SortedArgs b;
+    if (!make_planned(b, plan, M, n_mask, B, k, recs, v, xs, pc, grad_acc_mc, scratch, scratch_bytes, ptab))
+        return FSLD_EINVAL;
+    b.mc = 1;
+    return status_of(launch_planned_loss_grad(b, sq_out, reinterpret_cast<cudaStream_t>(stream)));
+}
+
 extern "C" int fsld_loss_grad_step_planned(int M, int mode, int n_mask, const fsld_image_rec* recs, const void* plan,
                                            int B, int k, const void* v, const void* xs, const int8_t* pc,
                                            const void* ptab, double scale, double lam, void* grad, double* sq_out, double* loss,

@@ -171,6 +171,11 @@ __device__ __forceinline__ void red_f32x2(float* addr, float x, float y) {
     asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(addr), "f"(x), "f"(y) : "memory");
 }
 
+// the same on a multicast address (fsld_nvls_bind): NVSwitch adds into every rank's copy
+__device__ __forceinline__ void red_mc_f32x2(float* addr, float x, float y) {
+    asm volatile("multimem.red.relaxed.sys.global.add.v2.f32 [%0], {%1, %2};" ::"l"(addr), "f"(x), "f"(y) : "memory");
+}
+
 __device__ __forceinline__ void red_fixed(long long* addr, double val, double fx) {
     atomicAdd(reinterpret_cast<unsigned long long*>(addr),
               static_cast<unsigned long long>(__double2ll_rn(val * fx)));

@@ -145,6 +145,7 @@ struct SortedArgs {
     int* gate;               // non-NULL: the binning kernels run only if *gate != 0 (set by the check)
     int cap_pairs, cap_items;
     float out_scale;         // the flush adds out_scale * (sum of contributions) to acc (1 = plain accumulator)
+    int mc;                  // acc is a multicast address (fsld_nvls): the flush is multimem.red (table kernel)
     // fused step (table-driven kernel, fsld_loss_grad_step_planned): acc = lam v first (each CTA a
     // slice, ||v||^2 partials in fnorm), the flushes wait until every slice is written (ctl[6]), and
     // the last CTA to finish (ctl[7]) forms *fsq / *floss and re-arms both counters -- the whole

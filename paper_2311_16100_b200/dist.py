@@ -214,3 +214,145 @@ def sharded_step(op, v, batch, lam: float, n_total: int | None = None, buf: Pack
     if buf.with_hutch and k > 0:
         hs = (scale / k) * buf.work_hutch().double() + lam
     return loss, grad, hs
+
+
+def exchange_fd(fd: int, group=None, tag: str = "fsld") -> int:
+    """Rank 0's file descriptor, duplicated into every rank of the node (SCM_RIGHTS over abstract
+    unix sockets, fsld_fd_listen / fsld_fd_send / fsld_fd_recv).  Rank 0 returns its own fd."""
+    import ctypes
+    import uuid
+
+    from . import _capi as C
+
+    lib = C.load()
+    rank, ws = dist.get_rank(group), dist.get_world_size(group)
+    token = [uuid.uuid4().hex[:16] if rank == 0 else None]
+    dist.broadcast_object_list(token, src=0, group=group)
+    name = lambda r: f"{tag}-{token[0]}-{r}".encode()  # noqa: E731
+    sock = ctypes.c_int(-1)
+    if rank > 0:
+        C.check(lib.fsld_fd_listen(name(rank), ctypes.byref(sock)), "fd_listen")
+    dist.barrier(group)
+    if rank == 0:
+        for r in range(1, ws):
+            C.check(lib.fsld_fd_send(name(r), int(fd)), "fd_send")
+        out = int(fd)
+    else:
+        got = ctypes.c_int(-1)
+        C.check(lib.fsld_fd_recv(sock.value, ctypes.byref(got)), "fd_recv")
+        out = got.value
+    dist.barrier(group)
+    return out
+
+
+class NvlsGroup:
+    """A gradient accumulator shared through NVSwitch multicast (include/fsld_b200.h, fsld_nvls_*).
+
+    Every rank holds a local copy (``uc``, read and zeroed by its epilogue) and the multicast
+    address (``mc``) its brick pass flushes into: each flush lands in every rank's copy, so after
+    ``barrier(sq, sq_total)`` all copies hold the sum over ranks of the partial adjoints and
+    sq_total the sum of the ranks' |r|^2 in rank order -- the exchange rides on the pass instead of
+    an all-reduce after it (optim.py:186-189: the objective is a sum over images).
+    With no process group (or world 1) the group has one member: the same kernels, no exchange.
+    """
+
+    def __init__(self, n_voxels: int, group=None):
+        import ctypes
+
+        from . import _capi as C
+
+        self._C = C
+        lib = C.load()
+        multi = dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1
+        ws = dist.get_world_size(group) if multi else 1
+        rank = dist.get_rank(group) if multi else 0
+        self.n_ranks, self.rank = ws, rank
+        self.data_bytes = int(n_voxels) * 8
+        h = ctypes.c_void_p()
+        self._h = None
+        size = ctypes.c_size_t(0)
+        fd = ctypes.c_int(-1)
+
+        def agree(st: int, what: str) -> None:  # every rank learns whether every rank succeeded
+            sts = [st]
+            if multi:
+                sts = [None] * ws
+                dist.all_gather_object(sts, st, group=group)
+            if any(x != 0 for x in sts):
+                if h.value:
+                    lib.fsld_nvls_destroy(h)
+                raise C.FsldError(f"{what}: status {sts}")
+
+        st = lib.fsld_nvls_create(ws, self.data_bytes, ctypes.byref(size), ctypes.byref(fd), ctypes.byref(h)) \
+            if rank == 0 else 0
+        agree(st, "fsld_nvls_create")
+        if multi:
+            meta = [int(size.value)]
+            dist.broadcast_object_list(meta, src=0, group=group)
+            got = exchange_fd(fd.value if rank == 0 else -1, group)
+            st = lib.fsld_nvls_import(got, ws, rank, self.data_bytes, meta[0], ctypes.byref(h)) if rank > 0 else 0
+            agree(st, "fsld_nvls_import")
+            size.value = meta[0]
+        self.size = int(size.value)
+        # every device joins the team before any memory is bound
+        agree(lib.fsld_nvls_add_device(h), "fsld_nvls_add_device")
+        uc, mc = ctypes.c_void_p(), ctypes.c_void_p()
+        agree(lib.fsld_nvls_bind(h, ctypes.byref(uc), ctypes.byref(mc)), "fsld_nvls_bind")
+        self._h = h
+        self.uc, self.mc = int(uc.value), int(mc.value)
+
+    def barrier(self, sq_in=None, sq_out=None, stream=None) -> None:
+        from .engine import _stream, ctypes_ptr
+
+        self._C.check(self._C.load().fsld_nvls_barrier(self._h, ctypes_ptr(sq_in), ctypes_ptr(sq_out),
+                                                        _stream() if stream is None else stream), "nvls_barrier")
+
+    def check(self) -> None:
+        self._C.check(self._C.load().fsld_nvls_status(self._h), "nvls barrier (a peer did not arrive)")
+
+    def close(self) -> None:
+        if self._h:
+            self._C.load().fsld_nvls_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def nvls_available(device: int = 0) -> bool:
+    from . import _capi as C
+
+    try:
+        return bool(C.load().fsld_nvls_supported(int(device)))
+    except OSError:
+        return False
+
+
+def nvls_planned_step(eng, g: NvlsGroup, plan, k: int, v, scale: float, lam: float, grad, sq, sq_total, loss,
+                      norm_scratch, events=None) -> None:
+    """One data-parallel loss+grad step over NVLS (stream-ordered, CUDA-graph capturable):
+    barrier (every copy zeroed) -> the brick pass of batch k of ``plan`` flushing into the multicast
+    accumulator -> barrier (all flushes landed, |r|^2 summed over ranks) -> grad = scale uc + lam v,
+    uc <- 0, loss."""
+    from . import _capi as C
+    from .engine import _stream, ctypes_ptr
+
+    lib = C.load()
+    s = _stream()
+    scr = eng.scratch(plan.B)
+    g.barrier(stream=s)
+    if events is not None:
+        events[0].record()
+    C.check(lib.fsld_loss_grad_planned_mc(eng.M, eng.mode_id, eng.n_mask, ctypes_ptr(eng.recs), ctypes_ptr(plan.buf),
+                                          plan.B, int(k), ctypes_ptr(v), ctypes_ptr(eng.x), ctypes_ptr(eng.pc),
+                                          ctypes_ptr(eng.ptab), g.mc, ctypes_ptr(sq), ctypes_ptr(scr),
+                                          scr.numel() * 8, s), "loss_grad_planned_mc")
+    if events is not None:
+        events[1].record()
+    g.barrier(sq, sq_total, stream=s)
+    C.check(lib.fsld_grad_epilogue(eng.M ** 3, g.uc, ctypes_ptr(v), float(scale), float(lam), ctypes_ptr(grad),
+                                   ctypes_ptr(sq_total), ctypes_ptr(loss), 0, ctypes_ptr(norm_scratch),
+                                   norm_scratch.numel() * 8, s), "epilogue")

@@ -167,3 +167,48 @@ def test_touched_ball_contains_every_scatter_target(golden):
     touched = np.flatnonzero(np.abs(acc) > 0)
     assert np.isin(touched, ball).all()
     assert ball.size < M ** 3
+
+
+def _fd_worker(rank, world_size, port, out_path):
+    """dist.exchange_fd: rank 0's fd (here a memfd with a payload) duplicated into rank 1 over the
+    library's SCM_RIGHTS socket path -- the hand-over NvlsGroup uses for the multicast handle."""
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world_size)
+    fd = -1
+    if rank == 0:
+        fd = os.memfd_create("fsld-test")
+        os.write(fd, b"fsld-nvls-handle")
+    got = D.exchange_fd(fd)
+    data = os.pread(got, 16, 0)
+    with open(out_path + f".{rank}", "wb") as f:
+        f.write(data + (b"|same" if got == fd else b"|dup"))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_fd_exchange_over_unix_socket():
+    with tempfile.TemporaryDirectory() as d:
+        out = os.path.join(d, "fd")
+        mp.start_processes(_fd_worker, args=(2, _free_port(), out), nprocs=2, start_method="spawn")
+        r0, r1 = open(out + ".0", "rb").read(), open(out + ".1", "rb").read()
+    assert r0 == b"fsld-nvls-handle|same"
+    assert r1 == b"fsld-nvls-handle|dup"
+
+
+def test_fd_passing_rejects_bad_arguments():
+    import ctypes
+
+    from paper_2311_16100_b200 import _capi as C
+
+    lib = C.load()
+    s = ctypes.c_int(-1)
+    assert lib.fsld_fd_listen(b"", ctypes.byref(s)) == C.FSLD_EINVAL
+    assert lib.fsld_fd_listen(b"x" * 200, ctypes.byref(s)) == C.FSLD_EINVAL
+    assert lib.fsld_fd_send(b"fsld-none", -1) == C.FSLD_EINVAL
+    assert lib.fsld_fd_recv(-1, ctypes.byref(s)) == C.FSLD_EINVAL
+    # NVLS entry points validate before touching a driver
+    h = ctypes.c_void_p()
+    sz, fd = ctypes.c_size_t(), ctypes.c_int()
+    assert lib.fsld_nvls_create(0, 1024, ctypes.byref(sz), ctypes.byref(fd), ctypes.byref(h)) == C.FSLD_EINVAL
+    assert lib.fsld_nvls_import(-1, 2, 1, 1024, 1 << 21, ctypes.byref(h)) == C.FSLD_EINVAL
+    assert lib.fsld_nvls_barrier(None, None, None, None) == C.FSLD_EINVAL
+    assert lib.fsld_nvls_supported(0) in (0, 1)
