@@ -820,7 +820,13 @@ cudaError_t launch_slab_items(const SortedArgs& a, const SlabMap& map, int G, in
 }
 
 // One batch of a plan: its work items are ready; re-arm its claim counter and run.
+#ifdef FSLD_EXP_NO_GEO2
+static void exp_l0_once(const SortedArgs& a, cudaStream_t s);
+#endif
 cudaError_t launch_planned_loss_grad(const SortedArgs& a, double* sq_out, cudaStream_t s) {
+#ifdef FSLD_EXP_NO_GEO2
+    exp_l0_once(a, s);
+#endif
     cudaError_t e = cudaMemsetAsync(a.ctl + 1, 0, sizeof(int), s);
     if (e != cudaSuccess) return e;
     return a.zbits ? launch_sorted_main<true>(a, sq_out, s) : launch_sorted_main<false>(a, sq_out, s);
@@ -829,8 +835,28 @@ cudaError_t launch_planned_loss_grad(const SortedArgs& a, double* sq_out, cudaSt
 // The whole loss+grad step of batch k of a plan with the epilogue fused around the brick pass:
 // grad = lam v (+ ||v||^2 partials), the brick pass adding scale * contributions into grad, and one
 // finalize of sq and the loss.  a.acc = grad, a.v = v.
+#ifdef FSLD_EXP_NO_GEO2
+__global__ void exp_l0_into_f_kernel(void* ptab) {
+    const long long npx = reinterpret_cast<const TabHeader*>(ptab)->npx;
+    float2* tf = const_cast<float2*>(tab_f(ptab));
+    const float4* tg = tab_geo(ptab, npx);
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < npx; i += (long long)gridDim.x * blockDim.x)
+        tf[i].x = tg[i].w;
+}
+static void exp_l0_once(const SortedArgs& a, cudaStream_t s) {
+    static const void* done = nullptr;
+    if (a.ptab && done != a.ptab) {
+        exp_l0_into_f_kernel<<<1184, 256, 0, s>>>(const_cast<void*>(a.ptab));
+        done = a.ptab;
+    }
+}
+#endif
+
 cudaError_t launch_planned_loss_grad_step(SortedArgs a, int64_t nvox, double scale, double lam, double* sq_out,
                                           double* loss, double* norm_part, int n_norm, cudaStream_t s) {
+#ifdef FSLD_EXP_NO_GEO2
+    exp_l0_once(a, s);
+#endif
     if (a.ptab && !a.nn) {  // the table-driven kernels do the whole step in one launch
         int grid = 0;
         cudaError_t e = v3_grid<false, false>(grid);

@@ -89,6 +89,17 @@ __device__ __forceinline__ void load_pix3(const SortedArgs& a, const float2* tf,
     p.f = make_float2(t, 1.f - t);
     p.geo = make_float4(t, 0.5f * t, 1.f - t, __int_as_float((int)(g & 511)));
     p.x = make_float2(t, t);
+#elif defined(FSLD_EXP_NO_GEO2)  // ablation (results wrong): footprint not loaded, the real corner index
+    // from f.x's bits (copied there once by exp_l0_into_f_kernel): realistic bank patterns, 16 B / pixel
+    p.f = __ldg(tf + g);
+    const float t = (float)(g & 1023) * 1e-3f;
+    p.geo = make_float4(t, 0.5f * t, 1.f - t, p.f.x);
+    p.x = has_x ? __ldg(a.xs + g) : make_float2(0.f, 0.f);
+#elif defined(FSLD_EXP_NO_F)  // ablation (results wrong): f not loaded
+    const float t = (float)(g & 1023) * 1e-3f;
+    p.f = make_float2(t, 1.f - t);
+    p.geo = __ldg(tg + g);
+    p.x = has_x ? __ldg(a.xs + g) : make_float2(0.f, 0.f);
 #else
     p.f = __ldg(tf + g);
     p.geo = __ldg(tg + g);
