@@ -91,3 +91,15 @@ def test_hessian_exact_diag_public_api(data):
     assert O.relative_l2(got, ref) < TOL
     again = F.exact_diag(poses, d.ctfs, lam, "tri", F.GridSpec(d.M), d.mask)
     assert np.array_equal(got.view(np.uint64), again.view(np.uint64))
+
+
+@pytest.mark.parametrize("M", [17, 33])
+def test_brick_diag_odd_sizes_vs_oracle(M):
+    """Odd M (the half-open z range, bricks cut by the grid edge) and a ragged last chunk."""
+    d = cfg_data.make(M, 1100, "tri", ctf=True, shifts=False, snr=0.05, seed=M)
+    recs = records_for(d.M, d.quats, None, d.ctfs)
+    for det in (True, False):
+        e = SliceEngine(d.M, "tri", d.mask, recs, None, deterministic=det)
+        assert e.ptab is not None
+        got = _diag(e, np.arange(1100))
+        assert O.relative_l2(got, O.exact_diag(d.oop, 0.0)) < TOL
