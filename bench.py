@@ -352,6 +352,15 @@ def run_b200(args):
     scr = eng.scratch(B)
     nscr = eng._norm_scratch()
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    flush_mode = os.environ.get("FSLD_BENCH_FLUSH", "clean")
+    flush_rd = torch.ones(L2_FLUSH_BYTES // 8, dtype=torch.float32, device=dev) if flush_mode == "clean" else None
+
+    def l2_flush(i):
+        if flush_mode == "none":
+            return
+        flush.fill_(float(i))
+        if flush_rd is not None:  # read > L2 afterwards: the fill's dirty lines are written back now
+            flush_rd.sum()
     gen = np.random.default_rng(1234 + rank)
     n_steps = args.warmup + args.steps
     batches = [torch.from_numpy(gen.choice(eng.n_images, B, replace=False).astype(np.int32)).to(dev)
@@ -469,7 +478,7 @@ def run_b200(args):
     # kernel-only timing (events around the fused loss+grad call, eager)
     kev = [(E(), E()) for _ in range(args.steps)]
     for i in range(args.steps):
-        flush.fill_(float(i))
+        l2_flush(i)
         if use_plan:
             planned_step(plan_t, i, *kev[i])
         else:
@@ -514,7 +523,7 @@ def run_b200(args):
         if world > 1:
             dist.barrier()
         for i in range(args.steps):
-            flush.fill_(float(i))  # L2 flush between timed steps (outside the step events)
+            l2_flush(i)  # L2 flush between timed steps (outside the step events)
             s0, s1 = ev[i]
             s0.record()
             if graphs is not None:
@@ -592,7 +601,7 @@ def run_b200(args):
                                if eng.table_path else
                                "complex64 images / volume / gradient, fp32 coordinates, CTF and shift phases as exact "
                                "64-bit fixed-point turns; int32 fixed-point shared-memory adjoint; fp64 loss sums"),
-                "n_images_per_gpu": eng.n_images, "l2": "flushed between timed steps (512 MB write)",
+                "n_images_per_gpu": eng.n_images, "l2": {"write": "flushed between timed steps (512 MB write)", "none": "not flushed (inputs > L2)"}.get(flush_mode, "flushed between timed steps (512 MB write, then a 256 MB read: the flush's dirty lines are written back before the step, not during it)"),
                 "allreduce_bytes": (8 * nball + 8) if dp and nvg is None else 0,
                 "collectives_per_step": 1 if dp and nvg is None else 0,
                 "exchange": (("NVLS: per-item multimem.red.add.v2.f32 flush into the multicast accumulator "
