@@ -206,8 +206,12 @@ __global__ void __launch_bounds__(BTHREADS, (HUTCH || DIAG) ? 4 : FSLD_V3_MINB) 
     __syncthreads();
     int cur = 0;  // ring slot of the current item
     if (S.ring_desc[0].x >= 0) stage_item3(0);
-    bool init_seen = !a.fuse;
-    if (a.fuse) {  // this CTA's slice of acc = lam v, ||v||^2 partial; then count the slice as written
+    bool init_seen = !a.fuse;  // (fused step) every CTA's slice of acc = lam v is written
+    bool init_done = !a.fuse;  // this CTA's slice is written
+    // this CTA's slice of acc = lam v, ||v||^2 partial; then count the slice as written -- before the
+    // first item (writing it just before the CTA's first flush instead, overlapped with the other
+    // CTAs' first items, measured 0.1445 vs 0.136 ms per step: the first flushes then wait longer)
+    auto fused_init = [&]() {
         const int64_t n = (int64_t)M * M * M;
         const int64_t lo = n * blockIdx.x / gridDim.x, hi = n * (blockIdx.x + 1) / gridDim.x;
         double s2 = 0.0;
@@ -226,7 +230,10 @@ __global__ void __launch_bounds__(BTHREADS, (HUTCH || DIAG) ? 4 : FSLD_V3_MINB) 
             a.fnorm[blockIdx.x] = t;
             atomicAdd(a.ctl + 6, 1);
         }
-    }
+        __syncthreads();  // (S.red is free again)
+        init_done = true;
+    };
+    if (!init_done) fused_init();
 
     for (;;) {
         if (S.ring_desc[cur].x < 0) break;
@@ -518,6 +525,7 @@ __global__ void __launch_bounds__(BTHREADS, (HUTCH || DIAG) ? 4 : FSLD_V3_MINB) 
             __syncthreads();
         }
         if (!init_seen) {  // (fused step) every CTA's slice of acc = lam v is in place before the first add
+            if (!init_done) fused_init();
             if (threadIdx.x == 0)
                 while (*reinterpret_cast<volatile int*>(a.ctl + 6) < (int)gridDim.x) __nanosleep(64);
             __syncthreads();
@@ -577,6 +585,7 @@ __global__ void __launch_bounds__(BTHREADS, (HUTCH || DIAG) ? 4 : FSLD_V3_MINB) 
         }
         cur = nxs;
     }
+    if (!init_done) fused_init();  // (fused step, a CTA that got no item)
     if constexpr (!DET) {  // (deterministic mode: the loss partials are per item, a.part[item index])
         for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
         if (lane == 0) S.red[warp] = lsum;
