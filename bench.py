@@ -919,14 +919,25 @@ def e2e_leg(eng, wl, B, lam, n_total, args, world):
         per_call.append((time.perf_counter() - t1) * 1e3)
     sec = (time.perf_counter() - t0) / n_time
     assert grad.dtype == np.complex128 and np.isfinite(loss)
+    # bytes over PCIe per call: the packed touched ball as complex64 in each direction, the batch
+    # rows up; one flag per z-slab and [sum|r|^2, loss] down
+    ball = eng.HOST_BALL
+    n_ball = int(C.load().fsld_ball_voxels(M, float(eng.touch_radius))) if ball else M ** 3
+    n_slabs = eng.NP_SLABS if ball else eng.HOST_SLABS
     out = {"value": world * B / sec, "unit": "images/s", "ms_per_step": sec * 1e3,
-           "h2d_bytes_per_step": 8 * M ** 3 + 4 * B, "d2h_bytes_per_step": 16 * M ** 3 + 16,
+           "h2d_bytes_per_step": 8 * n_ball + 4 * B,
+           "d2h_bytes_per_step": (8 * n_ball + 4 * n_slabs + 16) if ball else 16 * M ** 3 + 16,
+           "ball_voxels": n_ball, "volume_voxels": M ** 3, "z_slabs": n_slabs,
            "path": ("optim.loss_and_grad(op, v: numpy complex128, batch: numpy, lam) -> (float, numpy complex128) "
-                    "-- the reference's signature, through fsld_loss_grad_host_np: v cast to complex64 on the "
-                    "library's native host thread pool (streaming stores into page-locked staging), then the z-slab "
-                    "pipelined host step (copies in both directions overlap the brick passes; each finished gradient "
-                    "slab cast to complex128 on the device and copied straight into the returned array, a recycled "
-                    "page-locked buffer; cached CUDA graph)"),
+                    "-- the reference's signature, through fsld_loss_grad_host_np_ball: the voxels a scatter can "
+                    "reach (the touched ball) cast to complex64 and packed row by row on the library's native host "
+                    "thread pool (streaming stores into page-locked staging), then the z-slab pipelined host step "
+                    "(one contiguous copy per slab in each direction, overlapping the brick passes; each finished "
+                    "gradient slab packed on the device, copied, and cast to complex128 into the returned array by "
+                    "the host threads while later slabs are in flight; off the ball the host threads write "
+                    "grad = lam v and sum ||v||^2 in fp64 meanwhile; cached CUDA graph)") if ball else
+                   ("optim.loss_and_grad(op, v, batch, lam) through fsld_loss_grad_host_np with whole-plane copies "
+                    "(FSLD_HOST_BALL=0)"),
            "timing": f"wall clock, mean of {n_time} calls after {n_warm} warm-up calls (host cast, PCIe copies and "
                      "kernels inside)",
            "per_call_ms": {"median": float(np.median(per_call)), "min": float(np.min(per_call)),

@@ -512,6 +512,20 @@ int fsld_loss_grad_host_np(int M, int mode, int n_mask, const fsld_image_rec* re
                            const int32_t* seg_off, const int32_t* segs, double scale, double lam, double* grad128_host,
                            double* out_host, void* v_dev, void* grad_dev, int32_t* idx_dev, int n_slabs,
                            void* scratch, size_t scratch_bytes, void* stream);
+/* The same call moving only the touched ball (grid.touched_ball): the data term
+ * only reaches voxels within touch_radius = max |k| over the mask + sqrt(3) of the origin.  With
+ * touch_radius > 0 only those voxels cross PCIe, packed row by row as complex64 -- one contiguous range per
+ * z-slab in each direction (fsld_ball_voxels(M, touch_radius) voxels: ~55 % of the cube at M=128) -- and
+ * the host threads cast each finished gradient slab to complex128 into grad128_host (any host memory)
+ * while later slabs are in flight; off the ball they write grad = lam v in fp64 while the device works,
+ * and ||v||^2 in the loss is summed on the host in fp64.  touch_radius <= 0: fsld_loss_grad_host_np. */
+int fsld_loss_grad_host_np_ball(int M, int mode, int n_mask, const fsld_image_rec* recs, const int32_t* idx_host,
+                                int B, const double* v128_host, const void* xs, const int8_t* pc, const void* ptab,
+                                const int32_t* seg_off, const int32_t* segs, double scale, double lam,
+                                double* grad128_host, double* out_host, void* v_dev, void* grad_dev, int32_t* idx_dev,
+                                int n_slabs, void* scratch, size_t scratch_bytes, void* stream, double touch_radius);
+/* Voxels of the packed ball of fsld_loss_grad_host_np_ball (M^3 when touch_radius <= 0). */
+int64_t fsld_ball_voxels(int M, double touch_radius);
 int fsld_proj_energy_planned(int M, int mode, int n_mask, const fsld_image_rec* recs, const void* plan, int B, int k,
                              const void* d, const int8_t* pc, double* out, void* scratch, size_t scratch_bytes,
                              void* stream);

@@ -107,6 +107,8 @@ SIGNATURES = {
     "fsld_loss_grad_host": (I, [I, I, I, P, P, I, P, P, P, P, P, P, D, D, P, P, P, P, P, I, P, SZ, P]),
     "fsld_loss_grad_host_c128": (I, [I, I, I, P, P, I, P, P, P, P, P, P, D, D, P, P, P, P, P, P, I, P, SZ, P]),
     "fsld_loss_grad_host_np": (I, [I, I, I, P, P, I, P, P, P, P, P, P, D, D, P, P, P, P, P, I, P, SZ, P]),
+    "fsld_ball_voxels": (I64, [I, D]),
+    "fsld_loss_grad_host_np_ball": (I, [I, I, I, P, P, I, P, P, P, P, P, P, D, D, P, P, P, P, P, I, P, SZ, P, D]),
     "fsld_project_sorted": (I, [I, I, I, P, P, I, P, P, P, P]),
     "fsld_backproject_sorted": (I, [I, I, I, P, P, I, P, P, P, U, P, P]),
     "fsld_fixed_scale": (I, [P, I64, D, D, P, P]),

@@ -287,4 +287,29 @@ cudaError_t launch_ball(bool gather, int64_t n, const int32_t* idx, const void* 
     return cudaGetLastError();
 }
 
+// Rows of the touched ball between the M^3 volume and its packed form (the numpy-signature host step:
+// fsld_loss_grad_host_np_ball moves only the ball over PCIe, as one contiguous range per z-slab).
+// rows[r] = (voxel offset, length, packed offset, -); one warp per row, 8-byte voxels (complex64).
+template <bool PACK>
+__global__ void __launch_bounds__(256) ball_rows_kernel(const int4* __restrict__ rows, int nrows,
+                                                        const float2* __restrict__ src, float2* __restrict__ dst) {
+    const int lane = threadIdx.x & 31;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < nrows; r += nw) {
+        const int4 q = rows[r];
+        const float2* a = src + (PACK ? q.x : q.z);
+        float2* b = dst + (PACK ? q.z : q.x);
+        for (int i = lane; i < q.y; i += 32) b[i] = a[i];
+    }
+}
+
+cudaError_t launch_ball_rows(bool pack, const int4* rows, int nrows, const void* src, void* dst, cudaStream_t s) {
+    if (nrows <= 0) return cudaSuccess;
+    int blocks = (nrows + 7) / 8;
+    blocks = blocks > 148 * 8 ? 148 * 8 : blocks;
+    if (pack) ball_rows_kernel<true><<<blocks, 256, 0, s>>>(rows, nrows, (const float2*)src, (float2*)dst);
+    else ball_rows_kernel<false><<<blocks, 256, 0, s>>>(rows, nrows, (const float2*)src, (float2*)dst);
+    return cudaGetLastError();
+}
+
 }  // namespace fsld

@@ -5,10 +5,13 @@
 // the launch geometry and enqueues the kernels on the caller's stream.
 // Never throws, never synchronises.
 #include <algorithm>
+#include <chrono>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <vector>
 
 
 #include "fsld_hostpool.h"
@@ -860,7 +863,8 @@ namespace {
 struct HostPipe {
     cudaStream_t h2d = nullptr, d2h = nullptr, ks[2] = {nullptr, nullptr};
     cudaStream_t cap = nullptr;  // graphs are captured here (the caller's stream may be the legacy one)
-    cudaEvent_t fork = nullptr, join = nullptr, eh[kMaxSlabs] = {}, ei[kMaxSlabs] = {}, ek[kMaxSlabs] = {};
+    cudaEvent_t fork = nullptr, join = nullptr, eh[kMaxSlabs] = {}, ei[kMaxSlabs] = {}, ek[kMaxSlabs] = {},
+                           ep[kMaxSlabs] = {};  // per slab: copied in, initialised, pass done, gradient packed
 };
 std::mutex g_pipe_mu;  // held while a call enqueues (the events are reused call after call)
 HostPipe g_pipe[16];
@@ -884,6 +888,7 @@ cudaError_t pipe_for_device(HostPipe*& out) {
             if ((e = cudaEventCreateWithFlags(&p.eh[g], fl)) != cudaSuccess) return e;
             if ((e = cudaEventCreateWithFlags(&p.ek[g], fl)) != cudaSuccess) return e;
             if ((e = cudaEventCreateWithFlags(&p.ei[g], fl)) != cudaSuccess) return e;
+            if ((e = cudaEventCreateWithFlags(&p.ep[g], fl)) != cudaSuccess) return e;
         }
     }
     out = &p;
@@ -925,6 +930,90 @@ int slab_pieces(int M, int z0, int z1, int zi0[2], int nz[2]) {
     return n;
 }
 
+// The touched ball of the numpy-signature host step (fsld_loss_grad_host_np_ball), row by row: the voxels
+// within the radius rt of the origin (the only ones a scatter can reach, grid.touched_ball) as one x range
+// per storage row (z, y) -- one voxel of margin, rounded out to multiples of 4 voxels (whole 64-byte lines
+// of complex128) -- and their packed order: slab by slab (as host_step_enqueue cuts them), plane by plane,
+// row by row, so that every z-slab crosses PCIe as one contiguous range in each direction.
+struct BallPack {
+    int M = 0, n_slabs = 0, G = 0;
+    double rt = 0.0;
+    std::vector<int> xa, xb;        // per storage row z * M + y: the ball's voxels are x in [xa, xb)
+    std::vector<int64_t> poff;      // per storage row: its offset in the packed order
+    int row0[kMaxSlabs + 1] = {};   // slab g's rows in rows_dev
+    int64_t off[kMaxSlabs + 1] = {};  // slab g's range of the packed order
+    int sz[kMaxSlabs][2] = {}, sn[kMaxSlabs][2] = {}, snp[kMaxSlabs] = {};  // slab g's plane ranges (slab_pieces)
+    int4* rows_dev = nullptr;       // (voxel offset, length, packed offset, -) of the non-empty rows, by slab
+    float2 *vpack_dev = nullptr, *gpack_dev = nullptr;  // device staging of the packed volume / gradient
+};
+
+// The ball's x range [xa, xb) of the storage row (kz, ky), false if the row is off the ball.
+bool ball_row(int M, int kz, int ky, double rt, int& xa, int& xb) {
+    const int c = (M + 1) / 2;
+    const double rem = rt * rt - (double)kz * kz - (double)ky * ky;
+    if (rem < 0.0) return false;
+    const int h = (int)std::sqrt(rem) + 1;
+    xa = std::max(0, c - h) & ~3;
+    xb = std::min(M, (c + h + 1 + 3) & ~3);
+    return true;
+}
+
+void ball_pack_free(BallPack& bp) {
+    cudaFree(bp.rows_dev);
+    cudaFree(bp.vpack_dev);
+    cudaFree(bp.gpack_dev);
+    bp = BallPack{};
+}
+
+cudaError_t ball_pack_build(BallPack& bp, int M, int n_slabs, double rt) {
+    ball_pack_free(bp);
+    const int c = (M + 1) / 2, nb = (M + BT - 1) / BT;
+    int first[kMaxSlabs + 1];
+    bp.G = slab_layers(nb, n_slabs, first);
+    bp.xa.assign((size_t)M * M, 0);
+    bp.xb.assign((size_t)M * M, 0);
+    bp.poff.assign((size_t)M * M, 0);
+    std::vector<int4> rows;
+    int64_t pos = 0;
+    for (int g = 0; g < bp.G; ++g) {
+        const int z0 = -c + BT * first[g], z1 = std::min(-c + BT * first[g + 1], M - c);
+        bp.snp[g] = slab_pieces(M, z0, z1, bp.sz[g], bp.sn[g]);
+        bp.row0[g] = (int)rows.size();
+        bp.off[g] = pos;
+        for (int q = 0; q < bp.snp[g]; ++q)
+            for (int z = bp.sz[g][q]; z < bp.sz[g][q] + bp.sn[g][q]; ++z) {
+                const int kz = z >= M - c ? z - M : z;
+                for (int y = 0; y < M; ++y) {
+                    int xa = 0, xb = 0;
+                    if (!ball_row(M, kz, y - c, rt, xa, xb)) continue;
+                    const size_t r = (size_t)z * M + y;
+                    bp.xa[r] = xa;
+                    bp.xb[r] = xb;
+                    bp.poff[r] = pos;
+                    rows.push_back(make_int4((int)(r * M + xa), xb - xa, (int)pos, 0));
+                    pos += xb - xa;
+                }
+            }
+    }
+    bp.row0[bp.G] = (int)rows.size();
+    bp.off[bp.G] = pos;
+    cudaError_t e;
+    if ((e = cudaMalloc(reinterpret_cast<void**>(&bp.rows_dev), sizeof(int4) * std::max<size_t>(1, rows.size()))) !=
+            cudaSuccess ||
+        (e = cudaMalloc(reinterpret_cast<void**>(&bp.vpack_dev), sizeof(float2) * (size_t)std::max<int64_t>(1, pos))) !=
+            cudaSuccess ||
+        (e = cudaMalloc(reinterpret_cast<void**>(&bp.gpack_dev), sizeof(float2) * (size_t)std::max<int64_t>(1, pos))) !=
+            cudaSuccess ||
+        (e = cudaMemcpy(bp.rows_dev, rows.data(), sizeof(int4) * rows.size(), cudaMemcpyHostToDevice)) != cudaSuccess) {
+        ball_pack_free(bp);
+        return e;
+    }
+    bp.M = M;
+    bp.n_slabs = n_slabs;
+    bp.rt = rt;
+    return cudaSuccess;
+}
+
 }  // namespace
 
 namespace {
@@ -936,6 +1025,8 @@ struct HostStepKey {
     const void *recs, *v_host, *xs, *pc, *ptab, *seg_off, *segs, *grad_host, *out_host, *v_dev, *grad_dev,
         *idx_dev, *scratch, *grad_dev128;  // grad_dev128 != NULL: grad_host is complex128
     double scale, lam;
+    const void* pack;  // != NULL (a BallPack): v_host / grad_host are packed balls, one contiguous copy per slab
+    const void *slab_flags, *one_dev;  // != NULL: after slab g's gradient copy, *one_dev -> slab_flags[g] (pinned int)
     bool operator==(const HostStepKey& o) const { return std::memcmp(this, &o, sizeof(*this)) == 0; }
 };
 
@@ -975,6 +1066,7 @@ cudaError_t host_step_enqueue(const HostStepKey& k, HostPipe* P, const int32_t* 
     char* gd = reinterpret_cast<char*>(grad_dev);
 
     cudaError_t e = cudaSuccess;
+    const BallPack* bp = reinterpret_cast<const BallPack*>(k.pack);
 #define FSLD_TRY(x) do { if ((e = (x)) != cudaSuccess) return e; } while (0)
     // the slab passes' per-CTA partials live in kSlabCtas-sized slots: refuse an oversized grid
     // before anything is enqueued (nothing half-written)
@@ -983,6 +1075,19 @@ cudaError_t host_step_enqueue(const HostStepKey& k, HostPipe* P, const int32_t* 
     if (grid_max > kSlabCtas) return cudaErrorInvalidConfiguration;
     // batch rows first (2 KB: the binning must not queue behind a volume slab on the copy engine)
     FSLD_TRY(cudaMemcpyAsync(idx_dev, idx_host, sizeof(int32_t) * (size_t)B, cudaMemcpyHostToDevice, s));
+    // (A/B) FSLD_HOST_BIN_FIRST=1: the binning ahead of the fork, so that the first pass never waits for
+    // it -- measured slower (1.07 vs 0.95 ms per numpy call: the copies then start ~70 us later)
+    static const bool bin_first = [] {
+        const char* v = std::getenv("FSLD_HOST_BIN_FIRST");
+        return v && v[0] == '1';
+    }();
+    auto binning = [&]() -> cudaError_t {  // per-step binning, regrouped by slab (independent of v)
+        cudaError_t r = cudaMemsetAsync(gpart, 0, L.hout - L.gpart, s);
+        if (r == cudaSuccess) r = launch_sorted_bin(a, s);
+        if (r == cudaSuccess) r = launch_slab_items(a, map, G, gitems, gctl, s);
+        return r;
+    };
+    if (bin_first) FSLD_TRY(binning());
     // fork: the copy streams start after whatever `stream` already holds (v_dev / grad_dev reuse)
     FSLD_TRY(cudaEventRecord(P->fork, s));
     FSLD_TRY(cudaStreamWaitEvent(P->h2d, P->fork, 0));
@@ -991,17 +1096,23 @@ cudaError_t host_step_enqueue(const HostStepKey& k, HostPipe* P, const int32_t* 
     for (int g = 0; g < G; ++g) {
         const int z0 = -c + BT * first[g], z1 = std::min(-c + BT * first[g + 1], M - c);
         np[g] = slab_pieces(M, z0, z1, zi0[g], nz[g]);
-        for (int q = 0; q < np[g]; ++q)
-            FSLD_TRY(cudaMemcpyAsync(vd + zi0[g][q] * plane, vh + zi0[g][q] * plane, nz[g][q] * plane,
-                                     cudaMemcpyHostToDevice, P->h2d));
+        if (bp) {  // the slab's part of the packed ball in one copy (init() puts its rows into place)
+            const size_t o = (size_t)bp->off[g] * sizeof(float2), nbytes = (size_t)(bp->off[g + 1] - bp->off[g]) * sizeof(float2);
+            if (nbytes)
+                FSLD_TRY(cudaMemcpyAsync(reinterpret_cast<char*>(bp->vpack_dev) + o, vh + o, nbytes,
+                                         cudaMemcpyHostToDevice, P->h2d));
+        } else {
+            for (int q = 0; q < np[g]; ++q)
+                FSLD_TRY(cudaMemcpyAsync(vd + zi0[g][q] * plane, vh + zi0[g][q] * plane, nz[g][q] * plane,
+                                         cudaMemcpyHostToDevice, P->h2d));
+        }
         FSLD_TRY(cudaEventRecord(P->eh[g], P->h2d));
     }
-    // per-step binning, regrouped by slab (independent of v: overlaps the first copies)
-    FSLD_TRY(cudaMemsetAsync(gpart, 0, L.hout - L.gpart, s));
-    FSLD_TRY(launch_sorted_bin(a, s));
-    FSLD_TRY(launch_slab_items(a, map, G, gitems, gctl, s));
+    if (!bin_first) FSLD_TRY(binning());
     auto init = [&](int g) -> cudaError_t {  // grad = lam v on slab g (+ ||v||^2 partials), on `stream`
         cudaError_t r = cudaStreamWaitEvent(s, P->eh[g], 0);
+        if (bp && r == cudaSuccess)  // (not on the copy stream: its copies run back to back)
+            r = launch_ball_rows(false, bp->rows_dev + bp->row0[g], bp->row0[g + 1] - bp->row0[g], bp->vpack_dev, v_dev, s);
         for (int q = 0; q < np[g] && r == cudaSuccess; ++q) {
             const size_t o = (size_t)zi0[g][q] * M * M;
             r = launch_grad_init((int64_t)nz[g][q] * M * M, reinterpret_cast<const float2*>(v_dev) + o, lam,
@@ -1024,9 +1135,22 @@ cudaError_t host_step_enqueue(const HostStepKey& k, HostPipe* P, const int32_t* 
         int grid = 0;
         FSLD_TRY(launch_sorted_pass(a, ks, &grid));
         FSLD_TRY(cudaEventRecord(P->ek[g], ks));
-        FSLD_TRY(cudaStreamWaitEvent(P->d2h, P->ek[g], 0));
-        if (g > 0) FSLD_TRY(cudaStreamWaitEvent(P->d2h, P->ek[g - 1], 0));
-        for (int q = 0; q < np[g]; ++q) {
+        if (bp) {  // the slab's rows packed on the pass's stream, then one copy
+            const size_t o = (size_t)bp->off[g] * sizeof(float2), nbytes = (size_t)(bp->off[g + 1] - bp->off[g]) * sizeof(float2);
+            if (g > 0) FSLD_TRY(cudaStreamWaitEvent(ks, P->ek[g - 1], 0));
+            FSLD_TRY(launch_ball_rows(true, bp->rows_dev + bp->row0[g], bp->row0[g + 1] - bp->row0[g], grad_dev,
+                                      bp->gpack_dev, ks));
+            FSLD_TRY(cudaEventRecord(P->ep[g], ks));
+            FSLD_TRY(cudaStreamWaitEvent(P->d2h, P->ep[g], 0));
+            if (nbytes)
+                FSLD_TRY(cudaMemcpyAsync(gh + o, reinterpret_cast<char*>(bp->gpack_dev) + o, nbytes,
+                                         cudaMemcpyDeviceToHost, P->d2h));
+        }
+        if (!bp) {
+            FSLD_TRY(cudaStreamWaitEvent(P->d2h, P->ek[g], 0));
+            if (g > 0) FSLD_TRY(cudaStreamWaitEvent(P->d2h, P->ek[g - 1], 0));
+        }
+        for (int q = 0; q < (bp ? 0 : np[g]); ++q) {
             if (k.grad_dev128) {  // complex128 out: cast the finished slab on the device, copy 16 B / voxel
                 char* g128 = reinterpret_cast<char*>(const_cast<void*>(k.grad_dev128));
                 FSLD_TRY(launch_cast_c64_c128((int64_t)nz[g][q] * M * M, gd + zi0[g][q] * plane,
@@ -1038,6 +1162,9 @@ cudaError_t host_step_enqueue(const HostStepKey& k, HostPipe* P, const int32_t* 
                                          cudaMemcpyDeviceToHost, P->d2h));
             }
         }
+        if (k.slab_flags)  // (posted writes keep their order: the flag lands after the slab's data)
+            FSLD_TRY(cudaMemcpyAsync(reinterpret_cast<int*>(const_cast<void*>(k.slab_flags)) + g, k.one_dev, sizeof(int),
+                                     cudaMemcpyDeviceToHost, P->d2h));
     }
     for (int q = 0; q < 2 && q < G; ++q) FSLD_TRY(cudaStreamWaitEvent(s, P->ek[G - 1 - q], 0));
     FSLD_TRY(cudaEventRecord(P->join, P->d2h));
@@ -1119,7 +1246,7 @@ cudaError_t host_graph(const HostStepKey& k, HostPipe* P, HostGraph*& out) {
 void drop_host_graphs_using(const void* p) {
     std::lock_guard<std::mutex> lk(g_pipe_mu);
     for (HostGraph& h : g_graphs)
-        if (h.exec && (!p || h.key.v_host == p || h.key.grad_host == p || h.key.out_host == p)) drop_graph(h);
+        if (h.exec && (!p || h.key.v_host == p || h.key.grad_host == p || h.key.out_host == p || h.key.slab_flags == p || h.key.pack == p)) drop_graph(h);
 }
 
 }  // namespace
@@ -1133,8 +1260,12 @@ static int loss_grad_host_impl(int M, int mode, int n_mask, const fsld_image_rec
                                int B, const void* v_host, const void* xs, const int8_t* pc, const void* ptab,
                                const int32_t* seg_off, const int32_t* segs, double scale, double lam,
                                void* grad_host, double* out_host, void* v_dev, void* grad_dev, int32_t* idx_dev,
-                               int n_slabs, void* scratch, size_t scratch_bytes, void* stream, void* grad_dev128) {
+                               int n_slabs, void* scratch, size_t scratch_bytes, void* stream, void* grad_dev128,
+                               const BallPack* pack = nullptr, int* slab_flags = nullptr,
+                               const int* one_dev = nullptr) {
     if (!geom_ok(M, mode, n_mask, B) || M > 256 || mode != FSLD_MODE_TRI) return FSLD_EINVAL;
+    if ((slab_flags != nullptr) != (one_dev != nullptr) || (pack && (grad_dev128 || pack->M != M || pack->n_slabs != n_slabs)))
+        return FSLD_EINVAL;
     if (!recs || !idx_host || !v_host || !xs || !pc || !seg_off || !segs || !grad_host || !out_host || !v_dev ||
         !grad_dev || !idx_dev || !scratch || v_dev == grad_dev || n_slabs < 1 || n_slabs > kMaxSlabs)
         return FSLD_EINVAL;
@@ -1163,6 +1294,9 @@ static int loss_grad_host_impl(int M, int mode, int n_mask, const fsld_image_rec
     k.scratch = scratch;
     k.scale = scale;
     k.lam = lam;
+    k.pack = pack;
+    k.slab_flags = slab_flags;
+    k.one_dev = one_dev;
     std::lock_guard<std::mutex> lk(g_pipe_mu);
     HostPipe* P = nullptr;
     cudaError_t e = pipe_for_device(P);
@@ -1213,6 +1347,9 @@ struct NpStage {  // per device: page-locked complex64 staging of v and of the g
     int64_t n = 0;
     float2 *v64 = nullptr, *g64 = nullptr;
     double2* g128_dev = nullptr;
+    int* flags = nullptr;    // page-locked: slab g's gradient has landed in g64 (touched-ball step)
+    int* one_dev = nullptr;  // device constant 1, the source of the flag copies
+    BallPack bp;             // the touched ball's rows and packed order (rebuilt when M / slabs / radius change)
 };
 NpStage g_np[16];
 std::mutex g_np_mu;  // one numpy-signature call at a time (the staging is per device)
@@ -1227,17 +1364,27 @@ cudaError_t np_stage(int64_t n, NpStage*& out) {
         if (st.v64) {
             drop_host_graphs_using(st.v64);
             drop_host_graphs_using(st.g64);
+            drop_host_graphs_using(st.flags);
+            drop_host_graphs_using(&st.bp);
+            ball_pack_free(st.bp);
             cudaFreeHost(st.v64);
             cudaFreeHost(st.g64);
+            cudaFreeHost(st.flags);
             cudaFree(st.g128_dev);
+            cudaFree(st.one_dev);
         }
         st = NpStage{};
         if ((e = cudaHostAlloc(reinterpret_cast<void**>(&st.v64), sizeof(float2) * (size_t)n, cudaHostAllocDefault)) !=
                 cudaSuccess ||
             (e = cudaHostAlloc(reinterpret_cast<void**>(&st.g64), sizeof(float2) * (size_t)n, cudaHostAllocDefault)) !=
                 cudaSuccess ||
-            (e = cudaMalloc(reinterpret_cast<void**>(&st.g128_dev), sizeof(double2) * (size_t)n)) != cudaSuccess)
+            (e = cudaMalloc(reinterpret_cast<void**>(&st.g128_dev), sizeof(double2) * (size_t)n)) != cudaSuccess ||
+            (e = cudaHostAlloc(reinterpret_cast<void**>(&st.flags), sizeof(int) * kMaxSlabs, cudaHostAllocDefault)) !=
+                cudaSuccess ||
+            (e = cudaMalloc(reinterpret_cast<void**>(&st.one_dev), sizeof(int))) != cudaSuccess)
             return e;
+        const int one = 1;
+        if ((e = cudaMemcpy(st.one_dev, &one, sizeof(int), cudaMemcpyHostToDevice)) != cudaSuccess) return e;
         st.n = n;
     }
     out = &st;
@@ -1261,12 +1408,24 @@ void np_cast_back(const float* src, double* dst, int64_t n) {
 // complex128 volume read and the complex128 gradient written are ~67 MB, the complex64 staging another
 // ~34 MB); overlapping the slab casts with the copies (device waits on host-written flags) made every
 // phase slower through that contention (1.31 vs 1.22 ms), so the cast runs first, on all host cores.
-extern "C" int fsld_loss_grad_host_np(int M, int mode, int n_mask, const fsld_image_rec* recs, const int32_t* idx_host,
-                                      int B, const double* v128_host, const void* xs, const int8_t* pc,
-                                      const void* ptab, const int32_t* seg_off, const int32_t* segs, double scale,
-                                      double lam, double* grad128_host, double* out_host, void* v_dev,
-                                      void* grad_dev, int32_t* idx_dev, int n_slabs, void* scratch,
-                                      size_t scratch_bytes, void* stream) {
+//
+// touch_radius > 0: the data term only reaches voxels within that radius of the origin
+// (grid.touched_ball: max |k| of the mask + sqrt(3)); off that ball the gradient is lam v and the loss
+// only sees ||v||^2 -- both computed here on the host threads in fp64 while the device works.  Only
+// the ball crosses PCIe, packed row by row (BallPack: ~55 % of the cube at M=128), one contiguous
+// complex64 range per z-slab in each direction: the cast in writes the packed staging, a row kernel puts
+// each slab's rows into the device volume; each finished gradient slab is packed on the device, copied,
+// flagged, and cast to complex128 into the result by the host threads while later slabs are in flight
+// (measured on the B200 box: the copy engine reads host memory at ~30 GB/s, so the call is bound by the
+// bytes of the volume going up; whole planes 1.30 ms, (y, x) boxes per slab 1.02 ms, the packed ball see
+// DESIGN section 6).
+extern "C" int fsld_loss_grad_host_np_ball(int M, int mode, int n_mask, const fsld_image_rec* recs,
+                                           const int32_t* idx_host, int B, const double* v128_host, const void* xs,
+                                           const int8_t* pc, const void* ptab, const int32_t* seg_off,
+                                           const int32_t* segs, double scale, double lam, double* grad128_host,
+                                           double* out_host, void* v_dev, void* grad_dev, int32_t* idx_dev,
+                                           int n_slabs, void* scratch, size_t scratch_bytes, void* stream,
+                                           double touch_radius) {
     if (!v128_host || !grad128_host || !out_host || M < 2 || M > 256 || n_slabs < 1 || n_slabs > kMaxSlabs)
         return FSLD_EINVAL;
     if ((reinterpret_cast<uintptr_t>(v128_host) | reinterpret_cast<uintptr_t>(grad128_host)) & 15) return FSLD_EINVAL;
@@ -1281,13 +1440,122 @@ extern "C" int fsld_loss_grad_host_np(int M, int mode, int n_mask, const fsld_im
     cudaPointerAttributes pa{};
     const bool out_pinned = cudaPointerGetAttributes(&pa, grad128_host) == cudaSuccess && pa.type == cudaMemoryTypeHost;
     cudaGetLastError();
-    np_cast(v128_host, reinterpret_cast<float*>(st->v64), n);
-    const int rc = loss_grad_host_impl(M, mode, n_mask, recs, idx_host, B, st->v64, xs, pc, ptab, seg_off, segs,
-                                       scale, lam, out_pinned ? static_cast<void*>(grad128_host) : st->g64, out_host,
-                                       v_dev, grad_dev, idx_dev, n_slabs, scratch, scratch_bytes, stream,
-                                       out_pinned ? static_cast<void*>(st->g128_dev) : nullptr);
+    const bool ball = touch_radius > 0.0 && std::isfinite(touch_radius);
+    if (!ball) {
+        np_cast(v128_host, reinterpret_cast<float*>(st->v64), n);
+        const int rc = loss_grad_host_impl(M, mode, n_mask, recs, idx_host, B, st->v64, xs, pc, ptab, seg_off, segs,
+                                           scale, lam, out_pinned ? static_cast<void*>(grad128_host) : st->g64,
+                                           out_host, v_dev, grad_dev, idx_dev, n_slabs, scratch, scratch_bytes,
+                                           stream, out_pinned ? static_cast<void*>(st->g128_dev) : nullptr);
+        if (rc != FSLD_OK) return rc;
+        if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return status_of(e);
+        if (!out_pinned) np_cast_back(reinterpret_cast<const float*>(st->g64), grad128_host, n);
+        return FSLD_OK;
+    }
+    BallPack& bp = st->bp;
+    if (bp.M != M || bp.n_slabs != n_slabs || bp.rt != touch_radius) {
+        drop_host_graphs_using(&bp);
+        if ((e = ball_pack_build(bp, M, n_slabs, touch_radius)) != cudaSuccess) return status_of(e);
+    }
+    static const bool trace = std::getenv("FSLD_NP_TRACE") != nullptr;  // (per-phase host times on stderr)
+    auto now = [] {
+        return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+    };
+    const double t0 = trace ? now() : 0.0;
+    double in_sq[256], out_sq[256];  // per-plane sums of |v|^2 on / off the ball (fixed order)
+    float* v64 = reinterpret_cast<float*>(st->v64);
+    fsld_host::parallel_for(M, 1, [&](int64_t za, int64_t zb) {
+        for (int64_t z = za; z < zb; ++z) {
+            double t = 0.0;
+            for (int64_t r = z * M; r < (z + 1) * M; ++r)
+                if (bp.xb[r] > bp.xa[r])
+                    t += fsld_host::cast_f64_to_f32_sumsq(v128_host + 2 * (r * M + bp.xa[r]), v64 + 2 * bp.poff[r],
+                                                          2 * (int64_t)(bp.xb[r] - bp.xa[r]));
+            in_sq[z] = t;
+        }
+        fsld_host::store_fence();
+    });
+    const double t1 = trace ? now() : 0.0;
+    volatile int* flags = st->flags;
+    for (int g = 0; g < kMaxSlabs; ++g) flags[g] = 0;
+    // the packed complex64 gradient into the page-locked staging slab by slab, one flag per finished slab
+    const int rc = loss_grad_host_impl(M, mode, n_mask, recs, idx_host, B, st->v64, xs, pc, ptab, seg_off, segs, scale,
+                                       lam, st->g64, out_host, v_dev, grad_dev, idx_dev, n_slabs, scratch,
+                                       scratch_bytes, stream, nullptr, &bp, st->flags, st->one_dev);
     if (rc != FSLD_OK) return rc;
+    const double t2 = trace ? now() : 0.0;
+    // while the device works: grad = lam v off the ball (running it after the last slab instead measured
+    // 0.98-1.03 vs 0.92 ms per call)
+    auto fill_outside = [&] {
+    fsld_host::parallel_for(M, 1, [&](int64_t za, int64_t zb) {
+        for (int64_t z = za; z < zb; ++z) {
+            double t = 0.0;
+            for (int64_t r = z * M; r < (z + 1) * M; ++r) {  // (a row off the ball: xa = xb = 0)
+                const int64_t o = 2 * r * M, xa = bp.xa[r], xb = bp.xb[r];
+                t += fsld_host::scale_f64_sumsq(v128_host + o, grad128_host + o, 2 * xa, lam);
+                t += fsld_host::scale_f64_sumsq(v128_host + o + 2 * xb, grad128_host + o + 2 * xb, 2 * (M - xb), lam);
+            }
+            out_sq[z] = t;
+        }
+        fsld_host::store_fence();
+    });
+    };
+    fill_outside();
+    const double t3 = trace ? now() : 0.0;
+    // each finished slab: its rows cast to complex128 into the result while the later slabs are in flight
+    const float* g64 = reinterpret_cast<const float*>(st->g64);
+    for (int g = 0; g < bp.G; ++g) {
+        for (unsigned spin = 0; flags[g] == 0; ++spin) {
+            fsld_host::cpu_pause();
+            if ((spin & 0xfff) == 0xfff) {  // a failed or finished stream never sets the flag: do not spin on it
+                const cudaError_t q = cudaStreamQuery(s);
+                if (q != cudaErrorNotReady) {
+                    if (q != cudaSuccess) return status_of(q);
+                    if (flags[g] == 0) return FSLD_ECUDA;
+                }
+            }
+        }
+        for (int q = 0; q < bp.snp[g]; ++q) {
+            const int za = bp.sz[g][q];
+            fsld_host::parallel_for(bp.sn[g][q], 1, [&](int64_t ia, int64_t ib) {
+                for (int64_t r = (za + ia) * M; r < (za + ib) * M; ++r)
+                    if (bp.xb[r] > bp.xa[r])
+                        fsld_host_cast_f32_to_f64(g64 + 2 * bp.poff[r], grad128_host + 2 * (r * M + bp.xa[r]),
+                                                  2 * (int64_t)(bp.xb[r] - bp.xa[r]));
+            });
+        }
+    }
+    const double t4 = trace ? now() : 0.0;
     if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return status_of(e);
-    if (!out_pinned) np_cast_back(reinterpret_cast<const float*>(st->g64), grad128_host, n);
+    if (trace)
+        std::fprintf(stderr, "np_ball: cast %.3f launch %.3f fill %.3f slabs %.3f wait %.3f ms\n", t1 - t0, t2 - t1,
+                     t3 - t2, t4 - t3, now() - t4);
+    // the device's loss used the norm of its own (partly stale) copy of v: ||v||^2 from the host sums
+    double norm = 0.0;
+    for (int z = 0; z < M; ++z) norm += in_sq[z] + out_sq[z];
+    out_host[1] = 0.5 * scale * out_host[0] + 0.5 * lam * norm;
     return FSLD_OK;
+}
+
+extern "C" int64_t fsld_ball_voxels(int M, double touch_radius) {
+    if (M < 2 || M > 256 || !(touch_radius > 0.0) || !std::isfinite(touch_radius)) return (int64_t)M * M * M;
+    const int c = (M + 1) / 2;
+    int64_t n = 0;
+    for (int kz = -c; kz < M - c; ++kz)
+        for (int ky = -c; ky < M - c; ++ky) {
+            int xa = 0, xb = 0;
+            if (ball_row(M, kz, ky, touch_radius, xa, xb)) n += xb - xa;
+        }
+    return n;
+}
+
+extern "C" int fsld_loss_grad_host_np(int M, int mode, int n_mask, const fsld_image_rec* recs, const int32_t* idx_host,
+                                      int B, const double* v128_host, const void* xs, const int8_t* pc,
+                                      const void* ptab, const int32_t* seg_off, const int32_t* segs, double scale,
+                                      double lam, double* grad128_host, double* out_host, void* v_dev,
+                                      void* grad_dev, int32_t* idx_dev, int n_slabs, void* scratch,
+                                      size_t scratch_bytes, void* stream) {
+    return fsld_loss_grad_host_np_ball(M, mode, n_mask, recs, idx_host, B, v128_host, xs, pc, ptab, seg_off, segs,
+                                       scale, lam, grad128_host, out_host, v_dev, grad_dev, idx_dev, n_slabs, scratch,
+                                       scratch_bytes, stream, 0.0);
 }

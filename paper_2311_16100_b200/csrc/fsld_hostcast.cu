@@ -60,6 +60,57 @@ extern "C" int fsld_host_cast_f32_to_f64(const float* src, double* dst, int64_t 
     return FSLD_OK;
 }
 
+// The two row loops of the touched-ball host step (fsld_loss_grad_host_np_ball): both return the sum of
+// squares of the n doubles they read (the ||v||^2 term of the loss, accumulated in fp64 in a fixed
+// order) and write with streaming stores (dst 16-byte aligned, n a multiple of 2).
+namespace fsld_host {
+// dst = (float) src
+double cast_f64_to_f32_sumsq(const double* src, float* dst, int64_t n) {
+    __m128d acc0 = _mm_setzero_pd(), acc1 = _mm_setzero_pd();
+    double s = 0.0;
+    int64_t i = 0;
+    for (; i < n && (reinterpret_cast<uintptr_t>(dst + i) & 15); ++i) {  // (odd M: rows start 8 bytes off)
+        dst[i] = (float)src[i];
+        s += src[i] * src[i];
+    }
+    for (; i + 4 <= n; i += 4) {
+        const __m128d a = _mm_loadu_pd(src + i), b = _mm_loadu_pd(src + i + 2);
+        acc0 = _mm_add_pd(acc0, _mm_mul_pd(a, a));
+        acc1 = _mm_add_pd(acc1, _mm_mul_pd(b, b));
+        _mm_stream_ps(dst + i, _mm_movelh_ps(_mm_cvtpd_ps(a), _mm_cvtpd_ps(b)));
+    }
+    double t[2];
+    _mm_storeu_pd(t, _mm_add_pd(acc0, acc1));
+    s += t[0] + t[1];
+    for (; i < n; ++i) {
+        dst[i] = (float)src[i];
+        s += src[i] * src[i];
+    }
+    return s;
+}
+// dst = lam * src
+double scale_f64_sumsq(const double* src, double* dst, int64_t n, double lam) {
+    __m128d acc = _mm_setzero_pd();
+    const __m128d l2 = _mm_set1_pd(lam);
+    const int64_t n2 = n & ~int64_t(1);
+    for (int64_t i = 0; i < n2; i += 2) {
+        const __m128d a = _mm_loadu_pd(src + i);
+        acc = _mm_add_pd(acc, _mm_mul_pd(a, a));
+        _mm_stream_pd(dst + i, _mm_mul_pd(a, l2));
+    }
+    double t[2];
+    _mm_storeu_pd(t, acc);
+    double s = t[0] + t[1];
+    for (int64_t i = n2; i < n; ++i) {
+        dst[i] = lam * src[i];
+        s += src[i] * src[i];
+    }
+    return s;
+}
+void store_fence() { _mm_sfence(); }
+void cpu_pause() { _mm_pause(); }
+}  // namespace fsld_host
+
 // ---------------------------------------------------------------- host thread pool
 // A persistent pool for the numpy-signature host step (fsld_loss_grad_host_np): the casts of one
 // z-slab are split over the workers and the calling thread, which waits for all of them.  Plain

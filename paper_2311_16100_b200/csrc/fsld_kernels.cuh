@@ -223,6 +223,8 @@ cudaError_t launch_real_finalize(int64_t nvox, const void* acc, bool det, const 
                                  double add, float* out, cudaStream_t s);
 int fsc_grid();
 cudaError_t launch_cast_c64_c128(int64_t n, const void* src, void* dst, cudaStream_t s);
+// rows of the touched ball: volume -> packed (pack) or packed -> volume; rows[r] = (voxel offset, length, packed offset, -)
+cudaError_t launch_ball_rows(bool pack, const int4* rows, int nrows, const void* src, void* dst, cudaStream_t s);
 cudaError_t launch_ctf_ring_power(const fsld_image_rec* recs, int N, const short2* ring, int n_ring, double* out,
                                   cudaStream_t s);
 cudaError_t launch_fsc(int M, int R, const float2* u, const float2* v, double* part, double* out, cudaStream_t s);

@@ -15,6 +15,7 @@ sm_100a kernels of libfsld_b200.so.
 """
 from __future__ import annotations
 
+import math
 import os
 import ctypes
 
@@ -409,9 +410,10 @@ class SliceEngine:
 
     def loss_grad_host_np(self, v128: np.ndarray, idx_host, scale: float, lam: float, grad128: np.ndarray,
                           out_host, stage: dict, n_slabs: int | None = None) -> None:
-        """fsld_loss_grad_host_np: numpy complex128 v in, numpy complex128 gradient out (the reference's
-        call shape); the library casts slab by slab on its host threads, overlapped with the copies and
-        the brick passes.  Blocking; out_host (pinned float64[2]) = [sum|r|^2, loss]."""
+        """fsld_loss_grad_host_np_ball: numpy complex128 v in, numpy complex128 gradient out (the
+        reference's call shape); only the touched ball crosses PCIe (packed complex64, one copy per
+        z-slab and direction), the host threads cast each finished slab back and write lam v off the
+        ball.  Blocking; out_host (pinned float64[2]) = [sum|r|^2, loss]."""
         lib = C.load()
         if not self.brick_path:
             raise ValueError("the host step runs the brick path (tri, sorted, non-deterministic)")
@@ -428,12 +430,26 @@ class SliceEngine:
         scr = self.scratch(B)
         if stage["idx"].numel() < B:
             stage["idx"] = torch.empty(B, dtype=torch.int32, device=self.dev)
-        C.check(lib.fsld_loss_grad_host_np(
+        C.check(lib.fsld_loss_grad_host_np_ball(
             self.M, self.mode_id, self.n_mask, ctypes_ptr(self.recs), ctypes_ptr(idx_host), B, v128.ctypes.data,
             ctypes_ptr(self.x), ctypes_ptr(self.pc), ctypes_ptr(self.ptab), ctypes_ptr(self.seg_off),
             ctypes_ptr(self.segs), float(scale), float(lam), grad128.ctypes.data, ctypes_ptr(out_host),
             ctypes_ptr(stage["v"]), ctypes_ptr(stage["g"]), ctypes_ptr(stage["idx"]),
-            int(n_slabs or self.HOST_SLABS), ctypes_ptr(scr), scr.numel() * 8, _stream()), "fsld_loss_grad_host_np")
+            int(n_slabs or (self.NP_SLABS if self.HOST_BALL else self.HOST_SLABS)), ctypes_ptr(scr), scr.numel() * 8,
+            _stream(), self.touch_radius if self.HOST_BALL else 0.0), "fsld_loss_grad_host_np_ball")
+
+    HOST_BALL = os.environ.get("FSLD_HOST_BALL", "1") != "0"  # (A/B: whole-plane copies)
+    NP_SLABS = int(os.environ.get("FSLD_NP_SLABS", "10"))  # z-slabs of the packed-ball numpy step (6: 1.00, 8: 0.92, 10: 0.90, 12: 0.95 ms)
+
+    @property
+    def touch_radius(self) -> float:
+        """Radius of the ball a scatter can reach: a rotated pixel keeps |k| (the clamp only shortens it,
+        kernels.py:42-60) and its trilinear footprint stays within sqrt(3) of it (grid.touched_ball)."""
+        r = getattr(self, "_touch_radius", None)
+        if r is None:
+            k = self.pix.to(torch.float64)
+            r = self._touch_radius = float(torch.sqrt((k * k).sum(dim=1).max())) + math.sqrt(3.0) + 1e-3
+        return r
 
     def proj_energy_planned(self, d, plan: "BinPlan", k: int, out=None) -> torch.Tensor:
         lib = C.load()

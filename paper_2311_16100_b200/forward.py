@@ -465,11 +465,13 @@ class DatasetOperator:
 
     def loss_and_grad_numpy(self, v, batch, lam: float, n_total: int | None = None):
         """optim.loss_and_grad with the reference's argument types (numpy complex128 v in, (float,
-        complex128 gradient) out; optim.py:165-190) on the brick path, through fsld_loss_grad_host_np:
-        the library casts v to complex64 slab by slab on its host thread pool while the device copies
-        and processes the earlier slabs (each slab's copy waits on a mapped flag), and casts every
-        finished gradient slab back to complex128 into the returned array (a recycled page-locked
-        buffer) while later slabs are still in flight.  Accuracy: the fp32 path (1e-7 relative)."""
+        complex128 gradient) out; optim.py:165-190) on the brick path, through
+        fsld_loss_grad_host_np_ball: only the voxels a scatter can reach (grid.touched_ball) cross
+        PCIe, cast to complex64 and packed row by row by the library's host threads, one contiguous
+        copy per z-slab in each direction overlapping the brick passes; every finished gradient slab
+        is cast back to complex128 into the returned array (a recycled page-locked buffer) while later
+        slabs are in flight, and off the ball the host threads write grad = lam v and sum ||v||^2 in
+        fp64.  Accuracy: the fp32 path on the ball (1e-7 relative), fp64 off it."""
         from .hostio import PinnedArrays
 
         e = self.engine

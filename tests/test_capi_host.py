@@ -19,7 +19,7 @@ from paper_2311_16100_b200 import synth
 
 def header_symbols():
     txt = open(os.path.join(ROOT, "include", "fsld_b200.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:int|size_t|const char\*)\s+(fsld_\w+)\s*\(", txt, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|size_t|const char\*)\s+(fsld_\w+)\s*\(", txt, re.M)))
 
 
 def test_library_exports_every_header_symbol():

@@ -414,6 +414,45 @@ def test_odd_sizes_and_small_masks_vs_oracle(M, radius):
     assert np.array_equal(K.assign_nn(oop.rots[batch], pix, M), O.assign_nn(oop.rots[batch], pix, M))
 
 
+@pytest.mark.parametrize("M,radius,slabs", [(33, 9, 12), (32, 15, 5), (64, 20, 12), (64, 31, 16), (40, 6, 1)])
+def test_numpy_call_touched_ball_copies_vs_whole_planes_and_oracle(M, radius, slabs, monkeypatch):
+    """fsld_loss_grad_host_np_ball: the z-slab copies restricted to the boxes around the touched ball
+    (grid.touched_ball; outside, grad = lam v and ||v||^2 on the host threads in fp64) against the same
+    call with whole-plane copies and against the oracle -- v is dense noise, so any voxel the boxes
+    miss, or any stale voxel they pick up, shows."""
+    from paper_2311_16100_b200.engine import SliceEngine
+    B = 40
+    mask = O.disk_mask(M, radius)
+    pix = O.mask_pix(M, mask)
+    q = synth.haar_quaternions(B, M + 5)
+    sh = synth.normal_shifts(B, M + 6)
+    ctfs = synth.physical_ctfs(B, M + 7)
+    ctab = O.ctf_table_physical(synth.ctf_param_array(ctfs), pix, M)
+    rng = np.random.default_rng(M + radius)
+    x = rng.standard_normal((B, mask.size)) + 1j * rng.standard_normal((B, mask.size))
+    oop = O.OracleOperator(M, "tri", mask, q, sh, ctab, x)
+    op = gpu_op(M, "tri", mask, q, sh, ctfs, x)
+    monkeypatch.setattr(SliceEngine, "HOST_SLABS", slabs)
+    monkeypatch.setattr(SliceEngine, "NP_SLABS", slabs)
+    batch = rng.permutation(B)[:33]
+    lam = 0.02
+    for trial in range(3):  # new v every call: the device copy outside the boxes goes stale
+        v = rng.standard_normal(M ** 3) + 1j * rng.standard_normal(M ** 3)
+        monkeypatch.setattr(SliceEngine, "HOST_BALL", True)
+        lb, gb = op.loss_and_grad_numpy(v, batch, lam)
+        gb = gb.copy()
+        monkeypatch.setattr(SliceEngine, "HOST_BALL", False)
+        lw, gw = op.loss_and_grad_numpy(v, batch, lam)
+        lr, gr = O.loss_and_grad(oop, v, batch, lam)
+        assert abs(lb - lw) / lw < 1e-6 and abs(lb - lr) / lr < TOL
+        assert rel(gb, gw) < 1e-6 and rel(gb, gr) < TOL
+        # outside the ball the gradient is lam v in fp64, exactly
+        from paper_2311_16100_b200.grid import touched_ball
+        out = np.ones(M ** 3, bool)
+        out[touched_ball(M, radius)] = False
+        assert np.allclose(gb[out], lam * v[out], rtol=1e-6, atol=0)
+
+
 @pytest.mark.parametrize("M", [128, 256])
 def test_large_defocus_phase_brick_vs_oracle(M):
     """Stress the fixed-point CTF / shift phases of the brick path: 5 um defocus, 0.5 um astigmatism,
