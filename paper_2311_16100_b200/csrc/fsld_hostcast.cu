@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <atomic>
+#include <chrono>
 #include <condition_variable>
 #include <functional>
 #include <mutex>
@@ -126,7 +127,7 @@ struct Pool {
     int64_t n = 0, grain = 1;
     std::atomic<int64_t> next{0};
     int active = 0;
-    unsigned long long gen = 0;
+    std::atomic<unsigned long long> gen{0};
     bool stop = false;
 
     void run_chunks() {
@@ -136,14 +137,26 @@ struct Pool {
             (*fn)(i0, std::min(n, i0 + grain));
         }
     }
+    // A worker that has just finished a job spins for a short while before it blocks: the host step
+    // issues a dozen small jobs per call (one per z-slab), a few tens of microseconds apart, and a
+    // condition-variable wake-up of 15 sleeping threads costs about as much as one of those jobs.
+    static constexpr long long kSpinNs = 400000;
     void loop() {
         unsigned long long seen = 0;
         for (;;) {
+            const auto t0 = std::chrono::steady_clock::now();
+            for (unsigned it = 0; gen.load(std::memory_order_acquire) == seen; ++it) {
+                _mm_pause();
+                if ((it & 63) == 63 &&
+                    std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count() >
+                        kSpinNs)
+                    break;
+            }
             {
                 std::unique_lock<std::mutex> lk(m);
-                cv.wait(lk, [&] { return stop || gen != seen; });
+                cv.wait(lk, [&] { return stop || gen.load(std::memory_order_relaxed) != seen; });
                 if (stop) return;
-                seen = gen;
+                seen = gen.load(std::memory_order_relaxed);
             }
             run_chunks();
             std::lock_guard<std::mutex> lk(m);
@@ -191,7 +204,7 @@ void parallel_for(int64_t n, int64_t grain, const std::function<void(int64_t, in
         P.grain = grain;
         P.next.store(0);
         P.active = (int)P.workers.size();
-        ++P.gen;
+        P.gen.fetch_add(1, std::memory_order_release);
     }
     P.cv.notify_all();
     P.run_chunks();
