@@ -515,7 +515,7 @@ int fsld_loss_grad_host_np(int M, int mode, int n_mask, const fsld_image_rec* re
 /* The same call moving only the touched ball (grid.touched_ball): the data term
  * only reaches voxels within touch_radius = max |k| over the mask + sqrt(3) of the origin.  With
  * touch_radius > 0 only those voxels cross PCIe, packed row by row as complex64 -- one contiguous range per
- * z-slab in each direction (fsld_ball_voxels(M, touch_radius) voxels: ~55 % of the cube at M=128) -- and
+ * z-slab in each direction (fsld_ball_voxels(M, touch_radius) voxels: ~58 % of the cube at M=128) -- and
  * the host threads cast each finished gradient slab to complex128 into grad128_host (any host memory)
  * while later slabs are in flight; off the ball they write grad = lam v in fp64 while the device works,
  * and ||v||^2 in the loss is summed on the host in fp64.  touch_radius <= 0: fsld_loss_grad_host_np. */

@@ -1412,7 +1412,7 @@ void np_cast_back(const float* src, double* dst, int64_t n) {
 // touch_radius > 0: the data term only reaches voxels within that radius of the origin
 // (grid.touched_ball: max |k| of the mask + sqrt(3)); off that ball the gradient is lam v and the loss
 // only sees ||v||^2 -- both computed here on the host threads in fp64 while the device works.  Only
-// the ball crosses PCIe, packed row by row (BallPack: ~55 % of the cube at M=128), one contiguous
+// the ball crosses PCIe, packed row by row (BallPack: ~58 % of the cube at M=128), one contiguous
 // complex64 range per z-slab in each direction: the cast in writes the packed staging, a row kernel puts
 // each slab's rows into the device volume; each finished gradient slab is packed on the device, copied,
 // flagged, and cast to complex128 into the result by the host threads while later slabs are in flight
