@@ -229,3 +229,20 @@ def test_host_casts_are_exact_roundings_any_alignment():
     out = np.zeros(2 * 300001, np.float32)
     cast_native(lib.fsld_host_cast_f64_to_f32, big.ctypes.data, out.ctypes.data, big.size, 8, 4)
     assert np.array_equal(out, big.astype(np.float32))
+
+
+def test_ball_voxels_covers_the_touched_ball():
+    """fsld_ball_voxels (the packed ball of fsld_loss_grad_host_np_ball; host code, no device call): at
+    least the voxels grid.touched_ball lists, rows rounded out to 4 voxels, the whole cube without a radius."""
+    import math
+    from paper_2311_16100_b200.grid import touched_ball
+    lib = C.load()
+    for M, R in [(16, 7), (32, 8), (33, 15), (64, 31), (128, 63)]:
+        n = lib.fsld_ball_voxels(M, R + 0.5 + math.sqrt(3.0))
+        nb = len(touched_ball(M, R))
+        assert nb <= n <= M ** 3
+        assert n % 4 == 0 or M % 4
+        if M >= 64:
+            assert n < 0.75 * M ** 3 and n < 1.25 * nb
+    assert lib.fsld_ball_voxels(32, 0.0) == 32 ** 3
+    assert lib.fsld_ball_voxels(32, float("inf")) == 32 ** 3
